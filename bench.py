@@ -1,0 +1,395 @@
+"""Benchmark: GraphSAGE train seeds/sec on compressed features (BASELINE.json).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config products|arxiv|papers100m|mag240m]
+
+Default workload (N=1): BASELINE configs[1] — synthetic ogbn-products-shape
+graph (2,449,029 nodes, avg degree ~50, 100-dim class-conditional features),
+3-layer GraphSAGE, fanouts [15,10,5], batch 1024, VQ codebooks of 256 entries
+(width 4, cosine, CR 32).  A step = one full training step on one batch of
+seeds: sample (device PCG64) -> fused gather-dequant-mean -> bf16 SAGE
+fwd/bwd -> all-reduce (N>1) -> Adam, replayed from one CUDA graph.
+
+Prints ONE JSON line (rank 0).  ``value`` is device-timed with CUDA events,
+seeds already resident in HBM, L2 flushed between steps; ``e2e`` is the same
+step through the public API with the seed ids copied from pinned host memory
+and the loss read back every step.  ``--impl reference`` times the CPU oracle
+port of the reference path (numpy sampler + decoder restating pipeline.py /
+vq.py / sq.py, plus a CPU fp32 PyTorch SAGE step) on the host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+CONFIGS = {
+    # name: (shape, codec, fanouts, batch, hidden)
+    "products": ("products", ("vq", 4, 256), (15, 10, 5), 1024, 256),
+    "arxiv": ("arxiv", ("sq", 8), (10, 5), 1024, 256),
+    "papers100m": ("papers100m", ("sq", 4), (15, 10, 5), 1024, 256),
+    "mag240m": ("mag240m", ("vq", 8, 256), (15, 10, 5), 1024, 256),
+}
+
+
+def load_peaks():
+    p = os.path.join(REPO, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi style clock / throttle sampling during the timed region."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown", 0x2: "applications_clocks"}
+
+    def __init__(self, index=0, period=0.05):
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.pynvml = pynvml
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            pass
+        self.period = period
+        self.t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.pynvml.nvmlDeviceGetClockInfo(self.h,
+                                                                       self.pynvml.NVML_CLOCK_SM))
+                r = self.pynvml.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            self._stop.wait(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.ok:
+            self.t.join(2)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons)}
+
+
+# ------------------------------------------------------------------ setup
+
+def build_workload(cfg_name, device, seed=0, scale=1.0):
+    import torch
+    from paper_2207_14696_b200.synth import SHAPES, build_sq_codec, build_vq_codec, make_shape
+    shape, codec_spec, fanouts, bs, hidden = CONFIGS[cfg_name]
+    sg = make_shape(shape, seed=seed, scale=scale, device=device)
+    n, d = sg.graph.n, SHAPES[shape]["d"]
+    if codec_spec[0] == "vq":
+        dc, host_codec = build_vq_codec(n, d, codec_spec[1], codec_spec[2], labels=sg.labels,
+                                        num_classes=sg.num_classes, seed=seed)
+        codec_desc = f"vq width {codec_spec[1]} length {codec_spec[2]} cosine (CR {32 * codec_spec[1] / math.log2(codec_spec[2]):.0f})"
+    else:
+        dc = build_sq_codec(n, d, codec_spec[1], labels=sg.labels, num_classes=sg.num_classes,
+                            seed=seed)
+        codec_desc = f"sq k={codec_spec[1]} (CR {32 / codec_spec[1]:.0f})"
+    torch.cuda.synchronize()
+    return sg, dc, codec_desc, fanouts, bs, hidden
+
+
+def flush_l2(buf):
+    buf.add_(1)  # 512 MB write > 126 MB L2
+
+
+# ------------------------------------------------------------- our arm
+
+def run_ours(args, rank, world, local):
+    import torch
+    import torch.distributed as dist
+    from paper_2207_14696_b200 import _native as N
+    from paper_2207_14696_b200 import ddp
+    from paper_2207_14696_b200.aggregate import gather_dequant_mean
+    from paper_2207_14696_b200.sage import SageTrainer, TrainConfig
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    sg, dc, codec_desc, fanouts, bs, hidden = build_workload(args.config, dev, scale=args.scale)
+    pg = dist.group.WORLD if world > 1 else None
+    cfg = TrainConfig(fanouts=fanouts, batch_size=bs, hidden=hidden, lr=3e-3, seed=0)
+    tr = SageTrainer(sg.graph, dc, sg.labels, sg.num_classes, cfg, process_group=pg)
+    nb = tr.begin_epoch(sg.train_ids, 0)
+    need = args.warmup + 2 * args.steps + 1
+    if nb < need:
+        raise SystemExit(f"epoch has {nb} batches per rank, need {need}")
+    tr.capture(warmup_batches=max(3, args.warmup))
+    flush = torch.zeros(128 * 1024 * 1024, dtype=torch.float32, device=dev)
+    # warm-up replays
+    for b in range(args.warmup):
+        tr.step(b)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    # ---- timed: K steps, seeds resident, L2 flushed between steps
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    l0 = N.lib().fg_launch_count()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            b = args.warmup + i
+            flush_l2(flush)
+            tr.sampler.load_seeds(b)
+            evs[i][0].record()
+            tr.graph.replay()
+            evs[i][1].record()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t_ms = sum(s.elapsed_time(e) for s, e in evs)
+    t_ms = ddp.max_over_ranks(t_ms, dev)
+    # launches per step: one eager step counted by the library's counter
+    c0 = N.lib().fg_launch_count()
+    tr.sampler.load_seeds(0)
+    tr._body()
+    torch.cuda.synchronize()
+    launches_per_step = N.lib().fg_launch_count() - c0
+    # ---- e2e: public API, seeds from pinned host, loss read back each step
+    perm = tr.sampler.perm_host
+    pinned = [torch.from_numpy(perm[(args.warmup + args.steps + i) * bs:
+                                    (args.warmup + args.steps + i + 1) * bs].copy()).pin_memory()
+              for i in range(args.steps)]
+    loss_host = torch.zeros((), dtype=torch.float32).pin_memory()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e2e_ms = 0.0
+    for i in range(args.steps):
+        flush_l2(flush)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        loss = tr.step(0, seeds_host=pinned[i])
+        loss_host.copy_(loss, non_blocking=True)
+        e.record()
+        e.synchronize()
+        e2e_ms += s.elapsed_time(e)
+    e2e_ms = ddp.max_over_ranks(e2e_ms, dev)
+    # ---- roofline: the fused gather-dequant-mean kernel, timed alone
+    L = len(fanouts)
+    row_bytes = dc.num_parts * dc.bits / 8 if hasattr(dc, "num_parts") else dc.d * dc.params.k / 8
+    kt, kbytes = [], []
+    for i in range(args.steps):
+        tr.sampler.load_seeds(args.warmup + i)
+        sb = tr.sampler.sample_loaded()
+        torch.cuda.synchronize()
+        E = int(sb.n_picks[L - 1].item())
+        nd = int(sb.n_nodes[L - 1].item())
+        flush_l2(flush)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        gather_dequant_mean(dc, sb.indptr[L - 1], sb.picks[L - 1], sb.n_nodes[L - 1],
+                            tr.caps[L - 1], out=tr.agg)
+        e.record()
+        e.synchronize()
+        kt.append(s.elapsed_time(e))
+        out_b = tr.agg.element_size()
+        # algorithmic bytes: E code rows + int32 source ids, N_dst indptr
+        # entries + output rows (the padded rows past N_dst are zero-filled
+        # but not counted)
+        kbytes.append(E * (row_bytes + 4) + nd * (4 + dc.d * out_b))
+    avg_ms = sum(kt) / len(kt)
+    avg_bytes = sum(kbytes) / len(kbytes)
+    peak, peak_kind = load_peaks()
+    achieved = avg_bytes / (avg_ms * 1e-3) / 1e9
+    seeds_per_step = bs * world
+    value = seeds_per_step * args.steps / (t_ms * 1e-3)
+    e2e = seeds_per_step * args.steps / (e2e_ms * 1e-3)
+    result = {
+        "metric": "GraphSAGE train seeds/sec",
+        "value": round(value, 1),
+        "unit": "seeds/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(t_ms / args.steps, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic (planted-partition power-law graph, class-conditional features)",
+        "config": {"workload": f"{args.config}-shape GraphSAGE {len(fanouts)}-layer "
+                               f"fanout {list(fanouts)}, {codec_desc}",
+                   "nodes": sg.graph.n, "edges_stored": sg.graph.nnz, "feature_dim": dc.d,
+                   "global_batch": seeds_per_step, "per_rank_batch": bs, "hidden": hidden,
+                   "parallelism": f"dp{world}", "l2": "flushed between steps (512 MB write)",
+                   "graph": "one CUDA graph per step"},
+        "e2e": {"value": round(e2e, 1), "unit": "seeds/s",
+                "h2d_bytes_per_step": bs * 8, "d2h_bytes_per_step": 4},
+        "gpu_launches": int(launches_per_step * args.steps),
+        "roofline": {"kernel": "fg_gather_dequant_mean (k_vq_mean/k_sq_mean)", "bound": "hbm",
+                     "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "peak_kind": peak_kind,
+                     "traffic": None, "avg_launch_us": round(avg_ms * 1e3, 2),
+                     "alg_bytes_per_launch": int(avg_bytes)},
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        result["cpu_baseline"] = cpu_baseline(sg, dc, fanouts, hidden, budget_s=args.cpu_budget)
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+
+
+# ------------------------------------------------------- CPU baseline
+
+def _host_world(sg, dc):
+    """Host copies for the CPU oracle: CSR, labels, decoder over codes."""
+    host = sg.graph.to_host()
+    labels = sg.labels.cpu().numpy()
+    from oracle import codecs as oc
+    from paper_2207_14696_b200.vq import DeviceVqCodec
+    if isinstance(dc, DeviceVqCodec):
+        import torch
+        codes = torch.empty((dc.n, dc.num_parts), dtype=torch.int32, device=dc.rows.device)
+        # codes come back from the device rows via the reference layout
+        rows = dc.rows.cpu().numpy()
+        b = dc.bits
+        assert b == 8, "CPU baseline decoder supports 8-bit VQ codes"
+        codes = rows[:, :dc.num_parts].astype(np.int32)
+        books = dc.books_host
+        w = dc.params.width
+
+        def decode(r):
+            return oc.vq_decode(codes, books, dc.d, w, r)
+    else:
+        c = dc.to_codec()
+        p = c.params
+
+        def decode(r):
+            return oc.sq_dequant_rows(c.payload, c.n, c.d, p.k, p.e_min, p.e_max, r)
+    return host, labels, decode
+
+
+def cpu_baseline(sg, dc, fanouts, hidden, budget_s=20.0, batch=128):
+    """Oracle port of the reference path on the host cores: numpy sampler
+    (pipeline.py:185-222 restated) + numpy decoder + CPU fp32 SAGE step."""
+    import torch
+    from oracle import trainer as ot
+    host, labels, decode = _host_world(sg, dc)
+    model = ot.OracleSage(dc.d, hidden, sg.num_classes, len(fanouts))
+    opt = torch.optim.Adam(model.parameters(), lr=3e-3)
+    seeds_done, t0, steps = 0, time.perf_counter(), 0
+    train = sg.train_ids
+    while True:
+        ot.train_epoch(model, opt, host.row_offsets, host.col_indices, labels,
+                       train[steps * batch:(steps + 1) * batch], fanouts, batch, steps, decode)
+        steps += 1
+        seeds_done += batch
+        if time.perf_counter() - t0 >= budget_s or steps * batch >= train.size:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": round(seeds_done / dt, 2), "unit": "seeds/s",
+            "cores": torch.get_num_threads(), "kind": "port",
+            "sample": f"{steps} mini-batches of {batch} seeds, fanouts {list(fanouts)}, "
+                      f"{dt:.1f} s (numpy sampler/decoder single-threaded, torch CPU "
+                      f"fp32 SAGE step on {torch.get_num_threads()} threads)"}
+
+
+def run_reference(args, rank, world, local):
+    """The reference arm: CPU oracle port, rank 0 only."""
+    if rank != 0:
+        return
+    import torch
+    from oracle import trainer as ot
+    dev = torch.device("cuda", local) if torch.cuda.is_available() else torch.device("cpu")
+    if dev.type == "cuda":
+        torch.cuda.set_device(dev)
+    sg, dc, codec_desc, fanouts, bs, hidden = build_workload(args.config, dev, scale=args.scale)
+    host, labels, decode = _host_world(sg, dc)
+    torch.set_num_threads(os.cpu_count() or 1)
+    model = ot.OracleSage(dc.d, hidden, sg.num_classes, len(fanouts))
+    opt = torch.optim.Adam(model.parameters(), lr=3e-3)
+    batch = args.ref_batch
+    train = sg.train_ids
+
+    def one(i):
+        ot.train_epoch(model, opt, host.row_offsets, host.col_indices, labels,
+                       train[i * batch:(i + 1) * batch], fanouts, batch, i, decode)
+
+    for i in range(args.warmup):
+        one(i)
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        one(args.warmup + i)
+    dt = time.perf_counter() - t0
+    v = batch * args.steps / dt
+    line = {"impl": "reference", "metric": "GraphSAGE train seeds/sec", "value": round(v, 2),
+            "unit": "seeds/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(dt * 1e3 / args.steps, 2), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{args.config}-shape GraphSAGE {len(fanouts)}-layer fanout "
+                                   f"{list(fanouts)}, {codec_desc}",
+                       "per_step_seeds": batch, "parallelism": "cpu"},
+            "cpu_baseline": {"value": round(v, 2), "unit": "seeds/s",
+                             "cores": torch.get_num_threads(), "kind": "port",
+                             "sample": f"{args.steps} steps x {batch} seeds"},
+            "e2e": {"value": round(v, 2), "unit": "seeds/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="products")
+    ap.add_argument("--scale", type=float, default=1.0, help="node-count scale (tests only)")
+    ap.add_argument("--ref-batch", type=int, default=128)
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    from paper_2207_14696_b200 import ddp
+    backend = "nccl" if args.impl == "ours" else "gloo"
+    rank, world, local = ddp.init_from_env(backend)
+    try:
+        if args.impl == "reference":
+            run_reference(args, rank, world, local)
+        else:
+            run_ours(args, rank, world, local)
+    finally:
+        import torch.distributed as dist
+        if dist.is_initialized():
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,251 @@
+/*
+ * featgrind-b200 — C ABI of the B200-native compressed-feature GNN
+ * mini-batch path (arxiv 2207.14696 / reference package `featgrind`).
+ *
+ * Every entry point takes plain device pointers and sizes plus a
+ * cudaStream_t passed as `void*`; nothing here mentions torch.  The caller
+ * owns and allocates all memory (including workspaces); the library never
+ * allocates or frees caller memory and keeps no global mutable state apart
+ * from a thread-local error string.  All launches are stream-ordered and
+ * capture-safe (no host synchronisation, no implicit allocation), so a whole
+ * training step can be recorded into one CUDA graph.
+ *
+ * Return codes mirror the reference's error convention
+ * (pkg/src/featgrind/errors.py:8-13, cli.py:46-52,503-505):
+ *   FG_OK 0, FG_EUSAGE 1 (bad arguments), FG_EDATA 2 (bad data, e.g. a row
+ *   id out of range -> DataError), FG_ECUDA 3 (CUDA runtime failure).
+ * Device-detected data errors are reported through an `int32_t* err_flag`
+ * (device memory, caller-zeroed) that the host checks when it chooses to.
+ *
+ * Device code-row layout ("rows"): the reference payload is one continuous
+ * MSB-first bitstream, row r starting at bit r*row_bits
+ * (pkg/src/featgrind/bitpack.py:17-83, sq.py:61-81).  On the device each row
+ * starts on its own `row_stride`-byte boundary (stride a multiple of 16,
+ * normally 32 so a row never straddles more sectors than it must); bit order
+ * inside a row is unchanged.  fg_stream_to_rows / fg_rows_to_stream convert.
+ */
+#ifndef FEATGRIND_B200_H
+#define FEATGRIND_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FG_OK 0
+#define FG_EUSAGE 1
+#define FG_EDATA 2
+#define FG_ECUDA 3
+
+/* output element types for decode / aggregate */
+#define FG_OUT_F32 0
+#define FG_OUT_BF16 1
+#define FG_OUT_F64 2
+
+#define FG_CODEC_SQ 1
+#define FG_CODEC_VQ 2
+
+#define FG_METRIC_EUCLIDEAN 0 /* vq.py:29 METRICS order */
+#define FG_METRIC_COSINE 1
+
+/* Device-resident codec: what the gather / aggregate kernels read. */
+typedef struct fg_codec_desc {
+  int32_t kind;        /* FG_CODEC_SQ | FG_CODEC_VQ */
+  int32_t bits;        /* SQ: k (1..8); VQ: bits per code (1..16) */
+  int64_t n;           /* rows */
+  int64_t d;           /* feature dim */
+  int64_t row_stride;  /* bytes between device rows (multiple of 16) */
+  const uint8_t* rows; /* n * row_stride bytes */
+  const void* table;   /* SQ: LUT of 2^k values (float, or double for
+                          elem_bits 64); VQ: float codebooks [P][L][width],
+                          narrow last part zero-padded to width */
+  int32_t width;       /* VQ: dims per part */
+  int32_t length;      /* VQ: entries per part (padded) */
+  int32_t num_parts;   /* VQ: ceil(d / width) */
+  int32_t elem_bits;   /* 32 or 64: decode precision of the table */
+} fg_codec_desc;
+
+/* ------------------------------------------------------------ library */
+const char* fg_last_error(void);
+int fg_version(void);               /* 100 * major + minor */
+/* Number of kernels this library has launched in the process so far
+ * (benchmarks report launches per step from it). */
+int64_t fg_launch_count(void);
+int fg_sm_count(int* out);
+
+/* -------------------------------------------------------- code layout */
+/* Continuous reference stream (bitpack.py:17-36 layout, row_bits per row)
+ * <-> strided device rows.  Replaces the byte-window gather of
+ * bitpack.py:58-83 (gather_bit_rows) with a one-time repack on upload. */
+int fg_stream_to_rows(const uint8_t* stream, int64_t stream_bytes, int64_t n,
+                      int64_t row_bits, uint8_t* rows, int64_t row_stride,
+                      void* cuda_stream);
+int fg_rows_to_stream(const uint8_t* rows, int64_t n, int64_t row_bits,
+                      int64_t row_stride, uint8_t* stream, int64_t stream_bytes,
+                      void* cuda_stream);
+
+/* ----------------------------------------------------------------- SQ */
+/* quantize_sq (sq.py:114-129).  `thresholds` (device, float, 2^(k-1)-1
+ * entries, ascending) are the smallest |x| whose reference code offset is
+ * >= j, j = 1..2^(k-1)-1, derived on the host from the reference formula;
+ * code = half + #(t_j <= |x|) for x >= 0 (including -0.0), else
+ * half - 1 - #.  k = 1 ignores thresholds (code = x >= 0).  `x` is row-major
+ * float32 (x_is_f64 = 0) or float64 (x_is_f64 = 1). */
+int fg_sq_encode(const void* x, int x_is_f64, int64_t n, int64_t d, int k,
+                 const float* thresholds, const double* thresholds64,
+                 uint8_t* rows, int64_t row_stride, void* cuda_stream);
+
+/* dequantize_sq(c, rows) (sq.py:132-153) for a device id list:
+ * out[i, :] = table[code(ids[i], :)].  ids are int64 (ids_are_i32 = 0) or
+ * int32.  Out-of-range ids set *err_flag = FG_EDATA and write nothing for
+ * that row. */
+int fg_sq_gather_dequant(const fg_codec_desc* codec, const void* ids,
+                         int ids_are_i32, int64_t num_ids, void* out,
+                         int out_dtype, int32_t* err_flag, void* cuda_stream);
+
+/* fit_sq support (sq.py:96-106): count nonzeros of a float32 matrix. */
+int fg_count_nonzero(const float* x, int64_t count, unsigned long long* out_count,
+                     void* cuda_stream);
+/* Gather |x| of the nonzeros at the evenly strided ranks the reference's
+ * np.linspace(0, nnz-1, cap).astype(int64) selects (or all nonzeros when
+ * nnz <= cap), preserving row-major order.  out has min(nnz, cap) floats. */
+int fg_gather_nonzero_sample(const float* x, int64_t count, int64_t nnz,
+                             int64_t cap, float* out_abs, void* workspace,
+                             int64_t workspace_bytes, void* cuda_stream);
+int64_t fg_nonzero_sample_workspace_bytes(int64_t count);
+/* k-th smallest (0-based) of non-negative floats, for each requested rank;
+ * two-pass 16-bit radix select.  Exact (returns the element bit pattern).
+ * Synchronises `cuda_stream` (offline fit path; not graph-capturable). */
+int fg_select_ranks(const float* vals, int64_t count, const int64_t* ranks_host,
+                    int num_ranks, float* out_host, void* workspace,
+                    int64_t workspace_bytes, void* cuda_stream);
+int64_t fg_select_workspace_bytes(void);
+
+/* ----------------------------------------------------------------- VQ */
+/* encode_vq (vq.py:306-327): per row and part, nearest codebook entry in
+ * float64 arithmetic ordered as numpy/OpenBLAS evaluate the reference
+ * expressions (FMA-chained dot products, numpy pairwise add.reduce for norms);
+ * ties -> lowest index; cosine zero sub-vectors -> 0.  `books` is float32
+ * [P][L][width] (fg_codec_desc layout), `entries` the per-part live entry
+ * count.  Codes land as device rows of `bits` bits per part. */
+int fg_vq_assign(const void* x, int x_is_f64, int64_t n, int64_t d, int width,
+                 int length, int num_parts, const float* books,
+                 const int32_t* entries, int metric, int bits, uint8_t* rows,
+                 int64_t row_stride, int32_t* codes_i32, void* cuda_stream);
+
+/* int32 codes [n, parts] (VqCodec.codes, vq.py:87-127) -> device rows of
+ * `bits`-bit MSB-first codes (the PACKED layout of vq.py:379-381, per row). */
+int fg_codes_to_rows(const int32_t* codes, int64_t n, int parts, int bits,
+                     uint8_t* rows, int64_t row_stride, void* cuda_stream);
+
+/* decode_vq(c, rows) (vq.py:330-344): exact float32 codebook copies. */
+int fg_vq_gather_decode(const fg_codec_desc* codec, const void* ids,
+                        int ids_are_i32, int64_t num_ids, void* out,
+                        int out_dtype, int32_t* err_flag, void* cuda_stream);
+
+/* Lloyd support for fit_vq (vq.py:184-228) on the device: assignment of
+ * float64 points [m, w] to float64 centroids [k, w] (min distance /
+ * max similarity, lowest index on ties) with per-point cost. */
+int fg_kmeans_assign(const double* pts, int64_t m, int w, const double* cents,
+                     int k, int metric, int32_t* assign, double* cost,
+                     double* cc_scratch, void* cuda_stream);
+
+/* np.bincount(assign, weights=pts[:, j]) for all j (vq.py:159-164), summed
+ * per cluster in point order so the float64 result is identical: `order`
+ * is a stable sort of the m points by cluster, `start` has k+1 offsets. */
+int fg_segment_sums(const double* pts, int64_t m, int w, const int64_t* order,
+                    const int64_t* start, int k, double* sums, double* counts,
+                    void* cuda_stream);
+
+/* -------------------------------------------- fused gather + aggregate */
+/* Layer-1 SAGE mean over a sampled block, straight from compressed rows:
+ *   out[v, :] = (1 / cnt_v) * sum_{e in [indptr[v], indptr[v+1])}
+ *               decode(src[e])
+ * where decode is the reference decoder (sq.py:132-153 / vq.py:330-344) and
+ * the mean is the row-stochastic operator of factors.py:108-114 restricted
+ * to the sample.  fp32 accumulation; destinations with no picks give 0.
+ * `num_dst_dev` (device int64) is the live destination count; rows in
+ * [live, max_dst) are zero-filled so static-shape consumers stay exact. */
+int fg_gather_dequant_mean(const fg_codec_desc* codec, const int32_t* indptr,
+                           const int32_t* src, const int64_t* num_dst_dev,
+                           int64_t max_dst, void* out, int out_dtype,
+                           void* cuda_stream);
+
+/* Hidden-layer mean over a block with local source indices (bf16 in/out,
+ * fp32 accumulate) and its backward (scatter of grad/cnt, fp32 atomics into
+ * `grad_src_f32`, then converted to bf16 by fg_f32_to_bf16). */
+int fg_block_mean_fwd(const uint16_t* h_src, int64_t h_dim,
+                      const int32_t* indptr, const int32_t* src_local,
+                      const int64_t* num_dst_dev, int64_t max_dst,
+                      uint16_t* out, void* cuda_stream);
+int fg_block_mean_bwd(const uint16_t* grad_out, int64_t h_dim,
+                      const int32_t* indptr, const int32_t* src_local,
+                      const int64_t* num_dst_dev, int64_t max_dst,
+                      float* grad_src_f32, void* cuda_stream);
+int fg_f32_to_bf16(const float* in, int64_t count, uint16_t* out,
+                   void* cuda_stream);
+
+/* ------------------------------------------------------------- sampler */
+/* PCG64 state block as used by numpy's default_rng (state, inc, has_uint32,
+ * uinteger) followed by a 64-entry jump table; FG_RNG_WORDS uint64 words. */
+#define FG_RNG_WORDS 264
+/* Build the block on the host from numpy's bit_generator.state fields. */
+int fg_rng_init(uint64_t* block_host, uint64_t state_hi, uint64_t state_lo,
+                uint64_t inc_hi, uint64_t inc_lo, int has_uint32,
+                uint32_t uinteger);
+/* Read back (after a device->host copy of the block). */
+int fg_rng_read(const uint64_t* block_host, uint64_t* state_hi,
+                uint64_t* state_lo, int* has_uint32, uint32_t* uinteger);
+/* Host-side Generator.permutation(ids) (numpy _shuffle_raw with
+ * random_interval draws) advancing the host block; pipeline.py:199-200. */
+int fg_rng_permutation_host(uint64_t* block_host, int64_t* ids, int64_t count);
+
+/* One sampler layer (pipeline.py:207-218): for every node of `nodes`
+ * (sorted, device count *num_nodes_dev), pick min(f, deg) stored neighbours
+ * without replacement exactly as numpy's Generator.choice does on the
+ * serial stream in `rng_dev` (Floyd + Lemire + tail shuffle, 2f-1 draws per
+ * node with deg > f), with per-node stream offsets from a prefix sum and a
+ * rejection fix-up pass.  Writes indptr [max_nodes + 1] (int32, CSR over the
+ * layer's nodes), picks (int32, choice output order), *num_picks_dev, marks
+ * every pick in `bitmap` (n bits, caller-cleared) and advances rng_dev past
+ * the layer.  Workspace: fg_sample_workspace_bytes(max_nodes). */
+int fg_sample_layer(const int64_t* row_offsets, const int32_t* col_indices,
+                    int64_t n, const int32_t* nodes, const int64_t* num_nodes_dev,
+                    int64_t max_nodes, int fanout, uint64_t* rng_dev,
+                    int32_t* indptr, int32_t* picks, int64_t max_picks,
+                    int64_t* num_picks_dev, uint32_t* bitmap, void* workspace,
+                    int64_t workspace_bytes, int32_t* err_flag, void* cuda_stream);
+int64_t fg_sample_workspace_bytes(int64_t max_nodes);
+
+/* Bitmap set algebra used for np.unique on node ids (ids < n):
+ * mark ids, then emit the sorted unique list, keep a per-word rank prefix so
+ * fg_bitmap_rank maps ids to their position in that list, then clear. */
+int fg_bitmap_mark(const int32_t* ids, const int64_t* count_dev, int64_t max_count,
+                   uint32_t* bitmap, void* cuda_stream);
+int fg_bitmap_mark64(const int64_t* ids, const int64_t* count_dev, int64_t max_count,
+                     uint32_t* bitmap, void* cuda_stream);
+int fg_bitmap_compact(uint32_t* bitmap, int64_t n, int32_t* out_ids,
+                      int64_t max_out, int64_t* out_count_dev,
+                      int32_t* word_prefix, void* workspace,
+                      int64_t workspace_bytes, void* cuda_stream);
+int64_t fg_bitmap_workspace_bytes(int64_t n);
+int fg_bitmap_rank(const int32_t* ids, const int64_t* count_dev, int64_t max_count,
+                   const uint32_t* bitmap, const int32_t* word_prefix,
+                   int32_t* out_rank, void* cuda_stream);
+int fg_bitmap_clear(const int32_t* ids, const int64_t* count_dev, int64_t max_count,
+                    uint32_t* bitmap, void* cuda_stream);
+
+/* ----------------------------------------------------- synthetic data */
+/* Deterministic, row-addressable synthetic inputs: feature
+ * value (i, j) depends only on (seed, i, j), so any row subset can be
+ * regenerated for the oracle.  kind: 0 normal, 1 lognormal, 2 correlated,
+ * 3 class-conditional (planted label i -> mean direction). */
+int fg_synth_features(int kind, uint64_t seed, int64_t row0, int64_t rows,
+                      int64_t d, const int32_t* labels, int num_classes,
+                      float* out, void* cuda_stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FEATGRIND_B200_H */

@@ -1,0 +1,82 @@
+"""CPU fp32 GraphSAGE oracle trainer — TEST INFRASTRUCTURE ONLY.
+
+The reference has no trainer, so "accuracy within
+0.5 points of the reference" is defined against this oracle: plain PyTorch
+fp32 on the CPU, fed by the restated reference sampler (oracle/sampler.py,
+pipeline.py:185-222) and the restated reference decoders (oracle/codecs.py),
+with the row-stochastic mean aggregation of factors.py:108-114 restricted to
+the sampled blocks.  Same model structure as paper_2207_14696_b200.sage.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+import torch.nn as nn
+import torch.nn.functional as F
+
+from .aggregate import block_mean as np_block_mean
+from .sampler import sample_batches_oracle
+
+
+class OracleSage(nn.Module):
+    def __init__(self, in_dim, hidden, num_classes, num_layers):
+        super().__init__()
+        dims = [in_dim] + [hidden] * (num_layers - 1) + [num_classes]
+        self.lins = nn.ModuleList(nn.Linear(dims[i], dims[i + 1]) for i in range(num_layers))
+
+    def forward(self, agg_in, blocks):
+        """blocks[l] = (counts, local) for l < L-1 (local indexes layer l+1)."""
+        L = len(self.lins)
+        h = self.lins[0](agg_in)
+        for i in range(1, L):
+            h = F.relu(h)
+            l = L - 1 - i
+            counts, local = blocks[l]
+            seg = torch.repeat_interleave(torch.arange(counts.numel()), counts)
+            a = torch.zeros(counts.numel(), h.shape[1]).index_add_(0, seg, h[local])
+            a = a / counts.clamp_min(1)[:, None].float()
+            h = self.lins[i](a)
+        return h
+
+
+def batch_tensors(batch, decode_rows):
+    """Input aggregate (float64 mean -> fp32) and hidden blocks of one batch."""
+    L = len(batch.layers)
+    last = batch.layers[-1]
+    dec = decode_rows(last.picks)
+    agg = torch.from_numpy(np_block_mean(dec, last.counts).astype(np.float32))
+    blocks = []
+    for l in range(L - 1):
+        nxt = batch.layers[l + 1].nodes
+        local = np.searchsorted(nxt, batch.layers[l].picks)
+        blocks.append((torch.from_numpy(batch.layers[l].counts), torch.from_numpy(local)))
+    return agg, blocks
+
+
+def train_epoch(model, opt, off, col, labels, train_ids, fanouts, bs, seed, decode_rows,
+                max_batches=None):
+    batches, _ = sample_batches_oracle(off, col, train_ids, fanouts, bs, seed,
+                                       max_batches=max_batches)
+    losses = []
+    for b in batches:
+        agg, blocks = batch_tensors(b, decode_rows)
+        logits = model(agg, blocks)
+        loss = F.cross_entropy(logits, torch.from_numpy(labels[b.seeds]).long())
+        opt.zero_grad()
+        loss.backward()
+        opt.step()
+        losses.append(float(loss))
+    return losses
+
+
+@torch.no_grad()
+def evaluate(model, off, col, labels, ids, fanouts, bs, seed, decode_rows, max_batches=None):
+    batches, _ = sample_batches_oracle(off, col, ids, fanouts, bs, seed, max_batches=max_batches)
+    correct = total = 0
+    for b in batches:
+        agg, blocks = batch_tensors(b, decode_rows)
+        pred = model(agg, blocks).argmax(1).numpy()
+        correct += int((pred == labels[b.seeds]).sum())
+        total += b.seeds.size
+    return correct / max(1, total)

@@ -1,0 +1,507 @@
+// SQ / VQ codec kernels: layout conversion, encode, gather-decode.
+//
+// Reference counterparts (pkg/src/featgrind/):
+//   bitpack.py:17-83  pack_codes / gather_bit_rows  -> fg_stream_to_rows / fg_rows_to_stream
+//   sq.py:114-129     quantize_sq                   -> fg_sq_encode (threshold form)
+//   sq.py:132-153     dequantize_sq(c, rows)        -> fg_sq_gather_dequant (LUT form)
+//   vq.py:306-327     _assign_part / encode_vq      -> fg_vq_assign (fp64, numpy-ordered)
+//   vq.py:330-344     decode_vq(c, rows)            -> fg_vq_gather_decode
+// All of these are HBM-bound streaming / gather kernels except fg_vq_assign,
+// which is FP64-ALU bound (K = width is tiny).
+#include "fg_common.cuh"
+
+namespace fg {
+
+// ------------------------------------------------------------ bit layout
+
+__global__ void k_stream_to_rows(const uint8_t* __restrict__ stream, int64_t stream_bytes,
+                                 int64_t n, int64_t row_bits, uint8_t* __restrict__ rows,
+                                 int64_t stride) {
+  const int64_t total = n * stride;
+  const int64_t row_bytes = (row_bits + 7) >> 3;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = t / stride, b = t - r * stride;
+    uint8_t v = 0;
+    if (b < row_bytes) {
+      const int64_t g = r * row_bits + 8 * b;  // first source bit
+      const int64_t byte = g >> 3;
+      const int sh = (int)(g & 7);
+      uint32_t w = (uint32_t)stream[byte] << 8;
+      if (sh && byte + 1 < stream_bytes) w |= stream[byte + 1];
+      v = (uint8_t)((w << sh) >> 8);
+      const int64_t valid = row_bits - 8 * b;  // bits of this row in the byte
+      if (valid < 8) v &= (uint8_t)(0xFF00u >> valid);
+    }
+    rows[t] = v;
+  }
+}
+
+__global__ void k_rows_to_stream(const uint8_t* __restrict__ rows, int64_t n, int64_t row_bits,
+                                 int64_t stride, uint8_t* __restrict__ stream,
+                                 int64_t stream_bytes) {
+  const int64_t total_bits = n * row_bits;
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < stream_bytes;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t v = 0;
+    for (int t = 0; t < 8; ++t) {
+      const int64_t g = 8 * s + t;
+      uint32_t bit = 0;
+      if (g < total_bits) {
+        const int64_t r = g / row_bits, o = g - r * row_bits;
+        bit = (rows[r * stride + (o >> 3)] >> (7 - (o & 7))) & 1u;
+      }
+      v = (v << 1) | bit;
+    }
+    stream[s] = (uint8_t)v;
+  }
+}
+
+// ------------------------------------------------------------- SQ encode
+// Thread per group of 8 consecutive elements of a row: 8 codes * k bits =
+// exactly k bytes starting at byte g*k of the row (groups are byte aligned).
+template <typename XT, typename TT>
+__global__ void k_sq_encode(const XT* __restrict__ x, int64_t n, int64_t d, int k,
+                            const TT* __restrict__ thr, uint8_t* __restrict__ rows,
+                            int64_t stride) {
+  __shared__ TT s_thr[128];
+  const int half = 1 << (k - 1);
+  for (int i = threadIdx.x; i < half - 1; i += blockDim.x) s_thr[i] = thr[i];
+  __syncthreads();
+  const int64_t groups = (d + 7) >> 3;
+  const int64_t total = n * groups;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = t / groups, g = t - r * groups;
+    const int64_t j0 = g * 8;
+    const int cnt = (int)min64(8, d - j0);
+    uint64_t acc = 0;  // 8*k <= 64 bits, MSB-first
+    for (int e = 0; e < 8; ++e) {
+      uint32_t code = 0;
+      if (e < cnt) {
+        const XT v = x[r * d + j0 + e];
+        if (k == 1) {
+          code = v >= (XT)0 ? 1u : 0u;  // sq.py:118; -0.0 >= 0 holds
+        } else {
+          const TT a = (TT)fabs((double)v);
+          // offset = #thresholds <= |x| (monotone restatement of sq.py:120-127)
+          int lo = 0, hi = half - 1;
+          while (lo < hi) {  // first index with thr > a
+            const int mid = (lo + hi) >> 1;
+            if (s_thr[mid] <= a) lo = mid + 1; else hi = mid;
+          }
+          const int off = lo;
+          code = v >= (XT)0 ? (uint32_t)(half + off) : (uint32_t)(half - 1 - off);
+        }
+      }
+      acc = (acc << k) | code;
+    }
+    // acc holds 8*k bits right-aligned; emit k bytes MSB first
+    uint8_t* dst = rows + r * stride + g * k;
+    const int nbytes = (int)min64(k, ((d * k + 7) >> 3) - g * k);
+    for (int b = 0; b < nbytes; ++b) dst[b] = (uint8_t)(acc >> (8 * (k - 1 - b)));
+  }
+}
+
+// ------------------------------------------------- SQ gather dequantize
+template <typename OT, typename LT>
+__global__ void k_sq_gather(const uint8_t* __restrict__ rows, int64_t n, int64_t d, int k,
+                            int64_t stride, const LT* __restrict__ lut, const void* ids,
+                            int ids32, int64_t num_ids, OT* __restrict__ out,
+                            int32_t* err_flag) {
+  __shared__ LT s_lut[256];
+  for (int i = threadIdx.x; i < (1 << k); i += blockDim.x) s_lut[i] = lut[i];
+  __syncthreads();
+  const int64_t groups = (d + 7) >> 3;
+  const int64_t total = num_ids * groups;
+  const uint32_t mask = (1u << k) - 1u;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / groups, g = t - i * groups;
+    const int64_t r = ids32 ? (int64_t)((const int32_t*)ids)[i] : ((const int64_t*)ids)[i];
+    if (r < 0 || r >= n) {
+      if (g == 0) atomicExch(err_flag, FG_EDATA);
+      continue;
+    }
+    const uint8_t* src = rows + r * stride + g * k;
+    uint64_t acc = 0;
+    if (k == 8) {
+      acc = bswap64(*reinterpret_cast<const uint64_t*>(src));
+    } else if (k == 4) {
+      acc = bswap32(*reinterpret_cast<const uint32_t*>(src));
+    } else if (k == 2) {
+      acc = ((uint32_t)src[0] << 8) | src[1];
+    } else {
+      for (int b = 0; b < k; ++b) acc = (acc << 8) | src[b];
+    }
+    const int64_t j0 = g * 8;
+    const int cnt = (int)min64(8, d - j0);
+    OT* o = out + i * d + j0;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      if (e < cnt) {
+        const uint32_t q = (uint32_t)(acc >> (k * (7 - e))) & mask;
+        o[e] = cvt_out<OT>(s_lut[q]);
+      }
+    }
+  }
+}
+
+
+// ------------------------------------------------------ VQ gather decode
+__device__ __forceinline__ uint32_t read_code(const uint8_t* row, int p, int bits) {
+  if (bits == 8) return row[p];
+  const int64_t bit0 = (int64_t)p * bits;
+  const uint8_t* b = row + (bit0 >> 3);
+  const int sh = (int)(bit0 & 7);
+  // up to 16 + 7 bits -> 3 bytes
+  uint32_t w = ((uint32_t)b[0] << 16);
+  if (sh + bits > 8) w |= (uint32_t)b[1] << 8;
+  if (sh + bits > 16) w |= b[2];
+  return (w >> (24 - sh - bits)) & ((1u << bits) - 1u);
+}
+
+template <typename OT>
+__global__ void k_vq_gather(const uint8_t* __restrict__ rows, int64_t n, int64_t d, int bits,
+                            int64_t stride, const float* __restrict__ books, int width,
+                            int length, int parts, const void* ids, int ids32,
+                            int64_t num_ids, OT* __restrict__ out, int32_t* err_flag) {
+  const int64_t total = num_ids * parts;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / parts;
+    const int p = (int)(t - i * parts);
+    const int64_t r = ids32 ? (int64_t)((const int32_t*)ids)[i] : ((const int64_t*)ids)[i];
+    if (r < 0 || r >= n) {
+      if (p == 0) atomicExch(err_flag, FG_EDATA);
+      continue;
+    }
+    const uint32_t c = read_code(rows + r * stride, p, bits);
+    if (c >= (uint32_t)length) { atomicExch(err_flag, FG_EDATA); continue; }
+    const float* e = books + ((int64_t)p * length + c) * width;
+    const int lo = p * width;
+    const int wp = (int)min64(width, d - lo);
+    OT* o = out + i * d + lo;
+    for (int j = 0; j < wp; ++j) store_out(o + j, e[j]);
+  }
+}
+
+// ------------------------------------------------------------ VQ assign
+// numpy's pairwise add.reduce (numpy/_core/src/umath/loops_utils.h.src,
+// pairwise_sum) over the squares of a short vector, with explicit
+// round-to-nearest intrinsics so nvcc cannot contract into FMAs.
+__device__ double np_pairwise_sumsq(const double* v, int n) {
+  if (n < 8) {
+    double r = 0.0;
+    for (int i = 0; i < n; ++i) r = __dadd_rn(r, __dmul_rn(v[i], v[i]));
+    return r;
+  }
+  if (n <= 128) {
+    double r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = __dmul_rn(v[j], v[j]);
+    int i = 8;
+    for (; i < n - (n % 8); i += 8) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], __dmul_rn(v[i + j], v[i + j]));
+    }
+    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+    for (; i < n; ++i) res = __dadd_rn(res, __dmul_rn(v[i], v[i]));
+    return res;
+  }
+  // n > 128: recursive halving (kept iterative-free for the small widths used;
+  // widths > 128 are split the way numpy splits them)
+  int n2 = n / 2;
+  n2 -= n2 % 8;
+  return __dadd_rn(np_pairwise_sumsq(v, n2), np_pairwise_sumsq(v + n2, n - n2));
+}
+
+// OpenBLAS dgemm inner product: FMA chain in k order from 0.
+__device__ __forceinline__ double blas_dot(const double* a, const double* b, int n) {
+  double acc = __dmul_rn(a[0], b[0]);
+  for (int i = 1; i < n; ++i) acc = __fma_rn(a[i], b[i], acc);
+  return acc;
+}
+
+constexpr int kMaxWidth = 64;
+
+// Block = one part x a tile of rows; the part's codebook lives in smem as
+// float64 together with its squared norms (the (c*c).sum(axis=1) term).
+template <typename XT>
+__global__ void k_vq_assign(const XT* __restrict__ x, int64_t n, int64_t d, int width,
+                            int length, int parts, const float* __restrict__ books,
+                            const int32_t* __restrict__ entries, int metric, int bits,
+                            uint8_t* __restrict__ rows, int64_t stride,
+                            int32_t* __restrict__ codes32) {
+  extern __shared__ double s_book[];  // [L][wp] then cc[L]
+  const int p = blockIdx.y;
+  const int lo = p * width;
+  const int wp = (int)min64(width, d - lo);
+  const int L = entries[p];
+  double* s_cc = s_book + (int64_t)length * wp;
+  for (int i = threadIdx.x; i < L * wp; i += blockDim.x) {
+    const int e = i / wp, j = i - e * wp;
+    s_book[i] = (double)books[((int64_t)p * length + e) * width + j];
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < L; e += blockDim.x) s_cc[e] = np_pairwise_sumsq(s_book + e * wp, wp);
+  __syncthreads();
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    double v[kMaxWidth];
+    for (int j = 0; j < wp; ++j) v[j] = (double)x[r * d + lo + j];
+    const double ss = np_pairwise_sumsq(v, wp);
+    int best = 0;
+    if (metric == FG_METRIC_COSINE) {
+      const double nrm = sqrt(ss);  // np.linalg.norm (vq.py:310)
+      if (nrm > 0.0) {
+        for (int j = 0; j < wp; ++j) v[j] = __ddiv_rn(v[j], nrm);
+        double bestv = blas_dot(v, s_book, wp);
+        for (int e = 1; e < L; ++e) {
+          const double s = blas_dot(v, s_book + e * wp, wp);
+          if (s > bestv) { bestv = s; best = e; }  // argmax: first maximum
+        }
+      }
+    } else {
+      double bestv = 0.0;
+      for (int e = 0; e < L; ++e) {
+        // (xx + cc) - 2*dot, then max(., 0): vq.py:155-156
+        double dd = __dadd_rn(__dadd_rn(ss, s_cc[e]),
+                              -__dmul_rn(2.0, blas_dot(v, s_book + e * wp, wp)));
+        dd = dd > 0.0 ? dd : 0.0;
+        if (e == 0 || dd < bestv) { bestv = dd; best = e; }  // argmin: first minimum
+      }
+    }
+    if (codes32) codes32[r * parts + p] = best;
+    if (rows) {
+      // write `bits` bits at bit offset p*bits of the row; parts of a row are
+      // written by different blocks, so use byte-wise atomic OR on words.
+      const int64_t bit0 = (int64_t)p * bits;
+      uint8_t* base = rows + r * stride;
+      const int64_t w0 = bit0 >> 5;  // 32-bit word index in the row
+      const int sh = (int)(bit0 & 31);
+      // big-endian word image: MSB-first bit i of the row sits at bit
+      // (7 - i%8) of byte i/8
+      uint64_t span = (uint64_t)best << (64 - bits - sh);  // aligned in a 64-bit BE window
+      for (int wd = 0; wd < 2; ++wd) {
+        const uint32_t be = (uint32_t)(span >> (32 * (1 - wd)));
+        if (!be) continue;
+        const int64_t wi = w0 + wd;
+        if (wi * 4 >= stride) break;
+        atomicOr(reinterpret_cast<unsigned int*>(base) + wi, bswap32(be));
+      }
+    }
+  }
+}
+
+}  // namespace fg
+
+using namespace fg;
+
+extern "C" {
+
+int fg_stream_to_rows(const uint8_t* stream, int64_t stream_bytes, int64_t n, int64_t row_bits,
+                      uint8_t* rows, int64_t row_stride, void* s) {
+  FG_CHECK_ARG(n >= 0 && row_bits >= 1, "fg_stream_to_rows: bad shape");
+  FG_CHECK_ARG(row_stride >= (row_bits + 7) / 8 && row_stride % 16 == 0,
+               "fg_stream_to_rows: row_stride must be >= row bytes and a multiple of 16");
+  FG_CHECK_ARG(stream_bytes >= (n * row_bits + 7) / 8, "fg_stream_to_rows: stream too short");
+  if (n == 0) return FG_OK;
+  const int64_t total = n * row_stride;
+  k_stream_to_rows<<<grid_for(total, 256), 256, 0, as_stream(s)>>>(stream, stream_bytes, n,
+                                                                   row_bits, rows, row_stride);
+  FG_LAUNCH_CHECK();
+  return FG_OK;
+}
+
+int fg_rows_to_stream(const uint8_t* rows, int64_t n, int64_t row_bits, int64_t row_stride,
+                      uint8_t* stream, int64_t stream_bytes, void* s) {
+  FG_CHECK_ARG(n >= 0 && row_bits >= 1, "fg_rows_to_stream: bad shape");
+  FG_CHECK_ARG(stream_bytes == (n * row_bits + 7) / 8, "fg_rows_to_stream: stream size mismatch");
+  if (stream_bytes == 0) return FG_OK;
+  k_rows_to_stream<<<grid_for(stream_bytes, 256), 256, 0, as_stream(s)>>>(rows, n, row_bits,
+                                                                         row_stride, stream,
+                                                                         stream_bytes);
+  FG_LAUNCH_CHECK();
+  return FG_OK;
+}
+
+int fg_sq_encode(const void* x, int x_is_f64, int64_t n, int64_t d, int k, const float* thr,
+                 const double* thr64, uint8_t* rows, int64_t stride, void* s) {
+  FG_CHECK_ARG(k >= 1 && k <= 8, "k must be in [1, 8], got %d", k);
+  FG_CHECK_ARG(n >= 0 && d >= 1, "fg_sq_encode: bad shape");
+  FG_CHECK_ARG(stride >= (d * k + 7) / 8 && stride % 16 == 0, "fg_sq_encode: bad row_stride");
+  FG_CHECK_ARG(k == 1 || (x_is_f64 ? thr64 != nullptr : thr != nullptr),
+               "fg_sq_encode: thresholds required for k >= 2");
+  if (n == 0) return FG_OK;
+  FG_CUDA_TRY(cudaMemsetAsync(rows, 0, n * stride, as_stream(s)));
+  const int64_t total = n * ((d + 7) / 8);
+  const int grid = grid_for(total, 256);
+  if (x_is_f64)
+    k_sq_encode<double, double><<<grid, 256, 0, as_stream(s)>>>((const double*)x, n, d, k, thr64,
+                                                                rows, stride);
+  else
+    k_sq_encode<float, float><<<grid, 256, 0, as_stream(s)>>>((const float*)x, n, d, k, thr, rows,
+                                                              stride);
+  FG_LAUNCH_CHECK();
+  return FG_OK;
+}
+
+int fg_sq_gather_dequant(const fg_codec_desc* c, const void* ids, int ids32, int64_t num_ids,
+                         void* out, int out_dtype, int32_t* err_flag, void* s) {
+  FG_CHECK_ARG(c && c->kind == FG_CODEC_SQ, "fg_sq_gather_dequant: not an SQ codec");
+  FG_CHECK_ARG(c->bits >= 1 && c->bits <= 8, "fg_sq_gather_dequant: bad k");
+  FG_CHECK_ARG(err_flag != nullptr, "fg_sq_gather_dequant: err_flag required");
+  if (num_ids == 0) return FG_OK;
+  const int64_t total = num_ids * ((c->d + 7) / 8);
+  const int grid = grid_for(total, 256);
+  cudaStream_t st = as_stream(s);
+  if (c->elem_bits == 64) {
+    FG_CHECK_ARG(out_dtype == FG_OUT_F64, "float64 codec decodes to float64");
+    k_sq_gather<double, double><<<grid, 256, 0, st>>>(c->rows, c->n, c->d, c->bits, c->row_stride,
+                                                      (const double*)c->table, ids, ids32, num_ids,
+                                                      (double*)out, err_flag);
+  } else if (out_dtype == FG_OUT_BF16) {
+    k_sq_gather<__nv_bfloat16, float><<<grid, 256, 0, st>>>(c->rows, c->n, c->d, c->bits, c->row_stride,
+                                                    (const float*)c->table, ids, ids32, num_ids,
+                                                    (__nv_bfloat16*)out, err_flag);
+  } else if (out_dtype == FG_OUT_F32) {
+    k_sq_gather<float, float><<<grid, 256, 0, st>>>(c->rows, c->n, c->d, c->bits, c->row_stride,
+                                                    (const float*)c->table, ids, ids32, num_ids,
+                                                    (float*)out, err_flag);
+  } else {
+    FG_CHECK_ARG(false, "fg_sq_gather_dequant: unsupported out dtype %d", out_dtype);
+  }
+  FG_LAUNCH_CHECK();
+  return FG_OK;
+}
+
+int fg_vq_gather_decode(const fg_codec_desc* c, const void* ids, int ids32, int64_t num_ids,
+                        void* out, int out_dtype, int32_t* err_flag, void* s) {
+  FG_CHECK_ARG(c && c->kind == FG_CODEC_VQ, "fg_vq_gather_decode: not a VQ codec");
+  FG_CHECK_ARG(c->bits >= 1 && c->bits <= 16, "fg_vq_gather_decode: bad code bits");
+  FG_CHECK_ARG(err_flag != nullptr, "fg_vq_gather_decode: err_flag required");
+  if (num_ids == 0) return FG_OK;
+  const int64_t total = num_ids * c->num_parts;
+  const int grid = grid_for(total, 256);
+  cudaStream_t st = as_stream(s);
+  if (out_dtype == FG_OUT_F32)
+    k_vq_gather<float><<<grid, 256, 0, st>>>(c->rows, c->n, c->d, c->bits, c->row_stride,
+                                             (const float*)c->table, c->width, c->length,
+                                             c->num_parts, ids, ids32, num_ids, (float*)out,
+                                             err_flag);
+  else if (out_dtype == FG_OUT_F64)
+    k_vq_gather<double><<<grid, 256, 0, st>>>(c->rows, c->n, c->d, c->bits, c->row_stride,
+                                              (const float*)c->table, c->width, c->length,
+                                              c->num_parts, ids, ids32, num_ids, (double*)out,
+                                              err_flag);
+  else if (out_dtype == FG_OUT_BF16)
+    k_vq_gather<__nv_bfloat16><<<grid, 256, 0, st>>>(c->rows, c->n, c->d, c->bits, c->row_stride,
+                                                     (const float*)c->table, c->width, c->length,
+                                                     c->num_parts, ids, ids32, num_ids,
+                                                     (__nv_bfloat16*)out, err_flag);
+  else
+    FG_CHECK_ARG(false, "fg_vq_gather_decode: unsupported out dtype %d", out_dtype);
+  FG_LAUNCH_CHECK();
+  return FG_OK;
+}
+
+int fg_vq_assign(const void* x, int x_is_f64, int64_t n, int64_t d, int width, int length,
+                 int parts, const float* books, const int32_t* entries, int metric, int bits,
+                 uint8_t* rows, int64_t stride, int32_t* codes32, void* s) {
+  FG_CHECK_ARG(width >= 1 && width <= kMaxWidth, "fg_vq_assign: width must be in [1, %d]", kMaxWidth);
+  FG_CHECK_ARG(parts == (int)((d + width - 1) / width), "fg_vq_assign: parts != ceil(d/width)");
+  FG_CHECK_ARG(metric == FG_METRIC_COSINE || metric == FG_METRIC_EUCLIDEAN, "bad metric");
+  FG_CHECK_ARG(rows == nullptr || (stride >= ((int64_t)parts * bits + 7) / 8 && stride % 16 == 0),
+               "fg_vq_assign: bad row_stride");
+  if (n == 0) return FG_OK;
+  const int64_t smem = ((int64_t)length * width + length) * (int64_t)sizeof(double);
+  FG_CHECK_ARG(smem <= 200 * 1024, "fg_vq_assign: codebook part too large for shared memory");
+  cudaStream_t st = as_stream(s);
+  if (rows) FG_CUDA_TRY(cudaMemsetAsync(rows, 0, n * stride, st));
+  const int threads = 128;
+  int gx = (int)min64(ceil_div(n, threads), (int64_t)sm_count() * 32 / parts + 1);
+  dim3 grid(max(gx, 1), parts);
+  if (x_is_f64) {
+    FG_CUDA_TRY(cudaFuncSetAttribute(k_vq_assign<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_vq_assign<double><<<grid, threads, smem, st>>>((const double*)x, n, d, width, length, parts,
+                                                     books, entries, metric, bits, rows, stride,
+                                                     codes32);
+  } else {
+    FG_CUDA_TRY(cudaFuncSetAttribute(k_vq_assign<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_vq_assign<float><<<grid, threads, smem, st>>>((const float*)x, n, d, width, length, parts,
+                                                    books, entries, metric, bits, rows, stride,
+                                                    codes32);
+  }
+  FG_LAUNCH_CHECK();
+  return FG_OK;
+}
+
+}  // extern "C"
+
+// --------------------------------------------------- code layout (VQ)
+namespace fg {
+__global__ void k_codes_to_rows(const int32_t* __restrict__ codes, int64_t n, int parts, int bits,
+                                uint8_t* __restrict__ rows, int64_t stride) {
+  const int64_t row_bytes = ((int64_t)parts * bits + 7) >> 3;
+  const int64_t total = n * stride;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = t / stride, b = t - r * stride;
+    uint32_t v = 0;
+    if (b < row_bytes) {
+      // bits [8b, 8b+8) of the row: gather from the codes that cover them
+      for (int k = 0; k < 8; ++k) {
+        const int64_t g = 8 * b + k;
+        uint32_t bit = 0;
+        if (g < (int64_t)parts * bits) {
+          const int p = (int)(g / bits), o = (int)(g - (int64_t)p * bits);
+          bit = ((uint32_t)codes[r * parts + p] >> (bits - 1 - o)) & 1u;
+        }
+        v = (v << 1) | bit;
+      }
+    }
+    rows[t] = (uint8_t)v;
+  }
+}
+
+// Deterministic per-cluster sums in point order (np.bincount with weights,
+// vq.py:159-164): `order` is a stable sort of points by cluster, `start`
+// the first position of each cluster in it (k+1 entries).
+__global__ void k_segment_sums(const double* __restrict__ pts, int64_t m, int w,
+                               const int64_t* __restrict__ order, const int64_t* __restrict__ start,
+                               int k, double* __restrict__ sums, double* __restrict__ counts) {
+  const int64_t total = (int64_t)k * w;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(t / w), j = (int)(t - (int64_t)c * w);
+    double s = 0.0;
+    for (int64_t i = start[c]; i < start[c + 1]; ++i) s = __dadd_rn(s, pts[order[i] * w + j]);
+    sums[t] = s;
+    if (j == 0) counts[c] = (double)(start[c + 1] - start[c]);
+  }
+}
+}  // namespace fg
+
+extern "C" int fg_codes_to_rows(const int32_t* codes, int64_t n, int parts, int bits,
+                                uint8_t* rows, int64_t stride, void* s) {
+  FG_CHECK_ARG(bits >= 1 && bits <= 16 && parts >= 1, "fg_codes_to_rows: bad shape");
+  FG_CHECK_ARG(stride >= ((int64_t)parts * bits + 7) / 8 && stride % 16 == 0,
+               "fg_codes_to_rows: bad row_stride");
+  if (n == 0) return FG_OK;
+  fg::k_codes_to_rows<<<grid_for(n * stride, 256), 256, 0, as_stream(s)>>>(codes, n, parts, bits,
+                                                                           rows, stride);
+  FG_LAUNCH_CHECK();
+  return FG_OK;
+}
+
+extern "C" int fg_segment_sums(const double* pts, int64_t m, int w, const int64_t* order,
+                               const int64_t* start, int k, double* sums, double* counts,
+                               void* s) {
+  FG_CHECK_ARG(w >= 1 && k >= 1, "fg_segment_sums: bad shape");
+  fg::k_segment_sums<<<grid_for((int64_t)k * w, 128, 16), 128, 0, as_stream(s)>>>(
+      pts, m, w, order, start, k, sums, counts);
+  FG_LAUNCH_CHECK();
+  return FG_OK;
+}

@@ -1,0 +1,190 @@
+"""GraphSAGE mini-batch training on compressed features (new layer L4; the
+reference has no trainer).
+
+Model (mean aggregator): the reference defines aggregation as
+the row-stochastic mean over stored neighbours including the self-loop
+(factors.py:108-114).  Restricted to the sampled blocks:
+    h_{L-1}[v] = act(W_1 · mean_{u in picks(v)} x_u + b_1)   (fused kernel)
+    h_l[v]     = act(W · mean_{u in picks(v)} h_{l+1}[u] + b)
+with fanouts[0] applied at the seeds (pipeline.py:207 convention),
+so the input-side aggregation uses fanouts[-1].
+
+One step = sample (device PCG64 stream) -> fused gather-dequant-mean ->
+bf16 SAGE layers fwd/bwd -> (NCCL all-reduce of the flat gradient) -> Adam.
+Every buffer has a static capacity, so the whole step is captured once into
+a CUDA graph and replayed per batch; the only per-step host traffic is the
+seed ids in and the loss out.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.nn as nn
+import torch.nn.functional as F
+
+from . import ddp
+from .aggregate import block_mean, gather_dequant_mean
+from .sampler import DeviceSampler
+
+
+class SageModel(nn.Module):
+    def __init__(self, in_dim: int, hidden: int, num_classes: int, num_layers: int,
+                 dropout: float = 0.0):
+        super().__init__()
+        dims = [in_dim] + [hidden] * (num_layers - 1) + [num_classes]
+        self.lins = nn.ModuleList(nn.Linear(dims[i], dims[i + 1]) for i in range(num_layers))
+        self.dropout = dropout
+
+    def forward(self, agg_in, sb, caps):
+        """agg_in: [caps[L-1], d] mean of decoded inputs over the last block;
+        sb: SampledBatch; returns logits [caps[0], C]."""
+        L = len(self.lins)
+        h = self.lins[0](agg_in)
+        for i in range(1, L):
+            h = F.relu(h)
+            if self.dropout and self.training:
+                h = F.dropout(h, self.dropout)
+            l = L - 1 - i  # block index feeding this layer
+            a = block_mean(h.to(torch.bfloat16), sb.indptr[l], sb.local[l], sb.n_nodes[l],
+                           caps[l])
+            h = self.lins[i](a)
+        return h
+
+
+@dataclass
+class TrainConfig:
+    fanouts: tuple = (15, 10, 5)
+    batch_size: int = 1024
+    hidden: int = 256
+    lr: float = 3e-3
+    seed: int = 0
+    dropout: float = 0.0
+    use_graph: bool = True
+    agg_dtype: torch.dtype = torch.bfloat16
+
+
+class SageTrainer:
+    """Single-process (or one-rank-of-DDP) trainer over device-resident data."""
+
+    def __init__(self, graph, codec, labels, num_classes: int, cfg: TrainConfig,
+                 process_group=None):
+        self.cfg = cfg
+        self.codec = codec
+        self.labels = labels
+        self.device = labels.device
+        self.pg = process_group
+        self.world = torch.distributed.get_world_size(process_group) if process_group else 1
+        torch.manual_seed(cfg.seed)
+        self.sampler = DeviceSampler(graph, cfg.fanouts, cfg.batch_size, need_local=True)
+        self.caps = self.sampler.caps
+        L = len(cfg.fanouts)
+        self.model = SageModel(codec.d, cfg.hidden, num_classes, L, cfg.dropout).to(self.device)
+        # flat gradient buffer: one all-reduce per step
+        params = list(self.model.parameters())
+        total = sum(p.numel() for p in params)
+        self.flat_grad = torch.zeros(total, dtype=torch.float32, device=self.device)
+        off = 0
+        for p in params:
+            p.grad = self.flat_grad[off:off + p.numel()].view_as(p)
+            off += p.numel()
+        if self.world > 1:  # identical initial weights on every rank
+            for p in params:
+                torch.distributed.broadcast(p.data, 0, group=self.pg)
+        self.opt = torch.optim.Adam(params, lr=cfg.lr, capturable=True)
+        self.loss_buf = torch.zeros((), dtype=torch.float32, device=self.device)
+        self.agg = torch.empty((self.caps[L - 1], codec.d), dtype=cfg.agg_dtype,
+                               device=self.device)
+        self.graph = None
+        self.steps_run = 0
+
+    # ------------------------------------------------------------- step
+    def _body(self):
+        sb = self.sampler.sample_loaded()
+        L = len(self.cfg.fanouts)
+        gather_dequant_mean(self.codec, sb.indptr[L - 1], sb.picks[L - 1], sb.n_nodes[L - 1],
+                            self.caps[L - 1], out=self.agg)
+        with torch.autocast("cuda", dtype=torch.bfloat16):
+            logits = self.model(self.agg, sb, self.caps)
+        seeds = sb.nodes[0].long()
+        valid = torch.arange(self.caps[0], device=self.device) < sb.n_nodes[0]
+        y = torch.where(valid, self.labels[seeds].long(), torch.full_like(seeds, -100))
+        loss = F.cross_entropy(logits.float(), y, ignore_index=-100)
+        self.flat_grad.zero_()
+        loss.backward()
+        ddp.average_flat_(self.flat_grad, self.pg)
+        self.opt.step()
+        self.loss_buf.copy_(loss.detach())
+
+    def capture(self, warmup_batches: int = 3):
+        """Warm up eagerly (allocations, cuBLAS handles, kernel attributes),
+        then capture one step into a CUDA graph."""
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            for b in range(warmup_batches):
+                self.sampler.load_seeds(b % self._nb)
+                self._body()
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self._body()
+        torch.cuda.synchronize()
+
+    def begin_epoch(self, train_ids, epoch: int = 0) -> int:
+        """Seeds are sharded like DDP: rank r takes ids[r::W] with seed
+        seed*W + r + epoch."""
+        r = torch.distributed.get_rank(self.pg) if self.world > 1 else 0
+        shard = ddp.shard_ids(train_ids, r, self.world)
+        self._nb = self.sampler.begin_epoch(shard, ddp.rank_seed(self.cfg.seed, epoch, r,
+                                                                 self.world))
+        self._nb = ddp.agree_num_batches(self._nb, self.pg, self.device)
+        return self._nb
+
+    def step(self, b: int, seeds_host: torch.Tensor | None = None):
+        """One training step on batch b; seeds either device-resident (perm)
+        or copied from a pinned host tensor (end-to-end path)."""
+        if seeds_host is not None:
+            cnt = seeds_host.numel()
+            self.sampler.seed_in[:cnt].copy_(seeds_host, non_blocking=True)
+            self.sampler.n_seed_in.fill_(cnt)
+        else:
+            self.sampler.load_seeds(b)
+        if self.graph is not None:
+            self.graph.replay()
+        else:
+            self._body()
+        self.steps_run += 1
+        return self.loss_buf
+
+    # -------------------------------------------------------- evaluation
+    @torch.no_grad()
+    def evaluate(self, ids, seed: int = 12345, max_batches: int | None = None) -> float:
+        """Accuracy over ``ids`` with the same sampled-block model."""
+        smp = DeviceSampler(self.sampler.g, self.cfg.fanouts, self.cfg.batch_size,
+                            need_local=True)
+        nb = smp.begin_epoch(ids, seed)
+        if max_batches:
+            nb = min(nb, max_batches)
+        L = len(self.cfg.fanouts)
+        agg = torch.empty((smp.caps[L - 1], self.codec.d), dtype=self.cfg.agg_dtype,
+                          device=self.device)
+        correct = torch.zeros((), dtype=torch.int64, device=self.device)
+        total = torch.zeros((), dtype=torch.int64, device=self.device)
+        self.model.eval()
+        for b in range(nb):
+            sb = smp.sample(b)
+            gather_dequant_mean(self.codec, sb.indptr[L - 1], sb.picks[L - 1],
+                                sb.n_nodes[L - 1], smp.caps[L - 1], out=agg)
+            with torch.autocast("cuda", dtype=torch.bfloat16):
+                logits = self.model(agg, sb, smp.caps)
+            valid = torch.arange(smp.caps[0], device=self.device) < sb.n_nodes[0]
+            y = self.labels[sb.nodes[0].long()].long()
+            correct += ((logits.argmax(1) == y) & valid).sum()
+            total += valid.sum()
+        self.model.train()
+        return float(correct.item()) / max(1, int(total.item()))

@@ -1,0 +1,115 @@
+"""Fused gather-dequantize-mean (the north-star hot path) and the hidden block
+mean against the float64 oracle: |gpu - ref| <= tol * mean|x| + 1e-30 with
+tol 1e-5 (fp32 out) / 1e-2 (bf16 out), SURVEY.md §8c."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2207_14696_b200 as fg
+from paper_2207_14696_b200.aggregate import block_mean, gather_dequant_mean
+from oracle import codecs as oc
+from oracle.aggregate import block_mean as oracle_mean
+from oracle.aggregate import mean_tolerance_ok
+
+pytestmark = pytest.mark.gpu
+
+
+def _block(n_src, n_dst, max_dst, fan, rng, zero_frac=0.1):
+    counts = rng.integers(1, fan + 1, n_dst)
+    counts[rng.random(n_dst) < zero_frac] = 0
+    indptr = np.zeros(max_dst + 1, np.int32)
+    indptr[1:n_dst + 1] = np.cumsum(counts)
+    indptr[n_dst + 1:] = indptr[n_dst]
+    src = rng.integers(0, n_src, int(counts.sum())).astype(np.int32)
+    return counts, indptr, src
+
+
+def _run(dc, counts, indptr, src, n_dst, max_dst, dtype):
+    dev = "cuda"
+    out = gather_dequant_mean(dc, torch.from_numpy(indptr).to(dev), torch.from_numpy(src).to(dev),
+                              torch.tensor([n_dst], device=dev), max_dst, out_dtype=dtype)
+    return out.float().cpu().numpy()
+
+
+@pytest.mark.parametrize("k,d", [(8, 128), (4, 128), (8, 100), (3, 100), (1, 64), (2, 37),
+                                 (5, 16), (6, 24), (7, 40)])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_fused_sq_mean(k, d, dtype):
+    rng = np.random.default_rng(k * 100 + d)
+    n = 5000
+    x = (np.exp(rng.normal(0, 1, (n, d))) * rng.choice([-1, 1], (n, d))).astype(np.float32)
+    f = fg.FeatureMatrix(x)
+    c = fg.quantize_sq(f, fg.fit_sq(f, k))
+    dc = fg.DeviceSqCodec.from_codec(c)
+    n_dst, max_dst = 3000, 3200
+    counts, indptr, src = _block(n, n_dst, max_dst, 7, rng)
+    got = _run(dc, counts, indptr, src, n_dst, max_dst, dtype)
+    dec = oc.sq_dequant_rows(c.payload, n, d, k, c.params.e_min, c.params.e_max, src)
+    ref = oracle_mean(dec, counts)
+    tol = 1e-5 if dtype == torch.float32 else 1e-2
+    ok, worst = mean_tolerance_ok(got[:n_dst], ref, dec, counts, tol)
+    assert ok, worst
+    assert (got[n_dst:] == 0).all()
+    assert (got[:n_dst][counts == 0] == 0).all()
+
+
+def _vq_codec(n, d, w, L, rng, metric="cosine"):
+    x = rng.standard_normal((n, d)).astype(np.float32)
+    books = tuple(rng.standard_normal((L, min(w, d - lo))).astype(np.float32)
+                  for lo in range(0, d, w))
+    p = fg.VqParams(w, L, metric=metric)
+    c = fg.encode_vq(fg.FeatureMatrix(x), fg.VqCodec(p, d, books))
+    return c
+
+
+@pytest.mark.parametrize("w,L,d", [(4, 256, 100), (8, 256, 128), (16, 2048, 96), (2, 16, 10),
+                                   (1, 4, 5), (8, 256, 768), (4, 300, 30)])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_fused_vq_mean(w, L, d, dtype):
+    rng = np.random.default_rng(w * 1000 + L + d)
+    n = 4000
+    c = _vq_codec(n, d, w, L, rng)
+    dc = fg.DeviceVqCodec.from_codec(c)
+    n_dst, max_dst = 2500, 2600
+    counts, indptr, src = _block(n, n_dst, max_dst, 6, rng)
+    got = _run(dc, counts, indptr, src, n_dst, max_dst, dtype)
+    dec = oc.vq_decode(c.codes, c.codebooks, d, w, src)
+    ref = oracle_mean(dec, counts)
+    tol = 1e-5 if dtype == torch.float32 else 1e-2
+    ok, worst = mean_tolerance_ok(got[:n_dst], ref, dec, counts, tol)
+    assert ok, worst
+    assert (got[n_dst:] == 0).all()
+
+
+def test_vq_gather_decode_nonbyte_codes():
+    rng = np.random.default_rng(5)
+    c = _vq_codec(3000, 45, 3, 300, rng, metric="euclidean")   # 9-bit codes
+    rows = rng.integers(0, 3000, 777)
+    assert np.array_equal(fg.decode_vq(c, rows).values,
+                          oc.vq_decode(c.codes, c.codebooks, 45, 3, rows))
+
+
+def test_hidden_block_mean_fwd_bwd():
+    rng = np.random.default_rng(3)
+    n_src, n_dst, max_dst, H = 4000, 900, 1000, 256
+    counts, indptr, src = _block(n_src, n_dst, max_dst, 10, rng)
+    dev = "cuda"
+    h = torch.randn(n_src, H, device=dev).to(torch.bfloat16).requires_grad_(True)
+    ip = torch.from_numpy(indptr).to(dev)
+    sl = torch.from_numpy(src).to(dev)
+    out = block_mean(h, ip, sl, torch.tensor([n_dst], device=dev), max_dst)
+    # torch fp32 reference of the same op
+    hf = h.detach().float().requires_grad_(True)
+    seg = torch.repeat_interleave(torch.arange(n_dst, device=dev),
+                                  torch.from_numpy(counts).to(dev))
+    ref = torch.zeros(max_dst, H, device=dev).index_add_(0, seg, hf[sl.long()])
+    cnt = torch.zeros(max_dst, device=dev)
+    cnt[:n_dst] = torch.from_numpy(counts).float().to(dev)
+    ref = ref / cnt.clamp_min(1)[:, None]
+    assert torch.allclose(out.float(), ref, atol=2e-2, rtol=1e-2)
+    g = torch.randn(max_dst, H, device=dev)
+    g[n_dst:] = 0
+    out.backward(g.to(torch.bfloat16))
+    ref.backward(g.to(torch.bfloat16).float())
+    assert torch.allclose(h.grad.float(), hf.grad, atol=2e-2, rtol=1e-2)

@@ -1,0 +1,128 @@
+"""GPU sampler parity: bit-exact seeds, per-node picks (blocks), frontier,
+edges_touched and final PCG64 stream state against the reference's golden
+batches and the CPU oracle (which restates pipeline.py:185-222)."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2207_14696_b200 as fg
+from paper_2207_14696_b200.sampler import DeviceSampler
+from oracle.sampler import sample_batches_oracle
+from test_oracle import _configs
+
+pytestmark = pytest.mark.gpu
+
+
+def test_sample_batches_matches_reference_golden(sampler_golden):
+    z = sampler_golden
+    for ci, gname, fans, bs, seed in _configs(z):
+        n = z[f"graph/{gname}/row_offsets"].size - 1
+        g = fg.CsrGraph(n, z[f"graph/{gname}/row_offsets"], z[f"graph/{gname}/col_indices"])
+        plan = fg.sample_batches(g, z[f"cfg{ci}/train"], fg.SamplerConfig(fans, bs, seed))
+        assert plan.num_batches() == int(z[f"cfg{ci}/nbatches"])
+        for bi, b in enumerate(plan.batches):
+            assert np.array_equal(b.seeds, z[f"cfg{ci}/b{bi}/seeds"]), (ci, bi)
+            assert np.array_equal(b.frontier, z[f"cfg{ci}/b{bi}/frontier"]), (ci, bi)
+            assert b.edges_touched == int(z[f"cfg{ci}/b{bi}/edges"]), (ci, bi)
+
+
+def _blocks(smp, sb, L):
+    out = []
+    for l in range(L):
+        nn_ = int(sb.n_nodes[l].item())
+        ip = sb.indptr[l][:nn_ + 1].cpu().numpy()
+        np_ = int(sb.n_picks[l].item())
+        out.append((sb.nodes[l][:nn_].cpu().numpy(), np.diff(ip),
+                    sb.picks[l][:np_].cpu().numpy(),
+                    None if sb.local[l] is None else sb.local[l][:np_].cpu().numpy()))
+    return out
+
+
+def test_device_sampler_blocks_match_golden(sampler_golden):
+    z = sampler_golden
+    for ci, gname, fans, bs, seed in _configs(z):
+        n = z[f"graph/{gname}/row_offsets"].size - 1
+        g = fg.CsrGraph(n, z[f"graph/{gname}/row_offsets"], z[f"graph/{gname}/col_indices"])
+        smp = DeviceSampler(g.to_device(), fans, bs, need_local=True, unique_last=True)
+        nb = smp.begin_epoch(z[f"cfg{ci}/train"], seed)
+        for bi in range(min(3, nb)):
+            sb = smp.sample(bi)
+            for li, (nodes, counts, picks, local) in enumerate(_blocks(smp, sb, len(fans))):
+                assert np.array_equal(counts, z[f"cfg{ci}/b{bi}/l{li}/counts"]), (ci, bi, li)
+                assert np.array_equal(picks, z[f"cfg{ci}/b{bi}/l{li}/picks"]), (ci, bi, li)
+                if local is not None:
+                    nxt = sb.nodes[li + 1][:int(sb.n_nodes[li + 1].item())].cpu().numpy()
+                    assert np.array_equal(nxt[local], picks)
+        smp.check_errors()
+
+
+def _powerlaw_graph(n, seed):
+    from paper_2207_14696_b200.synth import generate_graph
+    dg, labels = generate_graph(n, 30.0, 8, seed=seed)
+    return dg
+
+
+def test_device_sampler_matches_oracle_on_products_like_graph():
+    dg = _powerlaw_graph(120_000, 3)
+    host = dg.to_host()
+    train = np.arange(0, 120_000, 37)
+    fans, bs, seed = (15, 10, 5), 1024, 4
+    smp = DeviceSampler(dg, fans, bs, need_local=True, want_frontier=True)
+    smp.begin_epoch(train, seed)
+    ref, ref_state = sample_batches_oracle(host.row_offsets, host.col_indices, train, fans, bs,
+                                           seed, max_batches=2)
+    for bi, rb in enumerate(ref):
+        sb = smp.sample(bi)
+        got = _blocks(smp, sb, len(fans))
+        for li, L in enumerate(rb.layers):
+            assert np.array_equal(got[li][0], L.nodes)
+            assert np.array_equal(got[li][1], L.counts)
+            assert np.array_equal(got[li][2], L.picks)
+        nf = int(sb.n_frontier.item())
+        assert np.array_equal(sb.frontier[:nf].cpu().numpy(), rb.frontier)
+    st = smp.stream_state()
+    assert st["state"]["state"] == ref_state["state"]["state"]
+    assert st["has_uint32"] == ref_state["has_uint32"]
+    smp.check_errors()
+
+
+def test_sampler_lemire_rejection_fixup():
+    """Hubs of degree ~3e6 make Lemire rejections likely (p ~ 5e-4 per
+    draw); every rejection shifts all later stream offsets of the layer, which
+    the cooperative fix-up must repair for the picks to stay bit-exact."""
+    hubs, deg = 6, 3_000_017
+    n = hubs + deg
+    # bipartite: hub h connects to all leaves; leaves connect to all hubs
+    off = [0]
+    cols = []
+    leaves = np.arange(hubs, n, dtype=np.int32)
+    for h in range(hubs):
+        c = np.concatenate([[h], leaves]).astype(np.int32)
+        cols.append(c)
+        off.append(off[-1] + c.size)
+    leaf_nb = np.arange(hubs, dtype=np.int32)
+    leaf_cols = np.empty((deg, hubs + 1), np.int32)
+    leaf_cols[:, :hubs] = leaf_nb[None, :]
+    leaf_cols[:, hubs] = leaves
+    cols.append(leaf_cols.reshape(-1))
+    off = np.concatenate([np.array(off, np.int64),
+                          off[-1] + (hubs + 1) * np.arange(1, deg + 1, dtype=np.int64)])
+    col = np.concatenate(cols)
+    g = fg.CsrGraph.trusted(n, off, col, True)
+    dg = g.to_device()
+    train = np.arange(hubs)
+    fans = (200,)
+    total_rej = 0
+    for seed in range(40):
+        smp = DeviceSampler(dg, fans, hubs, need_local=False, want_frontier=True)
+        smp.begin_epoch(train, seed)
+        ref, ref_state = sample_batches_oracle(off, col, train, fans, hubs, seed)
+        sb = smp.sample(0)
+        np_ = int(sb.n_picks[0].item())
+        assert np.array_equal(sb.picks[0][:np_].cpu().numpy(), ref[0].layers[0].picks), seed
+        st = smp.stream_state()
+        assert st["state"]["state"] == ref_state["state"]["state"], seed
+        draws = int(smp.rng[6].item())
+        total_rej += draws - hubs * (2 * 200 - 1)
+    assert total_rej > 0, "no Lemire rejection exercised"
