@@ -226,71 +226,102 @@ __device__ __forceinline__ double blas_dot(const double* a, const double* b, int
 
 constexpr int kMaxWidth = 64;
 
-// Block = one part x a tile of rows; the part's codebook lives in smem as
-// float64 together with its squared norms (the (c*c).sum(axis=1) term).
+// Block = one part x a stripe of rows.  The part's codebook is staged in smem
+// as float64 together with its squared norms (the (c*c).sum(axis=1) term),
+// in tiles of `tile` entries when the whole part does not fit; the running
+// best is carried across tiles with the same strict comparison, so the
+// first-index tie rule is unchanged.
+__device__ __forceinline__ void vq_write_code(uint8_t* rows, int64_t stride, int64_t r, int p,
+                                              int bits, int best) {
+  // `bits` bits at bit offset p*bits of the row; parts of a row are written
+  // by different blocks, so OR big-endian word images atomically.
+  const int64_t bit0 = (int64_t)p * bits;
+  uint8_t* base = rows + r * stride;
+  const int64_t w0 = bit0 >> 5;
+  const int sh = (int)(bit0 & 31);
+  const uint64_t span = (uint64_t)best << (64 - bits - sh);
+  for (int wd = 0; wd < 2; ++wd) {
+    const uint32_t be = (uint32_t)(span >> (32 * (1 - wd)));
+    if (!be) continue;
+    const int64_t wi = w0 + wd;
+    if (wi * 4 >= stride) break;
+    atomicOr(reinterpret_cast<unsigned int*>(base) + wi, bswap32(be));
+  }
+}
+
 template <typename XT>
 __global__ void k_vq_assign(const XT* __restrict__ x, int64_t n, int64_t d, int width,
                             int length, int parts, const float* __restrict__ books,
                             const int32_t* __restrict__ entries, int metric, int bits,
                             uint8_t* __restrict__ rows, int64_t stride,
-                            int32_t* __restrict__ codes32) {
-  extern __shared__ double s_book[];  // [L][wp] then cc[L]
+                            int32_t* __restrict__ codes32, int tile) {
+  extern __shared__ double s_book[];  // [tile][wp] then cc[tile]
   const int p = blockIdx.y;
   const int lo = p * width;
   const int wp = (int)min64(width, d - lo);
   const int L = entries[p];
-  double* s_cc = s_book + (int64_t)length * wp;
-  for (int i = threadIdx.x; i < L * wp; i += blockDim.x) {
-    const int e = i / wp, j = i - e * wp;
-    s_book[i] = (double)books[((int64_t)p * length + e) * width + j];
-  }
-  __syncthreads();
-  for (int e = threadIdx.x; e < L; e += blockDim.x) s_cc[e] = np_pairwise_sumsq(s_book + e * wp, wp);
-  __syncthreads();
-  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
-       r += (int64_t)gridDim.x * blockDim.x) {
+  double* s_cc = s_book + (int64_t)tile * wp;
+  const bool cosine = metric == FG_METRIC_COSINE;
+  auto load_tile = [&](int t0) {
+    const int cnt = min(tile, L - t0);
+    for (int i = threadIdx.x; i < cnt * wp; i += blockDim.x) {
+      const int e = i / wp, j = i - e * wp;
+      s_book[i] = (double)books[((int64_t)p * length + t0 + e) * width + j];
+    }
+    __syncthreads();
+    if (!cosine)
+      for (int e = threadIdx.x; e < cnt; e += blockDim.x)
+        s_cc[e] = np_pairwise_sumsq(s_book + e * wp, wp);
+    __syncthreads();
+  };
+  const bool single = tile >= L;
+  if (single) load_tile(0);
+  const int64_t step = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n; base += step) {
+    const int64_t r = base + threadIdx.x;
+    const bool active = r < n;
     double v[kMaxWidth];
-    for (int j = 0; j < wp; ++j) v[j] = (double)x[r * d + lo + j];
-    const double ss = np_pairwise_sumsq(v, wp);
-    int best = 0;
-    if (metric == FG_METRIC_COSINE) {
-      const double nrm = sqrt(ss);  // np.linalg.norm (vq.py:310)
-      if (nrm > 0.0) {
-        for (int j = 0; j < wp; ++j) v[j] = __ddiv_rn(v[j], nrm);
-        double bestv = blas_dot(v, s_book, wp);
-        for (int e = 1; e < L; ++e) {
-          const double s = blas_dot(v, s_book + e * wp, wp);
-          if (s > bestv) { bestv = s; best = e; }  // argmax: first maximum
+    double ss = 0.0;
+    bool live = active;  // cosine rows with zero norm keep code 0
+    if (active) {
+      for (int j = 0; j < wp; ++j) v[j] = (double)x[r * d + lo + j];
+      ss = np_pairwise_sumsq(v, wp);
+      if (cosine) {
+        const double nrm = sqrt(ss);  // np.linalg.norm (vq.py:310)
+        if (nrm > 0.0) {
+          for (int j = 0; j < wp; ++j) v[j] = __ddiv_rn(v[j], nrm);
+        } else {
+          live = false;
         }
       }
-    } else {
-      double bestv = 0.0;
-      for (int e = 0; e < L; ++e) {
-        // (xx + cc) - 2*dot, then max(., 0): vq.py:155-156
-        double dd = __dadd_rn(__dadd_rn(ss, s_cc[e]),
-                              -__dmul_rn(2.0, blas_dot(v, s_book + e * wp, wp)));
-        dd = dd > 0.0 ? dd : 0.0;
-        if (e == 0 || dd < bestv) { bestv = dd; best = e; }  // argmin: first minimum
+    }
+    int best = 0;
+    double bestv = 0.0;
+    for (int t0 = 0; t0 < L; t0 += tile) {
+      if (!single) {
+        __syncthreads();
+        load_tile(t0);
+      }
+      if (live) {
+        const int cnt = min(tile, L - t0);
+        for (int e = 0; e < cnt; ++e) {
+          const int ge = t0 + e;
+          if (cosine) {
+            const double sv = blas_dot(v, s_book + e * wp, wp);
+            if (ge == 0 || sv > bestv) { bestv = sv; best = ge; }  // argmax: first maximum
+          } else {
+            // (xx + cc) - 2*dot, then max(., 0): vq.py:155-156
+            double dd = __dadd_rn(__dadd_rn(ss, s_cc[e]),
+                                  -__dmul_rn(2.0, blas_dot(v, s_book + e * wp, wp)));
+            dd = dd > 0.0 ? dd : 0.0;
+            if (ge == 0 || dd < bestv) { bestv = dd; best = ge; }  // argmin: first minimum
+          }
+        }
       }
     }
-    if (codes32) codes32[r * parts + p] = best;
-    if (rows) {
-      // write `bits` bits at bit offset p*bits of the row; parts of a row are
-      // written by different blocks, so use byte-wise atomic OR on words.
-      const int64_t bit0 = (int64_t)p * bits;
-      uint8_t* base = rows + r * stride;
-      const int64_t w0 = bit0 >> 5;  // 32-bit word index in the row
-      const int sh = (int)(bit0 & 31);
-      // big-endian word image: MSB-first bit i of the row sits at bit
-      // (7 - i%8) of byte i/8
-      uint64_t span = (uint64_t)best << (64 - bits - sh);  // aligned in a 64-bit BE window
-      for (int wd = 0; wd < 2; ++wd) {
-        const uint32_t be = (uint32_t)(span >> (32 * (1 - wd)));
-        if (!be) continue;
-        const int64_t wi = w0 + wd;
-        if (wi * 4 >= stride) break;
-        atomicOr(reinterpret_cast<unsigned int*>(base) + wi, bswap32(be));
-      }
+    if (active) {
+      if (codes32) codes32[r * parts + p] = best;
+      if (rows) vq_write_code(rows, stride, r, p, bits, best);
     }
   }
 }
@@ -416,8 +447,9 @@ int fg_vq_assign(const void* x, int x_is_f64, int64_t n, int64_t d, int width, i
   FG_CHECK_ARG(rows == nullptr || (stride >= ((int64_t)parts * bits + 7) / 8 && stride % 16 == 0),
                "fg_vq_assign: bad row_stride");
   if (n == 0) return FG_OK;
-  const int64_t smem = ((int64_t)length * width + length) * (int64_t)sizeof(double);
-  FG_CHECK_ARG(smem <= 200 * 1024, "fg_vq_assign: codebook part too large for shared memory");
+  const int64_t budget = 160 * 1024;  // bytes of smem for one codebook tile
+  const int tile = (int)min64(length, budget / ((int64_t)(width + 1) * sizeof(double)));
+  const int64_t smem = ((int64_t)tile * width + tile) * (int64_t)sizeof(double);
   cudaStream_t st = as_stream(s);
   if (rows) FG_CUDA_TRY(cudaMemsetAsync(rows, 0, n * stride, st));
   const int threads = 128;
@@ -427,12 +459,12 @@ int fg_vq_assign(const void* x, int x_is_f64, int64_t n, int64_t d, int width, i
     FG_CUDA_TRY(cudaFuncSetAttribute(k_vq_assign<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k_vq_assign<double><<<grid, threads, smem, st>>>((const double*)x, n, d, width, length, parts,
                                                      books, entries, metric, bits, rows, stride,
-                                                     codes32);
+                                                     codes32, tile);
   } else {
     FG_CUDA_TRY(cudaFuncSetAttribute(k_vq_assign<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k_vq_assign<float><<<grid, threads, smem, st>>>((const float*)x, n, d, width, length, parts,
                                                     books, entries, metric, bits, rows, stride,
-                                                    codes32);
+                                                    codes32, tile);
   }
   FG_LAUNCH_CHECK();
   return FG_OK;
