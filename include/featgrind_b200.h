@@ -165,12 +165,14 @@ int fg_segment_sums(const double* pts, int64_t m, int w, const int64_t* order,
  * where decode is the reference decoder (sq.py:132-153 / vq.py:330-344) and
  * the mean is the row-stochastic operator of factors.py:108-114 restricted
  * to the sample.  fp32 accumulation; destinations with no picks give 0.
- * `num_dst_dev` (device int64) is the live destination count; rows in
- * [live, max_dst) are zero-filled so static-shape consumers stay exact. */
+ * `num_dst_dev` (device int64) is the live destination count; only rows
+ * [0, live) are written (rows past it keep their previous contents, so a
+ * static-capacity buffer zeroed once stays finite).  `out_ld` is the row
+ * pitch in elements (0 = d); columns [d, out_ld) are never written. */
 int fg_gather_dequant_mean(const fg_codec_desc* codec, const int32_t* indptr,
                            const int32_t* src, const int64_t* num_dst_dev,
-                           int64_t max_dst, void* out, int out_dtype,
-                           void* cuda_stream);
+                           int64_t max_dst, void* out, int64_t out_ld,
+                           int out_dtype, void* cuda_stream);
 
 /* Hidden-layer mean over a block with local source indices (bf16 in/out,
  * fp32 accumulate) and its backward (scatter of grad/cnt, fp32 atomics into

@@ -52,7 +52,7 @@ _SIGS = {
     "fg_segment_sums": (ci, [vp, i64, ci, vp, vp, ci, vp, vp, vp]),
     "fg_vq_gather_decode": (ci, [C.POINTER(CodecDesc), vp, ci, i64, vp, ci, vp, vp]),
     "fg_kmeans_assign": (ci, [vp, i64, ci, vp, ci, ci, vp, vp, vp, vp]),
-    "fg_gather_dequant_mean": (ci, [C.POINTER(CodecDesc), vp, vp, vp, i64, vp, ci, vp]),
+    "fg_gather_dequant_mean": (ci, [C.POINTER(CodecDesc), vp, vp, vp, i64, vp, i64, ci, vp]),
     "fg_block_mean_fwd": (ci, [vp, i64, vp, vp, vp, i64, vp, vp]),
     "fg_block_mean_bwd": (ci, [vp, i64, vp, vp, vp, i64, vp, vp]),
     "fg_f32_to_bf16": (ci, [vp, i64, vp, vp]),

@@ -20,14 +20,28 @@ import torch
 from . import _native as N
 
 
+def padded_dim(d: int) -> int:
+    """Row pitch of aggregate buffers: 16-element aligned so the following
+    bf16 GEMM gets an aligned K (d=100 -> 112)."""
+    return (d + 15) // 16 * 16
+
+
+def alloc_aggregate(max_dst: int, d: int, dtype=torch.bfloat16, device="cuda"):
+    """Zeroed [max_dst, padded_dim(d)] buffer; the fused kernel only writes
+    live rows and the first d columns, so padding stays exactly zero."""
+    return torch.zeros((max_dst, padded_dim(d)), dtype=dtype, device=device)
+
+
 def gather_dequant_mean(codec, indptr, src, n_dst, max_dst: int, out=None,
                         out_dtype=torch.bfloat16):
-    """out[v] = mean_{e in indptr[v]:indptr[v+1]} decode(codec, src[e])."""
+    """out[v, :d] = mean_{e in indptr[v]:indptr[v+1]} decode(codec, src[e])
+    for live v < n_dst (rows past n_dst are not written)."""
     if out is None:
-        out = torch.empty((max_dst, codec.d), dtype=out_dtype, device=indptr.device)
+        out = alloc_aggregate(max_dst, codec.d, out_dtype, indptr.device)
+    assert out.shape[0] >= max_dst and out.shape[1] >= codec.d and out.is_contiguous()
     code = N.OUT_BF16 if out.dtype == torch.bfloat16 else N.OUT_F32
     N.call("fg_gather_dequant_mean", ctypes.byref(codec.desc), N.ptr(indptr), N.ptr(src),
-           N.ptr(n_dst), max_dst, N.ptr(out), code, N.stream_handle())
+           N.ptr(n_dst), max_dst, N.ptr(out), out.shape[1], code, N.stream_handle())
     return out
 
 

@@ -27,7 +27,7 @@ import torch.nn as nn
 import torch.nn.functional as F
 
 from . import ddp
-from .aggregate import block_mean, gather_dequant_mean
+from .aggregate import alloc_aggregate, block_mean, gather_dequant_mean, padded_dim
 from .sampler import DeviceSampler
 
 
@@ -82,7 +82,9 @@ class SageTrainer:
         self.sampler = DeviceSampler(graph, cfg.fanouts, cfg.batch_size, need_local=True)
         self.caps = self.sampler.caps
         L = len(cfg.fanouts)
-        self.model = SageModel(codec.d, cfg.hidden, num_classes, L, cfg.dropout).to(self.device)
+        # input layer sees the 16-aligned padded aggregate (zero columns past d)
+        self.model = SageModel(padded_dim(codec.d), cfg.hidden, num_classes, L,
+                               cfg.dropout).to(self.device)
         # flat gradient buffer: one all-reduce per step
         params = list(self.model.parameters())
         total = sum(p.numel() for p in params)
@@ -94,10 +96,9 @@ class SageTrainer:
         if self.world > 1:  # identical initial weights on every rank
             for p in params:
                 torch.distributed.broadcast(p.data, 0, group=self.pg)
-        self.opt = torch.optim.Adam(params, lr=cfg.lr, capturable=True)
+        self.opt = torch.optim.Adam(params, lr=cfg.lr, capturable=True, fused=True)
         self.loss_buf = torch.zeros((), dtype=torch.float32, device=self.device)
-        self.agg = torch.empty((self.caps[L - 1], codec.d), dtype=cfg.agg_dtype,
-                               device=self.device)
+        self.agg = alloc_aggregate(self.caps[L - 1], codec.d, cfg.agg_dtype, self.device)
         self.graph = None
         self.steps_run = 0
 
@@ -171,8 +172,7 @@ class SageTrainer:
         if max_batches:
             nb = min(nb, max_batches)
         L = len(self.cfg.fanouts)
-        agg = torch.empty((smp.caps[L - 1], self.codec.d), dtype=self.cfg.agg_dtype,
-                          device=self.device)
+        agg = alloc_aggregate(smp.caps[L - 1], self.codec.d, self.cfg.agg_dtype, self.device)
         correct = torch.zeros((), dtype=torch.int64, device=self.device)
         total = torch.zeros((), dtype=torch.int64, device=self.device)
         self.model.eval()

@@ -25,11 +25,16 @@ def _block(n_src, n_dst, max_dst, fan, rng, zero_frac=0.1):
     return counts, indptr, src
 
 
-def _run(dc, counts, indptr, src, n_dst, max_dst, dtype):
+def _run(dc, counts, indptr, src, n_dst, max_dst, dtype, pitch=None):
     dev = "cuda"
-    out = gather_dequant_mean(dc, torch.from_numpy(indptr).to(dev), torch.from_numpy(src).to(dev),
-                              torch.tensor([n_dst], device=dev), max_dst, out_dtype=dtype)
-    return out.float().cpu().numpy()
+    pitch = pitch or dc.d
+    out = torch.full((max_dst, pitch), 7.0, dtype=dtype, device=dev)  # sentinel
+    gather_dequant_mean(dc, torch.from_numpy(indptr).to(dev), torch.from_numpy(src).to(dev),
+                        torch.tensor([n_dst], device=dev), max_dst, out=out)
+    o = out.float().cpu().numpy()
+    # rows past the live count and columns past d are never written
+    assert (o[n_dst:] == 7.0).all() and (o[:, dc.d:] == 7.0).all()
+    return o[:, :dc.d]
 
 
 @pytest.mark.parametrize("k,d", [(8, 128), (4, 128), (8, 100), (3, 100), (1, 64), (2, 37),
@@ -44,14 +49,16 @@ def test_fused_sq_mean(k, d, dtype):
     dc = fg.DeviceSqCodec.from_codec(c)
     n_dst, max_dst = 3000, 3200
     counts, indptr, src = _block(n, n_dst, max_dst, 7, rng)
-    got = _run(dc, counts, indptr, src, n_dst, max_dst, dtype)
+    pitch = (d + 15) // 16 * 16 + (16 if d % 2 else 0)
+    got = _run(dc, counts, indptr, src, n_dst, max_dst, dtype, pitch)
     dec = oc.sq_dequant_rows(c.payload, n, d, k, c.params.e_min, c.params.e_max, src)
     ref = oracle_mean(dec, counts)
     tol = 1e-5 if dtype == torch.float32 else 1e-2
     ok, worst = mean_tolerance_ok(got[:n_dst], ref, dec, counts, tol)
     assert ok, worst
-    assert (got[n_dst:] == 0).all()
     assert (got[:n_dst][counts == 0] == 0).all()
+    got2 = _run(dc, counts, indptr, src, n_dst, max_dst, dtype)   # unpadded pitch
+    assert np.array_equal(got2[:n_dst], got[:n_dst])
 
 
 def _vq_codec(n, d, w, L, rng, metric="cosine"):
@@ -63,8 +70,9 @@ def _vq_codec(n, d, w, L, rng, metric="cosine"):
     return c
 
 
-@pytest.mark.parametrize("w,L,d", [(4, 256, 100), (8, 256, 128), (16, 2048, 96), (2, 16, 10),
-                                   (1, 4, 5), (8, 256, 768), (4, 300, 30)])
+@pytest.mark.parametrize("w,L,d", [(4, 256, 100), (8, 256, 100), (8, 256, 128), (16, 2048, 96),
+                                   (2, 16, 10), (1, 4, 5), (1, 256, 70), (2, 256, 33),
+                                   (16, 256, 40), (8, 256, 768), (4, 300, 30)])
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
 def test_fused_vq_mean(w, L, d, dtype):
     rng = np.random.default_rng(w * 1000 + L + d)
@@ -73,13 +81,14 @@ def test_fused_vq_mean(w, L, d, dtype):
     dc = fg.DeviceVqCodec.from_codec(c)
     n_dst, max_dst = 2500, 2600
     counts, indptr, src = _block(n, n_dst, max_dst, 6, rng)
-    got = _run(dc, counts, indptr, src, n_dst, max_dst, dtype)
+    got = _run(dc, counts, indptr, src, n_dst, max_dst, dtype, (d + 15) // 16 * 16)
     dec = oc.vq_decode(c.codes, c.codebooks, d, w, src)
     ref = oracle_mean(dec, counts)
     tol = 1e-5 if dtype == torch.float32 else 1e-2
     ok, worst = mean_tolerance_ok(got[:n_dst], ref, dec, counts, tol)
     assert ok, worst
-    assert (got[n_dst:] == 0).all()
+    got2 = _run(dc, counts, indptr, src, n_dst, max_dst, dtype)
+    assert np.array_equal(got2[:n_dst], got[:n_dst])
 
 
 def test_vq_gather_decode_nonbyte_codes():
