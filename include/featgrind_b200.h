@@ -175,18 +175,20 @@ int fg_gather_dequant_mean(const fg_codec_desc* codec, const int32_t* indptr,
                            int out_dtype, void* cuda_stream);
 
 /* Hidden-layer mean over a block with local source indices (bf16 in/out,
- * fp32 accumulate) and its backward (scatter of grad/cnt, fp32 atomics into
- * `grad_src_f32`, then converted to bf16 by fg_f32_to_bf16). */
+ * fp32 accumulate); `relu_in` applies max(0, .) to source rows on load (the
+ * previous layer's activation, fused).  Backward: scatter of grad/cnt with
+ * fp32 vector atomics into `grad_src_f32` (caller-zeroed), then
+ * fg_f32_to_bf16 converts, multiplying by (relu_mask > 0) when given. */
 int fg_block_mean_fwd(const uint16_t* h_src, int64_t h_dim,
                       const int32_t* indptr, const int32_t* src_local,
                       const int64_t* num_dst_dev, int64_t max_dst,
-                      uint16_t* out, void* cuda_stream);
+                      uint16_t* out, int relu_in, void* cuda_stream);
 int fg_block_mean_bwd(const uint16_t* grad_out, int64_t h_dim,
                       const int32_t* indptr, const int32_t* src_local,
                       const int64_t* num_dst_dev, int64_t max_dst,
                       float* grad_src_f32, void* cuda_stream);
-int fg_f32_to_bf16(const float* in, int64_t count, uint16_t* out,
-                   void* cuda_stream);
+int fg_f32_to_bf16(const float* in, int64_t count, const uint16_t* relu_mask,
+                   uint16_t* out, void* cuda_stream);
 
 /* ------------------------------------------------------------- sampler */
 /* PCG64 state block as used by numpy's default_rng (state, inc, has_uint32,

@@ -53,9 +53,9 @@ _SIGS = {
     "fg_vq_gather_decode": (ci, [C.POINTER(CodecDesc), vp, ci, i64, vp, ci, vp, vp]),
     "fg_kmeans_assign": (ci, [vp, i64, ci, vp, ci, ci, vp, vp, vp, vp]),
     "fg_gather_dequant_mean": (ci, [C.POINTER(CodecDesc), vp, vp, vp, i64, vp, i64, ci, vp]),
-    "fg_block_mean_fwd": (ci, [vp, i64, vp, vp, vp, i64, vp, vp]),
+    "fg_block_mean_fwd": (ci, [vp, i64, vp, vp, vp, i64, vp, ci, vp]),
     "fg_block_mean_bwd": (ci, [vp, i64, vp, vp, vp, i64, vp, vp]),
-    "fg_f32_to_bf16": (ci, [vp, i64, vp, vp]),
+    "fg_f32_to_bf16": (ci, [vp, i64, vp, vp, vp]),
     "fg_rng_init": (ci, [vp, u64, u64, u64, u64, ci, u32]),
     "fg_rng_read": (ci, [vp, C.POINTER(u64), C.POINTER(u64), C.POINTER(ci), C.POINTER(u32)]),
     "fg_rng_permutation_host": (ci, [vp, vp, i64]),

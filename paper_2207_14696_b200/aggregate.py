@@ -46,23 +46,33 @@ def gather_dequant_mean(codec, indptr, src, n_dst, max_dst: int, out=None,
 
 
 class BlockMean(torch.autograd.Function):
-    """h_dst[v] = mean over picks e of v of h_src[local[e]] (bf16, fp32 acc)."""
+    """h_dst[v] = mean over picks e of v of act(h_src[local[e]]) (bf16, fp32
+    accumulate), act = ReLU when ``relu`` (fused on load; its derivative is
+    applied in the backward's fp32 -> bf16 conversion)."""
 
     @staticmethod
-    def forward(ctx, h_src, indptr, local, n_dst, max_dst: int):
+    def forward(ctx, h_src, indptr, local, n_dst, max_dst: int, relu: bool = False):
         h_src = h_src.contiguous()
         H = h_src.shape[1]
         out = torch.empty((max_dst, H), dtype=torch.bfloat16, device=h_src.device)
         N.call("fg_block_mean_fwd", N.ptr(h_src), H, N.ptr(indptr), N.ptr(local), N.ptr(n_dst),
-               max_dst, N.ptr(out), N.stream_handle())
-        ctx.save_for_backward(indptr, local, n_dst)
+               max_dst, N.ptr(out), int(relu), N.stream_handle())
+        if relu:
+            ctx.save_for_backward(indptr, local, n_dst, h_src)
+        else:
+            ctx.save_for_backward(indptr, local, n_dst)
+        ctx.relu = relu
         ctx.max_dst = max_dst
         ctx.n_src = h_src.shape[0]
         return out
 
     @staticmethod
     def backward(ctx, g):
-        indptr, local, n_dst = ctx.saved_tensors
+        if ctx.relu:
+            indptr, local, n_dst, h_src = ctx.saved_tensors
+        else:
+            indptr, local, n_dst = ctx.saved_tensors
+            h_src = None
         g = g.contiguous().to(torch.bfloat16)
         H = g.shape[1]
         acc = torch.zeros((ctx.n_src, H), dtype=torch.float32, device=g.device)
@@ -70,9 +80,9 @@ class BlockMean(torch.autograd.Function):
         N.call("fg_block_mean_bwd", N.ptr(g), H, N.ptr(indptr), N.ptr(local), N.ptr(n_dst),
                ctx.max_dst, N.ptr(acc), s)
         gh = torch.empty((ctx.n_src, H), dtype=torch.bfloat16, device=g.device)
-        N.call("fg_f32_to_bf16", N.ptr(acc), acc.numel(), N.ptr(gh), s)
-        return gh, None, None, None, None
+        N.call("fg_f32_to_bf16", N.ptr(acc), acc.numel(), N.ptr(h_src), N.ptr(gh), s)
+        return gh, None, None, None, None, None
 
 
-def block_mean(h_src, indptr, local, n_dst, max_dst: int):
-    return BlockMean.apply(h_src, indptr, local, n_dst, max_dst)
+def block_mean(h_src, indptr, local, n_dst, max_dst: int, relu: bool = False):
+    return BlockMean.apply(h_src, indptr, local, n_dst, max_dst, relu)

@@ -33,6 +33,9 @@ __device__ __forceinline__ uint4 f32_to_bf16x8(const float* f) {
   return make_uint4(w[0], w[1], w[2], w[3]);
 }
 
+// RELU: apply max(0, .) to the source rows as they are loaded (the SAGE
+// activation of the previous layer, fused so it never makes its own pass).
+template <bool RELU>
 __global__ void __launch_bounds__(256)
 k_block_mean_fwd(const uint16_t* __restrict__ h, int64_t H, const int32_t* __restrict__ indptr,
                  const int32_t* __restrict__ srcl, const int64_t* __restrict__ ndst_dev,
@@ -60,14 +63,14 @@ k_block_mean_fwd(const uint16_t* __restrict__ h, int64_t H, const int32_t* __res
             float f[8];
             bf16x8_to_f32(q[u], f);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) acc[j] += f[j];
+            for (int j = 0; j < 8; ++j) acc[j] += RELU ? fmaxf(f[j], 0.f) : f[j];
           }
         }
       }
       if (cnt) {
-        const float fc = cnt;
+        const float inv = 1.0f / (float)cnt;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[j] = acc[j] / fc;
+        for (int j = 0; j < 8; ++j) acc[j] *= inv;
       }
     }
     reinterpret_cast<uint4*>(out + v * H)[c] = f32_to_bf16x8(acc);
@@ -99,12 +102,21 @@ k_block_mean_bwd(const uint16_t* __restrict__ g, int64_t H, const int32_t* __res
   }
 }
 
-__global__ void k_f32_to_bf16(const float* __restrict__ in, int64_t n8, uint16_t* __restrict__ out) {
+// fp32 gradient accumulator -> bf16; with `mask` (the pre-activation bf16
+// rows) multiplies by relu'(x) = (x > 0), i.e. threshold_backward fused in.
+__global__ void k_f32_to_bf16(const float* __restrict__ in, int64_t n8,
+                              const uint16_t* __restrict__ mask, uint16_t* __restrict__ out) {
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n8;
        t += (int64_t)gridDim.x * blockDim.x) {
     const float4 a = reinterpret_cast<const float4*>(in)[2 * t];
     const float4 b = reinterpret_cast<const float4*>(in)[2 * t + 1];
-    const float f[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    float f[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    if (mask) {
+      float m[8];
+      bf16x8_to_f32(__ldg(reinterpret_cast<const uint4*>(mask) + t), m);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) f[j] = m[j] > 0.f ? f[j] : 0.f;
+    }
     reinterpret_cast<uint4*>(out)[t] = f32_to_bf16x8(f);
   }
 }
@@ -116,12 +128,17 @@ using namespace fg;
 extern "C" {
 
 int fg_block_mean_fwd(const uint16_t* h, int64_t H, const int32_t* indptr, const int32_t* srcl,
-                      const int64_t* ndst, int64_t max_dst, uint16_t* out, void* s) {
+                      const int64_t* ndst, int64_t max_dst, uint16_t* out, int relu_in,
+                      void* s) {
   FG_CHECK_ARG(H % 8 == 0, "hidden dim must be a multiple of 8");
   if (max_dst == 0) return FG_OK;
   const int64_t total = max_dst * (H / 8);
-  k_block_mean_fwd<<<grid_for(total, 256), 256, 0, as_stream(s)>>>(h, H, indptr, srcl, ndst,
-                                                                   max_dst, out);
+  if (relu_in)
+    k_block_mean_fwd<true><<<grid_for(total, 256), 256, 0, as_stream(s)>>>(h, H, indptr, srcl,
+                                                                           ndst, max_dst, out);
+  else
+    k_block_mean_fwd<false><<<grid_for(total, 256), 256, 0, as_stream(s)>>>(h, H, indptr, srcl,
+                                                                            ndst, max_dst, out);
   FG_LAUNCH_CHECK();
   return FG_OK;
 }
@@ -137,10 +154,12 @@ int fg_block_mean_bwd(const uint16_t* g, int64_t H, const int32_t* indptr, const
   return FG_OK;
 }
 
-int fg_f32_to_bf16(const float* in, int64_t count, uint16_t* out, void* s) {
+int fg_f32_to_bf16(const float* in, int64_t count, const uint16_t* relu_mask, uint16_t* out,
+                   void* s) {
   FG_CHECK_ARG(count % 8 == 0, "count must be a multiple of 8");
   if (count == 0) return FG_OK;
-  k_f32_to_bf16<<<grid_for(count / 8, 256), 256, 0, as_stream(s)>>>(in, count / 8, out);
+  k_f32_to_bf16<<<grid_for(count / 8, 256), 256, 0, as_stream(s)>>>(in, count / 8, relu_mask,
+                                                                    out);
   FG_LAUNCH_CHECK();
   return FG_OK;
 }

@@ -45,12 +45,14 @@ class SageModel(nn.Module):
         L = len(self.lins)
         h = self.lins[0](agg_in)
         for i in range(1, L):
-            h = F.relu(h)
-            if self.dropout and self.training:
-                h = F.dropout(h, self.dropout)
             l = L - 1 - i  # block index feeding this layer
-            a = block_mean(h.to(torch.bfloat16), sb.indptr[l], sb.local[l], sb.n_nodes[l],
-                           caps[l])
+            if self.dropout and self.training:
+                h = F.dropout(F.relu(h), self.dropout)
+                a = block_mean(h.to(torch.bfloat16), sb.indptr[l], sb.local[l], sb.n_nodes[l],
+                               caps[l])
+            else:  # ReLU fused into the block-mean gather
+                a = block_mean(h.to(torch.bfloat16), sb.indptr[l], sb.local[l], sb.n_nodes[l],
+                               caps[l], relu=True)
             h = self.lins[i](a)
         return h
 

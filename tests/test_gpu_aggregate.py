@@ -122,3 +122,25 @@ def test_hidden_block_mean_fwd_bwd():
     out.backward(g.to(torch.bfloat16))
     ref.backward(g.to(torch.bfloat16).float())
     assert torch.allclose(h.grad.float(), hf.grad, atol=2e-2, rtol=1e-2)
+
+
+def test_hidden_block_mean_fused_relu():
+    rng = np.random.default_rng(4)
+    n_src, n_dst, max_dst, H = 3000, 700, 800, 128
+    counts, indptr, src = _block(n_src, n_dst, max_dst, 8, rng)
+    dev = "cuda"
+    h = torch.randn(n_src, H, device=dev).to(torch.bfloat16).requires_grad_(True)
+    ip, sl = torch.from_numpy(indptr).to(dev), torch.from_numpy(src).to(dev)
+    out = block_mean(h, ip, sl, torch.tensor([n_dst], device=dev), max_dst, relu=True)
+    hf = h.detach().float().requires_grad_(True)
+    seg = torch.repeat_interleave(torch.arange(n_dst, device=dev), torch.from_numpy(counts).to(dev))
+    ref = torch.zeros(max_dst, H, device=dev).index_add_(0, seg, torch.relu(hf)[sl.long()])
+    cnt = torch.zeros(max_dst, device=dev)
+    cnt[:n_dst] = torch.from_numpy(counts).float().to(dev)
+    ref = ref / cnt.clamp_min(1)[:, None]
+    assert torch.allclose(out.float(), ref, atol=2e-2, rtol=1e-2)
+    g = torch.randn(max_dst, H, device=dev)
+    g[n_dst:] = 0
+    out.backward(g.to(torch.bfloat16))
+    ref.backward(g.to(torch.bfloat16).float())
+    assert torch.allclose(h.grad.float(), hf.grad, atol=2e-2, rtol=1e-2)
