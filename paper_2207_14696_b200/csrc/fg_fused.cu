@@ -28,7 +28,7 @@
 namespace fg {
 
 constexpr int kTD = 128;     // destinations per tile
-constexpr int kSrcCap = kTD * 16;  // staged src ids per tile (fanout <= 16 fully staged)
+constexpr int kSrcCap = kTD * 8;   // staged src ids per tile (fanout <= 8 fully staged)
 
 __device__ __forceinline__ int64_t live_dst(const int64_t* p, int64_t cap) {
   const int64_t v = *p;
@@ -89,21 +89,116 @@ __device__ __forceinline__ void store_scaled(__nv_bfloat16* p, const u64* acc, f
   }
 }
 
-// Stage indptr[v0 .. v0+kTD] (clamped to max_dst) and the tile's src ids.
-__device__ __forceinline__ void stage_tile(const int32_t* __restrict__ indptr,
-                                           const int32_t* __restrict__ src, int64_t v0,
-                                           int64_t max_dst, int32_t* s_ip, int32_t* s_src,
-                                           int32_t& e0, int32_t& ecount) {
-  for (int t = threadIdx.x; t <= kTD; t += blockDim.x) {
-    const int64_t v = min64(v0 + t, max_dst);
-    s_ip[t] = __ldg(indptr + v);
+// ------------------------------------------------------- tile pipeline
+// Each persistent CTA walks tiles tile0, tile0+G, ... of kTD destinations.
+// Two smem buffers hold (indptr slice, src ids).  While tile t is computed,
+// the src ids of tile t+G (whose indptr slice is already in smem) and the
+// indptr slice of tile t+2G are loaded into registers, then stored after the
+// compute phase: the staging round trips overlap the code-row loads.
+constexpr int kThreads = 512;
+constexpr int kSrcPerThread = kSrcCap / kThreads;
+
+struct Stage {
+  int32_t ip;                   // one indptr entry (threads 0..kTD)
+  int32_t src[kSrcPerThread];   // src ids e0 + threadIdx.x + k*kThreads
+};
+
+__device__ __forceinline__ void stage_load_ip(const int32_t* __restrict__ indptr, int64_t tile,
+                                              int64_t max_dst, Stage& st) {
+  if (threadIdx.x <= kTD) st.ip = __ldg(indptr + min64(tile * kTD + threadIdx.x, max_dst));
+}
+__device__ __forceinline__ void stage_store_ip(int32_t* s_ip, const Stage& st) {
+  if (threadIdx.x <= kTD) s_ip[threadIdx.x] = st.ip;
+}
+__device__ __forceinline__ void stage_load_src(const int32_t* __restrict__ src, const int32_t* s_ip,
+                                               Stage& st) {
+  const int32_t e0 = s_ip[0], cnt = s_ip[kTD] - e0;
+  if (cnt > kSrcCap) return;  // compute falls back to global src loads
+#pragma unroll
+  for (int k = 0; k < kSrcPerThread; ++k) {
+    const int t = threadIdx.x + k * kThreads;
+    if (t < cnt) st.src[k] = __ldg(src + e0 + t);
   }
+}
+__device__ __forceinline__ void stage_store_src(int32_t* s_src, const int32_t* s_ip,
+                                                const Stage& st) {
+  const int32_t cnt = s_ip[kTD] - s_ip[0];
+  if (cnt > kSrcCap) return;
+#pragma unroll
+  for (int k = 0; k < kSrcPerThread; ++k) {
+    const int t = threadIdx.x + k * kThreads;
+    if (t < cnt) s_src[t] = st.src[k];
+  }
+}
+
+// Drives the pipeline; `compute(tile, s_ip, s_src)` processes one tile.
+template <typename F>
+__device__ __forceinline__ void tile_pipeline(const int32_t* __restrict__ indptr,
+                                              const int32_t* __restrict__ src, int64_t max_dst,
+                                              int64_t ntiles, int32_t* s_ip0, int32_t* s_ip1,
+                                              int32_t* s_src0, int32_t* s_src1, F&& compute) {
+  const int64_t step = gridDim.x;
+  int64_t tile = blockIdx.x;
+  Stage st, st2;
+  // prologue: buffer 0 <- (ip, src) of tile; buffer 1 <- ip of tile+step
+  stage_load_ip(indptr, tile, max_dst, st);
+  stage_store_ip(s_ip0, st);
   __syncthreads();
-  e0 = s_ip[0];
-  ecount = s_ip[kTD] - e0;
-  if (ecount <= kSrcCap)
-    for (int t = threadIdx.x; t < ecount; t += blockDim.x) s_src[t] = __ldg(src + e0 + t);
+  stage_load_src(src, s_ip0, st);
+  if (tile + step < ntiles) stage_load_ip(indptr, tile + step, max_dst, st2);
+  stage_store_src(s_src0, s_ip0, st);
+  if (tile + step < ntiles) stage_store_ip(s_ip1, st2);
   __syncthreads();
+  bool odd = false;
+  for (; tile < ntiles; tile += step) {
+    int32_t* ip_c = odd ? s_ip1 : s_ip0;
+    int32_t* ip_n = odd ? s_ip0 : s_ip1;
+    int32_t* src_c = odd ? s_src1 : s_src0;
+    int32_t* src_n = odd ? s_src0 : s_src1;
+    const bool has_n = tile + step < ntiles, has_nn = tile + 2 * step < ntiles;
+    if (has_n) stage_load_src(src, ip_n, st);
+    if (has_nn) stage_load_ip(indptr, tile + 2 * step, max_dst, st2);
+    compute(tile, ip_c, src_c);
+    __syncthreads();
+    if (has_n) stage_store_src(src_n, ip_n, st);
+    if (has_nn) stage_store_ip(ip_c, st2);
+    __syncthreads();
+    odd = !odd;
+  }
+}
+
+// --------------------------------------------- bulk async smem fill (TMA)
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+// Thread 0 launches cp.async.bulk copies of `bytes` (multiple of 16) from
+// global to shared, completing on `mbar`; everyone later waits with
+// bulk_wait.  The copy runs on the TMA engine while threads stage tiles.
+__device__ __forceinline__ void bulk_fill(void* dst, const void* src, uint32_t bytes,
+                                          uint64_t* mbar) {
+  if (threadIdx.x == 0) {
+    const uint32_t mb = smem_addr(mbar);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb));
+    asm volatile("fence.proxy.async.shared::cta;");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes));
+    const uint32_t chunk = 32768;
+    for (uint32_t off = 0; off < bytes; off += chunk) {
+      const uint32_t n = bytes - off < chunk ? bytes - off : chunk;
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+          ::"r"(smem_addr((char*)dst + off)), "l"((const char*)src + off), "r"(n), "r"(mb)
+          : "memory");
+    }
+  }
+}
+__device__ __forceinline__ void bulk_wait(uint64_t* mbar) {
+  const uint32_t mb = smem_addr(mbar);
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done) : "r"(mb) : "memory");
+  }
 }
 
 // ------------------------------------------------------------------- SQ
@@ -150,7 +245,7 @@ __device__ __forceinline__ uint32_t sq_code(uint64_t w0, uint64_t w1, int j) {
 }
 
 template <int K, typename OT>
-__global__ void __launch_bounds__(512, 2)
+__global__ void __launch_bounds__(kThreads, 2)
 k_sq_mean(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
           const float* __restrict__ lut, const int32_t* __restrict__ indptr,
           const int32_t* __restrict__ src, const int64_t* __restrict__ ndst_dev,
@@ -159,20 +254,23 @@ k_sq_mean(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
   constexpr int CB = 2 * K;
   constexpr int U = K >= 5 ? 4 : 8;  // picks whose loads are issued together
   extern __shared__ float s_mem[];
-  float* s_lut = s_mem;                                        // [Q][32]
-  int32_t* s_ip = reinterpret_cast<int32_t*>(s_mem + Q * 32);  // [kTD + 1]
-  int32_t* s_src = s_ip + kTD + 1;                             // [kSrcCap]
+  float* s_lut = s_mem;                                          // [Q][32]
+  int32_t* s_ip0 = reinterpret_cast<int32_t*>(s_mem + Q * 32);   // [kTD + 1] x 2
+  int32_t* s_ip1 = s_ip0 + kTD + 1;
+  int32_t* s_src0 = s_ip1 + kTD + 1;                             // [kSrcCap] x 2
+  int32_t* s_src1 = s_src0 + kSrcCap;
   const int lane = threadIdx.x & 31;
-  for (int i = threadIdx.x; i < Q * 32; i += blockDim.x) s_lut[i] = lut[i >> 5];
   const int64_t live = live_dst(ndst_dev, max_dst);
-  const int chunks = (int)((d + 15) >> 4);
   const int64_t ntiles = (live + kTD - 1) / kTD;
+  if ((int64_t)blockIdx.x >= ntiles) return;
+  for (int i = threadIdx.x; i < Q * 32; i += blockDim.x) s_lut[i] = lut[i >> 5];
+  const int chunks = (int)((d + 15) >> 4);
   const bool vec_ok = (ld % 16) == 0;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  tile_pipeline(indptr, src, max_dst, ntiles, s_ip0, s_ip1, s_src0, s_src1,
+                [&](int64_t tile, const int32_t* s_ip, const int32_t* s_src) {
     const int64_t v0 = tile * kTD;
-    int32_t e0, ecount;
-    stage_tile(indptr, src, v0, max_dst, s_ip, s_src, e0, ecount);
-    const bool staged = ecount <= kSrcCap;
+    const int32_t e0 = s_ip[0];
+    const bool staged = s_ip[kTD] - e0 <= kSrcCap;
     const int items = kTD * chunks;
     for (int it = threadIdx.x; it < items; it += blockDim.x) {
       const int vl = it / chunks;
@@ -213,12 +311,12 @@ k_sq_mean(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
       if (j0 + 16 <= d) {
         store_scaled<16>(o, acc, inv, vec_ok);
       } else {
-        for (int j = 0; j < 16 && j0 + j < d; ++j)
-          store_out(o + j, (j & 1 ? hi2(acc[j / 2]) : lo2(acc[j / 2])) * inv);
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (j0 + j < d) store_out(o + j, (j & 1 ? hi2(acc[j / 2]) : lo2(acc[j / 2])) * inv);
       }
     }
-    __syncthreads();  // s_ip / s_src reused by the next tile
-  }
+  });
 }
 
 // ---------------------------------------------------------- VQ (8-bit)
@@ -243,7 +341,7 @@ __device__ __forceinline__ void load_codes(const uint8_t* p, uint32_t* w) {
 }
 
 template <int W, typename OT, bool SMEM>
-__global__ void __launch_bounds__(512, 2)
+__global__ void __launch_bounds__(kThreads, 2)
 k_vq_mean8(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
            const float* __restrict__ books, int length, int parts,
            const int32_t* __restrict__ indptr, const int32_t* __restrict__ src,
@@ -252,28 +350,37 @@ k_vq_mean8(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
   constexpr int G = 32 / W;        // parts per thread
   constexpr int NW = (G + 3) / 4;  // 32-bit code words per load
   constexpr int U = 4;             // picks whose loads are issued together
+  __shared__ __align__(8) uint64_t s_mbar;
   extern __shared__ float4 s_mem4[];
   const int64_t nbook = SMEM ? (int64_t)parts * length * W : 0;
   float* s_book = reinterpret_cast<float*>(s_mem4);
-  int32_t* s_ip = reinterpret_cast<int32_t*>(s_book + ((nbook + 3) & ~3ll));
-  int32_t* s_src = s_ip + kTD + 1;
+  int32_t* s_ip0 = reinterpret_cast<int32_t*>(s_book + ((nbook + 3) & ~3ll));
+  int32_t* s_ip1 = s_ip0 + kTD + 1;
+  int32_t* s_src0 = s_ip1 + kTD + 1;
+  int32_t* s_src1 = s_src0 + kSrcCap;
+  const int64_t live = live_dst(ndst_dev, max_dst);
+  const int64_t ntiles = (live + kTD - 1) / kTD;
+  if ((int64_t)blockIdx.x >= ntiles) return;
   const float* book = books;
+  bool waited = !SMEM;
   if constexpr (SMEM) {
-    const float4* g4 = reinterpret_cast<const float4*>(books);
-    for (int64_t i = threadIdx.x; i < nbook / 4; i += blockDim.x) s_mem4[i] = __ldg(g4 + i);
-    for (int64_t i = (nbook & ~3ll) + threadIdx.x; i < nbook; i += blockDim.x)
-      s_book[i] = __ldg(books + i);
+    // codebook -> smem on the TMA engine, overlapping the tile staging
+    const uint32_t bytes = (uint32_t)(nbook * 4) & ~15u;
+    bulk_fill(s_book, books, bytes, &s_mbar);
+    for (int64_t i = bytes / 4 + threadIdx.x; i < nbook; i += blockDim.x) s_book[i] = __ldg(books + i);
     book = s_book;
   }
-  const int64_t live = live_dst(ndst_dev, max_dst);
   const int groups = (parts + G - 1) / G;
-  const int64_t ntiles = (live + kTD - 1) / kTD;
   const bool vec_ok = (ld % 16) == 0;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  tile_pipeline(indptr, src, max_dst, ntiles, s_ip0, s_ip1, s_src0, s_src1,
+                [&](int64_t tile, const int32_t* s_ip, const int32_t* s_src) {
+    if (!waited) {
+      bulk_wait(&s_mbar);
+      waited = true;
+    }
     const int64_t v0 = tile * kTD;
-    int32_t e0, ecount;
-    stage_tile(indptr, src, v0, max_dst, s_ip, s_src, e0, ecount);
-    const bool staged = ecount <= kSrcCap;
+    const int32_t e0 = s_ip[0];
+    const bool staged = s_ip[kTD] - e0 <= kSrcCap;
     const int items = kTD * groups;
     for (int it = threadIdx.x; it < items; it += blockDim.x) {
       const int vl = it / groups;
@@ -332,33 +439,38 @@ k_vq_mean8(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
       if (np == G && col0 + G * W <= d) {
         store_scaled<G * W>(o, acc, inv, vec_ok);
       } else {
-        for (int j = 0; j < G * W && col0 + j < d; ++j)
-          store_out(o + j, (j & 1 ? hi2(acc[j / 2]) : lo2(acc[j / 2])) * inv);
+#pragma unroll
+        for (int j = 0; j < G * W; ++j)
+          if (col0 + j < d && j < np * W)
+            store_out(o + j, (j & 1 ? hi2(acc[j / 2]) : lo2(acc[j / 2])) * inv);
       }
     }
-    __syncthreads();
-  }
+  });
+  if (!waited) bulk_wait(&s_mbar);  // never leave with a copy in flight
 }
 
 // ------------------------------------------------- VQ (any code width)
 template <int W, typename OT>
-__global__ void __launch_bounds__(512, 2)
+__global__ void __launch_bounds__(kThreads, 2)
 k_vq_mean_bits(const uint8_t* __restrict__ rows, int64_t d, int64_t stride, int bits,
                const float* __restrict__ books, int length, int parts,
                const int32_t* __restrict__ indptr, const int32_t* __restrict__ src,
                const int64_t* __restrict__ ndst_dev, int64_t max_dst, OT* __restrict__ out,
                int64_t ld) {
   extern __shared__ int32_t s_stage[];
-  int32_t* s_ip = s_stage;
-  int32_t* s_src = s_ip + kTD + 1;
+  int32_t* s_ip0 = s_stage;
+  int32_t* s_ip1 = s_ip0 + kTD + 1;
+  int32_t* s_src0 = s_ip1 + kTD + 1;
+  int32_t* s_src1 = s_src0 + kSrcCap;
   const int64_t live = live_dst(ndst_dev, max_dst);
   const int64_t ntiles = (live + kTD - 1) / kTD;
+  if ((int64_t)blockIdx.x >= ntiles) return;
   const uint32_t cmask = (1u << bits) - 1u;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  tile_pipeline(indptr, src, max_dst, ntiles, s_ip0, s_ip1, s_src0, s_src1,
+                [&](int64_t tile, const int32_t* s_ip, const int32_t* s_src) {
     const int64_t v0 = tile * kTD;
-    int32_t e0, ecount;
-    stage_tile(indptr, src, v0, max_dst, s_ip, s_src, e0, ecount);
-    const bool staged = ecount <= kSrcCap;
+    const int32_t e0 = s_ip[0];
+    const bool staged = s_ip[kTD] - e0 <= kSrcCap;
     const int items = kTD * parts;
     for (int it = threadIdx.x; it < items; it += blockDim.x) {
       const int vl = it / parts;
@@ -385,22 +497,23 @@ k_vq_mean_bits(const uint8_t* __restrict__ rows, int64_t d, int64_t stride, int 
       }
       const float inv = cnt ? 1.0f / (float)cnt : 0.0f;
       OT* o = out + v * ld + (int64_t)p * W;
-      for (int j = 0; j < W && (int64_t)p * W + j < d; ++j) store_out(o + j, acc[j] * inv);
+#pragma unroll
+      for (int j = 0; j < W; ++j)
+        if ((int64_t)p * W + j < d) store_out(o + j, acc[j] * inv);
     }
-    __syncthreads();
-  }
+  });
 }
 
 // ------------------------------------------------------------ launchers
 template <int K, typename OT>
 int launch_sq(const fg_codec_desc* c, const int32_t* indptr, const int32_t* src,
               const int64_t* ndst, int64_t max_dst, void* out, int64_t ld, cudaStream_t st) {
-  const int smem = (1 << K) * 32 * 4 + (kTD + 1 + kSrcCap) * 4;
+  const int smem = (1 << K) * 32 * 4 + 2 * (kTD + 1 + kSrcCap) * 4;
   auto kern = k_sq_mean<K, OT>;
   FG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const int grid = (int)min64(ceil_div(max_dst, kTD), (int64_t)sm_count() * 2);
-  kern<<<grid, 512, smem, st>>>(c->rows, c->d, c->row_stride, (const float*)c->table, indptr,
-                                src, ndst, max_dst, (OT*)out, ld);
+  kern<<<grid, kThreads, smem, st>>>(c->rows, c->d, c->row_stride, (const float*)c->table,
+                                     indptr, src, ndst, max_dst, (OT*)out, ld);
   FG_LAUNCH_CHECK();
   return FG_OK;
 }
@@ -426,12 +539,12 @@ template <int W, typename OT>
 int launch_vq(const fg_codec_desc* c, const int32_t* indptr, const int32_t* src,
               const int64_t* ndst, int64_t max_dst, void* out, int64_t ld, cudaStream_t st) {
   const int64_t book_bytes = (int64_t)c->num_parts * c->length * W * 4;
-  const int64_t stage_bytes = (kTD + 1 + kSrcCap) * 4;
+  const int64_t stage_bytes = 2 * (kTD + 1 + kSrcCap) * 4;
   const int64_t ntiles = ceil_div(max_dst, kTD);
   if (c->bits != 8) {
     auto kern = k_vq_mean_bits<W, OT>;
     const int grid = (int)min64(ntiles, (int64_t)sm_count() * 2);
-    kern<<<grid, 512, stage_bytes, st>>>(c->rows, c->d, c->row_stride, c->bits,
+    kern<<<grid, kThreads, stage_bytes, st>>>(c->rows, c->d, c->row_stride, c->bits,
                                          (const float*)c->table, c->length, c->num_parts, indptr,
                                          src, ndst, max_dst, (OT*)out, ld);
     FG_LAUNCH_CHECK();
@@ -444,13 +557,13 @@ int launch_vq(const fg_codec_desc* c, const int32_t* indptr, const int32_t* src,
     FG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem2));
     const int grid = (int)min64(ntiles, (int64_t)sm_count() * per_sm);
-    kern<<<grid, 512, smem2, st>>>(c->rows, c->d, c->row_stride, (const float*)c->table,
+    kern<<<grid, kThreads, smem2, st>>>(c->rows, c->d, c->row_stride, (const float*)c->table,
                                    c->length, c->num_parts, indptr, src, ndst, max_dst, (OT*)out,
                                    ld);
   } else {
     auto kern = k_vq_mean8<W, OT, false>;
     const int grid = (int)min64(ntiles, (int64_t)sm_count() * 2);
-    kern<<<grid, 512, stage_bytes, st>>>(c->rows, c->d, c->row_stride, (const float*)c->table,
+    kern<<<grid, kThreads, stage_bytes, st>>>(c->rows, c->d, c->row_stride, (const float*)c->table,
                                          c->length, c->num_parts, indptr, src, ndst, max_dst,
                                          (OT*)out, ld);
   }

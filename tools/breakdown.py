@@ -59,6 +59,23 @@ def main():
         gather_dequant_mean(dc, sb.indptr[L - 1], sb.picks[L - 1], sb.n_nodes[L - 1],
                             tr.caps[L - 1], out=tr.agg)
 
+    def fwd_part():
+        with torch.autocast("cuda", dtype=torch.bfloat16):
+            logits = tr.model(tr.agg, sb, tr.caps)
+        seeds = sb.nodes[0].long()
+        valid = torch.arange(tr.caps[0], device=dev) < sb.n_nodes[0]
+        y = torch.where(valid, tr.labels[seeds].long(), torch.full_like(seeds, -100))
+        return F.cross_entropy(logits.float(), y, ignore_index=-100)
+
+    gf, gfb, go = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gf):
+        fwd_part()
+    with torch.cuda.graph(gfb):
+        tr.flat_grad.zero_()
+        fwd_part().backward()
+    with torch.cuda.graph(go):
+        tr.opt.step()
+
     def model_part():
         with torch.autocast("cuda", dtype=torch.bfloat16):
             logits = tr.model(tr.agg, sb, tr.caps)
@@ -75,7 +92,8 @@ def main():
         tr._body()
     torch.cuda.synchronize()
     out = {"config": desc}
-    for name, g in [("sample", gs), ("aggregate", ga), ("model", gm), ("full_step", gfull)]:
+    for name, g in [("sample", gs), ("aggregate", ga), ("model", gm), ("fwd", gf),
+                    ("fwd_bwd", gfb), ("adam", go), ("full_step", gfull)]:
         out[name + "_us"] = round(timed(g, a.reps, flush), 1)
         out[name + "_warm_us"] = round(timed(g, a.reps, None), 1)
     out["live"] = [int(x.item()) for x in sb.n_nodes] + [int(sb.n_picks[-1].item())]

@@ -21,6 +21,8 @@ def main():
     ap.add_argument("--scale", type=float, default=1.0)
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
+    # run backward on this thread so its kernels fall inside the NVTX range
+    torch.autograd.set_multithreading_enabled(False)
     sg, dc, desc, fanouts, bs, hidden = bench.build_workload(a.config, dev, scale=a.scale)
     tr = SageTrainer(sg.graph, dc, sg.labels, sg.num_classes,
                      TrainConfig(fanouts=fanouts, batch_size=bs, hidden=hidden))
