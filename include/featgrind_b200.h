@@ -190,6 +190,33 @@ int fg_block_mean_bwd(const uint16_t* grad_out, int64_t h_dim,
 int fg_f32_to_bf16(const float* in, int64_t count, const uint16_t* relu_mask,
                    uint16_t* out, void* cuda_stream);
 
+/* Gather-form backward of the hidden block mean (deterministic, no float
+ * atomics).  fg_block_transpose writes unique keys (local_rank << 32 | edge)
+ * for the block's edges (INT64_MAX past the live edge count); after the
+ * caller sorts them ascending, fg_block_transpose_finish derives the
+ * transposed CSR t_indptr [cap_src + 1] and the dst of every edge t_dst;
+ * fg_block_mean_bwd_t then computes, for every source row r < cap_src,
+ *   out[r] = relu'(mask[r]) * sum_{i in t_indptr[r]..} g[t_dst[i]] / cnt(t_dst[i])
+ * in edge order (rows without edges get 0). */
+int fg_block_transpose(const int32_t* src_local, const int64_t* n_edges_dev,
+                       int64_t cap_e, int64_t* keys, void* cuda_stream);
+int fg_block_transpose_finish(const int64_t* sorted_keys,
+                              const int64_t* n_edges_dev, int64_t cap_e,
+                              const int32_t* indptr, const int64_t* num_dst_dev,
+                              int64_t max_dst, int64_t cap_src,
+                              int32_t* t_indptr, int32_t* t_dst, void* cuda_stream);
+int fg_block_mean_bwd_t(const uint16_t* grad_out, int64_t h_dim,
+                        const int32_t* t_indptr, const int32_t* t_dst,
+                        const int32_t* indptr, int64_t cap_src,
+                        const uint16_t* relu_mask, uint16_t* out, void* cuda_stream);
+
+/* Adam (torch.optim.Adam semantics) over a flat fp32 parameter buffer with
+ * a device step counter (graph-capturable; one update kernel). */
+int fg_adam_step(float* params, const float* grads, float* exp_avg,
+                 float* exp_avg_sq, int64_t n, int64_t* step_dev, float lr,
+                 float beta1, float beta2, float eps, float weight_decay,
+                 void* cuda_stream);
+
 /* ------------------------------------------------------------- sampler */
 /* PCG64 state block as used by numpy's default_rng (state, inc, has_uint32,
  * uinteger) followed by a 64-entry jump table; FG_RNG_WORDS uint64 words. */

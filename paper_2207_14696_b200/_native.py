@@ -56,6 +56,11 @@ _SIGS = {
     "fg_block_mean_fwd": (ci, [vp, i64, vp, vp, vp, i64, vp, ci, vp]),
     "fg_block_mean_bwd": (ci, [vp, i64, vp, vp, vp, i64, vp, vp]),
     "fg_f32_to_bf16": (ci, [vp, i64, vp, vp, vp]),
+    "fg_block_transpose": (ci, [vp, vp, i64, vp, vp]),
+    "fg_block_transpose_finish": (ci, [vp, vp, i64, vp, vp, i64, i64, vp, vp, vp]),
+    "fg_block_mean_bwd_t": (ci, [vp, i64, vp, vp, vp, i64, vp, vp, vp]),
+    "fg_adam_step": (ci, [vp, vp, vp, vp, i64, vp, C.c_float, C.c_float, C.c_float, C.c_float,
+                          C.c_float, vp]),
     "fg_rng_init": (ci, [vp, u64, u64, u64, u64, ci, u32]),
     "fg_rng_read": (ci, [vp, C.POINTER(u64), C.POINTER(u64), C.POINTER(ci), C.POINTER(u32)]),
     "fg_rng_permutation_host": (ci, [vp, vp, i64]),

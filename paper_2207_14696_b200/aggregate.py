@@ -21,15 +21,22 @@ from . import _native as N
 
 
 def padded_dim(d: int) -> int:
-    """Row pitch of aggregate buffers: 16-element aligned so the following
-    bf16 GEMM gets an aligned K (d=100 -> 112)."""
-    return (d + 15) // 16 * 16
+    """Row pitch of aggregate buffers: 16-element aligned (so the following
+    bf16 GEMM gets an aligned K) with at least one spare column, which holds
+    a constant 1 so the first layer's bias rides inside its weight GEMM
+    (d=100 -> 112, d=128 -> 144)."""
+    return (d + 1 + 15) // 16 * 16
 
 
-def alloc_aggregate(max_dst: int, d: int, dtype=torch.bfloat16, device="cuda"):
-    """Zeroed [max_dst, padded_dim(d)] buffer; the fused kernel only writes
-    live rows and the first d columns, so padding stays exactly zero."""
-    return torch.zeros((max_dst, padded_dim(d)), dtype=dtype, device=device)
+def alloc_aggregate(max_dst: int, d: int, dtype=torch.bfloat16, device="cuda",
+                    ones_col: bool = True):
+    """[max_dst, padded_dim(d)] buffer, zero except column d = 1 (bias
+    input).  The fused kernel only writes live rows and the first d
+    columns, so the padding keeps these values."""
+    out = torch.zeros((max_dst, padded_dim(d)), dtype=dtype, device=device)
+    if ones_col:
+        out[:, d] = 1
+    return out
 
 
 def gather_dequant_mean(codec, indptr, src, n_dst, max_dst: int, out=None,
@@ -51,38 +58,43 @@ class BlockMean(torch.autograd.Function):
     applied in the backward's fp32 -> bf16 conversion)."""
 
     @staticmethod
-    def forward(ctx, h_src, indptr, local, n_dst, max_dst: int, relu: bool = False):
+    def forward(ctx, h_src, indptr, local, n_dst, max_dst: int, relu: bool = False,
+                trans=None):
         h_src = h_src.contiguous()
         H = h_src.shape[1]
         out = torch.empty((max_dst, H), dtype=torch.bfloat16, device=h_src.device)
         N.call("fg_block_mean_fwd", N.ptr(h_src), H, N.ptr(indptr), N.ptr(local), N.ptr(n_dst),
                max_dst, N.ptr(out), int(relu), N.stream_handle())
-        if relu:
-            ctx.save_for_backward(indptr, local, n_dst, h_src)
-        else:
-            ctx.save_for_backward(indptr, local, n_dst)
+        t_indptr, t_dst = trans if trans is not None else (indptr, indptr)
+        ctx.save_for_backward(indptr, local, n_dst, h_src if relu else indptr, t_indptr, t_dst)
         ctx.relu = relu
+        ctx.gather_bwd = trans is not None
         ctx.max_dst = max_dst
         ctx.n_src = h_src.shape[0]
         return out
 
     @staticmethod
     def backward(ctx, g):
-        if ctx.relu:
-            indptr, local, n_dst, h_src = ctx.saved_tensors
-        else:
-            indptr, local, n_dst = ctx.saved_tensors
+        indptr, local, n_dst, h_src, t_indptr, t_dst = ctx.saved_tensors
+        if not ctx.relu:
             h_src = None
         g = g.contiguous().to(torch.bfloat16)
         H = g.shape[1]
+        if ctx.gather_bwd:  # deterministic gather over the block's transpose
+            gh = torch.empty((ctx.n_src, H), dtype=torch.bfloat16, device=g.device)
+            N.call("fg_block_mean_bwd_t", N.ptr(g), H, N.ptr(t_indptr), N.ptr(t_dst),
+                   N.ptr(indptr), ctx.n_src, N.ptr(h_src), N.ptr(gh), N.stream_handle())
+            return gh, None, None, None, None, None, None
         acc = torch.zeros((ctx.n_src, H), dtype=torch.float32, device=g.device)
         s = N.stream_handle()
         N.call("fg_block_mean_bwd", N.ptr(g), H, N.ptr(indptr), N.ptr(local), N.ptr(n_dst),
                ctx.max_dst, N.ptr(acc), s)
         gh = torch.empty((ctx.n_src, H), dtype=torch.bfloat16, device=g.device)
         N.call("fg_f32_to_bf16", N.ptr(acc), acc.numel(), N.ptr(h_src), N.ptr(gh), s)
-        return gh, None, None, None, None, None
+        return gh, None, None, None, None, None, None
 
 
-def block_mean(h_src, indptr, local, n_dst, max_dst: int, relu: bool = False):
-    return BlockMean.apply(h_src, indptr, local, n_dst, max_dst, relu)
+def block_mean(h_src, indptr, local, n_dst, max_dst: int, relu: bool = False, trans=None):
+    """``trans`` = (t_indptr, t_dst) of the block (DeviceSampler with
+    need_transpose) switches the backward to the deterministic gather."""
+    return BlockMean.apply(h_src, indptr, local, n_dst, max_dst, relu, trans)

@@ -165,3 +165,162 @@ int fg_f32_to_bf16(const float* in, int64_t count, const uint16_t* relu_mask, ui
 }
 
 }  // extern "C"
+
+// ------------------------------------------- gather-form (transposed) bwd
+// The block's transpose (source rank -> incoming edges) lets the backward of
+// the hidden block mean be a deterministic gather instead of fp32 atomics:
+//   grad_src[r] = act'(h[r]) * sum_{e in in(r)} grad_out[dst(e)] / cnt(dst(e))
+// summed in edge order.  Built per batch from unique 64-bit keys
+// (rank << 32 | edge), so any sort yields the same order.
+namespace fg {
+
+__global__ void k_transpose_keys(const int32_t* __restrict__ local, const int64_t* __restrict__ ne_dev,
+                                 int64_t cap_e, int64_t* __restrict__ keys) {
+  const int64_t ne = min64(*ne_dev, cap_e);
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < cap_e;
+       e += (int64_t)gridDim.x * blockDim.x)
+    keys[e] = e < ne ? (((int64_t)local[e] << 32) | e) : INT64_MAX;
+}
+
+// sorted keys -> t_indptr [cap_src + 1] and t_dst [cap_e] (dst of each edge)
+__global__ void k_transpose_finish(const int64_t* __restrict__ keys, const int64_t* __restrict__ ne_dev,
+                                   int64_t cap_e, const int32_t* __restrict__ indptr,
+                                   const int64_t* __restrict__ nd_dev, int64_t max_dst,
+                                   int64_t cap_src, int32_t* __restrict__ t_indptr,
+                                   int32_t* __restrict__ t_dst) {
+  const int64_t ne = min64(*ne_dev, cap_e);
+  const int64_t nd = min64(*nd_dev, max_dst);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= ne;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i < ne ? (keys[i] >> 32) : cap_src;
+    const int64_t rp = i > 0 ? (keys[i - 1] >> 32) : -1;
+    for (int64_t q = rp + 1; q <= r && q <= cap_src; ++q) t_indptr[q] = (int32_t)i;
+    if (i < ne) {
+      const int32_t e = (int32_t)(keys[i] & 0xFFFFFFFFll);
+      int64_t lo = 0, hi = nd;  // last v with indptr[v] <= e
+      while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (indptr[mid] <= e) lo = mid; else hi = mid;
+      }
+      t_dst[i] = (int32_t)lo;
+    }
+  }
+}
+
+template <bool RELU>
+__global__ void __launch_bounds__(256)
+k_block_mean_bwd_t(const uint16_t* __restrict__ g, int64_t H, const int32_t* __restrict__ t_indptr,
+                   const int32_t* __restrict__ t_dst, const int32_t* __restrict__ indptr,
+                   int64_t cap_src, const uint16_t* __restrict__ mask, uint16_t* __restrict__ out) {
+  const int64_t chunks = H >> 3;
+  const int64_t total = cap_src * chunks;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = t / chunks, c = t - r * chunks;
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const int32_t i0 = t_indptr[r], i1 = t_indptr[r + 1];
+    for (int32_t i = i0; i < i1; i += 4) {
+      uint4 q[4];
+      float sc[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (i + u < i1) {
+          const int32_t v = t_dst[i + u];
+          sc[u] = 1.0f / (float)(indptr[v + 1] - indptr[v]);
+          q[u] = __ldg(reinterpret_cast<const uint4*>(g + (int64_t)v * H) + c);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (i + u < i1) {
+          float f[8];
+          bf16x8_to_f32(q[u], f);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc[j] = fmaf(f[j], sc[u], acc[j]);
+        }
+      }
+    }
+    if (RELU) {
+      float m[8];
+      bf16x8_to_f32(__ldg(reinterpret_cast<const uint4*>(mask + r * H) + c), m);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] = m[j] > 0.f ? acc[j] : 0.f;
+    }
+    reinterpret_cast<uint4*>(out + r * H)[c] = f32_to_bf16x8(acc);
+  }
+}
+
+// ----------------------------------------------------------- flat Adam
+// torch.optim.Adam semantics (L2 weight decay folded into the gradient) over
+// one flat fp32 parameter buffer; the step counter lives on the device so
+// the update can sit inside a CUDA graph.
+__global__ void k_adam(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
+                       float* __restrict__ v, int64_t n, const int64_t* __restrict__ step,
+                       float lr, float b1, float b2, float eps, float wd) {
+  const int64_t t = *step + 1;
+  const float bc1 = 1.0f - powf(b1, (float)t);
+  const float bc2 = 1.0f - powf(b2, (float)t);
+  const float step_size = lr / bc1;
+  const float bc2_sqrt = sqrtf(bc2);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float gi = g[i];
+    if (wd != 0.f) gi += wd * p[i];
+    const float mi = b1 * m[i] + (1.0f - b1) * gi;
+    const float vi = b2 * v[i] + (1.0f - b2) * gi * gi;
+    m[i] = mi;
+    v[i] = vi;
+    p[i] -= step_size * mi / (sqrtf(vi) / bc2_sqrt + eps);
+  }
+}
+__global__ void k_step_inc(int64_t* step) { *step += 1; }
+
+}  // namespace fg
+
+extern "C" int fg_block_transpose(const int32_t* local, const int64_t* n_edges_dev, int64_t cap_e,
+                                  int64_t* keys, void* s) {
+  if (cap_e == 0) return FG_OK;
+  fg::k_transpose_keys<<<grid_for(cap_e, 256), 256, 0, as_stream(s)>>>(local, n_edges_dev, cap_e,
+                                                                       keys);
+  FG_LAUNCH_CHECK();
+  return FG_OK;
+}
+
+extern "C" int fg_block_transpose_finish(const int64_t* sorted_keys, const int64_t* n_edges_dev,
+                                         int64_t cap_e, const int32_t* indptr,
+                                         const int64_t* n_dst_dev, int64_t max_dst,
+                                         int64_t cap_src, int32_t* t_indptr, int32_t* t_dst,
+                                         void* s) {
+  fg::k_transpose_finish<<<grid_for(cap_e + 1, 256), 256, 0, as_stream(s)>>>(
+      sorted_keys, n_edges_dev, cap_e, indptr, n_dst_dev, max_dst, cap_src, t_indptr, t_dst);
+  FG_LAUNCH_CHECK();
+  return FG_OK;
+}
+
+extern "C" int fg_block_mean_bwd_t(const uint16_t* g, int64_t H, const int32_t* t_indptr,
+                                   const int32_t* t_dst, const int32_t* indptr, int64_t cap_src,
+                                   const uint16_t* relu_mask, uint16_t* out, void* s) {
+  FG_CHECK_ARG(H % 8 == 0, "hidden dim must be a multiple of 8");
+  if (cap_src == 0) return FG_OK;
+  const int64_t total = cap_src * (H / 8);
+  if (relu_mask)
+    fg::k_block_mean_bwd_t<true><<<grid_for(total, 256), 256, 0, as_stream(s)>>>(
+        g, H, t_indptr, t_dst, indptr, cap_src, relu_mask, out);
+  else
+    fg::k_block_mean_bwd_t<false><<<grid_for(total, 256), 256, 0, as_stream(s)>>>(
+        g, H, t_indptr, t_dst, indptr, cap_src, nullptr, out);
+  FG_LAUNCH_CHECK();
+  return FG_OK;
+}
+
+extern "C" int fg_adam_step(float* params, const float* grads, float* m, float* v, int64_t n,
+                            int64_t* step_dev, float lr, float beta1, float beta2, float eps,
+                            float weight_decay, void* s) {
+  if (n == 0) return FG_OK;
+  fg::k_adam<<<grid_for(n, 256, 4), 256, 0, as_stream(s)>>>(params, grads, m, v, n, step_dev, lr,
+                                                            beta1, beta2, eps, weight_decay);
+  FG_LAUNCH_CHECK();
+  fg::k_step_inc<<<1, 1, 0, as_stream(s)>>>(step_dev);
+  FG_LAUNCH_CHECK();
+  return FG_OK;
+}

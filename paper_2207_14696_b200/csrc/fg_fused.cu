@@ -167,6 +167,15 @@ __device__ __forceinline__ void tile_pipeline(const int32_t* __restrict__ indptr
   }
 }
 
+// one 16-byte shared-memory load (keeps the compiler from splitting it)
+__device__ __forceinline__ float4 lds128(const float* p) {
+  float4 r;
+  asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "r"((uint32_t)__cvta_generic_to_shared(p)));
+  return r;
+}
+
 // --------------------------------------------- bulk async smem fill (TMA)
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -415,7 +424,7 @@ k_vq_mean8(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
                 if constexpr (W >= 4) {
 #pragma unroll
                   for (int j = 0; j < W; j += 4) {
-                    const float4 f = SMEM ? *reinterpret_cast<const float4*>(ent + j)
+                    const float4 f = SMEM ? lds128(ent + j)
                                           : __ldg(reinterpret_cast<const float4*>(ent + j));
                     acc[(q * W + j) / 2] = fadd2(acc[(q * W + j) / 2], pack2(f.x, f.y));
                     acc[(q * W + j) / 2 + 1] = fadd2(acc[(q * W + j) / 2 + 1], pack2(f.z, f.w));

@@ -32,11 +32,24 @@ from .sampler import DeviceSampler
 
 
 class SageModel(nn.Module):
+    """Layer 0 consumes the padded aggregate whose column ``in_dim`` is a
+    constant 1, so its bias is a weight column (no separate bias reduction
+    over the ~150k-row activation in backward)."""
+
     def __init__(self, in_dim: int, hidden: int, num_classes: int, num_layers: int,
-                 dropout: float = 0.0):
+                 dropout: float = 0.0, in_pitch: int | None = None):
         super().__init__()
         dims = [in_dim] + [hidden] * (num_layers - 1) + [num_classes]
-        self.lins = nn.ModuleList(nn.Linear(dims[i], dims[i + 1]) for i in range(num_layers))
+        pitch = in_pitch or in_dim
+        first = nn.Linear(pitch, dims[1], bias=False)
+        with torch.no_grad():  # same init distribution as nn.Linear(in_dim, .)
+            ref = nn.Linear(in_dim, dims[1])
+            first.weight.zero_()
+            first.weight[:, :in_dim] = ref.weight
+            if pitch > in_dim:
+                first.weight[:, in_dim] = ref.bias
+        self.lins = nn.ModuleList([first] + [nn.Linear(dims[i], dims[i + 1])
+                                             for i in range(1, num_layers)])
         self.dropout = dropout
 
     def forward(self, agg_in, sb, caps):
@@ -52,9 +65,29 @@ class SageModel(nn.Module):
                                caps[l])
             else:  # ReLU fused into the block-mean gather
                 a = block_mean(h.to(torch.bfloat16), sb.indptr[l], sb.local[l], sb.n_nodes[l],
-                               caps[l], relu=True)
+                               caps[l], relu=True, trans=sb.trans[l] if sb.trans else None)
             h = self.lins[i](a)
         return h
+
+
+class FlatAdam:
+    """torch.optim.Adam(betas=(0.9, 0.999), eps=1e-8) over one flat buffer,
+    one kernel per step (``fg_adam_step``), device-side step counter."""
+
+    def __init__(self, param, grad, lr=1e-3, betas=(0.9, 0.999), eps=1e-8, weight_decay=0.0):
+        from . import _native as N
+        self.N = N
+        self.p, self.g = param, grad
+        self.m = torch.zeros_like(param)
+        self.v = torch.zeros_like(param)
+        self.t = torch.zeros(1, dtype=torch.int64, device=param.device)
+        self.lr, self.b1, self.b2, self.eps, self.wd = lr, betas[0], betas[1], eps, weight_decay
+
+    def step(self):
+        N = self.N
+        N.call("fg_adam_step", N.ptr(self.p), N.ptr(self.g), N.ptr(self.m), N.ptr(self.v),
+               self.p.numel(), N.ptr(self.t), self.lr, self.b1, self.b2, self.eps, self.wd,
+               N.stream_handle())
 
 
 @dataclass
@@ -81,24 +114,30 @@ class SageTrainer:
         self.pg = process_group
         self.world = torch.distributed.get_world_size(process_group) if process_group else 1
         torch.manual_seed(cfg.seed)
-        self.sampler = DeviceSampler(graph, cfg.fanouts, cfg.batch_size, need_local=True)
+        self.sampler = DeviceSampler(graph, cfg.fanouts, cfg.batch_size, need_local=True,
+                                     need_transpose=True)
         self.caps = self.sampler.caps
         L = len(cfg.fanouts)
         # input layer sees the 16-aligned padded aggregate (zero columns past d)
-        self.model = SageModel(padded_dim(codec.d), cfg.hidden, num_classes, L,
-                               cfg.dropout).to(self.device)
+        self.model = SageModel(codec.d, cfg.hidden, num_classes, L, cfg.dropout,
+                               in_pitch=padded_dim(codec.d)).to(self.device)
         # flat gradient buffer: one all-reduce per step
+        # one flat fp32 buffer each for params, grads and Adam moments: a
+        # single all-reduce and a single optimizer kernel per step
         params = list(self.model.parameters())
         total = sum(p.numel() for p in params)
+        self.flat_param = torch.zeros(total, dtype=torch.float32, device=self.device)
         self.flat_grad = torch.zeros(total, dtype=torch.float32, device=self.device)
         off = 0
         for p in params:
-            p.grad = self.flat_grad[off:off + p.numel()].view_as(p)
-            off += p.numel()
+            n = p.numel()
+            self.flat_param[off:off + n].copy_(p.data.reshape(-1))
+            p.data = self.flat_param[off:off + n].view_as(p)
+            p.grad = self.flat_grad[off:off + n].view_as(p)
+            off += n
         if self.world > 1:  # identical initial weights on every rank
-            for p in params:
-                torch.distributed.broadcast(p.data, 0, group=self.pg)
-        self.opt = torch.optim.Adam(params, lr=cfg.lr, capturable=True, fused=True)
+            torch.distributed.broadcast(self.flat_param, 0, group=self.pg)
+        self.opt = FlatAdam(self.flat_param, self.flat_grad, lr=cfg.lr)
         self.loss_buf = torch.zeros((), dtype=torch.float32, device=self.device)
         self.agg = alloc_aggregate(self.caps[L - 1], codec.d, cfg.agg_dtype, self.device)
         self.graph = None

@@ -102,6 +102,7 @@ class SampledBatch:
     local: list
     frontier: object = None
     n_frontier: object = None
+    trans: list = None   # per block (t_indptr, t_dst) or None
 
 
 class DeviceSampler:
@@ -109,7 +110,7 @@ class DeviceSampler:
 
     def __init__(self, graph: DeviceGraph, fanouts, batch_size: int, *,
                  need_local: bool = True, want_frontier: bool = False,
-                 unique_last: bool = False):
+                 unique_last: bool = False, need_transpose: bool = False):
         import torch
         N.require_cuda()
         self.g = graph
@@ -138,6 +139,17 @@ class DeviceSampler:
         self.picks = [z(pcaps[l]) for l in range(L)]
         self.n_picks = [z(1, dt=i64) for _ in range(L)]
         self.local = [z(pcaps[l]) if (need_local and l < L - 1) else None for l in range(L)]
+        # per hidden block: transpose (source rank -> edges) for the gather bwd
+        self.need_transpose = need_transpose and need_local
+        self.tkeys, self.tkeys_sorted, self.tkeys_idx, self.t_indptr, self.t_dst = \
+            [], [], [], [], []
+        if self.need_transpose:
+            for l in range(L - 1):
+                self.tkeys.append(z(pcaps[l], dt=i64))
+                self.tkeys_sorted.append(z(pcaps[l], dt=i64))
+                self.tkeys_idx.append(z(pcaps[l], dt=i64))
+                self.t_indptr.append(z(caps[l + 1] + 1))
+                self.t_dst.append(z(pcaps[l]))
         words = (n + 31) // 32
         self.bitmap = torch.zeros(words, dtype=torch.int32, device=dev)
         self.wprefix = torch.zeros(words, dtype=torch.int32, device=dev)
@@ -225,10 +237,14 @@ class DeviceSampler:
                 if self.local[l] is not None:
                     N.call("fg_bitmap_rank", N.ptr(self.picks[l]), N.ptr(self.n_picks[l]),
                            self.pcaps[l], bm, wp, N.ptr(self.local[l]), s)
+                    if self.need_transpose:
+                        self._transpose(l, s)
                 N.call("fg_bitmap_clear", N.ptr(self.nodes[l + 1]), N.ptr(self.n_nodes[l + 1]),
                        self.caps[l + 1], bm, s)
         out = SampledBatch(self.nodes, self.n_nodes, self.indptr, self.picks, self.n_picks,
                            self.local)
+        if self.need_transpose:
+            out.trans = [(self.t_indptr[l], self.t_dst[l]) for l in range(L - 1)] + [None]
         if self.want_frontier:
             N.call("fg_bitmap_compact", N.ptr(self.fbitmap), n, N.ptr(self.frontier), self.fcap,
                    N.ptr(self.n_frontier), None, N.ptr(self.ws_fbm), self.ws_fbm.numel(), s)
@@ -236,6 +252,17 @@ class DeviceSampler:
                    N.ptr(self.fbitmap), s)
             out.frontier, out.n_frontier = self.frontier, self.n_frontier
         return out
+
+    def _transpose(self, l: int, s) -> None:
+        """Block l's transpose: unique keys (rank << 32 | edge) sorted, then
+        CSR over source ranks + dst of each edge (deterministic order)."""
+        import torch
+        N.call("fg_block_transpose", N.ptr(self.local[l]), N.ptr(self.n_picks[l]), self.pcaps[l],
+               N.ptr(self.tkeys[l]), s)
+        torch.sort(self.tkeys[l], out=(self.tkeys_sorted[l], self.tkeys_idx[l]))
+        N.call("fg_block_transpose_finish", N.ptr(self.tkeys_sorted[l]), N.ptr(self.n_picks[l]),
+               self.pcaps[l], N.ptr(self.indptr[l]), N.ptr(self.n_nodes[l]), self.caps[l],
+               self.caps[l + 1], N.ptr(self.t_indptr[l]), N.ptr(self.t_dst[l]), s)
 
     def sample(self, b: int) -> SampledBatch:
         self.load_seeds(b)
