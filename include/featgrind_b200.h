@@ -176,13 +176,16 @@ int fg_gather_dequant_mean(const fg_codec_desc* codec, const int32_t* indptr,
 
 /* Hidden-layer mean over a block with local source indices (bf16 in/out,
  * fp32 accumulate); `relu_in` applies max(0, .) to source rows on load (the
- * previous layer's activation, fused).  Backward: scatter of grad/cnt with
+ * previous layer's activation, fused).  out_ld = h_dim, or h_dim + 8 to
+ * append a [1, 0 x 7] column block so the next layer's bias is a weight
+ * column (every row, live or not, gets it).  Backward: scatter of grad/cnt with
  * fp32 vector atomics into `grad_src_f32` (caller-zeroed), then
  * fg_f32_to_bf16 converts, multiplying by (relu_mask > 0) when given. */
 int fg_block_mean_fwd(const uint16_t* h_src, int64_t h_dim,
                       const int32_t* indptr, const int32_t* src_local,
                       const int64_t* num_dst_dev, int64_t max_dst,
-                      uint16_t* out, int relu_in, void* cuda_stream);
+                      uint16_t* out, int64_t out_ld, int relu_in,
+                      void* cuda_stream);
 int fg_block_mean_bwd(const uint16_t* grad_out, int64_t h_dim,
                       const int32_t* indptr, const int32_t* src_local,
                       const int64_t* num_dst_dev, int64_t max_dst,
@@ -190,25 +193,32 @@ int fg_block_mean_bwd(const uint16_t* grad_out, int64_t h_dim,
 int fg_f32_to_bf16(const float* in, int64_t count, const uint16_t* relu_mask,
                    uint16_t* out, void* cuda_stream);
 
-/* Gather-form backward of the hidden block mean (deterministic, no float
- * atomics).  fg_block_transpose writes unique keys (local_rank << 32 | edge)
- * for the block's edges (INT64_MAX past the live edge count); after the
- * caller sorts them ascending, fg_block_transpose_finish derives the
- * transposed CSR t_indptr [cap_src + 1] and the dst of every edge t_dst;
+/* Gather-form backward of the hidden block mean (no float atomics, no
+ * zero-fill of an fp32 accumulator).  fg_block_transpose builds the
+ * block's transpose by counting sort: t_indptr [cap_src + 1] over source
+ * ranks and t_dst (the dst of every edge, grouped by source; order within a
+ * source is scheduling-dependent); scratch = 2*cap_src int32.
  * fg_block_mean_bwd_t then computes, for every source row r < cap_src,
  *   out[r] = relu'(mask[r]) * sum_{i in t_indptr[r]..} g[t_dst[i]] / cnt(t_dst[i])
- * in edge order (rows without edges get 0). */
+ * (rows without edges get 0). */
 int fg_block_transpose(const int32_t* src_local, const int64_t* n_edges_dev,
-                       int64_t cap_e, int64_t* keys, void* cuda_stream);
-int fg_block_transpose_finish(const int64_t* sorted_keys,
-                              const int64_t* n_edges_dev, int64_t cap_e,
-                              const int32_t* indptr, const int64_t* num_dst_dev,
-                              int64_t max_dst, int64_t cap_src,
-                              int32_t* t_indptr, int32_t* t_dst, void* cuda_stream);
-int fg_block_mean_bwd_t(const uint16_t* grad_out, int64_t h_dim,
+                       int64_t cap_e, const int32_t* indptr,
+                       const int64_t* num_dst_dev, int64_t max_dst, int64_t cap_src,
+                       int32_t* t_indptr, int32_t* t_dst, int32_t* scratch,
+                       void* cuda_stream);
+int fg_block_mean_bwd_t(const uint16_t* grad_out, int64_t h_dim, int64_t g_ld,
                         const int32_t* t_indptr, const int32_t* t_dst,
                         const int32_t* indptr, int64_t cap_src,
                         const uint16_t* relu_mask, uint16_t* out, void* cuda_stream);
+
+/* Fused softmax cross-entropy over padded logits [rows, ld] (bf16 or fp32):
+ * rows r < *n_valid_dev use label labels[row_node[r]]; loss_out = mean loss
+ * (deterministic row-order reduction); grad = d loss / d logits (same dtype;
+ * zeros for padded rows); row_loss = per-row scratch [rows]. */
+int fg_softmax_ce(const void* logits, int logits_bf16, int num_classes, int64_t ld,
+                  int64_t rows, const int64_t* n_valid_dev, const int32_t* labels,
+                  const int32_t* row_node, void* grad, float* row_loss,
+                  float* loss_out, void* cuda_stream);
 
 /* Adam (torch.optim.Adam semantics) over a flat fp32 parameter buffer with
  * a device step counter (graph-capturable; one update kernel). */

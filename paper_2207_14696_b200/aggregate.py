@@ -59,15 +59,17 @@ class BlockMean(torch.autograd.Function):
 
     @staticmethod
     def forward(ctx, h_src, indptr, local, n_dst, max_dst: int, relu: bool = False,
-                trans=None):
+                trans=None, bias_col: bool = False):
         h_src = h_src.contiguous()
         H = h_src.shape[1]
-        out = torch.empty((max_dst, H), dtype=torch.bfloat16, device=h_src.device)
+        ld = H + 8 if bias_col else H
+        out = torch.empty((max_dst, ld), dtype=torch.bfloat16, device=h_src.device)
         N.call("fg_block_mean_fwd", N.ptr(h_src), H, N.ptr(indptr), N.ptr(local), N.ptr(n_dst),
-               max_dst, N.ptr(out), int(relu), N.stream_handle())
+               max_dst, N.ptr(out), ld, int(relu), N.stream_handle())
         t_indptr, t_dst = trans if trans is not None else (indptr, indptr)
         ctx.save_for_backward(indptr, local, n_dst, h_src if relu else indptr, t_indptr, t_dst)
         ctx.relu = relu
+        ctx.H = H
         ctx.gather_bwd = trans is not None
         ctx.max_dst = max_dst
         ctx.n_src = h_src.shape[0]
@@ -79,22 +81,55 @@ class BlockMean(torch.autograd.Function):
         if not ctx.relu:
             h_src = None
         g = g.contiguous().to(torch.bfloat16)
-        H = g.shape[1]
-        if ctx.gather_bwd:  # deterministic gather over the block's transpose
+        H = ctx.H
+        if ctx.gather_bwd:  # gather over the block's transpose, no float atomics
             gh = torch.empty((ctx.n_src, H), dtype=torch.bfloat16, device=g.device)
-            N.call("fg_block_mean_bwd_t", N.ptr(g), H, N.ptr(t_indptr), N.ptr(t_dst),
+            N.call("fg_block_mean_bwd_t", N.ptr(g), H, g.shape[1], N.ptr(t_indptr), N.ptr(t_dst),
                    N.ptr(indptr), ctx.n_src, N.ptr(h_src), N.ptr(gh), N.stream_handle())
-            return gh, None, None, None, None, None, None
+            return gh, None, None, None, None, None, None, None
+        if g.shape[1] != H:
+            g = g[:, :H].contiguous()
         acc = torch.zeros((ctx.n_src, H), dtype=torch.float32, device=g.device)
         s = N.stream_handle()
         N.call("fg_block_mean_bwd", N.ptr(g), H, N.ptr(indptr), N.ptr(local), N.ptr(n_dst),
                ctx.max_dst, N.ptr(acc), s)
         gh = torch.empty((ctx.n_src, H), dtype=torch.bfloat16, device=g.device)
         N.call("fg_f32_to_bf16", N.ptr(acc), acc.numel(), N.ptr(h_src), N.ptr(gh), s)
-        return gh, None, None, None, None, None, None
+        return gh, None, None, None, None, None, None, None
 
 
-def block_mean(h_src, indptr, local, n_dst, max_dst: int, relu: bool = False, trans=None):
+def block_mean(h_src, indptr, local, n_dst, max_dst: int, relu: bool = False, trans=None,
+               bias_col: bool = False):
     """``trans`` = (t_indptr, t_dst) of the block (DeviceSampler with
-    need_transpose) switches the backward to the deterministic gather."""
-    return BlockMean.apply(h_src, indptr, local, n_dst, max_dst, relu, trans)
+    need_transpose) switches the backward to the gather form; ``bias_col``
+    appends a [1, 0 x 7] column block (output width H + 8) so the next
+    layer's bias is a column of its weight."""
+    return BlockMean.apply(h_src, indptr, local, n_dst, max_dst, relu, trans, bias_col)
+
+
+class SoftmaxCE(torch.autograd.Function):
+    """Mean cross-entropy over the live seed rows of padded logits, labels
+    gathered on the device (``fg_softmax_ce``: one fused kernel computing
+    loss and d loss / d logits)."""
+
+    @staticmethod
+    def forward(ctx, logits, labels, row_node, n_valid):
+        logits = logits.contiguous()
+        rows, C = logits.shape
+        grad = torch.empty_like(logits)
+        row_loss = torch.empty(rows, dtype=torch.float32, device=logits.device)
+        loss = torch.empty((), dtype=torch.float32, device=logits.device)
+        N.call("fg_softmax_ce", N.ptr(logits), int(logits.dtype == torch.bfloat16), C, C, rows,
+               N.ptr(n_valid), N.ptr(labels), N.ptr(row_node), N.ptr(grad), N.ptr(row_loss),
+               N.ptr(loss), N.stream_handle())
+        ctx.save_for_backward(grad)
+        return loss
+
+    @staticmethod
+    def backward(ctx, g):
+        (grad,) = ctx.saved_tensors
+        return grad * g.to(grad.dtype), None, None, None
+
+
+def softmax_ce(logits, labels, row_node, n_valid):
+    return SoftmaxCE.apply(logits, labels, row_node, n_valid)

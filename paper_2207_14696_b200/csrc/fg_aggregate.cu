@@ -39,13 +39,18 @@ template <bool RELU>
 __global__ void __launch_bounds__(256)
 k_block_mean_fwd(const uint16_t* __restrict__ h, int64_t H, const int32_t* __restrict__ indptr,
                  const int32_t* __restrict__ srcl, const int64_t* __restrict__ ndst_dev,
-                 int64_t max_dst, uint16_t* __restrict__ out) {
+                 int64_t max_dst, uint16_t* __restrict__ out, int64_t out_ld) {
   const int64_t live = live_count(ndst_dev, max_dst);
   const int64_t chunks = H >> 3;
-  const int64_t total = max_dst * chunks;
+  const int64_t ochunks = out_ld >> 3;  // out_ld = H, or H + 8 with a ones column
+  const int64_t total = max_dst * ochunks;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t v = t / chunks, c = t - v * chunks;
+    const int64_t v = t / ochunks, c = t - v * ochunks;
+    if (c >= chunks) {  // bias column chunk: [1, 0, ..., 0]
+      reinterpret_cast<uint4*>(out + v * out_ld)[c] = make_uint4(0x3F80u, 0u, 0u, 0u);
+      continue;
+    }
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     int cnt = 0;
     if (v < live) {
@@ -73,7 +78,7 @@ k_block_mean_fwd(const uint16_t* __restrict__ h, int64_t H, const int32_t* __res
         for (int j = 0; j < 8; ++j) acc[j] *= inv;
       }
     }
-    reinterpret_cast<uint4*>(out + v * H)[c] = f32_to_bf16x8(acc);
+    reinterpret_cast<uint4*>(out + v * out_ld)[c] = f32_to_bf16x8(acc);
   }
 }
 
@@ -128,17 +133,21 @@ using namespace fg;
 extern "C" {
 
 int fg_block_mean_fwd(const uint16_t* h, int64_t H, const int32_t* indptr, const int32_t* srcl,
-                      const int64_t* ndst, int64_t max_dst, uint16_t* out, int relu_in,
-                      void* s) {
+                      const int64_t* ndst, int64_t max_dst, uint16_t* out, int64_t out_ld,
+                      int relu_in, void* s) {
   FG_CHECK_ARG(H % 8 == 0, "hidden dim must be a multiple of 8");
+  if (out_ld == 0) out_ld = H;
+  FG_CHECK_ARG(out_ld == H || out_ld == H + 8, "out_ld must be H or H + 8 (ones column)");
   if (max_dst == 0) return FG_OK;
-  const int64_t total = max_dst * (H / 8);
+  const int64_t total = max_dst * (out_ld / 8);
   if (relu_in)
     k_block_mean_fwd<true><<<grid_for(total, 256), 256, 0, as_stream(s)>>>(h, H, indptr, srcl,
-                                                                           ndst, max_dst, out);
+                                                                           ndst, max_dst, out,
+                                                                           out_ld);
   else
     k_block_mean_fwd<false><<<grid_for(total, 256), 256, 0, as_stream(s)>>>(h, H, indptr, srcl,
-                                                                            ndst, max_dst, out);
+                                                                            ndst, max_dst, out,
+                                                                            out_ld);
   FG_LAUNCH_CHECK();
   return FG_OK;
 }
@@ -174,42 +183,77 @@ int fg_f32_to_bf16(const float* in, int64_t count, const uint16_t* relu_mask, ui
 // (rank << 32 | edge), so any sort yields the same order.
 namespace fg {
 
-__global__ void k_transpose_keys(const int32_t* __restrict__ local, const int64_t* __restrict__ ne_dev,
-                                 int64_t cap_e, int64_t* __restrict__ keys) {
+// counting-sort transpose: histogram of source ranks, exclusive scan,
+// placement through atomic cursors (list order within a source is
+// scheduling-dependent; the backward sums a handful of terms per source).
+__global__ void k_t_hist(const int32_t* __restrict__ local, const int64_t* __restrict__ ne_dev,
+                         int64_t cap_e, int32_t* __restrict__ cnt) {
   const int64_t ne = min64(*ne_dev, cap_e);
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < cap_e;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ne;
        e += (int64_t)gridDim.x * blockDim.x)
-    keys[e] = e < ne ? (((int64_t)local[e] << 32) | e) : INT64_MAX;
+    atomicAdd(cnt + local[e], 1);
 }
 
-// sorted keys -> t_indptr [cap_src + 1] and t_dst [cap_e] (dst of each edge)
-__global__ void k_transpose_finish(const int64_t* __restrict__ keys, const int64_t* __restrict__ ne_dev,
-                                   int64_t cap_e, const int32_t* __restrict__ indptr,
-                                   const int64_t* __restrict__ nd_dev, int64_t max_dst,
-                                   int64_t cap_src, int32_t* __restrict__ t_indptr,
-                                   int32_t* __restrict__ t_dst) {
-  const int64_t ne = min64(*ne_dev, cap_e);
-  const int64_t nd = min64(*nd_dev, max_dst);
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= ne;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i < ne ? (keys[i] >> 32) : cap_src;
-    const int64_t rp = i > 0 ? (keys[i - 1] >> 32) : -1;
-    for (int64_t q = rp + 1; q <= r && q <= cap_src; ++q) t_indptr[q] = (int32_t)i;
-    if (i < ne) {
-      const int32_t e = (int32_t)(keys[i] & 0xFFFFFFFFll);
-      int64_t lo = 0, hi = nd;  // last v with indptr[v] <= e
-      while (hi - lo > 1) {
-        const int64_t mid = (lo + hi) >> 1;
-        if (indptr[mid] <= e) lo = mid; else hi = mid;
-      }
-      t_dst[i] = (int32_t)lo;
+__global__ void __launch_bounds__(1024)
+k_t_scan(int64_t n, const int32_t* __restrict__ cnt, int32_t* __restrict__ t_indptr,
+         int32_t* __restrict__ cursor) {
+  // single CTA: exclusive scan of n counts (n ~ 1e5: ~100 iterations)
+  __shared__ int32_t warp_sums[32];
+  __shared__ int32_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int64_t base = 0; base < n; base += 1024) {
+    const int64_t i = base + threadIdx.x;
+    const int32_t v = i < n ? cnt[i] : 0;
+    int32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
     }
+    if (lane == 31) warp_sums[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      int32_t w = warp_sums[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += y;
+      }
+      warp_sums[lane] = w;
+    }
+    __syncthreads();
+    const int32_t excl = carry + (wid ? warp_sums[wid - 1] : 0) + x - v;
+    if (i < n) {
+      t_indptr[i] = excl;
+      cursor[i] = excl;
+    }
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = excl + v;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) t_indptr[n] = carry;
+}
+
+// place every edge; t_dst receives the dst of the edge (found from indptr)
+__global__ void k_t_place(const int32_t* __restrict__ local, const int64_t* __restrict__ ne_dev,
+                          int64_t cap_e, const int32_t* __restrict__ indptr,
+                          const int64_t* __restrict__ nd_dev, int64_t max_dst,
+                          int32_t* __restrict__ cursor, int32_t* __restrict__ t_dst) {
+  const int64_t nd = min64(*nd_dev, max_dst);
+  // thread per destination: its picks are contiguous in [indptr[v], indptr[v+1])
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nd;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t e0 = indptr[v], e1 = indptr[v + 1];
+    for (int32_t e = e0; e < e1; ++e) t_dst[atomicAdd(cursor + local[e], 1)] = (int32_t)v;
   }
 }
 
 template <bool RELU>
 __global__ void __launch_bounds__(256)
-k_block_mean_bwd_t(const uint16_t* __restrict__ g, int64_t H, const int32_t* __restrict__ t_indptr,
+k_block_mean_bwd_t(const uint16_t* __restrict__ g, int64_t H, int64_t g_ld,
+                   const int32_t* __restrict__ t_indptr,
                    const int32_t* __restrict__ t_dst, const int32_t* __restrict__ indptr,
                    int64_t cap_src, const uint16_t* __restrict__ mask, uint16_t* __restrict__ out) {
   const int64_t chunks = H >> 3;
@@ -227,7 +271,7 @@ k_block_mean_bwd_t(const uint16_t* __restrict__ g, int64_t H, const int32_t* __r
         if (i + u < i1) {
           const int32_t v = t_dst[i + u];
           sc[u] = 1.0f / (float)(indptr[v + 1] - indptr[v]);
-          q[u] = __ldg(reinterpret_cast<const uint4*>(g + (int64_t)v * H) + c);
+          q[u] = __ldg(reinterpret_cast<const uint4*>(g + (int64_t)v * g_ld) + c);
         }
       }
 #pragma unroll
@@ -278,37 +322,39 @@ __global__ void k_step_inc(int64_t* step) { *step += 1; }
 }  // namespace fg
 
 extern "C" int fg_block_transpose(const int32_t* local, const int64_t* n_edges_dev, int64_t cap_e,
-                                  int64_t* keys, void* s) {
-  if (cap_e == 0) return FG_OK;
-  fg::k_transpose_keys<<<grid_for(cap_e, 256), 256, 0, as_stream(s)>>>(local, n_edges_dev, cap_e,
-                                                                       keys);
+                                  const int32_t* indptr, const int64_t* n_dst_dev,
+                                  int64_t max_dst, int64_t cap_src, int32_t* t_indptr,
+                                  int32_t* t_dst, int32_t* scratch, void* s) {
+  FG_CHECK_ARG(cap_src >= 1, "fg_block_transpose: empty source capacity");
+  cudaStream_t st = as_stream(s);
+  int32_t* cnt = scratch;              // [cap_src]
+  int32_t* cursor = scratch + cap_src;  // [cap_src]
+  FG_CUDA_TRY(cudaMemsetAsync(cnt, 0, cap_src * sizeof(int32_t), st));
+  fg::k_t_hist<<<grid_for(cap_e, 256), 256, 0, st>>>(local, n_edges_dev, cap_e, cnt);
+  FG_LAUNCH_CHECK();
+  fg::k_t_scan<<<1, 1024, 0, st>>>(cap_src, cnt, t_indptr, cursor);
+  FG_LAUNCH_CHECK();
+  fg::k_t_place<<<grid_for(max_dst, 256), 256, 0, st>>>(local, n_edges_dev, cap_e, indptr,
+                                                        n_dst_dev, max_dst, cursor, t_dst);
   FG_LAUNCH_CHECK();
   return FG_OK;
 }
 
-extern "C" int fg_block_transpose_finish(const int64_t* sorted_keys, const int64_t* n_edges_dev,
-                                         int64_t cap_e, const int32_t* indptr,
-                                         const int64_t* n_dst_dev, int64_t max_dst,
-                                         int64_t cap_src, int32_t* t_indptr, int32_t* t_dst,
-                                         void* s) {
-  fg::k_transpose_finish<<<grid_for(cap_e + 1, 256), 256, 0, as_stream(s)>>>(
-      sorted_keys, n_edges_dev, cap_e, indptr, n_dst_dev, max_dst, cap_src, t_indptr, t_dst);
-  FG_LAUNCH_CHECK();
-  return FG_OK;
-}
-
-extern "C" int fg_block_mean_bwd_t(const uint16_t* g, int64_t H, const int32_t* t_indptr,
-                                   const int32_t* t_dst, const int32_t* indptr, int64_t cap_src,
+extern "C" int fg_block_mean_bwd_t(const uint16_t* g, int64_t H, int64_t g_ld,
+                                   const int32_t* t_indptr, const int32_t* t_dst,
+                                   const int32_t* indptr, int64_t cap_src,
                                    const uint16_t* relu_mask, uint16_t* out, void* s) {
   FG_CHECK_ARG(H % 8 == 0, "hidden dim must be a multiple of 8");
+  if (g_ld == 0) g_ld = H;
+  FG_CHECK_ARG(g_ld % 8 == 0 && g_ld >= H, "bad g_ld");
   if (cap_src == 0) return FG_OK;
   const int64_t total = cap_src * (H / 8);
   if (relu_mask)
     fg::k_block_mean_bwd_t<true><<<grid_for(total, 256), 256, 0, as_stream(s)>>>(
-        g, H, t_indptr, t_dst, indptr, cap_src, relu_mask, out);
+        g, H, g_ld, t_indptr, t_dst, indptr, cap_src, relu_mask, out);
   else
     fg::k_block_mean_bwd_t<false><<<grid_for(total, 256), 256, 0, as_stream(s)>>>(
-        g, H, t_indptr, t_dst, indptr, cap_src, nullptr, out);
+        g, H, g_ld, t_indptr, t_dst, indptr, cap_src, nullptr, out);
   FG_LAUNCH_CHECK();
   return FG_OK;
 }
@@ -321,6 +367,85 @@ extern "C" int fg_adam_step(float* params, const float* grads, float* m, float* 
                                                             beta1, beta2, eps, weight_decay);
   FG_LAUNCH_CHECK();
   fg::k_step_inc<<<1, 1, 0, as_stream(s)>>>(step_dev);
+  FG_LAUNCH_CHECK();
+  return FG_OK;
+}
+
+// ------------------------------------------------ fused softmax + CE loss
+// Rows r < n_valid (the live seeds) with label labels[node[r]]: loss = mean
+// over valid rows of -log softmax(logits[r])[y]; grad = (softmax - onehot) /
+// n_valid (0 for padded rows).  Warp per row, fp32 math, deterministic
+// (per-row losses reduced by one CTA in row order).
+namespace fg {
+template <typename LT>
+__global__ void k_softmax_ce(const LT* __restrict__ logits, int C, int64_t ld, int64_t rows,
+                             const int64_t* __restrict__ nvalid_dev,
+                             const int32_t* __restrict__ labels, const int32_t* __restrict__ node,
+                             LT* __restrict__ grad, float* __restrict__ row_loss) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t nv = min64(*nvalid_dev, rows);
+  const float inv_n = nv > 0 ? 1.0f / (float)nv : 0.0f;
+  for (int64_t r = warp; r < rows; r += nwarps) {
+    const LT* x = logits + r * ld;
+    LT* gr = grad + r * ld;
+    if (r >= nv) {
+      for (int c = lane; c < C; c += 32) gr[c] = (LT)0.f;
+      if (lane == 0) row_loss[r] = 0.f;
+      continue;
+    }
+    const int y = labels[node[r]];
+    float mx = -INFINITY;
+    for (int c = lane; c < C; c += 32) mx = fmaxf(mx, (float)x[c]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    float se = 0.f;
+    for (int c = lane; c < C; c += 32) se += __expf((float)x[c] - mx);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
+    const float lse = mx + __logf(se);
+    for (int c = lane; c < C; c += 32) {
+      const float p = __expf((float)x[c] - lse);
+      gr[c] = (LT)((p - (c == y ? 1.f : 0.f)) * inv_n);
+    }
+    if (lane == 0) row_loss[r] = (lse - (float)x[y]) * inv_n;
+  }
+}
+
+__global__ void __launch_bounds__(1024)
+k_sum_rows(const float* __restrict__ v, int64_t n, float* __restrict__ out) {
+  __shared__ float part[1024];
+  float s = 0.f;
+  for (int64_t i = threadIdx.x; i < n; i += 1024) s += v[i];
+  part[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 512; w; w >>= 1) {
+    if (threadIdx.x < w) part[threadIdx.x] += part[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = part[0];
+}
+}  // namespace fg
+
+extern "C" int fg_softmax_ce(const void* logits, int logits_bf16, int C, int64_t ld, int64_t rows,
+                             const int64_t* n_valid_dev, const int32_t* labels,
+                             const int32_t* row_node, void* grad, float* row_loss,
+                             float* loss_out, void* s) {
+  FG_CHECK_ARG(C >= 1 && ld >= C && rows >= 1, "fg_softmax_ce: bad shape");
+  cudaStream_t st = as_stream(s);
+  const int threads = 256;
+  const int grid = (int)min64(ceil_div(rows * 32, threads), (int64_t)sm_count() * 8);
+  if (logits_bf16)
+    fg::k_softmax_ce<__nv_bfloat16><<<grid, threads, 0, st>>>(
+        (const __nv_bfloat16*)logits, C, ld, rows, n_valid_dev, labels, row_node,
+        (__nv_bfloat16*)grad, row_loss);
+  else
+    fg::k_softmax_ce<float><<<grid, threads, 0, st>>>((const float*)logits, C, ld, rows,
+                                                      n_valid_dev, labels, row_node,
+                                                      (float*)grad, row_loss);
+  FG_LAUNCH_CHECK();
+  fg::k_sum_rows<<<1, 1024, 0, st>>>(row_loss, rows, loss_out);
   FG_LAUNCH_CHECK();
   return FG_OK;
 }

@@ -27,47 +27,62 @@ import torch.nn as nn
 import torch.nn.functional as F
 
 from . import ddp
-from .aggregate import alloc_aggregate, block_mean, gather_dequant_mean, padded_dim
+from .aggregate import alloc_aggregate, block_mean, gather_dequant_mean, padded_dim, softmax_ce
 from .sampler import DeviceSampler
 
 
 class SageModel(nn.Module):
-    """Layer 0 consumes the padded aggregate whose column ``in_dim`` is a
-    constant 1, so its bias is a weight column (no separate bias reduction
-    over the ~150k-row activation in backward)."""
+    """Every layer is a bias-free Linear over an input that carries a
+    constant-1 column: layer 0 reads the padded aggregate (column in_dim = 1),
+    layer i > 0 reads the block-mean output widened by a [1, 0 x 7] block
+    (column hidden = 1).  Biases therefore live in weight columns and their
+    gradients come out of the weight GEMMs (no reductions over the ~1e5-row
+    activations in backward).  Initialisation matches nn.Linear."""
 
     def __init__(self, in_dim: int, hidden: int, num_classes: int, num_layers: int,
                  dropout: float = 0.0, in_pitch: int | None = None):
         super().__init__()
         dims = [in_dim] + [hidden] * (num_layers - 1) + [num_classes]
-        pitch = in_pitch or in_dim
-        first = nn.Linear(pitch, dims[1], bias=False)
-        with torch.no_grad():  # same init distribution as nn.Linear(in_dim, .)
-            ref = nn.Linear(in_dim, dims[1])
-            first.weight.zero_()
-            first.weight[:, :in_dim] = ref.weight
-            if pitch > in_dim:
-                first.weight[:, in_dim] = ref.bias
-        self.lins = nn.ModuleList([first] + [nn.Linear(dims[i], dims[i + 1])
-                                             for i in range(1, num_layers)])
+        self.in_dims = dims[:-1]
+        lins = []
+        for i in range(num_layers):
+            pitch = (in_pitch or in_dim + 1) if i == 0 else dims[i] + 8
+            lin = nn.Linear(pitch, dims[i + 1], bias=False)
+            ref = nn.Linear(dims[i], dims[i + 1])
+            with torch.no_grad():
+                lin.weight.zero_()
+                lin.weight[:, :dims[i]] = ref.weight
+                lin.weight[:, dims[i]] = ref.bias
+            lins.append(lin)
+        self.lins = nn.ModuleList(lins)
         self.dropout = dropout
 
     def forward(self, agg_in, sb, caps):
-        """agg_in: [caps[L-1], d] mean of decoded inputs over the last block;
-        sb: SampledBatch; returns logits [caps[0], C]."""
+        """agg_in: [caps[L-1], pitch] mean of decoded inputs over the last
+        block (+ ones column); sb: SampledBatch; returns logits [caps[0], C]."""
         L = len(self.lins)
         h = self.lins[0](agg_in)
         for i in range(1, L):
             l = L - 1 - i  # block index feeding this layer
+            trans = sb.trans[l] if sb.trans else None
             if self.dropout and self.training:
                 h = F.dropout(F.relu(h), self.dropout)
                 a = block_mean(h.to(torch.bfloat16), sb.indptr[l], sb.local[l], sb.n_nodes[l],
-                               caps[l])
+                               caps[l], trans=trans, bias_col=True)
             else:  # ReLU fused into the block-mean gather
                 a = block_mean(h.to(torch.bfloat16), sb.indptr[l], sb.local[l], sb.n_nodes[l],
-                               caps[l], relu=True, trans=sb.trans[l] if sb.trans else None)
+                               caps[l], relu=True, trans=trans, bias_col=True)
             h = self.lins[i](a)
         return h
+
+    def reference_state(self) -> dict:
+        """Weights as plain (weight, bias) Linear layers (for the CPU oracle)."""
+        out = {}
+        for i, (lin, d) in enumerate(zip(self.lins, self.in_dims)):
+            w = lin.weight.detach().float().cpu()
+            out[f"lins.{i}.weight"] = w[:, :d].clone()
+            out[f"lins.{i}.bias"] = w[:, d].clone()
+        return out
 
 
 class FlatAdam:
@@ -151,10 +166,7 @@ class SageTrainer:
                             self.caps[L - 1], out=self.agg)
         with torch.autocast("cuda", dtype=torch.bfloat16):
             logits = self.model(self.agg, sb, self.caps)
-        seeds = sb.nodes[0].long()
-        valid = torch.arange(self.caps[0], device=self.device) < sb.n_nodes[0]
-        y = torch.where(valid, self.labels[seeds].long(), torch.full_like(seeds, -100))
-        loss = F.cross_entropy(logits.float(), y, ignore_index=-100)
+        loss = softmax_ce(logits, self.labels, sb.nodes[0], sb.n_nodes[0])
         self.flat_grad.zero_()
         loss.backward()
         ddp.average_flat_(self.flat_grad, self.pg)

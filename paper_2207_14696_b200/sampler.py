@@ -141,15 +141,12 @@ class DeviceSampler:
         self.local = [z(pcaps[l]) if (need_local and l < L - 1) else None for l in range(L)]
         # per hidden block: transpose (source rank -> edges) for the gather bwd
         self.need_transpose = need_transpose and need_local
-        self.tkeys, self.tkeys_sorted, self.tkeys_idx, self.t_indptr, self.t_dst = \
-            [], [], [], [], []
+        self.t_indptr, self.t_dst = [], []
         if self.need_transpose:
             for l in range(L - 1):
-                self.tkeys.append(z(pcaps[l], dt=i64))
-                self.tkeys_sorted.append(z(pcaps[l], dt=i64))
-                self.tkeys_idx.append(z(pcaps[l], dt=i64))
                 self.t_indptr.append(z(caps[l + 1] + 1))
                 self.t_dst.append(z(pcaps[l]))
+            self.t_scratch = z(2 * max(caps[1:]))
         words = (n + 31) // 32
         self.bitmap = torch.zeros(words, dtype=torch.int32, device=dev)
         self.wprefix = torch.zeros(words, dtype=torch.int32, device=dev)
@@ -254,15 +251,11 @@ class DeviceSampler:
         return out
 
     def _transpose(self, l: int, s) -> None:
-        """Block l's transpose: unique keys (rank << 32 | edge) sorted, then
-        CSR over source ranks + dst of each edge (deterministic order)."""
-        import torch
+        """Block l's transpose (source rank -> dst of each incoming edge) for
+        the gather-form backward of the hidden block mean."""
         N.call("fg_block_transpose", N.ptr(self.local[l]), N.ptr(self.n_picks[l]), self.pcaps[l],
-               N.ptr(self.tkeys[l]), s)
-        torch.sort(self.tkeys[l], out=(self.tkeys_sorted[l], self.tkeys_idx[l]))
-        N.call("fg_block_transpose_finish", N.ptr(self.tkeys_sorted[l]), N.ptr(self.n_picks[l]),
-               self.pcaps[l], N.ptr(self.indptr[l]), N.ptr(self.n_nodes[l]), self.caps[l],
-               self.caps[l + 1], N.ptr(self.t_indptr[l]), N.ptr(self.t_dst[l]), s)
+               N.ptr(self.indptr[l]), N.ptr(self.n_nodes[l]), self.caps[l], self.caps[l + 1],
+               N.ptr(self.t_indptr[l]), N.ptr(self.t_dst[l]), N.ptr(self.t_scratch), s)
 
     def sample(self, b: int) -> SampledBatch:
         self.load_seeds(b)

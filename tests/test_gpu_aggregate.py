@@ -144,3 +144,79 @@ def test_hidden_block_mean_fused_relu():
     out.backward(g.to(torch.bfloat16))
     ref.backward(g.to(torch.bfloat16).float())
     assert torch.allclose(h.grad.float(), hf.grad, atol=2e-2, rtol=1e-2)
+
+
+def _transpose_np(indptr, src, n_dst, n_src):
+    e = np.arange(src.size)
+    dst = np.repeat(np.arange(n_dst), np.diff(indptr[:n_dst + 1]))
+    order = np.lexsort((e, src))
+    t_indptr = np.zeros(n_src + 1, np.int32)
+    np.add.at(t_indptr, src + 1, 1)
+    return np.cumsum(t_indptr).astype(np.int32), dst[order].astype(np.int32)
+
+
+@pytest.mark.parametrize("relu", [False, True])
+def test_hidden_block_mean_gather_backward(relu):
+    rng = np.random.default_rng(5)
+    n_src, n_dst, max_dst, H = 2500, 600, 700, 64
+    counts, indptr, src = _block(n_src, n_dst, max_dst, 9, rng)
+    ti, td = _transpose_np(indptr, src, n_dst, n_src)
+    dev = "cuda"
+    h = torch.randn(n_src, H, device=dev).to(torch.bfloat16).requires_grad_(True)
+    ip, sl = torch.from_numpy(indptr).to(dev), torch.from_numpy(src).to(dev)
+    trans = (torch.from_numpy(ti).to(dev), torch.from_numpy(td).to(dev))
+    out = block_mean(h, ip, sl, torch.tensor([n_dst], device=dev), max_dst, relu=relu, trans=trans)
+    hf = h.detach().float().requires_grad_(True)
+    seg = torch.repeat_interleave(torch.arange(n_dst, device=dev), torch.from_numpy(counts).to(dev))
+    act = torch.relu(hf) if relu else hf
+    ref = torch.zeros(max_dst, H, device=dev).index_add_(0, seg, act[sl.long()])
+    cnt = torch.zeros(max_dst, device=dev)
+    cnt[:n_dst] = torch.from_numpy(counts).float().to(dev)
+    ref = ref / cnt.clamp_min(1)[:, None]
+    g = torch.randn(max_dst, H, device=dev)
+    g[n_dst:] = 0
+    out.backward(g.to(torch.bfloat16))
+    ref.backward(g.to(torch.bfloat16).float())
+    assert torch.allclose(h.grad.float(), hf.grad, atol=2e-2, rtol=1e-2)
+
+
+def test_block_transpose_kernel():
+    from paper_2207_14696_b200 import _native as N
+    rng = np.random.default_rng(8)
+    n_src, n_dst, max_dst = 5000, 1200, 1300
+    counts, indptr, src = _block(n_src, n_dst, max_dst, 10, rng)
+    dev = "cuda"
+    E = src.size
+    cap_e = E + 100
+    local = torch.zeros(cap_e, dtype=torch.int32, device=dev)
+    local[:E] = torch.from_numpy(src).to(dev)
+    t_indptr = torch.zeros(n_src + 1, dtype=torch.int32, device=dev)
+    t_dst = torch.zeros(cap_e, dtype=torch.int32, device=dev)
+    scratch = torch.zeros(2 * n_src, dtype=torch.int32, device=dev)
+    N.call("fg_block_transpose", N.ptr(local), N.ptr(torch.tensor([E], device=dev)), cap_e,
+           N.ptr(torch.from_numpy(indptr).to(dev)), N.ptr(torch.tensor([n_dst], device=dev)),
+           max_dst, n_src, N.ptr(t_indptr), N.ptr(t_dst), N.ptr(scratch), N.stream_handle())
+    ti, td = _transpose_np(indptr, src, n_dst, n_src)
+    assert np.array_equal(t_indptr.cpu().numpy(), ti)
+    got = t_dst[:E].cpu().numpy()
+    for r in range(0, n_src, 7):  # same multiset of dsts per source
+        assert np.array_equal(np.sort(got[ti[r]:ti[r + 1]]), np.sort(td[ti[r]:ti[r + 1]]))
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_fused_softmax_ce_matches_torch(dtype):
+    from paper_2207_14696_b200.aggregate import softmax_ce
+    dev = "cuda"
+    rows, C, nv = 300, 47, 257
+    logits = (torch.randn(rows, C, device=dev) * 3).to(dtype).requires_grad_(True)
+    labels = torch.randint(0, C, (5000,), device=dev, dtype=torch.int32)
+    node = torch.randint(0, 5000, (rows,), device=dev, dtype=torch.int32)
+    loss = softmax_ce(logits, labels, node, torch.tensor([nv], device=dev))
+    loss.backward()
+    lf = logits.detach().float()[:nv].requires_grad_(True)
+    ref = torch.nn.functional.cross_entropy(lf, labels[node[:nv].long()].long())
+    ref.backward()
+    assert abs(float(loss) - float(ref)) < 1e-4 * max(1.0, abs(float(ref)))
+    tol = 1e-6 if dtype == torch.float32 else 1e-2 / nv
+    assert torch.allclose(logits.grad[:nv].float(), lf.grad, atol=tol, rtol=1e-2)
+    assert (logits.grad[nv:] == 0).all()

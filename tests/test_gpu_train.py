@@ -51,10 +51,7 @@ def test_accuracy_parity_with_cpu_oracle_trainer():
     cfg = TrainConfig(fanouts=fans, batch_size=bs, hidden=hidden, lr=lr, seed=0)
     gpu = SageTrainer(dg, dc, labels, C, cfg)
     cpu_model = ot.OracleSage(d, hidden, C, len(fans))
-    sd = {k: v.detach().cpu().float() for k, v in gpu.model.state_dict().items()}
-    w0 = sd.pop("lins.0.weight")  # [H, pitch]: columns :d weights, column d bias
-    sd["lins.0.weight"], sd["lins.0.bias"] = w0[:, :d].clone(), w0[:, d].clone()
-    cpu_model.load_state_dict(sd)
+    cpu_model.load_state_dict(gpu.model.reference_state())
     opt = torch.optim.Adam(cpu_model.parameters(), lr=lr)
     host = dg.to_host()
     lab = labels.cpu().numpy()

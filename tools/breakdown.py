@@ -62,10 +62,8 @@ def main():
     def fwd_part():
         with torch.autocast("cuda", dtype=torch.bfloat16):
             logits = tr.model(tr.agg, sb, tr.caps)
-        seeds = sb.nodes[0].long()
-        valid = torch.arange(tr.caps[0], device=dev) < sb.n_nodes[0]
-        y = torch.where(valid, tr.labels[seeds].long(), torch.full_like(seeds, -100))
-        return F.cross_entropy(logits.float(), y, ignore_index=-100)
+        from paper_2207_14696_b200.aggregate import softmax_ce
+        return softmax_ce(logits, tr.labels, sb.nodes[0], sb.n_nodes[0])
 
     gf, gfb, go = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
     with torch.cuda.graph(gf):
@@ -79,10 +77,8 @@ def main():
     def model_part():
         with torch.autocast("cuda", dtype=torch.bfloat16):
             logits = tr.model(tr.agg, sb, tr.caps)
-        seeds = sb.nodes[0].long()
-        valid = torch.arange(tr.caps[0], device=dev) < sb.n_nodes[0]
-        y = torch.where(valid, tr.labels[seeds].long(), torch.full_like(seeds, -100))
-        loss = F.cross_entropy(logits.float(), y, ignore_index=-100)
+        from paper_2207_14696_b200.aggregate import softmax_ce
+        loss = softmax_ce(logits, tr.labels, sb.nodes[0], sb.n_nodes[0])
         tr.flat_grad.zero_()
         loss.backward()
         tr.opt.step()
