@@ -194,21 +194,23 @@ int fg_f32_to_bf16(const float* in, int64_t count, const uint16_t* relu_mask,
                    uint16_t* out, void* cuda_stream);
 
 /* Gather-form backward of the hidden block mean (no float atomics, no
- * zero-fill of an fp32 accumulator).  fg_block_transpose builds the
- * block's transpose by counting sort: t_indptr [cap_src + 1] over source
- * ranks and t_dst (the dst of every edge, grouped by source; order within a
- * source is scheduling-dependent); scratch = 2*cap_src int32.
+ * zero-fill of an fp32 accumulator).  fg_block_transpose builds the block's
+ * transpose by counting sort (histogram, single-pass scan, placement):
+ * t_indptr [cap_src + 1] over source ranks, and per edge grouped by source
+ * its dst (t_dst) and weight 1/cnt(dst) (t_w); order within a source is
+ * scheduling-dependent.  scratch: fg_block_transpose_scratch_bytes(cap_src).
  * fg_block_mean_bwd_t then computes, for every source row r < cap_src,
- *   out[r] = relu'(mask[r]) * sum_{i in t_indptr[r]..} g[t_dst[i]] / cnt(t_dst[i])
- * (rows without edges get 0). */
+ *   out[r] = relu'(mask[r]) * sum_{i in t_indptr[r]..} t_w[i] * g[t_dst[i], :h_dim]
+ * (rows >= *n_src_dev or without edges get 0; g has row pitch g_ld). */
+int64_t fg_block_transpose_scratch_bytes(int64_t cap_src);
 int fg_block_transpose(const int32_t* src_local, const int64_t* n_edges_dev,
                        int64_t cap_e, const int32_t* indptr,
                        const int64_t* num_dst_dev, int64_t max_dst, int64_t cap_src,
-                       int32_t* t_indptr, int32_t* t_dst, int32_t* scratch,
-                       void* cuda_stream);
+                       int32_t* t_indptr, int32_t* t_dst, float* t_w, void* scratch,
+                       int64_t scratch_bytes, void* cuda_stream);
 int fg_block_mean_bwd_t(const uint16_t* grad_out, int64_t h_dim, int64_t g_ld,
                         const int32_t* t_indptr, const int32_t* t_dst,
-                        const int32_t* indptr, int64_t cap_src,
+                        const float* t_w, const int64_t* n_src_dev, int64_t cap_src,
                         const uint16_t* relu_mask, uint16_t* out, void* cuda_stream);
 
 /* Fused softmax cross-entropy over padded logits [rows, ld] (bf16 or fp32):

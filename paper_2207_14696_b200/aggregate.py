@@ -66,8 +66,10 @@ class BlockMean(torch.autograd.Function):
         out = torch.empty((max_dst, ld), dtype=torch.bfloat16, device=h_src.device)
         N.call("fg_block_mean_fwd", N.ptr(h_src), H, N.ptr(indptr), N.ptr(local), N.ptr(n_dst),
                max_dst, N.ptr(out), ld, int(relu), N.stream_handle())
-        t_indptr, t_dst = trans if trans is not None else (indptr, indptr)
-        ctx.save_for_backward(indptr, local, n_dst, h_src if relu else indptr, t_indptr, t_dst)
+        t_indptr, t_dst, t_w, n_src = trans if trans is not None else (indptr, indptr, n_dst,
+                                                                        n_dst)
+        ctx.save_for_backward(indptr, local, n_dst, h_src if relu else indptr, t_indptr, t_dst,
+                              t_w, n_src)
         ctx.relu = relu
         ctx.H = H
         ctx.gather_bwd = trans is not None
@@ -77,7 +79,7 @@ class BlockMean(torch.autograd.Function):
 
     @staticmethod
     def backward(ctx, g):
-        indptr, local, n_dst, h_src, t_indptr, t_dst = ctx.saved_tensors
+        indptr, local, n_dst, h_src, t_indptr, t_dst, t_w, n_src = ctx.saved_tensors
         if not ctx.relu:
             h_src = None
         g = g.contiguous().to(torch.bfloat16)
@@ -85,7 +87,8 @@ class BlockMean(torch.autograd.Function):
         if ctx.gather_bwd:  # gather over the block's transpose, no float atomics
             gh = torch.empty((ctx.n_src, H), dtype=torch.bfloat16, device=g.device)
             N.call("fg_block_mean_bwd_t", N.ptr(g), H, g.shape[1], N.ptr(t_indptr), N.ptr(t_dst),
-                   N.ptr(indptr), ctx.n_src, N.ptr(h_src), N.ptr(gh), N.stream_handle())
+                   N.ptr(t_w), N.ptr(n_src), ctx.n_src, N.ptr(h_src), N.ptr(gh),
+                   N.stream_handle())
             return gh, None, None, None, None, None, None, None
         if g.shape[1] != H:
             g = g[:, :H].contiguous()
@@ -100,8 +103,8 @@ class BlockMean(torch.autograd.Function):
 
 def block_mean(h_src, indptr, local, n_dst, max_dst: int, relu: bool = False, trans=None,
                bias_col: bool = False):
-    """``trans`` = (t_indptr, t_dst) of the block (DeviceSampler with
-    need_transpose) switches the backward to the gather form; ``bias_col``
+    """``trans`` = (t_indptr, t_dst, t_w, n_src) of the block (DeviceSampler
+    with need_transpose) switches the backward to the gather form; ``bias_col``
     appends a [1, 0 x 7] column block (output width H + 8) so the next
     layer's bias is a column of its weight."""
     return BlockMean.apply(h_src, indptr, local, n_dst, max_dst, relu, trans, bias_col)

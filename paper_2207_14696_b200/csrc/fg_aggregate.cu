@@ -5,6 +5,9 @@
 // row-stochastic mean of factors.py:108-114 over hidden rows; backward
 // scatters grad/cnt with fp32 vector atomics.  HBM/L2 bound.
 #include "fg_common.cuh"
+#include "fg_scan.cuh"
+
+#include <cub/block/block_scan.cuh>
 
 namespace fg {
 
@@ -194,59 +197,60 @@ __global__ void k_t_hist(const int32_t* __restrict__ local, const int64_t* __res
     atomicAdd(cnt + local[e], 1);
 }
 
-__global__ void __launch_bounds__(1024)
+// exclusive scan of the per-source counts (single pass, look-back);
+// writes t_indptr and the placement cursors
+constexpr int kTsPer = 8;
+__global__ void __launch_bounds__(256)
 k_t_scan(int64_t n, const int32_t* __restrict__ cnt, int32_t* __restrict__ t_indptr,
-         int32_t* __restrict__ cursor) {
-  // single CTA: exclusive scan of n counts (n ~ 1e5: ~100 iterations)
-  __shared__ int32_t warp_sums[32];
-  __shared__ int32_t carry;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int64_t base = 0; base < n; base += 1024) {
-    const int64_t i = base + threadIdx.x;
-    const int32_t v = i < n ? cnt[i] : 0;
-    int32_t x = v;
+         int32_t* __restrict__ cursor, unsigned long long* status, unsigned int* ctr,
+         unsigned int ntiles) {
+  using BS = cub::BlockScan<unsigned long long, 256>;
+  __shared__ typename BS::TempStorage tmp;
+  __shared__ unsigned int s_u32;
+  __shared__ unsigned long long s_u64;
+  const ScanState sc{status, ctr, ctr + 1};
+  const unsigned int tile = scan_take_tile(sc, &s_u32);
+  const int64_t i0 = (int64_t)tile * 256 * kTsPer + threadIdx.x * (int64_t)kTsPer;
+  int32_t v[kTsPer];
+  unsigned long long c = 0;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
-    }
-    if (lane == 31) warp_sums[wid] = x;
-    __syncthreads();
-    if (wid == 0) {
-      int32_t w = warp_sums[lane];
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int32_t y = __shfl_up_sync(0xffffffffu, w, o);
-        if (lane >= o) w += y;
-      }
-      warp_sums[lane] = w;
-    }
-    __syncthreads();
-    const int32_t excl = carry + (wid ? warp_sums[wid - 1] : 0) + x - v;
-    if (i < n) {
-      t_indptr[i] = excl;
-      cursor[i] = excl;
-    }
-    __syncthreads();
-    if (threadIdx.x == 1023) carry = excl + v;
-    __syncthreads();
+  for (int k = 0; k < kTsPer; ++k) {
+    v[k] = i0 + k < n ? cnt[i0 + k] : 0;
+    c += (unsigned long long)v[k];
   }
-  if (threadIdx.x == 0) t_indptr[n] = carry;
+  unsigned long long excl, agg;
+  BS(tmp).ExclusiveSum(c, excl, agg);
+  const unsigned long long prefix = scan_tile_prefix(sc, tile, agg, &s_u64);
+  int32_t pos = (int32_t)(prefix + excl);
+#pragma unroll
+  for (int k = 0; k < kTsPer; ++k) {
+    if (i0 + k < n) {
+      t_indptr[i0 + k] = pos;
+      cursor[i0 + k] = pos;
+    }
+    pos += v[k];
+  }
+  if (scan_last_block(sc, ntiles, &s_u32) && threadIdx.x == 0)
+    t_indptr[n] = (int32_t)(status[ntiles - 1] & kScanValMask);
 }
 
 // place every edge; t_dst receives the dst of the edge (found from indptr)
 __global__ void k_t_place(const int32_t* __restrict__ local, const int64_t* __restrict__ ne_dev,
                           int64_t cap_e, const int32_t* __restrict__ indptr,
                           const int64_t* __restrict__ nd_dev, int64_t max_dst,
-                          int32_t* __restrict__ cursor, int32_t* __restrict__ t_dst) {
+                          int32_t* __restrict__ cursor, int32_t* __restrict__ t_dst,
+                          float* __restrict__ t_w) {
   const int64_t nd = min64(*nd_dev, max_dst);
   // thread per destination: its picks are contiguous in [indptr[v], indptr[v+1])
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nd;
        v += (int64_t)gridDim.x * blockDim.x) {
     const int32_t e0 = indptr[v], e1 = indptr[v + 1];
-    for (int32_t e = e0; e < e1; ++e) t_dst[atomicAdd(cursor + local[e], 1)] = (int32_t)v;
+    const float w = e1 > e0 ? 1.0f / (float)(e1 - e0) : 0.f;
+    for (int32_t e = e0; e < e1; ++e) {
+      const int32_t slot = atomicAdd(cursor + local[e], 1);
+      t_dst[slot] = (int32_t)v;
+      t_w[slot] = w;
+    }
   }
 }
 
@@ -254,14 +258,20 @@ template <bool RELU>
 __global__ void __launch_bounds__(256)
 k_block_mean_bwd_t(const uint16_t* __restrict__ g, int64_t H, int64_t g_ld,
                    const int32_t* __restrict__ t_indptr,
-                   const int32_t* __restrict__ t_dst, const int32_t* __restrict__ indptr,
-                   int64_t cap_src, const uint16_t* __restrict__ mask, uint16_t* __restrict__ out) {
+                   const int32_t* __restrict__ t_dst, const float* __restrict__ t_w,
+                   const int64_t* __restrict__ nsrc_dev, int64_t cap_src,
+                   const uint16_t* __restrict__ mask, uint16_t* __restrict__ out) {
   const int64_t chunks = H >> 3;
   const int64_t total = cap_src * chunks;
+  const int64_t live = live_count(nsrc_dev, cap_src);
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = t / chunks, c = t - r * chunks;
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (r >= live) {  // padded source rows: zero gradient, no loads
+      reinterpret_cast<uint4*>(out + r * H)[c] = make_uint4(0u, 0u, 0u, 0u);
+      continue;
+    }
     const int32_t i0 = t_indptr[r], i1 = t_indptr[r + 1];
     for (int32_t i = i0; i < i1; i += 4) {
       uint4 q[4];
@@ -270,7 +280,7 @@ k_block_mean_bwd_t(const uint16_t* __restrict__ g, int64_t H, int64_t g_ld,
       for (int u = 0; u < 4; ++u) {
         if (i + u < i1) {
           const int32_t v = t_dst[i + u];
-          sc[u] = 1.0f / (float)(indptr[v + 1] - indptr[v]);
+          sc[u] = t_w[i + u];
           q[u] = __ldg(reinterpret_cast<const uint4*>(g + (int64_t)v * g_ld) + c);
         }
       }
@@ -321,28 +331,42 @@ __global__ void k_step_inc(int64_t* step) { *step += 1; }
 
 }  // namespace fg
 
+extern "C" int64_t fg_block_transpose_scratch_bytes(int64_t cap_src) {
+  const int64_t nt = ceil_div(cap_src > 0 ? cap_src : 1, 256 * fg::kTsPer);
+  return 2 * cap_src * 4 + 64 + nt * 8 + 256;
+}
+
 extern "C" int fg_block_transpose(const int32_t* local, const int64_t* n_edges_dev, int64_t cap_e,
                                   const int32_t* indptr, const int64_t* n_dst_dev,
                                   int64_t max_dst, int64_t cap_src, int32_t* t_indptr,
-                                  int32_t* t_dst, int32_t* scratch, void* s) {
+                                  int32_t* t_dst, float* t_w, void* scratch,
+                                  int64_t scratch_bytes, void* s) {
   FG_CHECK_ARG(cap_src >= 1, "fg_block_transpose: empty source capacity");
+  FG_CHECK_ARG(scratch_bytes >= fg_block_transpose_scratch_bytes(cap_src),
+               "fg_block_transpose: scratch too small");
   cudaStream_t st = as_stream(s);
-  int32_t* cnt = scratch;              // [cap_src]
-  int32_t* cursor = scratch + cap_src;  // [cap_src]
-  FG_CUDA_TRY(cudaMemsetAsync(cnt, 0, cap_src * sizeof(int32_t), st));
+  const int64_t nt = ceil_div(cap_src, 256 * fg::kTsPer);
+  // layout: [ctr 64 B | status nt*8 | cnt cap_src | cursor cap_src]; one memset
+  char* base = (char*)scratch;
+  unsigned int* ctr = (unsigned int*)base;
+  unsigned long long* status = (unsigned long long*)(base + 64);
+  int32_t* cnt = (int32_t*)(base + 64 + nt * 8);
+  int32_t* cursor = cnt + cap_src;
+  FG_CUDA_TRY(cudaMemsetAsync(scratch, 0, 64 + nt * 8 + cap_src * 4, st));
   fg::k_t_hist<<<grid_for(cap_e, 256), 256, 0, st>>>(local, n_edges_dev, cap_e, cnt);
   FG_LAUNCH_CHECK();
-  fg::k_t_scan<<<1, 1024, 0, st>>>(cap_src, cnt, t_indptr, cursor);
+  fg::k_t_scan<<<(unsigned)nt, 256, 0, st>>>(cap_src, cnt, t_indptr, cursor, status, ctr,
+                                             (unsigned)nt);
   FG_LAUNCH_CHECK();
   fg::k_t_place<<<grid_for(max_dst, 256), 256, 0, st>>>(local, n_edges_dev, cap_e, indptr,
-                                                        n_dst_dev, max_dst, cursor, t_dst);
+                                                        n_dst_dev, max_dst, cursor, t_dst, t_w);
   FG_LAUNCH_CHECK();
   return FG_OK;
 }
 
 extern "C" int fg_block_mean_bwd_t(const uint16_t* g, int64_t H, int64_t g_ld,
                                    const int32_t* t_indptr, const int32_t* t_dst,
-                                   const int32_t* indptr, int64_t cap_src,
+                                   const float* t_w, const int64_t* n_src_dev, int64_t cap_src,
                                    const uint16_t* relu_mask, uint16_t* out, void* s) {
   FG_CHECK_ARG(H % 8 == 0, "hidden dim must be a multiple of 8");
   if (g_ld == 0) g_ld = H;
@@ -351,10 +375,10 @@ extern "C" int fg_block_mean_bwd_t(const uint16_t* g, int64_t H, int64_t g_ld,
   const int64_t total = cap_src * (H / 8);
   if (relu_mask)
     fg::k_block_mean_bwd_t<true><<<grid_for(total, 256), 256, 0, as_stream(s)>>>(
-        g, H, g_ld, t_indptr, t_dst, indptr, cap_src, relu_mask, out);
+        g, H, g_ld, t_indptr, t_dst, t_w, n_src_dev, cap_src, relu_mask, out);
   else
     fg::k_block_mean_bwd_t<false><<<grid_for(total, 256), 256, 0, as_stream(s)>>>(
-        g, H, g_ld, t_indptr, t_dst, indptr, cap_src, nullptr, out);
+        g, H, g_ld, t_indptr, t_dst, t_w, n_src_dev, cap_src, nullptr, out);
   FG_LAUNCH_CHECK();
   return FG_OK;
 }

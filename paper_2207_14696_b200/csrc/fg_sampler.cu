@@ -8,20 +8,20 @@
 // rejected (probability (2^32 mod (j+1)) / 2^32).  So node i's first draw sits
 // at stream offset sum_{i'<i} draws(i'), a prefix sum; each thread jumps its
 // own PCG64 cursor there (128-bit LCG jump table) and runs Floyd serially.
-// A node whose Lemire draw was rejected consumed extra draws: every later node
-// of the layer is then redone with the corrected offset by a cooperative
-// fix-up kernel (rare: ~f*deg/2^32 per node).  Deterministic, no float math.
+// The prefix sum is single-pass (decoupled look-back, fg_scan.cuh) inside the
+// sampling kernel itself.  A node whose Lemire draw was rejected consumed
+// extra draws: every later node of the layer is then redone with the
+// corrected offset by the CTA that finishes last (rare: ~f*deg/2^32 per
+// node), which also advances the stream.  Deterministic, no float math.
 //
 // np.unique over node ids (< n) is done with a bitmap: mark, popcount
 // prefix, ordered emit (ascending ids), rank lookup, clear.
-#include <cooperative_groups.h>
 #include <cub/block/block_reduce.cuh>
 #include <cub/block/block_scan.cuh>
 
 #include "fg_common.cuh"
 #include "fg_pcg64.cuh"
-
-namespace cg = cooperative_groups;
+#include "fg_scan.cuh"
 
 namespace fg {
 
@@ -29,12 +29,15 @@ constexpr int kSampThreads = 256;
 constexpr int kLocalF = 32;           // fanouts up to this use a local index buffer
 constexpr int64_t kNoBad = INT64_MAX;
 
+// Layer workspace.  The head (counters + scalars + look-back status) is
+// zeroed by one memset per layer.
 struct LayerWs {
-  int64_t* block_sums;  // [2 * nb] (picks, draws) per block
-  int64_t* block_offs;  // [2 * nb]
+  unsigned int* ctr;    // [0] tile ticket, [1] done ticket
+  int64_t* scal;        // [0] total picks, [1] total draws, [2] bad key, [3] delta
+  unsigned long long* status;  // [nb] look-back status words
   int64_t* draw_off;    // [N] nominal stream offset per node
   uint32_t* used;       // [N] draws actually consumed
-  int64_t* scal;        // [8]: 0 total picks, 1 total draws, 2 bad slot 0, 3 bad slot 1, 4 delta
+  int64_t head_bytes;   // bytes to zero per layer
 };
 
 inline int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
@@ -43,17 +46,19 @@ inline LayerWs carve(void* ws, int64_t N) {
   const int64_t nb = ceil_div(N > 0 ? N : 1, kSampThreads);
   char* p = (char*)ws;
   LayerWs w;
-  w.block_sums = (int64_t*)p; p += align256(2 * nb * 8);
-  w.block_offs = (int64_t*)p; p += align256(2 * nb * 8);
+  w.ctr = (unsigned int*)p;
+  w.scal = (int64_t*)(p + 64);
+  w.status = (unsigned long long*)(p + 128);
+  w.head_bytes = align256(128 + nb * 8);
+  p += w.head_bytes;
   w.draw_off = (int64_t*)p; p += align256(N * 8);
-  w.used = (uint32_t*)p; p += align256(N * 4);
-  w.scal = (int64_t*)p; p += align256(8 * 8);
+  w.used = (uint32_t*)p;
   return w;
 }
 
 inline int64_t layer_ws_bytes(int64_t N) {
   const int64_t nb = ceil_div(N > 0 ? N : 1, kSampThreads);
-  return 2 * align256(2 * nb * 8) + align256(N * 8) + align256(N * 4) + align256(64);
+  return align256(128 + nb * 8) + align256(N * 8) + align256(N * 4);
 }
 
 __device__ __forceinline__ void node_counts(const int64_t* __restrict__ off,
@@ -109,137 +114,83 @@ __device__ uint32_t sample_node(const int64_t* __restrict__ off, const int32_t* 
   return used;
 }
 
+// packed per-node (picks, draws): draws in bits 30..61, picks in bits 0..29
+constexpr int kPickBits = 30;
+constexpr unsigned long long kPickMask = (1ull << kPickBits) - 1;
+
 __global__ void __launch_bounds__(kSampThreads)
-k_layer_count(const int64_t* __restrict__ off, const int32_t* __restrict__ nodes,
-              const int64_t* __restrict__ nlive, int64_t N, int f, LayerWs ws,
-              int32_t* err_flag) {
-  using BR = cub::BlockReduce<int64_t, kSampThreads>;
-  __shared__ typename BR::TempStorage tmp;
-  const int64_t i = blockIdx.x * (int64_t)kSampThreads + threadIdx.x;
+k_layer(const int64_t* __restrict__ off, const int32_t* __restrict__ col,
+        const int32_t* __restrict__ nodes, const int64_t* __restrict__ nlive, int64_t N, int f,
+        uint64_t* __restrict__ rng, LayerWs ws, int32_t* __restrict__ indptr,
+        int32_t* __restrict__ picks, int64_t max_picks, int64_t* __restrict__ num_picks,
+        int32_t* __restrict__ err_flag, unsigned int ntiles) {
+  using BS = cub::BlockScan<unsigned long long, kSampThreads>;
+  __shared__ typename BS::TempStorage tmp;
+  __shared__ unsigned int s_u32;
+  __shared__ unsigned long long s_u64;
+  __shared__ int64_t s_bad;
+  const ScanState sc{ws.status, ws.ctr, ws.ctr + 1};
+  const unsigned int tile = scan_take_tile(sc, &s_u32);
+  const int64_t i = (int64_t)tile * kSampThreads + threadIdx.x;
   const int64_t live = min64(*nlive, N);
   int64_t deg, cnt, draws;
   node_counts(off, nodes, i, live, f, deg, cnt, draws);
   if (deg > 10000 && f > deg / 50) atomicExch(err_flag, FG_EUSAGE);  // numpy's FY branch
-  const int64_t sp = BR(tmp).Sum(cnt);
-  __syncthreads();
-  const int64_t sd = BR(tmp).Sum(draws);
-  if (threadIdx.x == 0) {
-    ws.block_sums[2 * blockIdx.x] = sp;
-    ws.block_sums[2 * blockIdx.x + 1] = sd;
-  }
-}
-
-// single block: exclusive scan of per-block (picks, draws)
-__global__ void __launch_bounds__(1024)
-k_layer_scan(int64_t nb, LayerWs ws, int64_t* __restrict__ num_picks, int64_t max_picks,
-             int32_t* err_flag) {
-  using BS = cub::BlockScan<int64_t, 1024>;
-  __shared__ typename BS::TempStorage tmp;
-  __shared__ int64_t carry[2];
-  if (threadIdx.x == 0) carry[0] = carry[1] = 0;
-  __syncthreads();
-  for (int64_t base = 0; base < nb; base += 1024) {
-    const int64_t i = base + threadIdx.x;
-    for (int k = 0; k < 2; ++k) {
-      const int64_t v = i < nb ? ws.block_sums[2 * i + k] : 0;
-      int64_t ex, agg;
-      BS(tmp).ExclusiveSum(v, ex, agg);
-      __syncthreads();
-      if (i < nb) ws.block_offs[2 * i + k] = ex + carry[k];
-      __syncthreads();
-      if (threadIdx.x == 0) carry[k] += agg;
-      __syncthreads();
-    }
-  }
-  if (threadIdx.x == 0) {
-    ws.scal[0] = carry[0];
-    ws.scal[1] = carry[1];
-    ws.scal[2] = kNoBad;
-    ws.scal[3] = kNoBad;
-    ws.scal[4] = 0;
-    *num_picks = carry[0];
-    if (carry[0] > max_picks) atomicExch(err_flag, FG_EUSAGE);
-  }
-}
-
-__global__ void __launch_bounds__(kSampThreads)
-k_layer_sample(const int64_t* __restrict__ off, const int32_t* __restrict__ col,
-               const int32_t* __restrict__ nodes, const int64_t* __restrict__ nlive, int64_t N,
-               int f, const uint64_t* __restrict__ rng, LayerWs ws, int32_t* __restrict__ indptr,
-               int32_t* __restrict__ picks, int64_t max_picks, uint32_t* __restrict__ bitmap) {
-  using BS = cub::BlockScan<int64_t, kSampThreads>;
-  __shared__ typename BS::TempStorage tmp;
-  const int64_t i = blockIdx.x * (int64_t)kSampThreads + threadIdx.x;
-  const int64_t live = min64(*nlive, N);
-  int64_t deg, cnt, draws;
-  node_counts(off, nodes, i, live, f, deg, cnt, draws);
-  int64_t pick_off, draw_off;
-  BS(tmp).ExclusiveSum(cnt, pick_off);
-  __syncthreads();
-  BS(tmp).ExclusiveSum(draws, draw_off);
-  pick_off += ws.block_offs[2 * blockIdx.x];
-  draw_off += ws.block_offs[2 * blockIdx.x + 1];
+  const unsigned long long mine = ((unsigned long long)draws << kPickBits) | (unsigned long long)cnt;
+  unsigned long long excl, agg;
+  BS(tmp).ExclusiveSum(mine, excl, agg);
+  const unsigned long long prefix = scan_tile_prefix(sc, tile, agg, &s_u64);
+  const int64_t pick_off = (int64_t)((prefix & kPickMask) + (excl & kPickMask));
+  const int64_t draw_off = (int64_t)((prefix >> kPickBits) + (excl >> kPickBits));
   if (i < N) indptr[i] = (int32_t)pick_off;
   if (i == N - 1) indptr[N] = (int32_t)(pick_off + cnt);
-  if (i >= live || pick_off + cnt > max_picks) return;
-  ws.draw_off[i] = draw_off;
-  const uint32_t used = sample_node(off, col, nodes[i], f, rng, (uint64_t)draw_off,
-                                    picks + pick_off, bitmap);
-  ws.used[i] = used;
-  if ((int64_t)used != draws) atomicMin((long long*)&ws.scal[2], (long long)i);
-}
-
-// Cooperative fix-up + stream advance.  Every block reads the first rejecting
-// node; in the common case there is none and only the stream advance runs.
-__global__ void __launch_bounds__(kSampThreads)
-k_layer_fixup(const int64_t* __restrict__ off, const int32_t* __restrict__ col,
-              const int32_t* __restrict__ nodes, const int64_t* __restrict__ nlive, int64_t N,
-              int f, uint64_t* __restrict__ rng, LayerWs ws, const int32_t* __restrict__ indptr,
-              int32_t* __restrict__ picks, uint32_t* __restrict__ bitmap, int64_t n_nodes_graph) {
-  const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t gsize = (int64_t)gridDim.x * blockDim.x;
-  volatile int64_t* scal = ws.scal;
-  int64_t cur = scal[2];
-  int64_t delta = 0;
-  if (cur != kNoBad) {
-    cg::grid_group grid = cg::this_grid();
-    const int64_t live = min64(*nlive, N);
-    int rd = 2;
-    while (cur != kNoBad) {
-      const int64_t nominal = 2 * (int64_t)f - 1;
-      delta += (int64_t)ws.used[cur] - nominal;
-      const int wr = rd == 2 ? 3 : 2;
-      for (int64_t i = cur + 1 + gtid; i < live; i += gsize) {
-        const int32_t u = nodes[i];
-        const int64_t deg = off[u + 1] - off[u];
-        if (deg <= f) continue;  // no draws: picks unaffected by the stream
-        const uint32_t used = sample_node(off, col, u, f, rng, (uint64_t)(ws.draw_off[i] + delta),
-                                          picks + indptr[i], nullptr);
-        ws.used[i] = used;
-        if ((int64_t)used != nominal) atomicMin((long long*)&ws.scal[wr], (long long)i);
-      }
-      grid.sync();
-      cur = scal[wr];
-      grid.sync();
-      if (gtid == 0) scal[rd] = kNoBad;
-      grid.sync();
-      rd = wr;
-    }
-    // picks changed after the first rejection: rebuild this layer's marks
-    if (bitmap) {
-      const int64_t words = (n_nodes_graph + 31) >> 5;
-      for (int64_t w = gtid; w < words; w += gsize) bitmap[w] = 0;
-      grid.sync();
-      const int64_t total = scal[0];
-      for (int64_t e = gtid; e < total; e += gsize) {
-        const int32_t v = picks[e];
-        atomicOr(bitmap + (v >> 5), 1u << (v & 31));
-      }
-    }
-    if (gtid == 0) scal[4] = delta;
+  if (i < live && pick_off + cnt <= max_picks) {
+    ws.draw_off[i] = draw_off;
+    const uint32_t used = sample_node(off, col, nodes[i], f, rng, (uint64_t)draw_off,
+                                      picks + pick_off, nullptr);
+    ws.used[i] = used;
+    if ((int64_t)used != draws)
+      atomicMax((long long*)&ws.scal[2], (long long)(INT64_MAX - i));
   }
-  if (gtid == 0) {
-    const uint64_t T = (uint64_t)(scal[1] + delta);
+  if (!scan_last_block(sc, ntiles, &s_u32)) return;
+  // ---- last CTA: totals, rejection fix-up, stream advance
+  const unsigned long long total = ws.status[ntiles - 1] & kScanValMask;
+  const int64_t tot_picks = (int64_t)(total & kPickMask);
+  const int64_t tot_draws = (int64_t)(total >> kPickBits);
+  if (threadIdx.x == 0) {
+    *num_picks = tot_picks;
+    ws.scal[0] = tot_picks;
+    ws.scal[1] = tot_draws;
+    if (tot_picks > max_picks) atomicExch(err_flag, FG_EUSAGE);
+    s_bad = *(volatile int64_t*)&ws.scal[2];
+  }
+  __syncthreads();
+  int64_t bad = s_bad;
+  int64_t delta = 0;
+  const int64_t nominal = 2 * (int64_t)f - 1;
+  while (bad != 0) {
+    const int64_t b = INT64_MAX - bad;
+    delta += (int64_t)ws.used[b] - nominal;
+    __syncthreads();
+    if (threadIdx.x == 0) *(volatile int64_t*)&ws.scal[2] = 0;
+    __syncthreads();
+    for (int64_t k = b + 1 + threadIdx.x; k < live; k += blockDim.x) {
+      const int32_t u = nodes[k];
+      if (off[u + 1] - off[u] <= f) continue;  // no draws: unaffected
+      const uint32_t used = sample_node(off, col, u, f, rng, (uint64_t)(ws.draw_off[k] + delta),
+                                        picks + indptr[k], nullptr);
+      ws.used[k] = used;
+      if ((int64_t)used != nominal) atomicMax((long long*)&ws.scal[2], (long long)(INT64_MAX - k));
+    }
+    __threadfence_block();
+    __syncthreads();
+    if (threadIdx.x == 0) s_bad = *(volatile int64_t*)&ws.scal[2];
+    __syncthreads();
+    bad = s_bad;
+  }
+  if (threadIdx.x == 0) {
+    ws.scal[3] = delta;
+    const uint64_t T = (uint64_t)(tot_draws + delta);
     PcgCursor c = rng_cursor_at(rng, T);
     rng[RNG_STATE] = c.s.lo;
     rng[RNG_STATE + 1] = c.s.hi;
@@ -273,56 +224,30 @@ __global__ void k_mark64(const int64_t* __restrict__ ids, const int64_t* __restr
   }
 }
 
+// Single-pass compaction: popcounts, block scan, look-back prefix, ordered
+// emit of set bits (ascending ids) and the per-word rank prefix.
 __global__ void __launch_bounds__(kBmThreads)
-k_bm_count(const uint32_t* __restrict__ bm, int64_t words, int64_t* __restrict__ bsum) {
-  using BR = cub::BlockReduce<int64_t, kBmThreads>;
-  __shared__ typename BR::TempStorage tmp;
-  const int64_t w0 = blockIdx.x * kBmPerBlock + threadIdx.x * (int64_t)kBmWords;
-  int64_t c = 0;
-#pragma unroll
-  for (int k = 0; k < kBmWords; ++k)
-    if (w0 + k < words) c += __popc(bm[w0 + k]);
-  const int64_t s = BR(tmp).Sum(c);
-  if (threadIdx.x == 0) bsum[blockIdx.x] = s;
-}
-
-__global__ void __launch_bounds__(1024)
-k_bm_scan(int64_t nb, const int64_t* __restrict__ bsum, int64_t* __restrict__ boff,
-          int64_t* __restrict__ out_count) {
-  using BS = cub::BlockScan<int64_t, 1024>;
+k_bm_compact(const uint32_t* __restrict__ bm, int64_t words, unsigned long long* status,
+             unsigned int* ctr, int32_t* __restrict__ out, int64_t max_out,
+             int64_t* __restrict__ out_count, int32_t* __restrict__ wprefix, unsigned int ntiles) {
+  using BS = cub::BlockScan<unsigned long long, kBmThreads>;
   __shared__ typename BS::TempStorage tmp;
-  __shared__ int64_t carry;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  for (int64_t base = 0; base < nb; base += 1024) {
-    const int64_t i = base + threadIdx.x;
-    const int64_t v = i < nb ? bsum[i] : 0;
-    int64_t ex, agg;
-    BS(tmp).ExclusiveSum(v, ex, agg);
-    if (i < nb) boff[i] = ex + carry;
-    __syncthreads();
-    if (threadIdx.x == 0) carry += agg;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) *out_count = carry;
-}
-
-__global__ void __launch_bounds__(kBmThreads)
-k_bm_emit(const uint32_t* __restrict__ bm, int64_t words, const int64_t* __restrict__ boff,
-          int32_t* __restrict__ out, int64_t max_out, int32_t* __restrict__ wprefix) {
-  using BS = cub::BlockScan<int64_t, kBmThreads>;
-  __shared__ typename BS::TempStorage tmp;
-  const int64_t w0 = blockIdx.x * kBmPerBlock + threadIdx.x * (int64_t)kBmWords;
+  __shared__ unsigned int s_u32;
+  __shared__ unsigned long long s_u64;
+  const ScanState sc{status, ctr, ctr + 1};
+  const unsigned int tile = scan_take_tile(sc, &s_u32);
+  const int64_t w0 = (int64_t)tile * kBmPerBlock + threadIdx.x * (int64_t)kBmWords;
   uint32_t wv[kBmWords];
-  int64_t c = 0;
+  unsigned long long c = 0;
 #pragma unroll
   for (int k = 0; k < kBmWords; ++k) {
     wv[k] = (w0 + k < words) ? bm[w0 + k] : 0u;
     c += __popc(wv[k]);
   }
-  int64_t pos;
-  BS(tmp).ExclusiveSum(c, pos);
-  pos += boff[blockIdx.x];
+  unsigned long long excl, agg;
+  BS(tmp).ExclusiveSum(c, excl, agg);
+  const unsigned long long prefix = scan_tile_prefix(sc, tile, agg, &s_u64);
+  int64_t pos = (int64_t)(prefix + excl);
 #pragma unroll
   for (int k = 0; k < kBmWords; ++k) {
     if (w0 + k >= words) break;
@@ -335,6 +260,8 @@ k_bm_emit(const uint32_t* __restrict__ bm, int64_t words, const int64_t* __restr
       ++pos;
     }
   }
+  if (scan_last_block(sc, ntiles, &s_u32) && threadIdx.x == 0)
+    *out_count = (int64_t)(status[ntiles - 1] & kScanValMask);
 }
 
 __global__ void k_bm_rank(const int32_t* __restrict__ ids, const int64_t* __restrict__ cnt,
@@ -377,50 +304,31 @@ int fg_sample_layer(const int64_t* row_offsets, const int32_t* col_indices, int6
                fanout);
   FG_CHECK_ARG(max_nodes >= 1 && n >= 1, "fg_sample_layer: empty layer capacity");
   FG_CHECK_ARG(ws_bytes >= layer_ws_bytes(max_nodes), "fg_sample_layer: workspace too small");
-  FG_CHECK_ARG(max_picks < INT32_MAX, "fg_sample_layer: picks must fit int32 offsets");
+  FG_CHECK_ARG(max_picks < INT32_MAX && max_picks < (1ll << kPickBits),
+               "fg_sample_layer: picks must fit int32 offsets");
   FG_CHECK_ARG(row_offsets && col_indices && nodes && num_nodes_dev && rng_dev && indptr &&
                    picks && num_picks_dev && err_flag,
                "fg_sample_layer: null argument");
   cudaStream_t st = as_stream(s);
   LayerWs w = carve(ws, max_nodes);
   const int64_t nb = ceil_div(max_nodes, kSampThreads);
-  k_layer_count<<<(unsigned)nb, kSampThreads, 0, st>>>(row_offsets, nodes, num_nodes_dev,
-                                                       max_nodes, fanout, w, err_flag);
+  FG_CUDA_TRY(cudaMemsetAsync(ws, 0, w.head_bytes, st));
+  k_layer<<<(unsigned)nb, kSampThreads, 0, st>>>(row_offsets, col_indices, nodes, num_nodes_dev,
+                                                 max_nodes, fanout, rng_dev, w, indptr, picks,
+                                                 max_picks, num_picks_dev, err_flag,
+                                                 (unsigned)nb);
   FG_LAUNCH_CHECK();
-  k_layer_scan<<<1, 1024, 0, st>>>(nb, w, num_picks_dev, max_picks, err_flag);
-  FG_LAUNCH_CHECK();
-  k_layer_sample<<<(unsigned)nb, kSampThreads, 0, st>>>(row_offsets, col_indices, nodes,
-                                                        num_nodes_dev, max_nodes, fanout, rng_dev,
-                                                        w, indptr, picks, max_picks, bitmap);
-  FG_LAUNCH_CHECK();
-  // cooperative fix-up: grid sized to be co-resident
-  static thread_local int coop_blocks = 0;
-  if (coop_blocks == 0) {
-    int per_sm = 0;
-    FG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_layer_fixup,
-                                                              kSampThreads, 0));
-    coop_blocks = sm_count() * (per_sm < 2 ? (per_sm < 1 ? 1 : per_sm) : 2);
+  if (bitmap) {  // next layer's unique set: mark after any fix-up rewrote picks
+    k_mark32<<<grid_for(max_picks, 256), 256, 0, st>>>(picks, num_picks_dev, max_picks, bitmap);
+    FG_LAUNCH_CHECK();
   }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(coop_blocks);
-  cfg.blockDim = dim3(kSampThreads);
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  FG_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_layer_fixup, row_offsets, col_indices, nodes,
-                                 num_nodes_dev, max_nodes, fanout, rng_dev, w,
-                                 (const int32_t*)indptr, picks, bitmap, n));
-  count_launch();
   return FG_OK;
 }
 
 int64_t fg_bitmap_workspace_bytes(int64_t n) {
   const int64_t words = (n + 31) / 32;
   const int64_t nb = ceil_div(words > 0 ? words : 1, kBmPerBlock);
-  return 2 * align256(nb * 8);
+  return align256(64 + nb * 8);
 }
 
 int fg_bitmap_mark(const int32_t* ids, const int64_t* cnt, int64_t max_count, uint32_t* bm,
@@ -446,13 +354,11 @@ int fg_bitmap_compact(uint32_t* bm, int64_t n, int32_t* out_ids, int64_t max_out
   cudaStream_t st = as_stream(s);
   const int64_t words = (n + 31) / 32;
   const int64_t nb = ceil_div(words, kBmPerBlock);
-  int64_t* bsum = (int64_t*)ws;
-  int64_t* boff = (int64_t*)((char*)ws + align256(nb * 8));
-  k_bm_count<<<(unsigned)nb, kBmThreads, 0, st>>>(bm, words, bsum);
-  FG_LAUNCH_CHECK();
-  k_bm_scan<<<1, 1024, 0, st>>>(nb, bsum, boff, out_count);
-  FG_LAUNCH_CHECK();
-  k_bm_emit<<<(unsigned)nb, kBmThreads, 0, st>>>(bm, words, boff, out_ids, max_out, wprefix);
+  unsigned int* ctr = (unsigned int*)ws;
+  unsigned long long* status = (unsigned long long*)((char*)ws + 64);
+  FG_CUDA_TRY(cudaMemsetAsync(ws, 0, 64 + nb * 8, st));
+  k_bm_compact<<<(unsigned)nb, kBmThreads, 0, st>>>(bm, words, status, ctr, out_ids, max_out,
+                                                    out_count, wprefix, (unsigned)nb);
   FG_LAUNCH_CHECK();
   return FG_OK;
 }

@@ -141,12 +141,14 @@ class DeviceSampler:
         self.local = [z(pcaps[l]) if (need_local and l < L - 1) else None for l in range(L)]
         # per hidden block: transpose (source rank -> edges) for the gather bwd
         self.need_transpose = need_transpose and need_local
-        self.t_indptr, self.t_dst = [], []
+        self.t_indptr, self.t_dst, self.t_w = [], [], []
         if self.need_transpose:
             for l in range(L - 1):
                 self.t_indptr.append(z(caps[l + 1] + 1))
                 self.t_dst.append(z(pcaps[l]))
-            self.t_scratch = z(2 * max(caps[1:]))
+                self.t_w.append(z(pcaps[l], dt=torch.float32))
+            nbytes = N.lib().fg_block_transpose_scratch_bytes(max(caps[1:]))
+            self.t_scratch = torch.zeros(nbytes, dtype=torch.uint8, device=dev)
         words = (n + 31) // 32
         self.bitmap = torch.zeros(words, dtype=torch.int32, device=dev)
         self.wprefix = torch.zeros(words, dtype=torch.int32, device=dev)
@@ -241,7 +243,8 @@ class DeviceSampler:
         out = SampledBatch(self.nodes, self.n_nodes, self.indptr, self.picks, self.n_picks,
                            self.local)
         if self.need_transpose:
-            out.trans = [(self.t_indptr[l], self.t_dst[l]) for l in range(L - 1)] + [None]
+            out.trans = [(self.t_indptr[l], self.t_dst[l], self.t_w[l], self.n_nodes[l + 1])
+                         for l in range(L - 1)] + [None]
         if self.want_frontier:
             N.call("fg_bitmap_compact", N.ptr(self.fbitmap), n, N.ptr(self.frontier), self.fcap,
                    N.ptr(self.n_frontier), None, N.ptr(self.ws_fbm), self.ws_fbm.numel(), s)
@@ -255,7 +258,8 @@ class DeviceSampler:
         the gather-form backward of the hidden block mean."""
         N.call("fg_block_transpose", N.ptr(self.local[l]), N.ptr(self.n_picks[l]), self.pcaps[l],
                N.ptr(self.indptr[l]), N.ptr(self.n_nodes[l]), self.caps[l], self.caps[l + 1],
-               N.ptr(self.t_indptr[l]), N.ptr(self.t_dst[l]), N.ptr(self.t_scratch), s)
+               N.ptr(self.t_indptr[l]), N.ptr(self.t_dst[l]), N.ptr(self.t_w[l]),
+               N.ptr(self.t_scratch), self.t_scratch.numel(), s)
 
     def sample(self, b: int) -> SampledBatch:
         self.load_seeds(b)

@@ -148,11 +148,13 @@ def test_hidden_block_mean_fused_relu():
 
 def _transpose_np(indptr, src, n_dst, n_src):
     e = np.arange(src.size)
-    dst = np.repeat(np.arange(n_dst), np.diff(indptr[:n_dst + 1]))
+    cnt = np.diff(indptr[:n_dst + 1])
+    dst = np.repeat(np.arange(n_dst), cnt)
     order = np.lexsort((e, src))
     t_indptr = np.zeros(n_src + 1, np.int32)
     np.add.at(t_indptr, src + 1, 1)
-    return np.cumsum(t_indptr).astype(np.int32), dst[order].astype(np.int32)
+    w = (1.0 / np.maximum(cnt, 1)).astype(np.float32)[dst]
+    return np.cumsum(t_indptr).astype(np.int32), dst[order].astype(np.int32), w[order]
 
 
 @pytest.mark.parametrize("relu", [False, True])
@@ -160,11 +162,12 @@ def test_hidden_block_mean_gather_backward(relu):
     rng = np.random.default_rng(5)
     n_src, n_dst, max_dst, H = 2500, 600, 700, 64
     counts, indptr, src = _block(n_src, n_dst, max_dst, 9, rng)
-    ti, td = _transpose_np(indptr, src, n_dst, n_src)
+    ti, td, tw = _transpose_np(indptr, src, n_dst, n_src)
     dev = "cuda"
     h = torch.randn(n_src, H, device=dev).to(torch.bfloat16).requires_grad_(True)
     ip, sl = torch.from_numpy(indptr).to(dev), torch.from_numpy(src).to(dev)
-    trans = (torch.from_numpy(ti).to(dev), torch.from_numpy(td).to(dev))
+    trans = (torch.from_numpy(ti).to(dev), torch.from_numpy(td).to(dev),
+             torch.from_numpy(tw).to(dev), torch.tensor([n_src], device=dev))
     out = block_mean(h, ip, sl, torch.tensor([n_dst], device=dev), max_dst, relu=relu, trans=trans)
     hf = h.detach().float().requires_grad_(True)
     seg = torch.repeat_interleave(torch.arange(n_dst, device=dev), torch.from_numpy(counts).to(dev))
@@ -192,11 +195,16 @@ def test_block_transpose_kernel():
     local[:E] = torch.from_numpy(src).to(dev)
     t_indptr = torch.zeros(n_src + 1, dtype=torch.int32, device=dev)
     t_dst = torch.zeros(cap_e, dtype=torch.int32, device=dev)
-    scratch = torch.zeros(2 * n_src, dtype=torch.int32, device=dev)
-    N.call("fg_block_transpose", N.ptr(local), N.ptr(torch.tensor([E], device=dev)), cap_e,
-           N.ptr(torch.from_numpy(indptr).to(dev)), N.ptr(torch.tensor([n_dst], device=dev)),
-           max_dst, n_src, N.ptr(t_indptr), N.ptr(t_dst), N.ptr(scratch), N.stream_handle())
-    ti, td = _transpose_np(indptr, src, n_dst, n_src)
+    t_w = torch.zeros(cap_e, dtype=torch.float32, device=dev)
+    scratch = torch.zeros(N.lib().fg_block_transpose_scratch_bytes(n_src), dtype=torch.uint8,
+                          device=dev)
+    ne_t, nd_t = torch.tensor([E], device=dev), torch.tensor([n_dst], device=dev)
+    ip_t = torch.from_numpy(indptr).to(dev)  # keep every buffer alive until sync
+    N.call("fg_block_transpose", N.ptr(local), N.ptr(ne_t), cap_e, N.ptr(ip_t), N.ptr(nd_t),
+           max_dst, n_src, N.ptr(t_indptr), N.ptr(t_dst), N.ptr(t_w), N.ptr(scratch),
+           scratch.numel(), N.stream_handle())
+    torch.cuda.synchronize()
+    ti, td, tw = _transpose_np(indptr, src, n_dst, n_src)
     assert np.array_equal(t_indptr.cpu().numpy(), ti)
     got = t_dst[:E].cpu().numpy()
     for r in range(0, n_src, 7):  # same multiset of dsts per source
