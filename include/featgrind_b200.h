@@ -198,14 +198,16 @@ int fg_f32_to_bf16(const float* in, int64_t count, const uint16_t* relu_mask,
  * transpose by counting sort (histogram, single-pass scan, placement):
  * t_indptr [cap_src + 1] over source ranks, and per edge grouped by source
  * its dst (t_dst) and weight 1/cnt(dst) (t_w); order within a source is
- * scheduling-dependent.  scratch: fg_block_transpose_scratch_bytes(cap_src).
+ * scheduling-dependent.  max_per_dst bounds the picks per destination (the
+ * layer's fanout).  scratch: fg_block_transpose_scratch_bytes(cap_src).
  * fg_block_mean_bwd_t then computes, for every source row r < cap_src,
  *   out[r] = relu'(mask[r]) * sum_{i in t_indptr[r]..} t_w[i] * g[t_dst[i], :h_dim]
  * (rows >= *n_src_dev or without edges get 0; g has row pitch g_ld). */
 int64_t fg_block_transpose_scratch_bytes(int64_t cap_src);
 int fg_block_transpose(const int32_t* src_local, const int64_t* n_edges_dev,
                        int64_t cap_e, const int32_t* indptr,
-                       const int64_t* num_dst_dev, int64_t max_dst, int64_t cap_src,
+                       const int64_t* num_dst_dev, int64_t max_dst, int max_per_dst,
+                       int64_t cap_src,
                        int32_t* t_indptr, int32_t* t_dst, float* t_w, void* scratch,
                        int64_t scratch_bytes, void* cuda_stream);
 int fg_block_mean_bwd_t(const uint16_t* grad_out, int64_t h_dim, int64_t g_ld,

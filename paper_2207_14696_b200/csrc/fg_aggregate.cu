@@ -239,18 +239,21 @@ __global__ void k_t_place(const int32_t* __restrict__ local, const int64_t* __re
                           int64_t cap_e, const int32_t* __restrict__ indptr,
                           const int64_t* __restrict__ nd_dev, int64_t max_dst,
                           int32_t* __restrict__ cursor, int32_t* __restrict__ t_dst,
-                          float* __restrict__ t_w) {
+                          float* __restrict__ t_w, int fmax) {
   const int64_t nd = min64(*nd_dev, max_dst);
-  // thread per destination: its picks are contiguous in [indptr[v], indptr[v+1])
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nd;
-       v += (int64_t)gridDim.x * blockDim.x) {
+  // thread per (destination, pick slot k < fmax): picks of v are contiguous
+  // in [indptr[v], indptr[v+1]) and number at most fmax
+  const int64_t total = nd * fmax;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = t / fmax;
+    const int k = (int)(t - v * fmax);
     const int32_t e0 = indptr[v], e1 = indptr[v + 1];
-    const float w = e1 > e0 ? 1.0f / (float)(e1 - e0) : 0.f;
-    for (int32_t e = e0; e < e1; ++e) {
-      const int32_t slot = atomicAdd(cursor + local[e], 1);
-      t_dst[slot] = (int32_t)v;
-      t_w[slot] = w;
-    }
+    const int32_t e = e0 + k;
+    if (e >= e1) continue;
+    const int32_t slot = atomicAdd(cursor + local[e], 1);
+    t_dst[slot] = (int32_t)v;
+    t_w[slot] = 1.0f / (float)(e1 - e0);
   }
 }
 
@@ -272,6 +275,8 @@ k_block_mean_bwd_t(const uint16_t* __restrict__ g, int64_t H, int64_t g_ld,
       reinterpret_cast<uint4*>(out + r * H)[c] = make_uint4(0u, 0u, 0u, 0u);
       continue;
     }
+    uint4 mq = make_uint4(0u, 0u, 0u, 0u);
+    if (RELU) mq = __ldg(reinterpret_cast<const uint4*>(mask + r * H) + c);  // issued early
     const int32_t i0 = t_indptr[r], i1 = t_indptr[r + 1];
     for (int32_t i = i0; i < i1; i += 4) {
       uint4 q[4];
@@ -296,7 +301,7 @@ k_block_mean_bwd_t(const uint16_t* __restrict__ g, int64_t H, int64_t g_ld,
     }
     if (RELU) {
       float m[8];
-      bf16x8_to_f32(__ldg(reinterpret_cast<const uint4*>(mask + r * H) + c), m);
+      bf16x8_to_f32(mq, m);
 #pragma unroll
       for (int j = 0; j < 8; ++j) acc[j] = m[j] > 0.f ? acc[j] : 0.f;
     }
@@ -338,9 +343,10 @@ extern "C" int64_t fg_block_transpose_scratch_bytes(int64_t cap_src) {
 
 extern "C" int fg_block_transpose(const int32_t* local, const int64_t* n_edges_dev, int64_t cap_e,
                                   const int32_t* indptr, const int64_t* n_dst_dev,
-                                  int64_t max_dst, int64_t cap_src, int32_t* t_indptr,
-                                  int32_t* t_dst, float* t_w, void* scratch,
+                                  int64_t max_dst, int max_per_dst, int64_t cap_src,
+                                  int32_t* t_indptr, int32_t* t_dst, float* t_w, void* scratch,
                                   int64_t scratch_bytes, void* s) {
+  FG_CHECK_ARG(max_per_dst >= 1, "fg_block_transpose: max_per_dst must be >= 1");
   FG_CHECK_ARG(cap_src >= 1, "fg_block_transpose: empty source capacity");
   FG_CHECK_ARG(scratch_bytes >= fg_block_transpose_scratch_bytes(cap_src),
                "fg_block_transpose: scratch too small");
@@ -358,8 +364,8 @@ extern "C" int fg_block_transpose(const int32_t* local, const int64_t* n_edges_d
   fg::k_t_scan<<<(unsigned)nt, 256, 0, st>>>(cap_src, cnt, t_indptr, cursor, status, ctr,
                                              (unsigned)nt);
   FG_LAUNCH_CHECK();
-  fg::k_t_place<<<grid_for(max_dst, 256), 256, 0, st>>>(local, n_edges_dev, cap_e, indptr,
-                                                        n_dst_dev, max_dst, cursor, t_dst, t_w);
+  fg::k_t_place<<<grid_for(max_dst * max_per_dst, 256), 256, 0, st>>>(
+      local, n_edges_dev, cap_e, indptr, n_dst_dev, max_dst, cursor, t_dst, t_w, max_per_dst);
   FG_LAUNCH_CHECK();
   return FG_OK;
 }

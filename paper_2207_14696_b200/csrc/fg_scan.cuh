@@ -29,31 +29,53 @@ __device__ __forceinline__ unsigned int scan_take_tile(const ScanState& s, unsig
   return *smem_slot;
 }
 
+__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
 // Returns the exclusive prefix of `tile` given its aggregate (values are
-// non-negative sums of packed fields; must stay < 2^62).  All threads call.
+// non-negative sums of packed fields; must stay < 2^62).  All threads call;
+// warp 0 performs a 32-wide parallel look-back over predecessor tiles.
 __device__ __forceinline__ unsigned long long scan_tile_prefix(const ScanState& s, unsigned int tile,
                                                                unsigned long long agg,
                                                                unsigned long long* smem_slot) {
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {
     volatile unsigned long long* st = s.status;
+    const int lane = threadIdx.x;
     unsigned long long prefix = 0;
     if (tile == 0) {
-      st[0] = kScanFlagInc | agg;
+      if (lane == 0) st[0] = kScanFlagInc | agg;
     } else {
-      st[tile] = kScanFlagAgg | agg;
-      __threadfence();
-      int64_t j = (int64_t)tile - 1;
-      while (true) {
-        unsigned long long w;
-        do { w = st[j]; } while ((w >> 62) == 0);
-        prefix += w & kScanValMask;
-        if ((w >> 62) == 2) break;
-        --j;
+      if (lane == 0) {
+        st[tile] = kScanFlagAgg | agg;
+        __threadfence();
       }
-      __threadfence();
-      st[tile] = kScanFlagInc | (prefix + agg);
+      __syncwarp();
+      int64_t base = (int64_t)tile - 1;
+      while (true) {
+        const int64_t j = base - lane;
+        unsigned long long w = kScanFlagInc;  // before tile 0: prefix 0
+        if (j >= 0) w = st[j];
+        while (__any_sync(0xffffffffu, (w >> 62) == 0)) {
+          if ((w >> 62) == 0) w = st[j];
+        }
+        const unsigned int inc = __ballot_sync(0xffffffffu, (w >> 62) == 2);
+        if (inc) {
+          const int first = __ffs(inc) - 1;  // nearest predecessor with an inclusive prefix
+          prefix += warp_sum_u64(lane <= first ? (w & kScanValMask) : 0ull);
+          break;
+        }
+        prefix += warp_sum_u64(w & kScanValMask);
+        base -= 32;
+      }
+      if (lane == 0) {
+        __threadfence();
+        st[tile] = kScanFlagInc | (prefix + agg);
+      }
     }
-    *smem_slot = prefix;
+    if (lane == 0) *smem_slot = prefix;
   }
   __syncthreads();
   return *smem_slot;

@@ -257,8 +257,8 @@ class DeviceSampler:
         """Block l's transpose (source rank -> dst of each incoming edge) for
         the gather-form backward of the hidden block mean."""
         N.call("fg_block_transpose", N.ptr(self.local[l]), N.ptr(self.n_picks[l]), self.pcaps[l],
-               N.ptr(self.indptr[l]), N.ptr(self.n_nodes[l]), self.caps[l], self.caps[l + 1],
-               N.ptr(self.t_indptr[l]), N.ptr(self.t_dst[l]), N.ptr(self.t_w[l]),
+               N.ptr(self.indptr[l]), N.ptr(self.n_nodes[l]), self.caps[l], self.fanouts[l],
+               self.caps[l + 1], N.ptr(self.t_indptr[l]), N.ptr(self.t_dst[l]), N.ptr(self.t_w[l]),
                N.ptr(self.t_scratch), self.t_scratch.numel(), s)
 
     def sample(self, b: int) -> SampledBatch:

@@ -201,7 +201,7 @@ def test_block_transpose_kernel():
     ne_t, nd_t = torch.tensor([E], device=dev), torch.tensor([n_dst], device=dev)
     ip_t = torch.from_numpy(indptr).to(dev)  # keep every buffer alive until sync
     N.call("fg_block_transpose", N.ptr(local), N.ptr(ne_t), cap_e, N.ptr(ip_t), N.ptr(nd_t),
-           max_dst, n_src, N.ptr(t_indptr), N.ptr(t_dst), N.ptr(t_w), N.ptr(scratch),
+           max_dst, 10, n_src, N.ptr(t_indptr), N.ptr(t_dst), N.ptr(t_w), N.ptr(scratch),
            scratch.numel(), N.stream_handle())
     torch.cuda.synchronize()
     ti, td, tw = _transpose_np(indptr, src, n_dst, n_src)
