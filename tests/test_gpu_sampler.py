@@ -87,10 +87,12 @@ def test_device_sampler_matches_oracle_on_products_like_graph():
     smp.check_errors()
 
 
-def test_sampler_lemire_rejection_fixup():
+@pytest.mark.parametrize("fanout,seeds", [(200, 40), (16, 60), (8, 120)])
+def test_sampler_lemire_rejection_fixup(fanout, seeds):
     """Hubs of degree ~3e6 make Lemire rejections likely (p ~ 5e-4 per
     draw); every rejection shifts all later stream offsets of the layer, which
-    the cooperative fix-up must repair for the picks to stay bit-exact."""
+    the fix-up must repair for the picks to stay bit-exact.  fanout 200 runs
+    the thread-per-node path, 16 and 8 the lane-group paths (G = 32 / 16)."""
     hubs, deg = 6, 3_000_017
     n = hubs + deg
     # bipartite: hub h connects to all leaves; leaves connect to all hubs
@@ -112,9 +114,9 @@ def test_sampler_lemire_rejection_fixup():
     g = fg.CsrGraph.trusted(n, off, col, True)
     dg = g.to_device()
     train = np.arange(hubs)
-    fans = (200,)
+    fans = (fanout,)
     total_rej = 0
-    for seed in range(40):
+    for seed in range(seeds):
         smp = DeviceSampler(dg, fans, hubs, need_local=False, want_frontier=True)
         smp.begin_epoch(train, seed)
         ref, ref_state = sample_batches_oracle(off, col, train, fans, hubs, seed)
@@ -124,5 +126,5 @@ def test_sampler_lemire_rejection_fixup():
         st = smp.stream_state()
         assert st["state"]["state"] == ref_state["state"]["state"], seed
         draws = int(smp.rng[6].item())
-        total_rej += draws - hubs * (2 * 200 - 1)
+        total_rej += draws - hubs * (2 * fanout - 1)
     assert total_rej > 0, "no Lemire rejection exercised"
