@@ -31,7 +31,7 @@ constexpr int kLocalF = 32;           // fanouts up to this use a local index bu
 // Layer workspace.  The head (counters + scalars + look-back status) is
 // zeroed by one memset per layer.
 struct LayerWs {
-  unsigned int* ctr;    // [0] tile ticket, [1] done ticket
+  unsigned int* ctr;    // [0] tile ticket, [1] prefix done ticket, [2] sample done ticket
   int64_t* scal;        // [0] total picks, [1] total draws, [2] bad key, [3] delta
   unsigned long long* status;  // [nb] look-back status words
   int64_t* draw_off;    // [N] nominal stream offset per node
@@ -41,9 +41,8 @@ struct LayerWs {
 
 inline int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
 
-// look-back tiles the layer kernels may use: G=32 lane groups put 8 nodes in
-// a tile, the thread path 256
-inline int64_t layer_tiles(int64_t N) { return ceil_div(N > 0 ? N : 1, kSampThreads / 32); }
+// look-back tiles of the prefix kernel (256 nodes each)
+inline int64_t layer_tiles(int64_t N) { return ceil_div(N > 0 ? N : 1, kSampThreads); }
 
 inline LayerWs carve(void* ws, int64_t N) {
   const int64_t nb = layer_tiles(N);
@@ -128,19 +127,10 @@ __device__ void layer_finish(const int64_t* __restrict__ off, const int32_t* __r
                              uint64_t* __restrict__ rng, LayerWs ws,
                              const int32_t* __restrict__ indptr, int32_t* __restrict__ picks,
                              int64_t max_picks, int64_t* __restrict__ num_picks,
-                             int32_t* __restrict__ err_flag, unsigned int ntiles,
-                             int64_t* s_bad_slot) {
+                             int32_t* __restrict__ err_flag, int64_t* s_bad_slot) {
   int64_t& s_bad = *s_bad_slot;
-  const unsigned long long total = ws.status[ntiles - 1] & kScanValMask;
-  const int64_t tot_picks = (int64_t)(total & kPickMask);
-  const int64_t tot_draws = (int64_t)(total >> kPickBits);
-  if (threadIdx.x == 0) {
-    *num_picks = tot_picks;
-    ws.scal[0] = tot_picks;
-    ws.scal[1] = tot_draws;
-    if (tot_picks > max_picks) atomicExch(err_flag, FG_EUSAGE);
-    s_bad = *(volatile int64_t*)&ws.scal[2];
-  }
+  const int64_t tot_draws = ws.scal[1];  // from the prefix kernel
+  if (threadIdx.x == 0) s_bad = *(volatile int64_t*)&ws.scal[2];
   __syncthreads();
   int64_t bad = s_bad;
   int64_t delta = 0;
@@ -202,17 +192,18 @@ __global__ void k_mark64(const int64_t* __restrict__ ids, const int64_t* __restr
 }
 
 
+// Kernel 1 of a layer: per-node (picks, draws) counts and their exclusive
+// prefix in one pass (look-back); writes indptr and each node's stream
+// offset; the last CTA writes the totals.
 __global__ void __launch_bounds__(kSampThreads)
-k_layer(const int64_t* __restrict__ off, const int32_t* __restrict__ col,
-        const int32_t* __restrict__ nodes, const int64_t* __restrict__ nlive, int64_t N, int f,
-        uint64_t* __restrict__ rng, LayerWs ws, int32_t* __restrict__ indptr,
-        int32_t* __restrict__ picks, int64_t max_picks, int64_t* __restrict__ num_picks,
-        int32_t* __restrict__ err_flag, unsigned int ntiles) {
+k_layer_prefix(const int64_t* __restrict__ off, const int32_t* __restrict__ nodes,
+               const int64_t* __restrict__ nlive, int64_t N, int f, LayerWs ws,
+               int32_t* __restrict__ indptr, int64_t max_picks, int64_t* __restrict__ num_picks,
+               int32_t* __restrict__ err_flag, unsigned int ntiles) {
   using BS = cub::BlockScan<unsigned long long, kSampThreads>;
   __shared__ typename BS::TempStorage tmp;
   __shared__ unsigned int s_u32;
   __shared__ unsigned long long s_u64;
-  __shared__ int64_t s_bad;
   const ScanState sc{ws.status, ws.ctr, ws.ctr + 1};
   const unsigned int tile = scan_take_tile(sc, &s_u32);
   const int64_t i = (int64_t)tile * kSampThreads + threadIdx.x;
@@ -228,140 +219,164 @@ k_layer(const int64_t* __restrict__ off, const int32_t* __restrict__ col,
   const int64_t draw_off = (int64_t)((prefix >> kPickBits) + (excl >> kPickBits));
   if (i < N) indptr[i] = (int32_t)pick_off;
   if (i == N - 1) indptr[N] = (int32_t)(pick_off + cnt);
-  if (i < live && pick_off + cnt <= max_picks) {
-    ws.draw_off[i] = draw_off;
-    const uint32_t used = sample_node(off, col, nodes[i], f, rng, (uint64_t)draw_off,
-                                      picks + pick_off, nullptr);
-    ws.used[i] = used;
-    if ((int64_t)used != draws)
-      atomicMax((long long*)&ws.scal[2], (long long)(INT64_MAX - i));
+  if (i < live) ws.draw_off[i] = draw_off;
+  if (scan_last_block(sc, ntiles, &s_u32) && threadIdx.x == 0) {
+    const unsigned long long total = ws.status[ntiles - 1] & kScanValMask;
+    const int64_t tot_picks = (int64_t)(total & kPickMask);
+    *num_picks = tot_picks;
+    ws.scal[0] = tot_picks;
+    ws.scal[1] = (int64_t)(total >> kPickBits);
+    if (tot_picks > max_picks) atomicExch(err_flag, FG_EUSAGE);
   }
-  if (!scan_last_block(sc, ntiles, &s_u32)) return;
-  layer_finish(off, col, nodes, live, f, rng, ws, indptr, picks, max_picks, num_picks, err_flag,
-               ntiles, &s_bad);
 }
 
-// Lane-group variant for fanouts with 2f-1 <= G: a group of G lanes owns one
-// node.  Lane t computes the node's t-th 32-bit draw directly (group leader
-// jumps the PCG64 cursor to the node's stream offset; lanes step <= 16
-// outputs further through the jump table), all Lemire draws are evaluated in
-// parallel, then Floyd's duplicate rule and the tail shuffle run as f and
-// f-1 shuffle steps.  If any of the node's draws would be rejected by
-// Lemire, the leader redoes the node serially (exact numpy consumption).
-// Cuts the per-node critical path ~5x versus the serial thread path.
-template <int G>
+// Last CTA of the sampling kernel (done ticket ctr[2]): fix-up + advance.
+__device__ __forceinline__ bool sample_last_block(LayerWs ws, unsigned int nblocks,
+                                                  unsigned int* slot) {
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) *slot = atomicAdd(ws.ctr + 2, 1u) == nblocks - 1 ? 1u : 0u;
+  __syncthreads();
+  const bool last = *slot != 0;
+  if (last) __threadfence();
+  return last;
+}
+
+// Kernel 2 (D = 2f-1 > 32): thread per node, serial numpy-exact sampling.
 __global__ void __launch_bounds__(kSampThreads)
-k_layer_group(const int64_t* __restrict__ off, const int32_t* __restrict__ col,
-              const int32_t* __restrict__ nodes, const int64_t* __restrict__ nlive, int64_t N,
-              int f, uint64_t* __restrict__ rng, LayerWs ws, int32_t* __restrict__ indptr,
-              int32_t* __restrict__ picks, int64_t max_picks, int64_t* __restrict__ num_picks,
-              int32_t* __restrict__ err_flag, unsigned int ntiles) {
-  constexpr int NPB = kSampThreads / G;  // nodes per CTA tile
-  using BS = cub::BlockScan<unsigned long long, kSampThreads>;
-  __shared__ typename BS::TempStorage tmp;
+k_layer_sample(const int64_t* __restrict__ off, const int32_t* __restrict__ col,
+               const int32_t* __restrict__ nodes, const int64_t* __restrict__ nlive, int64_t N,
+               int f, uint64_t* __restrict__ rng, LayerWs ws, const int32_t* __restrict__ indptr,
+               int32_t* __restrict__ picks, int64_t max_picks, int64_t* __restrict__ num_picks,
+               int32_t* __restrict__ err_flag) {
   __shared__ unsigned int s_u32;
-  __shared__ unsigned long long s_u64;
   __shared__ int64_t s_bad;
-  __shared__ uint64_t s_tab[4 * 5];  // jump-table entries for 1, 2, 4, 8, 16 steps
-  if (threadIdx.x < 20) s_tab[threadIdx.x] = rng[RNG_TABLE + threadIdx.x];
-  const ScanState sc{ws.status, ws.ctr, ws.ctr + 1};
-  const unsigned int tile = scan_take_tile(sc, &s_u32);
-  const int gl = threadIdx.x % G;
-  const int64_t i = (int64_t)tile * NPB + threadIdx.x / G;
-  const unsigned int gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
   const int64_t live = min64(*nlive, N);
-  int64_t deg, cnt, draws;
-  node_counts(off, nodes, i, live, f, deg, cnt, draws);
-  if (gl == 0 && deg > 10000 && f > deg / 50) atomicExch(err_flag, FG_EUSAGE);
-  const unsigned long long mine =
-      gl == 0 ? (((unsigned long long)draws << kPickBits) | (unsigned long long)cnt) : 0ull;
-  unsigned long long excl, agg;
-  BS(tmp).ExclusiveSum(mine, excl, agg);
-  const unsigned long long prefix = scan_tile_prefix(sc, tile, agg, &s_u64);
-  excl = __shfl_sync(gmask, excl, 0, G);
-  const int64_t pick_off = (int64_t)((prefix & kPickMask) + (excl & kPickMask));
-  const int64_t draw_off = (int64_t)((prefix >> kPickBits) + (excl >> kPickBits));
-  if (gl == 0 && i < N) indptr[i] = (int32_t)pick_off;
-  if (gl == 0 && i == N - 1) indptr[N] = (int32_t)(pick_off + cnt);
-  if (i < live && pick_off + cnt <= max_picks) {
+  const int64_t i = blockIdx.x * (int64_t)kSampThreads + threadIdx.x;
+  if (i < live) {
     const int32_t u = nodes[i];
-    const int64_t b = off[u];
-    int32_t* out = picks + pick_off;
-    uint32_t used = 0;
-    if (deg <= f) {
-      for (int64_t t = gl; t < deg; t += G) out[t] = col[b + t];
-    } else {
-      // leader: cursor at the node's first draw; broadcast (state, buffered half)
-      uint64_t s_lo = 0, s_hi = 0;
-      uint32_t have = 0, hbuf = 0;
-      if (gl == 0) {
-        const PcgCursor c0 = rng_cursor_at(rng, (uint64_t)draw_off);
-        s_lo = c0.s.lo; s_hi = c0.s.hi; have = c0.have; hbuf = c0.hi;
-      }
-      s_lo = __shfl_sync(gmask, s_lo, 0, G);
-      s_hi = __shfl_sync(gmask, s_hi, 0, G);
-      have = __shfl_sync(gmask, have, 0, G);
-      hbuf = __shfl_sync(gmask, hbuf, 0, G);
-      const int D = 2 * f - 1;
-      uint32_t res = 0;
-      bool rej = false;
-      if (gl < D) {
-        uint32_t val;
-        if (have && gl == 0) {
-          val = hbuf;
-        } else {
-          const uint32_t q = have ? gl - 1 : gl;
-          uint32_t k = (q >> 1) + 1;  // outputs to step (<= 16)
-          u128 st = make_u128(s_hi, s_lo);
-#pragma unroll
-          for (int bit = 0; bit < 5; ++bit) {
-            if (k & (1u << bit)) {
-              const uint64_t* e = s_tab + 4 * bit;
-              st = muladd128(make_u128(e[1], e[0]), st, make_u128(e[3], e[2]));
-            }
-          }
-          const uint64_t o = xsl_rr(st);
-          val = (q & 1) ? (uint32_t)(o >> 32) : (uint32_t)o;
-        }
-        // range: Floyd step t < f draws on [0, deg-f+t]; shuffle draw t >= f on [0, 2f-1-t]
-        const uint32_t r = gl < f ? (uint32_t)(deg - f + gl) : (uint32_t)(2 * f - 1 - gl);
-        const uint32_t span = r + 1u;
-        const uint64_t m = (uint64_t)val * span;
-        const uint32_t low = (uint32_t)m;
-        if (low < span) rej = low < (0xFFFFFFFFu - r) % span;
-        res = (uint32_t)(m >> 32);
-      }
-      if (__any_sync(gmask, rej)) {
-        if (gl == 0) used = sample_node(off, col, u, f, rng, (uint64_t)draw_off, out, nullptr);
-      } else {
-        // Floyd: lane t < f ends holding the t-th chosen index
-        uint32_t sel = res;
-        for (int t = 0; t < f; ++t) {
-          const uint32_t vt = __shfl_sync(gmask, res, t, G);
-          const unsigned int hit = __ballot_sync(gmask, gl < t && sel == vt) & gmask;
-          if (gl == t && hit) sel = (uint32_t)(deg - f + t);
-        }
-        // tail shuffle: swap positions i and lemire(i) for i = f-1 .. 1
-        for (int ii = f - 1; ii >= 1; --ii) {
-          const uint32_t j = __shfl_sync(gmask, res, 2 * f - 1 - ii, G);
-          const uint32_t a = __shfl_sync(gmask, sel, ii, G);
-          const uint32_t bj = __shfl_sync(gmask, sel, (int)j, G);
-          if (gl == ii) sel = bj;
-          if (gl == (int)j) sel = a;
-        }
-        if (gl < f) out[gl] = col[b + sel];
-        used = (uint32_t)D;
-      }
-    }
-    if (gl == 0) {
-      ws.draw_off[i] = draw_off;
+    const int64_t deg = off[u + 1] - off[u];
+    const int32_t po = indptr[i];
+    const int64_t draws = deg > f ? 2 * (int64_t)f - 1 : 0;
+    if (po + min64(deg, f) <= max_picks) {
+      const uint32_t used = sample_node(off, col, u, f, rng, (uint64_t)ws.draw_off[i], picks + po,
+                                        nullptr);
       ws.used[i] = used;
       if ((int64_t)used != draws) atomicMax((long long*)&ws.scal[2], (long long)(INT64_MAX - i));
     }
   }
-  if (!scan_last_block(sc, ntiles, &s_u32)) return;
+  if (!sample_last_block(ws, gridDim.x, &s_u32)) return;
   layer_finish(off, col, nodes, live, f, rng, ws, indptr, picks, max_picks, num_picks, err_flag,
-               ntiles, &s_bad);
+               &s_bad);
+}
+
+// Kernel 2 (D = 2f-1 <= G): a group of G lanes owns one node.  Lane t
+// computes the node's t-th 32-bit draw directly (the group leader jumps the
+// PCG64 cursor to the node's stream offset; lanes step <= 16 outputs further
+// through the jump table), every Lemire draw is evaluated in parallel, then
+// Floyd's duplicate rule and the tail shuffle run as f and f-1 shuffle
+// steps.  If any draw of the node would be rejected by Lemire the leader
+// redoes the node serially (exact numpy consumption; the layer fix-up then
+// shifts later nodes).
+template <int G>
+__global__ void __launch_bounds__(kSampThreads)
+k_layer_sample_group(const int64_t* __restrict__ off, const int32_t* __restrict__ col,
+                     const int32_t* __restrict__ nodes, const int64_t* __restrict__ nlive,
+                     int64_t N, int f, uint64_t* __restrict__ rng, LayerWs ws,
+                     const int32_t* __restrict__ indptr, int32_t* __restrict__ picks,
+                     int64_t max_picks, int64_t* __restrict__ num_picks,
+                     int32_t* __restrict__ err_flag) {
+  constexpr int NPB = kSampThreads / G;
+  __shared__ unsigned int s_u32;
+  __shared__ int64_t s_bad;
+  __shared__ uint64_t s_tab[4 * 5];  // jump-table entries for 1, 2, 4, 8, 16 steps
+  if (threadIdx.x < 20) s_tab[threadIdx.x] = rng[RNG_TABLE + threadIdx.x];
+  __syncthreads();
+  const int gl = threadIdx.x % G;
+  const int64_t i = blockIdx.x * (int64_t)NPB + threadIdx.x / G;
+  const unsigned int gmask =
+      G == 32 ? 0xffffffffu : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
+  const int64_t live = min64(*nlive, N);
+  if (i < live) {
+    const int32_t u = nodes[i];
+    const int64_t b = off[u];
+    const int64_t deg = off[u + 1] - b;
+    const int32_t po = indptr[i];
+    const int64_t draw_off = ws.draw_off[i];
+    int32_t* out = picks + po;
+    uint32_t used = 0;
+    if (po + min64(deg, f) <= max_picks) {
+      if (deg <= f) {
+        for (int64_t t = gl; t < deg; t += G) out[t] = col[b + t];
+      } else {
+        uint64_t s_lo = 0, s_hi = 0;
+        uint32_t have = 0, hbuf = 0;
+        if (gl == 0) {
+          const PcgCursor c0 = rng_cursor_at(rng, (uint64_t)draw_off);
+          s_lo = c0.s.lo; s_hi = c0.s.hi; have = c0.have; hbuf = c0.hi;
+        }
+        s_lo = __shfl_sync(gmask, s_lo, 0, G);
+        s_hi = __shfl_sync(gmask, s_hi, 0, G);
+        have = __shfl_sync(gmask, have, 0, G);
+        hbuf = __shfl_sync(gmask, hbuf, 0, G);
+        const int D = 2 * f - 1;
+        uint32_t res = 0;
+        bool rej = false;
+        if (gl < D) {
+          uint32_t val;
+          if (have && gl == 0) {
+            val = hbuf;
+          } else {
+            const uint32_t q = have ? gl - 1 : gl;
+            const uint32_t k = (q >> 1) + 1;  // outputs to step (<= 16)
+            u128 st = make_u128(s_hi, s_lo);
+#pragma unroll
+            for (int bit = 0; bit < 5; ++bit) {
+              if (k & (1u << bit)) {
+                const uint64_t* e = s_tab + 4 * bit;
+                st = muladd128(make_u128(e[1], e[0]), st, make_u128(e[3], e[2]));
+              }
+            }
+            const uint64_t o = xsl_rr(st);
+            val = (q & 1) ? (uint32_t)(o >> 32) : (uint32_t)o;
+          }
+          // Floyd step t < f draws on [0, deg-f+t]; shuffle draw t >= f on [0, 2f-1-t]
+          const uint32_t r = gl < f ? (uint32_t)(deg - f + gl) : (uint32_t)(2 * f - 1 - gl);
+          const uint32_t span = r + 1u;
+          const uint64_t m = (uint64_t)val * span;
+          const uint32_t low = (uint32_t)m;
+          if (low < span) rej = low < (0xFFFFFFFFu - r) % span;
+          res = (uint32_t)(m >> 32);
+        }
+        if (__any_sync(gmask, rej)) {
+          if (gl == 0) used = sample_node(off, col, u, f, rng, (uint64_t)draw_off, out, nullptr);
+        } else {
+          uint32_t sel = res;  // lane t < f: t-th Floyd choice
+          for (int t = 0; t < f; ++t) {
+            const uint32_t vt = __shfl_sync(gmask, res, t, G);
+            const unsigned int hit = __ballot_sync(gmask, gl < t && sel == vt) & gmask;
+            if (gl == t && hit) sel = (uint32_t)(deg - f + t);
+          }
+          for (int ii = f - 1; ii >= 1; --ii) {  // tail shuffle
+            const uint32_t j = __shfl_sync(gmask, res, 2 * f - 1 - ii, G);
+            const uint32_t a = __shfl_sync(gmask, sel, ii, G);
+            const uint32_t bj = __shfl_sync(gmask, sel, (int)j, G);
+            if (gl == ii) sel = bj;
+            if (gl == (int)j) sel = a;
+          }
+          if (gl < f) out[gl] = col[b + sel];
+          used = (uint32_t)D;
+        }
+        if (gl == 0) {
+          ws.used[i] = used;
+          if ((int64_t)used != D) atomicMax((long long*)&ws.scal[2], (long long)(INT64_MAX - i));
+        }
+      }
+    }
+  }
+  if (!sample_last_block(ws, gridDim.x, &s_u32)) return;
+  layer_finish(off, col, nodes, live, f, rng, ws, indptr, picks, max_picks, num_picks, err_flag,
+               &s_bad);
 }
 
 // Single-pass compaction: popcounts, block scan, look-back prefix, ordered
@@ -452,25 +467,28 @@ int fg_sample_layer(const int64_t* row_offsets, const int32_t* col_indices, int6
   cudaStream_t st = as_stream(s);
   LayerWs w = carve(ws, max_nodes);
   FG_CUDA_TRY(cudaMemsetAsync(ws, 0, w.head_bytes, st));
+  const int64_t nt = ceil_div(max_nodes, kSampThreads);
+  k_layer_prefix<<<(unsigned)nt, kSampThreads, 0, st>>>(row_offsets, nodes, num_nodes_dev,
+                                                        max_nodes, fanout, w, indptr, max_picks,
+                                                        num_picks_dev, err_flag, (unsigned)nt);
+  FG_LAUNCH_CHECK();
   const int D = 2 * fanout - 1;
   if (D <= 32) {  // lane-group path: one group of G lanes per node
     const int G = D <= 16 ? 16 : 32;
     const int64_t nb = ceil_div(max_nodes, kSampThreads / G);
-    FG_CHECK_ARG(nb <= layer_tiles(max_nodes), "fg_sample_layer: workspace tiles");
     if (G == 16)
-      k_layer_group<16><<<(unsigned)nb, kSampThreads, 0, st>>>(
+      k_layer_sample_group<16><<<(unsigned)nb, kSampThreads, 0, st>>>(
           row_offsets, col_indices, nodes, num_nodes_dev, max_nodes, fanout, rng_dev, w, indptr,
-          picks, max_picks, num_picks_dev, err_flag, (unsigned)nb);
+          picks, max_picks, num_picks_dev, err_flag);
     else
-      k_layer_group<32><<<(unsigned)nb, kSampThreads, 0, st>>>(
+      k_layer_sample_group<32><<<(unsigned)nb, kSampThreads, 0, st>>>(
           row_offsets, col_indices, nodes, num_nodes_dev, max_nodes, fanout, rng_dev, w, indptr,
-          picks, max_picks, num_picks_dev, err_flag, (unsigned)nb);
+          picks, max_picks, num_picks_dev, err_flag);
   } else {
-    const int64_t nb = ceil_div(max_nodes, kSampThreads);
-    k_layer<<<(unsigned)nb, kSampThreads, 0, st>>>(row_offsets, col_indices, nodes,
-                                                   num_nodes_dev, max_nodes, fanout, rng_dev, w,
-                                                   indptr, picks, max_picks, num_picks_dev,
-                                                   err_flag, (unsigned)nb);
+    k_layer_sample<<<(unsigned)nt, kSampThreads, 0, st>>>(row_offsets, col_indices, nodes,
+                                                          num_nodes_dev, max_nodes, fanout,
+                                                          rng_dev, w, indptr, picks, max_picks,
+                                                          num_picks_dev, err_flag);
   }
   FG_LAUNCH_CHECK();
   if (bitmap) {  // next layer's unique set: mark after any fix-up rewrote picks
