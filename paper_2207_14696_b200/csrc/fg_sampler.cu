@@ -195,6 +195,47 @@ __global__ void k_mark64(const int64_t* __restrict__ ids, const int64_t* __restr
 // Kernel 1 of a layer: per-node (picks, draws) counts and their exclusive
 // prefix in one pass (look-back); writes indptr and each node's stream
 // offset; the last CTA writes the totals.
+// Register-resident Floyd + tail shuffle for a compile-time fanout F <= 16
+// (same draws and results as sample_node; no local-memory index buffer).
+template <int F>
+__device__ __forceinline__ uint32_t sample_node_reg(const int64_t* __restrict__ off,
+                                                    const int32_t* __restrict__ col, int32_t u,
+                                                    const uint64_t* blk, uint64_t q,
+                                                    int32_t* __restrict__ out) {
+  const int64_t b = off[u];
+  const int64_t deg = off[u + 1] - b;
+  if (deg <= F) {
+    for (int64_t t = 0; t < deg; ++t) out[t] = col[b + t];
+    return 0;
+  }
+  PcgCursor c = rng_cursor_at(blk, q);
+  uint32_t used = 0;
+  uint32_t idx[F];
+#pragma unroll
+  for (int t = 0; t < F; ++t) {
+    const uint32_t j = (uint32_t)(deg - F + t);
+    const uint32_t v = c.lemire(j, used);
+    bool dup = false;
+#pragma unroll
+    for (int s2 = 0; s2 < t; ++s2) dup |= idx[s2] == v;
+    idx[t] = dup ? j : v;
+  }
+#pragma unroll
+  for (int i = F - 1; i >= 1; --i) {
+    const uint32_t j = c.lemire((uint32_t)i, used);
+    uint32_t vj = idx[0];
+#pragma unroll
+    for (int s2 = 1; s2 < i; ++s2) vj = (uint32_t)s2 == j ? idx[s2] : vj;
+    vj = j == (uint32_t)i ? idx[i] : vj;
+#pragma unroll
+    for (int s2 = 0; s2 < i; ++s2) idx[s2] = (uint32_t)s2 == j ? idx[i] : idx[s2];
+    idx[i] = vj;
+  }
+#pragma unroll
+  for (int t = 0; t < F; ++t) out[t] = col[b + idx[t]];
+  return used;
+}
+
 __global__ void __launch_bounds__(kSampThreads)
 k_layer_prefix(const int64_t* __restrict__ off, const int32_t* __restrict__ nodes,
                const int64_t* __restrict__ nlive, int64_t N, int f, LayerWs ws,
@@ -242,7 +283,10 @@ __device__ __forceinline__ bool sample_last_block(LayerWs ws, unsigned int nbloc
   return last;
 }
 
-// Kernel 2 (D = 2f-1 > 32): thread per node, serial numpy-exact sampling.
+// Kernel 2, thread per node (large layers): serial numpy-exact sampling;
+// F > 0 selects the register-resident variant for that fanout.  The PCG64
+// block (state + jump table) is read from shared memory.
+template <int F>
 __global__ void __launch_bounds__(kSampThreads)
 k_layer_sample(const int64_t* __restrict__ off, const int32_t* __restrict__ col,
                const int32_t* __restrict__ nodes, const int64_t* __restrict__ nlive, int64_t N,
@@ -251,6 +295,9 @@ k_layer_sample(const int64_t* __restrict__ off, const int32_t* __restrict__ col,
                int32_t* __restrict__ err_flag) {
   __shared__ unsigned int s_u32;
   __shared__ int64_t s_bad;
+  __shared__ uint64_t s_blk[FG_RNG_WORDS];
+  for (int k = threadIdx.x; k < FG_RNG_WORDS; k += blockDim.x) s_blk[k] = rng[k];
+  __syncthreads();
   const int64_t live = min64(*nlive, N);
   const int64_t i = blockIdx.x * (int64_t)kSampThreads + threadIdx.x;
   if (i < live) {
@@ -259,8 +306,11 @@ k_layer_sample(const int64_t* __restrict__ off, const int32_t* __restrict__ col,
     const int32_t po = indptr[i];
     const int64_t draws = deg > f ? 2 * (int64_t)f - 1 : 0;
     if (po + min64(deg, f) <= max_picks) {
-      const uint32_t used = sample_node(off, col, u, f, rng, (uint64_t)ws.draw_off[i], picks + po,
-                                        nullptr);
+      const uint32_t used =
+          F > 0 ? sample_node_reg<(F > 0 ? F : 1)>(off, col, u, s_blk, (uint64_t)ws.draw_off[i],
+                                                   picks + po)
+                : sample_node(off, col, u, f, s_blk, (uint64_t)ws.draw_off[i], picks + po,
+                              nullptr);
       ws.used[i] = used;
       if ((int64_t)used != draws) atomicMax((long long*)&ws.scal[2], (long long)(INT64_MAX - i));
     }
@@ -289,9 +339,10 @@ k_layer_sample_group(const int64_t* __restrict__ off, const int32_t* __restrict_
   constexpr int NPB = kSampThreads / G;
   __shared__ unsigned int s_u32;
   __shared__ int64_t s_bad;
-  __shared__ uint64_t s_tab[4 * 5];  // jump-table entries for 1, 2, 4, 8, 16 steps
-  if (threadIdx.x < 20) s_tab[threadIdx.x] = rng[RNG_TABLE + threadIdx.x];
+  __shared__ uint64_t s_blk[FG_RNG_WORDS];  // PCG64 state + jump table
+  for (int k = threadIdx.x; k < FG_RNG_WORDS; k += blockDim.x) s_blk[k] = rng[k];
   __syncthreads();
+  const uint64_t* s_tab = s_blk + RNG_TABLE;  // entries for 1, 2, 4, 8, 16 steps
   const int gl = threadIdx.x % G;
   const int64_t i = blockIdx.x * (int64_t)NPB + threadIdx.x / G;
   const unsigned int gmask =
@@ -312,7 +363,7 @@ k_layer_sample_group(const int64_t* __restrict__ off, const int32_t* __restrict_
         uint64_t s_lo = 0, s_hi = 0;
         uint32_t have = 0, hbuf = 0;
         if (gl == 0) {
-          const PcgCursor c0 = rng_cursor_at(rng, (uint64_t)draw_off);
+          const PcgCursor c0 = rng_cursor_at(s_blk, (uint64_t)draw_off);
           s_lo = c0.s.lo; s_hi = c0.s.hi; have = c0.have; hbuf = c0.hi;
         }
         s_lo = __shfl_sync(gmask, s_lo, 0, G);
@@ -473,7 +524,7 @@ int fg_sample_layer(const int64_t* row_offsets, const int32_t* col_indices, int6
                                                         num_picks_dev, err_flag, (unsigned)nt);
   FG_LAUNCH_CHECK();
   const int D = 2 * fanout - 1;
-  if (D <= 32) {  // lane-group path: one group of G lanes per node
+  if (D <= 32 && max_nodes <= 32768) {  // small, latency-bound layer: G lanes per node
     const int G = D <= 16 ? 16 : 32;
     const int64_t nb = ceil_div(max_nodes, kSampThreads / G);
     if (G == 16)
@@ -485,10 +536,25 @@ int fg_sample_layer(const int64_t* row_offsets, const int32_t* col_indices, int6
           row_offsets, col_indices, nodes, num_nodes_dev, max_nodes, fanout, rng_dev, w, indptr,
           picks, max_picks, num_picks_dev, err_flag);
   } else {
-    k_layer_sample<<<(unsigned)nt, kSampThreads, 0, st>>>(row_offsets, col_indices, nodes,
-                                                          num_nodes_dev, max_nodes, fanout,
-                                                          rng_dev, w, indptr, picks, max_picks,
-                                                          num_picks_dev, err_flag);
+#define FG_SAMPLE_F(F)                                                                     \
+  k_layer_sample<F><<<(unsigned)nt, kSampThreads, 0, st>>>(                               \
+      row_offsets, col_indices, nodes, num_nodes_dev, max_nodes, fanout, rng_dev, w, indptr, \
+      picks, max_picks, num_picks_dev, err_flag)
+    switch (fanout) {
+      case 1: FG_SAMPLE_F(1); break;
+      case 2: FG_SAMPLE_F(2); break;
+      case 3: FG_SAMPLE_F(3); break;
+      case 4: FG_SAMPLE_F(4); break;
+      case 5: FG_SAMPLE_F(5); break;
+      case 6: FG_SAMPLE_F(6); break;
+      case 8: FG_SAMPLE_F(8); break;
+      case 10: FG_SAMPLE_F(10); break;
+      case 12: FG_SAMPLE_F(12); break;
+      case 15: FG_SAMPLE_F(15); break;
+      case 16: FG_SAMPLE_F(16); break;
+      default: FG_SAMPLE_F(0); break;
+    }
+#undef FG_SAMPLE_F
   }
   FG_LAUNCH_CHECK();
   if (bitmap) {  // next layer's unique set: mark after any fix-up rewrote picks

@@ -87,12 +87,15 @@ def test_device_sampler_matches_oracle_on_products_like_graph():
     smp.check_errors()
 
 
-@pytest.mark.parametrize("fanout,seeds", [(200, 40), (16, 60), (8, 120)])
-def test_sampler_lemire_rejection_fixup(fanout, seeds):
+@pytest.mark.parametrize("fanout,seeds,n_leaves", [(200, 40, 0), (16, 60, 0), (8, 120, 0),
+                                                    (5, 40, 40000)])
+def test_sampler_lemire_rejection_fixup(fanout, seeds, n_leaves):
     """Hubs of degree ~3e6 make Lemire rejections likely (p ~ 5e-4 per
     draw); every rejection shifts all later stream offsets of the layer, which
     the fix-up must repair for the picks to stay bit-exact.  fanout 200 runs
-    the thread-per-node path, 16 and 8 the lane-group paths (G = 32 / 16)."""
+    the thread-per-node path, 16 and 8 the lane-group paths (G = 32 / 16);
+    with 40k extra leaf seeds the layer is large enough for the register
+    thread path (F = 5)."""
     hubs, deg = 6, 3_000_017
     n = hubs + deg
     # bipartite: hub h connects to all leaves; leaves connect to all hubs
@@ -113,18 +116,19 @@ def test_sampler_lemire_rejection_fixup(fanout, seeds):
     col = np.concatenate(cols)
     g = fg.CsrGraph.trusted(n, off, col, True)
     dg = g.to_device()
-    train = np.arange(hubs)
+    train = np.arange(hubs + n_leaves)
+    bs = train.size
     fans = (fanout,)
     total_rej = 0
     for seed in range(seeds):
-        smp = DeviceSampler(dg, fans, hubs, need_local=False, want_frontier=True)
+        smp = DeviceSampler(dg, fans, bs, need_local=False, want_frontier=True)
         smp.begin_epoch(train, seed)
-        ref, ref_state = sample_batches_oracle(off, col, train, fans, hubs, seed)
+        ref, ref_state = sample_batches_oracle(off, col, train, fans, bs, seed)
         sb = smp.sample(0)
         np_ = int(sb.n_picks[0].item())
         assert np.array_equal(sb.picks[0][:np_].cpu().numpy(), ref[0].layers[0].picks), seed
         st = smp.stream_state()
         assert st["state"]["state"] == ref_state["state"]["state"], seed
         draws = int(smp.rng[6].item())
-        total_rej += draws - hubs * (2 * fanout - 1)
+        total_rej += draws - (hubs + n_leaves) * (2 * fanout - 1)
     assert total_rej > 0, "no Lemire rejection exercised"
