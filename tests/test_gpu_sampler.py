@@ -87,8 +87,27 @@ def test_device_sampler_matches_oracle_on_products_like_graph():
     smp.check_errors()
 
 
+def _seeds_with_hub_rejection(n_train, hubs, deg, fanout, want=2, limit=3000):
+    """Seeds whose stream rejects at least one Lemire draw while sampling
+    the hubs (which come first in the sorted layer), found with the oracle
+    PCG64 restatement."""
+    from oracle.pcg64 import Pcg64Stream
+    found = []
+    for seed in range(limit):
+        rng = np.random.default_rng(seed)
+        rng.permutation(np.arange(n_train))
+        st = Pcg64Stream.from_numpy(rng.bit_generator.state)
+        for _ in range(hubs):
+            st.choice_noreplace(deg, fanout)
+        if st.draws32 > hubs * (2 * fanout - 1):
+            found.append(seed)
+            if len(found) == want:
+                break
+    return found
+
+
 @pytest.mark.parametrize("fanout,seeds,n_leaves", [(200, 40, 0), (16, 60, 0), (8, 120, 0),
-                                                    (5, 40, 40000)])
+                                                    (5, None, 33000)])
 def test_sampler_lemire_rejection_fixup(fanout, seeds, n_leaves):
     """Hubs of degree ~3e6 make Lemire rejections likely (p ~ 5e-4 per
     draw); every rejection shifts all later stream offsets of the layer, which
@@ -120,7 +139,8 @@ def test_sampler_lemire_rejection_fixup(fanout, seeds, n_leaves):
     bs = train.size
     fans = (fanout,)
     total_rej = 0
-    for seed in range(seeds):
+    seed_list = range(seeds) if seeds else _seeds_with_hub_rejection(bs, hubs, deg + 1, fanout)
+    for seed in seed_list:
         smp = DeviceSampler(dg, fans, bs, need_local=False, want_frontier=True)
         smp.begin_epoch(train, seed)
         ref, ref_state = sample_batches_oracle(off, col, train, fans, bs, seed)
