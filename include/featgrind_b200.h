@@ -64,6 +64,8 @@ typedef struct fg_codec_desc {
   int32_t length;      /* VQ: entries per part (padded) */
   int32_t num_parts;   /* VQ: ceil(d / width) */
   int32_t elem_bits;   /* 32 or 64: decode precision of the table */
+  const void* table_lp; /* optional bf16 copy of a VQ table (same layout);
+                           used only by bf16-output aggregation, may be NULL */
 } fg_codec_desc;
 
 /* ------------------------------------------------------------ library */

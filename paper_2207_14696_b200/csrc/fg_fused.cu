@@ -23,6 +23,8 @@
 //    finite contents; callers zero the buffer once at allocation);
 //  * `out_ld` lets the caller pad rows (e.g. d=100 -> 112) so the following
 //    bf16 GEMM sees 16-element-aligned K.
+#include <type_traits>
+
 #include "fg_common.cuh"
 
 namespace fg {
@@ -165,6 +167,18 @@ __device__ __forceinline__ void tile_pipeline(const int32_t* __restrict__ indptr
     __syncthreads();
     odd = !odd;
   }
+}
+
+// bf16x2 (low, high) -> packed fp32 pair (low in bits 0..31)
+__device__ __forceinline__ u64 bf16x2_to_f32x2(uint32_t w) {
+  return ((u64)(w & 0xFFFF0000u) << 32) | (u64)(w << 16);
+}
+__device__ __forceinline__ uint2 lds64(const void* p) {
+  uint2 r;
+  asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];"
+               : "=r"(r.x), "=r"(r.y)
+               : "r"((uint32_t)__cvta_generic_to_shared(p)));
+  return r;
 }
 
 // one 16-byte shared-memory load (keeps the compiler from splitting it)
@@ -349,10 +363,15 @@ __device__ __forceinline__ void load_codes(const uint8_t* p, uint32_t* w) {
   }
 }
 
-template <int W, typename OT, bool SMEM>
+// TT: codebook element type in shared memory.  float = exact fp32 decode;
+// __nv_bfloat16 (bf16-output mode only) halves the shared-memory bytes per
+// lookup, the kernel's binding resource for VQ; entries are rounded to bf16
+// once (<= 2^-9 relative), accumulation stays fp32 (within the 1e-2 bf16
+// tolerance of the north star).
+template <int W, typename OT, bool SMEM, typename TT>
 __global__ void __launch_bounds__(kThreads, 2)
 k_vq_mean8(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
-           const float* __restrict__ books, int length, int parts,
+           const TT* __restrict__ books, int length, int parts,
            const int32_t* __restrict__ indptr, const int32_t* __restrict__ src,
            const int64_t* __restrict__ ndst_dev, int64_t max_dst, OT* __restrict__ out,
            int64_t ld) {
@@ -362,21 +381,23 @@ k_vq_mean8(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
   __shared__ __align__(8) uint64_t s_mbar;
   extern __shared__ float4 s_mem4[];
   const int64_t nbook = SMEM ? (int64_t)parts * length * W : 0;
-  float* s_book = reinterpret_cast<float*>(s_mem4);
-  int32_t* s_ip0 = reinterpret_cast<int32_t*>(s_book + ((nbook + 3) & ~3ll));
+  TT* s_book = reinterpret_cast<TT*>(s_mem4);
+  const int64_t book_bytes16 = (nbook * (int64_t)sizeof(TT) + 15) & ~15ll;
+  int32_t* s_ip0 = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(s_mem4) + book_bytes16);
   int32_t* s_ip1 = s_ip0 + kTD + 1;
   int32_t* s_src0 = s_ip1 + kTD + 1;
   int32_t* s_src1 = s_src0 + kSrcCap;
   const int64_t live = live_dst(ndst_dev, max_dst);
   const int64_t ntiles = (live + kTD - 1) / kTD;
   if ((int64_t)blockIdx.x >= ntiles) return;
-  const float* book = books;
+  const TT* book = books;
   bool waited = !SMEM;
   if constexpr (SMEM) {
     // codebook -> smem on the TMA engine, overlapping the tile staging
-    const uint32_t bytes = (uint32_t)(nbook * 4) & ~15u;
+    const uint32_t bytes = (uint32_t)(nbook * sizeof(TT)) & ~15u;
     bulk_fill(s_book, books, bytes, &s_mbar);
-    for (int64_t i = bytes / 4 + threadIdx.x; i < nbook; i += blockDim.x) s_book[i] = __ldg(books + i);
+    for (int64_t i = bytes / sizeof(TT) + threadIdx.x; i < nbook; i += blockDim.x)
+      s_book[i] = books[i];
     book = s_book;
   }
   const int groups = (parts + G - 1) / G;
@@ -420,8 +441,18 @@ k_vq_mean8(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
             for (int q = 0; q < G; ++q) {
               if (q < np) {
                 const uint32_t code = (cw[u][q >> 2] >> (8 * (q & 3))) & 0xFFu;
-                const float* ent = book + ((int64_t)(p0 + q) * length + code) * W;
-                if constexpr (W >= 4) {
+                const TT* ent = book + ((int64_t)(p0 + q) * length + code) * W;
+                if constexpr (!std::is_same<TT, float>::value) {
+                  // bf16 entries: W/4 x 8-byte loads, widened to fp32 pairs
+#pragma unroll
+                  for (int j = 0; j < W; j += 4) {
+                    const uint2 h = SMEM ? lds64(ent + j)
+                                         : __ldg(reinterpret_cast<const uint2*>(ent + j));
+                    acc[(q * W + j) / 2] = fadd2(acc[(q * W + j) / 2], bf16x2_to_f32x2(h.x));
+                    acc[(q * W + j) / 2 + 1] =
+                        fadd2(acc[(q * W + j) / 2 + 1], bf16x2_to_f32x2(h.y));
+                  }
+                } else if constexpr (W >= 4) {
 #pragma unroll
                   for (int j = 0; j < W; j += 4) {
                     const float4 f = SMEM ? lds128(ent + j)
@@ -559,18 +590,30 @@ int launch_vq(const fg_codec_desc* c, const int32_t* indptr, const int32_t* src,
     FG_LAUNCH_CHECK();
     return FG_OK;
   }
-  const int64_t smem2 = ((book_bytes + 15) & ~15ll) + stage_bytes;
-  if (smem2 <= 110 * 1024 || smem2 <= 220 * 1024) {
+  // bf16 output may read the bf16 copy of the codebooks (half the smem bytes)
+  const bool lp = std::is_same<OT, __nv_bfloat16>::value && c->table_lp != nullptr;
+  const int64_t tab_bytes = lp ? book_bytes / 2 : book_bytes;
+  const int64_t smem2 = ((tab_bytes + 15) & ~15ll) + stage_bytes;
+  if (smem2 <= 220 * 1024) {
     const int per_sm = smem2 <= 110 * 1024 ? 2 : 1;
-    auto kern = k_vq_mean8<W, OT, true>;
-    FG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem2));
     const int grid = (int)min64(ntiles, (int64_t)sm_count() * per_sm);
-    kern<<<grid, kThreads, smem2, st>>>(c->rows, c->d, c->row_stride, (const float*)c->table,
-                                   c->length, c->num_parts, indptr, src, ndst, max_dst, (OT*)out,
-                                   ld);
+    if (lp) {
+      auto kern = k_vq_mean8<W, OT, true, __nv_bfloat16>;
+      FG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem2));
+      kern<<<grid, kThreads, smem2, st>>>(c->rows, c->d, c->row_stride,
+                                          (const __nv_bfloat16*)c->table_lp, c->length,
+                                          c->num_parts, indptr, src, ndst, max_dst, (OT*)out, ld);
+    } else {
+      auto kern = k_vq_mean8<W, OT, true, float>;
+      FG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem2));
+      kern<<<grid, kThreads, smem2, st>>>(c->rows, c->d, c->row_stride, (const float*)c->table,
+                                          c->length, c->num_parts, indptr, src, ndst, max_dst,
+                                          (OT*)out, ld);
+    }
   } else {
-    auto kern = k_vq_mean8<W, OT, false>;
+    auto kern = k_vq_mean8<W, OT, false, float>;
     const int grid = (int)min64(ntiles, (int64_t)sm_count() * 2);
     kern<<<grid, kThreads, stage_bytes, st>>>(c->rows, c->d, c->row_stride, (const float*)c->table,
                                          c->length, c->num_parts, indptr, src, ndst, max_dst,

@@ -153,7 +153,7 @@ class DeviceSqCodec:
         self.lut = torch.from_numpy(sq_decode_table(params, elem_bits)).to(rows.device)
         self._closed = False
         self._desc = N.CodecDesc(N.CODEC_SQ, params.k, self.n, self.d, self.row_stride,
-                                 N.ptr(rows), N.ptr(self.lut), 0, 0, 0, elem_bits)
+                                 N.ptr(rows), N.ptr(self.lut), 0, 0, 0, elem_bits, None)
 
     # -- construction
     @classmethod
