@@ -442,7 +442,7 @@ k_vq_mean8(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
               if (q < np) {
                 const uint32_t code = (cw[u][q >> 2] >> (8 * (q & 3))) & 0xFFu;
                 const TT* ent = book + ((int64_t)(p0 + q) * length + code) * W;
-                if constexpr (!std::is_same<TT, float>::value) {
+                if constexpr (!std::is_same<TT, float>::value && W >= 4) {
                   // bf16 entries: W/4 x 8-byte loads, widened to fp32 pairs
 #pragma unroll
                   for (int j = 0; j < W; j += 4) {
@@ -591,7 +591,7 @@ int launch_vq(const fg_codec_desc* c, const int32_t* indptr, const int32_t* src,
     return FG_OK;
   }
   // bf16 output may read the bf16 copy of the codebooks (half the smem bytes)
-  const bool lp = std::is_same<OT, __nv_bfloat16>::value && c->table_lp != nullptr;
+  const bool lp = std::is_same<OT, __nv_bfloat16>::value && c->table_lp != nullptr && W >= 4;
   const int64_t tab_bytes = lp ? book_bytes / 2 : book_bytes;
   const int64_t smem2 = ((tab_bytes + 15) & ~15ll) + stage_bytes;
   if (smem2 <= 220 * 1024) {
