@@ -489,6 +489,130 @@ k_vq_mean8(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
   if (!waited) bulk_wait(&s_mbar);  // never leave with a copy in flight
 }
 
+// ------------------------------------------ VQ fast path (8-bit, bf16)
+// Specialised for the training configuration: 8-bit codes, bf16 output, bf16
+// codebooks in smem, W in {4, 8}.  v4 removed the per-lookup branches the
+// ncu instruction mix was dominated by (IMAD/LOP3/ISETP/BSSY ~45 %): the pick
+// count is dispatched once per item to a fully unrolled body, per-part smem
+// base addresses are precomputed, a zero "part" absorbs the lanes of a
+// partial last group, and every lookup is BFE + LEA + LDS + widen + FADD2.
+template <int W, int G, int C>
+__device__ __forceinline__ void vq_fast_body(const uint8_t* __restrict__ rows, int64_t stride,
+                                             const int32_t* sids, uint32_t base0,
+                                             uint32_t pstride, int p0, u64* acc) {
+  constexpr int NB = G;  // code bytes per pick for this thread
+  uint32_t cw[C][(NB + 3) / 4];
+#pragma unroll
+  for (int u = 0; u < C; ++u) load_codes<G>(rows + (int64_t)sids[u] * stride + p0, cw[u]);
+#pragma unroll
+  for (int u = 0; u < C; ++u) {
+#pragma unroll
+    for (int q = 0; q < G; ++q) {
+      const uint32_t code = (cw[u][q >> 2] >> (8 * (q & 3))) & 0xFFu;
+      const uint32_t addr = base0 + q * pstride + code * (uint32_t)(W * 2);
+      if constexpr (W == 4) {
+        uint32_t x, y;
+        asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(x), "=r"(y) : "r"(addr));
+        acc[q * 2] = fadd2(acc[q * 2], bf16x2_to_f32x2(x));
+        acc[q * 2 + 1] = fadd2(acc[q * 2 + 1], bf16x2_to_f32x2(y));
+      } else {  // W == 8
+        uint32_t x, y, z, w;
+        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(x), "=r"(y), "=r"(z), "=r"(w) : "r"(addr));
+        acc[q * 4] = fadd2(acc[q * 4], bf16x2_to_f32x2(x));
+        acc[q * 4 + 1] = fadd2(acc[q * 4 + 1], bf16x2_to_f32x2(y));
+        acc[q * 4 + 2] = fadd2(acc[q * 4 + 2], bf16x2_to_f32x2(z));
+        acc[q * 4 + 3] = fadd2(acc[q * 4 + 3], bf16x2_to_f32x2(w));
+      }
+    }
+  }
+}
+
+template <int W, int G>
+__global__ void __launch_bounds__(kThreads, 2)
+k_vq_mean8_fast(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
+                const __nv_bfloat16* __restrict__ books, int length, int parts,
+                const int32_t* __restrict__ indptr, const int32_t* __restrict__ src,
+                const int64_t* __restrict__ ndst_dev, int64_t max_dst,
+                __nv_bfloat16* __restrict__ out, int64_t ld) {
+  // G parts per thread: G * W = 16 fp32 accumulators keeps the whole body
+  // (5 unrolled picks) inside 64 registers
+  __shared__ __align__(8) uint64_t s_mbar;
+  extern __shared__ float4 s_mem4[];
+  const int64_t nbook = (int64_t)parts * length * W;           // bf16 elements
+  const int64_t zero_part = (int64_t)(G - 1) * length * W;     // zero parts after the last
+  __nv_bfloat16* s_book = reinterpret_cast<__nv_bfloat16*>(s_mem4);
+  const int64_t book_bytes16 = ((nbook + zero_part) * 2 + 15) & ~15ll;
+  int32_t* s_ip0 = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(s_mem4) + book_bytes16);
+  int32_t* s_ip1 = s_ip0 + kTD + 1;
+  int32_t* s_src0 = s_ip1 + kTD + 1;
+  int32_t* s_src1 = s_src0 + kSrcCap;
+  const int64_t live = live_dst(ndst_dev, max_dst);
+  const int64_t ntiles = (live + kTD - 1) / kTD;
+  if ((int64_t)blockIdx.x >= ntiles) return;
+  const uint32_t bytes = (uint32_t)(nbook * 2) & ~15u;
+  bulk_fill(s_book, books, bytes, &s_mbar);
+  for (int64_t i = bytes / 2 + threadIdx.x; i < nbook; i += blockDim.x) s_book[i] = books[i];
+  for (int64_t i = threadIdx.x; i < zero_part; i += blockDim.x)
+    s_book[nbook + i] = __float2bfloat16_rn(0.f);
+  const uint32_t s_base = smem_addr(s_book);
+  const int groups = (parts + G - 1) / G;
+  const bool vec_ok = (ld % 16) == 0;
+  bool waited = false;
+  tile_pipeline(indptr, src, max_dst, ntiles, s_ip0, s_ip1, s_src0, s_src1,
+                [&](int64_t tile, const int32_t* s_ip, const int32_t* s_src) {
+    if (!waited) {
+      bulk_wait(&s_mbar);
+      waited = true;
+    }
+    const int64_t v0 = tile * kTD;
+    const int32_t e0 = s_ip[0];
+    const bool staged = s_ip[kTD] - e0 <= kSrcCap;
+    const int items = kTD * groups;
+    for (int it = threadIdx.x; it < items; it += blockDim.x) {
+      const int vl = it / groups;
+      const int g = it - vl * groups;
+      const int64_t v = v0 + vl;
+      if (v >= live) break;
+      const int p0 = g * G;
+      const int np = min(G, parts - p0);
+      // parts p0 .. p0+G-1; past the last part the table is zero padded
+      const uint32_t pstride = (uint32_t)(length * W * 2);
+      const uint32_t base0 = s_base + (uint32_t)p0 * pstride;
+      u64 acc[G * W / 2];
+#pragma unroll
+      for (int j = 0; j < G * W / 2; ++j) acc[j] = 0ull;
+      const int a = s_ip[vl] - e0;
+      const int cnt = s_ip[vl + 1] - e0 - a;
+      for (int base = 0; base < cnt; base += 5) {  // batches of <= 5 picks
+        const int cb = min(cnt - base, 5);
+        int32_t sids[5];
+#pragma unroll
+        for (int u = 0; u < 5; ++u)
+          if (u < cb) sids[u] = staged ? s_src[a + base + u] : __ldg(src + e0 + a + base + u);
+        switch (cb) {
+          case 1: vq_fast_body<W, G, 1>(rows, stride, sids, base0, pstride, p0, acc); break;
+          case 2: vq_fast_body<W, G, 2>(rows, stride, sids, base0, pstride, p0, acc); break;
+          case 3: vq_fast_body<W, G, 3>(rows, stride, sids, base0, pstride, p0, acc); break;
+          case 4: vq_fast_body<W, G, 4>(rows, stride, sids, base0, pstride, p0, acc); break;
+          default: vq_fast_body<W, G, 5>(rows, stride, sids, base0, pstride, p0, acc); break;
+        }
+      }
+      const float inv = cnt ? 1.0f / (float)cnt : 0.0f;
+      const int64_t col0 = (int64_t)p0 * W;
+      __nv_bfloat16* o = out + v * ld + col0;
+      if (np == G && col0 + G * W <= d) {
+        store_scaled<G * W>(o, acc, inv, vec_ok);
+      } else {
+#pragma unroll
+        for (int j = 0; j < G * W; ++j)
+          if (col0 + j < d) o[j] = __float2bfloat16_rn((j & 1 ? hi2(acc[j / 2]) : lo2(acc[j / 2])) * inv);
+      }
+    }
+  });
+  if (!waited) bulk_wait(&s_mbar);
+}
+
 // ------------------------------------------------- VQ (any code width)
 template <int W, typename OT>
 __global__ void __launch_bounds__(kThreads, 2)
@@ -592,6 +716,24 @@ int launch_vq(const fg_codec_desc* c, const int32_t* indptr, const int32_t* src,
   }
   // bf16 output may read the bf16 copy of the codebooks (half the smem bytes)
   const bool lp = std::is_same<OT, __nv_bfloat16>::value && c->table_lp != nullptr && W >= 4;
+  if constexpr (std::is_same<OT, __nv_bfloat16>::value && (W == 4 || W == 8)) {
+    constexpr int GF = 16 / W;
+    const int64_t fast_smem =
+        (((book_bytes / 2) + (int64_t)(GF - 1) * c->length * W * 2 + 15) & ~15ll) +
+        stage_bytes;
+    if (lp && fast_smem <= 110 * 1024) {
+      auto kern = k_vq_mean8_fast<W, GF>;
+      FG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)fast_smem));
+      const int grid = (int)min64(ntiles, (int64_t)sm_count() * 2);
+      kern<<<grid, kThreads, fast_smem, st>>>(c->rows, c->d, c->row_stride,
+                                              (const __nv_bfloat16*)c->table_lp, c->length,
+                                              c->num_parts, indptr, src, ndst, max_dst,
+                                              (__nv_bfloat16*)out, ld);
+      FG_LAUNCH_CHECK();
+      return FG_OK;
+    }
+  }
   const int64_t tab_bytes = lp ? book_bytes / 2 : book_bytes;
   const int64_t smem2 = ((tab_bytes + 15) & ~15ll) + stage_bytes;
   if (smem2 <= 220 * 1024) {
