@@ -98,58 +98,69 @@ __device__ __forceinline__ void store_scaled(__nv_bfloat16* p, const u64* acc, f
 // indptr slice of tile t+2G are loaded into registers, then stored after the
 // compute phase: the staging round trips overlap the code-row loads.
 constexpr int kThreads = 512;
-constexpr int kSrcPerThread = kSrcCap / kThreads;
 
+template <int NT>
 struct Stage {
-  int32_t ip;                   // one indptr entry (threads 0..kTD)
-  int32_t src[kSrcPerThread];   // src ids e0 + threadIdx.x + k*kThreads
+  static constexpr int kPer = kSrcCap / NT;
+  int32_t ip;                 // one indptr entry (threads 0..kTD)
+  int32_t src[kPer];          // src ids e0 + threadIdx.x + k*NT
 };
 
+template <int NT>
 __device__ __forceinline__ void stage_load_ip(const int32_t* __restrict__ indptr, int64_t tile,
-                                              int64_t max_dst, Stage& st) {
-  if (threadIdx.x <= kTD) st.ip = __ldg(indptr + min64(tile * kTD + threadIdx.x, max_dst));
+                                              int64_t max_dst, Stage<NT>& st) {
+  for (int t = threadIdx.x; t <= kTD; t += NT)  // NT may be < kTD + 1
+    if (t == (int)threadIdx.x) st.ip = __ldg(indptr + min64(tile * kTD + t, max_dst));
 }
-__device__ __forceinline__ void stage_store_ip(int32_t* s_ip, const Stage& st) {
-  if (threadIdx.x <= kTD) s_ip[threadIdx.x] = st.ip;
+template <int NT>
+__device__ __forceinline__ void stage_store_ip(int32_t* s_ip, const Stage<NT>& st,
+                                               const int32_t* __restrict__ indptr, int64_t tile,
+                                               int64_t max_dst) {
+  if ((int)threadIdx.x <= kTD) s_ip[threadIdx.x] = st.ip;
+  // entries past the thread count (NT <= kTD) are loaded directly
+  for (int t = threadIdx.x + NT; t <= kTD; t += NT)
+    s_ip[t] = __ldg(indptr + min64(tile * kTD + t, max_dst));
 }
+template <int NT>
 __device__ __forceinline__ void stage_load_src(const int32_t* __restrict__ src, const int32_t* s_ip,
-                                               Stage& st) {
+                                               Stage<NT>& st) {
   const int32_t e0 = s_ip[0], cnt = s_ip[kTD] - e0;
   if (cnt > kSrcCap) return;  // compute falls back to global src loads
 #pragma unroll
-  for (int k = 0; k < kSrcPerThread; ++k) {
-    const int t = threadIdx.x + k * kThreads;
+  for (int k = 0; k < Stage<NT>::kPer; ++k) {
+    const int t = threadIdx.x + k * NT;
     if (t < cnt) st.src[k] = __ldg(src + e0 + t);
   }
 }
+template <int NT>
 __device__ __forceinline__ void stage_store_src(int32_t* s_src, const int32_t* s_ip,
-                                                const Stage& st) {
+                                                const Stage<NT>& st) {
   const int32_t cnt = s_ip[kTD] - s_ip[0];
   if (cnt > kSrcCap) return;
 #pragma unroll
-  for (int k = 0; k < kSrcPerThread; ++k) {
-    const int t = threadIdx.x + k * kThreads;
+  for (int k = 0; k < Stage<NT>::kPer; ++k) {
+    const int t = threadIdx.x + k * NT;
     if (t < cnt) s_src[t] = st.src[k];
   }
 }
 
 // Drives the pipeline; `compute(tile, s_ip, s_src)` processes one tile.
-template <typename F>
+template <int NT = kThreads, typename F>
 __device__ __forceinline__ void tile_pipeline(const int32_t* __restrict__ indptr,
                                               const int32_t* __restrict__ src, int64_t max_dst,
                                               int64_t ntiles, int32_t* s_ip0, int32_t* s_ip1,
                                               int32_t* s_src0, int32_t* s_src1, F&& compute) {
   const int64_t step = gridDim.x;
   int64_t tile = blockIdx.x;
-  Stage st, st2;
+  Stage<NT> st, st2;
   // prologue: buffer 0 <- (ip, src) of tile; buffer 1 <- ip of tile+step
-  stage_load_ip(indptr, tile, max_dst, st);
-  stage_store_ip(s_ip0, st);
+  stage_load_ip<NT>(indptr, tile, max_dst, st);
+  stage_store_ip<NT>(s_ip0, st, indptr, tile, max_dst);
   __syncthreads();
-  stage_load_src(src, s_ip0, st);
-  if (tile + step < ntiles) stage_load_ip(indptr, tile + step, max_dst, st2);
-  stage_store_src(s_src0, s_ip0, st);
-  if (tile + step < ntiles) stage_store_ip(s_ip1, st2);
+  stage_load_src<NT>(src, s_ip0, st);
+  if (tile + step < ntiles) stage_load_ip<NT>(indptr, tile + step, max_dst, st2);
+  stage_store_src<NT>(s_src0, s_ip0, st);
+  if (tile + step < ntiles) stage_store_ip<NT>(s_ip1, st2, indptr, tile + step, max_dst);
   __syncthreads();
   bool odd = false;
   for (; tile < ntiles; tile += step) {
@@ -158,12 +169,12 @@ __device__ __forceinline__ void tile_pipeline(const int32_t* __restrict__ indptr
     int32_t* src_c = odd ? s_src1 : s_src0;
     int32_t* src_n = odd ? s_src0 : s_src1;
     const bool has_n = tile + step < ntiles, has_nn = tile + 2 * step < ntiles;
-    if (has_n) stage_load_src(src, ip_n, st);
-    if (has_nn) stage_load_ip(indptr, tile + 2 * step, max_dst, st2);
+    if (has_n) stage_load_src<NT>(src, ip_n, st);
+    if (has_nn) stage_load_ip<NT>(indptr, tile + 2 * step, max_dst, st2);
     compute(tile, ip_c, src_c);
     __syncthreads();
-    if (has_n) stage_store_src(src_n, ip_n, st);
-    if (has_nn) stage_store_ip(ip_c, st2);
+    if (has_n) stage_store_src<NT>(src_n, ip_n, st);
+    if (has_nn) stage_store_ip<NT>(ip_c, st2, indptr, tile + 2 * step, max_dst);
     __syncthreads();
     odd = !odd;
   }
@@ -180,7 +191,6 @@ __device__ __forceinline__ uint2 lds64(const void* p) {
                : "r"((uint32_t)__cvta_generic_to_shared(p)));
   return r;
 }
-
 // one 16-byte shared-memory load (keeps the compiler from splitting it)
 __device__ __forceinline__ float4 lds128(const float* p) {
   float4 r;
@@ -528,15 +538,16 @@ __device__ __forceinline__ void vq_fast_body(const uint8_t* __restrict__ rows, i
   }
 }
 
+constexpr int kFastThreads = 256;  // 3 CTAs/SM -> 85 registers: 32 fp32 accumulators fit
+
 template <int W, int G>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kFastThreads, 3)
 k_vq_mean8_fast(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
                 const __nv_bfloat16* __restrict__ books, int length, int parts,
                 const int32_t* __restrict__ indptr, const int32_t* __restrict__ src,
                 const int64_t* __restrict__ ndst_dev, int64_t max_dst,
                 __nv_bfloat16* __restrict__ out, int64_t ld) {
-  // G parts per thread: G * W = 16 fp32 accumulators keeps the whole body
-  // (5 unrolled picks) inside 64 registers
+  // G parts per thread: G * W = 32 fp32 accumulators
   __shared__ __align__(8) uint64_t s_mbar;
   extern __shared__ float4 s_mem4[];
   const int64_t nbook = (int64_t)parts * length * W;           // bf16 elements
@@ -559,7 +570,7 @@ k_vq_mean8_fast(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
   const int groups = (parts + G - 1) / G;
   const bool vec_ok = (ld % 16) == 0;
   bool waited = false;
-  tile_pipeline(indptr, src, max_dst, ntiles, s_ip0, s_ip1, s_src0, s_src1,
+  tile_pipeline<kFastThreads>(indptr, src, max_dst, ntiles, s_ip0, s_ip1, s_src0, s_src1,
                 [&](int64_t tile, const int32_t* s_ip, const int32_t* s_src) {
     if (!waited) {
       bulk_wait(&s_mbar);
@@ -587,9 +598,10 @@ k_vq_mean8_fast(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
       for (int base = 0; base < cnt; base += 5) {  // batches of <= 5 picks
         const int cb = min(cnt - base, 5);
         int32_t sids[5];
+        const int32_t* sp = staged ? s_src + a + base : src + e0 + a + base;  // tile-uniform
 #pragma unroll
         for (int u = 0; u < 5; ++u)
-          if (u < cb) sids[u] = staged ? s_src[a + base + u] : __ldg(src + e0 + a + base + u);
+          if (u < cb) sids[u] = sp[u];
         switch (cb) {
           case 1: vq_fast_body<W, G, 1>(rows, stride, sids, base0, pstride, p0, acc); break;
           case 2: vq_fast_body<W, G, 2>(rows, stride, sids, base0, pstride, p0, acc); break;
@@ -717,16 +729,16 @@ int launch_vq(const fg_codec_desc* c, const int32_t* indptr, const int32_t* src,
   // bf16 output may read the bf16 copy of the codebooks (half the smem bytes)
   const bool lp = std::is_same<OT, __nv_bfloat16>::value && c->table_lp != nullptr && W >= 4;
   if constexpr (std::is_same<OT, __nv_bfloat16>::value && (W == 4 || W == 8)) {
-    constexpr int GF = 16 / W;
+    constexpr int GF = 32 / W;
     const int64_t fast_smem =
         (((book_bytes / 2) + (int64_t)(GF - 1) * c->length * W * 2 + 15) & ~15ll) +
         stage_bytes;
-    if (lp && fast_smem <= 110 * 1024) {
+    if (lp && fast_smem <= 76 * 1024) {  // three CTAs per SM (233 KB smem per SM)
       auto kern = k_vq_mean8_fast<W, GF>;
       FG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)fast_smem));
-      const int grid = (int)min64(ntiles, (int64_t)sm_count() * 2);
-      kern<<<grid, kThreads, fast_smem, st>>>(c->rows, c->d, c->row_stride,
+      const int grid = (int)min64(ntiles, (int64_t)sm_count() * 3);
+      kern<<<grid, kFastThreads, fast_smem, st>>>(c->rows, c->d, c->row_stride,
                                               (const __nv_bfloat16*)c->table_lp, c->length,
                                               c->num_parts, indptr, src, ndst, max_dst,
                                               (__nv_bfloat16*)out, ld);
