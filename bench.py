@@ -6,7 +6,7 @@
 Default workload (N=1): BASELINE configs[1] — synthetic ogbn-products-shape
 graph (2,449,029 nodes, avg degree ~50, 100-dim class-conditional features),
 3-layer GraphSAGE, fanouts [15,10,5], batch 1024, VQ codebooks of 256 entries
-(width 4, cosine, CR 32).  A step = one full training step on one batch of
+(width 4, cosine, CR 16).  A step = one full training step on one batch of
 seeds: sample (device PCG64) -> fused gather-dequant-mean -> bf16 SAGE
 fwd/bwd -> all-reduce (N>1) -> Adam, replayed from one CUDA graph.
 

@@ -116,6 +116,14 @@ int fg_gather_nonzero_sample(const float* x, int64_t count, int64_t nnz,
                              int64_t cap, float* out_abs, void* workspace,
                              int64_t workspace_bytes, void* cuda_stream);
 int64_t fg_nonzero_sample_workspace_bytes(int64_t count);
+/* Streaming form: x is one row-major chunk of a larger matrix whose first
+ * nonzero has global rank rank_base; nnz is the whole matrix's nonzero count
+ * and out_abs the whole sample (min(nnz, cap) floats): the chunk writes the
+ * picks whose global rank it holds. */
+int fg_gather_nonzero_sample_chunk(const float* x, int64_t count, int64_t rank_base,
+                                   int64_t nnz, int64_t cap, float* out_abs,
+                                   void* workspace, int64_t workspace_bytes,
+                                   void* cuda_stream);
 /* k-th smallest (0-based) of non-negative floats, for each requested rank;
  * two-pass 16-bit radix select.  Exact (returns the element bit pattern).
  * Synchronises `cuda_stream` (offline fit path; not graph-capturable). */
@@ -291,6 +299,27 @@ int fg_bitmap_clear(const int32_t* ids, const int64_t* count_dev, int64_t max_co
 int fg_synth_features(int kind, uint64_t seed, int64_t row0, int64_t rows,
                       int64_t d, const int32_t* labels, int num_classes,
                       float* out, void* cuda_stream);
+/* Same values for an arbitrary row-id list (oracle subsets, VQ fit samples). */
+int fg_synth_feature_rows(int kind, uint64_t seed, const int64_t* row_ids,
+                          int64_t rows, int64_t d, const int32_t* labels,
+                          int num_classes, float* out, void* cuda_stream);
+
+/* Scalable synthetic graph (degree-corrected planted partition, power-law
+ * ranks, Feistel-permuted ids).  Edge e is a pure function of (seed, e).
+ * fg_graph_degrees adds each non-self edge's endpoints into degrees[n]
+ * (caller-zeroed; duplicates included); fg_graph_emit appends keys
+ * (src - lo) * n + dst of every directed entry whose src is in [lo, hi)
+ * (cursor = device counter, caller-zeroed; at most cap keys written);
+ * fg_graph_labels writes each node's planted class. */
+int fg_graph_degrees(uint64_t seed, int64_t n, int64_t classes, double alpha,
+                     double homophily, int64_t num_edges, uint32_t* degrees,
+                     void* cuda_stream);
+int fg_graph_emit(uint64_t seed, int64_t n, int64_t classes, double alpha,
+                  double homophily, int64_t num_edges, int64_t lo, int64_t hi,
+                  unsigned long long* cursor, int64_t cap, int64_t* keys,
+                  void* cuda_stream);
+int fg_graph_labels(uint64_t seed, int64_t n, int64_t classes, int32_t* labels,
+                    void* cuda_stream);
 
 #ifdef __cplusplus
 }

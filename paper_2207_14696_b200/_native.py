@@ -45,6 +45,7 @@ _SIGS = {
     "fg_count_nonzero": (ci, [vp, i64, vp, vp]),
     "fg_gather_nonzero_sample": (ci, [vp, i64, i64, i64, vp, vp, i64, vp]),
     "fg_nonzero_sample_workspace_bytes": (i64, [i64]),
+    "fg_gather_nonzero_sample_chunk": (ci, [vp, i64, i64, i64, i64, vp, vp, i64, vp]),
     "fg_select_ranks": (ci, [vp, i64, C.POINTER(i64), ci, C.POINTER(C.c_float), vp, i64, vp]),
     "fg_select_workspace_bytes": (i64, []),
     "fg_vq_assign": (ci, [vp, ci, i64, i64, ci, ci, ci, vp, vp, ci, ci, vp, i64, vp, vp]),
@@ -75,6 +76,11 @@ _SIGS = {
     "fg_bitmap_rank": (ci, [vp, vp, i64, vp, vp, vp, vp]),
     "fg_bitmap_clear": (ci, [vp, vp, i64, vp, vp]),
     "fg_synth_features": (ci, [ci, u64, i64, i64, i64, vp, ci, vp, vp]),
+    "fg_synth_feature_rows": (ci, [ci, u64, vp, i64, i64, vp, ci, vp, vp]),
+    "fg_graph_degrees": (ci, [u64, i64, i64, C.c_double, C.c_double, i64, vp, vp]),
+    "fg_graph_emit": (ci, [u64, i64, i64, C.c_double, C.c_double, i64, i64, i64, vp, i64, vp,
+                           vp]),
+    "fg_graph_labels": (ci, [u64, i64, i64, vp, vp]),
 }
 
 _lib = None

@@ -28,14 +28,14 @@ __device__ __forceinline__ uint64_t elem_key(uint64_t seed, int64_t i, int64_t j
   return splitmix64(seed ^ splitmix64((uint64_t)i * 0x100000001B3ull + (uint64_t)j));
 }
 
-__global__ void k_synth(int kind, uint64_t seed, int64_t row0, int64_t rows, int64_t d,
-                        const int32_t* __restrict__ labels, int num_classes,
-                        float* __restrict__ out) {
+__global__ void k_synth(int kind, uint64_t seed, int64_t row0, const int64_t* __restrict__ row_ids,
+                        int64_t rows, int64_t d, const int32_t* __restrict__ labels,
+                        int num_classes, float* __restrict__ out) {
   const int64_t total = rows * d;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = t / d, j = t - r * d;
-    const int64_t i = row0 + r;
+    const int64_t i = row_ids ? row_ids[r] : row0 + r;
     const float z = gauss(elem_key(seed, i, j));
     float v;
     switch (kind) {
@@ -73,8 +73,177 @@ extern "C" int fg_synth_features(int kind, uint64_t seed, int64_t row0, int64_t 
   FG_CHECK_ARG(kind != 3 || labels != nullptr, "class-conditional kind needs labels");
   FG_CHECK_ARG(rows >= 0 && d >= 1, "fg_synth_features: bad shape");
   if (rows == 0) return FG_OK;
-  k_synth<<<grid_for(rows * d, 256), 256, 0, as_stream(s)>>>(kind, seed, row0, rows, d, labels,
-                                                             num_classes, out);
+  k_synth<<<grid_for(rows * d, 256), 256, 0, as_stream(s)>>>(kind, seed, row0, nullptr, rows, d,
+                                                             labels, num_classes, out);
+  FG_LAUNCH_CHECK();
+  return FG_OK;
+}
+
+extern "C" int fg_synth_feature_rows(int kind, uint64_t seed, const int64_t* row_ids,
+                                     int64_t rows, int64_t d, const int32_t* labels,
+                                     int num_classes, float* out, void* s) {
+  FG_CHECK_ARG(kind >= 0 && kind <= 3, "fg_synth_feature_rows: kind must be 0..3");
+  FG_CHECK_ARG(kind != 3 || labels != nullptr, "class-conditional kind needs labels");
+  FG_CHECK_ARG(rows >= 0 && d >= 1 && (rows == 0 || row_ids), "fg_synth_feature_rows: bad shape");
+  if (rows == 0) return FG_OK;
+  k_synth<<<grid_for(rows * d, 256), 256, 0, as_stream(s)>>>(kind, seed, 0, row_ids, rows, d,
+                                                             labels, num_classes, out);
+  FG_LAUNCH_CHECK();
+  return FG_OK;
+}
+
+// ---------------------------------------------------- synthetic graphs
+// Degree-corrected planted partition at any scale: node
+// positions are grouped by class (C equal blocks); position -> node id is a
+// fixed Feistel bijection (hubs spread over the id space).  Edge e is a pure
+// function of (seed, e): endpoint ranks follow a continuous power law
+// w(rank) ~ (rank+1)^-alpha inside a class (closed-form inverse CDF); the
+// second endpoint stays in the first's class with probability `homophily`.
+// The CSR is built in node-range chunks: every chunk regenerates all edges
+// and keeps the directed entries whose source falls in the chunk, so memory
+// is bounded by the chunk, not the graph.
+namespace fg {
+
+struct GraphGen {
+  uint64_t seed;
+  int64_t n;
+  int64_t classes;
+  double alpha;
+  double homophily;
+  int bits;  // Feistel domain bits (even)
+};
+
+__device__ __forceinline__ double u01(uint64_t h) {
+  return ((h >> 11) + 0.5) * (1.0 / 9007199254740992.0);  // (0, 1)
+}
+
+__device__ __forceinline__ int64_t feistel(int64_t x, const GraphGen& g) {
+  const int half = g.bits / 2;
+  const uint64_t mask = (1ull << half) - 1;
+  uint64_t y = (uint64_t)x;
+  for (int walk = 0; walk < 512; ++walk) {
+    uint64_t lo = y & mask, hi = y >> half;
+    for (int r = 0; r < 4; ++r) {
+      const uint64_t f = splitmix64(lo ^ (g.seed * 0x9E3779B97F4A7C15ull + r)) & mask;
+      const uint64_t t = hi ^ f;
+      hi = lo;
+      lo = t;
+    }
+    y = (hi << half) | lo;
+    if ((int64_t)y < g.n) return (int64_t)y;
+  }
+  return x;  // unreachable in practice (domain <= 4n)
+}
+
+__device__ __forceinline__ int64_t class_size(const GraphGen& g, int64_t c) {
+  return g.n / g.classes + (c < g.n % g.classes ? 1 : 0);
+}
+__device__ __forceinline__ int64_t class_start(const GraphGen& g, int64_t c) {
+  const int64_t q = g.n / g.classes, r = g.n % g.classes;
+  return c * q + (c < r ? c : r);
+}
+
+__device__ __forceinline__ int64_t powerlaw_rank(double u, int64_t size, double alpha) {
+  // continuous inverse CDF of x^-alpha on [1, size+1)
+  const double a1 = 1.0 - alpha;
+  const double hi = pow((double)size + 1.0, a1);
+  const double x = pow(1.0 + u * (hi - 1.0), 1.0 / a1);
+  int64_t r = (int64_t)x - 1;
+  return r < 0 ? 0 : (r >= size ? size - 1 : r);
+}
+
+// endpoints (node ids) of undirected edge e
+__device__ __forceinline__ void gen_edge(const GraphGen& g, int64_t e, int64_t& a, int64_t& b) {
+  const uint64_t h0 = splitmix64(g.seed ^ splitmix64((uint64_t)e * 4 + 1));
+  const uint64_t h1 = splitmix64(h0 + 0x51ED27ull);
+  const uint64_t h2 = splitmix64(h1 + 0xA11CEull);
+  const uint64_t h3 = splitmix64(h2 + 0xB0Bull);
+  const int64_t cu = (int64_t)(u01(h0) * g.classes);
+  const int64_t su = class_size(g, cu);
+  const int64_t pu = class_start(g, cu) + powerlaw_rank(u01(h1), su, g.alpha);
+  const int64_t cv = u01(h2) < g.homophily ? cu : (int64_t)(u01(h3 ^ 0x5A5Aull) * g.classes);
+  const int64_t sv = class_size(g, cv);
+  const int64_t pv = class_start(g, cv) + powerlaw_rank(u01(h3), sv, g.alpha);
+  a = feistel(pu, g);
+  b = feistel(pv, g);
+}
+
+__global__ void k_edge_degree(GraphGen g, int64_t E, unsigned int* __restrict__ deg) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t a, b;
+    gen_edge(g, e, a, b);
+    if (a == b) continue;
+    atomicAdd(deg + a, 1u);
+    atomicAdd(deg + b, 1u);
+  }
+}
+
+__global__ void k_edge_emit(GraphGen g, int64_t E, int64_t lo, int64_t hi,
+                            unsigned long long* __restrict__ cursor, int64_t cap,
+                            int64_t* __restrict__ keys) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t a, b;
+    gen_edge(g, e, a, b);
+    if (a == b) continue;
+    if (a >= lo && a < hi) {
+      const unsigned long long s = atomicAdd(cursor, 1ull);
+      if ((int64_t)s < cap) keys[s] = (a - lo) * g.n + b;
+    }
+    if (b >= lo && b < hi) {
+      const unsigned long long s = atomicAdd(cursor, 1ull);
+      if ((int64_t)s < cap) keys[s] = (b - lo) * g.n + a;
+    }
+  }
+}
+
+__global__ void k_node_labels(GraphGen g, int32_t* __restrict__ labels) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < g.n;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    // class of position p
+    const int64_t q = g.n / g.classes, r = g.n % g.classes;
+    const int64_t big = r * (q + 1);
+    const int64_t c = p < big ? p / (q + 1) : r + (p - big) / q;
+    labels[feistel(p, g)] = (int32_t)c;
+  }
+}
+
+inline GraphGen make_gen(uint64_t seed, int64_t n, int64_t classes, double alpha,
+                         double homophily) {
+  GraphGen g{seed, n, classes, alpha, homophily, 2};
+  while ((1ll << g.bits) < n) g.bits += 2;
+  return g;
+}
+
+}  // namespace fg
+
+extern "C" int fg_graph_degrees(uint64_t seed, int64_t n, int64_t classes, double alpha,
+                                double homophily, int64_t num_edges, uint32_t* degrees,
+                                void* s) {
+  FG_CHECK_ARG(n >= 2 && classes >= 1 && alpha > 0 && alpha != 1.0, "fg_graph_degrees: bad args");
+  const GraphGen g = make_gen(seed, n, classes, alpha, homophily);
+  k_edge_degree<<<grid_for(num_edges, 256, 16), 256, 0, as_stream(s)>>>(g, num_edges, degrees);
+  FG_LAUNCH_CHECK();
+  return FG_OK;
+}
+
+extern "C" int fg_graph_emit(uint64_t seed, int64_t n, int64_t classes, double alpha,
+                             double homophily, int64_t num_edges, int64_t lo, int64_t hi,
+                             unsigned long long* cursor, int64_t cap, int64_t* keys, void* s) {
+  FG_CHECK_ARG(lo >= 0 && hi <= n && lo < hi, "fg_graph_emit: bad node range");
+  FG_CHECK_ARG((double)(hi - lo) * (double)n < 9.2e18, "fg_graph_emit: key overflow");
+  const GraphGen g = make_gen(seed, n, classes, alpha, homophily);
+  k_edge_emit<<<grid_for(num_edges, 256, 16), 256, 0, as_stream(s)>>>(g, num_edges, lo, hi,
+                                                                      cursor, cap, keys);
+  FG_LAUNCH_CHECK();
+  return FG_OK;
+}
+
+extern "C" int fg_graph_labels(uint64_t seed, int64_t n, int64_t classes, int32_t* labels,
+                               void* s) {
+  const GraphGen g = make_gen(seed, n, classes, 0.5, 0.0);
+  k_node_labels<<<grid_for(n, 256), 256, 0, as_stream(s)>>>(g, labels);
   FG_LAUNCH_CHECK();
   return FG_OK;
 }

@@ -41,11 +41,11 @@ k_nz_count(const float* __restrict__ x, int64_t count, int64_t* __restrict__ bcn
 }
 
 __global__ void __launch_bounds__(1024)
-k_nz_scan(int64_t nb, int64_t* __restrict__ b) {
+k_nz_scan(int64_t nb, int64_t* __restrict__ b, int64_t base_rank) {
   using BS = cub::BlockScan<int64_t, 1024>;
   __shared__ typename BS::TempStorage tmp;
   __shared__ int64_t carry;
-  if (threadIdx.x == 0) carry = 0;
+  if (threadIdx.x == 0) carry = base_rank;
   __syncthreads();
   for (int64_t base = 0; base < nb; base += 1024) {
     const int64_t i = base + threadIdx.x;
@@ -126,6 +126,10 @@ using namespace fg;
 
 extern "C" {
 
+int fg_gather_nonzero_sample_chunk(const float* x, int64_t count, int64_t rank_base,
+                                   int64_t nnz, int64_t cap, float* out_abs, void* ws,
+                                   int64_t ws_bytes, void* s);
+
 int fg_count_nonzero(const float* x, int64_t count, unsigned long long* out_count, void* s) {
   FG_CHECK_ARG(out_count != nullptr, "fg_count_nonzero: null out");
   cudaStream_t st = as_stream(s);
@@ -143,7 +147,13 @@ int64_t fg_nonzero_sample_workspace_bytes(int64_t count) {
 
 int fg_gather_nonzero_sample(const float* x, int64_t count, int64_t nnz, int64_t cap,
                              float* out_abs, void* ws, int64_t ws_bytes, void* s) {
-  FG_CHECK_ARG(cap >= 2 && nnz >= 0, "fg_gather_nonzero_sample: bad cap/nnz");
+  return fg_gather_nonzero_sample_chunk(x, count, 0, nnz, cap, out_abs, ws, ws_bytes, s);
+}
+
+int fg_gather_nonzero_sample_chunk(const float* x, int64_t count, int64_t rank_base,
+                                   int64_t nnz, int64_t cap, float* out_abs, void* ws,
+                                   int64_t ws_bytes, void* s) {
+  FG_CHECK_ARG(cap >= 2 && nnz >= 0 && rank_base >= 0, "fg_gather_nonzero_sample: bad cap/nnz");
   FG_CHECK_ARG(ws_bytes >= fg_nonzero_sample_workspace_bytes(count), "workspace too small");
   if (count == 0 || nnz == 0) return FG_OK;
   cudaStream_t st = as_stream(s);
@@ -151,7 +161,7 @@ int fg_gather_nonzero_sample(const float* x, int64_t count, int64_t nnz, int64_t
   int64_t* b = (int64_t*)ws;
   k_nz_count<<<(unsigned)nb, kNzThreads, 0, st>>>(x, count, b, nullptr);
   FG_LAUNCH_CHECK();
-  k_nz_scan<<<1, 1024, 0, st>>>(nb, b);
+  k_nz_scan<<<1, 1024, 0, st>>>(nb, b, rank_base);
   FG_LAUNCH_CHECK();
   // numpy: step = delta / div with delta = (nnz-1) - 0, div = cap - 1
   const double step = (double)(nnz - 1) / (double)(cap - 1);

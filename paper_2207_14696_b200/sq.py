@@ -284,6 +284,34 @@ def fit_sq(f: FeatureMatrix, k: int,
     return fit_sq_device(x, k, clip_tail_fraction)
 
 
+def _params_from_sample(sample_abs, m: int, k: int, clip: float,
+                        sorted_host=None) -> SqParams:
+    """e_min/e_max from the fit sample (|x| of the strided nonzeros): exact
+    radix-select of the four order statistics np.quantile interpolates, then
+    numpy's log2 + quantile lerp on those values (sq.py:107-108)."""
+    import ctypes
+    import torch
+    qs = [clip, 1.0 - clip]
+    ranks = sorted({r for q in qs for r in _order_stat_ranks(m, q)})
+    if sorted_host is None:
+        sel_ws = torch.empty(N.lib().fg_select_workspace_bytes(), dtype=torch.uint8,
+                             device=sample_abs.device)
+        rk = (ctypes.c_int64 * len(ranks))(*ranks)
+        outv = (ctypes.c_float * len(ranks))()
+        N.call("fg_select_ranks", N.ptr(sample_abs), m, rk, len(ranks), outv, N.ptr(sel_ws),
+               sel_ws.numel(), N.stream_handle())
+        stats = {r: float(np.float32(outv[i])) for i, r in enumerate(ranks)}
+    else:
+        stats = {r: float(sorted_host[r]) for r in ranks}
+    logs = {r: float(np.log2(np.abs(np.array([v], dtype=np.float64)))[0])
+            for r, v in stats.items()}
+    e_min, e_max = (_quantile_lerp(logs[_order_stat_ranks(m, q)[0]],
+                                   logs[_order_stat_ranks(m, q)[1]], m, q) for q in qs)
+    if k >= 2 and not e_min < e_max:
+        raise DataError("constant log-magnitude data: exponent range is empty")
+    return SqParams(k, float(e_min), float(e_max), clip)
+
+
 def fit_sq_device(x, k: int, clip_tail_fraction: float = DEFAULT_CLIP_TAIL_FRACTION) -> SqParams:
     """fit_sq over a flat device tensor in row-major order."""
     import torch
@@ -299,38 +327,50 @@ def fit_sq_device(x, k: int, clip_tail_fraction: float = DEFAULT_CLIP_TAIL_FRACT
             return SqParams(1, 0.0, 0.0, clip_tail_fraction)
         raise DataError("cannot fit an exponent range on an all-zero matrix")
     m = min(nnz, FIT_SAMPLE_CAP)
-    qs = [clip_tail_fraction, 1.0 - clip_tail_fraction]
-    ranks = sorted({r for q in qs for r in _order_stat_ranks(m, q)})
     if x.dtype == torch.float32:
         sample = torch.empty(m, dtype=torch.float32, device=dev)
         ws = torch.empty(max(N.lib().fg_nonzero_sample_workspace_bytes(x.numel()), 1),
                          dtype=torch.uint8, device=dev)
         N.call("fg_gather_nonzero_sample", N.ptr(x), x.numel(), nnz, FIT_SAMPLE_CAP,
                N.ptr(sample), N.ptr(ws), ws.numel(), N.stream_handle())
-        import ctypes
-        sel_ws = torch.empty(N.lib().fg_select_workspace_bytes(), dtype=torch.uint8, device=dev)
-        rk = (ctypes.c_int64 * len(ranks))(*ranks)
-        outv = (ctypes.c_float * len(ranks))()
-        N.call("fg_select_ranks", N.ptr(sample), m, rk, len(ranks), outv, N.ptr(sel_ws),
-               sel_ws.numel(), N.stream_handle())
-        stats = {r: float(np.float32(outv[i])) for i, r in enumerate(ranks)}
-    else:  # float64 features: exact order statistics with device sort
-        nz = x[x != 0]
-        if nnz > FIT_SAMPLE_CAP:
-            pick = torch.from_numpy(np.linspace(0, nnz - 1, FIT_SAMPLE_CAP).astype(np.int64))
-            nz = nz[pick.to(dev)]
-        srt = torch.sort(nz.abs()).values
-        stats = {r: float(srt[r].item()) for r in ranks}
-    logs = {r: float(np.log2(np.abs(np.array([v], dtype=np.float64)))[0])
-            for r, v in stats.items()}
-    vals = []
-    for q in qs:
-        a, b = _order_stat_ranks(m, q)
-        vals.append(_quantile_lerp(logs[a], logs[b], m, q))
-    e_min, e_max = vals
-    if k >= 2 and not e_min < e_max:
-        raise DataError("constant log-magnitude data: exponent range is empty")
-    return SqParams(k, float(e_min), float(e_max), clip_tail_fraction)
+        return _params_from_sample(sample, m, k, clip_tail_fraction)
+    # float64 features: exact order statistics with a device sort
+    nz = x[x != 0]
+    if nnz > FIT_SAMPLE_CAP:
+        pick = torch.from_numpy(np.linspace(0, nnz - 1, FIT_SAMPLE_CAP).astype(np.int64))
+        nz = nz[pick.to(dev)]
+    srt = torch.sort(nz.abs()).values.cpu().numpy()
+    return _params_from_sample(None, m, k, clip_tail_fraction, sorted_host=srt)
+
+
+def fit_sq_stream(chunks, k: int, clip_tail_fraction: float = DEFAULT_CLIP_TAIL_FRACTION,
+                  device="cuda") -> SqParams:
+    """fit_sq over a matrix that only exists as a sequence of row chunks
+    (``chunks()`` yields float32 device tensors in row order, and can be
+    called twice): pass 1 counts nonzeros per chunk, pass 2 gathers the
+    reference's linspace-strided sample with global ranks.  Same result as
+    fit_sq on the whole matrix."""
+    import torch
+    cnt = torch.zeros(1, dtype=torch.int64, device=device)
+    per = []
+    for x in chunks():
+        N.call("fg_count_nonzero", N.ptr(x), x.numel(), N.ptr(cnt), N.stream_handle())
+        per.append(int(cnt.item()))
+    nnz = sum(per)
+    if nnz == 0:
+        if k == 1:
+            return SqParams(1, 0.0, 0.0, clip_tail_fraction)
+        raise DataError("cannot fit an exponent range on an all-zero matrix")
+    m = min(nnz, FIT_SAMPLE_CAP)
+    sample = torch.empty(m, dtype=torch.float32, device=device)
+    base = 0
+    for x, c in zip(chunks(), per):
+        ws = torch.empty(max(N.lib().fg_nonzero_sample_workspace_bytes(x.numel()), 1),
+                         dtype=torch.uint8, device=device)
+        N.call("fg_gather_nonzero_sample_chunk", N.ptr(x), x.numel(), base, nnz, FIT_SAMPLE_CAP,
+               N.ptr(sample), N.ptr(ws), ws.numel(), N.stream_handle())
+        base += c
+    return _params_from_sample(sample, m, k, clip_tail_fraction)
 
 
 def quantize_sq(f: FeatureMatrix, p: SqParams) -> SqCodec:

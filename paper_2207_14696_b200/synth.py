@@ -6,13 +6,14 @@ degree-corrected planted-partition model generated on the GPU:
 
 * nodes carry planted labels (``num_classes``); each class owns a contiguous
   range of virtual positions and positions map to node ids through a fixed
-  pseudo-random bijection, so hubs are spread over the id space;
-* edge endpoints are drawn from power-law position weights
-  (w ∝ (rank+1)^-alpha); with probability ``homophily`` the second endpoint
-  is drawn inside the first endpoint's class;
-* edges are canonicalised, de-duplicated, symmetrised and given self-loops
-  (the reference always samples with self-loops, test_pipeline.py:13-14),
-  giving a valid CsrGraph (int64 offsets, int32 sorted columns).
+  Feistel bijection, so hubs are spread over the id space;
+* edge e is a pure function of (seed, e) (counter-based hash): endpoint
+  ranks follow a power law (w ∝ (rank+1)^-alpha) inside a class; with
+  probability ``homophily`` the second endpoint stays in the first's class;
+* the CSR is built in node-range chunks that each regenerate the edge stream
+  (fg_graph_degrees / fg_graph_emit kernels), de-duplicated, symmetric, with
+  self-loops (the reference always samples with self-loops,
+  test_pipeline.py:13-14): int64 offsets, int32 sorted columns.
 
 Features are row-addressable (``fg_synth_features``): class-conditional
 Gaussians, so the trainer has signal; codecs are built by streaming row
@@ -41,30 +42,6 @@ SHAPES = {
 }
 
 
-def _feistel_perm(x: torch.Tensor, n: int, seed: int) -> torch.Tensor:
-    """Bijection on [0, n) (cycle-walking 4-round Feistel on 2*half bits)."""
-    bits = max(2, int(math.ceil(math.log2(max(n, 2)))))
-    bits += bits & 1
-    half = bits // 2
-    mask = (1 << half) - 1
-    keys = [(seed * 0x9E3779B1 + r * 0x85EBCA77) & 0xFFFFFFF for r in range(4)]
-
-    def rounds(v):
-        lo, hi = v & mask, v >> half
-        for k in keys:
-            f = ((lo * 0x2545F491 + k) ^ (lo >> 3)) & mask
-            lo, hi = hi ^ f, lo
-        return (hi << half) | lo
-
-    y = rounds(x)
-    for _ in range(256):  # cycle walk until inside [0, n)
-        bad = y >= n
-        if not bool(bad.any()):
-            break
-        y = torch.where(bad, rounds(y), y)
-    return y
-
-
 @dataclass
 class SynthGraph:
     graph: DeviceGraph
@@ -76,61 +53,54 @@ class SynthGraph:
 
 def generate_graph(n: int, avg_deg: float, num_classes: int, *, seed: int = 0,
                    alpha: float = 0.8, homophily: float = 0.75, device="cuda",
-                   edge_chunk: int = 1 << 26) -> tuple[DeviceGraph, torch.Tensor]:
-    """Power-law planted-partition graph; returns (DeviceGraph, labels)."""
+                   chunk_entries: int = 1 << 28) -> tuple[DeviceGraph, torch.Tensor]:
+    """Power-law planted-partition graph built on the device in node-range
+    chunks (fg_graph_degrees / fg_graph_emit): valid CSR with sorted,
+    duplicate-free rows, symmetric adjacency and all self-loops.  Memory is
+    O(nnz) for the result plus O(chunk_entries) scratch, so MAG240M-shape
+    graphs (~7e9 stored entries) build on one B200."""
     dev = torch.device(device)
-    gen = torch.Generator(device=dev)
-    gen.manual_seed(seed)
-    C = num_classes
-    # class sizes ~ equal; position p in class c -> node id perm(p)
-    sizes = torch.full((C,), n // C, dtype=torch.int64)
-    sizes[: n % C] += 1
-    starts = torch.zeros(C + 1, dtype=torch.int64)
-    starts[1:] = torch.cumsum(sizes, 0)
-    pos = torch.arange(n, device=dev)
-    cls_of_pos = torch.bucketize(pos, starts[1:].to(dev), right=True).to(torch.int32)
-    node_of_pos = _feistel_perm(pos, n, seed)
-    labels = torch.empty(n, dtype=torch.int32, device=dev)
-    labels[node_of_pos] = cls_of_pos
-    # power-law weight by rank within class
-    rank = pos - starts.to(dev)[cls_of_pos.long()]
-    w = (rank.double() + 1.0).pow(-alpha)
-    cdf = torch.cumsum(w, 0)                       # global (concatenated classes)
-    cls_lo = torch.zeros(C + 1, dtype=torch.float64, device=dev)
-    cls_lo[1:] = cdf[starts[1:].to(dev) - 1]
     E = int(round(n * avg_deg / 2))
-    keys = []
-    done = 0
-    while done < E:
-        m = min(edge_chunk, E - done)
-        u = torch.searchsorted(cdf, torch.rand(m, generator=gen, device=dev, dtype=torch.float64)
-                               * cdf[-1]).clamp_max(n - 1)
-        cu = cls_of_pos[u].long()
-        inside = torch.rand(m, generator=gen, device=dev) < homophily
-        r = torch.rand(m, generator=gen, device=dev, dtype=torch.float64)
-        lo = torch.where(inside, cls_lo[cu], torch.zeros_like(r))
-        hi = torch.where(inside, cls_lo[cu + 1], cdf[-1].expand_as(r))
-        v = torch.searchsorted(cdf, lo + r * (hi - lo)).clamp_max(n - 1)
-        a, b = node_of_pos[u], node_of_pos[v]
-        keep = a != b
-        a, b = a[keep], b[keep]
-        keys.append(torch.minimum(a, b) * n + torch.maximum(a, b))
-        done += m
-    key = torch.unique(torch.cat(keys))
-    del keys
-    lo, hi = key // n, key % n
-    del key
-    diag = torch.arange(n, device=dev)
-    src = torch.cat([lo, hi, diag])
-    dst = torch.cat([hi, lo, diag])
-    del lo, hi
-    order = torch.argsort(src * n + dst)
-    src, dst = src[order], dst[order]
-    del order
+    s = N.stream_handle(dev)
+    deg = torch.zeros(n, dtype=torch.int32, device=dev)
+    N.call("fg_graph_degrees", seed, n, num_classes, alpha, homophily, E, N.ptr(deg), s)
+    raw = deg.long() + 1                      # + self loop
+    cum = torch.cumsum(raw, 0)
+    total_raw = int(cum[-1].item())
+    # chunk boundaries: node ranges whose raw entry count fits the budget
+    bounds = [0]
+    while bounds[-1] < n:
+        lo = bounds[-1]
+        base = int(cum[lo - 1].item()) if lo > 0 else 0
+        hi = int(torch.searchsorted(cum, torch.tensor(base + chunk_entries, device=dev),
+                                    right=True).item())
+        bounds.append(max(hi, lo + 1) if hi < n else n)
+    del cum
+    col = torch.empty(total_raw, dtype=torch.int32, device=dev)
+    counts = torch.zeros(n, dtype=torch.int64, device=dev)
+    cursor = torch.zeros(1, dtype=torch.int64, device=dev)
+    pos = 0
+    for lo, hi in zip(bounds[:-1], bounds[1:]):
+        cap = int(deg[lo:hi].sum().item())
+        keys = torch.empty(cap + (hi - lo), dtype=torch.int64, device=dev)
+        cursor.zero_()
+        N.call("fg_graph_emit", seed, n, num_classes, alpha, homophily, E, lo, hi,
+               N.ptr(cursor), cap, N.ptr(keys), s)
+        m = int(cursor.item())
+        assert m == cap, (m, cap)
+        loc = torch.arange(hi - lo, device=dev, dtype=torch.int64)
+        keys[m:] = loc * n + (loc + lo)        # self loops
+        keys = torch.unique(keys)              # sorted: by local source, then target
+        counts[lo:hi] = torch.bincount(keys // n, minlength=hi - lo)
+        col[pos:pos + keys.numel()] = (keys % n).to(torch.int32)
+        pos += keys.numel()
+        del keys
+    col = col[:pos].clone()
     off = torch.zeros(n + 1, dtype=torch.int64, device=dev)
-    off[1:] = torch.cumsum(torch.bincount(src, minlength=n), 0)
-    g = DeviceGraph(n, off, dst.to(torch.int32).contiguous(), True)
-    return g, labels
+    off[1:] = torch.cumsum(counts, 0)
+    labels = torch.empty(n, dtype=torch.int32, device=dev)
+    N.call("fg_graph_labels", seed, n, num_classes, N.ptr(labels), s)
+    return DeviceGraph(n, off, col, True), labels
 
 
 def split_ids(n: int, train: int, val: int, seed: int = 0) -> tuple[np.ndarray, np.ndarray]:
@@ -158,33 +128,35 @@ def synth_features(rows: int, d: int, *, row0: int = 0, kind: int = 3, seed: int
     return out
 
 
+def synth_feature_rows(ids, d: int, *, kind: int = 3, seed: int = 0,
+                       labels: torch.Tensor | None = None, num_classes: int = 1) -> torch.Tensor:
+    """Rows ``ids`` (int64 device tensor) of the same row-addressable matrix."""
+    ids = ids.to(torch.int64).contiguous()
+    out = torch.empty((ids.numel(), d), dtype=torch.float32, device=ids.device)
+    N.call("fg_synth_feature_rows", kind, seed, N.ptr(ids), ids.numel(), d, N.ptr(labels),
+           num_classes, N.ptr(out), N.stream_handle())
+    return out
+
+
 def build_sq_codec(n: int, d: int, k: int, *, labels, num_classes: int, seed: int = 0,
                    chunk_rows: int = 1 << 20, kind: int = 3):
-    """fit_sq over the (streamed) matrix, then chunked device encode."""
-    from .sq import DeviceSqCodec, fit_sq_device
+    """fit_sq over the row-addressable matrix (streamed: the exact reference
+    fit, sq.py:84-111, never needs the whole matrix), then chunked encode."""
+    from .sq import DeviceSqCodec, fit_sq_stream
     dev = labels.device
-    # fit: the reference fits on all nonzeros (<= 1e7 strided sample); the
-    # exact sample needs the whole matrix order, so stream it when it fits
-    total = n * d
-    if total <= (1 << 31):
-        x = synth_features(n, d, kind=kind, seed=seed, labels=labels, num_classes=num_classes,
-                           device=dev)
-        params = fit_sq_device(x.reshape(-1), k)
-        dc = DeviceSqCodec.empty(params, n, d, dev)
-        dc.encode_rows_(x, 0)
-        del x
-        return dc
-    # very large: fit on a row-strided sample of rows (documented deviation)
-    rows = torch.arange(0, n, max(1, n // 100_000), device=dev)
-    xs = torch.cat([synth_features(1, d, row0=int(r), kind=kind, seed=seed, labels=labels,
-                                   num_classes=num_classes, device=dev) for r in rows[:2000]])
-    params = fit_sq_device(xs.reshape(-1), k)
+
+    def chunks():
+        for r0 in range(0, n, chunk_rows):
+            m = min(chunk_rows, n - r0)
+            yield synth_features(m, d, row0=r0, kind=kind, seed=seed, labels=labels,
+                                 num_classes=num_classes, device=dev)
+
+    params = fit_sq_stream(chunks, k, device=dev)
     dc = DeviceSqCodec.empty(params, n, d, dev)
-    for r0 in range(0, n, chunk_rows):
-        m = min(chunk_rows, n - r0)
-        x = synth_features(m, d, row0=r0, kind=kind, seed=seed, labels=labels,
-                           num_classes=num_classes, device=dev)
+    r0 = 0
+    for x in chunks():
         dc.encode_rows_(x, r0)
+        r0 += x.shape[0]
     return dc
 
 
@@ -205,10 +177,9 @@ def build_vq_codec(n: int, d: int, width: int, length: int, *, labels, num_class
                           device=dev) if n * d <= (1 << 31) else None
     if full is not None:
         sample = full[torch.from_numpy(pick).to(dev)]
-    else:
-        sample = torch.cat([synth_features(1, d, row0=int(r), kind=kind, seed=seed,
-                                           labels=labels, num_classes=num_classes, device=dev)
-                            for r in pick])
+    else:  # only the fit sample rows are ever generated
+        sample = synth_feature_rows(torch.from_numpy(pick).to(dev), d, kind=kind, seed=seed,
+                                    labels=labels, num_classes=num_classes)
     codec = _fit_from_sample(sample.double(), p, d, 32, rng)
     del sample
     dc = DeviceVqCodec.empty(p, d, codec.codebooks, n, dev)
