@@ -259,22 +259,24 @@ __device__ __forceinline__ void load_chunk(const uint8_t* p, uint64_t& w0, uint6
   }
 }
 
-template <int K>
+// Extracts the BW-bit field starting at bit j*K of the MSB-first chunk (BW = K
+// for one code, 2K for the pair (code j, code j+1) with code j in the high bits).
+template <int K, int BW = K>
 __device__ __forceinline__ uint32_t sq_code(uint64_t w0, uint64_t w1, int j) {
-  constexpr int Q = 1 << K;
+  constexpr int Q = 1 << BW;
   const int bit = j * K;
   const int byte = bit >> 3;
   const int inb = bit & 7;
   const uint64_t word = byte < 8 ? w0 : w1;
-  if (K == 8 || inb + K <= 8) {
+  if (BW == 8 || inb + BW <= 8) {
     const uint32_t by = (uint32_t)(word >> (8 * (byte & 7))) & 0xFFu;
-    return (by >> (8 - inb - K)) & (Q - 1);
+    return (by >> (8 - inb - BW)) & (Q - 1);
   }
   const int byte2 = byte + 1;
   const uint64_t word2 = byte2 < 8 ? w0 : w1;
   const uint32_t hi = (uint32_t)(word >> (8 * (byte & 7))) & 0xFFu;
   const uint32_t lo = (uint32_t)(word2 >> (8 * (byte2 & 7))) & 0xFFu;
-  return (((hi << 8) | lo) >> (16 - inb - K)) & (Q - 1);
+  return (((hi << 8) | lo) >> (16 - inb - BW)) & (Q - 1);
 }
 
 template <int K, typename OT>
@@ -286,9 +288,16 @@ k_sq_mean(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
   constexpr int Q = 1 << K;
   constexpr int CB = 2 * K;
   constexpr int U = K >= 5 ? 4 : 8;  // picks whose loads are issued together
+  // k <= 4: one LDS.64 fetches the decoded PAIR (code j, code j+1) from a
+  // 2^(2k)-entry table of float2, halving lookups and field extracts; the
+  // pair lands in a u64 that feeds FADD2 directly.  Each table is replicated
+  // per lane (entry * 32 + lane) so lookups are bank-conflict free.
+  constexpr bool PAIR = 2 * K <= 8;
+  constexpr int LW = PAIR ? (1 << (2 * K)) * 64 : Q * 32;  // table size in floats
   extern __shared__ float s_mem[];
   float* s_lut = s_mem;                                          // [Q][32]
-  int32_t* s_ip0 = reinterpret_cast<int32_t*>(s_mem + Q * 32);   // [kTD + 1] x 2
+  u64* s_lut2 = reinterpret_cast<u64*>(s_mem);                   // [Q*Q][32]
+  int32_t* s_ip0 = reinterpret_cast<int32_t*>(s_mem + LW);       // [kTD + 1] x 2
   int32_t* s_ip1 = s_ip0 + kTD + 1;
   int32_t* s_src0 = s_ip1 + kTD + 1;                             // [kSrcCap] x 2
   int32_t* s_src1 = s_src0 + kSrcCap;
@@ -296,7 +305,14 @@ k_sq_mean(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
   const int64_t live = live_dst(ndst_dev, max_dst);
   const int64_t ntiles = (live + kTD - 1) / kTD;
   if ((int64_t)blockIdx.x >= ntiles) return;
-  for (int i = threadIdx.x; i < Q * 32; i += blockDim.x) s_lut[i] = lut[i >> 5];
+  if constexpr (PAIR) {
+    for (int i = threadIdx.x; i < Q * Q * 32; i += blockDim.x) {
+      const int pv = i >> 5;
+      s_lut2[i] = pack2(lut[pv >> K], lut[pv & (Q - 1)]);
+    }
+  } else {
+    for (int i = threadIdx.x; i < Q * 32; i += blockDim.x) s_lut[i] = lut[i >> 5];
+  }
   const int chunks = (int)((d + 15) >> 4);
   const bool vec_ok = (ld % 16) == 0;
   tile_pipeline(indptr, src, max_dst, ntiles, s_ip0, s_ip1, s_src0, s_src1,
@@ -331,9 +347,14 @@ k_sq_mean(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
           if (base + u < cnt) {
 #pragma unroll
             for (int j = 0; j < 16; j += 2) {
-              const float x0 = s_lut[sq_code<K>(w[u][0], w[u][1], j) * 32 + lane];
-              const float x1 = s_lut[sq_code<K>(w[u][0], w[u][1], j + 1) * 32 + lane];
-              acc[j / 2] = fadd2(acc[j / 2], pack2(x0, x1));
+              if constexpr (PAIR) {
+                const u64 x = s_lut2[sq_code<K, 2 * K>(w[u][0], w[u][1], j) * 32 + lane];
+                acc[j / 2] = fadd2(acc[j / 2], x);
+              } else {
+                const float x0 = s_lut[sq_code<K>(w[u][0], w[u][1], j) * 32 + lane];
+                const float x1 = s_lut[sq_code<K>(w[u][0], w[u][1], j + 1) * 32 + lane];
+                acc[j / 2] = fadd2(acc[j / 2], pack2(x0, x1));
+              }
             }
           }
         }
@@ -680,11 +701,274 @@ k_vq_mean_bits(const uint8_t* __restrict__ rows, int64_t d, int64_t stride, int 
   });
 }
 
+// ----------------------------------------- SQ mean, TMA row staging
+// k_sq_mean spends most of its time waiting on its own row loads (ncu: long
+// scoreboard stalls, DRAM 17 % busy): each thread has only `fanout` 8-byte
+// loads in flight and issues them in bursts between compute phases.  Here the
+// code rows of the NEXT tile are copied into shared memory by cp.async.bulk
+// (one TMA copy per sampled edge, completing on a per-buffer mbarrier) while
+// the current tile is decoded from shared memory, so the HBM gather runs in
+// the background and needs no registers.  (Measured on papers100M-shape,
+// k=4, 64 B rows: 38 us vs 41 us for the register kernel and 45 us for a
+// per-thread 16 B LDGSTS variant; cp.async.bulk operands are warp-uniform,
+// so per-lane rows issue through a 32-step ELECT loop.)  Pipeline depth per
+// persistent CTA: indptr slices 3 tiles ahead (4-slot smem ring), src ids 2 ahead
+// (registers), code rows 1 ahead (2 smem buffers).  A tile whose edges
+// exceed the row buffer falls back to direct register loads.
+constexpr int kBulkThreads = 512;
+constexpr int kBulkRowCap = 1024;                          // rows per buffer, max
+constexpr int kBulkSidPer = kBulkRowCap / kBulkThreads;    // src ids per thread
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
+  const uint32_t mb = smem_addr(bar);
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done) : "r"(mb), "r"(parity) : "memory");
+  }
+}
+
+// one 2K-byte chunk of 16 codes from shared memory (byte 0 in the low bits)
+template <int K>
+__device__ __forceinline__ void lds_chunk(const uint8_t* p, uint64_t& w0, uint64_t& w1) {
+  constexpr int CB = 2 * K;
+  const uint32_t a = smem_addr(p);
+  w0 = w1 = 0;
+  if constexpr (CB == 16) {
+    uint32_t x, y, z, w;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(x), "=r"(y), "=r"(z), "=r"(w) : "r"(a));
+    w0 = ((uint64_t)y << 32) | x;
+    w1 = ((uint64_t)w << 32) | z;
+  } else if constexpr (CB == 8) {
+    uint32_t x, y;
+    asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(x), "=r"(y) : "r"(a));
+    w0 = ((uint64_t)y << 32) | x;
+  } else if constexpr (CB == 4) {
+    uint32_t x;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(x) : "r"(a));
+    w0 = x;
+  } else {  // CB even: 2-byte aligned halves
+#pragma unroll
+    for (int b = 0; b < CB; b += 2) {
+      uint16_t h;
+      asm volatile("ld.shared.u16 %0, [%1];" : "=h"(h) : "r"(a + b));
+      if (b < 8) w0 |= (uint64_t)h << (8 * b); else w1 |= (uint64_t)h << (8 * (b - 8));
+    }
+  }
+}
+
+template <int K, bool PAIR>
+__device__ __forceinline__ void sq_accumulate(u64 (&acc)[8], uint64_t w0, uint64_t w1,
+                                              const float* s_lut, const u64* s_lut2, int lane) {
+#pragma unroll
+  for (int j = 0; j < 16; j += 2) {
+    if constexpr (PAIR) {
+      acc[j / 2] = fadd2(acc[j / 2], s_lut2[sq_code<K, 2 * K>(w0, w1, j) * 32 + lane]);
+    } else {
+      const float x0 = s_lut[sq_code<K>(w0, w1, j) * 32 + lane];
+      const float x1 = s_lut[sq_code<K>(w0, w1, j + 1) * 32 + lane];
+      acc[j / 2] = fadd2(acc[j / 2], pack2(x0, x1));
+    }
+  }
+}
+
+template <typename OT>
+__device__ __forceinline__ void sq_store(OT* o, const u64 (&acc)[8], float inv, int j0, int64_t d,
+                                         bool vec_ok) {
+  if (j0 + 16 <= d) {
+    store_scaled<16>(o, acc, inv, vec_ok);
+  } else {
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (j0 + j < d) store_out(o + j, (j & 1 ? hi2(acc[j / 2]) : lo2(acc[j / 2])) * inv);
+  }
+}
+
+template <int K, typename OT>
+__global__ void __launch_bounds__(kBulkThreads, 1)
+k_sq_mean_bulk(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
+               const float* __restrict__ lut, const int32_t* __restrict__ indptr,
+               const int32_t* __restrict__ src, const int64_t* __restrict__ ndst_dev,
+               int64_t max_dst, OT* __restrict__ out, int64_t ld, int td, int row_cap, int rb) {
+  constexpr int NT = kBulkThreads;
+  constexpr int Q = 1 << K;
+  constexpr bool PAIR = 2 * K <= 8;
+  constexpr int LW = PAIR ? (1 << (2 * K)) * 64 : Q * 32;   // LUT floats
+  constexpr int IPW = ((kTD + 1) * 4 + 3) & ~3;              // indptr ring ints
+  extern __shared__ __align__(128) float s_mem[];
+  float* s_lut = s_mem;
+  u64* s_lut2 = reinterpret_cast<u64*>(s_mem);
+  int32_t* s_ip = reinterpret_cast<int32_t*>(s_mem + LW);   // [4][kTD + 1]
+  uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_ip + IPW);  // [2]
+  uint8_t* s_rows = reinterpret_cast<uint8_t*>(s_bar + 2);   // [2][row_cap * rb]
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int64_t live = live_dst(ndst_dev, max_dst);
+  const int64_t ntiles = (live + td - 1) / td;
+  if ((int64_t)blockIdx.x >= ntiles) return;
+  const int64_t G = gridDim.x;
+  if constexpr (PAIR) {
+    for (int i = tid; i < Q * Q * 32; i += NT) {
+      const int pv = i >> 5;
+      s_lut2[i] = pack2(lut[pv >> K], lut[pv & (Q - 1)]);
+    }
+  } else {
+    for (int i = tid; i < Q * 32; i += NT) s_lut[i] = lut[i >> 5];
+  }
+  if (tid == 0) {
+    mbar_init(s_bar, 1);
+    mbar_init(s_bar + 1, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  const int chunks = (int)((d + 15) >> 4);
+  const bool vec_ok = (ld % 16) == 0;
+  auto tile_of = [&](int64_t k) { return (int64_t)blockIdx.x + k * G; };
+  auto ip_slot = [&](int64_t k) { return s_ip + (int)(k & 3) * (kTD + 1); };
+  auto load_ip = [&](int64_t tile) -> int32_t {
+    return tid <= td ? __ldg(indptr + min64(tile * td + tid, live)) : 0;
+  };
+  auto store_ip = [&](int32_t* slot, int32_t v) { if (tid <= td) slot[tid] = v; };
+  int32_t sid[kBulkSidPer];
+  auto load_sids = [&](const int32_t* ip) {
+    const int32_t e0 = ip[0], ne = ip[td] - e0;
+    if (ne > row_cap) return;
+#pragma unroll
+    for (int j = 0; j < kBulkSidPer; ++j) {
+      const int e = tid + j * NT;
+      if (e < ne) sid[j] = __ldg(src + e0 + e);
+    }
+  };
+  auto issue_rows = [&](const int32_t* ip, int b) {
+    const int32_t ne = ip[td] - ip[0];
+    if (ne > row_cap) return;
+    const uint32_t bar = smem_addr(s_bar + b);
+    uint8_t* dst = s_rows + (int64_t)b * row_cap * rb;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (tid == 0)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                   ::"r"(bar), "r"((uint32_t)ne * (uint32_t)rb) : "memory");
+#pragma unroll
+    for (int j = 0; j < kBulkSidPer; ++j) {
+      const int e = tid + j * NT;
+      if (e < ne)
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+            ::"r"(smem_addr(dst + (int64_t)e * rb)), "l"(rows + (int64_t)sid[j] * stride),
+              "r"(rb), "r"(bar) : "memory");
+    }
+  };
+  // prologue: indptr of tiles 0..2, rows of tile 0 in flight, src ids of tile 1
+  {
+    int32_t r[3];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) r[q] = tile_of(q) < ntiles ? load_ip(tile_of(q)) : 0;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) if (tile_of(q) < ntiles) store_ip(ip_slot(q), r[q]);
+  }
+  __syncthreads();
+  load_sids(ip_slot(0));
+  issue_rows(ip_slot(0), 0);
+  if (tile_of(1) < ntiles) load_sids(ip_slot(1));
+  uint32_t phase = 0;
+  for (int64_t k = 0; tile_of(k) < ntiles; ++k) {
+    const int64_t tile = tile_of(k);
+    const int b = (int)(k & 1);
+    if (tile_of(k + 1) < ntiles) issue_rows(ip_slot(k + 1), b ^ 1);
+    if (tile_of(k + 2) < ntiles) load_sids(ip_slot(k + 2));
+    const bool has3 = tile_of(k + 3) < ntiles;
+    int32_t ipr = 0;
+    if (has3) ipr = load_ip(tile_of(k + 3));
+    const int32_t* ip = ip_slot(k);
+    const int32_t e0 = ip[0];
+    const bool staged = ip[td] - e0 <= row_cap;
+    if (staged) {
+      mbar_wait_parity(s_bar + b, (phase >> b) & 1u);
+      phase ^= 1u << b;
+    }
+    const uint8_t* rbuf = s_rows + (int64_t)b * row_cap * rb;
+    const int items = td * chunks;
+    for (int it = tid; it < items; it += NT) {
+      const int vl = it / chunks;
+      const int c = it - vl * chunks;
+      const int64_t v = tile * td + vl;
+      if (v >= live) break;
+      u64 acc[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] = 0ull;
+      const int a = ip[vl] - e0;
+      const int cnt = ip[vl + 1] - e0 - a;
+      if (staged) {
+        const uint8_t* rp = rbuf + (int64_t)a * rb + c * (2 * K);
+        int p = 0;
+        for (; p + 4 <= cnt; p += 4) {
+          uint64_t w[4][2];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) lds_chunk<K>(rp + (p + u) * rb, w[u][0], w[u][1]);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) sq_accumulate<K, PAIR>(acc, w[u][0], w[u][1], s_lut, s_lut2, lane);
+        }
+        for (; p < cnt; ++p) {
+          uint64_t w0, w1;
+          lds_chunk<K>(rp + p * rb, w0, w1);
+          sq_accumulate<K, PAIR>(acc, w0, w1, s_lut, s_lut2, lane);
+        }
+      } else {
+        const int64_t boff = (int64_t)c * (2 * K);
+        for (int base = 0; base < cnt; base += 8) {
+          uint64_t w[8][2];
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (base + u < cnt)
+              load_chunk<K>(rows + (int64_t)__ldg(src + e0 + a + base + u) * stride + boff,
+                            w[u][0], w[u][1]);
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (base + u < cnt) sq_accumulate<K, PAIR>(acc, w[u][0], w[u][1], s_lut, s_lut2, lane);
+        }
+      }
+      const float inv = cnt ? 1.0f / (float)cnt : 0.0f;
+      sq_store(out + v * ld + c * 16, acc, inv, c * 16, d, vec_ok);
+    }
+    // slot k+3 (= k-1 mod 4) was last read before the previous barrier; the
+    // barrier below publishes it and retires row buffer b for tile k+2
+    if (has3) store_ip(ip_slot(k + 3), ipr);
+    __syncthreads();
+  }
+}
+
 // ------------------------------------------------------------ launchers
 template <int K, typename OT>
 int launch_sq(const fg_codec_desc* c, const int32_t* indptr, const int32_t* src,
               const int64_t* ndst, int64_t max_dst, void* out, int64_t ld, cudaStream_t st) {
-  const int smem = (1 << K) * 32 * 4 + 2 * (kTD + 1 + kSrcCap) * 4;
+  // TMA-staged variant: needs a row buffer holding a tile of >= 32
+  // destinations at fanout 8 next to the decode table
+  {
+    constexpr int kSmemBudget = 220 * 1024;
+    const int lut_b = 2 * K <= 8 ? (1 << (2 * K)) * 32 * 8 : (1 << K) * 32 * 4;
+    const int fixed = lut_b + ((((kTD + 1) * 4 + 3) & ~3) * 4) + 16;
+    const int chunks = (int)((c->d + 15) / 16);
+    const int rb = (chunks * 2 * K + 15) / 16 * 16;
+    int row_cap = (kSmemBudget - fixed) / (2 * rb);
+    if (row_cap > kBulkRowCap) row_cap = kBulkRowCap;
+    int td = kTD;
+    while (td > 32 && td * 8 > row_cap) td /= 2;
+    if (td * 8 <= row_cap && rb <= c->row_stride) {
+      const int smem = fixed + 2 * row_cap * rb;
+      auto kern = k_sq_mean_bulk<K, OT>;
+      FG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      const int grid = (int)min64(ceil_div(max_dst, td), (int64_t)sm_count());
+      kern<<<grid, kBulkThreads, smem, st>>>(c->rows, c->d, c->row_stride,
+                                             (const float*)c->table, indptr, src, ndst, max_dst,
+                                             (OT*)out, ld, td, row_cap, rb);
+      FG_LAUNCH_CHECK();
+      return FG_OK;
+    }
+  }
+  const int lut_bytes = 2 * K <= 8 ? (1 << (2 * K)) * 32 * 8 : (1 << K) * 32 * 4;
+  const int smem = lut_bytes + 2 * (kTD + 1 + kSrcCap) * 4;
   auto kern = k_sq_mean<K, OT>;
   FG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const int grid = (int)min64(ceil_div(max_dst, kTD), (int64_t)sm_count() * 2);

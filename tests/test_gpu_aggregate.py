@@ -37,10 +37,13 @@ def _run(dc, counts, indptr, src, n_dst, max_dst, dtype, pitch=None):
     return o[:, :dc.d]
 
 
-@pytest.mark.parametrize("k,d", [(8, 128), (4, 128), (8, 100), (3, 100), (1, 64), (2, 37),
-                                 (5, 16), (6, 24), (7, 40)])
+# fan 7: tiles staged in shared memory by TMA row copies; fan 40 and d 768:
+# tiles overflowing the row buffer take the direct-load fallback
+@pytest.mark.parametrize("k,d,fan", [(8, 128, 7), (4, 128, 7), (8, 100, 7), (3, 100, 7),
+                                     (1, 64, 7), (2, 37, 7), (5, 16, 7), (6, 24, 7), (7, 40, 7),
+                                     (4, 128, 40), (8, 128, 12), (4, 768, 7), (8, 1000, 3)])
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
-def test_fused_sq_mean(k, d, dtype):
+def test_fused_sq_mean(k, d, fan, dtype):
     rng = np.random.default_rng(k * 100 + d)
     n = 5000
     x = (np.exp(rng.normal(0, 1, (n, d))) * rng.choice([-1, 1], (n, d))).astype(np.float32)
@@ -48,7 +51,7 @@ def test_fused_sq_mean(k, d, dtype):
     c = fg.quantize_sq(f, fg.fit_sq(f, k))
     dc = fg.DeviceSqCodec.from_codec(c)
     n_dst, max_dst = 3000, 3200
-    counts, indptr, src = _block(n, n_dst, max_dst, 7, rng)
+    counts, indptr, src = _block(n, n_dst, max_dst, fan, rng)
     pitch = (d + 15) // 16 * 16 + (16 if d % 2 else 0)
     got = _run(dc, counts, indptr, src, n_dst, max_dst, dtype, pitch)
     dec = oc.sq_dequant_rows(c.payload, n, d, k, c.params.e_min, c.params.e_max, src)
