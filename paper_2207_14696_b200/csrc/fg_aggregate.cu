@@ -59,14 +59,19 @@ k_block_mean_fwd(const uint16_t* __restrict__ h, int64_t H, const int32_t* __res
     if (v < live) {
       const int32_t e0 = indptr[v], e1 = indptr[v + 1];
       cnt = e1 - e0;
-      for (int32_t e = e0; e < e1; e += 4) {
-        uint4 q[4];
+      // 8 picks per batch: the src-id loads, then the 8 row loads, all in flight
+      for (int32_t e = e0; e < e1; e += 8) {
+        int32_t sl[8];
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
+        for (int u = 0; u < 8; ++u)
+          if (e + u < e1) sl[u] = srcl[e + u];
+        uint4 q[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
           if (e + u < e1)
-            q[u] = __ldg(reinterpret_cast<const uint4*>(h + (int64_t)srcl[e + u] * H) + c);
+            q[u] = __ldg(reinterpret_cast<const uint4*>(h + (int64_t)sl[u] * H) + c);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < 8; ++u) {
           if (e + u < e1) {
             float f[8];
             bf16x8_to_f32(q[u], f);
@@ -257,55 +262,98 @@ __global__ void k_t_place(const int32_t* __restrict__ local, const int64_t* __re
   }
 }
 
-template <bool RELU>
-__global__ void __launch_bounds__(256)
+// Thread per (group of R consecutive source rows, 8-byte chunk of 4
+// columns).  Most sources have one or two transposed edges, so a thread per
+// row is a three-deep dependent load chain (t_indptr -> t_dst -> g row) with
+// nothing else in flight; R rows per thread issue R chains side by side
+// (8-byte chunks keep the R-way state in registers at 3 CTAs/SM).
+__device__ __forceinline__ void bf16x4_to_f32(const uint2 q, float* f) {
+  f[0] = __uint_as_float(q.x << 16);
+  f[1] = __uint_as_float(q.x & 0xFFFF0000u);
+  f[2] = __uint_as_float(q.y << 16);
+  f[3] = __uint_as_float(q.y & 0xFFFF0000u);
+}
+__device__ __forceinline__ uint2 f32_to_bf16x4(const float* f) {
+  const __nv_bfloat162 a = __floats2bfloat162_rn(f[0], f[1]);
+  const __nv_bfloat162 b = __floats2bfloat162_rn(f[2], f[3]);
+  return make_uint2(*reinterpret_cast<const uint32_t*>(&a), *reinterpret_cast<const uint32_t*>(&b));
+}
+
+template <bool RELU, int R>
+__global__ void __launch_bounds__(256, 3)
 k_block_mean_bwd_t(const uint16_t* __restrict__ g, int64_t H, int64_t g_ld,
                    const int32_t* __restrict__ t_indptr,
                    const int32_t* __restrict__ t_dst, const float* __restrict__ t_w,
                    const int64_t* __restrict__ nsrc_dev, int64_t cap_src,
                    const uint16_t* __restrict__ mask, uint16_t* __restrict__ out) {
-  const int64_t chunks = H >> 3;
-  const int64_t total = cap_src * chunks;
+  const int64_t chunks = H >> 2;
+  const int64_t ngroups = (cap_src + R - 1) / R;
+  const int64_t total = ngroups * chunks;
   const int64_t live = live_count(nsrc_dev, cap_src);
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = t / chunks, c = t - r * chunks;
-    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    if (r >= live) {  // padded source rows: zero gradient, no loads
-      reinterpret_cast<uint4*>(out + r * H)[c] = make_uint4(0u, 0u, 0u, 0u);
-      continue;
-    }
-    uint4 mq = make_uint4(0u, 0u, 0u, 0u);
-    if (RELU) mq = __ldg(reinterpret_cast<const uint4*>(mask + r * H) + c);  // issued early
-    const int32_t i0 = t_indptr[r], i1 = t_indptr[r + 1];
-    for (int32_t i = i0; i < i1; i += 4) {
-      uint4 q[4];
-      float sc[4];
+    const int64_t rg = t / chunks, c = t - rg * chunks;
+    const int64_t r0 = rg * R;
+    int32_t i0[R], i1[R];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if (i + u < i1) {
-          const int32_t v = t_dst[i + u];
-          sc[u] = t_w[i + u];
-          q[u] = __ldg(reinterpret_cast<const uint4*>(g + (int64_t)v * g_ld) + c);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if (i + u < i1) {
-          float f[8];
-          bf16x8_to_f32(q[u], f);
-#pragma unroll
-          for (int j = 0; j < 8; ++j) acc[j] = fmaf(f[j], sc[u], acc[j]);
-        }
+    for (int u = 0; u < R; ++u) {
+      i0[u] = i1[u] = 0;
+      if (r0 + u < live) {
+        i0[u] = t_indptr[r0 + u];
+        i1[u] = t_indptr[r0 + u + 1];
       }
     }
-    if (RELU) {
-      float m[8];
-      bf16x8_to_f32(mq, m);
+    int32_t v[R];
+    float w[R];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) acc[j] = m[j] > 0.f ? acc[j] : 0.f;
+    for (int u = 0; u < R; ++u)
+      if (i0[u] < i1[u]) { v[u] = t_dst[i0[u]]; w[u] = t_w[i0[u]]; }
+    uint2 q[R], mq[R];
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+      mq[u] = make_uint2(0u, 0u);
+      if (RELU && r0 + u < live) mq[u] = __ldg(reinterpret_cast<const uint2*>(mask + (r0 + u) * H) + c);
+      if (i0[u] < i1[u]) q[u] = __ldg(reinterpret_cast<const uint2*>(g + (int64_t)v[u] * g_ld) + c);
     }
-    reinterpret_cast<uint4*>(out + r * H)[c] = f32_to_bf16x8(acc);
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+      const int64_t r = r0 + u;
+      if (r >= cap_src) break;
+      float acc[4] = {0, 0, 0, 0};
+      if (i0[u] < i1[u]) {
+        float f[4];
+        bf16x4_to_f32(q[u], f);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[j] = f[j] * w[u];
+      }
+      // remaining transposed edges of this row (hub sources), 4 at a time
+      for (int32_t i = i0[u] + 1; i < i1[u]; i += 4) {
+        uint2 qq[4];
+        float sc[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (i + k < i1[u]) {
+            sc[k] = t_w[i + k];
+            qq[k] = __ldg(reinterpret_cast<const uint2*>(g + (int64_t)t_dst[i + k] * g_ld) + c);
+          }
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (i + k < i1[u]) {
+            float f[4];
+            bf16x4_to_f32(qq[k], f);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[j] = fmaf(f[j], sc[k], acc[j]);
+          }
+      }
+      if (RELU) {
+        float m[4];
+        bf16x4_to_f32(mq[u], m);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[j] = m[j] > 0.f ? acc[j] : 0.f;
+      }
+      // padded source rows (r >= live) get a zero gradient
+      reinterpret_cast<uint2*>(out + r * H)[c] = f32_to_bf16x4(acc);
+    }
   }
 }
 
@@ -378,12 +426,13 @@ extern "C" int fg_block_mean_bwd_t(const uint16_t* g, int64_t H, int64_t g_ld,
   if (g_ld == 0) g_ld = H;
   FG_CHECK_ARG(g_ld % 8 == 0 && g_ld >= H, "bad g_ld");
   if (cap_src == 0) return FG_OK;
-  const int64_t total = cap_src * (H / 8);
+  constexpr int R = 4;
+  const int64_t total = (cap_src + R - 1) / R * (H / 4);
   if (relu_mask)
-    fg::k_block_mean_bwd_t<true><<<grid_for(total, 256), 256, 0, as_stream(s)>>>(
+    fg::k_block_mean_bwd_t<true, R><<<grid_for(total, 256, 3), 256, 0, as_stream(s)>>>(
         g, H, g_ld, t_indptr, t_dst, t_w, n_src_dev, cap_src, relu_mask, out);
   else
-    fg::k_block_mean_bwd_t<false><<<grid_for(total, 256), 256, 0, as_stream(s)>>>(
+    fg::k_block_mean_bwd_t<false, R><<<grid_for(total, 256, 3), 256, 0, as_stream(s)>>>(
         g, H, g_ld, t_indptr, t_dst, t_w, n_src_dev, cap_src, nullptr, out);
   FG_LAUNCH_CHECK();
   return FG_OK;

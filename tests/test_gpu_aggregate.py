@@ -231,3 +231,70 @@ def test_fused_softmax_ce_matches_torch(dtype):
     tol = 1e-6 if dtype == torch.float32 else 1e-2 / nv
     assert torch.allclose(logits.grad[:nv].float(), lf.grad, atol=tol, rtol=1e-2)
     assert (logits.grad[nv:] == 0).all()
+
+
+# (128, 48, True, 40, 290): ~50 transposed edges per source row, so a tile's
+# edge slice overflows the shared-memory stage (direct-load path)
+@pytest.mark.parametrize("H,P,relu,fan,n_src", [(256, 112, True, 10, 2900), (256, 144, True, 5, 2900),
+                                                (128, 64, False, 15, 2900), (256, 160, True, 3, 2900),
+                                                (128, 48, True, 40, 290), (256, 112, True, 10, 100)])
+def test_block_mean_wgrad_tcgen05(H, P, relu, fan, n_src):
+    """Fused dH gather + tcgen05 dW against torch fp32 on the same bf16 dH."""
+    from paper_2207_14696_b200.aggregate import block_mean_wgrad, wgrad_supported
+    assert wgrad_supported(H, P)
+    rng = np.random.default_rng(H + P + fan)
+    cap_src, n_dst, max_dst = n_src + 200, 700, 760
+    counts, indptr, src = _block(n_src, n_dst, max_dst, fan, rng)
+    ti, td, tw = _transpose_np(indptr, src, n_dst, n_src)
+    dev = "cuda"
+    t_indptr = torch.zeros(cap_src + 1, dtype=torch.int32, device=dev)
+    t_indptr[:n_src + 1] = torch.from_numpy(ti).to(dev)
+    t_indptr[n_src + 1:] = int(ti[-1])
+    trans = (t_indptr, torch.from_numpy(td).to(dev), torch.from_numpy(tw).to(dev),
+             torch.tensor([n_src], device=dev))
+    g = torch.randn(max_dst, H + 8, device=dev).to(torch.bfloat16)
+    h = torch.randn(cap_src, H, device=dev).to(torch.bfloat16)
+    x = torch.randn(cap_src, P, device=dev).to(torch.bfloat16)
+    x[n_src:] = float("nan")  # rows past the live count must never be read
+    dw = block_mean_wgrad(g, trans, cap_src, h if relu else None, x)
+    torch.cuda.synchronize()
+    # reference: dH from the transposed lists, bf16-rounded as in the kernel
+    dst_t = torch.from_numpy(td).long().to(dev)
+    w_t = torch.from_numpy(tw).to(dev)
+    rows = torch.repeat_interleave(torch.arange(n_src, device=dev),
+                                   torch.from_numpy(np.diff(ti)).long().to(dev))
+    dh = torch.zeros(n_src, H, device=dev).index_add_(0, rows, g[dst_t, :H].float() * w_t[:, None])
+    if relu:
+        dh = dh * (h[:n_src].float() > 0)
+    dh = dh.to(torch.bfloat16).float()
+    ref = dh.t() @ x[:n_src].float()
+    # dH is summed in a different order here, so an element can round to the
+    # neighbouring bf16 value (2^-8 relative); layout/indexing errors are O(1)
+    err = (dw - ref).abs().max().item()
+    assert err <= 2e-3 * ref.abs().max().item() + 1e-4, err
+    assert torch.isfinite(dw).all()
+
+
+def test_input_block_mean_autograd_matches_unfused():
+    from paper_2207_14696_b200.aggregate import input_block_mean
+    rng = np.random.default_rng(11)
+    n_src, n_dst, max_dst, H, P = 2500, 600, 700, 256, 112
+    counts, indptr, src = _block(n_src, n_dst, max_dst, 10, rng)
+    ti, td, tw = _transpose_np(indptr, src, n_dst, n_src)
+    dev = "cuda"
+    ip, sl = torch.from_numpy(indptr).to(dev), torch.from_numpy(src).to(dev)
+    nd = torch.tensor([n_dst], device=dev)
+    trans = (torch.from_numpy(ti).to(dev), torch.from_numpy(td).to(dev),
+             torch.from_numpy(tw).to(dev), torch.tensor([n_src], device=dev))
+    x = torch.randn(n_src, P, device=dev).to(torch.bfloat16)
+    w1 = (torch.randn(H, P, device=dev) * 0.1).requires_grad_(True)
+    w2 = w1.detach().clone().requires_grad_(True)
+    a1 = input_block_mean(x, w1, ip, sl, nd, max_dst, trans)
+    h2 = torch.mm(x, w2.to(torch.bfloat16).t())
+    a2 = block_mean(h2, ip, sl, nd, max_dst, relu=True, trans=trans, bias_col=True)
+    assert torch.equal(a1, a2)
+    gout = torch.randn_like(a1.float()).to(torch.bfloat16)
+    a1.backward(gout)
+    a2.backward(gout)
+    scale = w2.grad.abs().max().item()
+    assert (w1.grad - w2.grad).abs().max().item() <= 2e-2 * scale
