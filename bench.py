@@ -147,7 +147,10 @@ def build_workload(cfg_name, device, seed=0, scale=1.0):
     import torch
     from paper_2207_14696_b200.synth import SHAPES, build_sq_codec, build_vq_codec, make_shape
     shape, codec_spec, fanouts, bs, hidden = CONFIGS[cfg_name]
+    t0 = time.perf_counter()
     sg = make_shape(shape, seed=seed, scale=scale, device=device)
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
     n, d = sg.graph.n, SHAPES[shape]["d"]
     if codec_spec[0] == "vq":
         dc, host_codec = build_vq_codec(n, d, codec_spec[1], codec_spec[2], labels=sg.labels,
@@ -158,6 +161,11 @@ def build_workload(cfg_name, device, seed=0, scale=1.0):
                             seed=seed)
         codec_desc = f"sq k={codec_spec[1]} (CR {32 / codec_spec[1]:.0f})"
     torch.cuda.synchronize()
+    t2 = time.perf_counter()
+    print(f"[bench] {cfg_name}: graph n={sg.graph.n} nnz={sg.graph.nnz} built in {t1 - t0:.1f} s, "
+          f"codec ({codec_desc}) in {t2 - t1:.1f} s, "
+          f"{torch.cuda.max_memory_allocated(device) / 2**30:.1f} GiB peak", file=sys.stderr,
+          flush=True)
     return sg, dc, codec_desc, fanouts, bs, hidden
 
 

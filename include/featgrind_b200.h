@@ -227,21 +227,23 @@ int fg_block_mean_bwd_t(const uint16_t* grad_out, int64_t h_dim, int64_t g_ld,
 
 /* Fused block-mean backward + input-layer weight gradient (tcgen05/TMEM).
  * For the SAGE input layer h = x W^T (x: [cap_src, p_dim] bf16 rows with a
- * ones column, W: [h_dim, p_dim]) followed by a ReLU block mean, computes
- *   dW = sum_{r < *n_src_dev} dH[r]^T x[r],
- *   dH[r] = relu'(h_mask[r]) * sum_{i in t_indptr[r]..} t_w[i] * g[t_dst[i], :h_dim]
- * into dw [h_dim, p_dim] fp32 (overwritten) without materialising dH.  The
- * transposed CSR is fg_block_transpose's; h_mask may be NULL (no ReLU).
- * Shapes: fg_block_mean_wgrad_supported(h_dim, p_dim) != 0 (h_dim 128 or 256,
- * p_dim % 16 == 0, p_dim <= 256).  scratch: fg_block_mean_wgrad_scratch_bytes
- * (one fp32 [h_dim, p_dim] partial per SM, reduced in fixed order:
- * deterministic).  No reference counterpart; differentiates
- * the mean aggregation of reference/pkg/src/featgrind/factors.py:108-114. */
+ * ones column, W: [h_dim, p_dim]) followed by a ReLU block mean over the
+ * block (indptr [max_dst + 1], local [edges]: source row of each edge), computes
+ *   dW = sum_{edges e of live dst v} ( relu'(h_mask[local[e]]) * g[v, :h_dim] / cnt_v )^T x[local[e]]
+ * (= dH^T x) into dw [h_dim, p_dim] fp32 (overwritten) without materialising
+ * dH; the GEMM's K dimension is the block's edges, 128 per tile.  h_mask may
+ * be NULL (no ReLU).  Shapes: fg_block_mean_wgrad_supported(h_dim, p_dim) != 0
+ * (h_dim 128 or 256, p_dim % 16 == 0, p_dim <= 160 at h_dim 256).  scratch:
+ * fg_block_mean_wgrad_scratch_bytes(h_dim, p_dim) (fp32 partials per SM,
+ * reduced in fixed order: deterministic).  The edge -> dst map is resolved
+ * in-kernel from indptr (each CTA owns a contiguous edge range).  No
+ * reference counterpart; differentiates the mean
+ * aggregation of reference/pkg/src/featgrind/factors.py:108-114. */
 int fg_block_mean_wgrad_supported(int64_t h_dim, int64_t p_dim);
 int64_t fg_block_mean_wgrad_scratch_bytes(int64_t h_dim, int64_t p_dim);
-int fg_block_mean_wgrad(const uint16_t* grad_out, int64_t g_ld, const int32_t* t_indptr,
-                        const int32_t* t_dst, const float* t_w, const int64_t* n_src_dev,
-                        int64_t cap_src, const uint16_t* h_mask, int64_t h_dim,
+int fg_block_mean_wgrad(const uint16_t* grad_out, int64_t g_ld, const int32_t* indptr,
+                        const int32_t* local, const int64_t* n_dst_dev, int64_t max_dst,
+                        const uint16_t* h_mask, int64_t h_dim,
                         const uint16_t* x, int64_t p_dim, float* dw, float* scratch,
                         int64_t scratch_bytes, void* cuda_stream);
 

@@ -114,22 +114,27 @@ def wgrad_supported(h_dim: int, p_dim: int) -> bool:
     return bool(N.lib().fg_block_mean_wgrad_supported(h_dim, p_dim))
 
 
-def block_mean_wgrad(g, trans, cap_src: int, h_mask, x, dw=None, scratch=None):
-    """dW = dH^T x with dH[r] = relu'(h_mask[r]) * sum over the transposed
-    block of t_w * g[t_dst] (``fg_block_mean_wgrad``: dH is built tile by
-    tile in shared memory and consumed by tcgen05 MMAs, never written to
-    HBM).  g: [cap_dst, >= H] bf16, x: [cap_src, P] bf16, h_mask:
-    [cap_src, H] bf16 or None; returns dw [H, P] fp32."""
-    t_indptr, t_dst, t_w, n_src = trans
-    H = h_mask.shape[1] if h_mask is not None else g.shape[1] - 8
+def wgrad_scratch(H: int, P: int, device) -> torch.Tensor:
+    nb = N.lib().fg_block_mean_wgrad_scratch_bytes(H, P)
+    return torch.empty((nb + 3) // 4, dtype=torch.float32, device=device)
+
+
+def block_mean_wgrad(g, indptr, local, n_dst, max_dst: int, h_mask, x, dw=None, scratch=None,
+                     H: int | None = None):
+    """dW = dH^T x for the block mean a[v] = mean_e relu(h[local[e]]) with
+    upstream gradient g = dL/da, computed as an edge-tiled GEMM
+    (``fg_block_mean_wgrad``: per-edge terms relu'(h[l_e]) * g[v_e] / cnt_v
+    are built in shared memory and consumed by tcgen05 MMAs; neither they
+    nor dH reach HBM).  g: [>= max_dst, >= H] bf16, x: [cap_src, P] bf16,
+    h_mask: [cap_src, H] bf16 or None; returns dw [H, P] fp32."""
+    H = H or (h_mask.shape[1] if h_mask is not None else g.shape[1] - 8)
     P = x.shape[1]
     if dw is None:
         dw = torch.empty((H, P), dtype=torch.float32, device=x.device)
     if scratch is None:
-        scratch = torch.empty(N.lib().fg_block_mean_wgrad_scratch_bytes(H, P) // 4,
-                              dtype=torch.float32, device=x.device)
-    N.call("fg_block_mean_wgrad", N.ptr(g), g.stride(0), N.ptr(t_indptr), N.ptr(t_dst),
-           N.ptr(t_w), N.ptr(n_src), cap_src, N.ptr(h_mask) if h_mask is not None else None, H,
+        scratch = wgrad_scratch(H, P, x.device)
+    N.call("fg_block_mean_wgrad", N.ptr(g), g.stride(0), N.ptr(indptr), N.ptr(local),
+           N.ptr(n_dst), max_dst, N.ptr(h_mask) if h_mask is not None else None, H,
            N.ptr(x), P, N.ptr(dw), N.ptr(scratch), scratch.numel() * 4, N.stream_handle())
     return dw
 
@@ -137,28 +142,29 @@ def block_mean_wgrad(g, trans, cap_src: int, h_mask, x, dw=None, scratch=None):
 class InputBlockMean(torch.autograd.Function):
     """a = block_mean(relu(x @ W^T)) for the SAGE input layer (bias folded in
     W via x's ones column).  Forward: one bf16 GEMM + the block-mean gather;
-    backward: ``block_mean_wgrad`` (fused dH gather + tcgen05 dW), no dx (x
+    backward: ``block_mean_wgrad`` (edge-tiled fused tcgen05 dW), no dx (x
     is the decoded input aggregate, not a parameter)."""
 
     @staticmethod
-    def forward(ctx, x, w, indptr, local, n_dst, max_dst, trans, bias_col, scratch):
+    def forward(ctx, x, w, indptr, local, n_dst, max_dst, bias_col, scratch):
         h = torch.mm(x, w.to(torch.bfloat16).t())
         out = block_mean(h, indptr, local, n_dst, max_dst, relu=True, trans=None,
                          bias_col=bias_col)
-        ctx.save_for_backward(x, h)
-        ctx.trans, ctx.scratch = trans, scratch
+        ctx.save_for_backward(x, h, indptr, local, n_dst)
+        ctx.max_dst, ctx.scratch = max_dst, scratch
         return out
 
     @staticmethod
     def backward(ctx, ga):
-        x, h = ctx.saved_tensors
-        dw = block_mean_wgrad(ga.contiguous(), ctx.trans, h.shape[0], h, x, scratch=ctx.scratch)
-        return None, dw, None, None, None, None, None, None, None
+        x, h, indptr, local, n_dst = ctx.saved_tensors
+        dw = block_mean_wgrad(ga.contiguous(), indptr, local, n_dst, ctx.max_dst, h, x,
+                              scratch=ctx.scratch)
+        return None, dw, None, None, None, None, None, None
 
 
-def input_block_mean(x, w, indptr, local, n_dst, max_dst: int, trans, bias_col: bool = True,
+def input_block_mean(x, w, indptr, local, n_dst, max_dst: int, bias_col: bool = True,
                      scratch=None):
-    return InputBlockMean.apply(x, w, indptr, local, n_dst, max_dst, trans, bias_col, scratch)
+    return InputBlockMean.apply(x, w, indptr, local, n_dst, max_dst, bias_col, scratch)
 
 
 class SoftmaxCE(torch.autograd.Function):

@@ -23,6 +23,7 @@
 //    finite contents; callers zero the buffer once at allocation);
 //  * `out_ld` lets the caller pad rows (e.g. d=100 -> 112) so the following
 //    bf16 GEMM sees 16-element-aligned K.
+#include <algorithm>
 #include <type_traits>
 
 #include "fg_common.cuh"
@@ -149,9 +150,12 @@ template <int NT = kThreads, typename F>
 __device__ __forceinline__ void tile_pipeline(const int32_t* __restrict__ indptr,
                                               const int32_t* __restrict__ src, int64_t max_dst,
                                               int64_t ntiles, int32_t* s_ip0, int32_t* s_ip1,
-                                              int32_t* s_src0, int32_t* s_src1, F&& compute) {
-  const int64_t step = gridDim.x;
-  int64_t tile = blockIdx.x;
+                                              int32_t* s_src0, int32_t* s_src1, F&& compute,
+                                              int64_t tile0 = -1, int64_t step = -1) {
+  // default: CTA b walks tiles b, b + grid, ...; part-sliced kernels pass
+  // their own (first tile, stride) so one slice's CTAs cover every tile
+  if (step < 0) step = gridDim.x;
+  int64_t tile = tile0 < 0 ? (int64_t)blockIdx.x : tile0;
   Stage<NT> st, st2;
   // prologue: buffer 0 <- (ip, src) of tile; buffer 1 <- ip of tile+step
   stage_load_ip<NT>(indptr, tile, max_dst, st);
@@ -567,28 +571,39 @@ k_vq_mean8_fast(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
                 const __nv_bfloat16* __restrict__ books, int length, int parts,
                 const int32_t* __restrict__ indptr, const int32_t* __restrict__ src,
                 const int64_t* __restrict__ ndst_dev, int64_t max_dst,
-                __nv_bfloat16* __restrict__ out, int64_t ld) {
-  // G parts per thread: G * W = 32 fp32 accumulators
+                __nv_bfloat16* __restrict__ out, int64_t ld, int slice_parts, int nslices) {
+  // G parts per thread: G * W = 32 fp32 accumulators.  Part slicing: when
+  // the whole bf16 codebook does not fit the smem budget (MAG240M-shape:
+  // 96 parts x 256 x 8 = 393 KB), CTA b serves parts [s*SP, s*SP+SP) of
+  // every tile with s = b % nslices; the slices of one tile run on
+  // neighbouring CTAs at the same time, so a code row's sectors are fetched
+  // from DRAM once and the sibling slices hit L2.
   __shared__ __align__(8) uint64_t s_mbar;
   extern __shared__ float4 s_mem4[];
-  const int64_t nbook = (int64_t)parts * length * W;           // bf16 elements
-  const int64_t zero_part = (int64_t)(G - 1) * length * W;     // zero parts after the last
+  const int slice = (int)(blockIdx.x % nslices);
+  const int part_base = slice * slice_parts;
+  const int lparts = min(slice_parts, parts - part_base);  // parts in this slice
+  const int zp = (G - parts % G) % G;                      // zero parts after the last
+  const int64_t nbook = (int64_t)lparts * length * W;      // bf16 elements
+  const int64_t zero_part = (int64_t)zp * length * W;
   __nv_bfloat16* s_book = reinterpret_cast<__nv_bfloat16*>(s_mem4);
-  const int64_t book_bytes16 = ((nbook + zero_part) * 2 + 15) & ~15ll;
+  const int64_t book_bytes16 = (((int64_t)slice_parts + zp) * length * W * 2 + 15) & ~15ll;
   int32_t* s_ip0 = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(s_mem4) + book_bytes16);
   int32_t* s_ip1 = s_ip0 + kTD + 1;
   int32_t* s_src0 = s_ip1 + kTD + 1;
   int32_t* s_src1 = s_src0 + kSrcCap;
   const int64_t live = live_dst(ndst_dev, max_dst);
   const int64_t ntiles = (live + kTD - 1) / kTD;
-  if ((int64_t)blockIdx.x >= ntiles) return;
+  const int64_t tile0 = blockIdx.x / nslices, tstep = gridDim.x / nslices;
+  if (tile0 >= ntiles) return;
+  const __nv_bfloat16* gbook = books + (int64_t)part_base * length * W;
   const uint32_t bytes = (uint32_t)(nbook * 2) & ~15u;
-  bulk_fill(s_book, books, bytes, &s_mbar);
-  for (int64_t i = bytes / 2 + threadIdx.x; i < nbook; i += blockDim.x) s_book[i] = books[i];
+  bulk_fill(s_book, gbook, bytes, &s_mbar);
+  for (int64_t i = bytes / 2 + threadIdx.x; i < nbook; i += blockDim.x) s_book[i] = gbook[i];
   for (int64_t i = threadIdx.x; i < zero_part; i += blockDim.x)
     s_book[nbook + i] = __float2bfloat16_rn(0.f);
   const uint32_t s_base = smem_addr(s_book);
-  const int groups = (parts + G - 1) / G;
+  const int groups = (lparts + G - 1) / G;
   const bool vec_ok = (ld % 16) == 0;
   bool waited = false;
   tile_pipeline<kFastThreads>(indptr, src, max_dst, ntiles, s_ip0, s_ip1, s_src0, s_src1,
@@ -606,11 +621,12 @@ k_vq_mean8_fast(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
       const int g = it - vl * groups;
       const int64_t v = v0 + vl;
       if (v >= live) break;
-      const int p0 = g * G;
-      const int np = min(G, parts - p0);
+      const int p0 = g * G;                  // slice-local part
+      const int np = min(G, lparts - p0);
       // parts p0 .. p0+G-1; past the last part the table is zero padded
       const uint32_t pstride = (uint32_t)(length * W * 2);
       const uint32_t base0 = s_base + (uint32_t)p0 * pstride;
+      const int pg = part_base + p0;         // global part (code byte, column)
       u64 acc[G * W / 2];
 #pragma unroll
       for (int j = 0; j < G * W / 2; ++j) acc[j] = 0ull;
@@ -624,15 +640,15 @@ k_vq_mean8_fast(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
         for (int u = 0; u < 5; ++u)
           if (u < cb) sids[u] = sp[u];
         switch (cb) {
-          case 1: vq_fast_body<W, G, 1>(rows, stride, sids, base0, pstride, p0, acc); break;
-          case 2: vq_fast_body<W, G, 2>(rows, stride, sids, base0, pstride, p0, acc); break;
-          case 3: vq_fast_body<W, G, 3>(rows, stride, sids, base0, pstride, p0, acc); break;
-          case 4: vq_fast_body<W, G, 4>(rows, stride, sids, base0, pstride, p0, acc); break;
-          default: vq_fast_body<W, G, 5>(rows, stride, sids, base0, pstride, p0, acc); break;
+          case 1: vq_fast_body<W, G, 1>(rows, stride, sids, base0, pstride, pg, acc); break;
+          case 2: vq_fast_body<W, G, 2>(rows, stride, sids, base0, pstride, pg, acc); break;
+          case 3: vq_fast_body<W, G, 3>(rows, stride, sids, base0, pstride, pg, acc); break;
+          case 4: vq_fast_body<W, G, 4>(rows, stride, sids, base0, pstride, pg, acc); break;
+          default: vq_fast_body<W, G, 5>(rows, stride, sids, base0, pstride, pg, acc); break;
         }
       }
       const float inv = cnt ? 1.0f / (float)cnt : 0.0f;
-      const int64_t col0 = (int64_t)p0 * W;
+      const int64_t col0 = (int64_t)pg * W;
       __nv_bfloat16* o = out + v * ld + col0;
       if (np == G && col0 + G * W <= d) {
         store_scaled<G * W>(o, acc, inv, vec_ok);
@@ -642,7 +658,7 @@ k_vq_mean8_fast(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
           if (col0 + j < d) o[j] = __float2bfloat16_rn((j & 1 ? hi2(acc[j / 2]) : lo2(acc[j / 2])) * inv);
       }
     }
-  });
+  }, tile0, tstep);
   if (!waited) bulk_wait(&s_mbar);
 }
 
@@ -1014,18 +1030,32 @@ int launch_vq(const fg_codec_desc* c, const int32_t* indptr, const int32_t* src,
   const bool lp = std::is_same<OT, __nv_bfloat16>::value && c->table_lp != nullptr && W >= 4;
   if constexpr (std::is_same<OT, __nv_bfloat16>::value && (W == 4 || W == 8)) {
     constexpr int GF = 32 / W;
-    const int64_t fast_smem =
-        (((book_bytes / 2) + (int64_t)(GF - 1) * c->length * W * 2 + 15) & ~15ll) +
-        stage_bytes;
-    if (lp && fast_smem <= 76 * 1024) {  // three CTAs per SM (233 KB smem per SM)
+    constexpr int64_t kFastSmem = 76 * 1024;  // three CTAs per SM (233 KB smem per SM)
+    const int64_t part_bytes = (int64_t)c->length * W * 2;
+    const int zp = (GF - c->num_parts % GF) % GF;
+    // parts per slice: the whole codebook when it fits, else the largest
+    // multiple of GF whose slice (+ zero pad + tile stage) fits
+    int sp = c->num_parts;
+    auto smem_for = [&](int s) {
+      return ((((int64_t)s + zp) * part_bytes + 15) & ~15ll) + stage_bytes;
+    };
+    if (smem_for(sp) > kFastSmem) {
+      sp = (int)((kFastSmem - stage_bytes) / part_bytes) - zp;
+      sp = sp / GF * GF;
+    }
+    if (lp && sp >= GF) {
+      const int ns = (int)ceil_div(c->num_parts, sp);
+      const int64_t fast_smem = smem_for(sp);
       auto kern = k_vq_mean8_fast<W, GF>;
       FG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)fast_smem));
-      const int grid = (int)min64(ntiles, (int64_t)sm_count() * 3);
+      // grid: a multiple of the slice count, ~3 CTAs per SM in total
+      const int64_t per_slice = std::max<int64_t>(1, min64(ntiles, (int64_t)sm_count() * 3 / ns));
+      const int grid = (int)(per_slice * ns);
       kern<<<grid, kFastThreads, fast_smem, st>>>(c->rows, c->d, c->row_stride,
                                               (const __nv_bfloat16*)c->table_lp, c->length,
                                               c->num_parts, indptr, src, ndst, max_dst,
-                                              (__nv_bfloat16*)out, ld);
+                                              (__nv_bfloat16*)out, ld, sp, ns);
       FG_LAUNCH_CHECK();
       return FG_OK;
     }

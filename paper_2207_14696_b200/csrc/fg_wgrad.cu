@@ -3,37 +3,43 @@
 //
 // The SAGE input layer computes h = X W^T (X: [cap_src, P] aggregated input
 // features with a ones column, W: [H, P]) and the next block averages
-// relu(h) over sampled neighbours.  Its backward is
-//     dH[r]  = (h[r] > 0) * sum_{(r -> v) in block} w_rv g[v]     (rows r)
-//     dW     = dH^T X                                              ([H, P])
-// Done as two library calls (gather kernel writing dH, then a split-K GEMM)
-// the ~1e5 x H activation gradient makes a round trip through HBM and the
-// GEMM re-reads it: ~270 MB of traffic at products shape.  Here dH tiles are
-// built in shared memory straight from the gather and fed to tcgen05.mma as
-// the A operand; X tiles stream in by cp.async as the B operand; dW
-// accumulates in TMEM across all tiles of a persistent CTA.  dH never
-// exists in HBM.  Partial dW per CTA goes to a scratch slab that a second
-// kernel reduces in fixed CTA order (deterministic).
+// relu(h) over sampled neighbours: a[v] = (1/cnt_v) sum_{e in v} relu(h[l_e]).
+// Its weight gradient is
+//     dW = sum_r dH[r]^T X[r],  dH[r] = relu'(h[r]) * sum_{e: l_e = r} g[v_e] / cnt_{v_e}
+// and, because the ReLU mask is a per-row diagonal scaling, equally
+//     dW = sum_e  A_e^T X[l_e],   A_e = bf16( relu'(h[l_e]) * g[v_e] / cnt_{v_e} )
+// a GEMM whose K dimension is the block's sampled EDGES.  Tiling K by edges
+// (128 per tile) gives every tile identical work -- no per-row edge loops,
+// so hub sources (thousands of incoming edges) cannot stall a CTA -- and it
+// needs no transposed CSR.  A tiles are built in shared memory from the
+// gathers (two 16-byte loads per lane per edge, all in flight together) and
+// fed to tcgen05.mma; X rows stream in by cp.async as B; dW accumulates in
+// TMEM across the persistent CTA's tiles.  Neither dH nor the per-edge
+// products ever reach HBM.  Per-CTA partials are reduced in fixed order
+// (deterministic).
 //
 // Operand layouts (no swizzle, "MN-major" canonical core-matrix layout: a
 // core matrix is 8 K-rows x 16 bytes of 8 consecutive MN elements):
-//   A = dH^T  [M = H features][K = 128 rows]: core (mb, kb) at (kb*H/8 + mb)*128
-//   B = X     [K = 128 rows][N = P cols]:     core (nb, kb) at (kb*P/8 + nb)*128
-// so K-adjacent cores are H/8*128 (A) / P/8*128 (B) bytes apart (LBO) and
-// MN-adjacent cores 128 bytes apart (SBO).
+//   A = [M = H features][K = 128 edges]: core (mb, kb) at (kb*H/8 + mb)*144
+//     (cores padded to 144 B so per-lane core stores are bank-conflict free)
+//   B = X [K = 128 edges][N = P cols]:   core (nb, kb) at (kb*P/8 + nb)*128
+// so K-adjacent cores are H/8*144 (A) / P/8*128 (B) bytes apart (LBO) and
+// MN-adjacent cores 144 (A) / 128 (B) bytes apart (SBO).
 //
 // The reference has no trainer (the GraphSAGE model is
 // new in this build); the aggregation being differentiated is its
 // row-stochastic neighbour mean (reference/pkg/src/featgrind/factors.py:108-114).
-// Numerics: dH is rounded to bf16 before the MMA (as the bf16 autograd path
-// it replaces does), accumulation is fp32 in TMEM.
+// Numerics: each edge term is rounded to bf16 before the MMA (the unfused
+// bf16 autograd path rounds the per-row sums instead), accumulation is fp32
+// in TMEM.
 #include "fg_common.cuh"
 
 namespace fg {
 
 constexpr int kWgThreads = 512;
-constexpr int kWgKT = 128;        // source rows per tile (MMA K extent)
-constexpr int kWgEdgeCap = 2048;  // transposed edges staged per tile
+constexpr int kWgKT = 128;        // edges per tile (MMA K extent)
+constexpr int kWin = 256;         // indptr window per tile (dsts spanned by its edges)
+constexpr int kCoreA = 144;       // A core-matrix pitch: 128 B + 16 B bank-rotation pad
 
 __device__ __forceinline__ uint32_t wg_smem(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -100,28 +106,46 @@ __device__ __forceinline__ uint4 f32_bf16x8(const float* f) {
   return make_uint4(w[0], w[1], w[2], w[3]);
 }
 
+// last v in [lo, hi) with indptr[v] <= e (indptr[lo] <= e): a 32-ary search
+// by one warp, ~log32(n_dst) rounds of coalesced L2 loads.
+__device__ __forceinline__ int64_t warp_find_dst(const int32_t* __restrict__ indptr, int64_t lo,
+                                                 int64_t hi, int64_t e, int lane) {
+  while (hi - lo > 1) {
+    const int64_t step = (hi - lo + 31) / 32;
+    const int64_t p = lo + lane * step;
+    const bool ok = p < hi && (int64_t)__ldg(indptr + p) <= e;
+    const unsigned m = __ballot_sync(0xFFFFFFFFu, ok);
+    lo += (int64_t)(31 - __clz(m)) * step;
+    hi = min64(hi, lo + step);
+  }
+  return lo;
+}
+
 // One persistent CTA per SM.  H in {128, 256}; P % 16 == 0, P <= 256;
 // (H / 128) * P <= 512 TMEM columns.
 __global__ void __launch_bounds__(kWgThreads, 1)
 k_block_mean_wgrad(const uint16_t* __restrict__ g, int64_t g_ld,
-                   const int32_t* __restrict__ t_indptr, const int32_t* __restrict__ t_dst,
-                   const float* __restrict__ t_w, const int64_t* __restrict__ nsrc_dev,
-                   int64_t cap_src, const uint16_t* __restrict__ hmask, int H,
+                   const int32_t* __restrict__ indptr, const int64_t* __restrict__ ndst_dev,
+                   int64_t max_dst, const int32_t* __restrict__ local,
+                   const uint16_t* __restrict__ hmask, int H,
                    const uint16_t* __restrict__ x, int P, float* __restrict__ partial,
                    uint32_t tmem_cols) {
   extern __shared__ __align__(1024) uint8_t wg_mem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int a_bytes = H * kWgKT * 2, b_bytes = kWgKT * P * 2;
+  const int a_bytes = (H / 8) * (kWgKT / 8) * kCoreA, b_bytes = kWgKT * P * 2;
   uint8_t* sA[2] = {wg_mem, wg_mem + a_bytes};
   uint8_t* sB[2] = {wg_mem + 2 * a_bytes, wg_mem + 2 * a_bytes + b_bytes};
-  int32_t* s_ip = reinterpret_cast<int32_t*>(wg_mem + 2 * a_bytes + 2 * b_bytes);  // [KT + 1]
-  int32_t* s_dst = s_ip + kWgKT + 4;                                                  // [EdgeCap]
-  float* s_w = reinterpret_cast<float*>(s_dst + kWgEdgeCap);                         // [EdgeCap]
-  uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_w + kWgEdgeCap);                  // [3]
+  int32_t* s_l = reinterpret_cast<int32_t*>(wg_mem + 2 * a_bytes + 2 * b_bytes);  // [KT]
+  int32_t* s_v = s_l + kWgKT;                                                     // [KT]
+  float* s_w = reinterpret_cast<float*>(s_v + kWgKT);                             // [KT]
+  int32_t* s_win = reinterpret_cast<int32_t*>(s_w + kWgKT);                       // [Win + 1]
+  int64_t* s_vw = reinterpret_cast<int64_t*>(s_win + kWin + 1 + 1);               // [1] (8-B aligned)
+  uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_vw + 1);                        // [3]
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(s_bar + 3);
 
-  const int64_t live = min64(*nsrc_dev, cap_src);
-  const int64_t ntiles = (live + kWgKT - 1) / kWgKT;
+  const int64_t live_dst = min64(*ndst_dev, max_dst);
+  const int64_t nedges = live_dst > 0 ? (int64_t)indptr[live_dst] : 0;
+  const int64_t ntiles = (nedges + kWgKT - 1) / kWgKT;
   const int64_t G = gridDim.x;
 
   if (warp == 0) {
@@ -141,19 +165,73 @@ k_block_mean_wgrad(const uint16_t* __restrict__ g, int64_t g_ld,
   const uint32_t tmem = *s_tmem;
 
   const int HB = H >> 3, PB = P >> 3;  // 16-byte chunks per row
-  const uint32_t a_lbo = (uint32_t)HB * 128, b_lbo = (uint32_t)PB * 128;
+  const uint32_t a_lbo = (uint32_t)HB * kCoreA, b_lbo = (uint32_t)PB * 128;
   const uint32_t idesc = umma_idesc_bf16_mn(P);
   uint32_t phase = 0;
   int64_t k = 0;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += G, ++k) {
+  // CTA b owns the contiguous tile range [T*b/G, T*(b+1)/G), so the dst of
+  // its edges only moves forward: each tile resolves v_e inside a window of
+  // kWin+1 indptr entries starting at the dst of its first edge.  Warp 0
+  // finds the next tile's window start and loads that window (registers)
+  // while the current tile builds; every thread < 128 does the same for the
+  // next tile's source ids.
+  const int64_t t_lo = ntiles * blockIdx.x / G, t_hi = ntiles * (blockIdx.x + 1) / G;
+  constexpr int kWinPer = (kWin + 1 + 31) / 32;
+  int32_t pl = -1;
+  int32_t pwin[kWinPer];
+  int64_t pvw = 0;
+  auto load_next = [&](int64_t tile, int64_t vw) {  // vw: dst of the tile's first edge
+    if (tid < kWgKT) {
+      const int64_t e = tile * kWgKT + tid;
+      pl = e < nedges ? __ldg(local + e) : -1;
+    }
+    if (warp == 0) {
+      pvw = vw;
+#pragma unroll
+      for (int u = 0; u < kWinPer; ++u) {
+        const int64_t v = vw + lane + 32 * u;
+        pwin[u] = v <= live_dst ? __ldg(indptr + v) : INT32_MAX;
+      }
+    }
+  };
+  if (t_lo < t_hi && warp == 0)
+    load_next(t_lo, warp_find_dst(indptr, 0, live_dst, t_lo * kWgKT, lane));
+  if (t_lo < t_hi && tid < kWgKT && warp != 0) load_next(t_lo, 0);
+  for (int64_t tile = t_lo; tile < t_hi; ++tile, ++k) {
     const int s = (int)(k & 1);
     if (k >= 2) {  // MMAs of tile k-2 have finished reading buffer s
       wg_bar_wait(s_bar + s, (phase >> s) & 1u);
       phase ^= 1u << s;
     }
-    const int64_t r0 = tile * kWgKT;
-    // ---- B = X tile by cp.async (rows past `live` read row 0 of a zero pad:
-    // they are multiplied by zero dH rows, but must be finite -> zero-fill)
+    if (tid < kWgKT) s_l[tid] = pl;
+    if (warp == 0) {
+#pragma unroll
+      for (int u = 0; u < kWinPer; ++u)
+        if (lane + 32 * u <= kWin) s_win[lane + 32 * u] = pwin[u];
+      if (lane == 0) *s_vw = pvw;
+    }
+    __syncthreads();
+    const int64_t vw = *s_vw;
+    if (tile + 1 < t_hi) {
+      // dst of the next tile's first edge: in this window unless dsts
+      // without edges push it past the window (then a global search)
+      const int64_t en = (tile + 1) * kWgKT;
+      int64_t vn = 0;
+      if (warp == 0) {
+        if (en < (int64_t)s_win[kWin]) {
+          int lo = 0, hi = kWin;  // last j with s_win[j] <= en
+          while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if ((int64_t)s_win[mid] <= en) lo = mid; else hi = mid;
+          }
+          vn = vw + lo;
+        } else {
+          vn = warp_find_dst(indptr, vw, live_dst, en, lane);
+        }
+      }
+      load_next(tile + 1, warp == 0 ? vn : 0);  // lands while this tile builds
+    }
+    // ---- B = X rows of the edges' sources by cp.async (dead slots zero-fill)
     {
       const uint32_t bbase = wg_smem(sB[s]);
       for (int i = tid; i < kWgKT * PB; i += kWgThreads) {
@@ -161,86 +239,93 @@ k_block_mean_wgrad(const uint16_t* __restrict__ g, int64_t g_ld,
         const int nb = q % PB, kb = q / PB;
         const int r = kb * 8 + rr;
         const uint32_t dst = bbase + (uint32_t)((kb * PB + nb) * 128 + rr * 16);
-        const int64_t gr = r0 + r;
-        const int bytes = gr < live ? 16 : 0;  // src-size 0 -> zero fill
-        const uint16_t* src = x + (gr < live ? gr : 0) * (int64_t)P + nb * 8;
+        const int32_t l = s_l[r];
+        const int bytes = l >= 0 ? 16 : 0;  // src-size 0 -> zero fill
+        const uint16_t* src = x + (int64_t)(l >= 0 ? l : 0) * P + nb * 8;
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;"
                      ::"r"(dst), "l"(src), "r"(bytes) : "memory");
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
     }
-    // ---- transposed CSR slice of this tile
-    if (tid <= kWgKT) s_ip[tid] = t_indptr[min64(r0 + tid, live)];
-    __syncthreads();
-    const int32_t ebase = s_ip[0];
-    const int32_t ne = s_ip[kWgKT] - ebase;
-    const bool staged = ne <= kWgEdgeCap;
-    if (staged)
-      for (int i = tid; i < ne; i += kWgThreads) {
-        s_dst[i] = t_dst[ebase + i];
-        s_w[i] = t_w[ebase + i];
-      }
-    __syncthreads();
-    // ---- A = dH^T tile: item = (row r, 8-feature chunk c); a warp covers
-    // 8 rows x 4 chunks so its 16-byte smem stores hit distinct banks
+    // ---- A: warp -> core-matrix K group kb (8 edges); lane -> 8-feature
+    // chunk (H = 256; for H = 128 half-warps take kb = 2w, 2w+1).  All 16
+    // gathers of the group (g row of the dst, mask row of the source) are
+    // issued before any is consumed.  The lane's 8 x 16 B result is one core
+    // matrix; the 144-byte core pitch spreads a store wavefront over all banks.
     {
       const uint32_t abase = wg_smem(sA[s]);
-      const int groups = (kWgKT / 8) * (HB / 4);  // warp items per tile
-      for (int wi = warp; wi < groups; wi += kWgThreads / 32) {
-        const int rg = wi / (HB / 4), cg = wi - rg * (HB / 4);
-        const int r = rg * 8 + (lane & 7);
-        const int c = cg * 4 + (lane >> 3);
-        const int64_t gr = r0 + r;
-        float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        if (gr < live) {
-          uint4 mq = make_uint4(0u, 0u, 0u, 0u);
-          if (hmask) mq = __ldg(reinterpret_cast<const uint4*>(hmask + gr * H) + c);
-          const int32_t e0 = s_ip[r] - ebase, e1 = s_ip[r + 1] - ebase;
-          for (int32_t e = e0; e < e1; e += 2) {
-            int32_t v0, v1 = 0;
-            float w0, w1 = 0.f;
-            if (staged) { v0 = s_dst[e]; w0 = s_w[e]; } else { v0 = t_dst[ebase + e]; w0 = t_w[ebase + e]; }
-            const bool two = e + 1 < e1;
-            if (two) {
-              if (staged) { v1 = s_dst[e + 1]; w1 = s_w[e + 1]; }
-              else { v1 = t_dst[ebase + e + 1]; w1 = t_w[ebase + e + 1]; }
+      const int sub = lane / HB;
+      const int c = lane - sub * HB;
+      const int gpw = 32 / HB;
+      for (int kb = warp * gpw + sub; kb < kWgKT / 8; kb += (kWgThreads / 32) * gpw) {
+        if (c < 8) {  // resolve dst + weight of the group's 8 edges
+          const int r = kb * 8 + c;
+          const int64_t e = tile * kWgKT + r;
+          int32_t v = 0;
+          float wt = 0.f;
+          if (s_l[r] >= 0) {
+            int64_t vv;
+            if (e < (int64_t)s_win[kWin]) {
+              int lo = 0, hi = kWin;
+              while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if ((int64_t)s_win[mid] <= e) lo = mid; else hi = mid;
+              }
+              vv = vw + lo;
+              wt = 1.0f / (float)(s_win[lo + 1] - s_win[lo]);
+            } else {  // past the window (dsts without edges): serial search
+              int64_t lo = vw, hi = live_dst;
+              while (hi - lo > 1) {
+                const int64_t mid = (lo + hi) >> 1;
+                if ((int64_t)__ldg(indptr + mid) <= e) lo = mid; else hi = mid;
+              }
+              vv = lo;
+              wt = 1.0f / (float)(__ldg(indptr + lo + 1) - __ldg(indptr + lo));
             }
-            const uint4 q0 = __ldg(reinterpret_cast<const uint4*>(g + (int64_t)v0 * g_ld) + c);
-            uint4 q1 = make_uint4(0u, 0u, 0u, 0u);
-            if (two) q1 = __ldg(reinterpret_cast<const uint4*>(g + (int64_t)v1 * g_ld) + c);
-            float f[8];
-            bf16x8_f32(q0, f);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) acc[j] = fmaf(f[j], w0, acc[j]);
-            if (two) {
-              bf16x8_f32(q1, f);
-#pragma unroll
-              for (int j = 0; j < 8; ++j) acc[j] = fmaf(f[j], w1, acc[j]);
-            }
+            v = (int32_t)vv;
           }
-          if (hmask) {
-            float m[8];
-            bf16x8_f32(mq, m);
+          s_v[r] = v;
+          s_w[r] = wt;
+        }
+        __syncwarp();
+        uint4 q[8], m[8];
+        float w[8];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) acc[j] = m[j] > 0.f ? acc[j] : 0.f;
+        for (int rr = 0; rr < 8; ++rr) {
+          const int r = kb * 8 + rr;
+          const int32_t l = s_l[r];
+          w[rr] = s_w[r];
+          q[rr] = make_uint4(0u, 0u, 0u, 0u);
+          m[rr] = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);  // 1.0
+          if (l >= 0) {
+            q[rr] = __ldg(reinterpret_cast<const uint4*>(g + (int64_t)s_v[r] * g_ld) + c);
+            if (hmask) m[rr] = __ldg(reinterpret_cast<const uint4*>(hmask + (int64_t)l * H) + c);
           }
         }
-        const uint4 o = f32_bf16x8(acc);
-        const uint32_t dst = abase + (uint32_t)(((r >> 3) * HB + c) * 128 + (r & 7) * 16);
-        asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};"
-                     ::"r"(dst), "r"(o.x), "r"(o.y), "r"(o.z), "r"(o.w) : "memory");
+        const uint32_t core = abase + (uint32_t)((kb * HB + c) * kCoreA);
+#pragma unroll
+        for (int rr = 0; rr < 8; ++rr) {
+          float f[8], mm[8], o8[8];
+          bf16x8_f32(q[rr], f);
+          bf16x8_f32(m[rr], mm);
+#pragma unroll
+          for (int t = 0; t < 8; ++t) o8[t] = mm[t] > 0.f ? f[t] * w[rr] : 0.f;
+          const uint4 o = f32_bf16x8(o8);
+          asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};"
+                       ::"r"(core + rr * 16), "r"(o.x), "r"(o.y), "r"(o.z), "r"(o.w) : "memory");
+        }
       }
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
-    // ---- MMA issue (one thread): dW[half] += A[half] . B over K = 128 rows
+    // ---- MMA issue (one thread): dW[half] += A[half] . B over K = 128 edges
     if (tid == 0) {
       asm volatile("tcgen05.fence::after_thread_sync;");
       const uint32_t abase = wg_smem(sA[s]), bbase = wg_smem(sB[s]);
       for (int half = 0; half < H / 128; ++half) {
         for (int ks = 0; ks < kWgKT / 16; ++ks) {
-          const uint64_t ad = umma_desc(abase + half * 16 * 128 + ks * 2 * a_lbo, a_lbo, 128);
+          const uint64_t ad = umma_desc(abase + half * 16 * kCoreA + ks * 2 * a_lbo, a_lbo, kCoreA);
           const uint64_t bd = umma_desc(bbase + ks * 2 * b_lbo, b_lbo, 128);
           umma_bf16(tmem + (uint32_t)(half * P), ad, bd, idesc, (k > 0 || ks > 0) ? 1u : 0u);
         }
@@ -296,27 +381,64 @@ k_block_mean_wgrad(const uint16_t* __restrict__ g, int64_t g_ld,
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tmem_cols));
 }
 
-// dw[i] = sum_b partial[b][i] in CTA order (deterministic).
-__global__ void k_wgrad_reduce(const float* __restrict__ partial, int nb, int64_t n,
-                               float* __restrict__ dw) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+// dw[i] = sum_b partial[b][i] in CTA order (deterministic), two passes:
+// segment j of kRedSeg sums partials [j*nb/S, (j+1)*nb/S) in order (float4
+// columns, loads issued 8 ahead), then one pass sums the S segment results
+// in order.  ~17 MB of partials (148 x 256 x 112 fp32) stream at HBM rate
+// instead of one 148-deep dependent chain per output.
+constexpr int kRedSeg = 8;
+
+__global__ void k_wgrad_reduce_seg(const float4* __restrict__ partial, int nb, int64_t n4,
+                                   float4* __restrict__ seg) {
+  const int j = blockIdx.y;
+  const int b0 = (int)((int64_t)nb * j / kRedSeg), b1 = (int)((int64_t)nb * (j + 1) / kRedSeg);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
        i += (int64_t)gridDim.x * blockDim.x) {
-    float s = 0.f;
-    for (int b = 0; b < nb; ++b) s += partial[(int64_t)b * n + i];
-    dw[i] = s;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    int b = b0;
+    for (; b + 8 <= b1; b += 8) {
+      float4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldcs(partial + (int64_t)(b + u) * n4 + i);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        acc.x += v[u].x; acc.y += v[u].y; acc.z += v[u].z; acc.w += v[u].w;
+      }
+    }
+    for (; b < b1; ++b) {
+      const float4 v = __ldcs(partial + (int64_t)b * n4 + i);
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+    seg[(int64_t)j * n4 + i] = acc;
+  }
+}
+
+__global__ void k_wgrad_reduce_fin(const float4* __restrict__ seg, int64_t n4,
+                                   float4* __restrict__ dw) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float4 acc = seg[i];
+#pragma unroll
+    for (int j = 1; j < kRedSeg; ++j) {
+      const float4 v = seg[(int64_t)j * n4 + i];
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+    dw[i] = acc;
   }
 }
 
 static int wgrad_smem_bytes(int H, int P) {
-  return 2 * H * kWgKT * 2 + 2 * kWgKT * P * 2 + (kWgKT + 4) * 4 + kWgEdgeCap * 8 + 3 * 8 + 16;
+  return 2 * (H / 8) * (kWgKT / 8) * kCoreA + 2 * kWgKT * P * 2 + 3 * kWgKT * 4 +
+         (kWin + 2) * 4 + 8 + 3 * 8 + 16;
 }
 
 }  // namespace fg
 
 using namespace fg;
 
+// scratch = [nb][H][P] fp32 partials | [kRedSeg][H][P] segment sums
 extern "C" int64_t fg_block_mean_wgrad_scratch_bytes(int64_t H, int64_t P) {
-  return (int64_t)sm_count() * H * P * 4;
+  return ((int64_t)sm_count() + kRedSeg) * H * P * 4;
 }
 
 extern "C" int fg_block_mean_wgrad_supported(int64_t H, int64_t P) {
@@ -326,27 +448,36 @@ extern "C" int fg_block_mean_wgrad_supported(int64_t H, int64_t P) {
   return wgrad_smem_bytes((int)H, (int)P) <= 227 * 1024 ? 1 : 0;
 }
 
-extern "C" int fg_block_mean_wgrad(const uint16_t* g, int64_t g_ld, const int32_t* t_indptr,
-                                   const int32_t* t_dst, const float* t_w,
-                                   const int64_t* n_src_dev, int64_t cap_src,
-                                   const uint16_t* h_mask, int64_t H, const uint16_t* x,
-                                   int64_t P, float* dw, float* scratch, int64_t scratch_bytes,
-                                   void* s) {
+extern "C" int fg_block_mean_wgrad(const uint16_t* g, int64_t g_ld, const int32_t* indptr,
+                                   const int32_t* local, const int64_t* n_dst_dev,
+                                   int64_t max_dst, const uint16_t* h_mask, int64_t H,
+                                   const uint16_t* x, int64_t P, float* dw, float* scratch,
+                                   int64_t scratch_bytes, void* s) {
+  FG_CHECK_ARG(g != nullptr && indptr != nullptr && local != nullptr && n_dst_dev != nullptr &&
+                   x != nullptr && dw != nullptr && scratch != nullptr,
+               "null argument");
   FG_CHECK_ARG(fg_block_mean_wgrad_supported(H, P), "unsupported shape H=%lld P=%lld",
                (long long)H, (long long)P);
   FG_CHECK_ARG(g_ld >= H && g_ld % 8 == 0, "bad g_ld");
   const int nb = sm_count();
-  FG_CHECK_ARG(scratch_bytes >= (int64_t)nb * H * P * 4, "scratch too small");
+  FG_CHECK_ARG(scratch_bytes >= fg_block_mean_wgrad_scratch_bytes(H, P), "scratch too small");
+  cudaStream_t st = as_stream(s);
+  float* seg_f = scratch + (int64_t)nb * H * P;
   const int smem = wgrad_smem_bytes((int)H, (int)P);
   FG_CUDA_TRY(cudaFuncSetAttribute(k_block_mean_wgrad, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    smem));
   uint32_t cols = 32;
   while (cols < (uint32_t)((H / 128) * P)) cols <<= 1;
-  k_block_mean_wgrad<<<nb, kWgThreads, smem, as_stream(s)>>>(
-      g, g_ld, t_indptr, t_dst, t_w, n_src_dev, cap_src, h_mask, (int)H, x, (int)P, scratch, cols);
+  k_block_mean_wgrad<<<nb, kWgThreads, smem, st>>>(g, g_ld, indptr, n_dst_dev, max_dst, local,
+                                                   h_mask, (int)H, x, (int)P, scratch, cols);
   FG_LAUNCH_CHECK();
-  const int64_t n = H * P;
-  k_wgrad_reduce<<<grid_for(n, 256), 256, 0, as_stream(s)>>>(scratch, nb, n, dw);
+  const int64_t n4 = H * P / 4;  // P % 16 == 0
+  float4* seg = reinterpret_cast<float4*>(seg_f);
+  const dim3 rg((unsigned)((n4 + 255) / 256), kRedSeg);
+  k_wgrad_reduce_seg<<<rg, 256, 0, st>>>(reinterpret_cast<const float4*>(scratch), nb, n4, seg);
+  FG_LAUNCH_CHECK();
+  k_wgrad_reduce_fin<<<(unsigned)((n4 + 255) / 256), 256, 0, st>>>(
+      seg, n4, reinterpret_cast<float4*>(dw));
   FG_LAUNCH_CHECK();
   return FG_OK;
 }

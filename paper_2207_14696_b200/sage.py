@@ -27,7 +27,9 @@ import torch.nn as nn
 import torch.nn.functional as F
 
 from . import ddp
-from .aggregate import alloc_aggregate, block_mean, gather_dequant_mean, padded_dim, softmax_ce
+from . import _native as N
+from .aggregate import (alloc_aggregate, block_mean, gather_dequant_mean, input_block_mean,
+                        padded_dim, softmax_ce, wgrad_scratch, wgrad_supported)
 from .sampler import DeviceSampler
 
 
@@ -56,13 +58,30 @@ class SageModel(nn.Module):
             lins.append(lin)
         self.lins = nn.ModuleList(lins)
         self.dropout = dropout
+        self.fuse_input = True
 
-    def forward(self, agg_in, sb, caps):
+    def fused_input_ok(self) -> bool:
+        """Input layer + first hidden block mean through ``input_block_mean``
+        (backward = edge-tiled tcgen05 dW, fg_wgrad.cu) when there is a hidden
+        block, no dropout, and the shape is one the kernel takes."""
+        w = self.lins[0].weight
+        return (self.fuse_input and len(self.lins) > 1 and not self.dropout
+                and wgrad_supported(w.shape[0], w.shape[1]))
+
+    def forward(self, agg_in, sb, caps, wgrad_scratch=None):
         """agg_in: [caps[L-1], pitch] mean of decoded inputs over the last
         block (+ ones column); sb: SampledBatch; returns logits [caps[0], C]."""
         L = len(self.lins)
-        h = self.lins[0](agg_in)
-        for i in range(1, L):
+        first = 1
+        if self.training and self.fused_input_ok():
+            l = L - 2
+            h = input_block_mean(agg_in, self.lins[0].weight, sb.indptr[l], sb.local[l],
+                                 sb.n_nodes[l], caps[l], True, wgrad_scratch)
+            h = self.lins[1](h)
+            first = 2
+        else:
+            h = self.lins[0](agg_in)
+        for i in range(first, L):
             l = L - 1 - i  # block index feeding this layer
             trans = sb.trans[l] if sb.trans else None
             if self.dropout and self.training:
@@ -129,13 +148,16 @@ class SageTrainer:
         self.pg = process_group
         self.world = torch.distributed.get_world_size(process_group) if process_group else 1
         torch.manual_seed(cfg.seed)
-        self.sampler = DeviceSampler(graph, cfg.fanouts, cfg.batch_size, need_local=True,
-                                     need_transpose=True)
-        self.caps = self.sampler.caps
         L = len(cfg.fanouts)
         # input layer sees the 16-aligned padded aggregate (zero columns past d)
         self.model = SageModel(codec.d, cfg.hidden, num_classes, L, cfg.dropout,
                                in_pitch=padded_dim(codec.d)).to(self.device)
+        # the fused input layer needs no transpose of its block (block L-2)
+        fused = self.model.fused_input_ok()
+        self.sampler = DeviceSampler(graph, cfg.fanouts, cfg.batch_size, need_local=True,
+                                     need_transpose=True,
+                                     transpose_layers=range(L - 2) if fused else None)
+        self.caps = self.sampler.caps
         # flat gradient buffer: one all-reduce per step
         # one flat fp32 buffer each for params, grads and Adam moments: a
         # single all-reduce and a single optimizer kernel per step
@@ -155,6 +177,10 @@ class SageTrainer:
         self.opt = FlatAdam(self.flat_param, self.flat_grad, lr=cfg.lr)
         self.loss_buf = torch.zeros((), dtype=torch.float32, device=self.device)
         self.agg = alloc_aggregate(self.caps[L - 1], codec.d, cfg.agg_dtype, self.device)
+        w0 = self.model.lins[0].weight
+        self.wgrad_scratch = None
+        if fused:
+            self.wgrad_scratch = wgrad_scratch(w0.shape[0], w0.shape[1], self.device)
         self.graph = None
         self.steps_run = 0
 
@@ -165,7 +191,7 @@ class SageTrainer:
         gather_dequant_mean(self.codec, sb.indptr[L - 1], sb.picks[L - 1], sb.n_nodes[L - 1],
                             self.caps[L - 1], out=self.agg)
         with torch.autocast("cuda", dtype=torch.bfloat16):
-            logits = self.model(self.agg, sb, self.caps)
+            logits = self.model(self.agg, sb, self.caps, self.wgrad_scratch)
         loss = softmax_ce(logits, self.labels, sb.nodes[0], sb.n_nodes[0])
         self.flat_grad.zero_()
         loss.backward()

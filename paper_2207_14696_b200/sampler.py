@@ -110,7 +110,8 @@ class DeviceSampler:
 
     def __init__(self, graph: DeviceGraph, fanouts, batch_size: int, *,
                  need_local: bool = True, want_frontier: bool = False,
-                 unique_last: bool = False, need_transpose: bool = False):
+                 unique_last: bool = False, need_transpose: bool = False,
+                 transpose_layers=None):
         import torch
         N.require_cuda()
         self.g = graph
@@ -140,13 +141,16 @@ class DeviceSampler:
         self.n_picks = [z(1, dt=i64) for _ in range(L)]
         self.local = [z(pcaps[l]) if (need_local and l < L - 1) else None for l in range(L)]
         # per hidden block: transpose (source rank -> edges) for the gather bwd
+        # (``transpose_layers`` limits it to some hidden blocks; default all)
         self.need_transpose = need_transpose and need_local
+        self.t_layers = set(range(L - 1) if transpose_layers is None else transpose_layers)
         self.t_indptr, self.t_dst, self.t_w = [], [], []
         if self.need_transpose:
             for l in range(L - 1):
-                self.t_indptr.append(z(caps[l + 1] + 1))
-                self.t_dst.append(z(pcaps[l]))
-                self.t_w.append(z(pcaps[l], dt=torch.float32))
+                on = l in self.t_layers
+                self.t_indptr.append(z(caps[l + 1] + 1) if on else None)
+                self.t_dst.append(z(pcaps[l]) if on else None)
+                self.t_w.append(z(pcaps[l], dt=torch.float32) if on else None)
             nbytes = N.lib().fg_block_transpose_scratch_bytes(max(caps[1:]))
             self.t_scratch = torch.zeros(nbytes, dtype=torch.uint8, device=dev)
         words = (n + 31) // 32
@@ -236,7 +240,7 @@ class DeviceSampler:
                 if self.local[l] is not None:
                     N.call("fg_bitmap_rank", N.ptr(self.picks[l]), N.ptr(self.n_picks[l]),
                            self.pcaps[l], bm, wp, N.ptr(self.local[l]), s)
-                    if self.need_transpose:
+                    if self.need_transpose and l in self.t_layers:
                         self._transpose(l, s)
                 N.call("fg_bitmap_clear", N.ptr(self.nodes[l + 1]), N.ptr(self.n_nodes[l + 1]),
                        self.caps[l + 1], bm, s)
@@ -244,7 +248,7 @@ class DeviceSampler:
                            self.local)
         if self.need_transpose:
             out.trans = [(self.t_indptr[l], self.t_dst[l], self.t_w[l], self.n_nodes[l + 1])
-                         for l in range(L - 1)] + [None]
+                         if l in self.t_layers else None for l in range(L - 1)] + [None]
         if self.want_frontier:
             N.call("fg_bitmap_compact", N.ptr(self.fbitmap), n, N.ptr(self.frontier), self.fcap,
                    N.ptr(self.n_frontier), None, N.ptr(self.ws_fbm), self.ws_fbm.numel(), s)
@@ -252,6 +256,22 @@ class DeviceSampler:
                    N.ptr(self.fbitmap), s)
             out.frontier, out.n_frontier = self.frontier, self.n_frontier
         return out
+
+    def _transpose_on(self, l: int) -> None:
+        """Allocate block l's transpose buffers (for a sampler built without
+        them; tests use this to run both backward forms on one batch)."""
+        import torch
+        if self.t_indptr[l] is None:
+            dev = self.device
+            self.t_indptr[l] = torch.zeros(self.caps[l + 1] + 1, dtype=torch.int32, device=dev)
+            self.t_dst[l] = torch.zeros(self.pcaps[l], dtype=torch.int32, device=dev)
+            self.t_w[l] = torch.zeros(self.pcaps[l], dtype=torch.float32, device=dev)
+            if not hasattr(self, "t_scratch"):
+                nbytes = N.lib().fg_block_transpose_scratch_bytes(max(self.caps[1:]))
+                self.t_scratch = torch.zeros(nbytes, dtype=torch.uint8, device=dev)
+
+    def block_trans(self, l: int):
+        return (self.t_indptr[l], self.t_dst[l], self.t_w[l], self.n_nodes[l + 1])
 
     def _transpose(self, l: int, s) -> None:
         """Block l's transpose (source rank -> dst of each incoming edge) for

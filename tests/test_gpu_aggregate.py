@@ -75,7 +75,8 @@ def _vq_codec(n, d, w, L, rng, metric="cosine"):
 
 @pytest.mark.parametrize("w,L,d", [(4, 256, 100), (8, 256, 100), (8, 256, 128), (16, 2048, 96),
                                    (2, 16, 10), (1, 4, 5), (1, 256, 70), (2, 256, 33),
-                                   (16, 256, 40), (8, 256, 768), (4, 300, 30)])
+                                   (16, 256, 40), (8, 256, 768), (4, 300, 30),
+                                   (4, 256, 402), (8, 256, 260)])
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
 def test_fused_vq_mean(w, L, d, dtype):
     rng = np.random.default_rng(w * 1000 + L + d)
@@ -233,46 +234,61 @@ def test_fused_softmax_ce_matches_torch(dtype):
     assert (logits.grad[nv:] == 0).all()
 
 
-# (128, 48, True, 40, 290): ~50 transposed edges per source row, so a tile's
-# edge slice overflows the shared-memory stage (direct-load path)
+# fan 40 over 290 sources: ~100 edges per source row (hub rows); n_src 100:
+# fewer edges than one 128-edge tile per CTA
 @pytest.mark.parametrize("H,P,relu,fan,n_src", [(256, 112, True, 10, 2900), (256, 144, True, 5, 2900),
                                                 (128, 64, False, 15, 2900), (256, 160, True, 3, 2900),
-                                                (128, 48, True, 40, 290), (256, 112, True, 10, 100)])
+                                                (128, 48, True, 40, 290), (256, 112, True, 10, 100),
+                                                (128, 80, True, 10, 2900), (256, 16, True, 2, 50),
+                                                (256, 112, True, -3, 2900)])
 def test_block_mean_wgrad_tcgen05(H, P, relu, fan, n_src):
-    """Fused dH gather + tcgen05 dW against torch fp32 on the same bf16 dH."""
+    """Edge-tiled fused tcgen05 dW against torch fp32 on the same bf16
+    per-edge terms."""
     from paper_2207_14696_b200.aggregate import block_mean_wgrad, wgrad_supported
     assert wgrad_supported(H, P)
-    rng = np.random.default_rng(H + P + fan)
+    rng = np.random.default_rng(H + P + abs(fan))
     cap_src, n_dst, max_dst = n_src + 200, 700, 760
-    counts, indptr, src = _block(n_src, n_dst, max_dst, fan, rng)
-    ti, td, tw = _transpose_np(indptr, src, n_dst, n_src)
+    # fan < 0: 97 % of destinations without edges, so one 128-edge tile spans
+    # more destinations than the kernel's indptr window (slow-path search)
+    zf = 0.97 if fan < 0 else 0.1
+    fan = abs(fan)
+    if zf > 0.5:
+        n_dst, max_dst = 20000, 20100
+    counts, indptr, src = _block(n_src, n_dst, max_dst, fan, rng, zero_frac=zf)
     dev = "cuda"
-    t_indptr = torch.zeros(cap_src + 1, dtype=torch.int32, device=dev)
-    t_indptr[:n_src + 1] = torch.from_numpy(ti).to(dev)
-    t_indptr[n_src + 1:] = int(ti[-1])
-    trans = (t_indptr, torch.from_numpy(td).to(dev), torch.from_numpy(tw).to(dev),
-             torch.tensor([n_src], device=dev))
+    ip = torch.from_numpy(indptr).to(dev)
+    local = torch.full((max_dst * fan,), -7, dtype=torch.int32, device=dev)  # capacity > live
+    local[:src.size] = torch.from_numpy(src).to(dev)
     g = torch.randn(max_dst, H + 8, device=dev).to(torch.bfloat16)
     h = torch.randn(cap_src, H, device=dev).to(torch.bfloat16)
     x = torch.randn(cap_src, P, device=dev).to(torch.bfloat16)
     x[n_src:] = float("nan")  # rows past the live count must never be read
-    dw = block_mean_wgrad(g, trans, cap_src, h if relu else None, x)
+    dw = block_mean_wgrad(g, ip, local, torch.tensor([n_dst], device=dev), max_dst,
+                          h if relu else None, x, H=H)
     torch.cuda.synchronize()
-    # reference: dH from the transposed lists, bf16-rounded as in the kernel
-    dst_t = torch.from_numpy(td).long().to(dev)
-    w_t = torch.from_numpy(tw).to(dev)
-    rows = torch.repeat_interleave(torch.arange(n_src, device=dev),
-                                   torch.from_numpy(np.diff(ti)).long().to(dev))
-    dh = torch.zeros(n_src, H, device=dev).index_add_(0, rows, g[dst_t, :H].float() * w_t[:, None])
+    # reference: per-edge terms bf16-rounded as in the kernel, fp32 GEMM
+    dst = torch.repeat_interleave(torch.arange(n_dst, device=dev),
+                                  torch.from_numpy(counts).long().to(dev))
+    l = torch.from_numpy(src).long().to(dev)
+    w = 1.0 / torch.from_numpy(counts).float().to(dev)[dst]
+    term = g[dst, :H].float() * w[:, None]
     if relu:
-        dh = dh * (h[:n_src].float() > 0)
-    dh = dh.to(torch.bfloat16).float()
-    ref = dh.t() @ x[:n_src].float()
-    # dH is summed in a different order here, so an element can round to the
-    # neighbouring bf16 value (2^-8 relative); layout/indexing errors are O(1)
+        term = term * (h[l].float() > 0)
+    ref = term.to(torch.bfloat16).float().t() @ x[l].float()
     err = (dw - ref).abs().max().item()
-    assert err <= 2e-3 * ref.abs().max().item() + 1e-4, err
+    assert err <= 1e-3 * ref.abs().max().item() + 1e-4, err
     assert torch.isfinite(dw).all()
+
+
+def test_block_mean_wgrad_empty_block():
+    from paper_2207_14696_b200.aggregate import block_mean_wgrad
+    dev = "cuda"
+    ip = torch.zeros(11, dtype=torch.int32, device=dev)
+    local = torch.zeros(40, dtype=torch.int32, device=dev)
+    x = torch.randn(30, 48, device=dev).to(torch.bfloat16)
+    g = torch.randn(10, 136, device=dev).to(torch.bfloat16)
+    dw = block_mean_wgrad(g, ip, local, torch.tensor([0], device=dev), 10, None, x, H=128)
+    assert (dw == 0).all()
 
 
 def test_input_block_mean_autograd_matches_unfused():
@@ -289,12 +305,12 @@ def test_input_block_mean_autograd_matches_unfused():
     x = torch.randn(n_src, P, device=dev).to(torch.bfloat16)
     w1 = (torch.randn(H, P, device=dev) * 0.1).requires_grad_(True)
     w2 = w1.detach().clone().requires_grad_(True)
-    a1 = input_block_mean(x, w1, ip, sl, nd, max_dst, trans)
+    a1 = input_block_mean(x, w1, ip, sl, nd, max_dst)
     h2 = torch.mm(x, w2.to(torch.bfloat16).t())
     a2 = block_mean(h2, ip, sl, nd, max_dst, relu=True, trans=trans, bias_col=True)
     assert torch.equal(a1, a2)
     gout = torch.randn_like(a1.float()).to(torch.bfloat16)
     a1.backward(gout)
     a2.backward(gout)
-    scale = w2.grad.abs().max().item()
-    assert (w1.grad - w2.grad).abs().max().item() <= 2e-2 * scale
+    rel = ((w1.grad - w2.grad).norm() / w2.grad.norm()).item()
+    assert rel < 1e-2, rel

@@ -8,6 +8,8 @@ import numpy as np
 import pytest
 import torch
 
+from paper_2207_14696_b200 import _native as N
+from paper_2207_14696_b200.aggregate import gather_dequant_mean, softmax_ce
 from paper_2207_14696_b200.sage import SageTrainer, TrainConfig
 from paper_2207_14696_b200.synth import build_sq_codec, build_vq_codec, generate_graph, split_ids
 from oracle import codecs as oc
@@ -86,3 +88,46 @@ def test_vq_three_layer_training_runs():
     last = float(t.loss_buf.item())
     assert np.isfinite(last) and last < first
     t.sampler.check_errors()
+
+
+@pytest.mark.parametrize("vq", [False, True])
+def test_fused_input_layer_grads_match_unfused(vq):
+    """The trainer's fused input layer (GEMM + block mean forward, fused dH
+    gather + tcgen05 dW backward) gives the same gradients as the unfused
+    bf16 torch path on a real sampled batch."""
+    dg, labels, dc, train, val = _small_world(vq=vq, d=100 if vq else 64)
+    cfg = TrainConfig(fanouts=(15, 10, 5), batch_size=512, hidden=128, use_graph=False)
+    t = SageTrainer(dg, dc, labels, 8, cfg)
+    assert t.wgrad_scratch is not None
+    t.begin_epoch(train, 0)
+    grads = []
+    t.sampler.load_seeds(0)
+    sb = t.sampler.sample_loaded()  # one batch for both paths (the stream advances)
+    if sb.trans[1] is None:  # the fused trainer skips block 1's transpose
+        t.sampler._transpose_on(1)
+        t.sampler._transpose(1, N.stream_handle())
+        sb.trans[1] = t.sampler.block_trans(1)
+    for fused in (True, False):
+        t.model.fuse_input = fused
+        assert t.model.fused_input_ok() == fused
+        L = 3
+        gather_dequant_mean(dc, sb.indptr[L - 1], sb.picks[L - 1], sb.n_nodes[L - 1],
+                            t.caps[L - 1], out=t.agg)
+        with torch.autocast("cuda", dtype=torch.bfloat16):
+            logits = t.model(t.agg, sb, t.caps, t.wgrad_scratch)
+        loss = softmax_ce(logits, labels, sb.nodes[0], sb.n_nodes[0])
+        t.flat_grad.zero_()
+        loss.backward()
+        grads.append(t.flat_grad.clone())
+    g0, g1 = grads
+    assert torch.isfinite(g0).all()
+    # per layer: relative L2 error between the two bf16 paths (dH is summed
+    # in a different order and dW accumulates in fp32 TMEM instead of a bf16
+    # GEMM output, so single elements near cancellation can differ more)
+    off = 0
+    for lin in t.model.lins:
+        n = lin.weight.numel()
+        a, b = g0[off:off + n], g1[off:off + n]
+        rel = ((a - b).norm() / b.norm()).item()
+        assert rel < 1e-2, (off, rel)
+        off += n
