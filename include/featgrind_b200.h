@@ -257,11 +257,16 @@ int fg_softmax_ce(const void* logits, int logits_bf16, int num_classes, int64_t 
                   float* loss_out, void* cuda_stream);
 
 /* Adam (torch.optim.Adam semantics) over a flat fp32 parameter buffer with
- * a device step counter (graph-capturable; one update kernel). */
+ * a device step counter (graph-capturable; one update kernel).  step_dev
+ * points at TWO int64: [steps taken, 0] (the second is the kernel's
+ * block-completion counter; the last block advances the step).  params_bf16
+ * (nullable) receives a bf16 copy of the updated parameters. */
 int fg_adam_step(float* params, const float* grads, float* exp_avg,
                  float* exp_avg_sq, int64_t n, int64_t* step_dev, float lr,
                  float beta1, float beta2, float eps, float weight_decay,
-                 void* cuda_stream);
+                 uint16_t* params_bf16, void* cuda_stream);
+/* out[i] = bf16(in[i]) (round to nearest even). */
+int fg_f32_to_bf16_plain(const float* in, int64_t count, uint16_t* out, void* cuda_stream);
 
 /* ------------------------------------------------------------- sampler */
 /* PCG64 state block as used by numpy's default_rng (state, inc, has_uint32,

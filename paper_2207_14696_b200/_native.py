@@ -65,7 +65,8 @@ _SIGS = {
     "fg_block_mean_wgrad": (ci, [vp, i64, vp, vp, vp, i64, vp, i64, vp, i64, vp, vp, i64, vp]),
     "fg_softmax_ce": (ci, [vp, ci, ci, i64, i64, vp, vp, vp, vp, vp, vp, vp]),
     "fg_adam_step": (ci, [vp, vp, vp, vp, i64, vp, C.c_float, C.c_float, C.c_float, C.c_float,
-                          C.c_float, vp]),
+                          C.c_float, vp, vp]),
+    "fg_f32_to_bf16_plain": (ci, [vp, i64, vp, vp]),
     "fg_rng_init": (ci, [vp, u64, u64, u64, u64, ci, u32]),
     "fg_rng_read": (ci, [vp, C.POINTER(u64), C.POINTER(u64), C.POINTER(ci), C.POINTER(u32)]),
     "fg_rng_permutation_host": (ci, [vp, vp, i64]),

@@ -360,11 +360,15 @@ k_block_mean_bwd_t(const uint16_t* __restrict__ g, int64_t H, int64_t g_ld,
 // ----------------------------------------------------------- flat Adam
 // torch.optim.Adam semantics (L2 weight decay folded into the gradient) over
 // one flat fp32 parameter buffer; the step counter lives on the device so
-// the update can sit inside a CUDA graph.
+// the update can sit inside a CUDA graph.  step[0] = steps taken, step[1] =
+// block-completion counter: the last block to finish advances step[0] (no
+// separate increment launch).  Optionally writes a bf16 shadow copy of the
+// updated parameters (the next forward's GEMM operands: no cast kernels).
 __global__ void k_adam(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
-                       float* __restrict__ v, int64_t n, const int64_t* __restrict__ step,
-                       float lr, float b1, float b2, float eps, float wd) {
-  const int64_t t = *step + 1;
+                       float* __restrict__ v, int64_t n, int64_t* __restrict__ step,
+                       float lr, float b1, float b2, float eps, float wd,
+                       __nv_bfloat16* __restrict__ p_bf16) {
+  const int64_t t = *(volatile int64_t*)step + 1;
   const float bc1 = 1.0f - powf(b1, (float)t);
   const float bc2 = 1.0f - powf(b2, (float)t);
   const float step_size = lr / bc1;
@@ -377,10 +381,25 @@ __global__ void k_adam(float* __restrict__ p, const float* __restrict__ g, float
     const float vi = b2 * v[i] + (1.0f - b2) * gi * gi;
     m[i] = mi;
     v[i] = vi;
-    p[i] -= step_size * mi / (sqrtf(vi) / bc2_sqrt + eps);
+    const float pn = p[i] - step_size * mi / (sqrtf(vi) / bc2_sqrt + eps);
+    p[i] = pn;
+    if (p_bf16) p_bf16[i] = __float2bfloat16_rn(pn);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long* ctr = reinterpret_cast<unsigned long long*>(step + 1);
+    if (atomicAdd(ctr, 1ull) == gridDim.x - 1) {  // every block has read step[0]
+      step[0] = t;
+      *ctr = 0ull;
+    }
   }
 }
-__global__ void k_step_inc(int64_t* step) { *step += 1; }
+
+__global__ void k_to_bf16(const float* __restrict__ p, int64_t n, __nv_bfloat16* __restrict__ o) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    o[i] = __float2bfloat16_rn(p[i]);
+}
 
 }  // namespace fg
 
@@ -440,12 +459,19 @@ extern "C" int fg_block_mean_bwd_t(const uint16_t* g, int64_t H, int64_t g_ld,
 
 extern "C" int fg_adam_step(float* params, const float* grads, float* m, float* v, int64_t n,
                             int64_t* step_dev, float lr, float beta1, float beta2, float eps,
-                            float weight_decay, void* s) {
+                            float weight_decay, uint16_t* params_bf16, void* s) {
   if (n == 0) return FG_OK;
-  fg::k_adam<<<grid_for(n, 256, 4), 256, 0, as_stream(s)>>>(params, grads, m, v, n, step_dev, lr,
-                                                            beta1, beta2, eps, weight_decay);
+  fg::k_adam<<<grid_for(n, 256, 4), 256, 0, as_stream(s)>>>(
+      params, grads, m, v, n, step_dev, lr, beta1, beta2, eps, weight_decay,
+      reinterpret_cast<__nv_bfloat16*>(params_bf16));
   FG_LAUNCH_CHECK();
-  fg::k_step_inc<<<1, 1, 0, as_stream(s)>>>(step_dev);
+  return FG_OK;
+}
+
+extern "C" int fg_f32_to_bf16_plain(const float* in, int64_t n, uint16_t* out, void* s) {
+  if (n == 0) return FG_OK;
+  fg::k_to_bf16<<<grid_for(n, 256, 4), 256, 0, as_stream(s)>>>(
+      in, n, reinterpret_cast<__nv_bfloat16*>(out));
   FG_LAUNCH_CHECK();
   return FG_OK;
 }

@@ -106,22 +106,27 @@ class SageModel(nn.Module):
 
 class FlatAdam:
     """torch.optim.Adam(betas=(0.9, 0.999), eps=1e-8) over one flat buffer,
-    one kernel per step (``fg_adam_step``), device-side step counter."""
+    one kernel per step (``fg_adam_step``), device-side step counter; keeps
+    an optional bf16 shadow of the parameters for the next forward."""
 
-    def __init__(self, param, grad, lr=1e-3, betas=(0.9, 0.999), eps=1e-8, weight_decay=0.0):
+    def __init__(self, param, grad, lr=1e-3, betas=(0.9, 0.999), eps=1e-8, weight_decay=0.0,
+                 param_bf16=None):
         from . import _native as N
         self.N = N
-        self.p, self.g = param, grad
+        self.p, self.g, self.pb = param, grad, param_bf16
         self.m = torch.zeros_like(param)
         self.v = torch.zeros_like(param)
-        self.t = torch.zeros(1, dtype=torch.int64, device=param.device)
+        self.t = torch.zeros(2, dtype=torch.int64, device=param.device)  # [step, block ctr]
         self.lr, self.b1, self.b2, self.eps, self.wd = lr, betas[0], betas[1], eps, weight_decay
+        if self.pb is not None:
+            N.call("fg_f32_to_bf16_plain", N.ptr(param), param.numel(), N.ptr(self.pb),
+                   N.stream_handle())
 
     def step(self):
         N = self.N
         N.call("fg_adam_step", N.ptr(self.p), N.ptr(self.g), N.ptr(self.m), N.ptr(self.v),
                self.p.numel(), N.ptr(self.t), self.lr, self.b1, self.b2, self.eps, self.wd,
-               N.stream_handle())
+               N.ptr(self.pb) if self.pb is not None else None, N.stream_handle())
 
 
 @dataclass
@@ -174,7 +179,19 @@ class SageTrainer:
             off += n
         if self.world > 1:  # identical initial weights on every rank
             torch.distributed.broadcast(self.flat_param, 0, group=self.pg)
-        self.opt = FlatAdam(self.flat_param, self.flat_grad, lr=cfg.lr)
+        # bf16 shadow of the parameters (written by the Adam kernel): the
+        # explicit step's GEMM operands, so no per-step weight casts
+        self.flat_bf16 = torch.zeros(total, dtype=torch.bfloat16, device=self.device)
+        self.w_bf16, self.w_grad = [], []
+        off = 0
+        for p in params:
+            n = p.numel()
+            self.w_bf16.append(self.flat_bf16[off:off + n].view_as(p))
+            self.w_grad.append(self.flat_grad[off:off + n].view_as(p))
+            off += n
+        self.opt = FlatAdam(self.flat_param, self.flat_grad, lr=cfg.lr, param_bf16=self.flat_bf16)
+        # explicit forward/backward (no autograd) unless dropout is on
+        self.explicit = not cfg.dropout
         self.loss_buf = torch.zeros((), dtype=torch.float32, device=self.device)
         self.agg = alloc_aggregate(self.caps[L - 1], codec.d, cfg.agg_dtype, self.device)
         w0 = self.model.lins[0].weight
@@ -186,6 +203,68 @@ class SageTrainer:
 
     # ------------------------------------------------------------- step
     def _body(self):
+        if self.explicit:
+            return self._body_explicit()
+        return self._body_autograd()
+
+    def _body_explicit(self):
+        """One training step with the backward written out (SageModel's
+        math, bf16 GEMMs on the Adam kernel's bf16 weight shadow, fp32 weight
+        gradients straight into the flat gradient buffer): no autograd
+        bookkeeping, weight casts, gradient zero-fill or accumulation kernels.
+
+        forward   in_0 = agg;  h_i = in_i W_i^T;  in_{i+1} = mean_block(relu h_i) (+ ones col)
+        backward  dW_i = dh_i^T in_i;  d in_i = dh_i W_i[:, :H];
+                  dh_{i-1} = relu'(h_{i-1}) * mean_block^T(d in_i)
+        with the input layer's dW_0 from the edge-tiled tcgen05 kernel when
+        the shape allows (fg_block_mean_wgrad)."""
+        sb = self.sampler.sample_loaded()
+        L = len(self.cfg.fanouts)
+        caps = self.caps
+        s = N.stream_handle()
+        gather_dequant_mean(self.codec, sb.indptr[L - 1], sb.picks[L - 1], sb.n_nodes[L - 1],
+                            caps[L - 1], out=self.agg)
+        W, dW = self.w_bf16, self.w_grad
+        ins, hs = [self.agg], []
+        for i in range(L):
+            h = torch.mm(ins[i], W[i].t())
+            hs.append(h)
+            if i < L - 1:
+                l = L - 2 - i  # block feeding layer i+1
+                H = h.shape[1]
+                a = torch.empty((caps[l], H + 8), dtype=torch.bfloat16, device=self.device)
+                N.call("fg_block_mean_fwd", N.ptr(h), H, N.ptr(sb.indptr[l]), N.ptr(sb.local[l]),
+                       N.ptr(sb.n_nodes[l]), caps[l], N.ptr(a), H + 8, 1, s)
+                ins.append(a)
+        logits = hs[-1]
+        C = logits.shape[1]
+        dh = torch.empty_like(logits)
+        row_loss = torch.empty(logits.shape[0], dtype=torch.float32, device=self.device)
+        N.call("fg_softmax_ce", N.ptr(logits), 1, C, C, logits.shape[0], N.ptr(sb.n_nodes[0]),
+               N.ptr(self.labels), N.ptr(sb.nodes[0]), N.ptr(dh), N.ptr(row_loss),
+               N.ptr(self.loss_buf), s)
+        fused = self.wgrad_scratch is not None
+        for i in range(L - 1, -1, -1):
+            torch.mm(dh.t(), ins[i], out_dtype=torch.float32, out=dW[i])
+            if i == 0:
+                break
+            H = hs[i - 1].shape[1]
+            din = torch.mm(dh, W[i][:, :H])
+            l = L - 1 - i  # block feeding layer i
+            if fused and i == 1:
+                N.call("fg_block_mean_wgrad", N.ptr(din), H, N.ptr(sb.indptr[l]),
+                       N.ptr(sb.local[l]), N.ptr(sb.n_nodes[l]), caps[l], N.ptr(hs[0]), H,
+                       N.ptr(self.agg), self.agg.shape[1], N.ptr(dW[0]),
+                       N.ptr(self.wgrad_scratch), self.wgrad_scratch.numel() * 4, s)
+                break
+            t_indptr, t_dst, t_w, n_src = sb.trans[l]
+            dh = torch.empty_like(hs[i - 1])
+            N.call("fg_block_mean_bwd_t", N.ptr(din), H, H, N.ptr(t_indptr), N.ptr(t_dst),
+                   N.ptr(t_w), N.ptr(n_src), dh.shape[0], N.ptr(hs[i - 1]), N.ptr(dh), s)
+        ddp.average_flat_(self.flat_grad, self.pg)
+        self.opt.step()
+
+    def _body_autograd(self):
         sb = self.sampler.sample_loaded()
         L = len(self.cfg.fanouts)
         gather_dequant_mean(self.codec, sb.indptr[L - 1], sb.picks[L - 1], sb.n_nodes[L - 1],

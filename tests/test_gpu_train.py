@@ -131,3 +131,32 @@ def test_fused_input_layer_grads_match_unfused(vq):
         rel = ((a - b).norm() / b.norm()).item()
         assert rel < 1e-2, (off, rel)
         off += n
+
+
+@pytest.mark.parametrize("hidden,vq", [(128, False), (64, True), (256, True)])
+def test_explicit_step_matches_autograd_step(hidden, vq):
+    """The trainer's explicit forward/backward (bf16 weight shadow, fp32
+    weight gradients straight into the flat buffer) gives the autograd
+    step's gradients on the same batch, and the same Adam update."""
+    dg, labels, dc, train, val = _small_world(vq=vq, d=100 if vq else 64)
+    cfg = TrainConfig(fanouts=(15, 10, 5), batch_size=512, hidden=hidden, use_graph=False)
+    ts = []
+    for explicit in (True, False):
+        torch.manual_seed(0)
+        t = SageTrainer(dg, dc, labels, 8, cfg)
+        t.explicit = explicit
+        t.begin_epoch(train, 0)
+        t.step(0)
+        ts.append(t)
+    a, b = ts
+    assert abs(float(a.loss_buf) - float(b.loss_buf)) < 2e-2 * abs(float(b.loss_buf))
+    off = 0
+    for lin in a.model.lins:
+        n = lin.weight.numel()
+        ga, gb = a.flat_grad[off:off + n], b.flat_grad[off:off + n]
+        rel = ((ga - gb).norm() / gb.norm()).item()
+        assert rel < 2e-2, (off, rel)
+        off += n
+    # the Adam step and its bf16 shadow
+    assert int(a.opt.t[0]) == 1 and int(a.opt.t[1]) == 0
+    assert torch.equal(a.flat_bf16, a.flat_param.to(torch.bfloat16))
