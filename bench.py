@@ -190,7 +190,7 @@ def run_ours(args, rank, world, local):
     cfg = TrainConfig(fanouts=fanouts, batch_size=bs, hidden=hidden, lr=3e-3, seed=0)
     tr = SageTrainer(sg.graph, dc, sg.labels, sg.num_classes, cfg, process_group=pg)
     nb = tr.begin_epoch(sg.train_ids, 0)
-    need = args.warmup + 2 * args.steps + 1
+    need = args.warmup + 2 * args.steps + 3
     if nb < need:
         raise SystemExit(f"epoch has {nb} batches per rank, need {need}")
     tr.capture(warmup_batches=max(3, args.warmup))
@@ -209,9 +209,9 @@ def run_ours(args, rank, world, local):
         for i in range(args.steps):
             b = args.warmup + i
             flush_l2(flush)
-            tr.sampler.load_seeds(b)
+            tr.prepare(b)  # stage seeds (device copy), outside the timed region
             evs[i][0].record()
-            tr.graph.replay()
+            tr.replay(b)
             evs[i][1].record()
         torch.cuda.synchronize()
     if world > 1:
@@ -219,16 +219,21 @@ def run_ours(args, rank, world, local):
     t_ms = sum(s.elapsed_time(e) for s, e in evs)
     t_ms = ddp.max_over_ranks(t_ms, dev)
     # launches per step: one eager step counted by the library's counter
+    b = args.warmup + args.steps
+    tr.prepare(b)
+    torch.cuda.synchronize()
     c0 = N.lib().fg_launch_count()
-    tr.sampler.load_seeds(0)
-    tr._body()
+    tr._body(b % len(tr.samplers))
     torch.cuda.synchronize()
     launches_per_step = N.lib().fg_launch_count() - c0
     # ---- e2e: public API, seeds from pinned host, loss read back each step
+    # step b's host input: the seeds of the batch it samples (b+1 when the
+    # trainer pipelines sampling one batch ahead, else b)
     perm = tr.sampler.perm_host
-    pinned = [torch.from_numpy(perm[(args.warmup + args.steps + i) * bs:
-                                    (args.warmup + args.steps + i + 1) * bs].copy()).pin_memory()
-              for i in range(args.steps)]
+    b0 = args.warmup + args.steps + 1
+    ahead = 1 if tr.pipeline else 0
+    pinned = [torch.from_numpy(perm[(b0 + i + ahead) * bs:(b0 + i + ahead + 1) * bs].copy())
+              .pin_memory() for i in range(args.steps)]
     loss_host = torch.zeros((), dtype=torch.float32).pin_memory()
     torch.cuda.synchronize()
     if world > 1:
@@ -238,7 +243,7 @@ def run_ours(args, rank, world, local):
         flush_l2(flush)
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
-        loss = tr.step(0, seeds_host=pinned[i])
+        loss = tr.step(b0 + i, seeds_host=pinned[i])
         loss_host.copy_(loss, non_blocking=True)
         e.record()
         e.synchronize()

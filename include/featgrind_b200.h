@@ -248,13 +248,16 @@ int fg_block_mean_wgrad(const uint16_t* grad_out, int64_t g_ld, const int32_t* i
                         int64_t scratch_bytes, void* cuda_stream);
 
 /* Fused softmax cross-entropy over padded logits [rows, ld] (bf16 or fp32):
- * rows r < *n_valid_dev use label labels[row_node[r]]; loss_out = mean loss
- * (deterministic row-order reduction); grad = d loss / d logits (same dtype;
- * zeros for padded rows); row_loss = per-row scratch [rows]. */
+ * rows r < *n_valid_dev use label labels[row_node[r]] over the first
+ * num_classes columns; loss_out = mean loss (deterministic row-order
+ * reduction by the last CTA); grad [rows, ld] = d loss / d logits (same
+ * dtype; zeros for padded rows and for columns >= num_classes); row_loss =
+ * per-row scratch [rows]; counter = one zero-initialised uint32 (re-armed by
+ * the kernel). */
 int fg_softmax_ce(const void* logits, int logits_bf16, int num_classes, int64_t ld,
                   int64_t rows, const int64_t* n_valid_dev, const int32_t* labels,
                   const int32_t* row_node, void* grad, float* row_loss,
-                  float* loss_out, void* cuda_stream);
+                  float* loss_out, unsigned int* counter, void* cuda_stream);
 
 /* Adam (torch.optim.Adam semantics) over a flat fp32 parameter buffer with
  * a device step counter (graph-capturable; one update kernel).  step_dev

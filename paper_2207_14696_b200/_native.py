@@ -63,7 +63,7 @@ _SIGS = {
     "fg_block_mean_wgrad_supported": (ci, [i64, i64]),
     "fg_block_mean_wgrad_scratch_bytes": (i64, [i64, i64]),
     "fg_block_mean_wgrad": (ci, [vp, i64, vp, vp, vp, i64, vp, i64, vp, i64, vp, vp, i64, vp]),
-    "fg_softmax_ce": (ci, [vp, ci, ci, i64, i64, vp, vp, vp, vp, vp, vp, vp]),
+    "fg_softmax_ce": (ci, [vp, ci, ci, i64, i64, vp, vp, vp, vp, vp, vp, vp, vp]),
     "fg_adam_step": (ci, [vp, vp, vp, vp, i64, vp, C.c_float, C.c_float, C.c_float, C.c_float,
                           C.c_float, vp, vp]),
     "fg_f32_to_bf16_plain": (ci, [vp, i64, vp, vp]),

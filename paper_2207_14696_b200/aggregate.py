@@ -168,28 +168,30 @@ def input_block_mean(x, w, indptr, local, n_dst, max_dst: int, bias_col: bool = 
 
 
 class SoftmaxCE(torch.autograd.Function):
-    """Mean cross-entropy over the live seed rows of padded logits, labels
-    gathered on the device (``fg_softmax_ce``: one fused kernel computing
-    loss and d loss / d logits)."""
+    """Mean cross-entropy over the live seed rows of padded logits (classes
+    past ``num_classes`` are padding), labels gathered on the device
+    (``fg_softmax_ce``: one fused kernel computing loss and d loss / d
+    logits)."""
 
     @staticmethod
-    def forward(ctx, logits, labels, row_node, n_valid):
+    def forward(ctx, logits, labels, row_node, n_valid, num_classes):
         logits = logits.contiguous()
-        rows, C = logits.shape
+        rows, ld = logits.shape
         grad = torch.empty_like(logits)
         row_loss = torch.empty(rows, dtype=torch.float32, device=logits.device)
         loss = torch.empty((), dtype=torch.float32, device=logits.device)
-        N.call("fg_softmax_ce", N.ptr(logits), int(logits.dtype == torch.bfloat16), C, C, rows,
-               N.ptr(n_valid), N.ptr(labels), N.ptr(row_node), N.ptr(grad), N.ptr(row_loss),
-               N.ptr(loss), N.stream_handle())
+        ctr = torch.zeros(1, dtype=torch.int32, device=logits.device)
+        N.call("fg_softmax_ce", N.ptr(logits), int(logits.dtype == torch.bfloat16),
+               num_classes or ld, ld, rows, N.ptr(n_valid), N.ptr(labels), N.ptr(row_node),
+               N.ptr(grad), N.ptr(row_loss), N.ptr(loss), N.ptr(ctr), N.stream_handle())
         ctx.save_for_backward(grad)
         return loss
 
     @staticmethod
     def backward(ctx, g):
         (grad,) = ctx.saved_tensors
-        return grad * g.to(grad.dtype), None, None, None
+        return grad * g.to(grad.dtype), None, None, None, None
 
 
-def softmax_ce(logits, labels, row_node, n_valid):
-    return SoftmaxCE.apply(logits, labels, row_node, n_valid)
+def softmax_ce(logits, labels, row_node, n_valid, num_classes: int | None = None):
+    return SoftmaxCE.apply(logits, labels, row_node, n_valid, num_classes)

@@ -486,7 +486,8 @@ template <typename LT>
 __global__ void k_softmax_ce(const LT* __restrict__ logits, int C, int64_t ld, int64_t rows,
                              const int64_t* __restrict__ nvalid_dev,
                              const int32_t* __restrict__ labels, const int32_t* __restrict__ node,
-                             LT* __restrict__ grad, float* __restrict__ row_loss) {
+                             LT* __restrict__ grad, float* __restrict__ row_loss,
+                             unsigned int* __restrict__ done, float* __restrict__ loss_out) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -496,7 +497,7 @@ __global__ void k_softmax_ce(const LT* __restrict__ logits, int C, int64_t ld, i
     const LT* x = logits + r * ld;
     LT* gr = grad + r * ld;
     if (r >= nv) {
-      for (int c = lane; c < C; c += 32) gr[c] = (LT)0.f;
+      for (int c = lane; c < ld; c += 32) gr[c] = (LT)0.f;
       if (lane == 0) row_loss[r] = 0.f;
       continue;
     }
@@ -514,43 +515,53 @@ __global__ void k_softmax_ce(const LT* __restrict__ logits, int C, int64_t ld, i
       const float p = __expf((float)x[c] - lse);
       gr[c] = (LT)((p - (c == y ? 1.f : 0.f)) * inv_n);
     }
+    for (int c = C + lane; c < ld; c += 32) gr[c] = (LT)0.f;  // padded classes
     if (lane == 0) row_loss[r] = (lse - (float)x[y]) * inv_n;
+  }
+  // the last CTA to finish sums the per-row losses in row order
+  // (deterministic) and re-arms the completion counter
+  __shared__ bool last;
+  __shared__ float part[256];
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  float acc = 0.f;
+  const int64_t per = (rows + blockDim.x - 1) / blockDim.x;
+  const int64_t r0 = threadIdx.x * per, r1 = min64(rows, r0 + per);
+  for (int64_t r = r0; r < r1; ++r) acc += *(volatile float*)(row_loss + r);
+  part[threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int i = 0; i < (int)blockDim.x; ++i) t += part[i];
+    *loss_out = t;
+    *done = 0u;
   }
 }
 
-__global__ void __launch_bounds__(1024)
-k_sum_rows(const float* __restrict__ v, int64_t n, float* __restrict__ out) {
-  __shared__ float part[1024];
-  float s = 0.f;
-  for (int64_t i = threadIdx.x; i < n; i += 1024) s += v[i];
-  part[threadIdx.x] = s;
-  __syncthreads();
-  for (int w = 512; w; w >>= 1) {
-    if (threadIdx.x < w) part[threadIdx.x] += part[threadIdx.x + w];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) *out = part[0];
-}
 }  // namespace fg
 
 extern "C" int fg_softmax_ce(const void* logits, int logits_bf16, int C, int64_t ld, int64_t rows,
                              const int64_t* n_valid_dev, const int32_t* labels,
                              const int32_t* row_node, void* grad, float* row_loss,
-                             float* loss_out, void* s) {
+                             float* loss_out, unsigned int* counter, void* s) {
   FG_CHECK_ARG(C >= 1 && ld >= C && rows >= 1, "fg_softmax_ce: bad shape");
+  FG_CHECK_ARG(counter != nullptr && loss_out != nullptr && row_loss != nullptr,
+               "fg_softmax_ce: null argument");
   cudaStream_t st = as_stream(s);
   const int threads = 256;
   const int grid = (int)min64(ceil_div(rows * 32, threads), (int64_t)sm_count() * 8);
   if (logits_bf16)
     fg::k_softmax_ce<__nv_bfloat16><<<grid, threads, 0, st>>>(
         (const __nv_bfloat16*)logits, C, ld, rows, n_valid_dev, labels, row_node,
-        (__nv_bfloat16*)grad, row_loss);
+        (__nv_bfloat16*)grad, row_loss, counter, loss_out);
   else
     fg::k_softmax_ce<float><<<grid, threads, 0, st>>>((const float*)logits, C, ld, rows,
                                                       n_valid_dev, labels, row_node,
-                                                      (float*)grad, row_loss);
-  FG_LAUNCH_CHECK();
-  fg::k_sum_rows<<<1, 1024, 0, st>>>(row_loss, rows, loss_out);
+                                                      (float*)grad, row_loss, counter, loss_out);
   FG_LAUNCH_CHECK();
   return FG_OK;
 }

@@ -31,8 +31,9 @@ constexpr int kLocalF = 32;           // fanouts up to this use a local index bu
 // Layer workspace.  The head (counters + scalars + look-back status) is
 // zeroed by one memset per layer.
 struct LayerWs {
-  unsigned int* ctr;    // [0] tile ticket, [1] prefix done ticket, [2] sample done ticket
-  int64_t* scal;        // [0] total picks, [1] total draws, [2] bad key, [3] delta
+  unsigned int* ctr;    // [0] tile ticket, [1] prefix done, [2] sample done, [3] fix-up done
+  int64_t* scal;        // [0] total picks, [1] total draws, [2] bad key, [3] delta,
+                        // [4] bad key of the parallel fix-up pass
   unsigned long long* status;  // [nb] look-back status words
   int64_t* draw_off;    // [N] nominal stream offset per node
   uint32_t* used;       // [N] draws actually consumed
@@ -127,13 +128,14 @@ __device__ void layer_finish(const int64_t* __restrict__ off, const int32_t* __r
                              uint64_t* __restrict__ rng, LayerWs ws,
                              const int32_t* __restrict__ indptr, int32_t* __restrict__ picks,
                              int64_t max_picks, int64_t* __restrict__ num_picks,
-                             int32_t* __restrict__ err_flag, int64_t* s_bad_slot) {
+                             int32_t* __restrict__ err_flag, int64_t* s_bad_slot,
+                             int64_t delta0 = 0) {
   int64_t& s_bad = *s_bad_slot;
   const int64_t tot_draws = ws.scal[1];  // from the prefix kernel
   if (threadIdx.x == 0) s_bad = *(volatile int64_t*)&ws.scal[2];
   __syncthreads();
   int64_t bad = s_bad;
-  int64_t delta = 0;
+  int64_t delta = delta0;
   const int64_t nominal = 2 * (int64_t)f - 1;
   while (bad != 0) {
     const int64_t b = INT64_MAX - bad;
@@ -316,6 +318,9 @@ k_layer_sample(const int64_t* __restrict__ off, const int32_t* __restrict__ col,
     }
   }
   if (!sample_last_block(ws, gridDim.x, &s_u32)) return;
+  // a rejection leaves the layer to k_layer_fixup (parallel re-sample of the
+  // later nodes); otherwise finish here (advance the stream)
+  if (*(volatile int64_t*)&ws.scal[2] != 0) return;
   layer_finish(off, col, nodes, live, f, rng, ws, indptr, picks, max_picks, num_picks, err_flag,
                &s_bad);
 }
@@ -426,8 +431,60 @@ k_layer_sample_group(const int64_t* __restrict__ off, const int32_t* __restrict_
     }
   }
   if (!sample_last_block(ws, gridDim.x, &s_u32)) return;
+  // a rejection leaves the layer to k_layer_fixup (parallel re-sample of the
+  // later nodes); otherwise finish here (advance the stream)
+  if (*(volatile int64_t*)&ws.scal[2] != 0) return;
   layer_finish(off, col, nodes, live, f, rng, ws, indptr, picks, max_picks, num_picks, err_flag,
                &s_bad);
+}
+
+// Kernel 3 (no-op unless the sampling kernel saw a Lemire rejection): the
+// first rejecting node b consumed delta extra draws, so every later node's
+// draws start delta further into the stream.  All of them are re-sampled in
+// parallel (thread per node) at the corrected offsets; a rejection among
+// them (rare squared) is handled by the last CTA's serial loop
+// (layer_finish), which also advances the stream.
+__global__ void __launch_bounds__(kSampThreads)
+k_layer_fixup(const int64_t* __restrict__ off, const int32_t* __restrict__ col,
+              const int32_t* __restrict__ nodes, const int64_t* __restrict__ nlive, int64_t N,
+              int f, uint64_t* __restrict__ rng, LayerWs ws, const int32_t* __restrict__ indptr,
+              int32_t* __restrict__ picks, int64_t max_picks, int64_t* __restrict__ num_picks,
+              int32_t* __restrict__ err_flag) {
+  const int64_t bad = ws.scal[2];
+  if (bad == 0) return;  // uniform across the grid: nothing to redo
+  __shared__ unsigned int s_u32;
+  __shared__ int64_t s_bad;
+  __shared__ uint64_t s_blk[FG_RNG_WORDS];
+  for (int k = threadIdx.x; k < FG_RNG_WORDS; k += blockDim.x) s_blk[k] = rng[k];
+  __syncthreads();
+  const int64_t live = min64(*nlive, N);
+  const int64_t b = INT64_MAX - bad;
+  const int64_t nominal = 2 * (int64_t)f - 1;
+  const int64_t delta = (int64_t)ws.used[b] - nominal;
+  const int64_t i = blockIdx.x * (int64_t)kSampThreads + threadIdx.x;
+  if (i > b && i < live) {
+    const int32_t u = nodes[i];
+    const int64_t deg = off[u + 1] - off[u];
+    const int32_t po = indptr[i];
+    if (deg > f && po + f <= max_picks) {
+      const uint32_t used = sample_node(off, col, u, f, s_blk,
+                                        (uint64_t)(ws.draw_off[i] + delta), picks + po, nullptr);
+      ws.used[i] = used;
+      if ((int64_t)used != nominal) atomicMax((long long*)&ws.scal[4], (long long)(INT64_MAX - i));
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_u32 = atomicAdd(ws.ctr + 3, 1u) == gridDim.x - 1 ? 1u : 0u;
+  __syncthreads();
+  if (!s_u32) return;
+  __threadfence();
+  // the serial loop continues from the pass's first rejection (if any) with
+  // the shift accumulated so far
+  if (threadIdx.x == 0) ws.scal[2] = *(volatile int64_t*)&ws.scal[4];
+  __syncthreads();
+  layer_finish(off, col, nodes, live, f, rng, ws, indptr, picks, max_picks, num_picks, err_flag,
+               &s_bad, delta);
 }
 
 // Single-pass compaction: popcounts, block scan, look-back prefix, ordered
@@ -556,6 +613,11 @@ int fg_sample_layer(const int64_t* row_offsets, const int32_t* col_indices, int6
     }
 #undef FG_SAMPLE_F
   }
+  FG_LAUNCH_CHECK();
+  k_layer_fixup<<<(unsigned)nt, kSampThreads, 0, st>>>(row_offsets, col_indices, nodes,
+                                                       num_nodes_dev, max_nodes, fanout, rng_dev, w,
+                                                       indptr, picks, max_picks, num_picks_dev,
+                                                       err_flag);
   FG_LAUNCH_CHECK();
   if (bitmap) {  // next layer's unique set: mark after any fix-up rewrote picks
     k_mark32<<<grid_for(max_picks, 256), 256, 0, st>>>(picks, num_picks_dev, max_picks, bitmap);

@@ -46,15 +46,22 @@ class SageModel(nn.Module):
         super().__init__()
         dims = [in_dim] + [hidden] * (num_layers - 1) + [num_classes]
         self.in_dims = dims[:-1]
+        self.out_dims = dims[1:]
+        self.num_classes = num_classes
+        # the class dimension is padded to a multiple of 8 (zero weight rows:
+        # their logits are 0, their gradients 0, Adam leaves them at 0) so
+        # every GEMM operand is 16-byte aligned (aligned cuBLAS kernels)
+        c_pad = (num_classes + 7) // 8 * 8
         lins = []
         for i in range(num_layers):
             pitch = (in_pitch or in_dim + 1) if i == 0 else dims[i] + 8
-            lin = nn.Linear(pitch, dims[i + 1], bias=False)
+            rows = c_pad if i == num_layers - 1 else dims[i + 1]
+            lin = nn.Linear(pitch, rows, bias=False)
             ref = nn.Linear(dims[i], dims[i + 1])
             with torch.no_grad():
                 lin.weight.zero_()
-                lin.weight[:, :dims[i]] = ref.weight
-                lin.weight[:, dims[i]] = ref.bias
+                lin.weight[:dims[i + 1], :dims[i]] = ref.weight
+                lin.weight[:dims[i + 1], dims[i]] = ref.bias
             lins.append(lin)
         self.lins = nn.ModuleList(lins)
         self.dropout = dropout
@@ -99,8 +106,9 @@ class SageModel(nn.Module):
         out = {}
         for i, (lin, d) in enumerate(zip(self.lins, self.in_dims)):
             w = lin.weight.detach().float().cpu()
-            out[f"lins.{i}.weight"] = w[:, :d].clone()
-            out[f"lins.{i}.bias"] = w[:, d].clone()
+            o = self.out_dims[i]
+            out[f"lins.{i}.weight"] = w[:o, :d].clone()
+            out[f"lins.{i}.bias"] = w[:o, d].clone()
         return out
 
 
@@ -139,6 +147,9 @@ class TrainConfig:
     dropout: float = 0.0
     use_graph: bool = True
     agg_dtype: torch.dtype = torch.bfloat16
+    # sample batch b+1 on a side stream while batch b trains (two sampler
+    # slots sharing one PCG64 stream: the batches are the same as serial)
+    pipeline: bool = True
 
 
 class SageTrainer:
@@ -159,9 +170,16 @@ class SageTrainer:
                                in_pitch=padded_dim(codec.d)).to(self.device)
         # the fused input layer needs no transpose of its block (block L-2)
         fused = self.model.fused_input_ok()
+        tl = range(L - 2) if fused else None
         self.sampler = DeviceSampler(graph, cfg.fanouts, cfg.batch_size, need_local=True,
-                                     need_transpose=True,
-                                     transpose_layers=range(L - 2) if fused else None)
+                                     need_transpose=True, transpose_layers=tl)
+        self.samplers = [self.sampler]
+        self.pipeline = cfg.pipeline
+        if self.pipeline:
+            self.samplers.append(DeviceSampler(graph, cfg.fanouts, cfg.batch_size,
+                                               need_local=True, need_transpose=True,
+                                               transpose_layers=tl, share=self.sampler))
+            self.side = torch.cuda.Stream(self.device)
         self.caps = self.sampler.caps
         # flat gradient buffer: one all-reduce per step
         # one flat fp32 buffer each for params, grads and Adam moments: a
@@ -193,21 +211,40 @@ class SageTrainer:
         # explicit forward/backward (no autograd) unless dropout is on
         self.explicit = not cfg.dropout
         self.loss_buf = torch.zeros((), dtype=torch.float32, device=self.device)
+        self.ce_ctr = torch.zeros(1, dtype=torch.int32, device=self.device)
         self.agg = alloc_aggregate(self.caps[L - 1], codec.d, cfg.agg_dtype, self.device)
         w0 = self.model.lins[0].weight
         self.wgrad_scratch = None
         if fused:
             self.wgrad_scratch = wgrad_scratch(w0.shape[0], w0.shape[1], self.device)
         self.graph = None
+        self.graphs = {}
+        self._primed, self._next = False, 0
         self.steps_run = 0
 
     # ------------------------------------------------------------- step
-    def _body(self):
+    def _train(self, sb):
         if self.explicit:
-            return self._body_explicit()
-        return self._body_autograd()
+            return self._train_explicit(sb)
+        return self._train_autograd(sb)
 
-    def _body_explicit(self):
+    def _body(self, k: int = 0):
+        """One step.  Serial: sample slot 0's loaded seeds, then train.
+        Pipelined: train the batch already in slot k on the current stream
+        while the side stream samples the next batch (seeds already loaded)
+        into slot 1-k; the side stream first waits for the work already
+        queued (the previous step still reading slot 1-k) and is joined
+        before the step ends."""
+        if not self.pipeline:
+            return self._train(self.sampler.sample_loaded())
+        cur = torch.cuda.current_stream()
+        self.side.wait_stream(cur)
+        with torch.cuda.stream(self.side):
+            self.samplers[1 - k].sample_loaded()
+        self._train(self.samplers[k].batch_view())
+        cur.wait_stream(self.side)
+
+    def _train_explicit(self, sb):
         """One training step with the backward written out (SageModel's
         math, bf16 GEMMs on the Adam kernel's bf16 weight shadow, fp32 weight
         gradients straight into the flat gradient buffer): no autograd
@@ -218,7 +255,6 @@ class SageTrainer:
                   dh_{i-1} = relu'(h_{i-1}) * mean_block^T(d in_i)
         with the input layer's dW_0 from the edge-tiled tcgen05 kernel when
         the shape allows (fg_block_mean_wgrad)."""
-        sb = self.sampler.sample_loaded()
         L = len(self.cfg.fanouts)
         caps = self.caps
         s = N.stream_handle()
@@ -237,12 +273,12 @@ class SageTrainer:
                        N.ptr(sb.n_nodes[l]), caps[l], N.ptr(a), H + 8, 1, s)
                 ins.append(a)
         logits = hs[-1]
-        C = logits.shape[1]
+        ld = logits.shape[1]
         dh = torch.empty_like(logits)
         row_loss = torch.empty(logits.shape[0], dtype=torch.float32, device=self.device)
-        N.call("fg_softmax_ce", N.ptr(logits), 1, C, C, logits.shape[0], N.ptr(sb.n_nodes[0]),
-               N.ptr(self.labels), N.ptr(sb.nodes[0]), N.ptr(dh), N.ptr(row_loss),
-               N.ptr(self.loss_buf), s)
+        N.call("fg_softmax_ce", N.ptr(logits), 1, self.model.num_classes, ld, logits.shape[0],
+               N.ptr(sb.n_nodes[0]), N.ptr(self.labels), N.ptr(sb.nodes[0]), N.ptr(dh),
+               N.ptr(row_loss), N.ptr(self.loss_buf), N.ptr(self.ce_ctr), s)
         fused = self.wgrad_scratch is not None
         for i in range(L - 1, -1, -1):
             torch.mm(dh.t(), ins[i], out_dtype=torch.float32, out=dW[i])
@@ -264,14 +300,14 @@ class SageTrainer:
         ddp.average_flat_(self.flat_grad, self.pg)
         self.opt.step()
 
-    def _body_autograd(self):
-        sb = self.sampler.sample_loaded()
+    def _train_autograd(self, sb):
         L = len(self.cfg.fanouts)
         gather_dequant_mean(self.codec, sb.indptr[L - 1], sb.picks[L - 1], sb.n_nodes[L - 1],
                             self.caps[L - 1], out=self.agg)
         with torch.autocast("cuda", dtype=torch.bfloat16):
             logits = self.model(self.agg, sb, self.caps, self.wgrad_scratch)
-        loss = softmax_ce(logits, self.labels, sb.nodes[0], sb.n_nodes[0])
+        loss = softmax_ce(logits, self.labels, sb.nodes[0], sb.n_nodes[0],
+                          self.model.num_classes)
         self.flat_grad.zero_()
         loss.backward()
         ddp.average_flat_(self.flat_grad, self.pg)
@@ -280,19 +316,28 @@ class SageTrainer:
 
     def capture(self, warmup_batches: int = 3):
         """Warm up eagerly (allocations, cuBLAS handles, kernel attributes),
-        then capture one step into a CUDA graph."""
+        then capture the step into CUDA graphs (one per sampler slot).  The
+        PCG64 stream is restored afterwards, so the epoch's batches are
+        unchanged by the warm-up (the warm-up steps do update the model)."""
+        rng_save = self.sampler.rng.clone()
+        nxt = self._next
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s):
             for b in range(warmup_batches):
-                self.sampler.load_seeds(b % self._nb)
-                self._body()
+                self.prepare(b)
+                self._body(b % len(self.samplers))
         torch.cuda.current_stream().wait_stream(s)
         torch.cuda.synchronize()
-        self.graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(self.graph):
-            self._body()
+        for k in range(len(self.samplers)):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._body(k)
+            self.graphs[k] = g
         torch.cuda.synchronize()
+        self.graph = self.graphs[0]
+        self.sampler.rng.copy_(rng_save)
+        self._primed, self._next = False, nxt
 
     def begin_epoch(self, train_ids, epoch: int = 0) -> int:
         """Seeds are sharded like DDP: rank r takes ids[r::W] with seed
@@ -302,23 +347,47 @@ class SageTrainer:
         self._nb = self.sampler.begin_epoch(shard, ddp.rank_seed(self.cfg.seed, epoch, r,
                                                                  self.world))
         self._nb = ddp.agree_num_batches(self._nb, self.pg, self.device)
+        self._primed, self._next = False, 0
         return self._nb
 
-    def step(self, b: int, seeds_host: torch.Tensor | None = None):
-        """One training step on batch b; seeds either device-resident (perm)
-        or copied from a pinned host tensor (end-to-end path)."""
+    def prepare(self, b: int, seeds_host: torch.Tensor | None = None) -> None:
+        """Stage the inputs of step b.  Serial: batch b's seeds (from the
+        device permutation, or copied from pinned host memory).  Pipelined:
+        batch b must already be sampled into slot b % 2 (the previous step
+        did it; otherwise it is sampled here first), and this loads the seeds
+        of batch b+1 -- ``seeds_host`` if given, else the permutation slice
+        (wrapping at the epoch end) -- for the step to sample."""
+        if not self.pipeline:
+            if seeds_host is not None:
+                self.sampler.load_seeds_host(seeds_host)
+            else:
+                self.sampler.load_seeds(b)
+            return
+        if not (self._primed and self._next == b):
+            cur = self.samplers[b % 2]
+            cur.load_seeds(b % self._nb)
+            cur.sample_loaded()
+        nxt = self.samplers[(b + 1) % 2]
         if seeds_host is not None:
-            cnt = seeds_host.numel()
-            self.sampler.seed_in[:cnt].copy_(seeds_host, non_blocking=True)
-            self.sampler.n_seed_in.fill_(cnt)
+            nxt.load_seeds_host(seeds_host)
         else:
-            self.sampler.load_seeds(b)
-        if self.graph is not None:
-            self.graph.replay()
+            nxt.load_seeds((b + 1) % self._nb)
+        self._primed, self._next = True, b + 1
+
+    def replay(self, b: int):
+        """Run step b (after ``prepare(b)``) from its CUDA graph, or eagerly."""
+        k = b % len(self.samplers)
+        if k in self.graphs:
+            self.graphs[k].replay()
         else:
-            self._body()
+            self._body(k)
         self.steps_run += 1
         return self.loss_buf
+
+    def step(self, b: int, seeds_host: torch.Tensor | None = None):
+        """One training step on batch b (see ``prepare`` for ``seeds_host``)."""
+        self.prepare(b, seeds_host)
+        return self.replay(b)
 
     # -------------------------------------------------------- evaluation
     @torch.no_grad()
@@ -342,7 +411,8 @@ class SageTrainer:
                 logits = self.model(agg, sb, smp.caps)
             valid = torch.arange(smp.caps[0], device=self.device) < sb.n_nodes[0]
             y = self.labels[sb.nodes[0].long()].long()
-            correct += ((logits.argmax(1) == y) & valid).sum()
+            pred = logits[:, :self.model.num_classes].argmax(1)
+            correct += ((pred == y) & valid).sum()
             total += valid.sum()
         self.model.train()
         return float(correct.item()) / max(1, int(total.item()))

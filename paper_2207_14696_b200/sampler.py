@@ -111,7 +111,11 @@ class DeviceSampler:
     def __init__(self, graph: DeviceGraph, fanouts, batch_size: int, *,
                  need_local: bool = True, want_frontier: bool = False,
                  unique_last: bool = False, need_transpose: bool = False,
-                 transpose_layers=None):
+                 transpose_layers=None, share: "DeviceSampler | None" = None):
+        """``share``: a second buffer set (slot) for pipelined training that
+        continues ``share``'s PCG64 stream, permutation and scratch (only the
+        per-batch outputs are its own), so batch b+1 can be sampled into one
+        slot while batch b trains from the other."""
         import torch
         N.require_cuda()
         self.g = graph
@@ -151,8 +155,20 @@ class DeviceSampler:
                 self.t_indptr.append(z(caps[l + 1] + 1) if on else None)
                 self.t_dst.append(z(pcaps[l]) if on else None)
                 self.t_w.append(z(pcaps[l], dt=torch.float32) if on else None)
-            nbytes = N.lib().fg_block_transpose_scratch_bytes(max(caps[1:]))
-            self.t_scratch = torch.zeros(nbytes, dtype=torch.uint8, device=dev)
+            if share is None:
+                self._alloc_t_scratch()
+        self.owner = share or self
+        if share is not None:  # shared stream state + scratch
+            assert share.fanouts == self.fanouts and share.bs == self.bs and share.g is graph
+            self.bitmap, self.wprefix = share.bitmap, share.wprefix
+            self.ws_bm, self.ws_layer, self.err = share.ws_bm, share.ws_layer, share.err
+            self.rng = share.rng
+            if self.need_transpose:
+                if not hasattr(share, "t_scratch"):
+                    share._alloc_t_scratch()
+                self.t_scratch = share.t_scratch
+            self.want_frontier = False
+            return
         words = (n + 31) // 32
         self.bitmap = torch.zeros(words, dtype=torch.int32, device=dev)
         self.wprefix = torch.zeros(words, dtype=torch.int32, device=dev)
@@ -170,6 +186,11 @@ class DeviceSampler:
         self.rng = torch.zeros(N.RNG_WORDS, dtype=torch.int64, device=dev)
         self._inc = 0
         self.perm = None
+
+    def _alloc_t_scratch(self) -> None:
+        import torch
+        nbytes = N.lib().fg_block_transpose_scratch_bytes(max(self.caps[1:]))
+        self.t_scratch = torch.zeros(nbytes, dtype=torch.uint8, device=self.device)
 
     # ------------------------------------------------------------- epoch
     def begin_epoch(self, train_ids, seed: int) -> int:
@@ -203,10 +224,28 @@ class DeviceSampler:
     def load_seeds(self, b: int) -> None:
         """Device copy of batch b's slice of the permutation into the static
         seed buffer (used by the device-resident timed path)."""
+        perm = self.owner.perm
         lo = b * self.bs
-        cnt = min(self.bs, self.perm.numel() - lo)
-        self.seed_in[:cnt].copy_(self.perm[lo:lo + cnt])
+        cnt = min(self.bs, perm.numel() - lo)
+        self.seed_in[:cnt].copy_(perm[lo:lo + cnt])
         self.n_seed_in.fill_(cnt)
+
+    def load_seeds_host(self, seeds) -> None:
+        """Seeds from a (pinned) host tensor: the end-to-end input copy."""
+        cnt = seeds.numel()
+        self.seed_in[:cnt].copy_(seeds, non_blocking=True)
+        self.n_seed_in.fill_(cnt)
+
+    def batch_view(self) -> SampledBatch:
+        """The SampledBatch over this slot's static output buffers (what
+        ``sample_loaded`` returns, without sampling)."""
+        L = len(self.fanouts)
+        out = SampledBatch(self.nodes, self.n_nodes, self.indptr, self.picks, self.n_picks,
+                           self.local)
+        if self.need_transpose:
+            out.trans = [(self.t_indptr[l], self.t_dst[l], self.t_w[l], self.n_nodes[l + 1])
+                         if l in self.t_layers else None for l in range(L - 1)] + [None]
+        return out
 
     # ------------------------------------------------------------ sample
     def sample_loaded(self) -> SampledBatch:

@@ -63,7 +63,7 @@ def main():
         with torch.autocast("cuda", dtype=torch.bfloat16):
             logits = tr.model(tr.agg, sb, tr.caps)
         from paper_2207_14696_b200.aggregate import softmax_ce
-        return softmax_ce(logits, tr.labels, sb.nodes[0], sb.n_nodes[0])
+        return softmax_ce(logits, tr.labels, sb.nodes[0], sb.n_nodes[0], tr.model.num_classes)
 
     gf, gfb, go = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
     with torch.cuda.graph(gf):
@@ -78,7 +78,7 @@ def main():
         with torch.autocast("cuda", dtype=torch.bfloat16):
             logits = tr.model(tr.agg, sb, tr.caps)
         from paper_2207_14696_b200.aggregate import softmax_ce
-        loss = softmax_ce(logits, tr.labels, sb.nodes[0], sb.n_nodes[0])
+        loss = softmax_ce(logits, tr.labels, sb.nodes[0], sb.n_nodes[0], tr.model.num_classes)
         tr.flat_grad.zero_()
         loss.backward()
         tr.opt.step()
