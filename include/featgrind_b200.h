@@ -138,11 +138,22 @@ int64_t fg_select_workspace_bytes(void);
  * expressions (FMA-chained dot products, numpy pairwise add.reduce for norms);
  * ties -> lowest index; cosine zero sub-vectors -> 0.  `books` is float32
  * [P][L][width] (fg_codec_desc layout), `entries` the per-part live entry
- * count.  Codes land as device rows of `bits` bits per part. */
+ * count.  Codes land as device rows of `bits` bits per part.
+ * fg_vq_assign: widths <= 16 run the distance step on the 5th-gen tensor
+ * cores (tcgen05.mma kind::tf32, 3xTF32 split operands, scores in TMEM) as a
+ * screen, then re-score in float64 (the exact expression order above) every
+ * row whose best entry is not separated from the runner-up by 20x the
+ * screening error bound -- codes identical to the float64 path.
+ * fg_vq_assign_fp64: the float64 CUDA-core path for every row (reference
+ * timing / cross-check); same arguments. */
 int fg_vq_assign(const void* x, int x_is_f64, int64_t n, int64_t d, int width,
                  int length, int num_parts, const float* books,
                  const int32_t* entries, int metric, int bits, uint8_t* rows,
                  int64_t row_stride, int32_t* codes_i32, void* cuda_stream);
+int fg_vq_assign_fp64(const void* x, int x_is_f64, int64_t n, int64_t d, int width,
+                      int length, int num_parts, const float* books,
+                      const int32_t* entries, int metric, int bits, uint8_t* rows,
+                      int64_t row_stride, int32_t* codes_i32, void* cuda_stream);
 
 /* int32 codes [n, parts] (VqCodec.codes, vq.py:87-127) -> device rows of
  * `bits`-bit MSB-first codes (the PACKED layout of vq.py:379-381, per row). */

@@ -49,6 +49,7 @@ _SIGS = {
     "fg_select_ranks": (ci, [vp, i64, C.POINTER(i64), ci, C.POINTER(C.c_float), vp, i64, vp]),
     "fg_select_workspace_bytes": (i64, []),
     "fg_vq_assign": (ci, [vp, ci, i64, i64, ci, ci, ci, vp, vp, ci, ci, vp, i64, vp, vp]),
+    "fg_vq_assign_fp64": (ci, [vp, ci, i64, i64, ci, ci, ci, vp, vp, ci, ci, vp, i64, vp, vp]),
     "fg_codes_to_rows": (ci, [vp, i64, ci, ci, vp, i64, vp]),
     "fg_segment_sums": (ci, [vp, i64, ci, vp, vp, ci, vp, vp, vp]),
     "fg_vq_gather_decode": (ci, [C.POINTER(CodecDesc), vp, ci, i64, vp, ci, vp, vp]),

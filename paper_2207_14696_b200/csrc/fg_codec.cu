@@ -326,6 +326,293 @@ __global__ void k_vq_assign(const XT* __restrict__ x, int64_t n, int64_t d, int 
   }
 }
 
+// ---------------------------------------- VQ assign on the tensor cores
+// Screening GEMM + exact recheck.  For one codebook part (width w <= 16,
+// entries N <= 256 per chunk) the scores S = X^ C^T of a 128-row tile are
+// one tcgen05.mma chain (kind::tf32, M = 128, N = 256, K = 8 per MMA) into
+// TMEM.  Operands are split 3xTF32 (x = xh + xl, c = ch + cl; D = xh.ch +
+// xh.cl + xl.ch), so a score is within ~5e-6 * sum|x_i c_i| of the float64
+// value.  Thread r of the epilogue (TMEM lane r = row r) reads its scores,
+// finds the screening best and counts entries within a tolerance 20x that
+// bound; with a single candidate (the common case) it is provably the float64
+// argmin/argmax, otherwise the candidates are re-scored in float64 with the
+// reference's exact operation order (blas_dot, np_pairwise_sumsq) and the
+// first-index tie rule.  Codes are therefore bit-identical to the fp64 path
+// (k_vq_assign above / vq.py:306-327).
+constexpr int kTcRows = 128;
+constexpr int kTcN = 256;
+
+__device__ __forceinline__ uint32_t tc_smem(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ uint64_t tc_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;  // Blackwell descriptor version; SWIZZLE_NONE
+  return d;
+}
+// kind::tf32, D f32, A/B tf32 K-major, M = 128, N = n
+__host__ __device__ constexpr uint32_t tc_idesc_tf32(int n) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) |
+         ((uint32_t)(128 >> 4) << 24);
+}
+__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                       uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n"
+      ::"r"(tmem_d), "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void tc_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t mb = tc_smem(bar);
+  uint32_t done = 0;
+  while (!done)
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done) : "r"(mb), "r"(parity) : "memory");
+}
+// tf32 split: hi = top 19 bits (truncation), lo = exact remainder
+__device__ __forceinline__ void tf32_split(float v, uint32_t& hi, uint32_t& lo) {
+  hi = __float_as_uint(v) & 0xFFFFE000u;
+  lo = __float_as_uint(v - __uint_as_float(hi));
+}
+// byte offset of element (row, k) in a K-major no-swizzle operand whose K
+// extent is KB core columns of 4 tf32: core (row/8, k/4) at
+// ((row/8) * KB + k/4) * 128, row-in-core stride 16 B
+__device__ __forceinline__ uint32_t tc_off(int row, int k, int KB) {
+  return (uint32_t)((((row >> 3) * KB + (k >> 2)) << 7) + ((row & 7) << 4) + ((k & 3) << 2));
+}
+
+template <typename XT>
+__global__ void __launch_bounds__(kTcRows, 1)
+k_vq_assign_tc(const XT* __restrict__ x, int64_t n, int64_t d, int width, int length, int parts,
+               const float* __restrict__ books, const int32_t* __restrict__ entries, int metric,
+               int bits, uint8_t* __restrict__ rows, int64_t stride,
+               int32_t* __restrict__ codes32, int KB) {
+  // smem: A hi/lo [128 x 4KB floats], B hi/lo [256 x 4KB], cc [256], bar, tmem slot
+  extern __shared__ __align__(128) uint8_t tc_mem[];
+  const int a_bytes = kTcRows * KB * 16, b_bytes = kTcN * KB * 16;
+  uint8_t* sAh = tc_mem;
+  uint8_t* sAl = sAh + a_bytes;
+  uint8_t* sBh = sAl + a_bytes;
+  uint8_t* sBl = sBh + b_bytes;
+  float* s_cc = reinterpret_cast<float*>(sBl + b_bytes);          // [256] fp32 |c|^2 (screen)
+  double* s_ccd = reinterpret_cast<double*>(s_cc + kTcN);         // [256] fp64 |c|^2 (exact)
+  uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_ccd + kTcN);
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(s_bar + 1);
+  float* s_cmax = reinterpret_cast<float*>(s_tmem + 1);
+
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int p = blockIdx.y;
+  const int lo = p * width;
+  const int wp = (int)min64(width, d - lo);
+  const int L = entries[p];
+  const bool cosine = metric == FG_METRIC_COSINE;
+  const float* book = books + (int64_t)p * length * width;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 ::"r"(tc_smem(s_tmem)), "r"(kTcN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tc_smem(s_bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *s_tmem;
+  const uint32_t idesc = tc_idesc_tf32(kTcN);
+  uint32_t phase = 0;
+  const int64_t ntiles = (n + kTcRows - 1) / kTcRows;
+  const int nchunks = (L + kTcN - 1) / kTcN;
+  int64_t tile = blockIdx.x;
+  // per-row state carried across chunks
+  for (; tile < ntiles; tile += gridDim.x) {
+    const int64_t r = tile * kTcRows + tid;
+    const bool active = r < n;
+    double v[16];
+    double ss = 0.0;
+    bool live = active;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = 0.0;
+    if (active) {
+      for (int j = 0; j < wp; ++j) v[j] = (double)x[r * d + lo + j];
+      ss = np_pairwise_sumsq(v, wp);
+      if (cosine) {
+        const double nrm = sqrt(ss);  // np.linalg.norm (vq.py:310)
+        if (nrm > 0.0) {
+          for (int j = 0; j < wp; ++j) v[j] = __ddiv_rn(v[j], nrm);
+        } else {
+          live = false;
+        }
+      }
+    }
+    double xn1 = 0.0;  // sum |x_j| for the screening bound
+    for (int j = 0; j < wp; ++j) xn1 += fabs(v[j]);
+    // A row: split of the (normalised) row, zero padded to K = 4 * KB
+    for (int k = 0; k < 4 * KB; ++k) {
+      uint32_t h = 0, l = 0;
+      if (live && k < wp) tf32_split((float)v[k], h, l);
+      *reinterpret_cast<uint32_t*>(sAh + tc_off(tid, k, KB)) = h;
+      *reinterpret_cast<uint32_t*>(sAl + tc_off(tid, k, KB)) = l;
+    }
+    int best = 0;
+    double bestv = 0.0;  // exact value of the current best (when resolved)
+    bool have = false;
+    for (int ch = 0; ch < nchunks; ++ch) {
+      const int e0 = ch * kTcN;
+      const int cnt = min(kTcN, L - e0);
+      __syncthreads();  // previous chunk's epilogue done with B / TMEM
+      // B: this chunk's entries (split) + their norms
+      for (int i = tid; i < kTcN * 4 * KB; i += kTcRows) {
+        const int e = i / (4 * KB), k = i - e * (4 * KB);
+        uint32_t h = 0, l = 0;
+        if (e < cnt && k < wp) tf32_split(book[(int64_t)(e0 + e) * width + k], h, l);
+        *reinterpret_cast<uint32_t*>(sBh + tc_off(e, k, KB)) = h;
+        *reinterpret_cast<uint32_t*>(sBl + tc_off(e, k, KB)) = l;
+      }
+      float cm = 0.f;
+      for (int e = tid; e < kTcN; e += kTcRows) {
+        double cd = 0.0, c1 = 0.0;
+        double cv[16];
+        if (e < cnt) {
+          for (int j = 0; j < wp; ++j) {
+            cv[j] = (double)book[(int64_t)(e0 + e) * width + j];
+            c1 = fmax(c1, fabs(cv[j]));
+          }
+          cd = np_pairwise_sumsq(cv, wp);
+        }
+        s_ccd[e] = cd;
+        s_cc[e] = (float)cd;
+        cm = fmaxf(cm, (float)c1);
+      }
+      // chunk max |c_j| (for the screening bound)
+      for (int o = 16; o; o >>= 1) cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, o));
+      if ((tid & 31) == 0) s_cmax[warp] = cm;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncthreads();
+      if (tid == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t lbo = 128, sbo = (uint32_t)KB * 128;
+        int acc = 0;
+        for (int kk = 0; kk < KB; kk += 2) {  // K = 8 tf32 per MMA (2 core columns)
+          const uint32_t off = (uint32_t)kk * 128;
+          tc_mma(tmem, tc_desc(tc_smem(sAh) + off, lbo, sbo), tc_desc(tc_smem(sBh) + off, lbo, sbo),
+                 idesc, acc);
+          tc_mma(tmem, tc_desc(tc_smem(sAh) + off, lbo, sbo), tc_desc(tc_smem(sBl) + off, lbo, sbo),
+                 idesc, 1u);
+          tc_mma(tmem, tc_desc(tc_smem(sAl) + off, lbo, sbo), tc_desc(tc_smem(sBh) + off, lbo, sbo),
+                 idesc, 1u);
+          acc = 1;
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                     ::"r"(tc_smem(s_bar)) : "memory");
+      }
+      tc_wait(s_bar, phase);
+      phase ^= 1u;
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const float cmax = fmaxf(fmaxf(s_cmax[0], s_cmax[1]), fmaxf(s_cmax[2], s_cmax[3]));
+      // screening tolerance: 20x the 3xTF32 score error bound
+      const float tol_dot = 1e-4f * (float)xn1 * cmax + 1e-30f;
+      const float tol = cosine ? tol_dot : 2.f * tol_dot + 1e-6f * (float)(ss + (double)cmax * cmax * wp);
+      const float ssf = (float)ss;
+      // pass 1: screening best of this chunk (first max / first min)
+      float sb = 0.f;
+      int sbi = -1;
+      const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
+      for (int c0 = 0; c0 < kTcN; c0 += 32) {
+        uint32_t q[32];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+            "%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(q[0]), "=r"(q[1]), "=r"(q[2]), "=r"(q[3]), "=r"(q[4]), "=r"(q[5]), "=r"(q[6]),
+              "=r"(q[7]), "=r"(q[8]), "=r"(q[9]), "=r"(q[10]), "=r"(q[11]), "=r"(q[12]),
+              "=r"(q[13]), "=r"(q[14]), "=r"(q[15]), "=r"(q[16]), "=r"(q[17]), "=r"(q[18]),
+              "=r"(q[19]), "=r"(q[20]), "=r"(q[21]), "=r"(q[22]), "=r"(q[23]), "=r"(q[24]),
+              "=r"(q[25]), "=r"(q[26]), "=r"(q[27]), "=r"(q[28]), "=r"(q[29]), "=r"(q[30]),
+              "=r"(q[31])
+            : "r"(lane_base + (uint32_t)c0));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int e = c0 + j;
+          if (e >= cnt) break;
+          const float dot = __uint_as_float(q[j]);
+          const float sc = cosine ? dot : fmaxf(ssf + s_cc[e] - 2.f * dot, 0.f);
+          if (sbi < 0 || (cosine ? sc > sb : sc < sb)) { sb = sc; sbi = e; }
+        }
+      }
+      // pass 2: candidates within tol of the screening best; exact recheck
+      // unless the best is alone
+      int ncand = 0;
+      int cidx[4];
+      for (int c0 = 0; c0 < kTcN; c0 += 32) {  // warp-uniform (tcgen05.ld is collective)
+        uint32_t q[32];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+            "%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(q[0]), "=r"(q[1]), "=r"(q[2]), "=r"(q[3]), "=r"(q[4]), "=r"(q[5]), "=r"(q[6]),
+              "=r"(q[7]), "=r"(q[8]), "=r"(q[9]), "=r"(q[10]), "=r"(q[11]), "=r"(q[12]),
+              "=r"(q[13]), "=r"(q[14]), "=r"(q[15]), "=r"(q[16]), "=r"(q[17]), "=r"(q[18]),
+              "=r"(q[19]), "=r"(q[20]), "=r"(q[21]), "=r"(q[22]), "=r"(q[23]), "=r"(q[24]),
+              "=r"(q[25]), "=r"(q[26]), "=r"(q[27]), "=r"(q[28]), "=r"(q[29]), "=r"(q[30]),
+              "=r"(q[31])
+            : "r"(lane_base + (uint32_t)c0));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int e = c0 + j;
+          if (e >= cnt) break;
+          const float dot = __uint_as_float(q[j]);
+          const float sc = cosine ? dot : fmaxf(ssf + s_cc[e] - 2.f * dot, 0.f);
+          const bool cand = cosine ? sc >= sb - tol : sc <= sb + tol;
+          if (cand) {
+            if (ncand < 4) cidx[ncand] = e;
+            ++ncand;
+          }
+        }
+      }
+      // (tcgen05.ld above is warp-collective: every lane ran the loops)
+      if (live) {
+        // candidates of this chunk to merge: the lone screening best, or all
+        // entries within tol re-scored exactly (plus the exact value of the
+        // carried best from earlier chunks, already in bestv)
+        auto exact = [&](int e) -> double {
+          double cvv[16];
+          for (int j = 0; j < wp; ++j) cvv[j] = (double)book[(int64_t)(e0 + e) * width + j];
+          const double dt = blas_dot(v, cvv, wp);
+          if (cosine) return dt;
+          double dd = __dadd_rn(__dadd_rn(ss, s_ccd[e]), -__dmul_rn(2.0, dt));
+          return dd > 0.0 ? dd : 0.0;
+        };
+        auto take = [&](int e, double val) {
+          const int ge = e0 + e;
+          if (!have || (cosine ? val > bestv : val < bestv)) { bestv = val; best = ge; have = true; }
+        };
+        if (ncand <= 1) {
+          take(sbi, exact(sbi));
+        } else if (ncand <= 4) {  // near-tie: exact float64 scores of the candidates
+          for (int c = 0; c < ncand; ++c) take(cidx[c], exact(cidx[c]));
+        } else {  // many near-ties: exact scores of the whole chunk
+          for (int e = 0; e < cnt; ++e) take(e, exact(e));
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+    }
+    if (active) {
+      const int code = live ? best : 0;
+      if (codes32) codes32[r * parts + p] = code;
+      if (rows) vq_write_code(rows, stride, r, p, bits, code);
+    }
+  }
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTcN));
+}
+
 }  // namespace fg
 
 using namespace fg;
@@ -438,15 +725,41 @@ int fg_vq_gather_decode(const fg_codec_desc* c, const void* ids, int ids32, int6
   return FG_OK;
 }
 
-int fg_vq_assign(const void* x, int x_is_f64, int64_t n, int64_t d, int width, int length,
-                 int parts, const float* books, const int32_t* entries, int metric, int bits,
-                 uint8_t* rows, int64_t stride, int32_t* codes32, void* s) {
+static int vq_assign_impl(const void* x, int x_is_f64, int64_t n, int64_t d, int width,
+                          int length, int parts, const float* books, const int32_t* entries,
+                          int metric, int bits, uint8_t* rows, int64_t stride, int32_t* codes32,
+                          void* s, bool allow_tc) {
   FG_CHECK_ARG(width >= 1 && width <= kMaxWidth, "fg_vq_assign: width must be in [1, %d]", kMaxWidth);
   FG_CHECK_ARG(parts == (int)((d + width - 1) / width), "fg_vq_assign: parts != ceil(d/width)");
   FG_CHECK_ARG(metric == FG_METRIC_COSINE || metric == FG_METRIC_EUCLIDEAN, "bad metric");
   FG_CHECK_ARG(rows == nullptr || (stride >= ((int64_t)parts * bits + 7) / 8 && stride % 16 == 0),
                "fg_vq_assign: bad row_stride");
   if (n == 0) return FG_OK;
+  if (allow_tc && width <= 16) {  // tensor-core screen + exact recheck
+    cudaStream_t st = as_stream(s);
+    if (rows) FG_CUDA_TRY(cudaMemsetAsync(rows, 0, n * stride, st));
+    const int KB = width <= 8 ? 2 : 4;
+    const int64_t smem = 2 * (int64_t)kTcRows * KB * 16 + 2 * (int64_t)kTcN * KB * 16 +
+                         kTcN * 4 + kTcN * 8 + 8 + 8 + 16;
+    const int64_t ntiles = ceil_div(n, kTcRows);
+    const int gx = (int)std::max<int64_t>(1, min64(ntiles, ceil_div(2 * sm_count(), parts)));
+    dim3 grid(gx, parts);
+    if (x_is_f64) {
+      FG_CUDA_TRY(cudaFuncSetAttribute(k_vq_assign_tc<double>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      k_vq_assign_tc<double><<<grid, kTcRows, smem, st>>>((const double*)x, n, d, width, length,
+                                                          parts, books, entries, metric, bits,
+                                                          rows, stride, codes32, KB);
+    } else {
+      FG_CUDA_TRY(cudaFuncSetAttribute(k_vq_assign_tc<float>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      k_vq_assign_tc<float><<<grid, kTcRows, smem, st>>>((const float*)x, n, d, width, length,
+                                                         parts, books, entries, metric, bits,
+                                                         rows, stride, codes32, KB);
+    }
+    FG_LAUNCH_CHECK();
+    return FG_OK;
+  }
   const int64_t budget = 160 * 1024;  // bytes of smem for one codebook tile
   const int tile = (int)min64(length, budget / ((int64_t)(width + 1) * sizeof(double)));
   const int64_t smem = ((int64_t)tile * width + tile) * (int64_t)sizeof(double);
@@ -468,6 +781,20 @@ int fg_vq_assign(const void* x, int x_is_f64, int64_t n, int64_t d, int width, i
   }
   FG_LAUNCH_CHECK();
   return FG_OK;
+}
+
+int fg_vq_assign(const void* x, int x_is_f64, int64_t n, int64_t d, int width, int length,
+                 int parts, const float* books, const int32_t* entries, int metric, int bits,
+                 uint8_t* rows, int64_t stride, int32_t* codes32, void* s) {
+  return vq_assign_impl(x, x_is_f64, n, d, width, length, parts, books, entries, metric, bits,
+                        rows, stride, codes32, s, true);
+}
+
+int fg_vq_assign_fp64(const void* x, int x_is_f64, int64_t n, int64_t d, int width, int length,
+                      int parts, const float* books, const int32_t* entries, int metric, int bits,
+                      uint8_t* rows, int64_t stride, int32_t* codes32, void* s) {
+  return vq_assign_impl(x, x_is_f64, n, d, width, length, parts, books, entries, metric, bits,
+                        rows, stride, codes32, s, false);
 }
 
 }  // extern "C"

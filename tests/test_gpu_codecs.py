@@ -141,3 +141,52 @@ def test_device_codec_close_and_bf16():
     dc.close()
     with pytest.raises(fg.DataError):
         dc.gather(ids)
+
+
+def _assign_dev(x, books, w, metric, fp64):
+    """fg_vq_assign (tensor-core screen) or fg_vq_assign_fp64 on device rows."""
+    import torch
+    from paper_2207_14696_b200 import _native as N
+    from paper_2207_14696_b200.vq import DeviceVqCodec, METRICS
+    n, d = x.shape
+    L = max(b.shape[0] for b in books)
+    p = fg.VqParams(w, L, metric=metric)
+    dc = DeviceVqCodec.empty(p, d, books, n, "cuda")
+    xt = torch.from_numpy(x).cuda()
+    codes = torch.empty((n, dc.num_parts), dtype=torch.int32, device="cuda")
+    N.call("fg_vq_assign_fp64" if fp64 else "fg_vq_assign", N.ptr(xt), 0, n, d, w, L,
+           dc.num_parts, N.ptr(dc.table), N.ptr(dc.entries), METRICS.index(metric), dc.bits,
+           N.ptr(dc.rows), dc.row_stride, N.ptr(codes), N.stream_handle())
+    return codes.cpu().numpy(), dc
+
+
+@pytest.mark.parametrize("metric", ["cosine", "euclidean"])
+@pytest.mark.parametrize("w,L,d", [(4, 256, 100), (8, 256, 96), (16, 64, 40), (3, 300, 14),
+                                   (8, 1000, 24), (1, 16, 5)])
+def test_vq_assign_tensor_core_screen_exact_under_ties(metric, w, L, d):
+    """Rows equal to codebook entries, duplicated entries (exact ties -> first
+    index), entries a few ulps apart and zero rows: the tcgen05 screen plus
+    float64 recheck returns the float64 path's codes, which are the oracle's."""
+    r = np.random.default_rng(w * 7 + L + d)
+    parts = (d + w - 1) // w
+    books = []
+    for p in range(parts):
+        wp = min(w, d - p * w)
+        b = r.standard_normal((L, wp)).astype(np.float32)
+        b[5] = b[2]                                       # exact duplicate
+        b[7] = np.nextafter(b[3], np.float32(np.inf))     # one ulp apart
+        b[9] = b[4] * np.float32(1.0000001)
+        books.append(b)
+    n = 20_000
+    x = r.standard_normal((n, d)).astype(np.float32)
+    for p in range(parts):  # rows that sit exactly on / between entries
+        sl = slice(p * w, min(d, p * w + w))
+        x[:2000, sl] = books[p][r.integers(0, L, 2000)]
+        x[2000:3000, sl] = 0.5 * (books[p][2] + books[p][3])
+        x[3000:3100, sl] = 0.0
+    x[4000:4100] *= np.float32(1e-20)
+    got, _ = _assign_dev(x, books, w, metric, fp64=False)
+    ref, _ = _assign_dev(x, books, w, metric, fp64=True)
+    assert np.array_equal(got, ref), (metric, int((got != ref).sum()))
+    want = oc.vq_assign(x[:3000], tuple(books), w, metric)
+    assert np.array_equal(got[:3000], want)

@@ -39,7 +39,8 @@ def main():
     dev = torch.device("cuda", 0)
     sg, dc, desc, fanouts, bs, hidden = bench.build_workload(a.config, dev)
     tr = SageTrainer(sg.graph, dc, sg.labels, sg.num_classes,
-                     TrainConfig(fanouts=fanouts, batch_size=bs, hidden=hidden))
+                     TrainConfig(fanouts=fanouts, batch_size=bs, hidden=hidden,
+                                 pipeline=False))
     tr.begin_epoch(sg.train_ids, 0)
     L = len(fanouts)
     flush = torch.zeros(128 * 1024 * 1024, device=dev)

@@ -28,13 +28,14 @@ def main():
                      TrainConfig(fanouts=fanouts, batch_size=bs, hidden=hidden))
     tr.begin_epoch(sg.train_ids, 0)
     for b in range(3):
-        tr.sampler.load_seeds(b)
-        tr._body()
+        tr.step(b)
     torch.cuda.synchronize()
     for i in range(a.steps):
-        tr.sampler.load_seeds(3 + i)
+        b = 3 + i
+        tr.prepare(b)  # seeds of the batch this step samples (outside the range)
+        torch.cuda.synchronize()
         torch.cuda.nvtx.range_push("step")
-        tr._body()
+        tr._body(b % len(tr.samplers))
         torch.cuda.synchronize()
         torch.cuda.nvtx.range_pop()
     print("profiled", a.steps, "steps of", desc)

@@ -17,7 +17,8 @@ def main():
     dev = torch.device("cuda", 0)
     sg, dc, desc, fanouts, bs, hidden = bench.build_workload(cfg, dev)
     tr = SageTrainer(sg.graph, dc, sg.labels, sg.num_classes,
-                     TrainConfig(fanouts=fanouts, batch_size=bs, hidden=hidden))
+                     TrainConfig(fanouts=fanouts, batch_size=bs, hidden=hidden,
+                                 pipeline=False))
     tr.begin_epoch(sg.train_ids, 0)
     for b in range(3):
         tr.sampler.load_seeds(b)
