@@ -341,6 +341,7 @@ __global__ void k_vq_assign(const XT* __restrict__ x, int64_t n, int64_t d, int 
 // (k_vq_assign above / vq.py:306-327).
 constexpr int kTcRows = 128;
 constexpr int kTcN = 256;
+constexpr int kTcCand = 8;  // near-tie candidates re-scored exactly before a full rescoring
 
 __device__ __forceinline__ uint32_t tc_smem(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -429,44 +430,55 @@ k_vq_assign_tc(const XT* __restrict__ x, int64_t n, int64_t d, int width, int le
   const int64_t ntiles = (n + kTcRows - 1) / kTcRows;
   const int nchunks = (L + kTcN - 1) / kTcN;
   int64_t tile = blockIdx.x;
+  bool b_ready = false;
   // per-row state carried across chunks
   for (; tile < ntiles; tile += gridDim.x) {
     const int64_t r = tile * kTcRows + tid;
     const bool active = r < n;
-    double v[16];
+    float xf[16];
     double ss = 0.0;
     bool live = active;
 #pragma unroll
-    for (int j = 0; j < 16; ++j) v[j] = 0.0;
+    for (int j = 0; j < 16; ++j) xf[j] = 0.f;
     if (active) {
-      for (int j = 0; j < wp; ++j) v[j] = (double)x[r * d + lo + j];
-      ss = np_pairwise_sumsq(v, wp);
+      for (int j = 0; j < wp; ++j) {
+        const double xv = (double)x[r * d + lo + j];
+        xf[j] = (float)xv;
+        ss = fma(xv, xv, ss);  // > 0 iff the sub-vector is non-zero (no fp64 underflow)
+      }
       if (cosine) {
-        const double nrm = sqrt(ss);  // np.linalg.norm (vq.py:310)
-        if (nrm > 0.0) {
-          for (int j = 0; j < wp; ++j) v[j] = __ddiv_rn(v[j], nrm);
+        if (ss > 0.0) {
+          const float inv = (float)(1.0 / sqrt(ss));  // screening only: ~1e-7 relative
+          for (int j = 0; j < wp; ++j) xf[j] *= inv;
         } else {
           live = false;
         }
       }
     }
-    double xn1 = 0.0;  // sum |x_j| for the screening bound
-    for (int j = 0; j < wp; ++j) xn1 += fabs(v[j]);
+    float xn1 = 0.f;  // sum |x_j| for the screening bound
+    for (int j = 0; j < wp; ++j) xn1 += fabsf(xf[j]);
     // A row: split of the (normalised) row, zero padded to K = 4 * KB
     for (int k = 0; k < 4 * KB; ++k) {
       uint32_t h = 0, l = 0;
-      if (live && k < wp) tf32_split((float)v[k], h, l);
+      if (live && k < wp) tf32_split(xf[k], h, l);
       *reinterpret_cast<uint32_t*>(sAh + tc_off(tid, k, KB)) = h;
       *reinterpret_cast<uint32_t*>(sAl + tc_off(tid, k, KB)) = l;
     }
-    int best = 0;
-    double bestv = 0.0;  // exact value of the current best (when resolved)
-    bool have = false;
+    // screening best / runner-up over all chunks, and the largest tolerance
+    float sb = 0.f, s2 = 0.f, tolmax = 0.f;
+    int sbi = -1;
+    bool has2 = false;
+    int cand[kTcCand];
+    int ncand = 0, prev_best = -1;
+    bool prev_tie = false;
     for (int ch = 0; ch < nchunks; ++ch) {
       const int e0 = ch * kTcN;
       const int cnt = min(kTcN, L - e0);
       __syncthreads();  // previous chunk's epilogue done with B / TMEM
-      // B: this chunk's entries (split) + their norms
+      // B: this chunk's entries (split) + their norms (once per CTA when the
+      // codebook part is a single chunk)
+      if (nchunks > 1 || !b_ready) {
+      b_ready = true;
       for (int i = tid; i < kTcN * 4 * KB; i += kTcRows) {
         const int e = i / (4 * KB), k = i - e * (4 * KB);
         uint32_t h = 0, l = 0;
@@ -492,6 +504,7 @@ k_vq_assign_tc(const XT* __restrict__ x, int64_t n, int64_t d, int width, int le
       // chunk max |c_j| (for the screening bound)
       for (int o = 16; o; o >>= 1) cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, o));
       if ((tid & 31) == 0) s_cmax[warp] = cm;
+      }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncthreads();
       if (tid == 0) {
@@ -516,39 +529,11 @@ k_vq_assign_tc(const XT* __restrict__ x, int64_t n, int64_t d, int width, int le
       asm volatile("tcgen05.fence::after_thread_sync;");
       const float cmax = fmaxf(fmaxf(s_cmax[0], s_cmax[1]), fmaxf(s_cmax[2], s_cmax[3]));
       // screening tolerance: 20x the 3xTF32 score error bound
-      const float tol_dot = 1e-4f * (float)xn1 * cmax + 1e-30f;
-      const float tol = cosine ? tol_dot : 2.f * tol_dot + 1e-6f * (float)(ss + (double)cmax * cmax * wp);
+      const float tol_dot = 1e-4f * xn1 * cmax + 1e-30f;
       const float ssf = (float)ss;
-      // pass 1: screening best of this chunk (first max / first min)
-      float sb = 0.f;
-      int sbi = -1;
+      const float tol = cosine ? tol_dot : 2.f * tol_dot + 1e-6f * (ssf + cmax * cmax * wp);
+      tolmax = fmaxf(tolmax, tol);
       const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
-      for (int c0 = 0; c0 < kTcN; c0 += 32) {
-        uint32_t q[32];
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
-            "%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-            : "=r"(q[0]), "=r"(q[1]), "=r"(q[2]), "=r"(q[3]), "=r"(q[4]), "=r"(q[5]), "=r"(q[6]),
-              "=r"(q[7]), "=r"(q[8]), "=r"(q[9]), "=r"(q[10]), "=r"(q[11]), "=r"(q[12]),
-              "=r"(q[13]), "=r"(q[14]), "=r"(q[15]), "=r"(q[16]), "=r"(q[17]), "=r"(q[18]),
-              "=r"(q[19]), "=r"(q[20]), "=r"(q[21]), "=r"(q[22]), "=r"(q[23]), "=r"(q[24]),
-              "=r"(q[25]), "=r"(q[26]), "=r"(q[27]), "=r"(q[28]), "=r"(q[29]), "=r"(q[30]),
-              "=r"(q[31])
-            : "r"(lane_base + (uint32_t)c0));
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int e = c0 + j;
-          if (e >= cnt) break;
-          const float dot = __uint_as_float(q[j]);
-          const float sc = cosine ? dot : fmaxf(ssf + s_cc[e] - 2.f * dot, 0.f);
-          if (sbi < 0 || (cosine ? sc > sb : sc < sb)) { sb = sc; sbi = e; }
-        }
-      }
-      // pass 2: candidates within tol of the screening best; exact recheck
-      // unless the best is alone
-      int ncand = 0;
-      int cidx[4];
       for (int c0 = 0; c0 < kTcN; c0 += 32) {  // warp-uniform (tcgen05.ld is collective)
         uint32_t q[32];
         asm volatile(
@@ -562,45 +547,94 @@ k_vq_assign_tc(const XT* __restrict__ x, int64_t n, int64_t d, int width, int le
               "=r"(q[31])
             : "r"(lane_base + (uint32_t)c0));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (c0 >= cnt) continue;
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           const int e = c0 + j;
-          if (e >= cnt) break;
           const float dot = __uint_as_float(q[j]);
-          const float sc = cosine ? dot : fmaxf(ssf + s_cc[e] - 2.f * dot, 0.f);
-          const bool cand = cosine ? sc >= sb - tol : sc <= sb + tol;
-          if (cand) {
-            if (ncand < 4) cidx[ncand] = e;
-            ++ncand;
+          float sc = cosine ? dot : fmaxf(fmaf(-2.f, dot, ssf + s_cc[e]), 0.f);
+          if (e >= cnt) sc = cosine ? -INFINITY : INFINITY;
+          if (sbi < 0) { sb = sc; sbi = e0 + e; continue; }
+          const bool better = cosine ? sc > sb : sc < sb;
+          if (better) { s2 = sb; has2 = true; sb = sc; sbi = e0 + e; }
+          else if (!has2 || (cosine ? sc > s2 : sc < s2)) { s2 = sc; has2 = true; }
+        }
+      }
+      // near-tie rows of the warp: record this chunk's entries within tol of
+      // the running best (a superset of those within tol of the final best)
+      const bool tie = live && has2 && !(cosine ? s2 < sb - tolmax : s2 > sb + tolmax);
+      if (tie && !prev_tie && prev_best >= 0) {
+        // entries of earlier chunks were all below the then-best by more
+        // than tol, so only that best itself can still be a candidate
+        if (ncand < kTcCand) cand[ncand] = prev_best;
+        ++ncand;
+      }
+      if (__any_sync(0xffffffffu, tie)) {
+        for (int c0 = 0; c0 < kTcN; c0 += 32) {
+          uint32_t q[32];
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+              "%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+              : "=r"(q[0]), "=r"(q[1]), "=r"(q[2]), "=r"(q[3]), "=r"(q[4]), "=r"(q[5]), "=r"(q[6]),
+                "=r"(q[7]), "=r"(q[8]), "=r"(q[9]), "=r"(q[10]), "=r"(q[11]), "=r"(q[12]),
+                "=r"(q[13]), "=r"(q[14]), "=r"(q[15]), "=r"(q[16]), "=r"(q[17]), "=r"(q[18]),
+                "=r"(q[19]), "=r"(q[20]), "=r"(q[21]), "=r"(q[22]), "=r"(q[23]), "=r"(q[24]),
+                "=r"(q[25]), "=r"(q[26]), "=r"(q[27]), "=r"(q[28]), "=r"(q[29]), "=r"(q[30]),
+                "=r"(q[31])
+              : "r"(lane_base + (uint32_t)c0));
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          if (!tie || c0 >= cnt) continue;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int e = c0 + j;
+            if (e >= cnt) break;
+            const float dot = __uint_as_float(q[j]);
+            const float sc = cosine ? dot : fmaxf(fmaf(-2.f, dot, ssf + s_cc[e]), 0.f);
+            if (cosine ? sc >= sb - tolmax : sc <= sb + tolmax) {
+              if (ncand < kTcCand) cand[ncand] = e0 + e;
+              ++ncand;
+            }
           }
         }
       }
-      // (tcgen05.ld above is warp-collective: every lane ran the loops)
-      if (live) {
-        // candidates of this chunk to merge: the lone screening best, or all
-        // entries within tol re-scored exactly (plus the exact value of the
-        // carried best from earlier chunks, already in bestv)
-        auto exact = [&](int e) -> double {
+      if (!tie) ncand = 0;  // no near-tie so far: nothing but sbi can matter
+      prev_tie = tie;
+      prev_best = sbi;
+      asm volatile("tcgen05.fence::before_thread_sync;");
+    }
+    int best = 0;
+    if (live) {
+      // the screening best is provably the float64 best unless the runner-up
+      // is within 2x the error bound (tol is 20x); near-ties re-score every
+      // entry in float64 with the reference's operation order (rare path)
+      const bool alone = !has2 || (cosine ? s2 < sb - tolmax : s2 > sb + tolmax);
+      if (alone) {
+        best = sbi;
+      } else {
+        double v[16];
+        for (int j = 0; j < wp; ++j) v[j] = (double)x[r * d + lo + j];
+        const double ssx = np_pairwise_sumsq(v, wp);
+        if (cosine) {
+          const double nrm = sqrt(ssx);  // np.linalg.norm (vq.py:310)
+          for (int j = 0; j < wp; ++j) v[j] = __ddiv_rn(v[j], nrm);
+        }
+        double bestv = 0.0;
+        const bool few = ncand <= kTcCand;  // else every entry
+        const int ne = few ? ncand : L;
+        for (int i = 0; i < ne; ++i) {
+          const int e = few ? cand[i] : i;
           double cvv[16];
-          for (int j = 0; j < wp; ++j) cvv[j] = (double)book[(int64_t)(e0 + e) * width + j];
+          for (int j = 0; j < wp; ++j) cvv[j] = (double)book[(int64_t)e * width + j];
           const double dt = blas_dot(v, cvv, wp);
-          if (cosine) return dt;
-          double dd = __dadd_rn(__dadd_rn(ss, s_ccd[e]), -__dmul_rn(2.0, dt));
-          return dd > 0.0 ? dd : 0.0;
-        };
-        auto take = [&](int e, double val) {
-          const int ge = e0 + e;
-          if (!have || (cosine ? val > bestv : val < bestv)) { bestv = val; best = ge; have = true; }
-        };
-        if (ncand <= 1) {
-          take(sbi, exact(sbi));
-        } else if (ncand <= 4) {  // near-tie: exact float64 scores of the candidates
-          for (int c = 0; c < ncand; ++c) take(cidx[c], exact(cidx[c]));
-        } else {  // many near-ties: exact scores of the whole chunk
-          for (int e = 0; e < cnt; ++e) take(e, exact(e));
+          double val = dt;
+          if (!cosine) {
+            val = __dadd_rn(__dadd_rn(ssx, np_pairwise_sumsq(cvv, wp)), -__dmul_rn(2.0, dt));
+            val = val > 0.0 ? val : 0.0;
+          }
+          // candidates ascend, so strict improvement keeps the first index
+          if (i == 0 || (cosine ? val > bestv : val < bestv)) { bestv = val; best = e; }
         }
       }
-      asm volatile("tcgen05.fence::before_thread_sync;");
     }
     if (active) {
       const int code = live ? best : 0;
