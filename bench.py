@@ -40,7 +40,15 @@ CONFIGS = {
     "arxiv": ("arxiv", ("sq", 8), (10, 5), 1024, 256),
     "papers100m": ("papers100m", ("sq", 4), (15, 10, 5), 1024, 256),
     "mag240m": ("mag240m", ("vq", 8, 256), (15, 10, 5), 1024, 256),
+    # BASELINE config E: aggregator variants through the fused gather path
+    "products-gcn": ("products", ("sq", 8), (15, 10, 5), 1024, 256, "gcn"),
+    "products-sq8": ("products", ("sq", 8), (15, 10, 5), 1024, 256),
 }
+
+
+def aggregator_of(cfg_name):
+    spec = CONFIGS[cfg_name]
+    return spec[5] if len(spec) > 5 else "mean"
 
 
 def committed_traffic(config):
@@ -146,7 +154,7 @@ class ClockSampler:
 def build_workload(cfg_name, device, seed=0, scale=1.0):
     import torch
     from paper_2207_14696_b200.synth import SHAPES, build_sq_codec, build_vq_codec, make_shape
-    shape, codec_spec, fanouts, bs, hidden = CONFIGS[cfg_name]
+    shape, codec_spec, fanouts, bs, hidden = CONFIGS[cfg_name][:5]
     t0 = time.perf_counter()
     sg = make_shape(shape, seed=seed, scale=scale, device=device)
     torch.cuda.synchronize()
@@ -187,7 +195,9 @@ def run_ours(args, rank, world, local):
     torch.cuda.set_device(dev)
     sg, dc, codec_desc, fanouts, bs, hidden = build_workload(args.config, dev, scale=args.scale)
     pg = dist.group.WORLD if world > 1 else None
-    cfg = TrainConfig(fanouts=fanouts, batch_size=bs, hidden=hidden, lr=3e-3, seed=0)
+    agg_kind = aggregator_of(args.config)
+    cfg = TrainConfig(fanouts=fanouts, batch_size=bs, hidden=hidden, lr=3e-3, seed=0,
+                      aggregator=agg_kind)
     tr = SageTrainer(sg.graph, dc, sg.labels, sg.num_classes, cfg, process_group=pg)
     nb = tr.begin_epoch(sg.train_ids, 0)
     need = args.warmup + 2 * args.steps + 3
@@ -265,7 +275,7 @@ def run_ours(args, rank, world, local):
         # enqueue, so the event pair brackets the kernel alone)
         s.record()
         gather_dequant_mean(dc, sb.indptr[L - 1], sb.picks[L - 1], sb.n_nodes[L - 1],
-                            tr.caps[L - 1], out=tr.agg)
+                            tr.caps[L - 1], out=tr.agg, edge_w=sb.ew[L - 1] if sb.ew else None)
         e.record()
         e.synchronize()
         kt.append(s.elapsed_time(e))
@@ -273,7 +283,9 @@ def run_ours(args, rank, world, local):
         # algorithmic bytes: E code rows + int32 source ids, N_dst indptr
         # entries + output rows (the padded rows past N_dst are zero-filled
         # but not counted)
-        kbytes.append(E * (row_bytes + 4) + nd * (4 + dc.d * out_b))
+        # (+4 B edge weight per pick for the weighted aggregators)
+        wb = 4 if agg_kind != "mean" else 0
+        kbytes.append(E * (row_bytes + 4 + wb) + nd * (4 + dc.d * out_b))
     avg_ms = sum(kt) / len(kt)
     ceiling = gather_ceiling(row_bytes)
     avg_bytes = sum(kbytes) / len(kbytes)
@@ -295,7 +307,8 @@ def run_ours(args, rank, world, local):
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic (planted-partition power-law graph, class-conditional features)",
-        "config": {"workload": f"{args.config}-shape GraphSAGE {len(fanouts)}-layer "
+        "config": {"workload": f"{args.config}-shape "
+                               f"{'GCN' if agg_kind == 'gcn' else 'GraphSAGE'} {len(fanouts)}-layer "
                                f"fanout {list(fanouts)}, {codec_desc}",
                    "nodes": sg.graph.n, "edges_stored": sg.graph.nnz, "feature_dim": dc.d,
                    "global_batch": seeds_per_step, "per_rank_batch": bs, "hidden": hidden,
@@ -317,7 +330,8 @@ def run_ours(args, rank, world, local):
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        result["cpu_baseline"] = cpu_baseline(sg, dc, fanouts, hidden, budget_s=args.cpu_budget)
+        result["cpu_baseline"] = cpu_baseline(sg, dc, fanouts, hidden, budget_s=args.cpu_budget,
+                                              aggregator=agg_kind)
     if rank == 0:
         print(json.dumps(result), flush=True)
 
@@ -352,7 +366,7 @@ def _host_world(sg, dc):
     return host, labels, decode
 
 
-def cpu_baseline(sg, dc, fanouts, hidden, budget_s=20.0, batch=128):
+def cpu_baseline(sg, dc, fanouts, hidden, budget_s=20.0, batch=128, aggregator="mean"):
     """Oracle port of the reference path on the host cores: numpy sampler
     (pipeline.py:185-222 restated) + numpy decoder + CPU fp32 SAGE step."""
     import torch
@@ -364,7 +378,8 @@ def cpu_baseline(sg, dc, fanouts, hidden, budget_s=20.0, batch=128):
     train = sg.train_ids
     while True:
         ot.train_epoch(model, opt, host.row_offsets, host.col_indices, labels,
-                       train[steps * batch:(steps + 1) * batch], fanouts, batch, steps, decode)
+                       train[steps * batch:(steps + 1) * batch], fanouts, batch, steps, decode,
+                       aggregator=aggregator)
         steps += 1
         seeds_done += batch
         if time.perf_counter() - t0 >= budget_s or steps * batch >= train.size:
@@ -396,7 +411,8 @@ def run_reference(args, rank, world, local):
 
     def one(i):
         ot.train_epoch(model, opt, host.row_offsets, host.col_indices, labels,
-                       train[i * batch:(i + 1) * batch], fanouts, batch, i, decode)
+                       train[i * batch:(i + 1) * batch], fanouts, batch, i, decode,
+                       aggregator=aggregator_of(args.config))
 
     for i in range(args.warmup):
         one(i)

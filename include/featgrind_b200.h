@@ -43,6 +43,10 @@ extern "C" {
 #define FG_OUT_BF16 1
 #define FG_OUT_F64 2
 
+/* aggregators (fg_block_edge_weights) */
+#define FG_AGG_MEAN 0
+#define FG_AGG_GCN 1
+
 #define FG_CODEC_SQ 1
 #define FG_CODEC_VQ 2
 
@@ -194,6 +198,24 @@ int fg_gather_dequant_mean(const fg_codec_desc* codec, const int32_t* indptr,
                            const int32_t* src, const int64_t* num_dst_dev,
                            int64_t max_dst, void* out, int64_t out_ld,
                            int out_dtype, void* cuda_stream);
+/* Aggregator variants through the same fused kernels: out[v, :d] =
+ * sum_{e in indptr[v]..indptr[v+1]} edge_w[e] * decode(codec, src[e]) (no
+ * 1/cnt; the weights carry the normalisation).  edge_w from
+ * fg_block_edge_weights (GCN) or any per-edge weights.  Same layouts and
+ * errors as fg_gather_dequant_mean. */
+int fg_gather_dequant_wsum(const fg_codec_desc* codec, const int32_t* indptr,
+                           const int32_t* src, const float* edge_w, const int64_t* num_dst_dev,
+                           int64_t max_dst, void* out, int64_t out_ld, int out_dtype,
+                           void* cuda_stream);
+/* Per-edge weights of a sampled block (dst v = slot of dst_nodes, edges
+ * indptr[v]..indptr[v+1] with source node ids src_nodes[e]):
+ * FG_AGG_MEAN -> 1/cnt_v; FG_AGG_GCN -> sqrt(deg(v)) / (cnt_v sqrt(deg(u))),
+ * the sampled estimator of D^-1/2 A D^-1/2 (full-graph degrees incl. the
+ * self-loop, from row_offsets). */
+int fg_block_edge_weights(int kind, const int64_t* row_offsets, const int32_t* dst_nodes,
+                          const int32_t* indptr, const int32_t* src_nodes,
+                          const int64_t* n_dst_dev, int64_t max_dst, float* edge_w,
+                          void* cuda_stream);
 
 /* Hidden-layer mean over a block with local source indices (bf16 in/out,
  * fp32 accumulate); `relu_in` applies max(0, .) to source rows on load (the
@@ -206,7 +228,7 @@ int fg_block_mean_fwd(const uint16_t* h_src, int64_t h_dim,
                       const int32_t* indptr, const int32_t* src_local,
                       const int64_t* num_dst_dev, int64_t max_dst,
                       uint16_t* out, int64_t out_ld, int relu_in,
-                      void* cuda_stream);
+                      const float* edge_w, void* cuda_stream);
 int fg_block_mean_bwd(const uint16_t* grad_out, int64_t h_dim,
                       const int32_t* indptr, const int32_t* src_local,
                       const int64_t* num_dst_dev, int64_t max_dst,
@@ -229,7 +251,8 @@ int fg_block_transpose(const int32_t* src_local, const int64_t* n_edges_dev,
                        int64_t cap_e, const int32_t* indptr,
                        const int64_t* num_dst_dev, int64_t max_dst, int max_per_dst,
                        int64_t cap_src,
-                       int32_t* t_indptr, int32_t* t_dst, float* t_w, void* scratch,
+                       int32_t* t_indptr, int32_t* t_dst, float* t_w,
+                       const float* edge_w, void* scratch,
                        int64_t scratch_bytes, void* cuda_stream);
 int fg_block_mean_bwd_t(const uint16_t* grad_out, int64_t h_dim, int64_t g_ld,
                         const int32_t* t_indptr, const int32_t* t_dst,
@@ -254,7 +277,7 @@ int fg_block_mean_wgrad_supported(int64_t h_dim, int64_t p_dim);
 int64_t fg_block_mean_wgrad_scratch_bytes(int64_t h_dim, int64_t p_dim);
 int fg_block_mean_wgrad(const uint16_t* grad_out, int64_t g_ld, const int32_t* indptr,
                         const int32_t* local, const int64_t* n_dst_dev, int64_t max_dst,
-                        const uint16_t* h_mask, int64_t h_dim,
+                        const float* edge_w, const uint16_t* h_mask, int64_t h_dim,
                         const uint16_t* x, int64_t p_dim, float* dw, float* scratch,
                         int64_t scratch_bytes, void* cuda_stream);
 

@@ -16,6 +16,7 @@ import torch.nn as nn
 import torch.nn.functional as F
 
 from .aggregate import block_mean as np_block_mean
+from .aggregate import block_wsum, gcn_weights
 from .sampler import sample_batches_oracle
 
 
@@ -26,41 +27,56 @@ class OracleSage(nn.Module):
         self.lins = nn.ModuleList(nn.Linear(dims[i], dims[i + 1]) for i in range(num_layers))
 
     def forward(self, agg_in, blocks):
-        """blocks[l] = (counts, local) for l < L-1 (local indexes layer l+1)."""
+        """blocks[l] = (counts, local[, weights]) for l < L-1 (local indexes
+        layer l+1); with weights the block is the weighted sum (GCN)."""
         L = len(self.lins)
         h = self.lins[0](agg_in)
         for i in range(1, L):
             h = F.relu(h)
             l = L - 1 - i
-            counts, local = blocks[l]
+            counts, local = blocks[l][0], blocks[l][1]
             seg = torch.repeat_interleave(torch.arange(counts.numel()), counts)
-            a = torch.zeros(counts.numel(), h.shape[1]).index_add_(0, seg, h[local])
-            a = a / counts.clamp_min(1)[:, None].float()
+            if len(blocks[l]) > 2:
+                a = torch.zeros(counts.numel(), h.shape[1]).index_add_(
+                    0, seg, h[local] * blocks[l][2][:, None])
+            else:
+                a = torch.zeros(counts.numel(), h.shape[1]).index_add_(0, seg, h[local])
+                a = a / counts.clamp_min(1)[:, None].float()
             h = self.lins[i](a)
         return h
 
 
-def batch_tensors(batch, decode_rows):
-    """Input aggregate (float64 mean -> fp32) and hidden blocks of one batch."""
+def batch_tensors(batch, decode_rows, aggregator="mean", off=None):
+    """Input aggregate (float64 -> fp32) and hidden blocks of one batch;
+    aggregator 'gcn' weights every block by gcn_weights (needs row offsets)."""
     L = len(batch.layers)
     last = batch.layers[-1]
     dec = decode_rows(last.picks)
-    agg = torch.from_numpy(np_block_mean(dec, last.counts).astype(np.float32))
+    if aggregator == "gcn":
+        w = gcn_weights(off, last.nodes, last.counts, last.picks)
+        agg = torch.from_numpy(block_wsum(dec, last.counts, w).astype(np.float32))
+    else:
+        agg = torch.from_numpy(np_block_mean(dec, last.counts).astype(np.float32))
     blocks = []
     for l in range(L - 1):
+        lay = batch.layers[l]
         nxt = batch.layers[l + 1].nodes
-        local = np.searchsorted(nxt, batch.layers[l].picks)
-        blocks.append((torch.from_numpy(batch.layers[l].counts), torch.from_numpy(local)))
+        local = np.searchsorted(nxt, lay.picks)
+        blk = (torch.from_numpy(lay.counts), torch.from_numpy(local))
+        if aggregator == "gcn":
+            wl = gcn_weights(off, lay.nodes, lay.counts, lay.picks).astype(np.float32)
+            blk = blk + (torch.from_numpy(wl),)
+        blocks.append(blk)
     return agg, blocks
 
 
 def train_epoch(model, opt, off, col, labels, train_ids, fanouts, bs, seed, decode_rows,
-                max_batches=None):
+                max_batches=None, aggregator="mean"):
     batches, _ = sample_batches_oracle(off, col, train_ids, fanouts, bs, seed,
                                        max_batches=max_batches)
     losses = []
     for b in batches:
-        agg, blocks = batch_tensors(b, decode_rows)
+        agg, blocks = batch_tensors(b, decode_rows, aggregator, off)
         logits = model(agg, blocks)
         loss = F.cross_entropy(logits, torch.from_numpy(labels[b.seeds]).long())
         opt.zero_grad()
@@ -71,11 +87,12 @@ def train_epoch(model, opt, off, col, labels, train_ids, fanouts, bs, seed, deco
 
 
 @torch.no_grad()
-def evaluate(model, off, col, labels, ids, fanouts, bs, seed, decode_rows, max_batches=None):
+def evaluate(model, off, col, labels, ids, fanouts, bs, seed, decode_rows, max_batches=None,
+             aggregator="mean"):
     batches, _ = sample_batches_oracle(off, col, ids, fanouts, bs, seed, max_batches=max_batches)
     correct = total = 0
     for b in batches:
-        agg, blocks = batch_tensors(b, decode_rows)
+        agg, blocks = batch_tensors(b, decode_rows, aggregator, off)
         pred = model(agg, blocks).argmax(1).numpy()
         correct += int((pred == labels[b.seeds]).sum())
         total += b.seeds.size

@@ -55,15 +55,19 @@ _SIGS = {
     "fg_vq_gather_decode": (ci, [C.POINTER(CodecDesc), vp, ci, i64, vp, ci, vp, vp]),
     "fg_kmeans_assign": (ci, [vp, i64, ci, vp, ci, ci, vp, vp, vp, vp]),
     "fg_gather_dequant_mean": (ci, [C.POINTER(CodecDesc), vp, vp, vp, i64, vp, i64, ci, vp]),
-    "fg_block_mean_fwd": (ci, [vp, i64, vp, vp, vp, i64, vp, i64, ci, vp]),
+    "fg_gather_dequant_wsum": (ci, [C.POINTER(CodecDesc), vp, vp, vp, vp, i64, vp, i64, ci,
+                                    vp]),
+    "fg_block_edge_weights": (ci, [ci, vp, vp, vp, vp, vp, i64, vp, vp]),
+    "fg_block_mean_fwd": (ci, [vp, i64, vp, vp, vp, i64, vp, i64, ci, vp, vp]),
     "fg_block_mean_bwd": (ci, [vp, i64, vp, vp, vp, i64, vp, vp]),
     "fg_f32_to_bf16": (ci, [vp, i64, vp, vp, vp]),
     "fg_block_transpose_scratch_bytes": (i64, [i64]),
-    "fg_block_transpose": (ci, [vp, vp, i64, vp, vp, i64, ci, i64, vp, vp, vp, vp, i64, vp]),
+    "fg_block_transpose": (ci, [vp, vp, i64, vp, vp, i64, ci, i64, vp, vp, vp, vp, vp, i64, vp]),
     "fg_block_mean_bwd_t": (ci, [vp, i64, i64, vp, vp, vp, vp, i64, vp, vp, vp]),
     "fg_block_mean_wgrad_supported": (ci, [i64, i64]),
     "fg_block_mean_wgrad_scratch_bytes": (i64, [i64, i64]),
-    "fg_block_mean_wgrad": (ci, [vp, i64, vp, vp, vp, i64, vp, i64, vp, i64, vp, vp, i64, vp]),
+    "fg_block_mean_wgrad": (ci, [vp, i64, vp, vp, vp, i64, vp, vp, i64, vp, i64, vp, vp, i64,
+                                 vp]),
     "fg_softmax_ce": (ci, [vp, ci, ci, i64, i64, vp, vp, vp, vp, vp, vp, vp, vp]),
     "fg_adam_step": (ci, [vp, vp, vp, vp, i64, vp, C.c_float, C.c_float, C.c_float, C.c_float,
                           C.c_float, vp, vp]),

@@ -40,15 +40,35 @@ def alloc_aggregate(max_dst: int, d: int, dtype=torch.bfloat16, device="cuda",
 
 
 def gather_dequant_mean(codec, indptr, src, n_dst, max_dst: int, out=None,
-                        out_dtype=torch.bfloat16):
+                        out_dtype=torch.bfloat16, edge_w=None):
     """out[v, :d] = mean_{e in indptr[v]:indptr[v+1]} decode(codec, src[e])
-    for live v < n_dst (rows past n_dst are not written)."""
+    for live v < n_dst (rows past n_dst are not written); with ``edge_w``
+    the edge-weighted sum sum_e edge_w[e] decode(codec, src[e]) instead
+    (aggregator variants, ``fg_gather_dequant_wsum``)."""
     if out is None:
         out = alloc_aggregate(max_dst, codec.d, out_dtype, indptr.device)
     assert out.shape[0] >= max_dst and out.shape[1] >= codec.d and out.is_contiguous()
     code = N.OUT_BF16 if out.dtype == torch.bfloat16 else N.OUT_F32
-    N.call("fg_gather_dequant_mean", ctypes.byref(codec.desc), N.ptr(indptr), N.ptr(src),
-           N.ptr(n_dst), max_dst, N.ptr(out), out.shape[1], code, N.stream_handle())
+    if edge_w is None:
+        N.call("fg_gather_dequant_mean", ctypes.byref(codec.desc), N.ptr(indptr), N.ptr(src),
+               N.ptr(n_dst), max_dst, N.ptr(out), out.shape[1], code, N.stream_handle())
+    else:
+        N.call("fg_gather_dequant_wsum", ctypes.byref(codec.desc), N.ptr(indptr), N.ptr(src),
+               N.ptr(edge_w), N.ptr(n_dst), max_dst, N.ptr(out), out.shape[1], code,
+               N.stream_handle())
+    return out
+
+
+AGGREGATORS = ("mean", "gcn")  # FG_AGG_MEAN, FG_AGG_GCN
+
+
+def edge_weights(kind: str, graph, dst_nodes, indptr, src_nodes, n_dst, max_dst: int, out):
+    """Per-edge weights of a sampled block (``fg_block_edge_weights``):
+    'mean' -> 1/cnt_v; 'gcn' -> sqrt(deg v) / (cnt_v sqrt(deg u)), the sampled
+    estimator of D^-1/2 A D^-1/2 over full-graph degrees."""
+    N.call("fg_block_edge_weights", AGGREGATORS.index(kind), N.ptr(graph.row_offsets),
+           N.ptr(dst_nodes), N.ptr(indptr), N.ptr(src_nodes), N.ptr(n_dst), max_dst, N.ptr(out),
+           N.stream_handle())
     return out
 
 
@@ -59,13 +79,14 @@ class BlockMean(torch.autograd.Function):
 
     @staticmethod
     def forward(ctx, h_src, indptr, local, n_dst, max_dst: int, relu: bool = False,
-                trans=None, bias_col: bool = False):
+                trans=None, bias_col: bool = False, edge_w=None):
         h_src = h_src.contiguous()
         H = h_src.shape[1]
         ld = H + 8 if bias_col else H
+        assert edge_w is None or trans is not None, "edge weights need the gather backward"
         out = torch.empty((max_dst, ld), dtype=torch.bfloat16, device=h_src.device)
         N.call("fg_block_mean_fwd", N.ptr(h_src), H, N.ptr(indptr), N.ptr(local), N.ptr(n_dst),
-               max_dst, N.ptr(out), ld, int(relu), N.stream_handle())
+               max_dst, N.ptr(out), ld, int(relu), N.ptr(edge_w), N.stream_handle())
         t_indptr, t_dst, t_w, n_src = trans if trans is not None else (indptr, indptr, n_dst,
                                                                         n_dst)
         ctx.save_for_backward(indptr, local, n_dst, h_src if relu else indptr, t_indptr, t_dst,
@@ -89,7 +110,7 @@ class BlockMean(torch.autograd.Function):
             N.call("fg_block_mean_bwd_t", N.ptr(g), H, g.shape[1], N.ptr(t_indptr), N.ptr(t_dst),
                    N.ptr(t_w), N.ptr(n_src), ctx.n_src, N.ptr(h_src), N.ptr(gh),
                    N.stream_handle())
-            return gh, None, None, None, None, None, None, None
+            return gh, None, None, None, None, None, None, None, None
         if g.shape[1] != H:
             g = g[:, :H].contiguous()
         acc = torch.zeros((ctx.n_src, H), dtype=torch.float32, device=g.device)
@@ -98,16 +119,17 @@ class BlockMean(torch.autograd.Function):
                ctx.max_dst, N.ptr(acc), s)
         gh = torch.empty((ctx.n_src, H), dtype=torch.bfloat16, device=g.device)
         N.call("fg_f32_to_bf16", N.ptr(acc), acc.numel(), N.ptr(h_src), N.ptr(gh), s)
-        return gh, None, None, None, None, None, None, None
+        return gh, None, None, None, None, None, None, None, None
 
 
 def block_mean(h_src, indptr, local, n_dst, max_dst: int, relu: bool = False, trans=None,
-               bias_col: bool = False):
+               bias_col: bool = False, edge_w=None):
     """``trans`` = (t_indptr, t_dst, t_w, n_src) of the block (DeviceSampler
     with need_transpose) switches the backward to the gather form; ``bias_col``
     appends a [1, 0 x 7] column block (output width H + 8) so the next
-    layer's bias is a column of its weight."""
-    return BlockMean.apply(h_src, indptr, local, n_dst, max_dst, relu, trans, bias_col)
+    layer's bias is a column of its weight; ``edge_w`` turns the mean into
+    the edge-weighted sum (the transpose must carry the same weights)."""
+    return BlockMean.apply(h_src, indptr, local, n_dst, max_dst, relu, trans, bias_col, edge_w)
 
 
 def wgrad_supported(h_dim: int, p_dim: int) -> bool:
@@ -120,7 +142,7 @@ def wgrad_scratch(H: int, P: int, device) -> torch.Tensor:
 
 
 def block_mean_wgrad(g, indptr, local, n_dst, max_dst: int, h_mask, x, dw=None, scratch=None,
-                     H: int | None = None):
+                     H: int | None = None, edge_w=None):
     """dW = dH^T x for the block mean a[v] = mean_e relu(h[local[e]]) with
     upstream gradient g = dL/da, computed as an edge-tiled GEMM
     (``fg_block_mean_wgrad``: per-edge terms relu'(h[l_e]) * g[v_e] / cnt_v
@@ -134,8 +156,8 @@ def block_mean_wgrad(g, indptr, local, n_dst, max_dst: int, h_mask, x, dw=None, 
     if scratch is None:
         scratch = wgrad_scratch(H, P, x.device)
     N.call("fg_block_mean_wgrad", N.ptr(g), g.stride(0), N.ptr(indptr), N.ptr(local),
-           N.ptr(n_dst), max_dst, N.ptr(h_mask) if h_mask is not None else None, H,
-           N.ptr(x), P, N.ptr(dw), N.ptr(scratch), scratch.numel() * 4, N.stream_handle())
+           N.ptr(n_dst), max_dst, N.ptr(edge_w), N.ptr(h_mask) if h_mask is not None else None,
+           H, N.ptr(x), P, N.ptr(dw), N.ptr(scratch), scratch.numel() * 4, N.stream_handle())
     return dw
 
 
@@ -146,25 +168,29 @@ class InputBlockMean(torch.autograd.Function):
     is the decoded input aggregate, not a parameter)."""
 
     @staticmethod
-    def forward(ctx, x, w, indptr, local, n_dst, max_dst, bias_col, scratch):
+    def forward(ctx, x, w, indptr, local, n_dst, max_dst, bias_col, scratch, edge_w):
         h = torch.mm(x, w.to(torch.bfloat16).t())
-        out = block_mean(h, indptr, local, n_dst, max_dst, relu=True, trans=None,
-                         bias_col=bias_col)
-        ctx.save_for_backward(x, h, indptr, local, n_dst)
-        ctx.max_dst, ctx.scratch = max_dst, scratch
+        h_src = h.contiguous()
+        H = h_src.shape[1]
+        ld = H + 8 if bias_col else H
+        out = torch.empty((max_dst, ld), dtype=torch.bfloat16, device=h.device)
+        N.call("fg_block_mean_fwd", N.ptr(h_src), H, N.ptr(indptr), N.ptr(local), N.ptr(n_dst),
+               max_dst, N.ptr(out), ld, 1, N.ptr(edge_w), N.stream_handle())
+        ctx.save_for_backward(x, h_src, indptr, local, n_dst)
+        ctx.max_dst, ctx.scratch, ctx.edge_w = max_dst, scratch, edge_w
         return out
 
     @staticmethod
     def backward(ctx, ga):
         x, h, indptr, local, n_dst = ctx.saved_tensors
         dw = block_mean_wgrad(ga.contiguous(), indptr, local, n_dst, ctx.max_dst, h, x,
-                              scratch=ctx.scratch)
-        return None, dw, None, None, None, None, None, None
+                              scratch=ctx.scratch, edge_w=ctx.edge_w)
+        return None, dw, None, None, None, None, None, None, None
 
 
 def input_block_mean(x, w, indptr, local, n_dst, max_dst: int, bias_col: bool = True,
-                     scratch=None):
-    return InputBlockMean.apply(x, w, indptr, local, n_dst, max_dst, bias_col, scratch)
+                     scratch=None, edge_w=None):
+    return InputBlockMean.apply(x, w, indptr, local, n_dst, max_dst, bias_col, scratch, edge_w)
 
 
 class SoftmaxCE(torch.autograd.Function):

@@ -42,7 +42,8 @@ template <bool RELU>
 __global__ void __launch_bounds__(256)
 k_block_mean_fwd(const uint16_t* __restrict__ h, int64_t H, const int32_t* __restrict__ indptr,
                  const int32_t* __restrict__ srcl, const int64_t* __restrict__ ndst_dev,
-                 int64_t max_dst, uint16_t* __restrict__ out, int64_t out_ld) {
+                 int64_t max_dst, uint16_t* __restrict__ out, int64_t out_ld,
+                 const float* __restrict__ ew) {
   const int64_t live = live_count(ndst_dev, max_dst);
   const int64_t chunks = H >> 3;
   const int64_t ochunks = out_ld >> 3;  // out_ld = H, or H + 8 with a ones column
@@ -66,21 +67,29 @@ k_block_mean_fwd(const uint16_t* __restrict__ h, int64_t H, const int32_t* __res
         for (int u = 0; u < 8; ++u)
           if (e + u < e1) sl[u] = srcl[e + u];
         uint4 q[8];
+        float wgt[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u)
-          if (e + u < e1)
+          if (e + u < e1) {
             q[u] = __ldg(reinterpret_cast<const uint4*>(h + (int64_t)sl[u] * H) + c);
+            wgt[u] = ew ? __ldg(ew + e + u) : 1.0f;
+          }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           if (e + u < e1) {
             float f[8];
             bf16x8_to_f32(q[u], f);
+            if (ew) {
 #pragma unroll
-            for (int j = 0; j < 8; ++j) acc[j] += RELU ? fmaxf(f[j], 0.f) : f[j];
+              for (int j = 0; j < 8; ++j) acc[j] = fmaf(wgt[u], RELU ? fmaxf(f[j], 0.f) : f[j], acc[j]);
+            } else {
+#pragma unroll
+              for (int j = 0; j < 8; ++j) acc[j] += RELU ? fmaxf(f[j], 0.f) : f[j];
+            }
           }
         }
       }
-      if (cnt) {
+      if (cnt && !ew) {
         const float inv = 1.0f / (float)cnt;
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[j] *= inv;
@@ -142,7 +151,7 @@ extern "C" {
 
 int fg_block_mean_fwd(const uint16_t* h, int64_t H, const int32_t* indptr, const int32_t* srcl,
                       const int64_t* ndst, int64_t max_dst, uint16_t* out, int64_t out_ld,
-                      int relu_in, void* s) {
+                      int relu_in, const float* edge_w, void* s) {
   FG_CHECK_ARG(H % 8 == 0, "hidden dim must be a multiple of 8");
   if (out_ld == 0) out_ld = H;
   FG_CHECK_ARG(out_ld == H || out_ld == H + 8, "out_ld must be H or H + 8 (ones column)");
@@ -151,11 +160,11 @@ int fg_block_mean_fwd(const uint16_t* h, int64_t H, const int32_t* indptr, const
   if (relu_in)
     k_block_mean_fwd<true><<<grid_for(total, 256), 256, 0, as_stream(s)>>>(h, H, indptr, srcl,
                                                                            ndst, max_dst, out,
-                                                                           out_ld);
+                                                                           out_ld, edge_w);
   else
     k_block_mean_fwd<false><<<grid_for(total, 256), 256, 0, as_stream(s)>>>(h, H, indptr, srcl,
                                                                             ndst, max_dst, out,
-                                                                            out_ld);
+                                                                            out_ld, edge_w);
   FG_LAUNCH_CHECK();
   return FG_OK;
 }
@@ -244,7 +253,7 @@ __global__ void k_t_place(const int32_t* __restrict__ local, const int64_t* __re
                           int64_t cap_e, const int32_t* __restrict__ indptr,
                           const int64_t* __restrict__ nd_dev, int64_t max_dst,
                           int32_t* __restrict__ cursor, int32_t* __restrict__ t_dst,
-                          float* __restrict__ t_w, int fmax) {
+                          float* __restrict__ t_w, int fmax, const float* __restrict__ ew) {
   const int64_t nd = min64(*nd_dev, max_dst);
   // thread per (destination, pick slot k < fmax): picks of v are contiguous
   // in [indptr[v], indptr[v+1]) and number at most fmax
@@ -258,7 +267,7 @@ __global__ void k_t_place(const int32_t* __restrict__ local, const int64_t* __re
     if (e >= e1) continue;
     const int32_t slot = atomicAdd(cursor + local[e], 1);
     t_dst[slot] = (int32_t)v;
-    t_w[slot] = 1.0f / (float)(e1 - e0);
+    t_w[slot] = ew ? ew[e] : 1.0f / (float)(e1 - e0);
   }
 }
 
@@ -411,8 +420,9 @@ extern "C" int64_t fg_block_transpose_scratch_bytes(int64_t cap_src) {
 extern "C" int fg_block_transpose(const int32_t* local, const int64_t* n_edges_dev, int64_t cap_e,
                                   const int32_t* indptr, const int64_t* n_dst_dev,
                                   int64_t max_dst, int max_per_dst, int64_t cap_src,
-                                  int32_t* t_indptr, int32_t* t_dst, float* t_w, void* scratch,
-                                  int64_t scratch_bytes, void* s) {
+                                  int32_t* t_indptr, int32_t* t_dst, float* t_w,
+                                  const float* edge_w, void* scratch, int64_t scratch_bytes,
+                                  void* s) {
   FG_CHECK_ARG(max_per_dst >= 1, "fg_block_transpose: max_per_dst must be >= 1");
   FG_CHECK_ARG(cap_src >= 1, "fg_block_transpose: empty source capacity");
   FG_CHECK_ARG(scratch_bytes >= fg_block_transpose_scratch_bytes(cap_src),
@@ -432,7 +442,8 @@ extern "C" int fg_block_transpose(const int32_t* local, const int64_t* n_edges_d
                                              (unsigned)nt);
   FG_LAUNCH_CHECK();
   fg::k_t_place<<<grid_for(max_dst * max_per_dst, 256), 256, 0, st>>>(
-      local, n_edges_dev, cap_e, indptr, n_dst_dev, max_dst, cursor, t_dst, t_w, max_per_dst);
+      local, n_edges_dev, cap_e, indptr, n_dst_dev, max_dst, cursor, t_dst, t_w, max_per_dst,
+      edge_w);
   FG_LAUNCH_CHECK();
   return FG_OK;
 }
@@ -562,6 +573,55 @@ extern "C" int fg_softmax_ce(const void* logits, int logits_bf16, int C, int64_t
     fg::k_softmax_ce<float><<<grid, threads, 0, st>>>((const float*)logits, C, ld, rows,
                                                       n_valid_dev, labels, row_node,
                                                       (float*)grad, row_loss, counter, loss_out);
+  FG_LAUNCH_CHECK();
+  return FG_OK;
+}
+
+// ------------------------------------------------- block edge weights
+// Per-edge aggregation weights of a sampled block.  FG_AGG_MEAN: 1/cnt_v
+// (the reference's row-stochastic mean, factors.py:108-114).  FG_AGG_GCN:
+// Kipf's symmetric normalisation D^-1/2 A D^-1/2 over the full graph's
+// degrees (self-loops included), estimated from the cnt_v sampled
+// neighbours: w_e = (deg_v / cnt_v) / sqrt(deg_v deg_u) = sqrt(deg_v) /
+// (cnt_v sqrt(deg_u)), so sum_e w_e x_u is unbiased for the full GCN sum.
+namespace fg {
+__global__ void k_edge_weights(int kind, const int64_t* __restrict__ off,
+                               const int32_t* __restrict__ dst_nodes,
+                               const int32_t* __restrict__ indptr,
+                               const int32_t* __restrict__ src_nodes,
+                               const int64_t* __restrict__ ndst_dev, int64_t max_dst,
+                               float* __restrict__ w) {
+  const int64_t live = min64(*ndst_dev, max_dst);
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < live;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t a = indptr[v], b = indptr[v + 1];
+    if (b == a) continue;
+    const float inv = 1.0f / (float)(b - a);
+    if (kind == FG_AGG_MEAN) {
+      for (int32_t e = a; e < b; ++e) w[e] = inv;
+    } else {
+      const int32_t dv = dst_nodes[v];
+      const float sv = sqrtf((float)(off[dv + 1] - off[dv])) * inv;
+      for (int32_t e = a; e < b; ++e) {
+        const int32_t u = src_nodes[e];
+        w[e] = sv * rsqrtf((float)(off[u + 1] - off[u]));
+      }
+    }
+  }
+}
+}  // namespace fg
+
+extern "C" int fg_block_edge_weights(int kind, const int64_t* row_offsets,
+                                     const int32_t* dst_nodes, const int32_t* indptr,
+                                     const int32_t* src_nodes, const int64_t* n_dst_dev,
+                                     int64_t max_dst, float* edge_w, void* s) {
+  FG_CHECK_ARG(kind == FG_AGG_MEAN || kind == FG_AGG_GCN, "unknown aggregator kind %d", kind);
+  FG_CHECK_ARG(indptr && n_dst_dev && edge_w, "fg_block_edge_weights: null argument");
+  FG_CHECK_ARG(kind == FG_AGG_MEAN || (row_offsets && dst_nodes && src_nodes),
+               "fg_block_edge_weights: GCN weights need the graph and node ids");
+  if (max_dst == 0) return FG_OK;
+  fg::k_edge_weights<<<grid_for(max_dst, 256), 256, 0, as_stream(s)>>>(
+      kind, row_offsets, dst_nodes, indptr, src_nodes, n_dst_dev, max_dst, edge_w);
   FG_LAUNCH_CHECK();
   return FG_OK;
 }

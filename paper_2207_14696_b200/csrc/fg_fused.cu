@@ -46,6 +46,22 @@ __device__ __forceinline__ u64 fadd2(u64 a, u64 b) {
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
   return d;
 }
+// packed fp32 pair fma (sm_100 FFMA2): a * b + c per lane of the pair
+__device__ __forceinline__ u64 ffma2(u64 a, u64 b, u64 c) {
+  u64 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+// acc += x (mean) or acc += w * x (edge-weighted sum; w2 = (w, w))
+template <bool WT>
+__device__ __forceinline__ u64 acc2(u64 acc, u64 x, u64 w2) {
+  if constexpr (WT) return ffma2(x, w2, acc);
+  else return fadd2(acc, x);
+}
+__device__ __forceinline__ u64 bcast2(float w) {
+  const u64 b = __float_as_uint(w);
+  return (b << 32) | b;
+}
 __device__ __forceinline__ u64 pack2(float x, float y) {
   return ((u64)__float_as_uint(y) << 32) | __float_as_uint(x);
 }
@@ -283,12 +299,12 @@ __device__ __forceinline__ uint32_t sq_code(uint64_t w0, uint64_t w1, int j) {
   return (((hi << 8) | lo) >> (16 - inb - BW)) & (Q - 1);
 }
 
-template <int K, typename OT>
+template <int K, typename OT, bool WT>
 __global__ void __launch_bounds__(kThreads, 2)
 k_sq_mean(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
           const float* __restrict__ lut, const int32_t* __restrict__ indptr,
           const int32_t* __restrict__ src, const int64_t* __restrict__ ndst_dev,
-          int64_t max_dst, OT* __restrict__ out, int64_t ld) {
+          int64_t max_dst, OT* __restrict__ out, int64_t ld, const float* __restrict__ ew) {
   constexpr int Q = 1 << K;
   constexpr int CB = 2 * K;
   constexpr int U = K >= 5 ? 4 : 8;  // picks whose loads are issued together
@@ -338,12 +354,14 @@ k_sq_mean(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
       const int64_t boff = (int64_t)c * CB;
       for (int base = 0; base < cnt; base += U) {
         uint64_t w[U][2];
+        u64 wt[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           if (base + u < cnt) {
             const int e = a + base + u;
             const int32_t sid = staged ? s_src[e] : __ldg(src + e0 + e);
             load_chunk<K>(rows + (int64_t)sid * stride + boff, w[u][0], w[u][1]);
+            if constexpr (WT) wt[u] = bcast2(__ldg(ew + e0 + e));
           }
         }
 #pragma unroll
@@ -353,17 +371,17 @@ k_sq_mean(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
             for (int j = 0; j < 16; j += 2) {
               if constexpr (PAIR) {
                 const u64 x = s_lut2[sq_code<K, 2 * K>(w[u][0], w[u][1], j) * 32 + lane];
-                acc[j / 2] = fadd2(acc[j / 2], x);
+                acc[j / 2] = acc2<WT>(acc[j / 2], x, wt[u]);
               } else {
                 const float x0 = s_lut[sq_code<K>(w[u][0], w[u][1], j) * 32 + lane];
                 const float x1 = s_lut[sq_code<K>(w[u][0], w[u][1], j + 1) * 32 + lane];
-                acc[j / 2] = fadd2(acc[j / 2], pack2(x0, x1));
+                acc[j / 2] = acc2<WT>(acc[j / 2], pack2(x0, x1), wt[u]);
               }
             }
           }
         }
       }
-      const float inv = cnt ? 1.0f / (float)cnt : 0.0f;
+      const float inv = WT ? 1.0f : (cnt ? 1.0f / (float)cnt : 0.0f);
       const int j0 = c * 16;
       OT* o = out + v * ld + j0;
       if (j0 + 16 <= d) {
@@ -403,13 +421,13 @@ __device__ __forceinline__ void load_codes(const uint8_t* p, uint32_t* w) {
 // lookup, the kernel's binding resource for VQ; entries are rounded to bf16
 // once (<= 2^-9 relative), accumulation stays fp32 (within the 1e-2 bf16
 // tolerance of the north star).
-template <int W, typename OT, bool SMEM, typename TT>
+template <int W, typename OT, bool SMEM, typename TT, bool WT = false>
 __global__ void __launch_bounds__(kThreads, 2)
 k_vq_mean8(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
            const TT* __restrict__ books, int length, int parts,
            const int32_t* __restrict__ indptr, const int32_t* __restrict__ src,
            const int64_t* __restrict__ ndst_dev, int64_t max_dst, OT* __restrict__ out,
-           int64_t ld) {
+           int64_t ld, const float* __restrict__ ew = nullptr) {
   constexpr int G = 32 / W;        // parts per thread
   constexpr int NW = (G + 3) / 4;  // 32-bit code words per load
   constexpr int U = 4;             // picks whose loads are issued together
@@ -461,12 +479,14 @@ k_vq_mean8(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
       const int cnt = s_ip[vl + 1] - e0 - a;
       for (int base = 0; base < cnt; base += U) {
         uint32_t cw[U][NW];
+        u64 wt[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           if (base + u < cnt) {
             const int e = a + base + u;
             const int32_t sid = staged ? s_src[e] : __ldg(src + e0 + e);
             load_codes<G>(rows + (int64_t)sid * stride + p0, cw[u]);
+            if constexpr (WT) wt[u] = bcast2(__ldg(ew + e0 + e));
           }
         }
 #pragma unroll
@@ -483,32 +503,32 @@ k_vq_mean8(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
                   for (int j = 0; j < W; j += 4) {
                     const uint2 h = SMEM ? lds64(ent + j)
                                          : __ldg(reinterpret_cast<const uint2*>(ent + j));
-                    acc[(q * W + j) / 2] = fadd2(acc[(q * W + j) / 2], bf16x2_to_f32x2(h.x));
+                    acc[(q * W + j) / 2] = acc2<WT>(acc[(q * W + j) / 2], bf16x2_to_f32x2(h.x), wt[u]);
                     acc[(q * W + j) / 2 + 1] =
-                        fadd2(acc[(q * W + j) / 2 + 1], bf16x2_to_f32x2(h.y));
+                        acc2<WT>(acc[(q * W + j) / 2 + 1], bf16x2_to_f32x2(h.y), wt[u]);
                   }
                 } else if constexpr (W >= 4) {
 #pragma unroll
                   for (int j = 0; j < W; j += 4) {
                     const float4 f = SMEM ? lds128(ent + j)
                                           : __ldg(reinterpret_cast<const float4*>(ent + j));
-                    acc[(q * W + j) / 2] = fadd2(acc[(q * W + j) / 2], pack2(f.x, f.y));
-                    acc[(q * W + j) / 2 + 1] = fadd2(acc[(q * W + j) / 2 + 1], pack2(f.z, f.w));
+                    acc[(q * W + j) / 2] = acc2<WT>(acc[(q * W + j) / 2], pack2(f.x, f.y), wt[u]);
+                    acc[(q * W + j) / 2 + 1] = acc2<WT>(acc[(q * W + j) / 2 + 1], pack2(f.z, f.w), wt[u]);
                   }
                 } else if constexpr (W == 2) {
                   const float2 f = SMEM ? *reinterpret_cast<const float2*>(ent)
                                         : __ldg(reinterpret_cast<const float2*>(ent));
-                  acc[q] = fadd2(acc[q], pack2(f.x, f.y));
+                  acc[q] = acc2<WT>(acc[q], pack2(f.x, f.y), wt[u]);
                 } else {  // W == 1: pair adjacent parts
                   const float f = SMEM ? ent[0] : __ldg(ent);
-                  acc[q / 2] = fadd2(acc[q / 2], (q & 1) ? pack2(0.f, f) : pack2(f, 0.f));
+                  acc[q / 2] = acc2<WT>(acc[q / 2], (q & 1) ? pack2(0.f, f) : pack2(f, 0.f), wt[u]);
                 }
               }
             }
           }
         }
       }
-      const float inv = cnt ? 1.0f / (float)cnt : 0.0f;
+      const float inv = WT ? 1.0f : (cnt ? 1.0f / (float)cnt : 0.0f);
       const int64_t col0 = (int64_t)p0 * W;
       OT* o = out + v * ld + col0;
       if (np == G && col0 + G * W <= d) {
@@ -531,10 +551,11 @@ k_vq_mean8(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
 // count is dispatched once per item to a fully unrolled body, per-part smem
 // base addresses are precomputed, a zero "part" absorbs the lanes of a
 // partial last group, and every lookup is BFE + LEA + LDS + widen + FADD2.
-template <int W, int G, int C>
+template <int W, int G, int C, bool WT = false>
 __device__ __forceinline__ void vq_fast_body(const uint8_t* __restrict__ rows, int64_t stride,
                                              const int32_t* sids, uint32_t base0,
-                                             uint32_t pstride, int p0, u64* acc) {
+                                             uint32_t pstride, int p0, u64* acc,
+                                             const u64* wt = nullptr) {
   constexpr int NB = G;  // code bytes per pick for this thread
   uint32_t cw[C][(NB + 3) / 4];
 #pragma unroll
@@ -548,16 +569,18 @@ __device__ __forceinline__ void vq_fast_body(const uint8_t* __restrict__ rows, i
       if constexpr (W == 4) {
         uint32_t x, y;
         asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(x), "=r"(y) : "r"(addr));
-        acc[q * 2] = fadd2(acc[q * 2], bf16x2_to_f32x2(x));
-        acc[q * 2 + 1] = fadd2(acc[q * 2 + 1], bf16x2_to_f32x2(y));
+        const u64 wu = WT ? wt[u] : 0ull;
+        acc[q * 2] = acc2<WT>(acc[q * 2], bf16x2_to_f32x2(x), wu);
+        acc[q * 2 + 1] = acc2<WT>(acc[q * 2 + 1], bf16x2_to_f32x2(y), wu);
       } else {  // W == 8
         uint32_t x, y, z, w;
         asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
                      : "=r"(x), "=r"(y), "=r"(z), "=r"(w) : "r"(addr));
-        acc[q * 4] = fadd2(acc[q * 4], bf16x2_to_f32x2(x));
-        acc[q * 4 + 1] = fadd2(acc[q * 4 + 1], bf16x2_to_f32x2(y));
-        acc[q * 4 + 2] = fadd2(acc[q * 4 + 2], bf16x2_to_f32x2(z));
-        acc[q * 4 + 3] = fadd2(acc[q * 4 + 3], bf16x2_to_f32x2(w));
+        const u64 wu = WT ? wt[u] : 0ull;
+        acc[q * 4] = acc2<WT>(acc[q * 4], bf16x2_to_f32x2(x), wu);
+        acc[q * 4 + 1] = acc2<WT>(acc[q * 4 + 1], bf16x2_to_f32x2(y), wu);
+        acc[q * 4 + 2] = acc2<WT>(acc[q * 4 + 2], bf16x2_to_f32x2(z), wu);
+        acc[q * 4 + 3] = acc2<WT>(acc[q * 4 + 3], bf16x2_to_f32x2(w), wu);
       }
     }
   }
@@ -565,13 +588,14 @@ __device__ __forceinline__ void vq_fast_body(const uint8_t* __restrict__ rows, i
 
 constexpr int kFastThreads = 256;  // 3 CTAs/SM -> 85 registers: 32 fp32 accumulators fit
 
-template <int W, int G>
+template <int W, int G, bool WT = false>
 __global__ void __launch_bounds__(kFastThreads, 3)
 k_vq_mean8_fast(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
                 const __nv_bfloat16* __restrict__ books, int length, int parts,
                 const int32_t* __restrict__ indptr, const int32_t* __restrict__ src,
                 const int64_t* __restrict__ ndst_dev, int64_t max_dst,
-                __nv_bfloat16* __restrict__ out, int64_t ld, int slice_parts, int nslices) {
+                __nv_bfloat16* __restrict__ out, int64_t ld, int slice_parts, int nslices,
+                const float* __restrict__ ew = nullptr) {
   // G parts per thread: G * W = 32 fp32 accumulators.  Part slicing: when
   // the whole bf16 codebook does not fit the smem budget (MAG240M-shape:
   // 96 parts x 256 x 8 = 393 KB), CTA b serves parts [s*SP, s*SP+SP) of
@@ -635,19 +659,23 @@ k_vq_mean8_fast(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
       for (int base = 0; base < cnt; base += 5) {  // batches of <= 5 picks
         const int cb = min(cnt - base, 5);
         int32_t sids[5];
+        u64 wt[5];
         const int32_t* sp = staged ? s_src + a + base : src + e0 + a + base;  // tile-uniform
 #pragma unroll
         for (int u = 0; u < 5; ++u)
-          if (u < cb) sids[u] = sp[u];
+          if (u < cb) {
+            sids[u] = sp[u];
+            if constexpr (WT) wt[u] = bcast2(__ldg(ew + e0 + a + base + u));
+          }
         switch (cb) {
-          case 1: vq_fast_body<W, G, 1>(rows, stride, sids, base0, pstride, pg, acc); break;
-          case 2: vq_fast_body<W, G, 2>(rows, stride, sids, base0, pstride, pg, acc); break;
-          case 3: vq_fast_body<W, G, 3>(rows, stride, sids, base0, pstride, pg, acc); break;
-          case 4: vq_fast_body<W, G, 4>(rows, stride, sids, base0, pstride, pg, acc); break;
-          default: vq_fast_body<W, G, 5>(rows, stride, sids, base0, pstride, pg, acc); break;
+          case 1: vq_fast_body<W, G, 1, WT>(rows, stride, sids, base0, pstride, pg, acc, wt); break;
+          case 2: vq_fast_body<W, G, 2, WT>(rows, stride, sids, base0, pstride, pg, acc, wt); break;
+          case 3: vq_fast_body<W, G, 3, WT>(rows, stride, sids, base0, pstride, pg, acc, wt); break;
+          case 4: vq_fast_body<W, G, 4, WT>(rows, stride, sids, base0, pstride, pg, acc, wt); break;
+          default: vq_fast_body<W, G, 5, WT>(rows, stride, sids, base0, pstride, pg, acc, wt); break;
         }
       }
-      const float inv = cnt ? 1.0f / (float)cnt : 0.0f;
+      const float inv = WT ? 1.0f : (cnt ? 1.0f / (float)cnt : 0.0f);
       const int64_t col0 = (int64_t)pg * W;
       __nv_bfloat16* o = out + v * ld + col0;
       if (np == G && col0 + G * W <= d) {
@@ -669,7 +697,7 @@ k_vq_mean_bits(const uint8_t* __restrict__ rows, int64_t d, int64_t stride, int 
                const float* __restrict__ books, int length, int parts,
                const int32_t* __restrict__ indptr, const int32_t* __restrict__ src,
                const int64_t* __restrict__ ndst_dev, int64_t max_dst, OT* __restrict__ out,
-               int64_t ld) {
+               int64_t ld, const float* __restrict__ ew) {
   extern __shared__ int32_t s_stage[];
   int32_t* s_ip0 = s_stage;
   int32_t* s_ip1 = s_ip0 + kTD + 1;
@@ -705,10 +733,16 @@ k_vq_mean_bits(const uint8_t* __restrict__ rows, int64_t d, int64_t stride, int 
         if (sh + bits > 16) wv |= __ldg(rb + 2);
         const uint32_t code = (wv >> (24 - sh - bits)) & cmask;
         const float* ent = books + ((int64_t)p * length + code) * W;
+        if (ew) {
+          const float we = __ldg(ew + e0 + a + k);
 #pragma unroll
-        for (int j = 0; j < W; ++j) acc[j] += __ldg(ent + j);
+          for (int j = 0; j < W; ++j) acc[j] = fmaf(we, __ldg(ent + j), acc[j]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < W; ++j) acc[j] += __ldg(ent + j);
+        }
       }
-      const float inv = cnt ? 1.0f / (float)cnt : 0.0f;
+      const float inv = ew ? 1.0f : (cnt ? 1.0f / (float)cnt : 0.0f);
       OT* o = out + v * ld + (int64_t)p * W;
 #pragma unroll
       for (int j = 0; j < W; ++j)
@@ -777,17 +811,18 @@ __device__ __forceinline__ void lds_chunk(const uint8_t* p, uint64_t& w0, uint64
   }
 }
 
-template <int K, bool PAIR>
+template <int K, bool PAIR, bool WT = false>
 __device__ __forceinline__ void sq_accumulate(u64 (&acc)[8], uint64_t w0, uint64_t w1,
-                                              const float* s_lut, const u64* s_lut2, int lane) {
+                                              const float* s_lut, const u64* s_lut2, int lane,
+                                              u64 wt = 0) {
 #pragma unroll
   for (int j = 0; j < 16; j += 2) {
     if constexpr (PAIR) {
-      acc[j / 2] = fadd2(acc[j / 2], s_lut2[sq_code<K, 2 * K>(w0, w1, j) * 32 + lane]);
+      acc[j / 2] = acc2<WT>(acc[j / 2], s_lut2[sq_code<K, 2 * K>(w0, w1, j) * 32 + lane], wt);
     } else {
       const float x0 = s_lut[sq_code<K>(w0, w1, j) * 32 + lane];
       const float x1 = s_lut[sq_code<K>(w0, w1, j + 1) * 32 + lane];
-      acc[j / 2] = fadd2(acc[j / 2], pack2(x0, x1));
+      acc[j / 2] = acc2<WT>(acc[j / 2], pack2(x0, x1), wt);
     }
   }
 }
@@ -804,12 +839,13 @@ __device__ __forceinline__ void sq_store(OT* o, const u64 (&acc)[8], float inv, 
   }
 }
 
-template <int K, typename OT>
+template <int K, typename OT, bool WT>
 __global__ void __launch_bounds__(kBulkThreads, 1)
 k_sq_mean_bulk(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
                const float* __restrict__ lut, const int32_t* __restrict__ indptr,
                const int32_t* __restrict__ src, const int64_t* __restrict__ ndst_dev,
-               int64_t max_dst, OT* __restrict__ out, int64_t ld, int td, int row_cap, int rb) {
+               int64_t max_dst, OT* __restrict__ out, int64_t ld, int td, int row_cap, int rb,
+               const float* __restrict__ ew) {
   constexpr int NT = kBulkThreads;
   constexpr int Q = 1 << K;
   constexpr bool PAIR = 2 * K <= 8;
@@ -918,34 +954,46 @@ k_sq_mean_bulk(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
       const int cnt = ip[vl + 1] - e0 - a;
       if (staged) {
         const uint8_t* rp = rbuf + (int64_t)a * rb + c * (2 * K);
+        const float* ewp = WT ? ew + e0 + a : nullptr;
         int p = 0;
         for (; p + 4 <= cnt; p += 4) {
           uint64_t w[4][2];
+          u64 wt[4];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) lds_chunk<K>(rp + (p + u) * rb, w[u][0], w[u][1]);
+          for (int u = 0; u < 4; ++u) {
+            lds_chunk<K>(rp + (p + u) * rb, w[u][0], w[u][1]);
+            if constexpr (WT) wt[u] = bcast2(__ldg(ewp + p + u));
+          }
 #pragma unroll
-          for (int u = 0; u < 4; ++u) sq_accumulate<K, PAIR>(acc, w[u][0], w[u][1], s_lut, s_lut2, lane);
+          for (int u = 0; u < 4; ++u)
+            sq_accumulate<K, PAIR, WT>(acc, w[u][0], w[u][1], s_lut, s_lut2, lane, WT ? wt[u] : 0);
         }
         for (; p < cnt; ++p) {
           uint64_t w0, w1;
           lds_chunk<K>(rp + p * rb, w0, w1);
-          sq_accumulate<K, PAIR>(acc, w0, w1, s_lut, s_lut2, lane);
+          sq_accumulate<K, PAIR, WT>(acc, w0, w1, s_lut, s_lut2, lane,
+                                     WT ? bcast2(__ldg(ewp + p)) : 0);
         }
       } else {
         const int64_t boff = (int64_t)c * (2 * K);
         for (int base = 0; base < cnt; base += 8) {
           uint64_t w[8][2];
+          u64 wt[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (base + u < cnt) {
+              load_chunk<K>(rows + (int64_t)__ldg(src + e0 + a + base + u) * stride + boff,
+                            w[u][0], w[u][1]);
+              if constexpr (WT) wt[u] = bcast2(__ldg(ew + e0 + a + base + u));
+            }
 #pragma unroll
           for (int u = 0; u < 8; ++u)
             if (base + u < cnt)
-              load_chunk<K>(rows + (int64_t)__ldg(src + e0 + a + base + u) * stride + boff,
-                            w[u][0], w[u][1]);
-#pragma unroll
-          for (int u = 0; u < 8; ++u)
-            if (base + u < cnt) sq_accumulate<K, PAIR>(acc, w[u][0], w[u][1], s_lut, s_lut2, lane);
+              sq_accumulate<K, PAIR, WT>(acc, w[u][0], w[u][1], s_lut, s_lut2, lane,
+                                         WT ? wt[u] : 0);
         }
       }
-      const float inv = cnt ? 1.0f / (float)cnt : 0.0f;
+      const float inv = WT ? 1.0f : (cnt ? 1.0f / (float)cnt : 0.0f);
       sq_store(out + v * ld + c * 16, acc, inv, c * 16, d, vec_ok);
     }
     // slot k+3 (= k-1 mod 4) was last read before the previous barrier; the
@@ -956,9 +1004,10 @@ k_sq_mean_bulk(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
 }
 
 // ------------------------------------------------------------ launchers
-template <int K, typename OT>
-int launch_sq(const fg_codec_desc* c, const int32_t* indptr, const int32_t* src,
-              const int64_t* ndst, int64_t max_dst, void* out, int64_t ld, cudaStream_t st) {
+template <int K, typename OT, bool WT>
+int launch_sq_w(const fg_codec_desc* c, const int32_t* indptr, const int32_t* src,
+                const int64_t* ndst, int64_t max_dst, void* out, int64_t ld, cudaStream_t st,
+                const float* ew) {
   // TMA-staged variant: needs a row buffer holding a tile of >= 32
   // destinations at fanout 8 next to the decode table
   {
@@ -973,47 +1022,57 @@ int launch_sq(const fg_codec_desc* c, const int32_t* indptr, const int32_t* src,
     while (td > 32 && td * 8 > row_cap) td /= 2;
     if (td * 8 <= row_cap && rb <= c->row_stride) {
       const int smem = fixed + 2 * row_cap * rb;
-      auto kern = k_sq_mean_bulk<K, OT>;
+      auto kern = k_sq_mean_bulk<K, OT, WT>;
       FG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       const int grid = (int)min64(ceil_div(max_dst, td), (int64_t)sm_count());
       kern<<<grid, kBulkThreads, smem, st>>>(c->rows, c->d, c->row_stride,
                                              (const float*)c->table, indptr, src, ndst, max_dst,
-                                             (OT*)out, ld, td, row_cap, rb);
+                                             (OT*)out, ld, td, row_cap, rb, ew);
       FG_LAUNCH_CHECK();
       return FG_OK;
     }
   }
   const int lut_bytes = 2 * K <= 8 ? (1 << (2 * K)) * 32 * 8 : (1 << K) * 32 * 4;
   const int smem = lut_bytes + 2 * (kTD + 1 + kSrcCap) * 4;
-  auto kern = k_sq_mean<K, OT>;
+  auto kern = k_sq_mean<K, OT, WT>;
   FG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const int grid = (int)min64(ceil_div(max_dst, kTD), (int64_t)sm_count() * 2);
   kern<<<grid, kThreads, smem, st>>>(c->rows, c->d, c->row_stride, (const float*)c->table,
-                                     indptr, src, ndst, max_dst, (OT*)out, ld);
+                                     indptr, src, ndst, max_dst, (OT*)out, ld, ew);
   FG_LAUNCH_CHECK();
   return FG_OK;
 }
 
+template <int K, typename OT>
+int launch_sq(const fg_codec_desc* c, const int32_t* indptr, const int32_t* src,
+              const int64_t* ndst, int64_t max_dst, void* out, int64_t ld, cudaStream_t st,
+              const float* ew) {
+  return ew ? launch_sq_w<K, OT, true>(c, indptr, src, ndst, max_dst, out, ld, st, ew)
+            : launch_sq_w<K, OT, false>(c, indptr, src, ndst, max_dst, out, ld, st, nullptr);
+}
+
 template <typename OT>
 int dispatch_sq(const fg_codec_desc* c, const int32_t* indptr, const int32_t* src,
-                const int64_t* ndst, int64_t max_dst, void* out, int64_t ld, cudaStream_t st) {
+                const int64_t* ndst, int64_t max_dst, void* out, int64_t ld, cudaStream_t st,
+                const float* ew) {
   switch (c->bits) {
-    case 1: return launch_sq<1, OT>(c, indptr, src, ndst, max_dst, out, ld, st);
-    case 2: return launch_sq<2, OT>(c, indptr, src, ndst, max_dst, out, ld, st);
-    case 3: return launch_sq<3, OT>(c, indptr, src, ndst, max_dst, out, ld, st);
-    case 4: return launch_sq<4, OT>(c, indptr, src, ndst, max_dst, out, ld, st);
-    case 5: return launch_sq<5, OT>(c, indptr, src, ndst, max_dst, out, ld, st);
-    case 6: return launch_sq<6, OT>(c, indptr, src, ndst, max_dst, out, ld, st);
-    case 7: return launch_sq<7, OT>(c, indptr, src, ndst, max_dst, out, ld, st);
-    case 8: return launch_sq<8, OT>(c, indptr, src, ndst, max_dst, out, ld, st);
+    case 1: return launch_sq<1, OT>(c, indptr, src, ndst, max_dst, out, ld, st, ew);
+    case 2: return launch_sq<2, OT>(c, indptr, src, ndst, max_dst, out, ld, st, ew);
+    case 3: return launch_sq<3, OT>(c, indptr, src, ndst, max_dst, out, ld, st, ew);
+    case 4: return launch_sq<4, OT>(c, indptr, src, ndst, max_dst, out, ld, st, ew);
+    case 5: return launch_sq<5, OT>(c, indptr, src, ndst, max_dst, out, ld, st, ew);
+    case 6: return launch_sq<6, OT>(c, indptr, src, ndst, max_dst, out, ld, st, ew);
+    case 7: return launch_sq<7, OT>(c, indptr, src, ndst, max_dst, out, ld, st, ew);
+    case 8: return launch_sq<8, OT>(c, indptr, src, ndst, max_dst, out, ld, st, ew);
   }
   set_error("bad SQ k %d", c->bits);
   return FG_EUSAGE;
 }
 
-template <int W, typename OT>
-int launch_vq(const fg_codec_desc* c, const int32_t* indptr, const int32_t* src,
-              const int64_t* ndst, int64_t max_dst, void* out, int64_t ld, cudaStream_t st) {
+template <int W, typename OT, bool WT>
+int launch_vq_w(const fg_codec_desc* c, const int32_t* indptr, const int32_t* src,
+                const int64_t* ndst, int64_t max_dst, void* out, int64_t ld, cudaStream_t st,
+                const float* ew) {
   const int64_t book_bytes = (int64_t)c->num_parts * c->length * W * 4;
   const int64_t stage_bytes = 2 * (kTD + 1 + kSrcCap) * 4;
   const int64_t ntiles = ceil_div(max_dst, kTD);
@@ -1022,7 +1081,7 @@ int launch_vq(const fg_codec_desc* c, const int32_t* indptr, const int32_t* src,
     const int grid = (int)min64(ntiles, (int64_t)sm_count() * 2);
     kern<<<grid, kThreads, stage_bytes, st>>>(c->rows, c->d, c->row_stride, c->bits,
                                          (const float*)c->table, c->length, c->num_parts, indptr,
-                                         src, ndst, max_dst, (OT*)out, ld);
+                                         src, ndst, max_dst, (OT*)out, ld, ew);
     FG_LAUNCH_CHECK();
     return FG_OK;
   }
@@ -1046,7 +1105,7 @@ int launch_vq(const fg_codec_desc* c, const int32_t* indptr, const int32_t* src,
     if (lp && sp >= GF) {
       const int ns = (int)ceil_div(c->num_parts, sp);
       const int64_t fast_smem = smem_for(sp);
-      auto kern = k_vq_mean8_fast<W, GF>;
+      auto kern = k_vq_mean8_fast<W, GF, WT>;
       FG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)fast_smem));
       // grid: a multiple of the slice count, ~3 CTAs per SM in total
@@ -1055,7 +1114,7 @@ int launch_vq(const fg_codec_desc* c, const int32_t* indptr, const int32_t* src,
       kern<<<grid, kFastThreads, fast_smem, st>>>(c->rows, c->d, c->row_stride,
                                               (const __nv_bfloat16*)c->table_lp, c->length,
                                               c->num_parts, indptr, src, ndst, max_dst,
-                                              (__nv_bfloat16*)out, ld, sp, ns);
+                                              (__nv_bfloat16*)out, ld, sp, ns, ew);
       FG_LAUNCH_CHECK();
       return FG_OK;
     }
@@ -1066,40 +1125,49 @@ int launch_vq(const fg_codec_desc* c, const int32_t* indptr, const int32_t* src,
     const int per_sm = smem2 <= 110 * 1024 ? 2 : 1;
     const int grid = (int)min64(ntiles, (int64_t)sm_count() * per_sm);
     if (lp) {
-      auto kern = k_vq_mean8<W, OT, true, __nv_bfloat16>;
+      auto kern = k_vq_mean8<W, OT, true, __nv_bfloat16, WT>;
       FG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem2));
       kern<<<grid, kThreads, smem2, st>>>(c->rows, c->d, c->row_stride,
                                           (const __nv_bfloat16*)c->table_lp, c->length,
-                                          c->num_parts, indptr, src, ndst, max_dst, (OT*)out, ld);
+                                          c->num_parts, indptr, src, ndst, max_dst, (OT*)out, ld, ew);
     } else {
-      auto kern = k_vq_mean8<W, OT, true, float>;
+      auto kern = k_vq_mean8<W, OT, true, float, WT>;
       FG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem2));
       kern<<<grid, kThreads, smem2, st>>>(c->rows, c->d, c->row_stride, (const float*)c->table,
                                           c->length, c->num_parts, indptr, src, ndst, max_dst,
-                                          (OT*)out, ld);
+                                          (OT*)out, ld, ew);
     }
   } else {
-    auto kern = k_vq_mean8<W, OT, false, float>;
+    auto kern = k_vq_mean8<W, OT, false, float, WT>;
     const int grid = (int)min64(ntiles, (int64_t)sm_count() * 2);
     kern<<<grid, kThreads, stage_bytes, st>>>(c->rows, c->d, c->row_stride, (const float*)c->table,
                                          c->length, c->num_parts, indptr, src, ndst, max_dst,
-                                         (OT*)out, ld);
+                                         (OT*)out, ld, ew);
   }
   FG_LAUNCH_CHECK();
   return FG_OK;
 }
 
+template <int W, typename OT>
+int launch_vq(const fg_codec_desc* c, const int32_t* indptr, const int32_t* src,
+              const int64_t* ndst, int64_t max_dst, void* out, int64_t ld, cudaStream_t st,
+              const float* ew) {
+  return ew ? launch_vq_w<W, OT, true>(c, indptr, src, ndst, max_dst, out, ld, st, ew)
+            : launch_vq_w<W, OT, false>(c, indptr, src, ndst, max_dst, out, ld, st, nullptr);
+}
+
 template <typename OT>
 int dispatch_vq(const fg_codec_desc* c, const int32_t* indptr, const int32_t* src,
-                const int64_t* ndst, int64_t max_dst, void* out, int64_t ld, cudaStream_t st) {
+                const int64_t* ndst, int64_t max_dst, void* out, int64_t ld, cudaStream_t st,
+                const float* ew) {
   switch (c->width) {
-    case 1: return launch_vq<1, OT>(c, indptr, src, ndst, max_dst, out, ld, st);
-    case 2: return launch_vq<2, OT>(c, indptr, src, ndst, max_dst, out, ld, st);
-    case 4: return launch_vq<4, OT>(c, indptr, src, ndst, max_dst, out, ld, st);
-    case 8: return launch_vq<8, OT>(c, indptr, src, ndst, max_dst, out, ld, st);
-    case 16: return launch_vq<16, OT>(c, indptr, src, ndst, max_dst, out, ld, st);
+    case 1: return launch_vq<1, OT>(c, indptr, src, ndst, max_dst, out, ld, st, ew);
+    case 2: return launch_vq<2, OT>(c, indptr, src, ndst, max_dst, out, ld, st, ew);
+    case 4: return launch_vq<4, OT>(c, indptr, src, ndst, max_dst, out, ld, st, ew);
+    case 8: return launch_vq<8, OT>(c, indptr, src, ndst, max_dst, out, ld, st, ew);
+    case 16: return launch_vq<16, OT>(c, indptr, src, ndst, max_dst, out, ld, st, ew);
   }
   set_error("fused VQ mean supports width in {1,2,4,8,16}, got %d", c->width);
   return FG_EUSAGE;
@@ -1109,9 +1177,9 @@ int dispatch_vq(const fg_codec_desc* c, const int32_t* indptr, const int32_t* sr
 
 using namespace fg;
 
-extern "C" int fg_gather_dequant_mean(const fg_codec_desc* c, const int32_t* indptr,
-                                      const int32_t* src, const int64_t* ndst, int64_t max_dst,
-                                      void* out, int64_t out_ld, int out_dtype, void* s) {
+static int gather_aggregate(const fg_codec_desc* c, const int32_t* indptr, const int32_t* src,
+                            const float* edge_w, const int64_t* ndst, int64_t max_dst, void* out,
+                            int64_t out_ld, int out_dtype, void* s) {
   FG_CHECK_ARG(c != nullptr && indptr != nullptr && ndst != nullptr, "null argument");
   FG_CHECK_ARG(c->elem_bits == 32, "fused aggregate needs a float32 decode table");
   FG_CHECK_ARG(out_dtype == FG_OUT_F32 || out_dtype == FG_OUT_BF16,
@@ -1125,17 +1193,31 @@ extern "C" int fg_gather_dequant_mean(const fg_codec_desc* c, const int32_t* ind
     FG_CHECK_ARG(c->row_stride >= ((c->d + 15) / 16) * 2 * c->bits,
                  "SQ row stride must cover ceil(d/16)*2k bytes (whole 16-code chunks)");
     return out_dtype == FG_OUT_F32
-               ? dispatch_sq<float>(c, indptr, src, ndst, max_dst, out, ld, st)
-               : dispatch_sq<__nv_bfloat16>(c, indptr, src, ndst, max_dst, out, ld, st);
+               ? dispatch_sq<float>(c, indptr, src, ndst, max_dst, out, ld, st, edge_w)
+               : dispatch_sq<__nv_bfloat16>(c, indptr, src, ndst, max_dst, out, ld, st, edge_w);
   }
   if (c->kind == FG_CODEC_VQ) {
     FG_CHECK_ARG(c->bits >= 1 && c->bits <= 16, "bad VQ code bits");
     FG_CHECK_ARG(c->bits != 8 || c->row_stride >= ((c->num_parts + 31) / 32) * 32,
                  "8-bit VQ rows must be padded to 32 bytes");
     return out_dtype == FG_OUT_F32
-               ? dispatch_vq<float>(c, indptr, src, ndst, max_dst, out, ld, st)
-               : dispatch_vq<__nv_bfloat16>(c, indptr, src, ndst, max_dst, out, ld, st);
+               ? dispatch_vq<float>(c, indptr, src, ndst, max_dst, out, ld, st, edge_w)
+               : dispatch_vq<__nv_bfloat16>(c, indptr, src, ndst, max_dst, out, ld, st, edge_w);
   }
   set_error("unknown codec kind %d", c->kind);
   return FG_EUSAGE;
+}
+
+extern "C" int fg_gather_dequant_mean(const fg_codec_desc* c, const int32_t* indptr,
+                                      const int32_t* src, const int64_t* ndst, int64_t max_dst,
+                                      void* out, int64_t out_ld, int out_dtype, void* s) {
+  return gather_aggregate(c, indptr, src, nullptr, ndst, max_dst, out, out_ld, out_dtype, s);
+}
+
+extern "C" int fg_gather_dequant_wsum(const fg_codec_desc* c, const int32_t* indptr,
+                                      const int32_t* src, const float* edge_w,
+                                      const int64_t* ndst, int64_t max_dst, void* out,
+                                      int64_t out_ld, int out_dtype, void* s) {
+  FG_CHECK_ARG(edge_w != nullptr, "fg_gather_dequant_wsum: null edge weights");
+  return gather_aggregate(c, indptr, src, edge_w, ndst, max_dst, out, out_ld, out_dtype, s);
 }

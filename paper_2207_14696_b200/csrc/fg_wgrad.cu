@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
 k_block_mean_wgrad(const uint16_t* __restrict__ g, int64_t g_ld,
                    const int32_t* __restrict__ indptr, const int64_t* __restrict__ ndst_dev,
                    int64_t max_dst, const int32_t* __restrict__ local,
-                   const uint16_t* __restrict__ hmask, int H,
+                   const float* __restrict__ ew, const uint16_t* __restrict__ hmask, int H,
                    const uint16_t* __restrict__ x, int P, float* __restrict__ partial,
                    uint32_t tmem_cols) {
   extern __shared__ __align__(1024) uint8_t wg_mem[];
@@ -272,7 +272,7 @@ k_block_mean_wgrad(const uint16_t* __restrict__ g, int64_t g_ld,
                 if ((int64_t)s_win[mid] <= e) lo = mid; else hi = mid;
               }
               vv = vw + lo;
-              wt = 1.0f / (float)(s_win[lo + 1] - s_win[lo]);
+              wt = ew ? __ldg(ew + e) : 1.0f / (float)(s_win[lo + 1] - s_win[lo]);
             } else {  // past the window (dsts without edges): serial search
               int64_t lo = vw, hi = live_dst;
               while (hi - lo > 1) {
@@ -280,7 +280,7 @@ k_block_mean_wgrad(const uint16_t* __restrict__ g, int64_t g_ld,
                 if ((int64_t)__ldg(indptr + mid) <= e) lo = mid; else hi = mid;
               }
               vv = lo;
-              wt = 1.0f / (float)(__ldg(indptr + lo + 1) - __ldg(indptr + lo));
+              wt = ew ? __ldg(ew + e) : 1.0f / (float)(__ldg(indptr + lo + 1) - __ldg(indptr + lo));
             }
             v = (int32_t)vv;
           }
@@ -450,7 +450,8 @@ extern "C" int fg_block_mean_wgrad_supported(int64_t H, int64_t P) {
 
 extern "C" int fg_block_mean_wgrad(const uint16_t* g, int64_t g_ld, const int32_t* indptr,
                                    const int32_t* local, const int64_t* n_dst_dev,
-                                   int64_t max_dst, const uint16_t* h_mask, int64_t H,
+                                   int64_t max_dst, const float* edge_w,
+                                   const uint16_t* h_mask, int64_t H,
                                    const uint16_t* x, int64_t P, float* dw, float* scratch,
                                    int64_t scratch_bytes, void* s) {
   FG_CHECK_ARG(g != nullptr && indptr != nullptr && local != nullptr && n_dst_dev != nullptr &&
@@ -469,7 +470,8 @@ extern "C" int fg_block_mean_wgrad(const uint16_t* g, int64_t g_ld, const int32_
   uint32_t cols = 32;
   while (cols < (uint32_t)((H / 128) * P)) cols <<= 1;
   k_block_mean_wgrad<<<nb, kWgThreads, smem, st>>>(g, g_ld, indptr, n_dst_dev, max_dst, local,
-                                                   h_mask, (int)H, x, (int)P, scratch, cols);
+                                                   edge_w, h_mask, (int)H, x, (int)P, scratch,
+                                                   cols);
   FG_LAUNCH_CHECK();
   const int64_t n4 = H * P / 4;  // P % 16 == 0
   float4* seg = reinterpret_cast<float4*>(seg_f);

@@ -83,7 +83,8 @@ class SageModel(nn.Module):
         if self.training and self.fused_input_ok():
             l = L - 2
             h = input_block_mean(agg_in, self.lins[0].weight, sb.indptr[l], sb.local[l],
-                                 sb.n_nodes[l], caps[l], True, wgrad_scratch)
+                                 sb.n_nodes[l], caps[l], True, wgrad_scratch,
+                                 sb.ew[l] if sb.ew else None)
             h = self.lins[1](h)
             first = 2
         else:
@@ -91,13 +92,14 @@ class SageModel(nn.Module):
         for i in range(first, L):
             l = L - 1 - i  # block index feeding this layer
             trans = sb.trans[l] if sb.trans else None
+            ew = sb.ew[l] if sb.ew else None
             if self.dropout and self.training:
                 h = F.dropout(F.relu(h), self.dropout)
                 a = block_mean(h.to(torch.bfloat16), sb.indptr[l], sb.local[l], sb.n_nodes[l],
-                               caps[l], trans=trans, bias_col=True)
+                               caps[l], trans=trans, bias_col=True, edge_w=ew)
             else:  # ReLU fused into the block-mean gather
                 a = block_mean(h.to(torch.bfloat16), sb.indptr[l], sb.local[l], sb.n_nodes[l],
-                               caps[l], relu=True, trans=trans, bias_col=True)
+                               caps[l], relu=True, trans=trans, bias_col=True, edge_w=ew)
             h = self.lins[i](a)
         return h
 
@@ -150,6 +152,9 @@ class TrainConfig:
     # sample batch b+1 on a side stream while batch b trains (two sampler
     # slots sharing one PCG64 stream: the batches are the same as serial)
     pipeline: bool = True
+    # "mean" (SAGE-mean, the reference's row-stochastic D^-1 A) or "gcn"
+    # (Kipf's D^-1/2 A D^-1/2, sampled estimator; BASELINE config E)
+    aggregator: str = "mean"
 
 
 class SageTrainer:
@@ -172,13 +177,15 @@ class SageTrainer:
         fused = self.model.fused_input_ok()
         tl = range(L - 2) if fused else None
         self.sampler = DeviceSampler(graph, cfg.fanouts, cfg.batch_size, need_local=True,
-                                     need_transpose=True, transpose_layers=tl)
+                                     need_transpose=True, transpose_layers=tl,
+                                     aggregator=cfg.aggregator)
         self.samplers = [self.sampler]
         self.pipeline = cfg.pipeline
         if self.pipeline:
             self.samplers.append(DeviceSampler(graph, cfg.fanouts, cfg.batch_size,
                                                need_local=True, need_transpose=True,
-                                               transpose_layers=tl, share=self.sampler))
+                                               transpose_layers=tl, share=self.sampler,
+                                               aggregator=cfg.aggregator))
             self.side = torch.cuda.Stream(self.device)
         self.caps = self.sampler.caps
         # flat gradient buffer: one all-reduce per step
@@ -258,8 +265,9 @@ class SageTrainer:
         L = len(self.cfg.fanouts)
         caps = self.caps
         s = N.stream_handle()
+        ew = sb.ew or [None] * L
         gather_dequant_mean(self.codec, sb.indptr[L - 1], sb.picks[L - 1], sb.n_nodes[L - 1],
-                            caps[L - 1], out=self.agg)
+                            caps[L - 1], out=self.agg, edge_w=ew[L - 1])
         W, dW = self.w_bf16, self.w_grad
         ins, hs = [self.agg], []
         for i in range(L):
@@ -270,7 +278,7 @@ class SageTrainer:
                 H = h.shape[1]
                 a = torch.empty((caps[l], H + 8), dtype=torch.bfloat16, device=self.device)
                 N.call("fg_block_mean_fwd", N.ptr(h), H, N.ptr(sb.indptr[l]), N.ptr(sb.local[l]),
-                       N.ptr(sb.n_nodes[l]), caps[l], N.ptr(a), H + 8, 1, s)
+                       N.ptr(sb.n_nodes[l]), caps[l], N.ptr(a), H + 8, 1, N.ptr(ew[l]), s)
                 ins.append(a)
         logits = hs[-1]
         ld = logits.shape[1]
@@ -289,7 +297,8 @@ class SageTrainer:
             l = L - 1 - i  # block feeding layer i
             if fused and i == 1:
                 N.call("fg_block_mean_wgrad", N.ptr(din), H, N.ptr(sb.indptr[l]),
-                       N.ptr(sb.local[l]), N.ptr(sb.n_nodes[l]), caps[l], N.ptr(hs[0]), H,
+                       N.ptr(sb.local[l]), N.ptr(sb.n_nodes[l]), caps[l], N.ptr(ew[l]),
+                       N.ptr(hs[0]), H,
                        N.ptr(self.agg), self.agg.shape[1], N.ptr(dW[0]),
                        N.ptr(self.wgrad_scratch), self.wgrad_scratch.numel() * 4, s)
                 break
@@ -303,7 +312,8 @@ class SageTrainer:
     def _train_autograd(self, sb):
         L = len(self.cfg.fanouts)
         gather_dequant_mean(self.codec, sb.indptr[L - 1], sb.picks[L - 1], sb.n_nodes[L - 1],
-                            self.caps[L - 1], out=self.agg)
+                            self.caps[L - 1], out=self.agg,
+                            edge_w=sb.ew[L - 1] if sb.ew else None)
         with torch.autocast("cuda", dtype=torch.bfloat16):
             logits = self.model(self.agg, sb, self.caps, self.wgrad_scratch)
         loss = softmax_ce(logits, self.labels, sb.nodes[0], sb.n_nodes[0],
@@ -394,7 +404,8 @@ class SageTrainer:
     def evaluate(self, ids, seed: int = 12345, max_batches: int | None = None) -> float:
         """Accuracy over ``ids`` with the same sampled-block model."""
         smp = DeviceSampler(self.sampler.g, self.cfg.fanouts, self.cfg.batch_size,
-                            need_local=True)
+                            need_local=True, aggregator=self.cfg.aggregator,
+                            need_transpose=self.cfg.aggregator != "mean")
         nb = smp.begin_epoch(ids, seed)
         if max_batches:
             nb = min(nb, max_batches)
@@ -406,7 +417,8 @@ class SageTrainer:
         for b in range(nb):
             sb = smp.sample(b)
             gather_dequant_mean(self.codec, sb.indptr[L - 1], sb.picks[L - 1],
-                                sb.n_nodes[L - 1], smp.caps[L - 1], out=agg)
+                                sb.n_nodes[L - 1], smp.caps[L - 1], out=agg,
+                                edge_w=sb.ew[L - 1] if sb.ew else None)
             with torch.autocast("cuda", dtype=torch.bfloat16):
                 logits = self.model(agg, sb, smp.caps)
             valid = torch.arange(smp.caps[0], device=self.device) < sb.n_nodes[0]

@@ -25,6 +25,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _native as N
+from .aggregate import AGGREGATORS
 from .errors import DataError
 from .graph import CsrGraph, DeviceGraph
 
@@ -103,6 +104,7 @@ class SampledBatch:
     frontier: object = None
     n_frontier: object = None
     trans: list = None   # per block (t_indptr, t_dst) or None
+    ew: list = None      # per block edge weights (aggregator variants) or None
 
 
 class DeviceSampler:
@@ -111,11 +113,14 @@ class DeviceSampler:
     def __init__(self, graph: DeviceGraph, fanouts, batch_size: int, *,
                  need_local: bool = True, want_frontier: bool = False,
                  unique_last: bool = False, need_transpose: bool = False,
-                 transpose_layers=None, share: "DeviceSampler | None" = None):
+                 transpose_layers=None, share: "DeviceSampler | None" = None,
+                 aggregator: str = "mean"):
         """``share``: a second buffer set (slot) for pipelined training that
         continues ``share``'s PCG64 stream, permutation and scratch (only the
         per-batch outputs are its own), so batch b+1 can be sampled into one
-        slot while batch b trains from the other."""
+        slot while batch b trains from the other.  ``aggregator`` 'gcn' also
+        emits per-edge weights for every block (fg_block_edge_weights); the
+        transposes then carry them for the backward."""
         import torch
         N.require_cuda()
         self.g = graph
@@ -144,6 +149,9 @@ class DeviceSampler:
         self.picks = [z(pcaps[l]) for l in range(L)]
         self.n_picks = [z(1, dt=i64) for _ in range(L)]
         self.local = [z(pcaps[l]) if (need_local and l < L - 1) else None for l in range(L)]
+        self.aggregator = aggregator
+        self.ew = ([z(pcaps[l], dt=torch.float32) for l in range(L)]
+                   if aggregator != "mean" else None)
         # per hidden block: transpose (source rank -> edges) for the gather bwd
         # (``transpose_layers`` limits it to some hidden blocks; default all)
         self.need_transpose = need_transpose and need_local
@@ -245,6 +253,7 @@ class DeviceSampler:
         if self.need_transpose:
             out.trans = [(self.t_indptr[l], self.t_dst[l], self.t_w[l], self.n_nodes[l + 1])
                          if l in self.t_layers else None for l in range(L - 1)] + [None]
+        out.ew = self.ew
         return out
 
     # ------------------------------------------------------------ sample
@@ -270,6 +279,11 @@ class DeviceSampler:
                    N.ptr(self.rng), N.ptr(self.indptr[l]), N.ptr(self.picks[l]), self.pcaps[l],
                    N.ptr(self.n_picks[l]), bm if expand else None, N.ptr(self.ws_layer),
                    self.ws_layer.numel(), N.ptr(self.err), s)
+            if self.ew is not None:
+                N.call("fg_block_edge_weights", AGGREGATORS.index(self.aggregator),
+                       N.ptr(self.g.row_offsets), N.ptr(self.nodes[l]), N.ptr(self.indptr[l]),
+                       N.ptr(self.picks[l]), N.ptr(self.n_nodes[l]), self.caps[l],
+                       N.ptr(self.ew[l]), s)
             if self.want_frontier:
                 N.call("fg_bitmap_mark", N.ptr(self.picks[l]), N.ptr(self.n_picks[l]),
                        self.pcaps[l], N.ptr(self.fbitmap), s)
@@ -283,11 +297,7 @@ class DeviceSampler:
                         self._transpose(l, s)
                 N.call("fg_bitmap_clear", N.ptr(self.nodes[l + 1]), N.ptr(self.n_nodes[l + 1]),
                        self.caps[l + 1], bm, s)
-        out = SampledBatch(self.nodes, self.n_nodes, self.indptr, self.picks, self.n_picks,
-                           self.local)
-        if self.need_transpose:
-            out.trans = [(self.t_indptr[l], self.t_dst[l], self.t_w[l], self.n_nodes[l + 1])
-                         if l in self.t_layers else None for l in range(L - 1)] + [None]
+        out = self.batch_view()
         if self.want_frontier:
             N.call("fg_bitmap_compact", N.ptr(self.fbitmap), n, N.ptr(self.frontier), self.fcap,
                    N.ptr(self.n_frontier), None, N.ptr(self.ws_fbm), self.ws_fbm.numel(), s)
@@ -318,7 +328,8 @@ class DeviceSampler:
         N.call("fg_block_transpose", N.ptr(self.local[l]), N.ptr(self.n_picks[l]), self.pcaps[l],
                N.ptr(self.indptr[l]), N.ptr(self.n_nodes[l]), self.caps[l], self.fanouts[l],
                self.caps[l + 1], N.ptr(self.t_indptr[l]), N.ptr(self.t_dst[l]), N.ptr(self.t_w[l]),
-               N.ptr(self.t_scratch), self.t_scratch.numel(), s)
+               N.ptr(self.ew[l]) if self.ew is not None else None, N.ptr(self.t_scratch),
+               self.t_scratch.numel(), s)
 
     def sample(self, b: int) -> SampledBatch:
         self.load_seeds(b)

@@ -7,6 +7,7 @@ import pytest
 import torch
 
 import paper_2207_14696_b200 as fg
+from paper_2207_14696_b200 import _native as N
 from paper_2207_14696_b200.aggregate import block_mean, gather_dequant_mean
 from oracle import codecs as oc
 from oracle.aggregate import block_mean as oracle_mean
@@ -205,7 +206,7 @@ def test_block_transpose_kernel():
     ne_t, nd_t = torch.tensor([E], device=dev), torch.tensor([n_dst], device=dev)
     ip_t = torch.from_numpy(indptr).to(dev)  # keep every buffer alive until sync
     N.call("fg_block_transpose", N.ptr(local), N.ptr(ne_t), cap_e, N.ptr(ip_t), N.ptr(nd_t),
-           max_dst, 10, n_src, N.ptr(t_indptr), N.ptr(t_dst), N.ptr(t_w), N.ptr(scratch),
+           max_dst, 10, n_src, N.ptr(t_indptr), N.ptr(t_dst), N.ptr(t_w), None, N.ptr(scratch),
            scratch.numel(), N.stream_handle())
     torch.cuda.synchronize()
     ti, td, tw = _transpose_np(indptr, src, n_dst, n_src)
@@ -323,3 +324,118 @@ def test_input_block_mean_autograd_matches_unfused():
     a2.backward(gout)
     rel = ((w1.grad - w2.grad).norm() / w2.grad.norm()).item()
     assert rel < 1e-2, rel
+
+
+# ----------------------------------------------------- aggregator variants
+def _run_wsum(dc, indptr, src, w, n_dst, max_dst, dtype, pitch):
+    dev = "cuda"
+    out = torch.full((max_dst, pitch), 7.0, dtype=dtype, device=dev)
+    gather_dequant_mean(dc, torch.from_numpy(indptr).to(dev), torch.from_numpy(src).to(dev),
+                        torch.tensor([n_dst], device=dev), max_dst, out=out,
+                        edge_w=torch.from_numpy(w.astype(np.float32)).to(dev))
+    o = out.float().cpu().numpy()
+    assert (o[n_dst:] == 7.0).all()
+    return o[:, :dc.d]
+
+
+@pytest.mark.parametrize("codec,fan", [(("sq", 8, 100), 7), (("sq", 4, 128), 7),
+                                       (("sq", 8, 128), 40), (("sq", 3, 100), 5),
+                                       (("vq", 4, 256, 100), 6), (("vq", 8, 256, 768), 5),
+                                       (("vq", 2, 256, 33), 6)])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_fused_weighted_sum_matches_oracle(codec, fan, dtype):
+    """fg_gather_dequant_wsum (GCN path through the fused kernels) against the
+    float64 oracle sum_e w_e x_e with random positive weights."""
+    from oracle.aggregate import block_wsum, wsum_tolerance_ok
+    rng = np.random.default_rng(fan + codec[1] + codec[-1])
+    n = 4000
+    if codec[0] == "sq":
+        k, d = codec[1], codec[2]
+        x = (np.exp(rng.normal(0, 1, (n, d))) * rng.choice([-1, 1], (n, d))).astype(np.float32)
+        f = fg.FeatureMatrix(x)
+        c = fg.quantize_sq(f, fg.fit_sq(f, k))
+        dc = fg.DeviceSqCodec.from_codec(c)
+    else:
+        w_, L, d = codec[1], codec[2], codec[3]
+        c = _vq_codec(n, d, w_, L, rng)
+        dc = fg.DeviceVqCodec.from_codec(c)
+    n_dst, max_dst = 2500, 2600
+    counts, indptr, src = _block(n, n_dst, max_dst, fan, rng)
+    wts = rng.uniform(0.05, 2.0, src.size)
+    got = _run_wsum(dc, indptr, src, wts, n_dst, max_dst, dtype, (d + 15) // 16 * 16)
+    if codec[0] == "sq":
+        dec = oc.sq_dequant_rows(c.payload, n, d, codec[1], c.params.e_min, c.params.e_max, src)
+    else:
+        dec = oc.vq_decode(c.codes, c.codebooks, d, codec[1], src)
+    ref = block_wsum(dec, counts, wts.astype(np.float32))
+    tol = 1e-5 if dtype == torch.float32 else 1e-2
+    ok, worst = wsum_tolerance_ok(got[:n_dst], ref, dec, counts, wts, tol)
+    assert ok, worst
+
+
+def test_block_edge_weights_gcn_and_mean():
+    from oracle.aggregate import gcn_weights
+    from paper_2207_14696_b200.aggregate import edge_weights
+    from paper_2207_14696_b200.synth import generate_graph
+    dg, _ = generate_graph(5000, 12.0, 4, seed=3)
+    host = dg.to_host()
+    rng = np.random.default_rng(1)
+    n_dst, max_dst = 700, 800
+    dst_nodes = np.sort(rng.choice(5000, n_dst, replace=False)).astype(np.int32)
+    counts, indptr, src = _block(5000, n_dst, max_dst, 9, rng)
+    dev = "cuda"
+    dn = torch.zeros(max_dst, dtype=torch.int32, device=dev)
+    dn[:n_dst] = torch.from_numpy(dst_nodes).to(dev)
+    args = (dg, dn, torch.from_numpy(indptr).to(dev), torch.from_numpy(src).to(dev),
+            torch.tensor([n_dst], device=dev), max_dst)
+    w = torch.zeros(src.size, dtype=torch.float32, device=dev)
+    edge_weights("gcn", *args, w)
+    want = gcn_weights(host.row_offsets, dst_nodes, counts, src)
+    np.testing.assert_allclose(w.cpu().numpy(), want, rtol=2e-6)
+    edge_weights("mean", *args, w)
+    np.testing.assert_allclose(w.cpu().numpy(), 1.0 / np.repeat(counts, counts), rtol=1e-7)
+
+
+def test_hidden_block_weighted_fwd_bwd_and_wgrad():
+    """Edge-weighted hidden block: forward (fg_block_mean_fwd with weights),
+    gather backward over a weighted transpose, and the edge-tiled wgrad with
+    weights, against torch fp32."""
+    from paper_2207_14696_b200.aggregate import block_mean_wgrad
+    rng = np.random.default_rng(21)
+    n_src, n_dst, max_dst, H, P = 3000, 800, 850, 256, 112
+    counts, indptr, src = _block(n_src, n_dst, max_dst, 10, rng)
+    wts = rng.uniform(0.1, 1.5, src.size).astype(np.float32)
+    dev = "cuda"
+    ip, sl = torch.from_numpy(indptr).to(dev), torch.from_numpy(src).to(dev)
+    nd = torch.tensor([n_dst], device=dev)
+    ew = torch.from_numpy(wts).to(dev)
+    # weighted transpose
+    cap_e = src.size
+    t_indptr = torch.zeros(n_src + 1, dtype=torch.int32, device=dev)
+    t_dst = torch.zeros(cap_e, dtype=torch.int32, device=dev)
+    t_w = torch.zeros(cap_e, dtype=torch.float32, device=dev)
+    scratch = torch.zeros(N.lib().fg_block_transpose_scratch_bytes(n_src), dtype=torch.uint8,
+                          device=dev)
+    ne_t = torch.tensor([cap_e], device=dev)
+    N.call("fg_block_transpose", N.ptr(sl), N.ptr(ne_t), cap_e, N.ptr(ip), N.ptr(nd), max_dst,
+           10, n_src, N.ptr(t_indptr), N.ptr(t_dst), N.ptr(t_w), N.ptr(ew), N.ptr(scratch),
+           scratch.numel(), N.stream_handle())
+    trans = (t_indptr, t_dst, t_w, torch.tensor([n_src], device=dev))
+    h = torch.randn(n_src, H, device=dev).to(torch.bfloat16).requires_grad_(True)
+    a = block_mean(h, ip, sl, nd, max_dst, relu=True, trans=trans, bias_col=True, edge_w=ew)
+    seg = torch.repeat_interleave(torch.arange(n_dst, device=dev),
+                                  torch.from_numpy(counts).long().to(dev))
+    hf = h.detach().float().requires_grad_(True)
+    ref = torch.zeros(n_dst, H, device=dev).index_add_(0, seg, torch.relu(hf[sl.long()]) *
+                                                       ew[:, None])
+    assert torch.allclose(a[:n_dst, :H].float(), ref, atol=2e-2, rtol=1e-2)
+    g = torch.randn(max_dst, H + 8, device=dev).to(torch.bfloat16)
+    a.backward(g)
+    ref.backward(g[:n_dst, :H].float())
+    assert torch.allclose(h.grad.float(), hf.grad, atol=2e-2, rtol=2e-2)
+    # weighted wgrad: dW = sum_e (relu'(h[l_e]) * w_e g[v_e])^T x[l_e]
+    x = torch.randn(n_src, P, device=dev).to(torch.bfloat16)
+    dw = block_mean_wgrad(g, ip, sl, nd, max_dst, h.detach(), x, H=H, edge_w=ew)
+    term = g[seg, :H].float() * ew[:, None] * (h.detach()[sl.long()].float() > 0)
+    want = term.to(torch.bfloat16).float().t() @ x[sl.long()].float()
+    assert (dw - want).abs().max().item() <= 1e-3 * want.abs().max().item() + 1e-4
