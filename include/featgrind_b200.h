@@ -327,7 +327,8 @@ int fg_rng_permutation_host(uint64_t* block_host, int64_t* ids, int64_t count);
  * node with deg > f), with per-node stream offsets from a prefix sum and a
  * rejection fix-up pass.  Writes indptr [max_nodes + 1] (int32, CSR over the
  * layer's nodes), picks (int32, choice output order), *num_picks_dev, marks
- * every pick in `bitmap` (n bits, caller-cleared) and advances rng_dev past
+ * every pick in `bitmap` (fg_bitmap_words(n) words, caller-cleared; may be NULL)
+ * and advances rng_dev past
  * the layer.  Workspace: fg_sample_workspace_bytes(max_nodes). */
 int fg_sample_layer(const int64_t* row_offsets, const int32_t* col_indices,
                     int64_t n, const int32_t* nodes, const int64_t* num_nodes_dev,
@@ -339,11 +340,15 @@ int64_t fg_sample_workspace_bytes(int64_t max_nodes);
 
 /* Bitmap set algebra used for np.unique on node ids (ids < n):
  * mark ids, then emit the sorted unique list, keep a per-word rank prefix so
- * fg_bitmap_rank maps ids to their position in that list, then clear. */
+ * fg_bitmap_rank maps ids to their position in that list, then clear.
+ * The bitmap is two-level: fg_bitmap_words(n) uint32 words (caller-zeroed):
+ * one bit per node plus one bit per non-empty node word, so compaction reads
+ * only the words that hold marks. */
+int64_t fg_bitmap_words(int64_t n);
 int fg_bitmap_mark(const int32_t* ids, const int64_t* count_dev, int64_t max_count,
-                   uint32_t* bitmap, void* cuda_stream);
+                   uint32_t* bitmap, int64_t n, void* cuda_stream);
 int fg_bitmap_mark64(const int64_t* ids, const int64_t* count_dev, int64_t max_count,
-                     uint32_t* bitmap, void* cuda_stream);
+                     uint32_t* bitmap, int64_t n, void* cuda_stream);
 int fg_bitmap_compact(uint32_t* bitmap, int64_t n, int32_t* out_ids,
                       int64_t max_out, int64_t* out_count_dev,
                       int32_t* word_prefix, void* workspace,
@@ -351,9 +356,9 @@ int fg_bitmap_compact(uint32_t* bitmap, int64_t n, int32_t* out_ids,
 int64_t fg_bitmap_workspace_bytes(int64_t n);
 int fg_bitmap_rank(const int32_t* ids, const int64_t* count_dev, int64_t max_count,
                    const uint32_t* bitmap, const int32_t* word_prefix,
-                   int32_t* out_rank, void* cuda_stream);
+                   int32_t* rank_out, void* cuda_stream);
 int fg_bitmap_clear(const int32_t* ids, const int64_t* count_dev, int64_t max_count,
-                    uint32_t* bitmap, void* cuda_stream);
+                    uint32_t* bitmap, int64_t n, void* cuda_stream);
 
 /* ----------------------------------------------------- synthetic data */
 /* Deterministic, row-addressable synthetic inputs: feature

@@ -78,12 +78,13 @@ _SIGS = {
     "fg_sample_layer": (ci, [vp, vp, i64, vp, vp, i64, ci, vp, vp, vp, i64, vp, vp, vp, i64,
                              vp, vp]),
     "fg_sample_workspace_bytes": (i64, [i64]),
-    "fg_bitmap_mark": (ci, [vp, vp, i64, vp, vp]),
-    "fg_bitmap_mark64": (ci, [vp, vp, i64, vp, vp]),
+    "fg_bitmap_words": (i64, [i64]),
+    "fg_bitmap_mark": (ci, [vp, vp, i64, vp, i64, vp]),
+    "fg_bitmap_mark64": (ci, [vp, vp, i64, vp, i64, vp]),
     "fg_bitmap_compact": (ci, [vp, i64, vp, i64, vp, vp, vp, i64, vp]),
     "fg_bitmap_workspace_bytes": (i64, [i64]),
     "fg_bitmap_rank": (ci, [vp, vp, i64, vp, vp, vp, vp]),
-    "fg_bitmap_clear": (ci, [vp, vp, i64, vp, vp]),
+    "fg_bitmap_clear": (ci, [vp, vp, i64, vp, i64, vp]),
     "fg_synth_features": (ci, [ci, u64, i64, i64, i64, vp, ci, vp, vp]),
     "fg_synth_feature_rows": (ci, [ci, u64, vp, i64, i64, vp, ci, vp, vp]),
     "fg_graph_degrees": (ci, [u64, i64, i64, C.c_double, C.c_double, i64, vp, vp]),

@@ -38,7 +38,7 @@ __device__ __forceinline__ uint4 f32_to_bf16x8(const float* f) {
 
 // RELU: apply max(0, .) to the source rows as they are loaded (the SAGE
 // activation of the previous layer, fused so it never makes its own pass).
-template <bool RELU>
+template <bool RELU, bool WT>
 __global__ void __launch_bounds__(256)
 k_block_mean_fwd(const uint16_t* __restrict__ h, int64_t H, const int32_t* __restrict__ indptr,
                  const int32_t* __restrict__ srcl, const int64_t* __restrict__ ndst_dev,
@@ -72,14 +72,14 @@ k_block_mean_fwd(const uint16_t* __restrict__ h, int64_t H, const int32_t* __res
         for (int u = 0; u < 8; ++u)
           if (e + u < e1) {
             q[u] = __ldg(reinterpret_cast<const uint4*>(h + (int64_t)sl[u] * H) + c);
-            wgt[u] = ew ? __ldg(ew + e + u) : 1.0f;
+            if constexpr (WT) wgt[u] = __ldg(ew + e + u);
           }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           if (e + u < e1) {
             float f[8];
             bf16x8_to_f32(q[u], f);
-            if (ew) {
+            if constexpr (WT) {
 #pragma unroll
               for (int j = 0; j < 8; ++j) acc[j] = fmaf(wgt[u], RELU ? fmaxf(f[j], 0.f) : f[j], acc[j]);
             } else {
@@ -89,7 +89,7 @@ k_block_mean_fwd(const uint16_t* __restrict__ h, int64_t H, const int32_t* __res
           }
         }
       }
-      if (cnt && !ew) {
+      if (cnt && !WT) {
         const float inv = 1.0f / (float)cnt;
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[j] *= inv;
@@ -157,14 +157,20 @@ int fg_block_mean_fwd(const uint16_t* h, int64_t H, const int32_t* indptr, const
   FG_CHECK_ARG(out_ld == H || out_ld == H + 8, "out_ld must be H or H + 8 (ones column)");
   if (max_dst == 0) return FG_OK;
   const int64_t total = max_dst * (out_ld / 8);
-  if (relu_in)
-    k_block_mean_fwd<true><<<grid_for(total, 256), 256, 0, as_stream(s)>>>(h, H, indptr, srcl,
-                                                                           ndst, max_dst, out,
-                                                                           out_ld, edge_w);
+  const int grid = grid_for(total, 256);
+  cudaStream_t st = as_stream(s);
+  if (relu_in && edge_w)
+    k_block_mean_fwd<true, true><<<grid, 256, 0, st>>>(h, H, indptr, srcl, ndst, max_dst, out,
+                                                        out_ld, edge_w);
+  else if (relu_in)
+    k_block_mean_fwd<true, false><<<grid, 256, 0, st>>>(h, H, indptr, srcl, ndst, max_dst, out,
+                                                         out_ld, nullptr);
+  else if (edge_w)
+    k_block_mean_fwd<false, true><<<grid, 256, 0, st>>>(h, H, indptr, srcl, ndst, max_dst, out,
+                                                         out_ld, edge_w);
   else
-    k_block_mean_fwd<false><<<grid_for(total, 256), 256, 0, as_stream(s)>>>(h, H, indptr, srcl,
-                                                                            ndst, max_dst, out,
-                                                                            out_ld, edge_w);
+    k_block_mean_fwd<false, false><<<grid, 256, 0, st>>>(h, H, indptr, srcl, ndst, max_dst, out,
+                                                          out_ld, nullptr);
   FG_LAUNCH_CHECK();
   return FG_OK;
 }

@@ -171,26 +171,33 @@ __device__ void layer_finish(const int64_t* __restrict__ off, const int32_t* __r
 
 // ------------------------------------------------------------- bitmap
 constexpr int kBmThreads = 256;
-constexpr int kBmWords = 8;  // words per thread
-constexpr int64_t kBmPerBlock = (int64_t)kBmThreads * kBmWords;
+
+// Two-level bitmap: level 0 = one bit per node (words0 words, a multiple of
+// 32), level 1 = one bit per level-0 word (at bm + words0), set by the
+// marker that turned the word non-zero.  Compaction walks level 1 and reads
+// only non-empty level-0 words (MAG240M-shape: 1 MB instead of 30 MB per
+// unique, and the word-prefix table is written only where ranks are asked).
+inline int64_t bm_words0(int64_t n) { return ((n + 31) / 32 + 31) / 32 * 32; }
+
+__device__ __forceinline__ void bm_mark(uint32_t* __restrict__ bm, int64_t words0, int64_t v) {
+  const int64_t w = v >> 5;
+  const uint32_t old = atomicOr(bm + w, 1u << (v & 31));
+  if (old == 0u) atomicOr(bm + words0 + (w >> 5), 1u << (w & 31));
+}
 
 __global__ void k_mark32(const int32_t* __restrict__ ids, const int64_t* __restrict__ cnt,
-                         int64_t max_count, uint32_t* __restrict__ bm) {
+                         int64_t max_count, uint32_t* __restrict__ bm, int64_t words0) {
   const int64_t live = min64(*cnt, max_count);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < live;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t v = ids[i];
-    atomicOr(bm + (v >> 5), 1u << (v & 31));
-  }
+       i += (int64_t)gridDim.x * blockDim.x)
+    bm_mark(bm, words0, ids[i]);
 }
 __global__ void k_mark64(const int64_t* __restrict__ ids, const int64_t* __restrict__ cnt,
-                         int64_t max_count, uint32_t* __restrict__ bm) {
+                         int64_t max_count, uint32_t* __restrict__ bm, int64_t words0) {
   const int64_t live = min64(*cnt, max_count);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < live;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t v = ids[i];
-    atomicOr(bm + (v >> 5), 1u << (v & 31));
-  }
+       i += (int64_t)gridDim.x * blockDim.x)
+    bm_mark(bm, words0, ids[i]);
 }
 
 
@@ -487,10 +494,12 @@ k_layer_fixup(const int64_t* __restrict__ off, const int32_t* __restrict__ col,
                &s_bad, delta);
 }
 
-// Single-pass compaction: popcounts, block scan, look-back prefix, ordered
-// emit of set bits (ascending ids) and the per-word rank prefix.
+// Single-pass compaction over level 1: thread per quarter of a level-1 word
+// (8 level-0 words = 256 node ids); popcounts of its non-empty words, block
+// scan, decoupled look-back prefix, ordered emit of the set bits (ascending
+// ids) and the word prefix of every non-empty level-0 word.
 __global__ void __launch_bounds__(kBmThreads)
-k_bm_compact(const uint32_t* __restrict__ bm, int64_t words, unsigned long long* status,
+k_bm_compact(const uint32_t* __restrict__ bm, int64_t words0, unsigned long long* status,
              unsigned int* ctr, int32_t* __restrict__ out, int64_t max_out,
              int64_t* __restrict__ out_count, int32_t* __restrict__ wprefix, unsigned int ntiles) {
   using BS = cub::BlockScan<unsigned long long, kBmThreads>;
@@ -499,27 +508,27 @@ k_bm_compact(const uint32_t* __restrict__ bm, int64_t words, unsigned long long*
   __shared__ unsigned long long s_u64;
   const ScanState sc{status, ctr, ctr + 1};
   const unsigned int tile = scan_take_tile(sc, &s_u32);
-  const int64_t w0 = (int64_t)tile * kBmPerBlock + threadIdx.x * (int64_t)kBmWords;
-  uint32_t wv[kBmWords];
+  // item = (level-1 word j, quarter qq): level-0 words 32j + 8qq .. +7
+  const int64_t l1w = words0 / 32;
+  const int64_t item = (int64_t)tile * kBmThreads + threadIdx.x;
+  const int64_t j = item >> 2;
+  const int qq = (int)(item & 3);
+  const uint32_t l1 = j < l1w ? (bm[words0 + j] >> (8 * qq)) & 0xFFu : 0u;
+  const int64_t wbase = j * 32 + 8 * qq;
   unsigned long long c = 0;
-#pragma unroll
-  for (int k = 0; k < kBmWords; ++k) {
-    wv[k] = (w0 + k < words) ? bm[w0 + k] : 0u;
-    c += __popc(wv[k]);
-  }
+  for (uint32_t x = l1; x; x &= x - 1) c += __popc(bm[wbase + (__ffs(x) - 1)]);
   unsigned long long excl, agg;
   BS(tmp).ExclusiveSum(c, excl, agg);
   const unsigned long long prefix = scan_tile_prefix(sc, tile, agg, &s_u64);
   int64_t pos = (int64_t)(prefix + excl);
-#pragma unroll
-  for (int k = 0; k < kBmWords; ++k) {
-    if (w0 + k >= words) break;
-    if (wprefix) wprefix[w0 + k] = (int32_t)pos;
-    uint32_t x = wv[k];
-    while (x) {
-      const int b = __ffs(x) - 1;
-      x &= x - 1;
-      if (pos < max_out) out[pos] = (int32_t)(((w0 + k) << 5) + b);
+  for (uint32_t x = l1; x; x &= x - 1) {
+    const int64_t w = wbase + (__ffs(x) - 1);
+    uint32_t bits = bm[w];
+    if (wprefix) wprefix[w] = (int32_t)pos;
+    while (bits) {
+      const int b = __ffs(bits) - 1;
+      bits &= bits - 1;
+      if (pos < max_out) out[pos] = (int32_t)((w << 5) + b);
       ++pos;
     }
   }
@@ -540,11 +549,14 @@ __global__ void k_bm_rank(const int32_t* __restrict__ ids, const int64_t* __rest
 }
 
 __global__ void k_bm_clear(const int32_t* __restrict__ ids, const int64_t* __restrict__ cnt,
-                           int64_t max_count, uint32_t* __restrict__ bm) {
+                           int64_t max_count, uint32_t* __restrict__ bm, int64_t words0) {
   const int64_t live = min64(*cnt, max_count);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < live;
-       i += (int64_t)gridDim.x * blockDim.x)
-    bm[ids[i] >> 5] = 0u;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t w = ids[i] >> 5;
+    bm[w] = 0u;
+    bm[words0 + (w >> 5)] = 0u;
+  }
 }
 
 }  // namespace fg
@@ -620,30 +632,35 @@ int fg_sample_layer(const int64_t* row_offsets, const int32_t* col_indices, int6
                                                        err_flag);
   FG_LAUNCH_CHECK();
   if (bitmap) {  // next layer's unique set: mark after any fix-up rewrote picks
-    k_mark32<<<grid_for(max_picks, 256), 256, 0, st>>>(picks, num_picks_dev, max_picks, bitmap);
+    k_mark32<<<grid_for(max_picks, 256), 256, 0, st>>>(picks, num_picks_dev, max_picks, bitmap,
+                                                       bm_words0(n));
     FG_LAUNCH_CHECK();
   }
   return FG_OK;
 }
 
+int64_t fg_bitmap_words(int64_t n) { return bm_words0(n) + bm_words0(n) / 32; }
+
 int64_t fg_bitmap_workspace_bytes(int64_t n) {
-  const int64_t words = (n + 31) / 32;
-  const int64_t nb = ceil_div(words > 0 ? words : 1, kBmPerBlock);
+  const int64_t l1w = bm_words0(n > 0 ? n : 1) / 32;
+  const int64_t nb = ceil_div(4 * l1w, kBmThreads);
   return align256(64 + nb * 8);
 }
 
 int fg_bitmap_mark(const int32_t* ids, const int64_t* cnt, int64_t max_count, uint32_t* bm,
-                   void* s) {
+                   int64_t n, void* s) {
   if (max_count == 0) return FG_OK;
-  k_mark32<<<grid_for(max_count, 256), 256, 0, as_stream(s)>>>(ids, cnt, max_count, bm);
+  k_mark32<<<grid_for(max_count, 256), 256, 0, as_stream(s)>>>(ids, cnt, max_count, bm,
+                                                               bm_words0(n));
   FG_LAUNCH_CHECK();
   return FG_OK;
 }
 
 int fg_bitmap_mark64(const int64_t* ids, const int64_t* cnt, int64_t max_count, uint32_t* bm,
-                     void* s) {
+                     int64_t n, void* s) {
   if (max_count == 0) return FG_OK;
-  k_mark64<<<grid_for(max_count, 256), 256, 0, as_stream(s)>>>(ids, cnt, max_count, bm);
+  k_mark64<<<grid_for(max_count, 256), 256, 0, as_stream(s)>>>(ids, cnt, max_count, bm,
+                                                               bm_words0(n));
   FG_LAUNCH_CHECK();
   return FG_OK;
 }
@@ -653,12 +670,12 @@ int fg_bitmap_compact(uint32_t* bm, int64_t n, int32_t* out_ids, int64_t max_out
   FG_CHECK_ARG(n >= 1 && n < INT32_MAX, "fg_bitmap_compact: n must be in [1, 2^31)");
   FG_CHECK_ARG(ws_bytes >= fg_bitmap_workspace_bytes(n), "fg_bitmap_compact: workspace too small");
   cudaStream_t st = as_stream(s);
-  const int64_t words = (n + 31) / 32;
-  const int64_t nb = ceil_div(words, kBmPerBlock);
+  const int64_t words0 = bm_words0(n);
+  const int64_t nb = ceil_div(4 * (words0 / 32), kBmThreads);
   unsigned int* ctr = (unsigned int*)ws;
   unsigned long long* status = (unsigned long long*)((char*)ws + 64);
   FG_CUDA_TRY(cudaMemsetAsync(ws, 0, 64 + nb * 8, st));
-  k_bm_compact<<<(unsigned)nb, kBmThreads, 0, st>>>(bm, words, status, ctr, out_ids, max_out,
+  k_bm_compact<<<(unsigned)nb, kBmThreads, 0, st>>>(bm, words0, status, ctr, out_ids, max_out,
                                                     out_count, wprefix, (unsigned)nb);
   FG_LAUNCH_CHECK();
   return FG_OK;
@@ -674,9 +691,10 @@ int fg_bitmap_rank(const int32_t* ids, const int64_t* cnt, int64_t max_count, co
 }
 
 int fg_bitmap_clear(const int32_t* ids, const int64_t* cnt, int64_t max_count, uint32_t* bm,
-                    void* s) {
+                    int64_t n, void* s) {
   if (max_count == 0) return FG_OK;
-  k_bm_clear<<<grid_for(max_count, 256), 256, 0, as_stream(s)>>>(ids, cnt, max_count, bm);
+  k_bm_clear<<<grid_for(max_count, 256), 256, 0, as_stream(s)>>>(ids, cnt, max_count, bm,
+                                                                  bm_words0(n));
   FG_LAUNCH_CHECK();
   return FG_OK;
 }

@@ -177,7 +177,7 @@ class DeviceSampler:
                 self.t_scratch = share.t_scratch
             self.want_frontier = False
             return
-        words = (n + 31) // 32
+        words = N.lib().fg_bitmap_words(n)  # two-level: node bits + non-empty-word bits
         self.bitmap = torch.zeros(words, dtype=torch.int32, device=dev)
         self.wprefix = torch.zeros(words, dtype=torch.int32, device=dev)
         self.ws_bm = torch.zeros(max(N.lib().fg_bitmap_workspace_bytes(n), 256),
@@ -264,13 +264,14 @@ class DeviceSampler:
         n = self.g.n
         bm, wp = N.ptr(self.bitmap), N.ptr(self.wprefix)
         # seeds = sort(perm slice): bitmap order gives ascending ids
-        N.call("fg_bitmap_mark64", N.ptr(self.seed_in), N.ptr(self.n_seed_in), self.bs, bm, s)
+        N.call("fg_bitmap_mark64", N.ptr(self.seed_in), N.ptr(self.n_seed_in), self.bs, bm, n, s)
         N.call("fg_bitmap_compact", bm, n, N.ptr(self.nodes[0]), self.caps[0],
                N.ptr(self.n_nodes[0]), None, N.ptr(self.ws_bm), self.ws_bm.numel(), s)
-        N.call("fg_bitmap_clear", N.ptr(self.nodes[0]), N.ptr(self.n_nodes[0]), self.caps[0], bm, s)
+        N.call("fg_bitmap_clear", N.ptr(self.nodes[0]), N.ptr(self.n_nodes[0]), self.caps[0], bm,
+               n, s)
         if self.want_frontier:
             N.call("fg_bitmap_mark", N.ptr(self.nodes[0]), N.ptr(self.n_nodes[0]), self.caps[0],
-                   N.ptr(self.fbitmap), s)
+                   N.ptr(self.fbitmap), n, s)
         for l, f in enumerate(self.fanouts):
             last = l == L - 1
             expand = (not last) or self.unique_last
@@ -286,7 +287,7 @@ class DeviceSampler:
                        N.ptr(self.ew[l]), s)
             if self.want_frontier:
                 N.call("fg_bitmap_mark", N.ptr(self.picks[l]), N.ptr(self.n_picks[l]),
-                       self.pcaps[l], N.ptr(self.fbitmap), s)
+                       self.pcaps[l], N.ptr(self.fbitmap), n, s)
             if expand:
                 N.call("fg_bitmap_compact", bm, n, N.ptr(self.nodes[l + 1]), self.caps[l + 1],
                        N.ptr(self.n_nodes[l + 1]), wp, N.ptr(self.ws_bm), self.ws_bm.numel(), s)
@@ -296,13 +297,13 @@ class DeviceSampler:
                     if self.need_transpose and l in self.t_layers:
                         self._transpose(l, s)
                 N.call("fg_bitmap_clear", N.ptr(self.nodes[l + 1]), N.ptr(self.n_nodes[l + 1]),
-                       self.caps[l + 1], bm, s)
+                       self.caps[l + 1], bm, n, s)
         out = self.batch_view()
         if self.want_frontier:
             N.call("fg_bitmap_compact", N.ptr(self.fbitmap), n, N.ptr(self.frontier), self.fcap,
                    N.ptr(self.n_frontier), None, N.ptr(self.ws_fbm), self.ws_fbm.numel(), s)
             N.call("fg_bitmap_clear", N.ptr(self.frontier), N.ptr(self.n_frontier), self.fcap,
-                   N.ptr(self.fbitmap), s)
+                   N.ptr(self.fbitmap), n, s)
             out.frontier, out.n_frontier = self.frontier, self.n_frontier
         return out
 

@@ -25,7 +25,8 @@ def main():
     torch.autograd.set_multithreading_enabled(False)
     sg, dc, desc, fanouts, bs, hidden = bench.build_workload(a.config, dev, scale=a.scale)
     tr = SageTrainer(sg.graph, dc, sg.labels, sg.num_classes,
-                     TrainConfig(fanouts=fanouts, batch_size=bs, hidden=hidden))
+                     TrainConfig(fanouts=fanouts, batch_size=bs, hidden=hidden,
+                                 aggregator=bench.aggregator_of(a.config)))
     tr.begin_epoch(sg.train_ids, 0)
     for b in range(3):
         tr.step(b)
