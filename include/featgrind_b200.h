@@ -265,8 +265,7 @@ int fg_block_mean_bwd_t(const uint16_t* grad_out, int64_t h_dim, int64_t g_ld,
  * block (indptr [max_dst + 1], local [edges]: source row of each edge), computes
  *   dW = sum_{edges e of live dst v} ( relu'(h_mask[local[e]]) * g[v, :h_dim] / cnt_v )^T x[local[e]]
  * (= dH^T x) into dw [h_dim, p_dim] fp32 (overwritten) without materialising
- * dH; the GEMM's K dimension is the block's edges, 128 per tile.  h_mask may
- * be NULL (no ReLU).  Shapes: fg_block_mean_wgrad_supported(h_dim, p_dim) != 0
+ * dH; the GEMM's K dimension is the block's edges, 128 per tile.  Shapes: fg_block_mean_wgrad_supported(h_dim, p_dim) != 0
  * (h_dim 128 or 256, p_dim % 16 == 0, p_dim <= 160 at h_dim 256).  scratch:
  * fg_block_mean_wgrad_scratch_bytes(h_dim, p_dim) (fp32 partials per SM,
  * reduced in fixed order: deterministic).  The edge -> dst map is resolved
@@ -277,9 +276,16 @@ int fg_block_mean_wgrad_supported(int64_t h_dim, int64_t p_dim);
 int64_t fg_block_mean_wgrad_scratch_bytes(int64_t h_dim, int64_t p_dim);
 int fg_block_mean_wgrad(const uint16_t* grad_out, int64_t g_ld, const int32_t* indptr,
                         const int32_t* local, const int64_t* n_dst_dev, int64_t max_dst,
-                        const float* edge_w, const uint16_t* h_mask, int64_t h_dim,
+                        const float* edge_w, const void* relu_mask, int mask_kind,
+                        int64_t h_dim,
                         const uint16_t* x, int64_t p_dim, float* dw, float* scratch,
                         int64_t scratch_bytes, void* cuda_stream);
+/* relu_mask / mask_kind of fg_block_mean_wgrad: 0 = no ReLU (relu_mask
+ * NULL), 1 = bf16 pre-activation rows [cap_src, h_dim], 2 = packed bits
+ * [cap_src, h_dim / 8] bytes from fg_relu_mask_bits (32 B per row at
+ * h_dim 256 instead of 512: the gradient kernel's largest gather). */
+int fg_relu_mask_bits(const uint16_t* h, int64_t rows, int64_t h_dim, uint8_t* out_bits,
+                      void* cuda_stream);
 
 /* Fused softmax cross-entropy over padded logits [rows, ld] (bf16 or fp32):
  * rows r < *n_valid_dev use label labels[row_node[r]] over the first

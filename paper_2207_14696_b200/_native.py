@@ -66,8 +66,9 @@ _SIGS = {
     "fg_block_mean_bwd_t": (ci, [vp, i64, i64, vp, vp, vp, vp, i64, vp, vp, vp]),
     "fg_block_mean_wgrad_supported": (ci, [i64, i64]),
     "fg_block_mean_wgrad_scratch_bytes": (i64, [i64, i64]),
-    "fg_block_mean_wgrad": (ci, [vp, i64, vp, vp, vp, i64, vp, vp, i64, vp, i64, vp, vp, i64,
-                                 vp]),
+    "fg_block_mean_wgrad": (ci, [vp, i64, vp, vp, vp, i64, vp, vp, ci, i64, vp, i64, vp, vp,
+                                 i64, vp]),
+    "fg_relu_mask_bits": (ci, [vp, i64, i64, vp, vp]),
     "fg_softmax_ce": (ci, [vp, ci, ci, i64, i64, vp, vp, vp, vp, vp, vp, vp, vp]),
     "fg_adam_step": (ci, [vp, vp, vp, vp, i64, vp, C.c_float, C.c_float, C.c_float, C.c_float,
                           C.c_float, vp, vp]),

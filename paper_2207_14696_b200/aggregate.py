@@ -136,6 +136,15 @@ def wgrad_supported(h_dim: int, p_dim: int) -> bool:
     return bool(N.lib().fg_block_mean_wgrad_supported(h_dim, p_dim))
 
 
+def relu_mask_bits(h, out=None):
+    """Packed ReLU mask of bf16 rows h [rows, H]: uint8 [rows, H/8]."""
+    rows, H = h.shape
+    if out is None:
+        out = torch.empty((rows, H // 8), dtype=torch.uint8, device=h.device)
+    N.call("fg_relu_mask_bits", N.ptr(h), rows, H, N.ptr(out), N.stream_handle())
+    return out
+
+
 def wgrad_scratch(H: int, P: int, device) -> torch.Tensor:
     nb = N.lib().fg_block_mean_wgrad_scratch_bytes(H, P)
     return torch.empty((nb + 3) // 4, dtype=torch.float32, device=device)
@@ -148,7 +157,8 @@ def block_mean_wgrad(g, indptr, local, n_dst, max_dst: int, h_mask, x, dw=None, 
     (``fg_block_mean_wgrad``: per-edge terms relu'(h[l_e]) * g[v_e] / cnt_v
     are built in shared memory and consumed by tcgen05 MMAs; neither they
     nor dH reach HBM).  g: [>= max_dst, >= H] bf16, x: [cap_src, P] bf16,
-    h_mask: [cap_src, H] bf16 or None; returns dw [H, P] fp32."""
+    h_mask: [cap_src, H] bf16 pre-activations, [cap_src, H/8] uint8 packed
+    ReLU bits (``relu_mask_bits``), or None; returns dw [H, P] fp32."""
     H = H or (h_mask.shape[1] if h_mask is not None else g.shape[1] - 8)
     P = x.shape[1]
     if dw is None:
@@ -156,7 +166,8 @@ def block_mean_wgrad(g, indptr, local, n_dst, max_dst: int, h_mask, x, dw=None, 
     if scratch is None:
         scratch = wgrad_scratch(H, P, x.device)
     N.call("fg_block_mean_wgrad", N.ptr(g), g.stride(0), N.ptr(indptr), N.ptr(local),
-           N.ptr(n_dst), max_dst, N.ptr(edge_w), N.ptr(h_mask) if h_mask is not None else None,
+           N.ptr(n_dst), max_dst, N.ptr(edge_w), N.ptr(h_mask),
+           0 if h_mask is None else (2 if h_mask.dtype == torch.uint8 else 1),
            H, N.ptr(x), P, N.ptr(dw), N.ptr(scratch), scratch.numel() * 4, N.stream_handle())
     return dw
 

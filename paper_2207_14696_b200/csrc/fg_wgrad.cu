@@ -127,7 +127,8 @@ __global__ void __launch_bounds__(kWgThreads, 1)
 k_block_mean_wgrad(const uint16_t* __restrict__ g, int64_t g_ld,
                    const int32_t* __restrict__ indptr, const int64_t* __restrict__ ndst_dev,
                    int64_t max_dst, const int32_t* __restrict__ local,
-                   const float* __restrict__ ew, const uint16_t* __restrict__ hmask, int H,
+                   const float* __restrict__ ew, const uint16_t* __restrict__ hmask,
+                   const uint8_t* __restrict__ mbits, int H,
                    const uint16_t* __restrict__ x, int P, float* __restrict__ partial,
                    uint32_t tmem_cols) {
   extern __shared__ __align__(1024) uint8_t wg_mem[];
@@ -288,7 +289,8 @@ k_block_mean_wgrad(const uint16_t* __restrict__ g, int64_t g_ld,
           s_w[r] = wt;
         }
         __syncwarp();
-        uint4 q[8], m[8];
+        uint4 q[8];
+        uint32_t mb[8];  // ReLU mask of the lane's 8 features (bit t = feature 8c+t)
         float w[8];
 #pragma unroll
         for (int rr = 0; rr < 8; ++rr) {
@@ -296,20 +298,28 @@ k_block_mean_wgrad(const uint16_t* __restrict__ g, int64_t g_ld,
           const int32_t l = s_l[r];
           w[rr] = s_w[r];
           q[rr] = make_uint4(0u, 0u, 0u, 0u);
-          m[rr] = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);  // 1.0
+          mb[rr] = 0xFFu;
           if (l >= 0) {
             q[rr] = __ldg(reinterpret_cast<const uint4*>(g + (int64_t)s_v[r] * g_ld) + c);
-            if (hmask) m[rr] = __ldg(reinterpret_cast<const uint4*>(hmask + (int64_t)l * H) + c);
+            if (mbits) {  // packed mask row: H/8 bytes, one per lane chunk
+              mb[rr] = __ldg(mbits + (int64_t)l * HB + c);
+            } else if (hmask) {
+              float mm[8];
+              bf16x8_f32(__ldg(reinterpret_cast<const uint4*>(hmask + (int64_t)l * H) + c), mm);
+              uint32_t bits = 0;
+#pragma unroll
+              for (int t = 0; t < 8; ++t) bits |= (mm[t] > 0.f ? 1u : 0u) << t;
+              mb[rr] = bits;
+            }
           }
         }
         const uint32_t core = abase + (uint32_t)((kb * HB + c) * kCoreA);
 #pragma unroll
         for (int rr = 0; rr < 8; ++rr) {
-          float f[8], mm[8], o8[8];
+          float f[8], o8[8];
           bf16x8_f32(q[rr], f);
-          bf16x8_f32(m[rr], mm);
 #pragma unroll
-          for (int t = 0; t < 8; ++t) o8[t] = mm[t] > 0.f ? f[t] * w[rr] : 0.f;
+          for (int t = 0; t < 8; ++t) o8[t] = (mb[rr] >> t) & 1u ? f[t] * w[rr] : 0.f;
           const uint4 o = f32_bf16x8(o8);
           asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};"
                        ::"r"(core + rr * 16), "r"(o.x), "r"(o.y), "r"(o.z), "r"(o.w) : "memory");
@@ -451,7 +461,7 @@ extern "C" int fg_block_mean_wgrad_supported(int64_t H, int64_t P) {
 extern "C" int fg_block_mean_wgrad(const uint16_t* g, int64_t g_ld, const int32_t* indptr,
                                    const int32_t* local, const int64_t* n_dst_dev,
                                    int64_t max_dst, const float* edge_w,
-                                   const uint16_t* h_mask, int64_t H,
+                                   const void* relu_mask, int mask_kind, int64_t H,
                                    const uint16_t* x, int64_t P, float* dw, float* scratch,
                                    int64_t scratch_bytes, void* s) {
   FG_CHECK_ARG(g != nullptr && indptr != nullptr && local != nullptr && n_dst_dev != nullptr &&
@@ -470,7 +480,12 @@ extern "C" int fg_block_mean_wgrad(const uint16_t* g, int64_t g_ld, const int32_
   uint32_t cols = 32;
   while (cols < (uint32_t)((H / 128) * P)) cols <<= 1;
   k_block_mean_wgrad<<<nb, kWgThreads, smem, st>>>(g, g_ld, indptr, n_dst_dev, max_dst, local,
-                                                   edge_w, h_mask, (int)H, x, (int)P, scratch,
+                                                   edge_w,
+                                                   mask_kind == 1 ? (const uint16_t*)relu_mask
+                                                                  : nullptr,
+                                                   mask_kind == 2 ? (const uint8_t*)relu_mask
+                                                                  : nullptr,
+                                                   (int)H, x, (int)P, scratch,
                                                    cols);
   FG_LAUNCH_CHECK();
   const int64_t n4 = H * P / 4;  // P % 16 == 0
@@ -480,6 +495,34 @@ extern "C" int fg_block_mean_wgrad(const uint16_t* g, int64_t g_ld, const int32_
   FG_LAUNCH_CHECK();
   k_wgrad_reduce_fin<<<(unsigned)((n4 + 255) / 256), 256, 0, st>>>(
       seg, n4, reinterpret_cast<float4*>(dw));
+  FG_LAUNCH_CHECK();
+  return FG_OK;
+}
+
+// ReLU mask bits of bf16 rows: out[r * H/8 + c] bit t = (h[r, 8c + t] > 0).
+// One thread per 8-feature chunk (a 16-byte load, a byte store); run right
+// after the GEMM that wrote h, while h is still in L2.
+namespace fg {
+__global__ void k_relu_bits(const uint16_t* __restrict__ h, int64_t rows, int64_t H,
+                            uint8_t* __restrict__ out) {
+  const int64_t chunks = rows * (H >> 3);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < chunks;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float f[8];
+    bf16x8_f32(__ldg(reinterpret_cast<const uint4*>(h) + i), f);
+    uint32_t b = 0;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) b |= (f[t] > 0.f ? 1u : 0u) << t;
+    out[i] = (uint8_t)b;
+  }
+}
+}  // namespace fg
+
+extern "C" int fg_relu_mask_bits(const uint16_t* h, int64_t rows, int64_t H, uint8_t* out,
+                                 void* s) {
+  FG_CHECK_ARG(H % 8 == 0, "fg_relu_mask_bits: H must be a multiple of 8");
+  if (rows == 0) return FG_OK;
+  fg::k_relu_bits<<<grid_for(rows * (H / 8), 256), 256, 0, as_stream(s)>>>(h, rows, H, out);
   FG_LAUNCH_CHECK();
   return FG_OK;
 }

@@ -270,9 +270,15 @@ class SageTrainer:
                             caps[L - 1], out=self.agg, edge_w=ew[L - 1])
         W, dW = self.w_bf16, self.w_grad
         ins, hs = [self.agg], []
+        fused = self.wgrad_scratch is not None
+        hbits = None
         for i in range(L):
             h = torch.mm(ins[i], W[i].t())
             hs.append(h)
+            if i == 0 and fused:  # packed ReLU mask while h0 is still in L2
+                hbits = torch.empty((h.shape[0], h.shape[1] // 8), dtype=torch.uint8,
+                                    device=self.device)
+                N.call("fg_relu_mask_bits", N.ptr(h), h.shape[0], h.shape[1], N.ptr(hbits), s)
             if i < L - 1:
                 l = L - 2 - i  # block feeding layer i+1
                 H = h.shape[1]
@@ -287,7 +293,6 @@ class SageTrainer:
         N.call("fg_softmax_ce", N.ptr(logits), 1, self.model.num_classes, ld, logits.shape[0],
                N.ptr(sb.n_nodes[0]), N.ptr(self.labels), N.ptr(sb.nodes[0]), N.ptr(dh),
                N.ptr(row_loss), N.ptr(self.loss_buf), N.ptr(self.ce_ctr), s)
-        fused = self.wgrad_scratch is not None
         for i in range(L - 1, -1, -1):
             torch.mm(dh.t(), ins[i], out_dtype=torch.float32, out=dW[i])
             if i == 0:
@@ -298,7 +303,7 @@ class SageTrainer:
             if fused and i == 1:
                 N.call("fg_block_mean_wgrad", N.ptr(din), H, N.ptr(sb.indptr[l]),
                        N.ptr(sb.local[l]), N.ptr(sb.n_nodes[l]), caps[l], N.ptr(ew[l]),
-                       N.ptr(hs[0]), H,
+                       N.ptr(hbits), 2, H,
                        N.ptr(self.agg), self.agg.shape[1], N.ptr(dW[0]),
                        N.ptr(self.wgrad_scratch), self.wgrad_scratch.numel() * 4, s)
                 break

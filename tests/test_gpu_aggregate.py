@@ -288,6 +288,16 @@ def test_block_mean_wgrad_tcgen05(H, P, relu, fan, n_src):
     err = (dw - ref).abs().max().item()
     assert err <= 1e-3 * ref.abs().max().item() + 1e-4, err
     assert torch.isfinite(dw).all()
+    if relu:  # packed ReLU bits give the identical result
+        from paper_2207_14696_b200.aggregate import relu_mask_bits
+        bits = relu_mask_bits(h)
+        assert bits.shape == (cap_src, H // 8)
+        hb = (h[:5].float() > 0).cpu().numpy()
+        want = np.packbits(hb.reshape(5, H // 8, 8), axis=2, bitorder="little")[..., 0]
+        assert np.array_equal(bits[:5].cpu().numpy(), want)
+        dw2 = block_mean_wgrad(g, ip, local, torch.tensor([n_dst], device=dev), max_dst, bits,
+                               x, H=H)
+        assert torch.equal(dw, dw2)
 
 
 def test_block_mean_wgrad_empty_block():
