@@ -271,14 +271,10 @@ class SageTrainer:
         W, dW = self.w_bf16, self.w_grad
         ins, hs = [self.agg], []
         fused = self.wgrad_scratch is not None
-        hbits = None
         for i in range(L):
             h = torch.mm(ins[i], W[i].t())
             hs.append(h)
-            if i == 0 and fused:  # packed ReLU mask while h0 is still in L2
-                hbits = torch.empty((h.shape[0], h.shape[1] // 8), dtype=torch.uint8,
-                                    device=self.device)
-                N.call("fg_relu_mask_bits", N.ptr(h), h.shape[0], h.shape[1], N.ptr(hbits), s)
+
             if i < L - 1:
                 l = L - 2 - i  # block feeding layer i+1
                 H = h.shape[1]
@@ -303,7 +299,7 @@ class SageTrainer:
             if fused and i == 1:
                 N.call("fg_block_mean_wgrad", N.ptr(din), H, N.ptr(sb.indptr[l]),
                        N.ptr(sb.local[l]), N.ptr(sb.n_nodes[l]), caps[l], N.ptr(ew[l]),
-                       N.ptr(hbits), 2, H,
+                       N.ptr(hs[0]), 1, H,
                        N.ptr(self.agg), self.agg.shape[1], N.ptr(dW[0]),
                        N.ptr(self.wgrad_scratch), self.wgrad_scratch.numel() * 4, s)
                 break
