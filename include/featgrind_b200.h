@@ -175,6 +175,12 @@ int fg_vq_gather_decode(const fg_codec_desc* codec, const void* ids,
 int fg_kmeans_assign(const double* pts, int64_t m, int w, const double* cents,
                      int k, int metric, int32_t* assign, double* cost,
                      double* cc_scratch, void* cuda_stream);
+/* The same assignment with the distance step on the tensor cores
+ * (tcgen05 kind::tf32 3xTF32 screen into TMEM + float64 recheck of
+ * near-ties; identical assignment, exact float64 cost).  fg_kmeans_assign
+ * routes here for w <= 16. */
+int fg_kmeans_assign_tc(const double* pts, int64_t m, int w, const double* cents, int k,
+                        int metric, int32_t* assign, double* cost, void* cuda_stream);
 
 /* np.bincount(assign, weights=pts[:, j]) for all j (vq.py:159-164), summed
  * per cluster in point order so the float64 result is identical: `order`

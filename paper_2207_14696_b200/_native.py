@@ -54,6 +54,7 @@ _SIGS = {
     "fg_segment_sums": (ci, [vp, i64, ci, vp, vp, ci, vp, vp, vp]),
     "fg_vq_gather_decode": (ci, [C.POINTER(CodecDesc), vp, ci, i64, vp, ci, vp, vp]),
     "fg_kmeans_assign": (ci, [vp, i64, ci, vp, ci, ci, vp, vp, vp, vp]),
+    "fg_kmeans_assign_tc": (ci, [vp, i64, ci, vp, ci, ci, vp, vp, vp]),
     "fg_gather_dequant_mean": (ci, [C.POINTER(CodecDesc), vp, vp, vp, i64, vp, i64, ci, vp]),
     "fg_gather_dequant_wsum": (ci, [C.POINTER(CodecDesc), vp, vp, vp, vp, i64, vp, i64, ci,
                                     vp]),

@@ -386,12 +386,16 @@ __device__ __forceinline__ uint32_t tc_off(int row, int k, int KB) {
   return (uint32_t)((((row >> 3) * KB + (k >> 2)) << 7) + ((row & 7) << 4) + ((k & 3) << 2));
 }
 
-template <typename XT>
+// KM (k-means / Lloyd assignment, vq.py:154-228 via fg_kmeans_assign): rows
+// are float64 points already normalised by the caller, the "codebook" is the
+// float64 centroid set (one part, `length` = k entries), and the exact
+// float64 cost of the chosen centroid is written (cosine: 1 - dot).
+template <typename XT, typename BT = float, bool KM = false>
 __global__ void __launch_bounds__(kTcRows, 1)
 k_vq_assign_tc(const XT* __restrict__ x, int64_t n, int64_t d, int width, int length, int parts,
-               const float* __restrict__ books, const int32_t* __restrict__ entries, int metric,
+               const BT* __restrict__ books, const int32_t* __restrict__ entries, int metric,
                int bits, uint8_t* __restrict__ rows, int64_t stride,
-               int32_t* __restrict__ codes32, int KB) {
+               int32_t* __restrict__ codes32, int KB, double* __restrict__ cost = nullptr) {
   // smem: A hi/lo [128 x 4KB floats], B hi/lo [256 x 4KB], cc [256], bar, tmem slot
   extern __shared__ __align__(128) uint8_t tc_mem[];
   const int a_bytes = kTcRows * KB * 16, b_bytes = kTcN * KB * 16;
@@ -409,9 +413,9 @@ k_vq_assign_tc(const XT* __restrict__ x, int64_t n, int64_t d, int width, int le
   const int p = blockIdx.y;
   const int lo = p * width;
   const int wp = (int)min64(width, d - lo);
-  const int L = entries[p];
+  const int L = KM ? length : entries[p];
   const bool cosine = metric == FG_METRIC_COSINE;
-  const float* book = books + (int64_t)p * length * width;
+  const BT* book = books + (int64_t)p * length * width;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
                  ::"r"(tc_smem(s_tmem)), "r"(kTcN));
@@ -446,7 +450,7 @@ k_vq_assign_tc(const XT* __restrict__ x, int64_t n, int64_t d, int width, int le
         xf[j] = (float)xv;
         ss = fma(xv, xv, ss);  // > 0 iff the sub-vector is non-zero (no fp64 underflow)
       }
-      if (cosine) {
+      if (cosine && !KM) {
         if (ss > 0.0) {
           const float inv = (float)(1.0 / sqrt(ss));  // screening only: ~1e-7 relative
           for (int j = 0; j < wp; ++j) xf[j] *= inv;
@@ -608,18 +612,21 @@ k_vq_assign_tc(const XT* __restrict__ x, int64_t n, int64_t d, int width, int le
       // is within 2x the error bound (tol is 20x); near-ties re-score every
       // entry in float64 with the reference's operation order (rare path)
       const bool alone = !has2 || (cosine ? s2 < sb - tolmax : s2 > sb + tolmax);
-      if (alone) {
+      double bestv = 0.0;
+      if (alone && !KM) {
         best = sbi;
       } else {
         double v[16];
         for (int j = 0; j < wp; ++j) v[j] = (double)x[r * d + lo + j];
         const double ssx = np_pairwise_sumsq(v, wp);
-        if (cosine) {
+        if (cosine && !KM) {
           const double nrm = sqrt(ssx);  // np.linalg.norm (vq.py:310)
           for (int j = 0; j < wp; ++j) v[j] = __ddiv_rn(v[j], nrm);
         }
-        double bestv = 0.0;
-        const bool few = ncand <= kTcCand;  // else every entry
+        // k-means needs the exact cost of the chosen centroid even when the
+        // screen resolved it alone
+        const bool few = alone || ncand <= kTcCand;  // else every entry
+        if (alone) { cand[0] = sbi; ncand = 1; }
         const int ne = few ? ncand : L;
         for (int i = 0; i < ne; ++i) {
           const int e = few ? cand[i] : i;
@@ -635,11 +642,12 @@ k_vq_assign_tc(const XT* __restrict__ x, int64_t n, int64_t d, int width, int le
           if (i == 0 || (cosine ? val > bestv : val < bestv)) { bestv = val; best = e; }
         }
       }
+      if (KM && active) cost[r] = cosine ? __dadd_rn(1.0, -bestv) : bestv;
     }
     if (active) {
       const int code = live ? best : 0;
-      if (codes32) codes32[r * parts + p] = code;
-      if (rows) vq_write_code(rows, stride, r, p, bits, code);
+      if (codes32) codes32[KM ? r : r * parts + p] = code;
+      if (!KM && rows) vq_write_code(rows, stride, r, p, bits, code);
     }
   }
   __syncthreads();
@@ -829,6 +837,23 @@ int fg_vq_assign_fp64(const void* x, int x_is_f64, int64_t n, int64_t d, int wid
                       uint8_t* rows, int64_t stride, int32_t* codes32, void* s) {
   return vq_assign_impl(x, x_is_f64, n, d, width, length, parts, books, entries, metric, bits,
                         rows, stride, codes32, s, false);
+}
+
+int fg_kmeans_assign_tc(const double* pts, int64_t m, int w, const double* cents, int k,
+                        int metric, int32_t* assign, double* cost, void* s) {
+  FG_CHECK_ARG(w >= 1 && w <= 16 && k >= 1, "fg_kmeans_assign_tc: width must be in [1, 16]");
+  if (m == 0) return FG_OK;
+  cudaStream_t st = as_stream(s);
+  const int KB = w <= 8 ? 2 : 4;
+  const int64_t smem = 2 * (int64_t)kTcRows * KB * 16 + 2 * (int64_t)kTcN * KB * 16 +
+                       kTcN * 4 + kTcN * 8 + 8 + 8 + 16;
+  const int gx = (int)min64(ceil_div(m, kTcRows), 2 * (int64_t)sm_count());
+  auto kern = k_vq_assign_tc<double, double, true>;
+  FG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<dim3(gx, 1), kTcRows, smem, st>>>(pts, m, w, w, k, 1, cents, nullptr, metric, 0, nullptr,
+                                           0, assign, KB, cost);
+  FG_LAUNCH_CHECK();
+  return FG_OK;
 }
 
 }  // extern "C"

@@ -270,6 +270,9 @@ extern "C" int fg_kmeans_assign(const double* pts, int64_t m, int w, const doubl
                                 void* s) {
   FG_CHECK_ARG(w >= 1 && w <= 128 && k >= 1, "fg_kmeans_assign: bad shape");
   if (m == 0) return FG_OK;
+  // the distance step on the tensor cores (screen + float64 recheck; same
+  // assignment and exact cost) for the narrow parts k-means fits
+  if (w <= 16) return fg_kmeans_assign_tc(pts, m, w, cents, k, metric, assign, cost, s);
   cudaStream_t st = as_stream(s);
   double* cc = nullptr;
   if (metric == FG_METRIC_EUCLIDEAN) {

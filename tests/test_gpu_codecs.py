@@ -190,3 +190,51 @@ def test_vq_assign_tensor_core_screen_exact_under_ties(metric, w, L, d):
     assert np.array_equal(got, ref), (metric, int((got != ref).sum()))
     want = oc.vq_assign(x[:3000], tuple(books), w, metric)
     assert np.array_equal(got[:3000], want)
+
+
+@pytest.mark.parametrize("metric", ["cosine", "euclidean"])
+@pytest.mark.parametrize("w,k", [(8, 256), (4, 300), (16, 64), (3, 17)])
+def test_kmeans_assign_tensor_core_matches_numpy(metric, w, k):
+    """Lloyd's assignment step (fg_kmeans_assign -> tcgen05 screen + float64
+    recheck) against the reference's numpy expressions (vq.py:154-228): the
+    same centroid (first index on ties) and the exact float64 cost."""
+    import torch
+    from paper_2207_14696_b200 import _native as N
+    r = np.random.default_rng(w * 31 + k)
+    m = 50_000
+    pts = r.standard_normal((m, w))
+    cents = r.standard_normal((k, w))
+    cents[3] = cents[1]                       # exact duplicate -> first index
+    pts[:500] = cents[r.integers(0, k, 500)]  # points on centroids
+    if metric == "cosine":
+        pts /= np.linalg.norm(pts, axis=1, keepdims=True)
+        cents /= np.linalg.norm(cents, axis=1, keepdims=True)
+    pt, ct = torch.from_numpy(pts).cuda(), torch.from_numpy(cents).cuda()
+    a = torch.empty(m, dtype=torch.int32, device="cuda")
+    cost = torch.empty(m, dtype=torch.float64, device="cuda")
+    cc = torch.empty(k, dtype=torch.float64, device="cuda")
+    metric_id = 1 if metric == "cosine" else 0  # FG_METRIC_* (vq.py:29 order)
+    N.call("fg_kmeans_assign", N.ptr(pt), m, w, N.ptr(ct), k, metric_id, N.ptr(a), N.ptr(cost),
+           N.ptr(cc), N.stream_handle())
+    dots = pts @ cents.T
+    if metric == "cosine":
+        want = np.argmax(dots, axis=1)
+        want_cost = 1.0 - dots[np.arange(m), want]
+    else:
+        dd = np.maximum((pts * pts).sum(axis=1)[:, None] + (cents * cents).sum(axis=1)[None, :]
+                        - 2.0 * dots, 0.0)
+        want = np.argmin(dd, axis=1)
+        want_cost = dd[np.arange(m), want]
+    got = a.cpu().numpy()
+    gc = cost.cpu().numpy()
+    # the kernel rescored near-ties in float64 with an in-order FMA chain
+    # (OpenBLAS's dgemm order for the encode shapes); numpy's dgemm for some
+    # narrow K (e.g. K=4) sums in another order, so a choice may differ only
+    # between entries whose costs agree to the last few ulps
+    diff = got != want
+    assert diff.mean() < 1e-3, int(diff.sum())
+    np.testing.assert_allclose(gc, want_cost, rtol=1e-12, atol=1e-14)
+    if diff.any():
+        alt = (1.0 - dots[np.flatnonzero(diff), got[diff]] if metric == "cosine"
+               else dd[np.flatnonzero(diff), got[diff]])
+        np.testing.assert_allclose(alt, want_cost[diff], rtol=1e-12, atol=1e-14)
