@@ -293,6 +293,30 @@ int fg_block_mean_wgrad(const uint16_t* grad_out, int64_t g_ld, const int32_t* i
 int fg_relu_mask_bits(const uint16_t* h, int64_t rows, int64_t h_dim, uint8_t* out_bits,
                       void* cuda_stream);
 
+/* Graph-attention (GAT) edge operators over a sampled block (config E;
+ * fg_gat.cu).  Per head k: q[v,k] = mean_{e in v} er[l_e,k] (destination
+ * query: the reference's blocks give no representation for a destination
+ * that did not sample itself), s = LeakyReLU(el[l_e,k] + q),
+ * alpha = softmax over v's edges, out[v, head k cols] = sum_e alpha z[l_e].
+ * local NULL = the source of edge e is row e (input layer over decoded
+ * picks).  el/er/q/alpha fp32 [rows, heads]; z bf16 [src rows, hf]
+ * (hf / heads a multiple of 8); out/dout/dz fp32.  Backward accumulates into
+ * del/der/dz/dalpha with atomics (callers zero them). */
+int fg_gat_softmax_fwd(const float* el, const float* er, const int32_t* indptr,
+                       const int32_t* local, int64_t max_dst, const int64_t* n_dst_dev,
+                       int heads, float slope, float* alpha, float* q, void* cuda_stream);
+int fg_gat_softmax_bwd(const float* el, const float* q, const float* alpha, const float* dalpha,
+                       const int32_t* indptr, const int32_t* local, int64_t max_dst,
+                       const int64_t* n_dst_dev, int heads, float slope, float* del,
+                       float* der, void* cuda_stream);
+int fg_gat_agg_fwd(const uint16_t* z, int64_t hf, int heads, const float* alpha,
+                   const int32_t* indptr, const int32_t* local, int64_t max_dst,
+                   const int64_t* n_dst_dev, float* out, void* cuda_stream);
+int fg_gat_agg_bwd(const uint16_t* z, int64_t hf, int heads, const float* alpha,
+                   const int32_t* indptr, const int32_t* local, int64_t max_dst,
+                   const int64_t* n_dst_dev, const float* dout, float* dz, float* dalpha,
+                   void* cuda_stream);
+
 /* Fused softmax cross-entropy over padded logits [rows, ld] (bf16 or fp32):
  * rows r < *n_valid_dev use label labels[row_node[r]] over the first
  * num_classes columns; loss_out = mean loss (deterministic row-order

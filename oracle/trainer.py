@@ -97,3 +97,97 @@ def evaluate(model, off, col, labels, ids, fanouts, bs, seed, decode_rows, max_b
         correct += int((pred == labels[b.seeds]).sum())
         total += b.seeds.size
     return correct / max(1, total)
+
+
+# ------------------------------------------------------------------- GAT
+class _OracleGatLayer(nn.Module):
+    """CPU fp32 restatement of paper_2207_14696_b200.gat.GatLayer (same
+    parameter names, so GPU weights load directly)."""
+
+    def __init__(self, in_dim, out_per_head, heads, out_pad=None):
+        super().__init__()
+        self.heads = heads
+        width = out_pad or out_per_head * heads
+        self.width = width
+        self.lin = nn.Linear(in_dim, width, bias=False)
+        self.attn_l = nn.Parameter(torch.zeros(heads, width // heads))
+        self.attn_r = nn.Parameter(torch.zeros(heads, width // heads))
+        self.bias = nn.Parameter(torch.zeros(width))
+
+    def forward(self, h, counts, local, slope=0.2):
+        z = self.lin(h)
+        zh = z.view(-1, self.heads, self.width // self.heads)
+        el = (zh * self.attn_l).sum(-1)
+        er = (zh * self.attn_r).sum(-1)
+        nd = counts.numel()
+        seg = torch.repeat_interleave(torch.arange(nd), counts)
+        cnt = counts.clamp_min(1).float()[:, None]
+        q = torch.zeros(nd, self.heads).index_add_(0, seg, er[local]) / cnt
+        s = F.leaky_relu(el[local] + q[seg], slope)
+        mx = torch.full((nd, self.heads), -float("inf")).index_reduce_(0, seg, s, "amax")
+        p = torch.exp(s - mx[seg])
+        den = torch.zeros(nd, self.heads).index_add_(0, seg, p)
+        alpha = p / den[seg]
+        msg = (alpha[:, :, None] * zh[local]).reshape(-1, self.width)
+        return torch.zeros(nd, self.width).index_add_(0, seg, msg) + self.bias
+
+
+class OracleGat(nn.Module):
+    def __init__(self, in_dim, hidden, num_classes, num_layers, heads=4):
+        super().__init__()
+        self.num_classes = num_classes
+        c_pad = (num_classes + 7) // 8 * 8
+        self.layers = nn.ModuleList(
+            _OracleGatLayer(in_dim if i == 0 else hidden, num_classes, 1, c_pad)
+            if i == num_layers - 1 else
+            _OracleGatLayer(in_dim if i == 0 else hidden, hidden // heads, heads)
+            for i in range(num_layers))
+
+    def forward(self, x_picks, blocks):
+        """x_picks: decoded rows of the last block's picks; blocks[l] =
+        (counts, local) with the last block's local = arange(picks)."""
+        L = len(self.layers)
+        h = x_picks
+        for i, layer in enumerate(self.layers):
+            counts, local = blocks[L - 1 - i]
+            h = layer(h, counts, local)
+            if i < L - 1:
+                h = F.elu(h)
+        return h[:, :self.num_classes]
+
+
+def gat_batch_tensors(batch, decode_rows):
+    L = len(batch.layers)
+    last = batch.layers[-1]
+    x = torch.from_numpy(np.asarray(decode_rows(last.picks), np.float32))
+    blocks = []
+    for l in range(L):
+        lay = batch.layers[l]
+        if l == L - 1:
+            local = np.arange(lay.picks.size)
+        else:
+            local = np.searchsorted(batch.layers[l + 1].nodes, lay.picks)
+        blocks.append((torch.from_numpy(lay.counts), torch.from_numpy(local)))
+    return x, blocks
+
+
+def gat_train_epoch(model, opt, off, col, labels, train_ids, fanouts, bs, seed, decode_rows):
+    batches, _ = sample_batches_oracle(off, col, train_ids, fanouts, bs, seed)
+    for b in batches:
+        x, blocks = gat_batch_tensors(b, decode_rows)
+        loss = F.cross_entropy(model(x, blocks), torch.from_numpy(labels[b.seeds]).long())
+        opt.zero_grad()
+        loss.backward()
+        opt.step()
+
+
+@torch.no_grad()
+def gat_evaluate(model, off, col, labels, ids, fanouts, bs, seed, decode_rows):
+    batches, _ = sample_batches_oracle(off, col, ids, fanouts, bs, seed)
+    correct = total = 0
+    for b in batches:
+        x, blocks = gat_batch_tensors(b, decode_rows)
+        pred = model(x, blocks).argmax(1).numpy()
+        correct += int((pred == labels[b.seeds]).sum())
+        total += b.seeds.size
+    return correct / max(1, total)

@@ -1,0 +1,231 @@
+// Graph-attention (GAT) edge kernels over sampled blocks — BASELINE config E's
+// second aggregator variant (PAPER.md:259-261, 1048-1055 list GAT among the
+// trained models; the reference itself has no model code).
+//
+// A block has destinations v (indptr over edges) and per-edge source rows
+// local[e] (for the input layer the source of edge e is decoded row e).  Per
+// head k, with projected source rows z and per-source scores
+// el[u,k] = <z[u,k,:], a_l[k]>, er[u,k] = <z[u,k,:], a_r[k]>:
+//   q[v,k]   = mean_{e in v} er[l_e, k]            (destination query, see below)
+//   s[e,k]   = LeakyReLU(el[l_e, k] + q[v, k])
+//   a[e,k]   = softmax over v's edges of s[., k]
+//   out[v,k] = sum_e a[e,k] z[l_e, k, :]
+// Standard GAT scores a destination with its own projected features; under the
+// reference's block semantics (pipeline.py:203-221: a layer expands only the
+// unique picks of the previous one) a destination that did not sample itself
+// has no representation at the layer below, so its query is
+// the mean of its sampled neighbours' er — computable for every destination.
+//
+// Forward: one thread per (destination, head).  Backward scatters into source
+// rows with fp32 atomics (dz, d el, d er): the attention backward is not
+// bitwise deterministic.
+#include "fg_common.cuh"
+
+namespace fg {
+
+__device__ __forceinline__ float leaky(float x, float s) { return x > 0.f ? x : s * x; }
+
+// alpha[e, k], q[v, k]
+__global__ void k_gat_softmax_fwd(const float* __restrict__ el, const float* __restrict__ er,
+                                  const int32_t* __restrict__ indptr,
+                                  const int32_t* __restrict__ local, int64_t ndst_live_cap,
+                                  const int64_t* __restrict__ ndst_dev, int heads, float slope,
+                                  float* __restrict__ alpha, float* __restrict__ q) {
+  const int64_t live = min64(*ndst_dev, ndst_live_cap);
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < live * heads;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = t / heads;
+    const int k = (int)(t - v * heads);
+    const int32_t e0 = indptr[v], e1 = indptr[v + 1];
+    if (e1 == e0) {
+      q[t] = 0.f;
+      continue;
+    }
+    float qs = 0.f;
+    for (int32_t e = e0; e < e1; ++e) {
+      const int64_t u = local ? local[e] : e;
+      qs += er[u * heads + k];
+    }
+    const float qv = qs / (float)(e1 - e0);
+    q[t] = qv;
+    float mx = -INFINITY;
+    for (int32_t e = e0; e < e1; ++e) {
+      const int64_t u = local ? local[e] : e;
+      mx = fmaxf(mx, leaky(el[u * heads + k] + qv, slope));
+    }
+    float den = 0.f;
+    for (int32_t e = e0; e < e1; ++e) {
+      const int64_t u = local ? local[e] : e;
+      const float p = __expf(leaky(el[u * heads + k] + qv, slope) - mx);
+      alpha[(int64_t)e * heads + k] = p;
+      den += p;
+    }
+    const float inv = 1.f / den;
+    for (int32_t e = e0; e < e1; ++e) alpha[(int64_t)e * heads + k] *= inv;
+  }
+}
+
+// d el[u,k] += dpre_e ; d er[u,k] += (sum_e' dpre_e') / cnt_v
+__global__ void k_gat_softmax_bwd(const float* __restrict__ el, const float* __restrict__ q,
+                                  const float* __restrict__ alpha, const float* __restrict__ dalpha,
+                                  const int32_t* __restrict__ indptr,
+                                  const int32_t* __restrict__ local, int64_t ndst_cap,
+                                  const int64_t* __restrict__ ndst_dev, int heads, float slope,
+                                  float* __restrict__ del, float* __restrict__ der) {
+  const int64_t live = min64(*ndst_dev, ndst_cap);
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < live * heads;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = t / heads;
+    const int k = (int)(t - v * heads);
+    const int32_t e0 = indptr[v], e1 = indptr[v + 1];
+    if (e1 == e0) continue;
+    float dot = 0.f;
+    for (int32_t e = e0; e < e1; ++e)
+      dot += alpha[(int64_t)e * heads + k] * dalpha[(int64_t)e * heads + k];
+    const float qv = q[t];
+    float dq = 0.f;
+    for (int32_t e = e0; e < e1; ++e) {
+      const int64_t u = local ? local[e] : e;
+      const float a = alpha[(int64_t)e * heads + k];
+      const float ds = a * (dalpha[(int64_t)e * heads + k] - dot);
+      const float pre = el[u * heads + k] + qv;
+      const float dpre = pre > 0.f ? ds : slope * ds;
+      atomicAdd(del + u * heads + k, dpre);
+      dq += dpre;
+    }
+    const float share = dq / (float)(e1 - e0);
+    for (int32_t e = e0; e < e1; ++e) {
+      const int64_t u = local ? local[e] : e;
+      atomicAdd(der + u * heads + k, share);
+    }
+  }
+}
+
+__device__ __forceinline__ void ld8(const __nv_bfloat16* p, float* f) {
+  const uint4 q = *reinterpret_cast<const uint4*>(p);
+  const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    f[2 * i] = __uint_as_float(w[i] << 16);
+    f[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+  }
+}
+
+// out[v, c*8 .. c*8+7] = sum_e alpha[e, head(c)] z[l_e, c*8 ..]; thread per
+// (destination, 8-feature chunk); rows past the live count are zeroed.
+__global__ void k_gat_agg_fwd(const __nv_bfloat16* __restrict__ z, int64_t hf, int heads,
+                              const float* __restrict__ alpha, const int32_t* __restrict__ indptr,
+                              const int32_t* __restrict__ local, int64_t max_dst,
+                              const int64_t* __restrict__ ndst_dev, float* __restrict__ out) {
+  const int64_t live = min64(*ndst_dev, max_dst);
+  const int64_t chunks = hf >> 3;
+  const int64_t F = hf / heads;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < max_dst * chunks;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = t / chunks, c = t - v * chunks;
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (v < live) {
+      const int k = (int)(c * 8 / F);
+      for (int32_t e = indptr[v]; e < indptr[v + 1]; ++e) {
+        const int64_t u = local ? local[e] : e;
+        const float a = alpha[(int64_t)e * heads + k];
+        float f[8];
+        ld8(z + u * hf + c * 8, f);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] = fmaf(a, f[j], acc[j]);
+      }
+    }
+    float4* o = reinterpret_cast<float4*>(out + v * hf + c * 8);
+    o[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    o[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+  }
+}
+
+// dz[l_e] += alpha_e * dout_v ; dalpha[e, k] += <dout_v, z[l_e]> over head k
+__global__ void k_gat_agg_bwd(const __nv_bfloat16* __restrict__ z, int64_t hf, int heads,
+                              const float* __restrict__ alpha, const int32_t* __restrict__ indptr,
+                              const int32_t* __restrict__ local, int64_t max_dst,
+                              const int64_t* __restrict__ ndst_dev, const float* __restrict__ dout,
+                              float* __restrict__ dz, float* __restrict__ dalpha) {
+  const int64_t live = min64(*ndst_dev, max_dst);
+  const int64_t chunks = hf >> 3;
+  const int64_t F = hf / heads;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < live * chunks;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = t / chunks, c = t - v * chunks;
+    const int k = (int)(c * 8 / F);
+    const float4 d0 = reinterpret_cast<const float4*>(dout + v * hf + c * 8)[0];
+    const float4 d1 = reinterpret_cast<const float4*>(dout + v * hf + c * 8)[1];
+    const float g[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
+    for (int32_t e = indptr[v]; e < indptr[v + 1]; ++e) {
+      const int64_t u = local ? local[e] : e;
+      const float a = alpha[(int64_t)e * heads + k];
+      float f[8];
+      ld8(z + u * hf + c * 8, f);
+      float dp = 0.f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) dp = fmaf(g[j], f[j], dp);
+      atomicAdd(dalpha + (int64_t)e * heads + k, dp);
+      float4* dst = reinterpret_cast<float4*>(dz + u * hf + c * 8);
+      atomicAdd(dst, make_float4(a * g[0], a * g[1], a * g[2], a * g[3]));
+      atomicAdd(dst + 1, make_float4(a * g[4], a * g[5], a * g[6], a * g[7]));
+    }
+  }
+}
+
+}  // namespace fg
+
+using namespace fg;
+
+extern "C" int fg_gat_softmax_fwd(const float* el, const float* er, const int32_t* indptr,
+                                  const int32_t* local, int64_t max_dst, const int64_t* n_dst_dev,
+                                  int heads, float slope, float* alpha, float* q, void* s) {
+  FG_CHECK_ARG(el && er && indptr && n_dst_dev && alpha && q && heads >= 1, "null argument");
+  if (max_dst == 0) return FG_OK;
+  k_gat_softmax_fwd<<<grid_for(max_dst * heads, 256), 256, 0, as_stream(s)>>>(
+      el, er, indptr, local, max_dst, n_dst_dev, heads, slope, alpha, q);
+  FG_LAUNCH_CHECK();
+  return FG_OK;
+}
+
+extern "C" int fg_gat_softmax_bwd(const float* el, const float* q, const float* alpha,
+                                  const float* dalpha, const int32_t* indptr,
+                                  const int32_t* local, int64_t max_dst,
+                                  const int64_t* n_dst_dev, int heads, float slope, float* del,
+                                  float* der, void* s) {
+  FG_CHECK_ARG(el && q && alpha && dalpha && indptr && n_dst_dev && del && der, "null argument");
+  if (max_dst == 0) return FG_OK;
+  k_gat_softmax_bwd<<<grid_for(max_dst * heads, 256), 256, 0, as_stream(s)>>>(
+      el, q, alpha, dalpha, indptr, local, max_dst, n_dst_dev, heads, slope, del, der);
+  FG_LAUNCH_CHECK();
+  return FG_OK;
+}
+
+extern "C" int fg_gat_agg_fwd(const uint16_t* z, int64_t hf, int heads, const float* alpha,
+                              const int32_t* indptr, const int32_t* local, int64_t max_dst,
+                              const int64_t* n_dst_dev, float* out, void* s) {
+  FG_CHECK_ARG(z && alpha && indptr && n_dst_dev && out, "null argument");
+  FG_CHECK_ARG(hf % 8 == 0 && heads >= 1 && (hf / heads) % 8 == 0,
+               "fg_gat_agg_fwd: per-head width must be a multiple of 8");
+  if (max_dst == 0) return FG_OK;
+  k_gat_agg_fwd<<<grid_for(max_dst * (hf / 8), 256), 256, 0, as_stream(s)>>>(
+      reinterpret_cast<const __nv_bfloat16*>(z), hf, heads, alpha, indptr, local, max_dst,
+      n_dst_dev, out);
+  FG_LAUNCH_CHECK();
+  return FG_OK;
+}
+
+extern "C" int fg_gat_agg_bwd(const uint16_t* z, int64_t hf, int heads, const float* alpha,
+                              const int32_t* indptr, const int32_t* local, int64_t max_dst,
+                              const int64_t* n_dst_dev, const float* dout, float* dz,
+                              float* dalpha, void* s) {
+  FG_CHECK_ARG(z && alpha && indptr && n_dst_dev && dout && dz && dalpha, "null argument");
+  FG_CHECK_ARG(hf % 8 == 0 && heads >= 1 && (hf / heads) % 8 == 0,
+               "fg_gat_agg_bwd: per-head width must be a multiple of 8");
+  if (max_dst == 0) return FG_OK;
+  k_gat_agg_bwd<<<grid_for(max_dst * (hf / 8), 256), 256, 0, as_stream(s)>>>(
+      reinterpret_cast<const __nv_bfloat16*>(z), hf, heads, alpha, indptr, local, max_dst,
+      n_dst_dev, dout, dz, dalpha);
+  FG_LAUNCH_CHECK();
+  return FG_OK;
+}
