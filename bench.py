@@ -43,6 +43,7 @@ CONFIGS = {
     # BASELINE config E: aggregator variants through the fused gather path
     "products-gcn": ("products", ("sq", 8), (15, 10, 5), 1024, 256, "gcn"),
     "products-sq8": ("products", ("sq", 8), (15, 10, 5), 1024, 256),
+    "products-gat": ("products", ("sq", 8), (15, 10, 5), 1024, 256, "gat"),
 }
 
 
@@ -196,9 +197,15 @@ def run_ours(args, rank, world, local):
     sg, dc, codec_desc, fanouts, bs, hidden = build_workload(args.config, dev, scale=args.scale)
     pg = dist.group.WORLD if world > 1 else None
     agg_kind = aggregator_of(args.config)
-    cfg = TrainConfig(fanouts=fanouts, batch_size=bs, hidden=hidden, lr=3e-3, seed=0,
-                      aggregator=agg_kind)
-    tr = SageTrainer(sg.graph, dc, sg.labels, sg.num_classes, cfg, process_group=pg)
+    if agg_kind == "gat":
+        from paper_2207_14696_b200.gat import GatConfig, GatTrainer
+        tr = GatTrainer(sg.graph, dc, sg.labels, sg.num_classes,
+                        GatConfig(fanouts=fanouts, batch_size=bs, hidden=hidden, lr=3e-3),
+                        process_group=pg)
+    else:
+        cfg = TrainConfig(fanouts=fanouts, batch_size=bs, hidden=hidden, lr=3e-3, seed=0,
+                          aggregator=agg_kind)
+        tr = SageTrainer(sg.graph, dc, sg.labels, sg.num_classes, cfg, process_group=pg)
     nb = tr.begin_epoch(sg.train_ids, 0)
     need = args.warmup + 2 * args.steps + 3
     if nb < need:
@@ -274,11 +281,18 @@ def run_ours(args, rank, world, local):
         # (the 512 MB flush still running on the device covers the host-side
         # enqueue, so the event pair brackets the kernel alone)
         s.record()
-        gather_dequant_mean(dc, sb.indptr[L - 1], sb.picks[L - 1], sb.n_nodes[L - 1],
-                            tr.caps[L - 1], out=tr.agg, edge_w=sb.ew[L - 1] if sb.ew else None)
+        if agg_kind == "gat":  # GAT decodes one row per pick (attention needs each source)
+            dc.gather(sb.picks[L - 1], out_dtype=torch.bfloat16, check=False)
+        else:
+            gather_dequant_mean(dc, sb.indptr[L - 1], sb.picks[L - 1], sb.n_nodes[L - 1],
+                                tr.caps[L - 1], out=tr.agg,
+                                edge_w=sb.ew[L - 1] if sb.ew else None)
         e.record()
         e.synchronize()
         kt.append(s.elapsed_time(e))
+        if agg_kind == "gat":  # E code rows + int32 ids in, E bf16 rows out
+            kbytes.append(E * (row_bytes + 4) + E * dc.d * 2)
+            continue
         out_b = tr.agg.element_size()
         # algorithmic bytes: E code rows + int32 source ids, N_dst indptr
         # entries + output rows (the padded rows past N_dst are zero-filled
@@ -308,7 +322,8 @@ def run_ours(args, rank, world, local):
         "dtype": "bf16",
         "data": "synthetic (planted-partition power-law graph, class-conditional features)",
         "config": {"workload": f"{args.config}-shape "
-                               f"{'GCN' if agg_kind == 'gcn' else 'GraphSAGE'} {len(fanouts)}-layer "
+                               f"{dict(gcn='GCN', gat='GAT').get(agg_kind, 'GraphSAGE')} "
+                               f"{len(fanouts)}-layer "
                                f"fanout {list(fanouts)}, {codec_desc}",
                    "nodes": sg.graph.n, "edges_stored": sg.graph.nnz, "feature_dim": dc.d,
                    "global_batch": seeds_per_step, "per_rank_batch": bs, "hidden": hidden,
@@ -317,7 +332,8 @@ def run_ours(args, rank, world, local):
         "e2e": {"value": round(e2e, 1), "unit": "seeds/s",
                 "h2d_bytes_per_step": bs * 8, "d2h_bytes_per_step": 4},
         "gpu_launches": int(launches_per_step * args.steps),
-        "roofline": {"kernel": "fg_gather_dequant_mean (k_vq_mean8_fast / k_sq_mean)",
+        "roofline": {"kernel": ("fg_sq_gather_dequant / fg_vq_gather_decode" if agg_kind == "gat"
+                               else "fg_gather_dequant_mean (k_vq_mean8_fast / k_sq_mean)"),
                      "bound": "hbm",
                      "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "peak_kind": peak_kind,
@@ -366,20 +382,33 @@ def _host_world(sg, dc):
     return host, labels, decode
 
 
+def oracle_model(ot, d, hidden, num_classes, fanouts, aggregator):
+    """CPU fp32 oracle model + one-batch train function for the aggregator."""
+    if aggregator == "gat":
+        def step(model, opt, host, labels, ids, fanouts, batch, seed, decode):
+            ot.gat_train_epoch(model, opt, host.row_offsets, host.col_indices, labels, ids,
+                               fanouts, batch, seed, decode)
+        return ot.OracleGat(d, hidden, num_classes, len(fanouts)), step
+
+    def step(model, opt, host, labels, ids, fanouts, batch, seed, decode):
+        ot.train_epoch(model, opt, host.row_offsets, host.col_indices, labels, ids, fanouts,
+                       batch, seed, decode, aggregator=aggregator)
+    return ot.OracleSage(d, hidden, num_classes, len(fanouts)), step
+
+
 def cpu_baseline(sg, dc, fanouts, hidden, budget_s=20.0, batch=128, aggregator="mean"):
     """Oracle port of the reference path on the host cores: numpy sampler
     (pipeline.py:185-222 restated) + numpy decoder + CPU fp32 SAGE step."""
     import torch
     from oracle import trainer as ot
     host, labels, decode = _host_world(sg, dc)
-    model = ot.OracleSage(dc.d, hidden, sg.num_classes, len(fanouts))
+    model, train_step = oracle_model(ot, dc.d, hidden, sg.num_classes, fanouts, aggregator)
     opt = torch.optim.Adam(model.parameters(), lr=3e-3)
     seeds_done, t0, steps = 0, time.perf_counter(), 0
     train = sg.train_ids
     while True:
-        ot.train_epoch(model, opt, host.row_offsets, host.col_indices, labels,
-                       train[steps * batch:(steps + 1) * batch], fanouts, batch, steps, decode,
-                       aggregator=aggregator)
+        train_step(model, opt, host, labels, train[steps * batch:(steps + 1) * batch], fanouts,
+                   batch, steps, decode)
         steps += 1
         seeds_done += batch
         if time.perf_counter() - t0 >= budget_s or steps * batch >= train.size:
@@ -404,15 +433,15 @@ def run_reference(args, rank, world, local):
     sg, dc, codec_desc, fanouts, bs, hidden = build_workload(args.config, dev, scale=args.scale)
     host, labels, decode = _host_world(sg, dc)
     torch.set_num_threads(os.cpu_count() or 1)
-    model = ot.OracleSage(dc.d, hidden, sg.num_classes, len(fanouts))
+    model, train_step = oracle_model(ot, dc.d, hidden, sg.num_classes, fanouts,
+                                     aggregator_of(args.config))
     opt = torch.optim.Adam(model.parameters(), lr=3e-3)
     batch = args.ref_batch
     train = sg.train_ids
 
     def one(i):
-        ot.train_epoch(model, opt, host.row_offsets, host.col_indices, labels,
-                       train[i * batch:(i + 1) * batch], fanouts, batch, i, decode,
-                       aggregator=aggregator_of(args.config))
+        train_step(model, opt, host, labels, train[i * batch:(i + 1) * batch], fanouts, batch,
+                   i, decode)
 
     for i in range(args.warmup):
         one(i)
