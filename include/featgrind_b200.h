@@ -312,6 +312,16 @@ int fg_gat_softmax_bwd(const float* el, const float* q, const float* alpha, cons
 int fg_gat_agg_fwd(const uint16_t* z, int64_t hf, int heads, const float* alpha,
                    const int32_t* indptr, const int32_t* local, int64_t max_dst,
                    const int64_t* n_dst_dev, float* out, void* cuda_stream);
+/* Input-layer form (source of edge e = decoded row e of x [E, d] bf16):
+ * out[v, k*d + j] = sum_e alpha[e,k] x[e,j] (fp32 [max_dst, heads*d]), so the
+ * projection applies to N_dst x heads aggregates instead of every pick;
+ * backward dalpha[e,k] = <dout[v, k*d:(k+1)*d], x[e]> for the live edges. */
+int fg_gat_xagg_fwd(const uint16_t* x, int64_t d, int heads, const float* alpha,
+                    const int32_t* indptr, int64_t max_dst, const int64_t* n_dst_dev,
+                    float* out, void* cuda_stream);
+int fg_gat_xagg_bwd(const uint16_t* x, int64_t d, int heads, const int32_t* indptr,
+                    int64_t max_dst, const int64_t* n_dst_dev, const float* dout, float* dalpha,
+                    int64_t e_cap, void* cuda_stream);
 int fg_gat_agg_bwd(const uint16_t* z, int64_t hf, int heads, const float* alpha,
                    const int32_t* indptr, const int32_t* local, int64_t max_dst,
                    const int64_t* n_dst_dev, const float* dout, float* dz, float* dalpha,

@@ -229,3 +229,105 @@ extern "C" int fg_gat_agg_bwd(const uint16_t* z, int64_t hf, int heads, const fl
   FG_LAUNCH_CHECK();
   return FG_OK;
 }
+
+// Input layer by linearity: sum_e alpha[e,k] (x_e W_k) = (sum_e alpha[e,k] x_e) W_k,
+// so the attention-weighted aggregate is taken over the decoded input rows
+// (one per pick, d columns) per head, and only N_dst x heads rows are
+// projected -- no per-pick projection or per-pick gradient.
+// out[v, k*d + j] = sum_{e in v} alpha[e, k] x[e, j]: block per 8
+// destinations (warp per destination), lanes over the heads*d columns.
+// dalpha[e, k] = <dout[v, k*d : (k+1)*d], x[e]>: warp per destination, one
+// warp-wide dot per (edge, head).
+namespace fg {
+constexpr int kMaxHeads = 8;
+__global__ void __launch_bounds__(256)
+k_gat_xagg_fwd(const __nv_bfloat16* __restrict__ x, int d, int heads,
+               const float* __restrict__ alpha, const int32_t* __restrict__ indptr,
+               int64_t max_dst, const int64_t* __restrict__ ndst_dev, float* __restrict__ out) {
+  // warp per destination; lane over input columns j; each x element is read
+  // once and multiplied by every head's alpha
+  const int64_t live = min64(*ndst_dev, max_dst);
+  const int lane = threadIdx.x & 31;
+  for (int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; v < max_dst;
+       v += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    float* o = out + v * (int64_t)heads * d;
+    const int32_t e0 = v < live ? indptr[v] : 0, e1 = v < live ? indptr[v + 1] : 0;
+    for (int j = lane; j < d; j += 32) {
+      float acc[kMaxHeads];
+#pragma unroll
+      for (int k = 0; k < kMaxHeads; ++k) acc[k] = 0.f;
+      for (int32_t e = e0; e < e1; ++e) {
+        const float xv = __bfloat162float(x[(int64_t)e * d + j]);
+#pragma unroll
+        for (int k = 0; k < kMaxHeads; ++k)
+          if (k < heads) acc[k] = fmaf(__ldg(alpha + (int64_t)e * heads + k), xv, acc[k]);
+      }
+#pragma unroll
+      for (int k = 0; k < kMaxHeads; ++k)
+        if (k < heads) o[k * d + j] = acc[k];
+    }
+  }
+}
+__global__ void __launch_bounds__(256)
+k_gat_xagg_bwd(const __nv_bfloat16* __restrict__ x, int d, int heads,
+               const int32_t* __restrict__ indptr, int64_t max_dst,
+               const int64_t* __restrict__ ndst_dev, const float* __restrict__ dout,
+               float* __restrict__ dalpha) {
+  // warp per destination; per edge the x row is read once and dotted with
+  // every head's slice of dout (one butterfly per head)
+  const int64_t live = min64(*ndst_dev, max_dst);
+  const int lane = threadIdx.x & 31;
+  for (int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; v < live;
+       v += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int32_t e0 = indptr[v], e1 = indptr[v + 1];
+    const float* g = dout + v * (int64_t)heads * d;
+    for (int32_t e = e0; e < e1; ++e) {
+      const __nv_bfloat16* xr = x + (int64_t)e * d;
+      float acc[kMaxHeads];
+#pragma unroll
+      for (int k = 0; k < kMaxHeads; ++k) acc[k] = 0.f;
+      for (int j = lane; j < d; j += 32) {
+        const float xv = __bfloat162float(xr[j]);
+#pragma unroll
+        for (int k = 0; k < kMaxHeads; ++k)
+          if (k < heads) acc[k] = fmaf(g[k * d + j], xv, acc[k]);
+      }
+#pragma unroll
+      for (int k = 0; k < kMaxHeads; ++k) {
+        if (k < heads) {
+          float a = acc[k];
+#pragma unroll
+          for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+          if (lane == 0) dalpha[(int64_t)e * heads + k] = a;
+        }
+      }
+    }
+  }
+}
+}  // namespace fg
+
+extern "C" int fg_gat_xagg_fwd(const uint16_t* x, int64_t d, int heads, const float* alpha,
+                               const int32_t* indptr, int64_t max_dst, const int64_t* n_dst_dev,
+                               float* out, void* s) {
+  FG_CHECK_ARG(x && alpha && indptr && n_dst_dev && out && heads >= 1 && heads <= 8 && d >= 1,
+               "fg_gat_xagg_fwd: bad argument (heads <= 8)");
+  if (max_dst == 0) return FG_OK;
+  fg::k_gat_xagg_fwd<<<grid_for(max_dst * 32, 256), 256, 0, as_stream(s)>>>(
+      reinterpret_cast<const __nv_bfloat16*>(x), (int)d, heads, alpha, indptr, max_dst, n_dst_dev,
+      out);
+  FG_LAUNCH_CHECK();
+  return FG_OK;
+}
+
+extern "C" int fg_gat_xagg_bwd(const uint16_t* x, int64_t d, int heads, const int32_t* indptr,
+                               int64_t max_dst, const int64_t* n_dst_dev, const float* dout,
+                               float* dalpha, int64_t e_cap, void* s) {
+  FG_CHECK_ARG(x && indptr && n_dst_dev && dout && dalpha && heads >= 1 && heads <= 8,
+               "fg_gat_xagg_bwd: bad argument (heads <= 8)");
+  if (max_dst == 0 || e_cap == 0) return FG_OK;
+  fg::k_gat_xagg_bwd<<<grid_for(max_dst * 32, 256), 256, 0, as_stream(s)>>>(
+      reinterpret_cast<const __nv_bfloat16*>(x), (int)d, heads, indptr, max_dst, n_dst_dev, dout,
+      dalpha);
+  FG_LAUNCH_CHECK();
+  return FG_OK;
+}

@@ -89,6 +89,89 @@ class GatAggregate(torch.autograd.Function):
         return dz, dalpha, None, None, None, None
 
 
+class PickScores(torch.autograd.Function):
+    """s = x c^T for the decoded picks x [E, d] (bf16) and c [2H, d]; the
+    backward dc = ds^T x has K = E (~5e5): split into 64 chunks reduced by
+    one batched GEMM instead of a single skinny cuBLAS call."""
+
+    @staticmethod
+    def forward(ctx, x, c):
+        ctx.save_for_backward(x)
+        return torch.mm(x, c.to(x.dtype).t()).float()
+
+    @staticmethod
+    def backward(ctx, ds):
+        (x,) = ctx.saved_tensors
+        E, d = x.shape
+        ch = 64
+        pad = (-E) % ch
+        xs = x if not pad else torch.cat([x, x.new_zeros(pad, d)])
+        gs = ds.to(x.dtype)
+        gs = gs if not pad else torch.cat([gs, gs.new_zeros(pad, gs.shape[1])])
+        part = torch.bmm(gs.view(ch, -1, gs.shape[1]).transpose(1, 2), xs.view(ch, -1, d))
+        return None, part.float().sum(0)
+
+
+def _chunked_sum_bmm(a, b, ch: int = 64):
+    """sum_n a[n]^T b[n] for a [N, p], b [N, q] with N ~ 1e5: 64 K-chunks in
+    one batched GEMM, then a sum (cuBLAS picks an 8-CTA kernel for the
+    single skinny K = N product)."""
+    n = a.shape[0]
+    pad = (-n) % ch
+    if pad:
+        a = torch.cat([a, a.new_zeros(pad, a.shape[1])])
+        b = torch.cat([b, b.new_zeros(pad, b.shape[1])])
+    return torch.bmm(a.view(ch, -1, a.shape[1]).transpose(1, 2),
+                     b.view(ch, -1, b.shape[1])).sum(0)
+
+
+class HeadProject(torch.autograd.Function):
+    """out[n, k*F:(k+1)*F] = agg[n, k*d:(k+1)*d] @ w[k]^T, w [H, F, d]."""
+
+    @staticmethod
+    def forward(ctx, agg, w):
+        n = agg.shape[0]
+        H, f, d = w.shape
+        a = agg.view(n, H, d).transpose(0, 1).to(torch.bfloat16)          # [H, n, d]
+        out = torch.bmm(a, w.to(torch.bfloat16).transpose(1, 2))           # [H, n, F]
+        ctx.save_for_backward(a, w)
+        return out.transpose(0, 1).reshape(n, H * f).float()
+
+    @staticmethod
+    def backward(ctx, dout):
+        a, w = ctx.saved_tensors
+        H, f, d = w.shape
+        n = a.shape[1]
+        g = dout.view(n, H, f).transpose(0, 1).to(torch.bfloat16)          # [H, n, F]
+        dw = torch.stack([_chunked_sum_bmm(g[k], a[k]) for k in range(H)])  # [H, F, d]
+        return None, dw.float()
+
+
+class GatInputAggregate(torch.autograd.Function):
+    """A[v, k*d:(k+1)*d] = sum_e alpha[e,k] x[e] over decoded pick rows x
+    (constant input: no dx)."""
+
+    @staticmethod
+    def forward(ctx, x, alpha, indptr, n_dst, max_dst: int):
+        x = x.to(torch.bfloat16).contiguous()
+        d, heads = x.shape[1], alpha.shape[1]
+        out = torch.empty((max_dst, heads * d), dtype=torch.float32, device=x.device)
+        N.call("fg_gat_xagg_fwd", N.ptr(x), d, heads, N.ptr(alpha), N.ptr(indptr), max_dst,
+               N.ptr(n_dst), N.ptr(out), N.stream_handle())
+        ctx.save_for_backward(x, indptr, n_dst)
+        ctx.max_dst, ctx.heads, ctx.e_cap = max_dst, heads, alpha.shape[0]
+        return out
+
+    @staticmethod
+    def backward(ctx, dout):
+        x, indptr, n_dst = ctx.saved_tensors
+        dalpha = torch.zeros((ctx.e_cap, ctx.heads), dtype=torch.float32, device=x.device)
+        N.call("fg_gat_xagg_bwd", N.ptr(x), x.shape[1], ctx.heads, N.ptr(indptr), ctx.max_dst,
+               N.ptr(n_dst), N.ptr(dout.float().contiguous()), N.ptr(dalpha), ctx.e_cap,
+               N.stream_handle())
+        return None, dalpha, None, None, None
+
+
 class GatLayer(nn.Module):
     def __init__(self, in_dim: int, out_per_head: int, heads: int, out_pad: int | None = None):
         super().__init__()
@@ -104,12 +187,33 @@ class GatLayer(nn.Module):
         self.bias = nn.Parameter(torch.zeros(width))
 
     def forward(self, h, indptr, local, n_dst, max_dst, e_cap, slope=0.2):
+        if local is None:
+            return self._forward_input(h, indptr, n_dst, max_dst, e_cap, slope)
         z = self.lin(h)                                           # [src, width]
-        zh = z.view(-1, self.heads, self.width // self.heads).float()
-        el = (zh * self.attn_l).sum(-1)
-        er = (zh * self.attn_r).sum(-1)
+        # el/er = z . a per head = h (W_k^T a_k): one skinny GEMM on h
+        H, f = self.heads, self.width // self.heads
+        w = self.lin.weight.view(H, f, -1)
+        c = torch.cat([torch.einsum("hfd,hf->hd", w, self.attn_l),
+                       torch.einsum("hfd,hf->hd", w, self.attn_r)])  # [2H, in]
+        s = torch.mm(h, c.to(h.dtype).t()).float()
+        el, er = s[:, :H], s[:, H:]
         alpha = GatAttention.apply(el, er, indptr, local, n_dst, max_dst, e_cap, slope)
         return GatAggregate.apply(z, alpha, indptr, local, n_dst, max_dst) + self.bias
+
+    def _forward_input(self, x, indptr, n_dst, max_dst, e_cap, slope):
+        """Same math for the input layer, rearranged by linearity: scores
+        el = x (W_k^T a_l[k]) per pick, the attention-weighted sum of the
+        decoded picks per head, then one [N_dst, d] x [d, F] product per head
+        -- no per-pick projection (518 K x 256 at products shape)."""
+        H, f = self.heads, self.width // self.heads
+        d = x.shape[1]
+        w = self.lin.weight.view(H, f, d)                       # [H, F, d]
+        c = torch.cat([torch.einsum("hfd,hf->hd", w, self.attn_l),
+                       torch.einsum("hfd,hf->hd", w, self.attn_r)])  # [2H, d]
+        s = PickScores.apply(x.to(torch.bfloat16), c)           # [E, 2H]
+        alpha = GatAttention.apply(s[:, :H], s[:, H:], indptr, None, n_dst, max_dst, e_cap, slope)
+        agg = GatInputAggregate.apply(x, alpha, indptr, n_dst, max_dst)   # [N, H*d]
+        return HeadProject.apply(agg, w) + self.bias
 
 
 class GatModel(nn.Module):

@@ -186,7 +186,9 @@ class SageTrainer:
                                                need_local=True, need_transpose=True,
                                                transpose_layers=tl, share=self.sampler,
                                                aggregator=cfg.aggregator))
-            self.side = torch.cuda.Stream(self.device)
+            # high priority: the latency-bound sampler kernels take SMs as soon as
+            # the wide training kernels free them
+            self.side = torch.cuda.Stream(self.device, priority=-1)
         self.caps = self.sampler.caps
         # flat gradient buffer: one all-reduce per step
         # one flat fp32 buffer each for params, grads and Adam moments: a

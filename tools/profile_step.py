@@ -24,9 +24,14 @@ def main():
     # run backward on this thread so its kernels fall inside the NVTX range
     torch.autograd.set_multithreading_enabled(False)
     sg, dc, desc, fanouts, bs, hidden = bench.build_workload(a.config, dev, scale=a.scale)
-    tr = SageTrainer(sg.graph, dc, sg.labels, sg.num_classes,
-                     TrainConfig(fanouts=fanouts, batch_size=bs, hidden=hidden,
-                                 aggregator=bench.aggregator_of(a.config)))
+    if bench.aggregator_of(a.config) == "gat":
+        from paper_2207_14696_b200.gat import GatConfig, GatTrainer
+        tr = GatTrainer(sg.graph, dc, sg.labels, sg.num_classes,
+                        GatConfig(fanouts=fanouts, batch_size=bs, hidden=hidden))
+    else:
+        tr = SageTrainer(sg.graph, dc, sg.labels, sg.num_classes,
+                         TrainConfig(fanouts=fanouts, batch_size=bs, hidden=hidden,
+                                     aggregator=bench.aggregator_of(a.config)))
     tr.begin_epoch(sg.train_ids, 0)
     for b in range(3):
         tr.step(b)
