@@ -257,3 +257,20 @@ def test_gcn_fused_input_layer_trains():
     losses = [float(t.step(b).item()) for b in range(nb)]
     assert np.isfinite(losses).all() and np.mean(losses[-5:]) < losses[0]
     t.sampler.check_errors()
+
+
+def test_measured_epoch_breakdown():
+    """measure.measure_epoch fills the reference's SimReport with measured
+    B200 stage times; SQ vs VQ reports compare on the same sampling plan."""
+    from paper_2207_14696_b200.measure import compare_reports, measure_epoch, render_text
+    reps = []
+    for vq in (False, True):
+        dg, labels, dc, train, val = _small_world(vq=vq, d=64)
+        t = SageTrainer(dg, dc, labels, 8, TrainConfig(fanouts=(10, 5), batch_size=256,
+                                                       hidden=64))
+        r = measure_epoch(t, train, "vq" if vq else "sq8", batches=5)
+        assert r.epoch_s > 0 and r.sample_s > 0 and r.dequant_s > 0 and r.compute_s > 0
+        assert r.workload["overlapped_epoch_s"] <= r.epoch_s * 1.5
+        reps.append(r)
+    out = compare_reports(reps[0], reps[1:])
+    assert len(render_text(out).splitlines()) == 4

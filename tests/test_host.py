@@ -265,3 +265,25 @@ def test_ddp_gloo_world2():
     assert out[0][2] == [1.5] * 5 and out[1][2] == [1.5] * 5
     assert out[0][3] == 1.0
     assert out[0][4] == [0, 2, 4, 6, 8, 10] and out[1][4] == [1, 3, 5, 7, 9]
+
+
+def test_measured_report_semantics_follow_the_reference():
+    """measure.SimReport / compare_reports / render_text keep the reference's
+    validation and dict form (pipeline.py:224-383)."""
+    from paper_2207_14696_b200.errors import DataError
+    from paper_2207_14696_b200.measure import SimReport, compare_reports, render_text
+    wl = {"graph_n": 10, "num_batches": 2, "fanouts": [5], "batch_size": 4, "seed": 0,
+          "measured_step_us": 1.0}
+    a = SimReport("vq", 1.0, 0.1, 0.5, 2.0, 3.6, 64.0, 1.0, 100, 25.0, wl)
+    b = SimReport("sq", 1.0, 0.1, 1.0, 2.0, 4.1, 64.0, 1.0, 400, 100.0,
+                  dict(wl, measured_step_us=2.0))
+    assert SimReport.from_dict(a.to_dict()) == a
+    out = compare_reports(b, [a])
+    assert out[0].speedup_vs_baseline == 1.0 and abs(out[1].speedup_vs_baseline - 4.1 / 3.6) < 1e-12
+    assert "speedup" in render_text(out).splitlines()[0]
+    with pytest.raises(DataError):
+        SimReport("x", 1.0, 0.0, 0.0, 0.0, 2.0, 0.0, 1.0, 0, 1.0, wl)
+    with pytest.raises(DataError):
+        compare_reports(a, [SimReport("y", 1, 0, 0, 0, 1, 0, 1.0, 0, 1.0, dict(wl, seed=1))])
+    with pytest.raises(DataError):
+        SimReport.from_dict({"label": "z"})
