@@ -337,7 +337,9 @@ k_block_mean_wgrad(const uint16_t* __restrict__ g, int64_t g_ld,
         for (int ks = 0; ks < kWgKT / 16; ++ks) {
           const uint64_t ad = umma_desc(abase + half * 16 * kCoreA + ks * 2 * a_lbo, a_lbo, kCoreA);
           const uint64_t bd = umma_desc(bbase + ks * 2 * b_lbo, b_lbo, 128);
+#ifndef FG_WGRAD_NO_MMA  // diagnostic build: everything but the tensor-core work
           umma_bf16(tmem + (uint32_t)(half * P), ad, bd, idesc, (k > 0 || ks > 0) ? 1u : 0u);
+#endif
         }
       }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
