@@ -565,6 +565,18 @@ __global__ void k_bm_clear(const int32_t* __restrict__ ids, const int64_t* __res
 
 using namespace fg;
 
+// Grid of the sampler's grid-stride helper kernels (mark / rank / clear):
+// FG_SAMPLER_PER_SM CTAs per SM (default 8).  Fewer CTAs leave more SM slots
+// to the training kernels the sampler overlaps with.
+static int sampler_grid(int64_t items) {
+  static const int per_sm = [] {
+    const char* e = getenv("FG_SAMPLER_PER_SM");
+    const int v = e ? atoi(e) : 8;
+    return v > 0 ? v : 8;
+  }();
+  return grid_for(items, 256, per_sm);
+}
+
 extern "C" {
 
 int64_t fg_sample_workspace_bytes(int64_t max_nodes) { return layer_ws_bytes(max_nodes); }
@@ -642,7 +654,7 @@ int fg_sample_layer(const int64_t* row_offsets, const int32_t* col_indices, int6
                                                        err_flag);
   FG_LAUNCH_CHECK();
   if (bitmap) {  // next layer's unique set: mark after any fix-up rewrote picks
-    k_mark32<<<grid_for(max_picks, 256), 256, 0, st>>>(picks, num_picks_dev, max_picks, bitmap,
+    k_mark32<<<sampler_grid(max_picks), 256, 0, st>>>(picks, num_picks_dev, max_picks, bitmap,
                                                        bm_words0(n));
     FG_LAUNCH_CHECK();
   }
@@ -660,7 +672,7 @@ int64_t fg_bitmap_workspace_bytes(int64_t n) {
 int fg_bitmap_mark(const int32_t* ids, const int64_t* cnt, int64_t max_count, uint32_t* bm,
                    int64_t n, void* s) {
   if (max_count == 0) return FG_OK;
-  k_mark32<<<grid_for(max_count, 256), 256, 0, as_stream(s)>>>(ids, cnt, max_count, bm,
+  k_mark32<<<sampler_grid(max_count), 256, 0, as_stream(s)>>>(ids, cnt, max_count, bm,
                                                                bm_words0(n));
   FG_LAUNCH_CHECK();
   return FG_OK;
@@ -669,7 +681,7 @@ int fg_bitmap_mark(const int32_t* ids, const int64_t* cnt, int64_t max_count, ui
 int fg_bitmap_mark64(const int64_t* ids, const int64_t* cnt, int64_t max_count, uint32_t* bm,
                      int64_t n, void* s) {
   if (max_count == 0) return FG_OK;
-  k_mark64<<<grid_for(max_count, 256), 256, 0, as_stream(s)>>>(ids, cnt, max_count, bm,
+  k_mark64<<<sampler_grid(max_count), 256, 0, as_stream(s)>>>(ids, cnt, max_count, bm,
                                                                bm_words0(n));
   FG_LAUNCH_CHECK();
   return FG_OK;
@@ -694,7 +706,7 @@ int fg_bitmap_compact(uint32_t* bm, int64_t n, int32_t* out_ids, int64_t max_out
 int fg_bitmap_rank(const int32_t* ids, const int64_t* cnt, int64_t max_count, const uint32_t* bm,
                    const int32_t* wprefix, int32_t* rank, void* s) {
   if (max_count == 0) return FG_OK;
-  k_bm_rank<<<grid_for(max_count, 256), 256, 0, as_stream(s)>>>(ids, cnt, max_count, bm, wprefix,
+  k_bm_rank<<<sampler_grid(max_count), 256, 0, as_stream(s)>>>(ids, cnt, max_count, bm, wprefix,
                                                                 rank);
   FG_LAUNCH_CHECK();
   return FG_OK;
@@ -703,7 +715,7 @@ int fg_bitmap_rank(const int32_t* ids, const int64_t* cnt, int64_t max_count, co
 int fg_bitmap_clear(const int32_t* ids, const int64_t* cnt, int64_t max_count, uint32_t* bm,
                     int64_t n, void* s) {
   if (max_count == 0) return FG_OK;
-  k_bm_clear<<<grid_for(max_count, 256), 256, 0, as_stream(s)>>>(ids, cnt, max_count, bm,
+  k_bm_clear<<<sampler_grid(max_count), 256, 0, as_stream(s)>>>(ids, cnt, max_count, bm,
                                                                   bm_words0(n));
   FG_LAUNCH_CHECK();
   return FG_OK;
