@@ -180,8 +180,13 @@ def build_vq_codec(n: int, d: int, width: int, length: int, *, labels, num_class
     else:  # only the fit sample rows are ever generated
         sample = synth_feature_rows(torch.from_numpy(pick).to(dev), d, kind=kind, seed=seed,
                                     labels=labels, num_classes=num_classes)
+    import sys
+    import time
+    t0 = time.perf_counter()
     codec = _fit_from_sample(sample.double(), p, d, 32, rng)
     del sample
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
     dc = DeviceVqCodec.empty(p, d, codec.codebooks, n, dev)
     for r0 in range(0, n, chunk_rows):
         m = min(chunk_rows, n - r0)
@@ -189,4 +194,7 @@ def build_vq_codec(n: int, d: int, width: int, length: int, *, labels, num_class
             m, d, row0=r0, kind=kind, seed=seed, labels=labels, num_classes=num_classes,
             device=dev)
         dc.encode_rows_(x, r0)
+    torch.cuda.synchronize()
+    print(f"[synth] vq codec: fit_vq on {rows} sample rows {t1 - t0:.1f} s, encode {n} rows "
+          f"{time.perf_counter() - t1:.1f} s", file=sys.stderr, flush=True)
     return dc, codec
