@@ -24,6 +24,8 @@
 //  * `out_ld` lets the caller pad rows (e.g. d=100 -> 112) so the following
 //    bf16 GEMM sees 16-element-aligned K.
 #include <algorithm>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <type_traits>
 
 #include "fg_common.cuh"
@@ -767,7 +769,8 @@ k_vq_mean_bits(const uint8_t* __restrict__ rows, int64_t d, int64_t stride, int 
 // exceed the row buffer falls back to direct register loads.
 constexpr int kBulkThreads = 512;
 constexpr int kBulkRowCap = 1024;                          // rows per buffer, max
-constexpr int kBulkSidPer = kBulkRowCap / kBulkThreads;    // src ids per thread
+constexpr int kBulkSidPer = 4;  // src ids per thread (kBulkRowCap / kBulkThreads, or one gather4)
+static_assert(kBulkSidPer * kBulkThreads >= kBulkRowCap, "row staging capacity");
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
@@ -839,13 +842,17 @@ __device__ __forceinline__ void sq_store(OT* o, const u64 (&acc)[8], float inv, 
   }
 }
 
-template <int K, typename OT, bool WT>
+// G4: rows staged by TMA tensor gathers (cp.async.bulk.tensor ... tile::gather4,
+// sm_100): one instruction moves 4 code rows of 4 consecutive edges (row
+// indices as coordinates), 4x fewer issue slots than per-row bulk copies,
+// whose operands must be warp-uniform (a 32-step elect loop per warp).
+template <int K, typename OT, bool WT, bool G4 = false>
 __global__ void __launch_bounds__(kBulkThreads, 1)
 k_sq_mean_bulk(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
                const float* __restrict__ lut, const int32_t* __restrict__ indptr,
                const int32_t* __restrict__ src, const int64_t* __restrict__ ndst_dev,
                int64_t max_dst, OT* __restrict__ out, int64_t ld, int td, int row_cap, int rb,
-               const float* __restrict__ ew) {
+               const float* __restrict__ ew, const __grid_constant__ CUtensorMap tmap) {
   constexpr int NT = kBulkThreads;
   constexpr int Q = 1 << K;
   constexpr bool PAIR = 2 * K <= 8;
@@ -856,7 +863,15 @@ k_sq_mean_bulk(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
   u64* s_lut2 = reinterpret_cast<u64*>(s_mem);
   int32_t* s_ip = reinterpret_cast<int32_t*>(s_mem + LW);   // [4][kTD + 1]
   uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_ip + IPW);  // [2]
-  uint8_t* s_rows = reinterpret_cast<uint8_t*>(s_bar + 2);   // [2][row_cap * rb]
+  // [2][buffer]: G4 packs rows in groups of 4 at a 128-byte-aligned group
+  // pitch (tensor-copy destinations must be 128-byte aligned)
+  uint8_t* s_rows = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(s_bar + 2) + 127) & ~static_cast<uintptr_t>(127));
+  const int gstride = (4 * rb + 127) & ~127;
+  const int64_t buf_bytes = G4 ? (int64_t)(row_cap >> 2) * gstride : (int64_t)row_cap * rb;
+  auto rowp = [&](const uint8_t* base, int e) -> const uint8_t* {
+    return G4 ? base + (int64_t)(e >> 2) * gstride + (e & 3) * rb : base + (int64_t)e * rb;
+  };
   const int tid = threadIdx.x, lane = tid & 31;
   const int64_t live = live_dst(ndst_dev, max_dst);
   const int64_t ntiles = (live + td - 1) / td;
@@ -884,32 +899,48 @@ k_sq_mean_bulk(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
   };
   auto store_ip = [&](int32_t* slot, int32_t v) { if (tid <= td) slot[tid] = v; };
   int32_t sid[kBulkSidPer];
+  // G4: thread t owns edges 4t .. 4t+3 (one gather4); else edges t + j*NT
+  auto edge_of = [&](int j) { return G4 ? 4 * tid + j : tid + j * NT; };
   auto load_sids = [&](const int32_t* ip) {
     const int32_t e0 = ip[0], ne = ip[td] - e0;
     if (ne > row_cap) return;
 #pragma unroll
     for (int j = 0; j < kBulkSidPer; ++j) {
-      const int e = tid + j * NT;
+      const int e = edge_of(j);
+      // G4 pads a partial last group with its last valid row (dummy copies
+      // into buffer slack; never read)
       if (e < ne) sid[j] = __ldg(src + e0 + e);
+      else if (G4 && 4 * tid < ne) sid[j] = sid[j > 0 ? j - 1 : 0];
     }
   };
   auto issue_rows = [&](const int32_t* ip, int b) {
     const int32_t ne = ip[td] - ip[0];
     if (ne > row_cap) return;
     const uint32_t bar = smem_addr(s_bar + b);
-    uint8_t* dst = s_rows + (int64_t)b * row_cap * rb;
+    uint8_t* dst = s_rows + (int64_t)b * buf_bytes;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    const uint32_t groups = G4 ? (uint32_t)((ne + 3) / 4) : 0u;
     if (tid == 0)
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
-                   ::"r"(bar), "r"((uint32_t)ne * (uint32_t)rb) : "memory");
-#pragma unroll
-    for (int j = 0; j < kBulkSidPer; ++j) {
-      const int e = tid + j * NT;
-      if (e < ne)
+                   ::"r"(bar), "r"((G4 ? groups * 4u : (uint32_t)ne) * (uint32_t)rb) : "memory");
+    if constexpr (G4) {
+      if ((uint32_t)tid < groups)
         asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-            ::"r"(smem_addr(dst + (int64_t)e * rb)), "l"(rows + (int64_t)sid[j] * stride),
-              "r"(rb), "r"(bar) : "memory");
+            "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];"
+            ::"r"(smem_addr(dst + (int64_t)tid * gstride)),
+              "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(0), "r"(sid[0]), "r"(sid[1]),
+              "r"(sid[2]), "r"(sid[3]), "r"(bar) : "memory");
+    } else {
+#pragma unroll
+      for (int j = 0; j < kBulkSidPer; ++j) {
+        const int e = tid + j * NT;
+        if (e < ne)
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+              ::"r"(smem_addr(dst + (int64_t)e * rb)), "l"(rows + (int64_t)sid[j] * stride),
+                "r"(rb), "r"(bar) : "memory");
+      }
     }
   };
   // prologue: indptr of tiles 0..2, rows of tile 0 in flight, src ids of tile 1
@@ -940,7 +971,7 @@ k_sq_mean_bulk(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
       mbar_wait_parity(s_bar + b, (phase >> b) & 1u);
       phase ^= 1u << b;
     }
-    const uint8_t* rbuf = s_rows + (int64_t)b * row_cap * rb;
+    const uint8_t* rbuf = s_rows + (int64_t)b * buf_bytes;
     const int items = td * chunks;
     for (int it = tid; it < items; it += NT) {
       const int vl = it / chunks;
@@ -953,7 +984,7 @@ k_sq_mean_bulk(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
       const int a = ip[vl] - e0;
       const int cnt = ip[vl + 1] - e0 - a;
       if (staged) {
-        const uint8_t* rp = rbuf + (int64_t)a * rb + c * (2 * K);
+        const int coff = c * (2 * K);
         const float* ewp = WT ? ew + e0 + a : nullptr;
         int p = 0;
         for (; p + 4 <= cnt; p += 4) {
@@ -961,7 +992,7 @@ k_sq_mean_bulk(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
           u64 wt[4];
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            lds_chunk<K>(rp + (p + u) * rb, w[u][0], w[u][1]);
+            lds_chunk<K>(rowp(rbuf, a + p + u) + coff, w[u][0], w[u][1]);
             if constexpr (WT) wt[u] = bcast2(__ldg(ewp + p + u));
           }
 #pragma unroll
@@ -970,7 +1001,7 @@ k_sq_mean_bulk(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
         }
         for (; p < cnt; ++p) {
           uint64_t w0, w1;
-          lds_chunk<K>(rp + p * rb, w0, w1);
+          lds_chunk<K>(rowp(rbuf, a + p) + coff, w0, w1);
           sq_accumulate<K, PAIR, WT>(acc, w0, w1, s_lut, s_lut2, lane,
                                      WT ? bcast2(__ldg(ewp + p)) : 0);
         }
@@ -1003,6 +1034,31 @@ k_sq_mean_bulk(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
   }
 }
 
+// 2-D uint8 tensor map over the code rows ([n][row_stride] bytes, box = the
+// first rb bytes of one row) for the gather4 row staging; false when the
+// driver entry point is unavailable (then per-row bulk copies are used).
+static bool code_row_tensor_map(const fg_codec_desc* c, int rb, CUtensorMap* m) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+            cudaSuccess || q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }();
+  memset(m, 0, sizeof(*m));
+  if (!encode || (reinterpret_cast<uintptr_t>(c->rows) & 15) || (c->row_stride & 15) || c->n < 1)
+    return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)c->row_stride, (cuuint64_t)c->n};
+  const cuuint64_t strides[1] = {(cuuint64_t)c->row_stride};
+  const cuuint32_t box[2] = {(cuuint32_t)rb, 1u};
+  const cuuint32_t estr[2] = {1u, 1u};
+  return encode(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)c->rows, dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+
 // ------------------------------------------------------------ launchers
 template <int K, typename OT, bool WT>
 int launch_sq_w(const fg_codec_desc* c, const int32_t* indptr, const int32_t* src,
@@ -1016,18 +1072,23 @@ int launch_sq_w(const fg_codec_desc* c, const int32_t* indptr, const int32_t* sr
     const int fixed = lut_b + ((((kTD + 1) * 4 + 3) & ~3) * 4) + 16;
     const int chunks = (int)((c->d + 15) / 16);
     const int rb = (chunks * 2 * K + 15) / 16 * 16;
-    int row_cap = (kSmemBudget - fixed) / (2 * rb);
+    CUtensorMap tmap;
+    const bool g4 = rb <= 256 && rb <= c->row_stride && code_row_tensor_map(c, rb, &tmap);
+    const int gstride = (4 * rb + 127) & ~127;  // G4 group pitch (128-B aligned)
+    int row_cap = g4 ? (kSmemBudget - fixed - 128) / (2 * gstride) * 4
+                     : (kSmemBudget - fixed - 128) / (2 * rb);
     if (row_cap > kBulkRowCap) row_cap = kBulkRowCap;
+    row_cap &= ~3;  // whole gather4 groups
     int td = kTD;
     while (td > 32 && td * 8 > row_cap) td /= 2;
     if (td * 8 <= row_cap && rb <= c->row_stride) {
-      const int smem = fixed + 2 * row_cap * rb;
-      auto kern = k_sq_mean_bulk<K, OT, WT>;
-      FG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      const int smem = fixed + 128 + 2 * (g4 ? (row_cap / 4) * gstride : row_cap * rb);
       const int grid = (int)min64(ceil_div(max_dst, td), (int64_t)sm_count());
+      auto kern = g4 ? k_sq_mean_bulk<K, OT, WT, true> : k_sq_mean_bulk<K, OT, WT, false>;
+      FG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       kern<<<grid, kBulkThreads, smem, st>>>(c->rows, c->d, c->row_stride,
                                              (const float*)c->table, indptr, src, ndst, max_dst,
-                                             (OT*)out, ld, td, row_cap, rb, ew);
+                                             (OT*)out, ld, td, row_cap, rb, ew, tmap);
       FG_LAUNCH_CHECK();
       return FG_OK;
     }
