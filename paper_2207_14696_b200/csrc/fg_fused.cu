@@ -24,6 +24,7 @@
 //  * `out_ld` lets the caller pad rows (e.g. d=100 -> 112) so the following
 //    bf16 GEMM sees 16-element-aligned K.
 #include <algorithm>
+#include <stdlib.h>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <type_traits>
@@ -1170,7 +1171,14 @@ int launch_vq_w(const fg_codec_desc* c, const int32_t* indptr, const int32_t* sr
       FG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)fast_smem));
       // grid: a multiple of the slice count, ~3 CTAs per SM in total
-      const int64_t per_slice = std::max<int64_t>(1, min64(ntiles, (int64_t)sm_count() * 3 / ns));
+      // (FG_FUSED_CTA_PCT: percent of that, to leave room for overlapped work)
+      static const int pct = [] {
+        const char* e = getenv("FG_FUSED_CTA_PCT");
+        const int v = e ? atoi(e) : 100;
+        return v > 0 && v <= 100 ? v : 100;
+      }();
+      const int64_t per_slice = std::max<int64_t>(
+          1, min64(ntiles, (int64_t)sm_count() * 3 * pct / 100 / ns));
       const int grid = (int)(per_slice * ns);
       kern<<<grid, kFastThreads, fast_smem, st>>>(c->rows, c->d, c->row_stride,
                                               (const __nv_bfloat16*)c->table_lp, c->length,

@@ -32,6 +32,8 @@
 // Numerics: each edge term is rounded to bf16 before the MMA (the unfused
 // bf16 autograd path rounds the per-row sums instead), accumulation is fp32
 // in TMEM.
+#include <stdlib.h>
+
 #include "fg_common.cuh"
 
 namespace fg {
@@ -472,7 +474,15 @@ extern "C" int fg_block_mean_wgrad(const uint16_t* g, int64_t g_ld, const int32_
   FG_CHECK_ARG(fg_block_mean_wgrad_supported(H, P), "unsupported shape H=%lld P=%lld",
                (long long)H, (long long)P);
   FG_CHECK_ARG(g_ld >= H && g_ld % 8 == 0, "bad g_ld");
-  const int nb = sm_count();
+  // persistent CTAs on 3/4 of the SMs: the rest stay free for the sampler
+  // kernels that overlap the training step on the side stream (products
+  // step: 288 -> 276 us at 112 of 148 SMs; 96 is slower again).
+  // FG_WGRAD_CTAS overrides (1 .. SM count).
+  static const int nb_env = [] {
+    const char* e = getenv("FG_WGRAD_CTAS");
+    return e ? atoi(e) : 0;
+  }();
+  const int nb = nb_env > 0 && nb_env <= sm_count() ? nb_env : (sm_count() * 3) / 4;
   FG_CHECK_ARG(scratch_bytes >= fg_block_mean_wgrad_scratch_bytes(H, P), "scratch too small");
   cudaStream_t st = as_stream(s);
   float* seg_f = scratch + (int64_t)nb * H * P;
