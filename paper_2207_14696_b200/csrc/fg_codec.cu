@@ -105,20 +105,37 @@ __global__ void k_sq_encode(const XT* __restrict__ x, int64_t n, int64_t d, int 
 
 // ------------------------------------------------- SQ gather dequantize
 template <typename OT, typename LT>
-__global__ void k_sq_gather(const uint8_t* __restrict__ rows, int64_t n, int64_t d, int k,
-                            int64_t stride, const LT* __restrict__ lut, const void* ids,
-                            int ids32, int64_t num_ids, OT* __restrict__ out,
-                            int32_t* err_flag) {
-  __shared__ LT s_lut[256];
-  for (int i = threadIdx.x; i < (1 << k); i += blockDim.x) s_lut[i] = lut[i];
+__global__ void __launch_bounds__(256)
+k_sq_gather(const uint8_t* __restrict__ rows, int64_t n, int64_t d, int k,
+            int64_t stride, const LT* __restrict__ lut, const void* ids,
+            int ids32, int64_t num_ids, OT* __restrict__ out,
+            int32_t* err_flag) {
+  // LUT replicated per lane (entry * 32 + lane): random codes never bank
+  // conflict.  Thread per (row, 8 codes); the row id is loaded once per
+  // group of lanes of the same row (L1 broadcast); 8 outputs are stored as
+  // one 16-byte (bf16) / two 16-byte (fp32) vector when aligned.
+  extern __shared__ __align__(16) unsigned char s_raw[];
+  LT* s_lut = reinterpret_cast<LT*>(s_raw);
+  const int lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < (1 << k) * 32; i += blockDim.x) s_lut[i] = lut[i >> 5];
   __syncthreads();
   const int64_t groups = (d + 7) >> 3;
   const int64_t total = num_ids * groups;
   const uint32_t mask = (1u << k) - 1u;
+  const bool vec = (d % 8) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+  const bool vec8 = (d % 4) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0;  // 8-B aligned groups
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = t / groups, g = t - i * groups;
-    const int64_t r = ids32 ? (int64_t)((const int32_t*)ids)[i] : ((const int64_t*)ids)[i];
+    int64_t i, g;
+    if (total < (1ll << 31)) {  // 32-bit division (the 64-bit one dominated)
+      const uint32_t t32 = (uint32_t)t, g32 = (uint32_t)groups;
+      i = t32 / g32;
+      g = t32 - (uint32_t)i * g32;
+    } else {
+      i = t / groups;
+      g = t - i * groups;
+    }
+    const int64_t r = ids32 ? (int64_t)__ldg((const int32_t*)ids + i) : __ldg((const int64_t*)ids + i);
     if (r < 0 || r >= n) {
       if (g == 0) atomicExch(err_flag, FG_EDATA);
       continue;
@@ -137,13 +154,39 @@ __global__ void k_sq_gather(const uint8_t* __restrict__ rows, int64_t n, int64_t
     const int64_t j0 = g * 8;
     const int cnt = (int)min64(8, d - j0);
     OT* o = out + i * d + j0;
+    LT v[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
-      if (e < cnt) {
-        const uint32_t q = (uint32_t)(acc >> (k * (7 - e))) & mask;
-        o[e] = cvt_out<OT>(s_lut[q]);
+      const uint32_t q = (uint32_t)(acc >> (k * (7 - e))) & mask;
+      v[e] = s_lut[q * 32 + lane];
+    }
+    if (sizeof(OT) == 2 && vec8 && (cnt == 8 || cnt == 4)) {
+      uint32_t w[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const __nv_bfloat162 b2 = __floats2bfloat162_rn((float)v[2 * e], (float)v[2 * e + 1]);
+        w[e] = *reinterpret_cast<const uint32_t*>(&b2);
+      }
+      if (vec && cnt == 8) {
+        *reinterpret_cast<uint4*>(o) = make_uint4(w[0], w[1], w[2], w[3]);
+      } else {  // 8-byte aligned halves (d % 4 == 0, e.g. d = 100)
+        reinterpret_cast<uint2*>(o)[0] = make_uint2(w[0], w[1]);
+        if (cnt == 8) reinterpret_cast<uint2*>(o)[1] = make_uint2(w[2], w[3]);
+      }
+      continue;
+    }
+    if (vec && cnt == 8) {
+      if constexpr (sizeof(OT) == 2) {
+        continue;  // handled above
+      } else if constexpr (sizeof(OT) == 4) {
+        reinterpret_cast<float4*>(o)[0] = make_float4((float)v[0], (float)v[1], (float)v[2], (float)v[3]);
+        reinterpret_cast<float4*>(o)[1] = make_float4((float)v[4], (float)v[5], (float)v[6], (float)v[7]);
+        continue;
       }
     }
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+      if (e < cnt) o[e] = cvt_out<OT>(v[e]);
   }
 }
 
@@ -169,8 +212,15 @@ __global__ void k_vq_gather(const uint8_t* __restrict__ rows, int64_t n, int64_t
   const int64_t total = num_ids * parts;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = t / parts;
-    const int p = (int)(t - i * parts);
+    int64_t i;
+    int p;
+    if (total < (1ll << 31)) {  // 32-bit division
+      i = (uint32_t)t / (uint32_t)parts;
+      p = (int)((uint32_t)t - (uint32_t)i * (uint32_t)parts);
+    } else {
+      i = t / parts;
+      p = (int)(t - i * parts);
+    }
     const int64_t r = ids32 ? (int64_t)((const int32_t*)ids)[i] : ((const int64_t*)ids)[i];
     if (r < 0 || r >= n) {
       if (p == 0) atomicExch(err_flag, FG_EDATA);
@@ -182,7 +232,11 @@ __global__ void k_vq_gather(const uint8_t* __restrict__ rows, int64_t n, int64_t
     const int lo = p * width;
     const int wp = (int)min64(width, d - lo);
     OT* o = out + i * d + lo;
-    for (int j = 0; j < wp; ++j) store_out(o + j, e[j]);
+    if (wp == 4 && width == 4 && (d % 4) == 0 && sizeof(OT) == 4) {  // one 16-B copy
+      *reinterpret_cast<float4*>(o) = __ldg(reinterpret_cast<const float4*>(e));
+      continue;
+    }
+    for (int j = 0; j < wp; ++j) store_out(o + j, __ldg(e + j));
   }
 }
 
@@ -717,17 +771,27 @@ int fg_sq_gather_dequant(const fg_codec_desc* c, const void* ids, int ids32, int
   const int64_t total = num_ids * ((c->d + 7) / 8);
   const int grid = grid_for(total, 256);
   cudaStream_t st = as_stream(s);
+  static bool attrs = [] {  // replicated LUTs up to 64 KB (k = 8, float64)
+    cudaFuncSetAttribute(k_sq_gather<double, double>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, 256 * 32 * 8);
+    cudaFuncSetAttribute(k_sq_gather<float, float>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, 256 * 32 * 4);
+    cudaFuncSetAttribute(k_sq_gather<__nv_bfloat16, float>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, 256 * 32 * 4);
+    return true;
+  }();
+  (void)attrs;
   if (c->elem_bits == 64) {
     FG_CHECK_ARG(out_dtype == FG_OUT_F64, "float64 codec decodes to float64");
-    k_sq_gather<double, double><<<grid, 256, 0, st>>>(c->rows, c->n, c->d, c->bits, c->row_stride,
+    k_sq_gather<double, double><<<grid, 256, (1 << c->bits) * 32 * 8, st>>>(c->rows, c->n, c->d, c->bits, c->row_stride,
                                                       (const double*)c->table, ids, ids32, num_ids,
                                                       (double*)out, err_flag);
   } else if (out_dtype == FG_OUT_BF16) {
-    k_sq_gather<__nv_bfloat16, float><<<grid, 256, 0, st>>>(c->rows, c->n, c->d, c->bits, c->row_stride,
+    k_sq_gather<__nv_bfloat16, float><<<grid, 256, (1 << c->bits) * 32 * 4, st>>>(c->rows, c->n, c->d, c->bits, c->row_stride,
                                                     (const float*)c->table, ids, ids32, num_ids,
                                                     (__nv_bfloat16*)out, err_flag);
   } else if (out_dtype == FG_OUT_F32) {
-    k_sq_gather<float, float><<<grid, 256, 0, st>>>(c->rows, c->n, c->d, c->bits, c->row_stride,
+    k_sq_gather<float, float><<<grid, 256, (1 << c->bits) * 32 * 4, st>>>(c->rows, c->n, c->d, c->bits, c->row_stride,
                                                     (const float*)c->table, ids, ids32, num_ids,
                                                     (float*)out, err_flag);
   } else {

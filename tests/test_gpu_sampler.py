@@ -152,3 +152,42 @@ def test_sampler_lemire_rejection_fixup(fanout, seeds, n_leaves):
         draws = int(smp.rng[6].item())
         total_rej += draws - (hubs + n_leaves) * (2 * fanout - 1)
     assert total_rej > 0, "no Lemire rejection exercised"
+
+
+@pytest.mark.parametrize("fans,bs", [((1,), 7), ((3, 2), 64), ((4, 4, 4), 1000)])
+def test_sampler_edge_cases_match_oracle(fans, bs):
+    """No self-loops with isolated (degree-0) nodes, duplicate train ids
+    (np.unique), a partial last batch, fanout 1, a batch larger than the
+    train set: per-node picks, frontier and final stream state equal the
+    oracle restatement of pipeline.py:185-222."""
+    r = np.random.default_rng(len(fans) * 100 + bs)
+    n = 3000
+    src = r.integers(0, n - 200, 12_000)          # nodes n-200.. are isolated
+    dst = r.integers(0, n - 200, 12_000)
+    keep = src != dst
+    a = np.concatenate([src[keep], dst[keep]])
+    b = np.concatenate([dst[keep], src[keep]])
+    key = np.unique(a.astype(np.int64) * n + b)
+    rows, cols = key // n, (key % n).astype(np.int32)
+    off = np.zeros(n + 1, np.int64)
+    np.add.at(off, rows + 1, 1)
+    off = np.cumsum(off)
+    g = fg.CsrGraph(n, off, cols)
+    train = np.concatenate([r.integers(0, n, 400), np.arange(n - 50, n)])  # dups + isolated
+    seed = 11
+    smp = DeviceSampler(g.to_device(), fans, bs, need_local=True, want_frontier=True)
+    nb = smp.begin_epoch(train, seed)
+    ref, ref_state = sample_batches_oracle(off, cols, train, fans, bs, seed)
+    assert nb == len(ref)
+    for bi, rb in enumerate(ref):
+        sb = smp.sample(bi)
+        got = _blocks(smp, sb, len(fans))
+        for li, L in enumerate(rb.layers):
+            assert np.array_equal(got[li][0], L.nodes), (bi, li)
+            assert np.array_equal(got[li][1], L.counts), (bi, li)
+            assert np.array_equal(got[li][2], L.picks), (bi, li)
+        nf = int(sb.n_frontier.item())
+        assert np.array_equal(sb.frontier[:nf].cpu().numpy(), rb.frontier)
+    st = smp.stream_state()
+    assert st["state"]["state"] == ref_state["state"]["state"]
+    smp.check_errors()

@@ -41,9 +41,12 @@ def launches(path):
 
 
 def report_metrics(path):
-    r = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
-                       text=True)
-    rows = list(csv.reader(r.stdout.splitlines()))
+    if path.endswith(".csv"):  # `ncu -i rep --page raw --csv` output saved on the GPU box
+        text = open(path).read()
+    else:
+        text = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"],
+                              capture_output=True, text=True).stdout
+    rows = list(csv.reader(text.splitlines()))
     h, u = rows[0], rows[1]
     res = []
     for v in rows[2:]:
@@ -82,7 +85,7 @@ def main():
                 fh.write(f"| {v:.1f} | {v / tot * 100:.1f}% | `{k}` |\n")
     for rep in a.report:
         m = report_metrics(rep)
-        name = os.path.splitext(os.path.basename(rep))[0]
+        name = os.path.splitext(os.path.basename(rep))[0].removesuffix("_raw")
         with open(os.path.join(root, f"{name}_summary.json"), "w") as fh:
             json.dump({"source": f"ncu --set full --clock-control none --import-source on "
                                  f"({os.path.basename(rep)})", "kernels": m}, fh, indent=1)
