@@ -396,70 +396,112 @@ def oracle_model(ot, d, hidden, num_classes, fanouts, aggregator):
     return ot.OracleSage(d, hidden, num_classes, len(fanouts)), step
 
 
+_PAR = {}  # host world shared with forked CPU-baseline workers (copy-on-write)
+
+
+def _par_worker(wid, nsteps, batch, barrier, q, warm=0):
+    """One shard-parallel CPU worker: its own batches of the train ids, one
+    thread (the reference is single-threaded numpy; parallelism is across
+    processes)."""
+    import torch
+    from oracle import trainer as ot
+    torch.set_num_threads(1)
+    c = _PAR
+    model, step = oracle_model(ot, c["d"], c["hidden"], c["classes"], c["fanouts"], c["agg"])
+    opt = torch.optim.Adam(model.parameters(), lr=3e-3)
+    train = c["train"]
+    nb = max(1, train.size // batch)
+    for i in range(warm):  # untimed warm-up batches
+        b = (wid * (nsteps + warm) + nsteps + i) % nb
+        step(model, opt, c["host"], c["labels"], train[b * batch:(b + 1) * batch], c["fanouts"],
+             batch, b, c["decode"])
+    barrier.wait()
+    t0 = time.perf_counter()
+    for i in range(nsteps):
+        b = (wid * (nsteps + warm) + i) % nb
+        step(model, opt, c["host"], c["labels"], train[b * batch:(b + 1) * batch], c["fanouts"],
+             batch, b, c["decode"])
+    q.put((wid, time.perf_counter() - t0))
+
+
+def cpu_parallel(sg, dc, fanouts, hidden, aggregator, batch, nsteps, workers=None, warm=0):
+    """Shard-parallel CPU run of the oracle port (P
+    processes over disjoint batches, P = host cores): returns (seeds,
+    wall seconds, workers)."""
+    import multiprocessing as mp
+    host, labels, decode = _host_world(sg, dc)
+    workers = workers or os.cpu_count() or 1
+    _PAR.update(host=host, labels=labels, decode=decode, d=dc.d, hidden=hidden,
+                classes=sg.num_classes, fanouts=fanouts, agg=aggregator, train=sg.train_ids)
+    ctx = mp.get_context("fork")
+    barrier, q = ctx.Barrier(workers + 1), ctx.Queue()
+    procs = [ctx.Process(target=_par_worker, args=(w, nsteps, batch, barrier, q, warm))
+             for w in range(workers)]
+    for pr in procs:
+        pr.start()
+    barrier.wait()
+    t0 = time.perf_counter()
+    done = [q.get(timeout=3600) for _ in range(workers)]
+    wall = time.perf_counter() - t0
+    for pr in procs:
+        pr.join(60)
+    _PAR.clear()
+    return workers * nsteps * batch, max(wall, max(t for _, t in done)), workers
+
+
 def cpu_baseline(sg, dc, fanouts, hidden, budget_s=20.0, batch=128, aggregator="mean"):
     """Oracle port of the reference path on the host cores: numpy sampler
     (pipeline.py:185-222 restated) + numpy decoder + CPU fp32 SAGE step."""
     import torch
     from oracle import trainer as ot
+    # probe one single-threaded batch to size the parallel run to ~budget_s
     host, labels, decode = _host_world(sg, dc)
     model, train_step = oracle_model(ot, dc.d, hidden, sg.num_classes, fanouts, aggregator)
     opt = torch.optim.Adam(model.parameters(), lr=3e-3)
-    seeds_done, t0, steps = 0, time.perf_counter(), 0
-    train = sg.train_ids
-    while True:
-        train_step(model, opt, host, labels, train[steps * batch:(steps + 1) * batch], fanouts,
-                   batch, steps, decode)
-        steps += 1
-        seeds_done += batch
-        if time.perf_counter() - t0 >= budget_s or steps * batch >= train.size:
-            break
-    dt = time.perf_counter() - t0
-    return {"value": round(seeds_done / dt, 2), "unit": "seeds/s",
-            "cores": torch.get_num_threads(), "kind": "port",
-            "sample": f"{steps} mini-batches of {batch} seeds, fanouts {list(fanouts)}, "
-                      f"{dt:.1f} s (numpy sampler/decoder single-threaded, torch CPU "
-                      f"fp32 SAGE step on {torch.get_num_threads()} threads)"}
+    nt = torch.get_num_threads()
+    torch.set_num_threads(1)
+    t0 = time.perf_counter()
+    train_step(model, opt, host, labels, sg.train_ids[:batch], fanouts, batch, 0, decode)
+    per = time.perf_counter() - t0
+    torch.set_num_threads(nt)
+    nsteps = max(1, int(budget_s / max(per, 1e-3)))
+    seeds, wall, workers = cpu_parallel(sg, dc, fanouts, hidden, aggregator, batch, nsteps)
+    return {"value": round(seeds / wall, 2), "unit": "seeds/s", "cores": workers,
+            "kind": "port",
+            "sample": f"{workers} processes x {nsteps} mini-batches of {batch} seeds, fanouts "
+                      f"{list(fanouts)}, {wall:.1f} s wall (oracle port: numpy sampler/decoder "
+                      f"+ CPU fp32 model step, one thread per process, disjoint batches)"}
 
 
 def run_reference(args, rank, world, local):
-    """The reference arm: CPU oracle port, rank 0 only."""
+    """The reference arm: the CPU oracle port of the reference path, rank 0
+    only, on every host core: P = cpu_count processes over disjoint batches
+    (one thread each: the reference is single-threaded numpy).  One step =
+    every process trains one batch of --ref-batch seeds."""
     if rank != 0:
         return
     import torch
-    from oracle import trainer as ot
     dev = torch.device("cuda", local) if torch.cuda.is_available() else torch.device("cpu")
     if dev.type == "cuda":
         torch.cuda.set_device(dev)
     sg, dc, codec_desc, fanouts, bs, hidden = build_workload(args.config, dev, scale=args.scale)
-    host, labels, decode = _host_world(sg, dc)
-    torch.set_num_threads(os.cpu_count() or 1)
-    model, train_step = oracle_model(ot, dc.d, hidden, sg.num_classes, fanouts,
-                                     aggregator_of(args.config))
-    opt = torch.optim.Adam(model.parameters(), lr=3e-3)
     batch = args.ref_batch
-    train = sg.train_ids
-
-    def one(i):
-        train_step(model, opt, host, labels, train[i * batch:(i + 1) * batch], fanouts, batch,
-                   i, decode)
-
-    for i in range(args.warmup):
-        one(i)
-    t0 = time.perf_counter()
-    for i in range(args.steps):
-        one(args.warmup + i)
-    dt = time.perf_counter() - t0
-    v = batch * args.steps / dt
+    seeds, dt, workers = cpu_parallel(sg, dc, fanouts, hidden, aggregator_of(args.config), batch,
+                                      args.steps, warm=args.warmup)
+    v = seeds / dt
+    agg = aggregator_of(args.config)
     line = {"impl": "reference", "metric": "GraphSAGE train seeds/sec", "value": round(v, 2),
             "unit": "seeds/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(dt * 1e3 / args.steps, 2), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"{args.config}-shape GraphSAGE {len(fanouts)}-layer fanout "
-                                   f"{list(fanouts)}, {codec_desc}",
-                       "per_step_seeds": batch, "parallelism": "cpu"},
-            "cpu_baseline": {"value": round(v, 2), "unit": "seeds/s",
-                             "cores": torch.get_num_threads(), "kind": "port",
-                             "sample": f"{args.steps} steps x {batch} seeds"},
+            "config": {"workload": f"{args.config}-shape "
+                                   f"{dict(gcn='GCN', gat='GAT').get(agg, 'GraphSAGE')} "
+                                   f"{len(fanouts)}-layer fanout {list(fanouts)}, {codec_desc}",
+                       "per_step_seeds": batch * workers, "parallelism": f"cpu x{workers}"},
+            "cpu_baseline": {"value": round(v, 2), "unit": "seeds/s", "cores": workers,
+                             "kind": "port",
+                             "sample": f"{args.steps} steps x {workers} processes x {batch} "
+                                       f"seeds (oracle port, one thread per process)"},
             "e2e": {"value": round(v, 2), "unit": "seeds/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
