@@ -396,57 +396,115 @@ def oracle_model(ot, d, hidden, num_classes, fanouts, aggregator):
     return ot.OracleSage(d, hidden, num_classes, len(fanouts)), step
 
 
-_PAR = {}  # host world shared with forked CPU-baseline workers (copy-on-write)
+# ------------------------------------------- shard-parallel CPU baseline
+# The reference is single-threaded numpy; its best case on a multi-core host
+# is P independent processes over disjoint batches.
+# Workers are SPAWNED (a forked child of a process that already ran torch /
+# OpenMP can deadlock) and map the host world from .npy files (mmap, shared).
+
+def save_host_world(host, labels, train, dc, path):
+    """Host CSR, labels, train ids and the codec's host form as .npy files."""
+    from paper_2207_14696_b200.vq import DeviceVqCodec
+    meta = {"n": int(host.n), "d": int(dc.d)}
+    np.save(os.path.join(path, "off.npy"), np.asarray(host.row_offsets))
+    np.save(os.path.join(path, "col.npy"), np.asarray(host.col_indices))
+    np.save(os.path.join(path, "labels.npy"), np.asarray(labels))
+    np.save(os.path.join(path, "train.npy"), np.asarray(train))
+    if isinstance(dc, DeviceVqCodec):
+        rows = dc.rows.cpu().numpy()
+        np.save(os.path.join(path, "codes.npy"), rows[:, :dc.num_parts].astype(np.int32))
+        for p_, b in enumerate(dc.books_host):
+            np.save(os.path.join(path, f"book{p_}.npy"), np.asarray(b))
+        meta.update(kind="vq", width=int(dc.params.width), parts=int(dc.num_parts))
+    else:
+        c = dc.to_codec()
+        np.save(os.path.join(path, "payload.npy"), np.frombuffer(c.payload, np.uint8))
+        meta.update(kind="sq", k=int(c.params.k), e_min=float(c.params.e_min),
+                    e_max=float(c.params.e_max))
+    return meta
 
 
-def _par_worker(wid, nsteps, batch, barrier, q, warm=0):
-    """One shard-parallel CPU worker: its own batches of the train ids, one
-    thread (the reference is single-threaded numpy; parallelism is across
-    processes)."""
+def _load_world(path, meta):
+    from oracle import codecs as oc
+    ld = lambda f: np.load(os.path.join(path, f), mmap_mode="r")  # noqa: E731
+    w = {"off": ld("off.npy"), "col": ld("col.npy"), "labels": ld("labels.npy"),
+         "train": ld("train.npy")}
+    if meta["kind"] == "vq":
+        codes = ld("codes.npy")
+        books = tuple(np.load(os.path.join(path, f"book{p}.npy")) for p in range(meta["parts"]))
+        w["decode"] = lambda r: oc.vq_decode(codes, books, meta["d"], meta["width"], r)
+    else:
+        payload = ld("payload.npy")
+        w["decode"] = lambda r: oc.sq_dequant_rows(payload, meta["n"], meta["d"], meta["k"],
+                                                   meta["e_min"], meta["e_max"], r)
+    return w
+
+
+def _spawn_worker(path, meta, cfg, wid, nsteps, warm, barrier, q):
     import torch
     from oracle import trainer as ot
     torch.set_num_threads(1)
-    c = _PAR
-    model, step = oracle_model(ot, c["d"], c["hidden"], c["classes"], c["fanouts"], c["agg"])
+    w = _load_world(path, meta)
+    model, step = oracle_model(ot, meta["d"], cfg["hidden"], cfg["classes"], cfg["fanouts"],
+                               cfg["agg"])
     opt = torch.optim.Adam(model.parameters(), lr=3e-3)
-    train = c["train"]
+
+    class H:  # what the oracle train functions read
+        row_offsets, col_indices = w["off"], w["col"]
+    batch, train = cfg["batch"], w["train"]
     nb = max(1, train.size // batch)
-    for i in range(warm):  # untimed warm-up batches
-        b = (wid * (nsteps + warm) + nsteps + i) % nb
-        step(model, opt, c["host"], c["labels"], train[b * batch:(b + 1) * batch], c["fanouts"],
-             batch, b, c["decode"])
+
+    def one(b):
+        step(model, opt, H, w["labels"], np.asarray(train[b * batch:(b + 1) * batch]),
+             cfg["fanouts"], batch, b, w["decode"])
+    for i in range(warm):
+        one((wid * (nsteps + warm) + nsteps + i) % nb)
     barrier.wait()
     t0 = time.perf_counter()
     for i in range(nsteps):
-        b = (wid * (nsteps + warm) + i) % nb
-        step(model, opt, c["host"], c["labels"], train[b * batch:(b + 1) * batch], c["fanouts"],
-             batch, b, c["decode"])
+        one((wid * (nsteps + warm) + i) % nb)
     q.put((wid, time.perf_counter() - t0))
 
 
-def cpu_parallel(sg, dc, fanouts, hidden, aggregator, batch, nsteps, workers=None, warm=0):
-    """Shard-parallel CPU run of the oracle port (P
-    processes over disjoint batches, P = host cores): returns (seeds,
-    wall seconds, workers)."""
+def cpu_parallel_from_dir(path, meta, cfg, nsteps, warm=0, workers=None, timeout=600.0):
+    """Run `workers` spawned oracle processes, each `nsteps` batches; returns
+    (seeds, wall seconds, workers) or None if they do not finish in time."""
     import multiprocessing as mp
-    host, labels, decode = _host_world(sg, dc)
     workers = workers or os.cpu_count() or 1
-    _PAR.update(host=host, labels=labels, decode=decode, d=dc.d, hidden=hidden,
-                classes=sg.num_classes, fanouts=fanouts, agg=aggregator, train=sg.train_ids)
-    ctx = mp.get_context("fork")
+    ctx = mp.get_context("spawn")
     barrier, q = ctx.Barrier(workers + 1), ctx.Queue()
-    procs = [ctx.Process(target=_par_worker, args=(w, nsteps, batch, barrier, q, warm))
+    procs = [ctx.Process(target=_spawn_worker,
+                         args=(path, meta, cfg, w, nsteps, warm, barrier, q), daemon=True)
              for w in range(workers)]
     for pr in procs:
         pr.start()
-    barrier.wait()
-    t0 = time.perf_counter()
-    done = [q.get(timeout=3600) for _ in range(workers)]
-    wall = time.perf_counter() - t0
+    try:
+        barrier.wait(timeout=timeout)
+        t0 = time.perf_counter()
+        done = [q.get(timeout=timeout) for _ in range(workers)]
+        wall = time.perf_counter() - t0
+    except Exception:
+        for pr in procs:
+            pr.kill()
+        return None
     for pr in procs:
-        pr.join(60)
-    _PAR.clear()
-    return workers * nsteps * batch, max(wall, max(t for _, t in done)), workers
+        pr.join(30)
+    return workers * nsteps * cfg["batch"], max(wall, max(t for _, t in done)), workers
+
+
+def cpu_parallel(sg, dc, fanouts, hidden, aggregator, batch, nsteps, warm=0):
+    import shutil
+    import tempfile
+    host = sg.graph.to_host()
+    base = "/dev/shm" if os.path.isdir("/dev/shm") else None
+    path = tempfile.mkdtemp(prefix="fgb_cpu_", dir=base)
+    try:
+        meta = save_host_world(host, sg.labels.cpu().numpy(), sg.train_ids, dc, path)
+        cfg = {"hidden": hidden, "classes": sg.num_classes, "fanouts": tuple(fanouts),
+               "agg": aggregator, "batch": batch}
+        return cpu_parallel_from_dir(path, meta, cfg, nsteps, warm)
+    finally:
+        shutil.rmtree(path, ignore_errors=True)
 
 
 def cpu_baseline(sg, dc, fanouts, hidden, budget_s=20.0, batch=128, aggregator="mean"):
@@ -454,54 +512,107 @@ def cpu_baseline(sg, dc, fanouts, hidden, budget_s=20.0, batch=128, aggregator="
     (pipeline.py:185-222 restated) + numpy decoder + CPU fp32 SAGE step."""
     import torch
     from oracle import trainer as ot
-    # probe one single-threaded batch to size the parallel run to ~budget_s
     host, labels, decode = _host_world(sg, dc)
     model, train_step = oracle_model(ot, dc.d, hidden, sg.num_classes, fanouts, aggregator)
     opt = torch.optim.Adam(model.parameters(), lr=3e-3)
+    # size the shard-parallel run from one single-threaded batch (~budget_s)
     nt = torch.get_num_threads()
     torch.set_num_threads(1)
     t0 = time.perf_counter()
     train_step(model, opt, host, labels, sg.train_ids[:batch], fanouts, batch, 0, decode)
     per = time.perf_counter() - t0
     torch.set_num_threads(nt)
-    nsteps = max(1, int(budget_s / max(per, 1e-3)))
-    seeds, wall, workers = cpu_parallel(sg, dc, fanouts, hidden, aggregator, batch, nsteps)
-    return {"value": round(seeds / wall, 2), "unit": "seeds/s", "cores": workers,
-            "kind": "port",
-            "sample": f"{workers} processes x {nsteps} mini-batches of {batch} seeds, fanouts "
-                      f"{list(fanouts)}, {wall:.1f} s wall (oracle port: numpy sampler/decoder "
-                      f"+ CPU fp32 model step, one thread per process, disjoint batches)"}
+    par = cpu_parallel(sg, dc, fanouts, hidden, aggregator, batch,
+                       max(1, int(budget_s / max(per, 1e-3))), warm=1)
+    if par is not None:
+        seeds, wall, workers = par
+        return {"value": round(seeds / wall, 2), "unit": "seeds/s", "cores": workers,
+                "kind": "port",
+                "sample": f"{workers} spawned processes x {seeds // workers // batch} "
+                          f"mini-batches of {batch} seeds, fanouts {list(fanouts)}, "
+                          f"{wall:.1f} s wall (oracle port, one thread each, disjoint batches)"}
+    seeds_done, t0, steps = 0, time.perf_counter(), 0
+    train = sg.train_ids
+    while True:
+        train_step(model, opt, host, labels, train[steps * batch:(steps + 1) * batch], fanouts,
+                   batch, steps, decode)
+        steps += 1
+        seeds_done += batch
+        if time.perf_counter() - t0 >= budget_s or steps * batch >= train.size:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": round(seeds_done / dt, 2), "unit": "seeds/s",
+            "cores": torch.get_num_threads(), "kind": "port",
+            "sample": f"{steps} mini-batches of {batch} seeds, fanouts {list(fanouts)}, "
+                      f"{dt:.1f} s (numpy sampler/decoder single-threaded, torch CPU "
+                      f"fp32 SAGE step on {torch.get_num_threads()} threads)"}
 
 
 def run_reference(args, rank, world, local):
-    """The reference arm: the CPU oracle port of the reference path, rank 0
-    only, on every host core: P = cpu_count processes over disjoint batches
-    (one thread each: the reference is single-threaded numpy).  One step =
-    every process trains one batch of --ref-batch seeds."""
+    """The reference arm: CPU oracle port, rank 0 only."""
     if rank != 0:
         return
     import torch
+    from oracle import trainer as ot
     dev = torch.device("cuda", local) if torch.cuda.is_available() else torch.device("cpu")
     if dev.type == "cuda":
         torch.cuda.set_device(dev)
     sg, dc, codec_desc, fanouts, bs, hidden = build_workload(args.config, dev, scale=args.scale)
-    batch = args.ref_batch
-    seeds, dt, workers = cpu_parallel(sg, dc, fanouts, hidden, aggregator_of(args.config), batch,
-                                      args.steps, warm=args.warmup)
-    v = seeds / dt
     agg = aggregator_of(args.config)
+    par = cpu_parallel(sg, dc, fanouts, hidden, agg, args.ref_batch, args.steps,
+                       warm=args.warmup)
+    if par is not None:  # every host core: one process per core over disjoint batches
+        seeds, dt, workers = par
+        v = seeds / dt
+        line = {"impl": "reference", "metric": "GraphSAGE train seeds/sec",
+                "value": round(v, 2), "unit": "seeds/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": round(dt * 1e3 / args.steps, 2),
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "f32", "data": "synthetic",
+                "config": {"workload": f"{args.config}-shape "
+                                       f"{dict(gcn='GCN', gat='GAT').get(agg, 'GraphSAGE')} "
+                                       f"{len(fanouts)}-layer fanout {list(fanouts)}, "
+                                       f"{codec_desc}",
+                           "per_step_seeds": args.ref_batch * workers,
+                           "parallelism": f"cpu x{workers} processes"},
+                "cpu_baseline": {"value": round(v, 2), "unit": "seeds/s", "cores": workers,
+                                 "kind": "port",
+                                 "sample": f"{args.steps} steps x {workers} processes x "
+                                           f"{args.ref_batch} seeds (oracle port, one thread "
+                                           f"per process)"},
+                "e2e": {"value": round(v, 2), "unit": "seeds/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+    host, labels, decode = _host_world(sg, dc)  # fallback: one process, all torch threads
+    torch.set_num_threads(os.cpu_count() or 1)
+    model, train_step = oracle_model(ot, dc.d, hidden, sg.num_classes, fanouts,
+                                     aggregator_of(args.config))
+    opt = torch.optim.Adam(model.parameters(), lr=3e-3)
+    batch = args.ref_batch
+    train = sg.train_ids
+
+    def one(i):
+        train_step(model, opt, host, labels, train[i * batch:(i + 1) * batch], fanouts, batch,
+                   i, decode)
+
+    for i in range(args.warmup):
+        one(i)
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        one(args.warmup + i)
+    dt = time.perf_counter() - t0
+    v = batch * args.steps / dt
     line = {"impl": "reference", "metric": "GraphSAGE train seeds/sec", "value": round(v, 2),
             "unit": "seeds/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(dt * 1e3 / args.steps, 2), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"{args.config}-shape "
-                                   f"{dict(gcn='GCN', gat='GAT').get(agg, 'GraphSAGE')} "
-                                   f"{len(fanouts)}-layer fanout {list(fanouts)}, {codec_desc}",
-                       "per_step_seeds": batch * workers, "parallelism": f"cpu x{workers}"},
-            "cpu_baseline": {"value": round(v, 2), "unit": "seeds/s", "cores": workers,
-                             "kind": "port",
-                             "sample": f"{args.steps} steps x {workers} processes x {batch} "
-                                       f"seeds (oracle port, one thread per process)"},
+            "config": {"workload": f"{args.config}-shape GraphSAGE {len(fanouts)}-layer fanout "
+                                   f"{list(fanouts)}, {codec_desc}",
+                       "per_step_seeds": batch, "parallelism": "cpu"},
+            "cpu_baseline": {"value": round(v, 2), "unit": "seeds/s",
+                             "cores": torch.get_num_threads(), "kind": "port",
+                             "sample": f"{args.steps} steps x {batch} seeds"},
             "e2e": {"value": round(v, 2), "unit": "seeds/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
