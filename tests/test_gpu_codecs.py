@@ -238,3 +238,58 @@ def test_kmeans_assign_tensor_core_matches_numpy(metric, w, k):
         alt = (1.0 - dots[np.flatnonzero(diff), got[diff]] if metric == "cosine"
                else dd[np.flatnonzero(diff), got[diff]])
         np.testing.assert_allclose(alt, want_cost[diff], rtol=1e-12, atol=1e-14)
+
+
+@pytest.mark.parametrize("k,d", [(8, 100), (4, 128), (3, 37), (1, 5)])
+def test_streaming_sqf1_device_load(tmp_path, k, d):
+    """SQF1 -> mmap -> pinned -> HBM in chunks (deviceio.load_sq_device, tiny
+    chunks to force many) gives the same device rows as the host loader."""
+    import torch
+    from paper_2207_14696_b200.deviceio import load_sq_device
+    r = np.random.default_rng(k * d)
+    x = (np.exp(r.normal(0, 1, (3001, d))) * r.choice([-1, 1], (3001, d))).astype(np.float32)
+    f = fg.FeatureMatrix(x)
+    c = fg.quantize_sq(f, fg.fit_sq(f, k))
+    path = str(tmp_path / "x.sqf")
+    fg.save_sq(c, path)
+    got = load_sq_device(path, chunk_bytes=4096)
+    want = fg.DeviceSqCodec.from_codec(fg.load_sq(path))
+    assert torch.equal(got.rows, want.rows)
+    assert got.params == want.params
+
+
+@pytest.mark.parametrize("w,L,d", [(4, 256, 100), (3, 300, 45)])
+def test_streaming_vqf1_device_load(tmp_path, w, L, d):
+    import torch
+    from paper_2207_14696_b200.deviceio import load_vq_device
+    r = np.random.default_rng(w + L)
+    if True:
+        x = r.standard_normal((2500, d)).astype(np.float32)
+        books = tuple(r.standard_normal((L, min(w, d - lo))).astype(np.float32)
+                      for lo in range(0, d, w))
+        c = fg.encode_vq(fg.FeatureMatrix(x), fg.VqCodec(fg.VqParams(w, L), d, books))
+    path = str(tmp_path / "x.vqf")
+    fg.save_vq(c, path)
+    got = load_vq_device(path, chunk_bytes=2048)
+    want = fg.DeviceVqCodec.from_codec(fg.load_vq(path))
+    assert torch.equal(got.rows, want.rows)
+    assert torch.equal(got.table, want.table)
+
+
+def test_streaming_csrg1_device_load(tmp_path):
+    import torch
+    from paper_2207_14696_b200 import formats
+    from paper_2207_14696_b200.deviceio import load_csrg_device
+    from paper_2207_14696_b200.synth import generate_graph
+    dg, _ = generate_graph(20_000, 10.0, 4, seed=2)
+    host = dg.to_host()
+    path = str(tmp_path / "g.csrg")
+    formats.write_csrg(path, host.n, host.row_offsets, host.col_indices, True)
+    got = load_csrg_device(path, chunk_bytes=10_000)
+    assert torch.equal(got.row_offsets, dg.row_offsets) and torch.equal(got.col_indices,
+                                                                         dg.col_indices)
+    raw = bytearray(open(path, "rb").read())
+    raw[formats.CSRG_HEADER.size + 8 * 5] = 0xFF  # corrupt an offset
+    open(path, "wb").write(bytes(raw))
+    with pytest.raises(fg.FormatError):
+        load_csrg_device(path)
