@@ -152,15 +152,23 @@ __device__ __forceinline__ void stage_load_src(const int32_t* __restrict__ src, 
     if (t < cnt) st.src[k] = __ldg(src + e0 + t);
   }
 }
+// pf_rows (optional): also prefetch each staged source's code row into L2,
+// so the next tile's row loads hit L2 instead of DRAM
 template <int NT>
 __device__ __forceinline__ void stage_store_src(int32_t* s_src, const int32_t* s_ip,
-                                                const Stage<NT>& st) {
+                                                const Stage<NT>& st,
+                                                const uint8_t* pf_rows = nullptr,
+                                                int64_t pf_stride = 0) {
   const int32_t cnt = s_ip[kTD] - s_ip[0];
   if (cnt > kSrcCap) return;
 #pragma unroll
   for (int k = 0; k < Stage<NT>::kPer; ++k) {
     const int t = threadIdx.x + k * NT;
-    if (t < cnt) s_src[t] = st.src[k];
+    if (t < cnt) {
+      s_src[t] = st.src[k];
+      if (pf_rows)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(pf_rows + (int64_t)st.src[k] * pf_stride));
+    }
   }
 }
 
@@ -170,7 +178,9 @@ __device__ __forceinline__ void tile_pipeline(const int32_t* __restrict__ indptr
                                               const int32_t* __restrict__ src, int64_t max_dst,
                                               int64_t ntiles, int32_t* s_ip0, int32_t* s_ip1,
                                               int32_t* s_src0, int32_t* s_src1, F&& compute,
-                                              int64_t tile0 = -1, int64_t step = -1) {
+                                              int64_t tile0 = -1, int64_t step = -1,
+                                              const uint8_t* pf_rows = nullptr,
+                                              int64_t pf_stride = 0) {
   // default: CTA b walks tiles b, b + grid, ...; part-sliced kernels pass
   // their own (first tile, stride) so one slice's CTAs cover every tile
   if (step < 0) step = gridDim.x;
@@ -182,7 +192,7 @@ __device__ __forceinline__ void tile_pipeline(const int32_t* __restrict__ indptr
   __syncthreads();
   stage_load_src<NT>(src, s_ip0, st);
   if (tile + step < ntiles) stage_load_ip<NT>(indptr, tile + step, max_dst, st2);
-  stage_store_src<NT>(s_src0, s_ip0, st);
+  stage_store_src<NT>(s_src0, s_ip0, st, pf_rows, pf_stride);
   if (tile + step < ntiles) stage_store_ip<NT>(s_ip1, st2, indptr, tile + step, max_dst);
   __syncthreads();
   bool odd = false;
@@ -196,7 +206,7 @@ __device__ __forceinline__ void tile_pipeline(const int32_t* __restrict__ indptr
     if (has_nn) stage_load_ip<NT>(indptr, tile + 2 * step, max_dst, st2);
     compute(tile, ip_c, src_c);
     __syncthreads();
-    if (has_n) stage_store_src<NT>(src_n, ip_n, st);
+    if (has_n) stage_store_src<NT>(src_n, ip_n, st, pf_rows, pf_stride);
     if (has_nn) stage_store_ip<NT>(ip_c, st2, indptr, tile + 2 * step, max_dst);
     __syncthreads();
     odd = !odd;
@@ -598,7 +608,7 @@ k_vq_mean8_fast(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
                 const int32_t* __restrict__ indptr, const int32_t* __restrict__ src,
                 const int64_t* __restrict__ ndst_dev, int64_t max_dst,
                 __nv_bfloat16* __restrict__ out, int64_t ld, int slice_parts, int nslices,
-                const float* __restrict__ ew = nullptr) {
+                const float* __restrict__ ew = nullptr, int pf = 0) {
   // G parts per thread: G * W = 32 fp32 accumulators.  Part slicing: when
   // the whole bf16 codebook does not fit the smem budget (MAG240M-shape:
   // 96 parts x 256 x 8 = 393 KB), CTA b serves parts [s*SP, s*SP+SP) of
@@ -689,7 +699,7 @@ k_vq_mean8_fast(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
           if (col0 + j < d) o[j] = __float2bfloat16_rn((j & 1 ? hi2(acc[j / 2]) : lo2(acc[j / 2])) * inv);
       }
     }
-  }, tile0, tstep);
+  }, tile0, tstep, pf ? rows + part_base : nullptr, stride);
   if (!waited) bulk_wait(&s_mbar);
 }
 
@@ -1180,10 +1190,14 @@ int launch_vq_w(const fg_codec_desc* c, const int32_t* indptr, const int32_t* sr
       const int64_t per_slice = std::max<int64_t>(
           1, min64(ntiles, (int64_t)sm_count() * 3 * pct / 100 / ns));
       const int grid = (int)(per_slice * ns);
+      static const int pf = [] {  // L2 prefetch of the next tile's code rows (default on)
+        const char* e = getenv("FG_FUSED_PREFETCH");
+        return e ? atoi(e) : 1;
+      }();
       kern<<<grid, kFastThreads, fast_smem, st>>>(c->rows, c->d, c->row_stride,
                                               (const __nv_bfloat16*)c->table_lp, c->length,
                                               c->num_parts, indptr, src, ndst, max_dst,
-                                              (__nv_bfloat16*)out, ld, sp, ns, ew);
+                                              (__nv_bfloat16*)out, ld, sp, ns, ew, pf);
       FG_LAUNCH_CHECK();
       return FG_OK;
     }
