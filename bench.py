@@ -161,13 +161,16 @@ def build_workload(cfg_name, device, seed=0, scale=1.0):
     torch.cuda.synchronize()
     t1 = time.perf_counter()
     n, d = sg.graph.n, SHAPES[shape]["d"]
+    import torch.distributed as dist
+    # N>1: rows encoded per rank block + one all-gather, VQ parts fitted round-robin
+    group = dist.group.WORLD if dist.is_initialized() and dist.get_world_size() > 1 else None
     if codec_spec[0] == "vq":
         dc, host_codec = build_vq_codec(n, d, codec_spec[1], codec_spec[2], labels=sg.labels,
-                                        num_classes=sg.num_classes, seed=seed)
+                                        num_classes=sg.num_classes, seed=seed, group=group)
         codec_desc = f"vq width {codec_spec[1]} length {codec_spec[2]} cosine (CR {32 * codec_spec[1] / math.log2(codec_spec[2]):.0f})"
     else:
         dc = build_sq_codec(n, d, codec_spec[1], labels=sg.labels, num_classes=sg.num_classes,
-                            seed=seed)
+                            seed=seed, group=group)
         codec_desc = f"sq k={codec_spec[1]} (CR {32 / codec_spec[1]:.0f})"
     torch.cuda.synchronize()
     t2 = time.perf_counter()

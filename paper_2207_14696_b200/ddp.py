@@ -63,3 +63,65 @@ def max_over_ranks(value: float, device=None) -> float:
     t = torch.tensor([value], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+# -- sharded preprocessing (SURVEY.md §8e "Preprocessing"): each rank encodes
+# a contiguous row block of the codec, one all-gather assembles the replica;
+# VQ parts are fitted round-robin and their codebooks broadcast by the owner.
+
+def world_of(group=None) -> tuple[int, int]:
+    if not dist.is_initialized():
+        return 0, 1
+    return dist.get_rank(group), dist.get_world_size(group)
+
+
+def row_block(n: int, rank: int, world: int) -> tuple[int, int, int]:
+    """Rows [r0, r1) encoded by ``rank``; every block is ``chunk`` rows long
+    except the tail (the gather buffer is padded to world*chunk rows)."""
+    chunk = -(-n // world) if n else 0
+    r0 = min(rank * chunk, n)
+    return r0, min(r0 + chunk, n), chunk
+
+
+def padded_rows(n: int, stride: int, world: int, device) -> torch.Tensor:
+    """Row buffer with room for world equal blocks; the codec uses [:n]."""
+    _, _, chunk = row_block(n, 0, world)
+    return torch.zeros((max(chunk * world, n), stride), dtype=torch.uint8, device=device)
+
+
+def allgather_rows_(buf: torch.Tensor, n: int, group=None) -> torch.Tensor:
+    """Every rank filled its own block of ``buf`` (padded_rows); afterwards
+    every rank holds all n rows.  NCCL gathers in place over NVLink; gloo (CPU
+    tests, several ranks on one device) stages through host memory."""
+    rank, world = world_of(group)
+    if world == 1:
+        return buf
+    _, _, chunk = row_block(n, rank, world)
+    if chunk == 0:
+        return buf
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(buf[:chunk * world], buf[rank * chunk:(rank + 1) * chunk],
+                                    group=group)
+        return buf
+    host = buf[:chunk * world].cpu()
+    outs = list(host.view(world, chunk, -1).unbind(0))
+    dist.all_gather(outs, host[rank * chunk:(rank + 1) * chunk].clone(), group=group)
+    buf[:chunk * world].copy_(host)
+    return buf
+
+
+def part_owner(part: int, world: int) -> int:
+    return part % world
+
+
+def share_parts(books: list, stats: list, group=None) -> None:
+    """Owner of part p (p % W) broadcasts its fitted codebook and stats."""
+    rank, world = world_of(group)
+    if world == 1:
+        return
+    for p in range(len(books)):
+        obj = [(books[p], stats[p]) if part_owner(p, world) == rank else None]
+        src = part_owner(p, world)
+        dist.broadcast_object_list(obj, src=dist.get_global_rank(group, src) if group else src,
+                                   group=group)
+        books[p], stats[p] = obj[0]

@@ -139,10 +139,13 @@ def synth_feature_rows(ids, d: int, *, kind: int = 3, seed: int = 0,
 
 
 def build_sq_codec(n: int, d: int, k: int, *, labels, num_classes: int, seed: int = 0,
-                   chunk_rows: int = 1 << 20, kind: int = 3):
+                   chunk_rows: int = 1 << 20, kind: int = 3, group=None):
     """fit_sq over the row-addressable matrix (streamed: the exact reference
-    fit, sq.py:84-111, never needs the whole matrix), then chunked encode."""
-    from .sq import DeviceSqCodec, fit_sq_stream
+    fit, sq.py:84-111, never needs the whole matrix), then chunked encode.
+    With a process group each rank encodes its own row block and one
+    all-gather assembles the replica (ddp.allgather_rows_)."""
+    from . import ddp
+    from .sq import DeviceSqCodec, fit_sq_stream, sq_row_stride
     dev = labels.device
 
     def chunks():
@@ -152,21 +155,37 @@ def build_sq_codec(n: int, d: int, k: int, *, labels, num_classes: int, seed: in
                                  num_classes=num_classes, device=dev)
 
     params = fit_sq_stream(chunks, k, device=dev)
-    dc = DeviceSqCodec.empty(params, n, d, dev)
-    r0 = 0
-    for x in chunks():
-        dc.encode_rows_(x, r0)
-        r0 += x.shape[0]
+    rank, world = ddp.world_of(group)
+    if world == 1:
+        dc = DeviceSqCodec.empty(params, n, d, dev)
+        r0 = 0
+        for x in chunks():
+            dc.encode_rows_(x, r0)
+            r0 += x.shape[0]
+        return dc
+    buf = ddp.padded_rows(n, sq_row_stride(d, k), world, dev)
+    dc = DeviceSqCodec(params, n, d, buf[:n])
+    b0, b1, _ = ddp.row_block(n, rank, world)
+    for r0 in range(b0, b1, chunk_rows):
+        m = min(chunk_rows, b1 - r0)
+        dc.encode_rows_(synth_features(m, d, row0=r0, kind=kind, seed=seed, labels=labels,
+                                       num_classes=num_classes, device=dev), r0)
+    ddp.allgather_rows_(buf, n, group)
     return dc
 
 
 def build_vq_codec(n: int, d: int, width: int, length: int, *, labels, num_classes: int,
                    seed: int = 0, chunk_rows: int = 1 << 20, kind: int = 3,
-                   max_iters: int = 50, restarts: int = 4, metric: str = "cosine"):
+                   max_iters: int = 50, restarts: int = 4, metric: str = "cosine",
+                   group=None):
     """fit_vq on the reference's default uniform sample (min(1, 1e6/n)),
-    then chunked device encode of every row."""
-    from .vq import DeviceVqCodec, VqParams, _fit_from_sample
+    then chunked device encode of every row.  With a process group, parts are
+    fitted round-robin across ranks and rows encoded per rank block, then
+    all-gathered."""
+    from . import ddp
+    from .vq import DeviceVqCodec, VqParams, _fit_from_sample, vq_row_stride
     dev = labels.device
+    rank, world = ddp.world_of(group)
     p = VqParams(width, length, metric=metric, kmeans_max_iters=max_iters, restarts=restarts,
                  seed=seed)
     frac = min(1.0, 1_000_000 / n)
@@ -183,17 +202,26 @@ def build_vq_codec(n: int, d: int, width: int, length: int, *, labels, num_class
     import sys
     import time
     t0 = time.perf_counter()
-    codec = _fit_from_sample(sample.double(), p, d, 32, rng)
+    codec = _fit_from_sample(sample.double(), p, d, 32, rng, group=group)
     del sample
     torch.cuda.synchronize()
     t1 = time.perf_counter()
-    dc = DeviceVqCodec.empty(p, d, codec.codebooks, n, dev)
-    for r0 in range(0, n, chunk_rows):
-        m = min(chunk_rows, n - r0)
+    if world == 1:
+        dc = DeviceVqCodec.empty(p, d, codec.codebooks, n, dev)
+        b0, b1, buf = 0, n, None
+    else:
+        buf = ddp.padded_rows(n, vq_row_stride(len(codec.codebooks), p.bits_per_code), world,
+                              dev)
+        dc = DeviceVqCodec(p, d, codec.codebooks, n, buf[:n], dev)
+        b0, b1, _ = ddp.row_block(n, rank, world)
+    for r0 in range(b0, b1, chunk_rows):
+        m = min(chunk_rows, b1 - r0)
         x = full[r0:r0 + m] if full is not None else synth_features(
             m, d, row0=r0, kind=kind, seed=seed, labels=labels, num_classes=num_classes,
             device=dev)
         dc.encode_rows_(x, r0)
+    if buf is not None:
+        ddp.allgather_rows_(buf, n, group)
     torch.cuda.synchronize()
     print(f"[synth] vq codec: fit_vq on {rows} sample rows {t1 - t0:.1f} s, encode {n} rows "
           f"{time.perf_counter() - t1:.1f} s", file=sys.stderr, flush=True)

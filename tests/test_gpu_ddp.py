@@ -70,3 +70,48 @@ def test_two_rank_trainer_stays_in_sync():
     assert out[0][2] and out[1][2]           # per-rank batches = reference sampler
     assert out[0][3] and out[1][3]           # identical parameters after 3 steps
     assert np.isfinite([o[4] for o in out]).all() and out[0][4] != out[1][4]  # own shards
+
+
+def _prep_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    from paper_2207_14696_b200.synth import build_sq_codec, build_vq_codec, generate_graph
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        n, C = 7_001, 5
+        _, labels = generate_graph(n, 8.0, C, seed=2)
+        out = {}
+        for g in (None, dist.group.WORLD):
+            sq = build_sq_codec(n, 40, 4, labels=labels, num_classes=C, seed=2,
+                                chunk_rows=1000, group=g)
+            vq, host = build_vq_codec(n, 24, 4, 16, labels=labels, num_classes=C, seed=2,
+                                      chunk_rows=1000, max_iters=8, restarts=2, group=g)
+            out[g is None] = (sq.rows.cpu().numpy().copy(), sq.params,
+                              vq.rows.cpu().numpy().copy(), [b.copy() for b in host.codebooks])
+        a, b = out[True], out[False]
+        q.put((rank, np.array_equal(a[0], b[0]) and a[1] == b[1],
+               np.array_equal(a[2], b[2]) and all(np.array_equal(x, y) for x, y in zip(a[3], b[3]))))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_preprocessing_matches_single_process():
+    """Row-block encode + all-gather and round-robin VQ part fitting give the
+    single-process codec bit for bit (SURVEY.md §8e preprocessing)."""
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_prep_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=600) for _ in range(2))
+    for p in procs:
+        p.join(120)
+    assert all(o[1] for o in out), "SQ rows differ"
+    assert all(o[2] for o in out), "VQ rows/codebooks differ"

@@ -13,6 +13,7 @@ import paper_2207_14696_b200 as fg
 from paper_2207_14696_b200 import _native as N
 from paper_2207_14696_b200 import ddp, formats
 from paper_2207_14696_b200.sampler import rng_block_from_numpy, rng_block_to_numpy
+from paper_2207_14696_b200.vq import VqParams, _fit_from_sample
 from paper_2207_14696_b200.sq import sq_decode_table, sq_thresholds, _quantile_lerp, \
     _order_stat_ranks
 from oracle import codecs as oc
@@ -231,6 +232,20 @@ def test_ddp_sharding_helpers():
     assert ddp.rank_seed(0, 0, 1, 2) == 1 and ddp.rank_seed(5, 1, 0, 4) == 24
 
 
+def _vq_sample():
+    import torch
+    return torch.randn(50, 10, generator=torch.Generator().manual_seed(0), dtype=torch.float64)
+
+
+def _fake_fit(owner):
+    """Stand-in for the GPU k-means (no kernels on CPU): depends on the part's
+    points and its restart seeds, records which rank fitted it."""
+    def fit(pts, p, capacity, seeds):
+        v = float(seeds[0] % 997) + float(pts.sum())
+        return np.full((2, pts.shape[1]), v, np.float32), {"owner": owner}
+    return fit
+
+
 def _gloo_worker(rank, world, port, q):
     import torch
     import torch.distributed as dist
@@ -242,7 +257,19 @@ def _gloo_worker(rank, world, port, q):
         ddp.average_flat_(flat)
         mx = ddp.max_over_ranks(0.5 * (rank + 1))
         shard = ddp.shard_ids(np.arange(11), rank, world)
-        q.put((rank, nb, flat.tolist(), mx, shard.tolist()))
+        # sharded preprocessing: row blocks + all-gather, round-robin VQ parts
+        n, stride = 11, 3
+        buf = ddp.padded_rows(n, stride, world, "cpu")
+        r0, r1, _ = ddp.row_block(n, rank, world)
+        buf[r0:r1] = (torch.arange(r0, r1)[:, None] * 7 + torch.arange(stride)).to(torch.uint8)
+        ddp.allgather_rows_(buf, n)
+        rows = buf[:n].tolist()
+        c = _fit_from_sample(_vq_sample(), VqParams(3, 4, metric="euclidean"), 10, 32,
+                             np.random.default_rng(5), group=dist.group.WORLD,
+                             fit_part=_fake_fit(rank))
+        books = [b.tolist() for b in c.codebooks]
+        owners = [st["owner"] for st in c.fit_stats]
+        q.put((rank, nb, flat.tolist(), mx, shard.tolist(), rows, books, owners))
     finally:
         dist.destroy_process_group()
 
@@ -265,6 +292,12 @@ def test_ddp_gloo_world2():
     assert out[0][2] == [1.5] * 5 and out[1][2] == [1.5] * 5
     assert out[0][3] == 1.0
     assert out[0][4] == [0, 2, 4, 6, 8, 10] and out[1][4] == [1, 3, 5, 7, 9]
+    want = [[(r * 7 + j) for j in range(3)] for r in range(11)]
+    assert out[0][5] == want and out[1][5] == want
+    single = _fit_from_sample(_vq_sample(), VqParams(3, 4, metric="euclidean"), 10, 32,
+                              np.random.default_rng(5), fit_part=_fake_fit(0))
+    assert out[0][6] == out[1][6] == [b.tolist() for b in single.codebooks]
+    assert out[0][7] == out[1][7] == [p % 2 for p in range(4)]   # parts round-robin
 
 
 def test_measured_report_semantics_follow_the_reference():
