@@ -235,6 +235,16 @@ int fg_block_mean_fwd(const uint16_t* h_src, int64_t h_dim,
                       const int64_t* num_dst_dev, int64_t max_dst,
                       uint16_t* out, int64_t out_ld, int relu_in,
                       const float* edge_w, void* cuda_stream);
+/* fg_block_mean_fwd with relu_in, additionally writing each source row's
+ * ReLU mask as packed bits (relu_bits [rows, h_dim/8], bit t of byte c =
+ * h[row, 8c+t] > 0) for every source the block reads -- the mask input of
+ * fg_block_mean_wgrad's mask_kind 2, produced while the rows are loaded
+ * anyway instead of by a separate pass. */
+int fg_block_mean_fwd_bits(const uint16_t* h_src, int64_t h_dim,
+                           const int32_t* indptr, const int32_t* src_local,
+                           const int64_t* num_dst_dev, int64_t max_dst,
+                           uint16_t* out, int64_t out_ld, const float* edge_w,
+                           uint8_t* relu_bits, void* cuda_stream);
 int fg_block_mean_bwd(const uint16_t* grad_out, int64_t h_dim,
                       const int32_t* indptr, const int32_t* src_local,
                       const int64_t* num_dst_dev, int64_t max_dst,

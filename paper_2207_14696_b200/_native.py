@@ -60,6 +60,7 @@ _SIGS = {
                                     vp]),
     "fg_block_edge_weights": (ci, [ci, vp, vp, vp, vp, vp, i64, vp, vp]),
     "fg_block_mean_fwd": (ci, [vp, i64, vp, vp, vp, i64, vp, i64, ci, vp, vp]),
+    "fg_block_mean_fwd_bits": (ci, [vp, i64, vp, vp, vp, i64, vp, i64, vp, vp, vp]),
     "fg_block_mean_bwd": (ci, [vp, i64, vp, vp, vp, i64, vp, vp]),
     "fg_f32_to_bf16": (ci, [vp, i64, vp, vp, vp]),
     "fg_block_transpose_scratch_bytes": (i64, [i64]),

@@ -38,12 +38,12 @@ __device__ __forceinline__ uint4 f32_to_bf16x8(const float* f) {
 
 // RELU: apply max(0, .) to the source rows as they are loaded (the SAGE
 // activation of the previous layer, fused so it never makes its own pass).
-template <bool RELU, bool WT>
+template <bool RELU, bool WT, bool MB = false>
 __global__ void __launch_bounds__(256)
 k_block_mean_fwd(const uint16_t* __restrict__ h, int64_t H, const int32_t* __restrict__ indptr,
                  const int32_t* __restrict__ srcl, const int64_t* __restrict__ ndst_dev,
                  int64_t max_dst, uint16_t* __restrict__ out, int64_t out_ld,
-                 const float* __restrict__ ew) {
+                 const float* __restrict__ ew, uint8_t* __restrict__ mbits = nullptr) {
   const int64_t live = live_count(ndst_dev, max_dst);
   const int64_t chunks = H >> 3;
   const int64_t ochunks = out_ld >> 3;  // out_ld = H, or H + 8 with a ones column
@@ -79,6 +79,12 @@ k_block_mean_fwd(const uint16_t* __restrict__ h, int64_t H, const int32_t* __res
           if (e + u < e1) {
             float f[8];
             bf16x8_to_f32(q[u], f);
+            if constexpr (MB) {  // the source's ReLU mask byte (bit t = feature 8c+t) for
+              uint32_t b = 0;    // the backward's edge-tiled dW (fg_wgrad.cu, mask_kind 2)
+#pragma unroll
+              for (int j = 0; j < 8; ++j) b |= (f[j] > 0.f ? 1u : 0u) << j;
+              mbits[(int64_t)sl[u] * chunks + c] = (uint8_t)b;
+            }
             if constexpr (WT) {
 #pragma unroll
               for (int j = 0; j < 8; ++j) acc[j] = fmaf(wgt[u], RELU ? fmaxf(f[j], 0.f) : f[j], acc[j]);
@@ -148,6 +154,27 @@ __global__ void k_f32_to_bf16(const float* __restrict__ in, int64_t n8,
 using namespace fg;
 
 extern "C" {
+
+int fg_block_mean_fwd_bits(const uint16_t* h, int64_t H, const int32_t* indptr,
+                           const int32_t* srcl, const int64_t* ndst, int64_t max_dst,
+                           uint16_t* out, int64_t out_ld, const float* edge_w,
+                           uint8_t* relu_bits, void* s) {
+  FG_CHECK_ARG(H % 8 == 0 && relu_bits != nullptr, "hidden dim must be a multiple of 8");
+  if (out_ld == 0) out_ld = H;
+  FG_CHECK_ARG(out_ld == H || out_ld == H + 8, "out_ld must be H or H + 8 (ones column)");
+  if (max_dst == 0) return FG_OK;
+  const int64_t total = max_dst * (out_ld / 8);
+  const int grid = grid_for(total, 256);
+  cudaStream_t st = as_stream(s);
+  if (edge_w)
+    k_block_mean_fwd<true, true, true><<<grid, 256, 0, st>>>(h, H, indptr, srcl, ndst, max_dst,
+                                                              out, out_ld, edge_w, relu_bits);
+  else
+    k_block_mean_fwd<true, false, true><<<grid, 256, 0, st>>>(h, H, indptr, srcl, ndst, max_dst,
+                                                               out, out_ld, nullptr, relu_bits);
+  FG_LAUNCH_CHECK();
+  return FG_OK;
+}
 
 int fg_block_mean_fwd(const uint16_t* h, int64_t H, const int32_t* indptr, const int32_t* srcl,
                       const int64_t* ndst, int64_t max_dst, uint16_t* out, int64_t out_ld,

@@ -19,6 +19,7 @@ seed ids in and the loss out.
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -224,8 +225,14 @@ class SageTrainer:
         self.agg = alloc_aggregate(self.caps[L - 1], codec.d, cfg.agg_dtype, self.device)
         w0 = self.model.lins[0].weight
         self.wgrad_scratch = None
+        self.relu_bits = None
         if fused:
             self.wgrad_scratch = wgrad_scratch(w0.shape[0], w0.shape[1], self.device)
+            # h0's packed ReLU mask, written by the first block mean's forward
+            # (FG_RELU_BITS=0: the wgrad kernel reads h0 itself)
+            if os.environ.get("FG_RELU_BITS", "1") != "0":
+                self.relu_bits = torch.empty((self.caps[L - 1], w0.shape[0] // 8),
+                                             dtype=torch.uint8, device=self.device)
         self.graph = None
         self.graphs = {}
         self._primed, self._next = False, 0
@@ -281,8 +288,15 @@ class SageTrainer:
                 l = L - 2 - i  # block feeding layer i+1
                 H = h.shape[1]
                 a = torch.empty((caps[l], H + 8), dtype=torch.bfloat16, device=self.device)
-                N.call("fg_block_mean_fwd", N.ptr(h), H, N.ptr(sb.indptr[l]), N.ptr(sb.local[l]),
-                       N.ptr(sb.n_nodes[l]), caps[l], N.ptr(a), H + 8, 1, N.ptr(ew[l]), s)
+                if fused and i == 0 and self.relu_bits is not None:
+                    # h0's ReLU mask as bits for the edge-tiled dW0 (mask_kind 2)
+                    N.call("fg_block_mean_fwd_bits", N.ptr(h), H, N.ptr(sb.indptr[l]),
+                           N.ptr(sb.local[l]), N.ptr(sb.n_nodes[l]), caps[l], N.ptr(a), H + 8,
+                           N.ptr(ew[l]), N.ptr(self.relu_bits), s)
+                else:
+                    N.call("fg_block_mean_fwd", N.ptr(h), H, N.ptr(sb.indptr[l]),
+                           N.ptr(sb.local[l]), N.ptr(sb.n_nodes[l]), caps[l], N.ptr(a), H + 8,
+                           1, N.ptr(ew[l]), s)
                 ins.append(a)
         logits = hs[-1]
         ld = logits.shape[1]
@@ -301,7 +315,8 @@ class SageTrainer:
             if fused and i == 1:
                 N.call("fg_block_mean_wgrad", N.ptr(din), H, N.ptr(sb.indptr[l]),
                        N.ptr(sb.local[l]), N.ptr(sb.n_nodes[l]), caps[l], N.ptr(ew[l]),
-                       N.ptr(hs[0]), 1, H,
+                       *((N.ptr(self.relu_bits), 2) if self.relu_bits is not None
+                         else (N.ptr(hs[0]), 1)), H,
                        N.ptr(self.agg), self.agg.shape[1], N.ptr(dW[0]),
                        N.ptr(self.wgrad_scratch), self.wgrad_scratch.numel() * 4, s)
                 break

@@ -448,3 +448,32 @@ def test_hidden_block_weighted_fwd_bwd_and_wgrad():
     term = g[seg, :H].float() * ew[:, None] * (h.detach()[sl.long()].float() > 0)
     want = term.to(torch.bfloat16).float().t() @ x[sl.long()].float()
     assert (dw - want).abs().max().item() <= 1e-3 * want.abs().max().item() + 1e-4
+
+
+@pytest.mark.parametrize("weighted", [False, True])
+def test_block_mean_fwd_emits_relu_bits(weighted):
+    """fg_block_mean_fwd_bits: same output as fg_block_mean_fwd(relu), and the
+    packed ReLU mask of every source the block reads equals relu_mask_bits."""
+    from paper_2207_14696_b200 import _native as N
+    from paper_2207_14696_b200.aggregate import relu_mask_bits
+    rng = np.random.default_rng(11 + weighted)
+    H, n_src, n_dst, max_dst, fan = 256, 3000, 900, 950, 7
+    counts, indptr, src = _block(n_src, n_dst, max_dst, fan, rng, zero_frac=0.1)
+    dev = "cuda"
+    ip = torch.from_numpy(indptr).to(dev)
+    local = torch.from_numpy(src).to(dev)
+    nd = torch.tensor([n_dst], device=dev)
+    h = torch.randn(n_src, H, device=dev).to(torch.bfloat16)
+    ew = torch.rand(max(src.size, 1), device=dev) if weighted else None
+    a = torch.empty((max_dst, H + 8), dtype=torch.bfloat16, device=dev)
+    b = torch.empty_like(a)
+    bits = torch.zeros((n_src, H // 8), dtype=torch.uint8, device=dev)
+    s = N.stream_handle()
+    N.call("fg_block_mean_fwd", N.ptr(h), H, N.ptr(ip), N.ptr(local), N.ptr(nd), max_dst,
+           N.ptr(a), H + 8, 1, N.ptr(ew), s)
+    N.call("fg_block_mean_fwd_bits", N.ptr(h), H, N.ptr(ip), N.ptr(local), N.ptr(nd), max_dst,
+           N.ptr(b), H + 8, N.ptr(ew), N.ptr(bits), s)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    used = torch.unique(local.long())
+    assert torch.equal(bits[used], relu_mask_bits(h)[used])
