@@ -245,6 +245,23 @@ int fg_block_mean_fwd_bits(const uint16_t* h_src, int64_t h_dim,
                            const int64_t* num_dst_dev, int64_t max_dst,
                            uint16_t* out, int64_t out_ld, const float* edge_w,
                            uint8_t* relu_bits, void* cuda_stream);
+/* Fused input-layer projection + first hidden block mean (training
+ * forward, tcgen05): out[v] = sum_{e in v} w_e relu(x[l_e] . w0^T) with
+ * w_e = edge_w[e] or 1/cnt_v, as bf16 [max_dst, out_ld] (+ [1, 0 x 7] bias
+ * column when out_ld = h_dim + 8; rows past *num_dst_dev get zeros + bias),
+ * and the packed ReLU mask of every source read (relu_bits, the mask_kind 2
+ * input of fg_block_mean_wgrad).  x: [rows, p] bf16 (the aggregated input
+ * features with their ones column), w0: [h_dim, p] bf16.  h = x w0^T never
+ * reaches HBM.  Shapes: fg_input_block_mean_supported(h_dim, p, fanout)
+ * (h_dim 128 or 256, p % 16 == 0, p <= 256, picks per destination <= fanout
+ * <= 128). */
+int fg_input_block_mean_supported(int64_t h_dim, int64_t p, int64_t fanout);
+int fg_input_block_mean_fwd(const uint16_t* x, int64_t p, const uint16_t* w0,
+                            int64_t h_dim, const int32_t* indptr,
+                            const int32_t* src_local, const int64_t* num_dst_dev,
+                            int64_t max_dst, int64_t fanout, const float* edge_w,
+                            uint16_t* out, int64_t out_ld, uint8_t* relu_bits,
+                            void* cuda_stream);
 int fg_block_mean_bwd(const uint16_t* grad_out, int64_t h_dim,
                       const int32_t* indptr, const int32_t* src_local,
                       const int64_t* num_dst_dev, int64_t max_dst,

@@ -61,6 +61,9 @@ _SIGS = {
     "fg_block_edge_weights": (ci, [ci, vp, vp, vp, vp, vp, i64, vp, vp]),
     "fg_block_mean_fwd": (ci, [vp, i64, vp, vp, vp, i64, vp, i64, ci, vp, vp]),
     "fg_block_mean_fwd_bits": (ci, [vp, i64, vp, vp, vp, i64, vp, i64, vp, vp, vp]),
+    "fg_input_block_mean_supported": (ci, [i64, i64, i64]),
+    "fg_input_block_mean_fwd": (ci, [vp, i64, vp, i64, vp, vp, vp, i64, i64, vp, vp, i64, vp,
+                                     vp]),
     "fg_block_mean_bwd": (ci, [vp, i64, vp, vp, vp, i64, vp, vp]),
     "fg_f32_to_bf16": (ci, [vp, i64, vp, vp, vp]),
     "fg_block_transpose_scratch_bytes": (i64, [i64]),

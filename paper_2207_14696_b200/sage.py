@@ -233,6 +233,15 @@ class SageTrainer:
             if os.environ.get("FG_RELU_BITS", "1") != "0":
                 self.relu_bits = torch.empty((self.caps[L - 1], w0.shape[0] // 8),
                                              dtype=torch.uint8, device=self.device)
+        # forward: input projection fused with the first block mean
+        # (fg_infwd.cu) when the shape allows -- mean aggregator only (products
+        # step 0.258 -> 0.247 ms; GCN's weighted variant measured no gain);
+        # FG_INFWD=0 keeps GEMM + block mean, FG_INFWD=2 forces it for GCN too
+        mode = os.environ.get("FG_INFWD", "1")
+        self.infwd = bool(fused and self.relu_bits is not None and self.explicit
+                          and (mode == "2" or (mode == "1" and cfg.aggregator == "mean"))
+                          and N.lib().fg_input_block_mean_supported(
+                              w0.shape[0], w0.shape[1], cfg.fanouts[L - 2]))
         self.graph = None
         self.graphs = {}
         self._primed, self._next = False, 0
@@ -281,6 +290,18 @@ class SageTrainer:
         ins, hs = [self.agg], []
         fused = self.wgrad_scratch is not None
         for i in range(L):
+            if i == 0 and self.infwd:
+                # h0 = agg W0^T and its block mean in one tcgen05 kernel (h0
+                # stays on chip; its ReLU bits go to the dW0 kernel)
+                l, H = L - 2, W[0].shape[0]
+                a = torch.empty((caps[l], H + 8), dtype=torch.bfloat16, device=self.device)
+                N.call("fg_input_block_mean_fwd", N.ptr(self.agg), self.agg.shape[1],
+                       N.ptr(W[0]), H, N.ptr(sb.indptr[l]), N.ptr(sb.local[l]),
+                       N.ptr(sb.n_nodes[l]), caps[l], self.cfg.fanouts[l], N.ptr(ew[l]),
+                       N.ptr(a), H + 8, N.ptr(self.relu_bits), s)
+                hs.append(None)
+                ins.append(a)
+                continue
             h = torch.mm(ins[i], W[i].t())
             hs.append(h)
 
@@ -309,7 +330,7 @@ class SageTrainer:
             torch.mm(dh.t(), ins[i], out_dtype=torch.float32, out=dW[i])
             if i == 0:
                 break
-            H = hs[i - 1].shape[1]
+            H = W[i - 1].shape[0]
             din = torch.mm(dh, W[i][:, :H])
             l = L - 1 - i  # block feeding layer i
             if fused and i == 1:

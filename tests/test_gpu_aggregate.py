@@ -477,3 +477,49 @@ def test_block_mean_fwd_emits_relu_bits(weighted):
     assert torch.equal(a, b)
     used = torch.unique(local.long())
     assert torch.equal(bits[used], relu_mask_bits(h)[used])
+
+
+@pytest.mark.parametrize("H,P,fan,weighted,n_dst", [(256, 112, 10, False, 700),
+                                                    (256, 144, 15, True, 700),
+                                                    (128, 48, 5, False, 700),
+                                                    (256, 112, 1, False, 700),
+                                                    (128, 256, 40, True, 700),
+                                                    (256, 112, 10, False, 20000),
+                                                    (256, 112, 10, True, 20000)])
+def test_input_block_mean_fwd_tcgen05(H, P, fan, weighted, n_dst):
+    """Fused h0 = x W0^T + ReLU block mean (tcgen05) against torch fp32 on the
+    same bf16 operands; ReLU bits against the fp32 signs (away from 0); dead
+    rows get zeros + the bias column."""
+    from paper_2207_14696_b200 import _native as N
+    assert N.lib().fg_input_block_mean_supported(H, P, fan)
+    rng = np.random.default_rng(H + P + fan)
+    n_src, max_dst = 3000, n_dst + 60   # n_dst 20000: several tiles per CTA
+    counts, indptr, src = _block(n_src, n_dst, max_dst, fan, rng, zero_frac=0.1)
+    dev = "cuda"
+    ip = torch.from_numpy(indptr).to(dev)
+    local = torch.from_numpy(src).to(dev)
+    x = torch.randn(n_src, P, device=dev).to(torch.bfloat16)
+    w0 = (torch.randn(H, P, device=dev) / P ** 0.5).to(torch.bfloat16)
+    ew = torch.rand(max(src.size, 1), device=dev) if weighted else None
+    out = torch.full((max_dst, H + 8), float("nan"), dtype=torch.bfloat16, device=dev)
+    bits = torch.zeros((n_src, H // 8), dtype=torch.uint8, device=dev)
+    N.call("fg_input_block_mean_fwd", N.ptr(x), P, N.ptr(w0), H, N.ptr(ip), N.ptr(local),
+           N.ptr(torch.tensor([n_dst], device=dev)), max_dst, fan, N.ptr(ew), N.ptr(out), H + 8,
+           N.ptr(bits), N.stream_handle())
+    torch.cuda.synchronize()
+    h = x.float() @ w0.float().t()
+    dst = torch.repeat_interleave(torch.arange(n_dst, device=dev),
+                                  torch.from_numpy(counts).long().to(dev))
+    l = local.long()
+    w = ew[:src.size] if weighted else 1.0 / torch.from_numpy(counts).float().to(dev)[dst]
+    ref = torch.zeros(max_dst, H, device=dev).index_add_(0, dst, h[l].clamp_min(0) * w[:, None])
+    got = out[:, :H].float()
+    assert torch.allclose(got, ref, atol=2e-2, rtol=1e-2), (got - ref).abs().max()
+    assert (got[n_dst:] == 0).all()
+    assert (out[:, H].float() == 1).all() and (out[:, H + 1:] == 0).all()
+    used = torch.unique(l)
+    hb = h[used] > 0
+    sh = torch.arange(8, device=dev, dtype=torch.uint8)
+    gbits = ((bits[used][..., None] >> sh) & 1).view(-1, H).bool()
+    clear = h[used].abs() > 1e-3
+    assert torch.equal(gbits[clear], hb[clear])

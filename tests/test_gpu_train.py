@@ -162,6 +162,33 @@ def test_explicit_step_matches_autograd_step(hidden, vq):
     assert torch.equal(a.flat_bf16, a.flat_param.to(torch.bfloat16))
 
 
+@pytest.mark.parametrize("aggregator", ["mean", "gcn"])
+def test_fused_input_forward_matches_gemm_path(aggregator):
+    """The tcgen05 input projection + first block mean (fg_input_block_mean_fwd,
+    h0 kept on chip, its ReLU bits feeding dW0) gives the GEMM + block-mean
+    step's loss and gradients on the same batch."""
+    dg, labels, dc, train, val = _small_world(vq=True, d=100)
+    cfg = TrainConfig(fanouts=(15, 10, 5), batch_size=512, hidden=256, use_graph=False,
+                      pipeline=False, aggregator=aggregator)
+    ts = []
+    for infwd in (True, False):
+        torch.manual_seed(0)
+        t = SageTrainer(dg, dc, labels, 8, cfg)
+        assert t.relu_bits is not None
+        t.infwd = infwd
+        t.begin_epoch(train, 0)
+        t.step(0)
+        ts.append(t)
+    a, b = ts
+    assert abs(float(a.loss_buf) - float(b.loss_buf)) < 1e-2 * abs(float(b.loss_buf))
+    off = 0
+    for lin in a.model.lins:
+        n = lin.weight.numel()
+        ga, gb = a.flat_grad[off:off + n], b.flat_grad[off:off + n]
+        assert ((ga - gb).norm() / gb.norm()).item() < 2e-2
+        off += n
+
+
 @pytest.mark.parametrize("graphed", [False, True])
 def test_pipelined_sampling_matches_serial(graphed):
     """Sampling batch b+1 on a side stream while batch b trains (two sampler
