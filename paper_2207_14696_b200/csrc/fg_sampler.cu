@@ -470,8 +470,8 @@ k_layer_fixup(const int64_t* __restrict__ off, const int32_t* __restrict__ col,
   const int64_t b = INT64_MAX - bad;
   const int64_t nominal = 2 * (int64_t)f - 1;
   const int64_t delta = (int64_t)ws.used[b] - nominal;
-  const int64_t i = blockIdx.x * (int64_t)kSampThreads + threadIdx.x;
-  if (i > b && i < live) {
+  for (int64_t i = b + 1 + blockIdx.x * (int64_t)kSampThreads + threadIdx.x; i < live;
+       i += (int64_t)gridDim.x * kSampThreads) {
     const int32_t u = nodes[i];
     const int64_t deg = off[u + 1] - off[u];
     const int32_t po = indptr[i];
@@ -648,7 +648,11 @@ int fg_sample_layer(const int64_t* row_offsets, const int32_t* col_indices, int6
 #undef FG_SAMPLE_F
   }
   FG_LAUNCH_CHECK();
-  k_layer_fixup<<<(unsigned)nt, kSampThreads, 0, st>>>(row_offsets, col_indices, nodes,
+  // grid-stride over the nodes after the first rejection: a few CTAs per SM
+  // (the common no-rejection case is one flag read per CTA; a capacity-sized
+  // grid of immediately-exiting CTAs cost ~9 us per MAG-scale layer)
+  const unsigned fix_grid = (unsigned)min64(nt, (int64_t)sm_count() * 4);
+  k_layer_fixup<<<fix_grid, kSampThreads, 0, st>>>(row_offsets, col_indices, nodes,
                                                        num_nodes_dev, max_nodes, fanout, rng_dev, w,
                                                        indptr, picks, max_picks, num_picks_dev,
                                                        err_flag);
