@@ -91,7 +91,7 @@ def padded_rows(n: int, stride: int, world: int, device) -> torch.Tensor:
 
 def allgather_rows_(buf: torch.Tensor, n: int, group=None) -> torch.Tensor:
     """Every rank filled its own block of ``buf`` (padded_rows); afterwards
-    every rank holds all n rows.  NCCL gathers in place over NVLink; gloo (CPU
+    every rank holds all n rows.  NCCL gathers over NVLink; gloo (CPU
     tests, several ranks on one device) stages through host memory."""
     rank, world = world_of(group)
     if world == 1:
@@ -100,8 +100,9 @@ def allgather_rows_(buf: torch.Tensor, n: int, group=None) -> torch.Tensor:
     if chunk == 0:
         return buf
     if dist.get_backend(group) == "nccl":
-        dist.all_gather_into_tensor(buf[:chunk * world], buf[rank * chunk:(rank + 1) * chunk],
-                                    group=group)
+        # the local block as a separate input (no aliasing of the output)
+        mine = buf[rank * chunk:(rank + 1) * chunk].clone()
+        dist.all_gather_into_tensor(buf[:chunk * world], mine, group=group)
         return buf
     host = buf[:chunk * world].cpu()
     outs = list(host.view(world, chunk, -1).unbind(0))
