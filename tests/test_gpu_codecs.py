@@ -293,3 +293,19 @@ def test_streaming_csrg1_device_load(tmp_path):
     open(path, "wb").write(bytes(raw))
     with pytest.raises(fg.FormatError):
         load_csrg_device(path)
+
+
+def test_batched_kmeanspp_matches_sequential():
+    """_kmeanspp_batched (all (part, restart) seedings advanced together, one
+    host sync per step) draws the same centroids as the per-job _kmeanspp
+    with the same Generators -- including jobs of different row counts."""
+    import torch
+    from paper_2207_14696_b200.vq import _kmeanspp, _kmeanspp_batched
+    g = torch.Generator(device="cuda").manual_seed(3)
+    pts = [torch.randn(n, 4, device="cuda", dtype=torch.float64, generator=g)
+           for n in (5000, 3700, 5000)]
+    seeds = [11, 12, 13]
+    seq = [_kmeanspp(p, 32, np.random.default_rng(s)) for p, s in zip(pts, seeds)]
+    bat = _kmeanspp_batched([(p, np.random.default_rng(s)) for p, s in zip(pts, seeds)], 32)
+    for a, b in zip(seq, bat):
+        assert torch.equal(a, b)
