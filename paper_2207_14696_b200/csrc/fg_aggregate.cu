@@ -578,11 +578,15 @@ __global__ void k_softmax_ce(const LT* __restrict__ logits, int C, int64_t ld, i
   for (int64_t r = r0; r < r1; ++r) acc += *(volatile float*)(row_loss + r);
   part[threadIdx.x] = acc;
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {  // fixed-shape tree (deterministic): 8 partials per lane, then xor
     float t = 0.f;
-    for (int i = 0; i < (int)blockDim.x; ++i) t += part[i];
-    *loss_out = t;
-    *done = 0u;
+    for (int i = threadIdx.x; i < (int)blockDim.x; i += 32) t += part[i];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (threadIdx.x == 0) {
+      *loss_out = t;
+      *done = 0u;
+    }
   }
 }
 
