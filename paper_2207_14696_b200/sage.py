@@ -189,7 +189,8 @@ class SageTrainer:
                                                aggregator=cfg.aggregator))
             # high priority: the latency-bound sampler kernels take SMs as soon as
             # the wide training kernels free them
-            self.side = torch.cuda.Stream(self.device, priority=-1)
+            self.side = torch.cuda.Stream(self.device,
+                                          priority=int(os.environ.get("FG_SIDE_PRIORITY", "-1")))
         self.caps = self.sampler.caps
         # flat gradient buffer: one all-reduce per step
         # one flat fp32 buffer each for params, grads and Adam moments: a
