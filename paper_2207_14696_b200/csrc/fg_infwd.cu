@@ -69,6 +69,7 @@ struct Meta {
   int32_t ip[kIfRows + 2]; // tile indptr window [D + 1]
   float inv[kIfRows];      // flush scale per destination
   uint32_t fmask[4];       // bit t of word c: edge 32c+t ends its destination
+  uint32_t emask[4];       // bit t of word c: destination 32c+t has no edges
 };
 
 template <bool WT>
@@ -148,7 +149,13 @@ k_input_block_mean_fwd(const uint16_t* __restrict__ x, int P, const uint16_t* __
       bool last = false;
       if (r < ne) {
         l = __ldg(local + e0 + r);
-        while (m.ip[j + 1] - e0 <= r) ++j;
+        // destination of edge r: binary search over the tile's window
+        int lo = 0, hi = nd;
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (m.ip[mid] - e0 <= r) lo = mid; else hi = mid;
+        }
+        j = lo;
         last = r + 1 == m.ip[j + 1] - e0;
         if (WT) m.w[r] = __ldg(ew + e0 + r);
       }
@@ -156,10 +163,13 @@ k_input_block_mean_fwd(const uint16_t* __restrict__ x, int P, const uint16_t* __
       m.j[r] = j;
       const unsigned fm = __ballot_sync(0xFFFFFFFFu, last);
       if (lane == 0) m.fmask[warp] = fm;
+      int cnt = 1;
       if (r < nd) {  // mean: scale the plain sum at the flush; weighted: sum as is
-        const int cnt = m.ip[r + 1] - m.ip[r];
+        cnt = m.ip[r + 1] - m.ip[r];
         m.inv[r] = WT ? 1.f : (cnt ? 1.0f / (float)cnt : 0.f);
       }
+      const unsigned em = __ballot_sync(0xFFFFFFFFu, cnt == 0);
+      if (lane == 0) m.emask[warp] = em;
     }
     __syncthreads();
   };
@@ -266,8 +276,9 @@ k_input_block_mean_fwd(const uint16_t* __restrict__ x, int P, const uint16_t* __
               wbits[lane];
         __syncwarp();
       }
-      for (int j = 0; j < nd; ++j)  // destinations without edges
-        if (m.ip[j + 1] == m.ip[j]) orow[(int64_t)j * out_ld] = 0;
+      for (int q = 0; q * 32 < nd; ++q)  // destinations without edges
+        for (uint32_t em = m.emask[q]; em; em &= em - 1)
+          orow[(int64_t)(q * 32 + __ffs(em) - 1) * out_ld] = 0;
     }
     if (out_ld > H && tid < nd)  // bias column block [1, 0, ..., 0]
       reinterpret_cast<uint4*>(out + (v0 + tid) * out_ld + H)[0] = make_uint4(0x3F80u, 0u, 0u, 0u);
