@@ -1,31 +1,44 @@
 """Benchmark: GraphSAGE train seeds/sec on compressed features (BASELINE.json).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config products|arxiv|papers100m|mag240m]
+                    [--config papers100m|products|arxiv|mag240m|products-gcn|...]
 
-Default workload (N=1): BASELINE configs[1] — synthetic ogbn-products-shape
-graph (2,449,029 nodes, avg degree ~50, 100-dim class-conditional features),
-3-layer GraphSAGE, fanouts [15,10,5], batch 1024, VQ codebooks of 256 entries
-(width 4, cosine, CR 16).  A step = one full training step on one batch of
-seeds: sample (device PCG64) -> fused gather-dequant-mean -> bf16 SAGE
-fwd/bwd -> all-reduce (N>1) -> Adam, replayed from one CUDA graph.
+Default workload: BASELINE config C, the one the metric's "seeds/sec at
+1/2/4/8 B200" is quoted on -- a synthetic ogbn-papers100M-shape graph
+(111,059,956 nodes, ~3.2e9 stored entries, 128-dim class-conditional
+features, 4-bit SQ), 3-layer GraphSAGE, fanouts [15,10,5], 1024 seeds per
+rank per step.  A step = one full training step on one batch: sample (device
+PCG64) -> fused gather-dequant-mean -> bf16 SAGE fwd/bwd -> all-reduce (N>1)
+-> Adam, replayed from one CUDA graph.
 
-Prints ONE JSON line (rank 0).  ``value`` is device-timed with CUDA events,
-seeds already resident in HBM, L2 flushed between steps; ``e2e`` is the same
-step through the public API with the seed ids copied from pinned host memory
-and the loss read back every step.  ``--impl reference`` times the CPU oracle
-port of the reference path (numpy sampler + decoder restating pipeline.py /
-vq.py / sq.py, plus a CPU fp32 PyTorch SAGE step) on the host cores.
+Prints ONE JSON line (rank 0).  ``value``: K steps device-timed with CUDA
+events, seeds resident in HBM, L2 flushed between steps, max over ranks;
+``e2e``: the same steps through the public API with the seed ids copied from
+pinned host memory and the loss read back every step; ``epoch``: one whole
+epoch (begin_epoch's host permutation + upload included) on the wall clock.
+
+``--gpus N`` (N > 1) without a torchrun environment re-launches itself under
+``torch.distributed.run`` with N ranks (NCCL, one GPU each).
+
+``--impl reference`` times the reference's own CPU implementation of the path
+(SURVEY.md §8(d)): the unmodified ``featgrind`` from ``baseline/_ref``
+(sample_batches + dequantize_sq of each batch's frontier, loader-only: the
+reference has no trainer) on every host core, over the SAME world -- graph,
+labels, split and SQ payload rebuilt bit-identically on the CPU by
+oracle/world.py (this process never loads the product library).
 """
 
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
+import shutil
+import socket
 import statistics
+import subprocess
 import sys
+import tempfile
 import threading
 import time
 
@@ -34,17 +47,28 @@ import numpy as np
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
+# BASELINE.json configs.  Shapes (nodes, dim, avg degree, classes, train
+# split) mirror paper_2207_14696_b200/synth.py SHAPES (tests check they are
+# equal); kept here so the reference arm needs no product import.
+SHAPES = {
+    "arxiv": dict(n=169_343, d=128, avg_deg=13.7, classes=40, train=90_941),
+    "products": dict(n=2_449_029, d=100, avg_deg=50.5, classes=47, train=196_615),
+    "papers100m": dict(n=111_059_956, d=128, avg_deg=29.1, classes=172, train=1_207_179),
+    "mag240m": dict(n=244_160_499, d=768, avg_deg=27.9, classes=153, train=1_112_392),
+}
 CONFIGS = {
-    # name: (shape, codec, fanouts, batch, hidden)
+    # name: (shape, codec, fanouts, batch, hidden[, aggregator])
+    "papers100m": ("papers100m", ("sq", 4), (15, 10, 5), 1024, 256),
     "products": ("products", ("vq", 4, 256), (15, 10, 5), 1024, 256),
     "arxiv": ("arxiv", ("sq", 8), (10, 5), 1024, 256),
-    "papers100m": ("papers100m", ("sq", 4), (15, 10, 5), 1024, 256),
     "mag240m": ("mag240m", ("vq", 8, 256), (15, 10, 5), 1024, 256),
     # BASELINE config E: aggregator variants through the fused gather path
     "products-gcn": ("products", ("sq", 8), (15, 10, 5), 1024, 256, "gcn"),
     "products-sq8": ("products", ("sq", 8), (15, 10, 5), 1024, 256),
     "products-gat": ("products", ("sq", 8), (15, 10, 5), 1024, 256, "gat"),
 }
+DEFAULT_CONFIG = "papers100m"
+METRIC = "GraphSAGE train seeds/sec"
 
 
 def aggregator_of(cfg_name):
@@ -52,20 +76,48 @@ def aggregator_of(cfg_name):
     return spec[5] if len(spec) > 5 else "mean"
 
 
+def shape_of(cfg_name, scale=1.0):
+    s = dict(SHAPES[CONFIGS[cfg_name][0]])
+    s["n"] = max(1000, int(s["n"] * scale))
+    s["train"] = max(1, int(s["train"] * scale))
+    return s
+
+
+def codec_desc(cfg_name):
+    c = CONFIGS[cfg_name][1]
+    if c[0] == "vq":
+        import math
+        return f"vq width {c[1]} length {c[2]} cosine (CR {32 * c[1] / math.log2(c[2]):.0f})"
+    return f"sq k={c[1]} (CR {32 // c[1]})"
+
+
+def workload_config(cfg_name, nnz, world, scale=1.0):
+    """The ``config`` object of the JSON line -- built the same way by both
+    arms from the workload alone."""
+    shape, _, fanouts, bs, hidden = CONFIGS[cfg_name][:5]
+    s = shape_of(cfg_name, scale)
+    agg = aggregator_of(cfg_name)
+    return {"workload": f"{shape}-shape {dict(gcn='GCN', gat='GAT').get(agg, 'GraphSAGE')} "
+                        f"{len(fanouts)}-layer fanout {list(fanouts)}, {codec_desc(cfg_name)}",
+            "nodes": s["n"], "edges_stored": int(nnz), "feature_dim": s["d"],
+            "fanouts": list(fanouts), "global_batch": bs * world, "per_rank_batch": bs,
+            "hidden": hidden, "train_ids": s["train"], "parallelism": f"dp{world}"}
+
+
 def committed_traffic(config):
-    """dram bytes per launch of the fused kernel from the committed ncu
-    capture of this workload (profiles/<round>/fused_<config>_summary.json,
-    written by tools/summarize_profiles.py), or None."""
+    """dram bytes per launch of the fused kernel from the newest committed ncu
+    --set full capture of this workload (profiles/<round>/fused_<config>_
+    summary.json, tools/summarize_profiles.py), and its file, or (None, None)."""
     import glob
-    best = None
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    best = (None, None)
     for f in sorted(glob.glob(os.path.join(REPO, "profiles", "*", f"fused_{config}_summary.json"))):
         try:
             k = json.load(open(f))["kernels"][0]
             rd = float(k["dram__bytes_read.sum"][0].replace(",", ""))
             wr = float(k["dram__bytes_write.sum"][0].replace(",", ""))
-            best = int(rd * scale[k["dram__bytes_read.sum"][1]] +
-                       wr * scale[k["dram__bytes_write.sum"][1]])
+            best = (int(rd * scale[k["dram__bytes_read.sum"][1]] +
+                        wr * scale[k["dram__bytes_write.sum"][1]]), os.path.relpath(f, REPO))
         except Exception:
             continue
     return best
@@ -74,9 +126,9 @@ def committed_traffic(config):
 def gather_ceiling(row_bytes):
     """Measured random-row gather throughput (rows + 8 B index per row) for
     the nearest probed row size, 7 GB table (tools/gather_probe.py,
-    profiles/*/gather_probe.json), or None.  A uniformly random gather of
-    small rows is bounded by DRAM sector/activation rate, far below the
-    sequential copy peak; this is the practical ceiling for the fused kernel."""
+    profiles/*/gather_probe.json), or None: a uniformly random gather of
+    small rows is bounded by the DRAM sector/activation rate, far below the
+    sequential copy peak."""
     import glob
     fs = sorted(glob.glob(os.path.join(REPO, "profiles", "*", "gather_probe.json")))
     if not fs:
@@ -93,8 +145,8 @@ def load_peaks():
     if os.path.exists(p):
         with open(p) as fh:
             d = json.load(fh)
-        return float(d["hbm_gbs"]), "measured"
-    return 6650.0, "fallback"
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
 
 
 class ClockSampler:
@@ -150,11 +202,23 @@ class ClockSampler:
                 "reasons": sorted(self.reasons)}
 
 
+def world_dir(prefix):
+    """A scratch directory for a host world, on tmpfs when it has room."""
+    for base in ("/dev/shm", None):
+        if base and not os.path.isdir(base):
+            continue
+        try:
+            return tempfile.mkdtemp(prefix=prefix, dir=base)
+        except OSError:
+            continue
+    raise RuntimeError("no scratch directory for the host world")
+
+
 # ------------------------------------------------------------------ setup
 
 def build_workload(cfg_name, device, seed=0, scale=1.0):
     import torch
-    from paper_2207_14696_b200.synth import SHAPES, build_sq_codec, build_vq_codec, make_shape
+    from paper_2207_14696_b200.synth import build_sq_codec, build_vq_codec, make_shape
     shape, codec_spec, fanouts, bs, hidden = CONFIGS[cfg_name][:5]
     t0 = time.perf_counter()
     sg = make_shape(shape, seed=seed, scale=scale, device=device)
@@ -165,20 +229,18 @@ def build_workload(cfg_name, device, seed=0, scale=1.0):
     # N>1: rows encoded per rank block + one all-gather, VQ parts fitted round-robin
     group = dist.group.WORLD if dist.is_initialized() and dist.get_world_size() > 1 else None
     if codec_spec[0] == "vq":
-        dc, host_codec = build_vq_codec(n, d, codec_spec[1], codec_spec[2], labels=sg.labels,
-                                        num_classes=sg.num_classes, seed=seed, group=group)
-        codec_desc = f"vq width {codec_spec[1]} length {codec_spec[2]} cosine (CR {32 * codec_spec[1] / math.log2(codec_spec[2]):.0f})"
+        dc, _ = build_vq_codec(n, d, codec_spec[1], codec_spec[2], labels=sg.labels,
+                               num_classes=sg.num_classes, seed=seed, group=group)
     else:
         dc = build_sq_codec(n, d, codec_spec[1], labels=sg.labels, num_classes=sg.num_classes,
                             seed=seed, group=group)
-        codec_desc = f"sq k={codec_spec[1]} (CR {32 / codec_spec[1]:.0f})"
     torch.cuda.synchronize()
     t2 = time.perf_counter()
     print(f"[bench] {cfg_name}: graph n={sg.graph.n} nnz={sg.graph.nnz} built in {t1 - t0:.1f} s, "
-          f"codec ({codec_desc}) in {t2 - t1:.1f} s, "
+          f"codec ({codec_desc(cfg_name)}) in {t2 - t1:.1f} s, "
           f"{torch.cuda.max_memory_allocated(device) / 2**30:.1f} GiB peak", file=sys.stderr,
           flush=True)
-    return sg, dc, codec_desc, fanouts, bs, hidden
+    return sg, dc, fanouts, bs, hidden
 
 
 def flush_l2(buf):
@@ -197,7 +259,7 @@ def run_ours(args, rank, world, local):
 
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
-    sg, dc, codec_desc, fanouts, bs, hidden = build_workload(args.config, dev, scale=args.scale)
+    sg, dc, fanouts, bs, hidden = build_workload(args.config, dev, scale=args.scale)
     pg = dist.group.WORLD if world > 1 else None
     agg_kind = aggregator_of(args.config)
     if agg_kind == "gat":
@@ -224,7 +286,6 @@ def run_ours(args, rank, world, local):
     # ---- timed: K steps, seeds resident, L2 flushed between steps
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
-    l0 = N.lib().fg_launch_count()
     with ClockSampler(local) as clk:
         for i in range(args.steps):
             b = args.warmup + i
@@ -269,6 +330,21 @@ def run_ours(args, rank, world, local):
         e.synchronize()
         e2e_ms += s.elapsed_time(e)
     e2e_ms = ddp.max_over_ranks(e2e_ms, dev)
+    # ---- one whole epoch on the wall clock (epoch 1: new permutation)
+    epoch = None
+    if not args.no_epoch:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        nb1 = tr.begin_epoch(sg.train_ids, 1)
+        for b in range(nb1):
+            tr.step(b)
+        torch.cuda.synchronize()
+        ep_s = ddp.max_over_ranks(time.perf_counter() - t0, dev)
+        epoch = {"seeds_per_s": round(nb1 * bs * world / ep_s, 1), "wall_s": round(ep_s, 4),
+                 "batches_per_rank": nb1, "includes": "begin_epoch (host permutation + "
+                 "upload) + every batch of the epoch, wall clock, max over ranks"}
     # ---- roofline: the fused gather-dequant-mean kernel, timed alone
     L = len(fanouts)
     row_bytes = dc.num_parts * dc.bits / 8 if hasattr(dc, "num_parts") else dc.d * dc.params.k / 8
@@ -298,9 +374,7 @@ def run_ours(args, rank, world, local):
             continue
         out_b = tr.agg.element_size()
         # algorithmic bytes: E code rows + int32 source ids, N_dst indptr
-        # entries + output rows (the padded rows past N_dst are zero-filled
-        # but not counted)
-        # (+4 B edge weight per pick for the weighted aggregators)
+        # entries + output rows (+4 B edge weight per pick when weighted)
         wb = 4 if agg_kind != "mean" else 0
         kbytes.append(E * (row_bytes + 4 + wb) + nd * (4 + dc.d * out_b))
     avg_ms = sum(kt) / len(kt)
@@ -308,11 +382,12 @@ def run_ours(args, rank, world, local):
     avg_bytes = sum(kbytes) / len(kbytes)
     peak, peak_kind = load_peaks()
     achieved = avg_bytes / (avg_ms * 1e-3) / 1e9
+    traffic, traffic_src = committed_traffic(args.config)
     seeds_per_step = bs * world
     value = seeds_per_step * args.steps / (t_ms * 1e-3)
     e2e = seeds_per_step * args.steps / (e2e_ms * 1e-3)
     result = {
-        "metric": "GraphSAGE train seeds/sec",
+        "metric": METRIC,
         "value": round(value, 1),
         "unit": "seeds/s",
         "n_gpus": world,
@@ -324,23 +399,19 @@ def run_ours(args, rank, world, local):
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic (planted-partition power-law graph, class-conditional features)",
-        "config": {"workload": f"{args.config}-shape "
-                               f"{dict(gcn='GCN', gat='GAT').get(agg_kind, 'GraphSAGE')} "
-                               f"{len(fanouts)}-layer "
-                               f"fanout {list(fanouts)}, {codec_desc}",
-                   "nodes": sg.graph.n, "edges_stored": sg.graph.nnz, "feature_dim": dc.d,
-                   "global_batch": seeds_per_step, "per_rank_batch": bs, "hidden": hidden,
-                   "parallelism": f"dp{world}", "l2": "flushed between steps (512 MB write)",
-                   "graph": "one CUDA graph per step"},
+        "config": workload_config(args.config, sg.graph.nnz, world, args.scale),
+        "timing": {"l2": "flushed between steps (512 MB write)",
+                   "graph": "one CUDA graph per step", "clock": "CUDA events, max over ranks"},
         "e2e": {"value": round(e2e, 1), "unit": "seeds/s",
                 "h2d_bytes_per_step": bs * 8, "d2h_bytes_per_step": 4},
+        "epoch": epoch,
         "gpu_launches": int(launches_per_step * args.steps),
         "roofline": {"kernel": ("fg_sq_gather_dequant / fg_vq_gather_decode" if agg_kind == "gat"
-                               else "fg_gather_dequant_mean (k_vq_mean8_fast / k_sq_mean)"),
+                               else "fg_gather_dequant_mean"),
                      "bound": "hbm",
                      "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "peak_kind": peak_kind,
-                     "traffic": committed_traffic(args.config),
+                     "traffic": traffic, "traffic_source": traffic_src,
                      "avg_launch_us": round(avg_ms * 1e3, 2),
                      "alg_bytes_per_launch": int(avg_bytes),
                      "random_gather_ceiling": ceiling,
@@ -349,308 +420,178 @@ def run_ours(args, rank, world, local):
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        result["cpu_baseline"] = cpu_baseline(sg, dc, fanouts, hidden, budget_s=args.cpu_budget,
-                                              aggregator=agg_kind)
+        try:
+            result["cpu_baseline"] = cpu_baseline(args, sg, dc, fanouts, bs)
+        except Exception as e:  # noqa: BLE001 - reported, never fatal to the GPU line
+            result["cpu_baseline"] = {"value": None, "unavailable": repr(e)[:300]}
     if rank == 0:
         print(json.dumps(result), flush=True)
 
 
 # ------------------------------------------------------- CPU baseline
 
-def _host_world(sg, dc):
-    """Host copies for the CPU oracle: CSR, labels, decoder over codes."""
-    host = sg.graph.to_host()
-    labels = sg.labels.cpu().numpy()
-    from oracle import codecs as oc
-    from paper_2207_14696_b200.vq import DeviceVqCodec
-    if isinstance(dc, DeviceVqCodec):
-        import torch
-        codes = torch.empty((dc.n, dc.num_parts), dtype=torch.int32, device=dc.rows.device)
-        # codes come back from the device rows via the reference layout
-        rows = dc.rows.cpu().numpy()
-        b = dc.bits
-        assert b == 8, "CPU baseline decoder supports 8-bit VQ codes"
-        codes = rows[:, :dc.num_parts].astype(np.int32)
-        books = dc.books_host
-        w = dc.params.width
-
-        def decode(r):
-            return oc.vq_decode(codes, books, dc.d, w, r)
-    else:
-        c = dc.to_codec()
-        p = c.params
-
-        def decode(r):
-            return oc.sq_dequant_rows(c.payload, c.n, c.d, p.k, p.e_min, p.e_max, r)
-    return host, labels, decode
-
-
-def oracle_model(ot, d, hidden, num_classes, fanouts, aggregator):
-    """CPU fp32 oracle model + one-batch train function for the aggregator."""
-    if aggregator == "gat":
-        def step(model, opt, host, labels, ids, fanouts, batch, seed, decode):
-            ot.gat_train_epoch(model, opt, host.row_offsets, host.col_indices, labels, ids,
-                               fanouts, batch, seed, decode)
-        return ot.OracleGat(d, hidden, num_classes, len(fanouts)), step
-
-    def step(model, opt, host, labels, ids, fanouts, batch, seed, decode):
-        ot.train_epoch(model, opt, host.row_offsets, host.col_indices, labels, ids, fanouts,
-                       batch, seed, decode, aggregator=aggregator)
-    return ot.OracleSage(d, hidden, num_classes, len(fanouts)), step
-
-
-# ------------------------------------------- shard-parallel CPU baseline
-# The reference is single-threaded numpy; its best case on a multi-core host
-# is P independent processes over disjoint batches (SURVEY.md §8d (ii)).
-# Workers are SPAWNED (a forked child of a process that already ran torch /
-# OpenMP can deadlock) and map the host world from .npy files (mmap, shared).
-
-def save_host_world(host, labels, train, dc, path):
-    """Host CSR, labels, train ids and the codec's host form as .npy files."""
-    from paper_2207_14696_b200.vq import DeviceVqCodec
-    meta = {"n": int(host.n), "d": int(dc.d)}
-    np.save(os.path.join(path, "off.npy"), np.asarray(host.row_offsets))
-    np.save(os.path.join(path, "col.npy"), np.asarray(host.col_indices))
-    np.save(os.path.join(path, "labels.npy"), np.asarray(labels))
-    np.save(os.path.join(path, "train.npy"), np.asarray(train))
-    if isinstance(dc, DeviceVqCodec):
-        rows = dc.rows.cpu().numpy()
-        np.save(os.path.join(path, "codes.npy"), rows[:, :dc.num_parts].astype(np.int32))
-        for p_, b in enumerate(dc.books_host):
-            np.save(os.path.join(path, f"book{p_}.npy"), np.asarray(b))
-        meta.update(kind="vq", width=int(dc.params.width), parts=int(dc.num_parts))
-    else:
-        c = dc.to_codec()
-        np.save(os.path.join(path, "payload.npy"), np.frombuffer(c.payload, np.uint8))
-        meta.update(kind="sq", k=int(c.params.k), e_min=float(c.params.e_min),
-                    e_max=float(c.params.e_max))
+def export_device_world(sg, dc, path):
+    """Our arm's device world as oracle/world.py files (CSR, labels, train
+    ids, the reference's continuous SQ payload): the CPU leg then times the
+    reference loader on exactly the data the GPU trained on."""
+    from paper_2207_14696_b200.sq import DeviceSqCodec
+    if not isinstance(dc, DeviceSqCodec):
+        raise RuntimeError("the reference loader baseline covers SQ workloads "
+                           "(dequantize_sq); VQ configs report no cpu_baseline")
+    host = sg.graph
+    host.row_offsets.cpu().numpy().tofile(os.path.join(path, "off.bin"))
+    host.col_indices.cpu().numpy().tofile(os.path.join(path, "col.bin"))
+    sg.labels.cpu().numpy().astype(np.int32).tofile(os.path.join(path, "labels.bin"))
+    np.asarray(sg.train_ids, np.int64).tofile(os.path.join(path, "train.bin"))
+    c = dc.to_codec()
+    np.frombuffer(c.payload, np.uint8).tofile(os.path.join(path, "payload.bin"))
+    meta = {"n": int(dc.n), "nnz": int(host.nnz), "d": int(dc.d), "k": int(c.params.k),
+            "e_min": float(c.params.e_min), "e_max": float(c.params.e_max),
+            "train": int(np.asarray(sg.train_ids).size), "seed": 0}
+    with open(os.path.join(path, "meta.json"), "w") as fh:
+        json.dump(meta, fh)
     return meta
 
 
-def _load_world(path, meta):
-    from oracle import codecs as oc
-    ld = lambda f: np.load(os.path.join(path, f), mmap_mode="r")  # noqa: E731
-    w = {"off": ld("off.npy"), "col": ld("col.npy"), "labels": ld("labels.npy"),
-         "train": ld("train.npy")}
-    if meta["kind"] == "vq":
-        codes = ld("codes.npy")
-        books = tuple(np.load(os.path.join(path, f"book{p}.npy")) for p in range(meta["parts"]))
-        w["decode"] = lambda r: oc.vq_decode(codes, books, meta["d"], meta["width"], r)
-    else:
-        payload = ld("payload.npy")
-        w["decode"] = lambda r: oc.sq_dequant_rows(payload, meta["n"], meta["d"], meta["k"],
-                                                   meta["e_min"], meta["e_max"], r)
-    return w
-
-
-def _spawn_worker(path, meta, cfg, wid, nsteps, warm, barrier, q):
-    import torch
-    from oracle import trainer as ot
-    torch.set_num_threads(1)
-    w = _load_world(path, meta)
-    model, step = oracle_model(ot, meta["d"], cfg["hidden"], cfg["classes"], cfg["fanouts"],
-                               cfg["agg"])
-    opt = torch.optim.Adam(model.parameters(), lr=3e-3)
-
-    class H:  # what the oracle train functions read
-        row_offsets, col_indices = w["off"], w["col"]
-    batch, train = cfg["batch"], w["train"]
-    nb = max(1, train.size // batch)
-
-    def one(b):
-        step(model, opt, H, w["labels"], np.asarray(train[b * batch:(b + 1) * batch]),
-             cfg["fanouts"], batch, b, w["decode"])
-    for i in range(warm):
-        one((wid * (nsteps + warm) + nsteps + i) % nb)
-    barrier.wait()
-    t0 = time.perf_counter()
-    for i in range(nsteps):
-        one((wid * (nsteps + warm) + i) % nb)
-    q.put((wid, time.perf_counter() - t0))
-
-
-def cpu_parallel_from_dir(path, meta, cfg, nsteps, warm=0, workers=None, timeout=600.0):
-    """Run `workers` spawned oracle processes, each `nsteps` batches; returns
-    (seeds, wall seconds, workers) or None if they do not finish in time."""
-    import multiprocessing as mp
-    workers = workers or os.cpu_count() or 1
-    ctx = mp.get_context("spawn")
-    barrier, q = ctx.Barrier(workers + 1), ctx.Queue()
-    procs = [ctx.Process(target=_spawn_worker,
-                         args=(path, meta, cfg, w, nsteps, warm, barrier, q), daemon=True)
-             for w in range(workers)]
-    for pr in procs:
-        pr.start()
+def cpu_baseline(args, sg, dc, fanouts, bs):
+    """The reference loader (featgrind.sample_batches + dequantize_sq of the
+    frontier) on every host core over our own world, bounded to ~cpu_budget
+    seconds of work."""
+    from oracle import loader as OL
+    path = world_dir("fgb_cpu_")
     try:
-        barrier.wait(timeout=timeout)
-        t0 = time.perf_counter()
-        done = [q.get(timeout=timeout) for _ in range(workers)]
-        wall = time.perf_counter() - t0
-    except Exception:
-        for pr in procs:
-            pr.kill()
-        return None
-    for pr in procs:
-        pr.join(30)
-    return workers * nsteps * cfg["batch"], max(wall, max(t for _, t in done)), workers
+        export_device_world(sg, dc, path)
+        probe = OL.run_pool(path, fanouts, bs, steps=1, warm=0, workers=1)
+        per = probe["wall_s"]
+        steps = max(1, int(args.cpu_budget / max(per, 1e-3)))
+        r = OL.run_pool(path, fanouts, bs, steps=steps, warm=1)
+    finally:
+        shutil.rmtree(path, ignore_errors=True)
+    info = OL.host_info()
+    return {"value": round(r["seeds_per_s"], 2), "unit": "seeds/s", "cores": r["workers"],
+            "kind": r["kind"],
+            "sample": f"{r['workers']} spawned processes x {r['steps']} batches of {bs} seeds "
+                      f"(featgrind.sample_batches {list(fanouts)} + dequantize_sq of the "
+                      f"frontier; loader only: the reference has no trainer), "
+                      f"{r['wall_s']:.1f} s wall, one thread each, over this run's world",
+            "host": info}
 
 
-def cpu_parallel(sg, dc, fanouts, hidden, aggregator, batch, nsteps, warm=0):
-    """None when the pool cannot run (no space for the world files, spawn
-    failure, timeout): callers fall back to the single-process timing."""
-    import shutil
-    import tempfile
-    host = sg.graph.to_host()
-    for base in ("/dev/shm", None):  # tmpfs first; /dev/shm may be small in containers
-        if base and not os.path.isdir(base):
-            continue
-        path = tempfile.mkdtemp(prefix="fgb_cpu_", dir=base)
-        try:
-            meta = save_host_world(host, sg.labels.cpu().numpy(), sg.train_ids, dc, path)
-            cfg = {"hidden": hidden, "classes": sg.num_classes, "fanouts": tuple(fanouts),
-                   "agg": aggregator, "batch": batch}
-            return cpu_parallel_from_dir(path, meta, cfg, nsteps, warm)
-        except Exception as e:  # noqa: BLE001 - any failure -> next base / fallback
-            print(f"[bench] shard-parallel CPU baseline unavailable under {base or 'tmp'}: "
-                  f"{e}", file=sys.stderr)
-        finally:
-            shutil.rmtree(path, ignore_errors=True)
-    return None
-
-
-def cpu_baseline(sg, dc, fanouts, hidden, budget_s=20.0, batch=128, aggregator="mean"):
-    """Oracle port of the reference path on the host cores: numpy sampler
-    (pipeline.py:185-222 restated) + numpy decoder + CPU fp32 SAGE step."""
-    import torch
-    from oracle import trainer as ot
-    host, labels, decode = _host_world(sg, dc)
-    model, train_step = oracle_model(ot, dc.d, hidden, sg.num_classes, fanouts, aggregator)
-    opt = torch.optim.Adam(model.parameters(), lr=3e-3)
-    # size the shard-parallel run from one single-threaded batch (~budget_s)
-    nt = torch.get_num_threads()
-    torch.set_num_threads(1)
-    t0 = time.perf_counter()
-    train_step(model, opt, host, labels, sg.train_ids[:batch], fanouts, batch, 0, decode)
-    per = time.perf_counter() - t0
-    torch.set_num_threads(nt)
-    par = cpu_parallel(sg, dc, fanouts, hidden, aggregator, batch,
-                       max(1, int(budget_s / max(per, 1e-3))), warm=1)
-    if par is not None:
-        seeds, wall, workers = par
-        return {"value": round(seeds / wall, 2), "unit": "seeds/s", "cores": workers,
-                "kind": "port",
-                "sample": f"{workers} spawned processes x {seeds // workers // batch} "
-                          f"mini-batches of {batch} seeds, fanouts {list(fanouts)}, "
-                          f"{wall:.1f} s wall (oracle port, one thread each, disjoint batches)"}
-    seeds_done, t0, steps = 0, time.perf_counter(), 0
-    train = sg.train_ids
-    while True:
-        train_step(model, opt, host, labels, train[steps * batch:(steps + 1) * batch], fanouts,
-                   batch, steps, decode)
-        steps += 1
-        seeds_done += batch
-        if time.perf_counter() - t0 >= budget_s or steps * batch >= train.size:
-            break
-    dt = time.perf_counter() - t0
-    return {"value": round(seeds_done / dt, 2), "unit": "seeds/s",
-            "cores": torch.get_num_threads(), "kind": "port",
-            "sample": f"{steps} mini-batches of {batch} seeds, fanouts {list(fanouts)}, "
-                      f"{dt:.1f} s (numpy sampler/decoder single-threaded, torch CPU "
-                      f"fp32 SAGE step on {torch.get_num_threads()} threads)"}
-
+# ------------------------------------------------------- reference arm
 
 def run_reference(args, rank, world, local):
-    """The reference arm: CPU oracle port, rank 0 only."""
+    """The reference arm: the reference's CPU loader on every host core over
+    the same world, rebuilt on the CPU (oracle/world.py) -- this process never
+    imports the product package or loads its library.  Rank 0 only."""
     if rank != 0:
         return
-    import torch
-    from oracle import trainer as ot
-    dev = torch.device("cuda", local) if torch.cuda.is_available() else torch.device("cpu")
-    if dev.type == "cuda":
-        torch.cuda.set_device(dev)
-    sg, dc, codec_desc, fanouts, bs, hidden = build_workload(args.config, dev, scale=args.scale)
-    agg = aggregator_of(args.config)
-    par = cpu_parallel(sg, dc, fanouts, hidden, agg, args.ref_batch, args.steps,
-                       warm=args.warmup)
-    if par is not None:  # every host core: one process per core over disjoint batches
-        seeds, dt, workers = par
-        v = seeds / dt
-        line = {"impl": "reference", "metric": "GraphSAGE train seeds/sec",
-                "value": round(v, 2), "unit": "seeds/s", "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": round(dt * 1e3 / args.steps, 2),
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-                "dtype": "f32", "data": "synthetic",
-                "config": {"workload": f"{args.config}-shape "
-                                       f"{dict(gcn='GCN', gat='GAT').get(agg, 'GraphSAGE')} "
-                                       f"{len(fanouts)}-layer fanout {list(fanouts)}, "
-                                       f"{codec_desc}",
-                           "per_step_seeds": args.ref_batch * workers,
-                           "parallelism": f"cpu x{workers} processes"},
-                "cpu_baseline": {"value": round(v, 2), "unit": "seeds/s", "cores": workers,
-                                 "kind": "port",
-                                 "sample": f"{args.steps} steps x {workers} processes x "
-                                           f"{args.ref_batch} seeds (oracle port, one thread "
-                                           f"per process)"},
-                "e2e": {"value": round(v, 2), "unit": "seeds/s", "h2d_bytes_per_step": 0,
-                        "d2h_bytes_per_step": 0}}
-        print(json.dumps(line), flush=True)
+    from oracle import loader as OL
+    from oracle import world as W
+    codec = CONFIGS[args.config][1]
+    _, _, fanouts, bs, _ = CONFIGS[args.config][:5]
+    if codec[0] != "sq":
+        print(json.dumps({"impl": "reference", "metric": METRIC,
+                          "unavailable": "the CPU reference world covers the SQ configs "
+                                         "(papers100m, arxiv, products-sq8/gcn); VQ fitting "
+                                         "the 1e6-row sample on the CPU takes hours"}),
+              flush=True)
         return
-    host, labels, decode = _host_world(sg, dc)  # fallback: one process, all torch threads
-    torch.set_num_threads(os.cpu_count() or 1)
-    model, train_step = oracle_model(ot, dc.d, hidden, sg.num_classes, fanouts,
-                                     aggregator_of(args.config))
-    opt = torch.optim.Adam(model.parameters(), lr=3e-3)
-    batch = args.ref_batch
-    train = sg.train_ids
-
-    def one(i):
-        train_step(model, opt, host, labels, train[i * batch:(i + 1) * batch], fanouts, batch,
-                   i, decode)
-
-    for i in range(args.warmup):
-        one(i)
-    t0 = time.perf_counter()
-    for i in range(args.steps):
-        one(args.warmup + i)
-    dt = time.perf_counter() - t0
-    v = batch * args.steps / dt
-    line = {"impl": "reference", "metric": "GraphSAGE train seeds/sec", "value": round(v, 2),
-            "unit": "seeds/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(dt * 1e3 / args.steps, 2), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"{args.config}-shape GraphSAGE {len(fanouts)}-layer fanout "
-                                   f"{list(fanouts)}, {codec_desc}",
-                       "per_step_seeds": batch, "parallelism": "cpu"},
-            "cpu_baseline": {"value": round(v, 2), "unit": "seeds/s",
-                             "cores": torch.get_num_threads(), "kind": "port",
-                             "sample": f"{args.steps} steps x {batch} seeds"},
+    s = shape_of(args.config, args.scale)
+    path = world_dir("fgb_ref_")
+    try:
+        t0 = time.perf_counter()
+        meta = W.build_world(path, n=s["n"], avg_deg=s["avg_deg"], classes=s["classes"],
+                             d=s["d"], train=s["train"], sq_k=codec[1], seed=0,
+                             log=lambda m: print(f"[bench/ref] {m}", file=sys.stderr, flush=True))
+        build_s = time.perf_counter() - t0
+        r = OL.run_pool(path, fanouts, bs, steps=args.steps, warm=args.warmup,
+                        workers=args.ref_workers or None)
+    finally:
+        shutil.rmtree(path, ignore_errors=True)
+    v = r["seeds_per_s"]
+    info = OL.host_info()
+    sample = (f"{args.steps} steps x {r['workers']} spawned processes x {bs} seeds "
+              f"(+{args.warmup} warm-up batches each): featgrind.sample_batches "
+              f"{list(fanouts)} + dequantize_sq of each batch's frontier "
+              f"({'unmodified featgrind from baseline/_ref' if r['kind'] == 'reference' else 'numpy port in oracle/'}); "
+              f"loader only (the reference has no trainer); one thread per process")
+    line = {"impl": "reference", "metric": METRIC, "value": round(v, 2), "unit": "seeds/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(r["wall_s"] * 1e3 / args.steps, 2), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64/f32 (numpy)",
+            "data": "synthetic (planted-partition power-law graph, class-conditional features)"
+                    " -- the GPU arm's world rebuilt bit-identically on the CPU",
+            "config": workload_config(args.config, meta["nnz"], world, args.scale),
+            "cpu_baseline": {"value": round(v, 2), "unit": "seeds/s", "cores": r["workers"],
+                             "kind": r["kind"], "sample": sample, "host": info},
             "e2e": {"value": round(v, 2), "unit": "seeds/s", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
+                    "d2h_bytes_per_step": 0},
+            "world_build_s": round(build_s, 1),
+            "work": {"frontier_rows": r["frontier_rows"], "edges_touched": r["edges_touched"]}}
     print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------- launcher
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def relaunch_distributed(n):
+    """Re-run this command under torch.distributed.run with n ranks."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}",
+           os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def init_dist(backend):
+    """torchrun environment -> (rank, world, local rank); the process group
+    is created only for world > 1."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", rank=rank, world_size=world,
+                                    device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo", rank=rank, world_size=world)
+    return rank, world, local
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", choices=sorted(CONFIGS), default="products")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default=DEFAULT_CONFIG)
     ap.add_argument("--scale", type=float, default=1.0, help="node-count scale (tests only)")
-    ap.add_argument("--ref-batch", type=int, default=128)
     ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--ref-workers", type=int, default=0, help="reference-arm processes "
+                    "(default: every host core)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-epoch", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    from paper_2207_14696_b200 import ddp
-    backend = "nccl" if args.impl == "ours" else "gloo"
-    rank, world, local = ddp.init_from_env(backend)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_distributed(args.gpus))
+    if args.impl == "reference":
+        # rank 0 alone runs the CPU arm; no process group is needed
+        rank = int(os.environ.get("RANK", "0"))
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        run_reference(args, rank, world, int(os.environ.get("LOCAL_RANK", "0")))
+        return
+    rank, world, local = init_dist("nccl")
     try:
-        if args.impl == "reference":
-            run_reference(args, rank, world, local)
-        else:
-            run_ours(args, rank, world, local)
+        run_ours(args, rank, world, local)
     finally:
         import torch.distributed as dist
         if dist.is_initialized():

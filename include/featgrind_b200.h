@@ -463,6 +463,12 @@ int fg_graph_emit(uint64_t seed, int64_t n, int64_t classes, double alpha,
 int fg_graph_labels(uint64_t seed, int64_t n, int64_t classes, int32_t* labels,
                     void* cuda_stream);
 
+/* Number of nodes i whose sorted row holds i (count is a device u64, zeroed
+ * by the call).  The device form of load_graph's self-loop flag check,
+ * graphstore.py:421-425 (all-or-none is the CsrGraph invariant, :125-127). */
+int fg_csr_self_loops(const int64_t* row_offsets, const int32_t* col_indices,
+                      int64_t n, unsigned long long* count, void* cuda_stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -103,6 +103,7 @@ _SIGS = {
     "fg_graph_emit": (ci, [u64, i64, i64, C.c_double, C.c_double, i64, i64, i64, vp, i64, vp,
                            vp]),
     "fg_graph_labels": (ci, [u64, i64, i64, vp, vp]),
+    "fg_csr_self_loops": (ci, [vp, vp, i64, vp, vp]),
 }
 
 _lib = None

@@ -6,6 +6,7 @@
 // generate_features kinds (pkg/src/featgrind/graphstore.py:291-324), plus a
 // class-conditional kind with planted labels for the trainer.
 #include "fg_common.cuh"
+#include "fg_detmath.cuh"
 
 namespace fg {
 
@@ -16,12 +17,15 @@ __device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
   return z ^ (z >> 31);
 }
 
-// two independent uniforms in (0, 1] from one 64-bit hash
+// Box-Muller from two 24-bit uniforms of one 64-bit hash, in float64 with the
+// deterministic elementary functions (fg_detmath.cuh), rounded once to float:
+// the same bits as the C restatement (oracle/fgoracle.c).
 __device__ __forceinline__ float gauss(uint64_t key) {
   const uint64_t h = splitmix64(key);
-  const float u1 = ((uint32_t)(h >> 40) + 1u) * (1.0f / 16777216.0f);  // (0, 1]
-  const float u2 = (uint32_t)(h & 0xFFFFFFu) * (1.0f / 16777216.0f);
-  return sqrtf(-2.0f * __logf(u1)) * __cosf(6.2831853f * u2);
+  const double u1 = (double)((uint32_t)(h >> 40) + 1u) * 0x1p-24;  // (0, 1]
+  const double u2 = (double)(uint32_t)(h & 0xFFFFFFu) * 0x1p-24;   // [0, 1)
+  const double ln_u1 = det::mul(det::log2(u1), 0x1.62e42fefa39efp-1);
+  return __double2float_rn(det::mul(__dsqrt_rn(det::mul(-2.0, ln_u1)), det::cos_turns(u2)));
 }
 
 __device__ __forceinline__ uint64_t elem_key(uint64_t seed, int64_t i, int64_t j) {
@@ -44,18 +48,19 @@ __global__ void k_synth(int kind, uint64_t seed, int64_t row0, const int64_t* __
         break;
       case 1: {  // lognormal magnitude, random sign
         const uint64_t sgn = splitmix64(elem_key(seed ^ 0x5151ull, i, j));
-        v = __expf(z) * ((sgn & 1) ? 1.f : -1.f);
+        const float mag = __double2float_rn(det::exp2(det::mul((double)z, 0x1.71547652b82fep+0)));
+        v = (sgn & 1) ? mag : -mag;
         break;
       }
       case 2: {  // correlated: shared direction + per-row noise (weight 0.9)
         const float s = gauss(elem_key(seed ^ 0xC0FFEEull, -1, j));
-        v = 0.9486833f * s + 0.31622777f * z;
+        v = __fadd_rn(__fmul_rn(0.9486833f, s), __fmul_rn(0.31622777f, z));
         break;
       }
       default: {  // class-conditional: mean direction of the planted label
         const int c = labels ? labels[i] : 0;
         const float m = gauss(elem_key(seed ^ 0xC1A55ull, c, j));
-        v = 0.6f * m + 0.8f * z;
+        v = __fadd_rn(__fmul_rn(0.6f, m), __fmul_rn(0.8f, z));
         break;
       }
     }
@@ -114,7 +119,7 @@ struct GraphGen {
 };
 
 __device__ __forceinline__ double u01(uint64_t h) {
-  return ((h >> 11) + 0.5) * (1.0 / 9007199254740992.0);  // (0, 1)
+  return det::mul(det::add((double)(h >> 11), 0.5), 0x1p-53);  // (0, 1)
 }
 
 __device__ __forceinline__ int64_t feistel(int64_t x, const GraphGen& g) {
@@ -145,9 +150,10 @@ __device__ __forceinline__ int64_t class_start(const GraphGen& g, int64_t c) {
 
 __device__ __forceinline__ int64_t powerlaw_rank(double u, int64_t size, double alpha) {
   // continuous inverse CDF of x^-alpha on [1, size+1)
-  const double a1 = 1.0 - alpha;
-  const double hi = pow((double)size + 1.0, a1);
-  const double x = pow(1.0 + u * (hi - 1.0), 1.0 / a1);
+  // (deterministic pow: the same bits as oracle/fgoracle.c)
+  const double a1 = det::sub(1.0, alpha);
+  const double hi = det::pow(det::add((double)size, 1.0), a1);
+  const double x = det::pow(det::fma(u, det::sub(hi, 1.0), 1.0), det::div(1.0, a1));
   int64_t r = (int64_t)x - 1;
   return r < 0 ? 0 : (r >= size ? size - 1 : r);
 }
@@ -158,10 +164,11 @@ __device__ __forceinline__ void gen_edge(const GraphGen& g, int64_t e, int64_t& 
   const uint64_t h1 = splitmix64(h0 + 0x51ED27ull);
   const uint64_t h2 = splitmix64(h1 + 0xA11CEull);
   const uint64_t h3 = splitmix64(h2 + 0xB0Bull);
-  const int64_t cu = (int64_t)(u01(h0) * g.classes);
+  const int64_t cu = (int64_t)det::mul(u01(h0), (double)g.classes);
   const int64_t su = class_size(g, cu);
   const int64_t pu = class_start(g, cu) + powerlaw_rank(u01(h1), su, g.alpha);
-  const int64_t cv = u01(h2) < g.homophily ? cu : (int64_t)(u01(h3 ^ 0x5A5Aull) * g.classes);
+  const int64_t cv =
+      u01(h2) < g.homophily ? cu : (int64_t)det::mul(u01(h3 ^ 0x5A5Aull), (double)g.classes);
   const int64_t sv = class_size(g, cv);
   const int64_t pv = class_start(g, cv) + powerlaw_rank(u01(h3), sv, g.alpha);
   a = feistel(pu, g);
@@ -244,6 +251,38 @@ extern "C" int fg_graph_labels(uint64_t seed, int64_t n, int64_t classes, int32_
                                void* s) {
   const GraphGen g = make_gen(seed, n, classes, 0.5, 0.0);
   k_node_labels<<<grid_for(n, 256), 256, 0, as_stream(s)>>>(g, labels);
+  FG_LAUNCH_CHECK();
+  return FG_OK;
+}
+
+// ------------------------------------------------ CSR self-loop census
+// Number of nodes whose (sorted) row holds the node itself: binary search per
+// row.  load_graph's self-loop flag check (graphstore.py:421-425) without the
+// nnz-sized row expansion.
+namespace fg {
+__global__ void k_csr_self_loops(const int64_t* __restrict__ off, const int32_t* __restrict__ col,
+                                 int64_t n, unsigned long long* __restrict__ count) {
+  unsigned long long mine = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = off[i], hi = off[i + 1];
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (col[mid] < i) lo = mid + 1; else hi = mid;
+    }
+    mine += (lo < off[i + 1] && col[lo] == i) ? 1ull : 0ull;
+  }
+  for (int o = 16; o; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+  if ((threadIdx.x & 31) == 0 && mine) atomicAdd(count, mine);
+}
+}  // namespace fg
+
+extern "C" int fg_csr_self_loops(const int64_t* row_offsets, const int32_t* col_indices, int64_t n,
+                                 unsigned long long* count, void* s) {
+  FG_CHECK_ARG(n >= 0 && count != nullptr, "fg_csr_self_loops: bad args");
+  FG_CUDA_TRY(cudaMemsetAsync(count, 0, sizeof(unsigned long long), as_stream(s)));
+  if (n == 0) return FG_OK;
+  k_csr_self_loops<<<grid_for(n, 256), 256, 0, as_stream(s)>>>(row_offsets, col_indices, n, count);
   FG_LAUNCH_CHECK();
   return FG_OK;
 }

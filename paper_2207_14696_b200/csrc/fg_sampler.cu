@@ -587,10 +587,8 @@ int fg_sample_layer(const int64_t* row_offsets, const int32_t* col_indices, int6
                     int64_t max_picks, int64_t* num_picks_dev, uint32_t* bitmap, void* ws,
                     int64_t ws_bytes, int32_t* err_flag, void* s) {
   FG_CHECK_ARG(fanout >= 1, "fanouts must be >= 1");
-  FG_CHECK_ARG(fanout <= 200,
-               "fanout %d > 200 can reach numpy's partial Fisher-Yates choice branch "
-               "(deg > 10000 and f > deg // 50), which this sampler does not emulate",
-               fanout);
+  // (numpy's partial Fisher-Yates branch, deg > 10000 and f > deg // 50, is
+  // flagged per node by k_layer_prefix: any fanout is accepted up front)
   FG_CHECK_ARG(max_nodes >= 1 && n >= 1, "fg_sample_layer: empty layer capacity");
   FG_CHECK_ARG(ws_bytes >= layer_ws_bytes(max_nodes), "fg_sample_layer: workspace too small");
   FG_CHECK_ARG(max_picks < INT32_MAX && max_picks < (1ll << kPickBits),

@@ -19,7 +19,7 @@ import torch
 
 from . import _native as N
 from . import formats
-from .errors import FormatError
+from .errors import DataError, FormatError
 
 
 def _stream_file(path: str, offset: int, nbytes: int, chunk_bytes: int, consume, device):
@@ -84,7 +84,13 @@ def load_sq_device(path: str, device="cuda", chunk_bytes: int = 256 << 20):
     want = formats.SQF_HEADER.size + (n * d * k + 7) // 8
     if os.path.getsize(path) != want:
         raise FormatError(f"{path}: expected {want} bytes, found {os.path.getsize(path)}")
-    dc = DeviceSqCodec.empty(SqParams(k, e_min, e_max, clip), n, d, device)
+    try:  # load_sq (sq.py:190-194): invalid params are format errors
+        params = SqParams(k, e_min, e_max, clip)
+        if n < 0 or d < 1:
+            raise DataError("invalid codec dimensions")
+    except DataError as e:
+        raise FormatError(f"{path}: {e}") from e
+    dc = DeviceSqCodec.empty(params, n, d, device)
     _stream_rows(path, formats.SQF_HEADER.size, n, d * k, dc.rows, dc.row_stride, chunk_bytes,
                  device)
     return dc
@@ -101,7 +107,16 @@ def load_vq_device(path: str, device="cuda", chunk_bytes: int = 256 << 20):
     metric_id, layout_id, width, length, num_parts, n, d = formats.read_vqf_header(hdr, path)
     if metric_id >= len(METRICS) or layout_id >= len(CODE_LAYOUTS):
         raise FormatError(f"{path}: unknown metric or layout id")
-    params = VqParams(width, length, METRICS[metric_id], CODE_LAYOUTS[layout_id])
+    try:  # mirror load_vq (vq.py:405-409, 438-439): bad params are format errors
+        params = VqParams(width, length, METRICS[metric_id], CODE_LAYOUTS[layout_id])
+        if params.num_parts(d) != num_parts:
+            raise FormatError(f"{path}: num_parts inconsistent with width and d")
+        if width > d:
+            raise FormatError(f"{path}: need 1 <= width <= d")
+    except DataError as e:
+        if isinstance(e, FormatError):
+            raise
+        raise FormatError(f"{path}: {e}") from e
     bits = params.bits_per_code
     if params.code_layout != "packed" and bits > 8:
         return DeviceVqCodec.from_codec(load_vq(path), device)
@@ -150,4 +165,13 @@ def load_csrg_device(path: str, device="cuda", chunk_bytes: int = 256 << 20):
         bad |= (col.min() < 0) | (col.max() >= n)
     if bool(bad):
         raise FormatError(f"{path}: invalid CSR (offsets or column range)")
+    # self-loops all-or-none and matching the header flag (graphstore.py:
+    # 125-127, 423-425): one binary search per row on the device
+    cnt = torch.zeros(1, dtype=torch.int64, device=device)
+    N.call("fg_csr_self_loops", N.ptr(off), N.ptr(col), n, N.ptr(cnt), N.stream_handle())
+    loops = int(cnt.item())
+    if loops not in (0, n):
+        raise FormatError(f"{path}: self-loops must be present on all nodes or none")
+    if (loops == n and n > 0) != bool(flags & 1):
+        raise FormatError(f"{path}: self-loop flag does not match contents")
     return DeviceGraph(n, off, col, bool(flags & 1))

@@ -191,3 +191,49 @@ def test_sampler_edge_cases_match_oracle(fans, bs):
     st = smp.stream_state()
     assert st["state"]["state"] == ref_state["state"]["state"]
     smp.check_errors()
+
+
+def test_sampler_fanout_above_200_small_graph():
+    """Fanouts above 200 are accepted (no blanket cap): on degrees <= 10000
+    numpy's choice stays on the Floyd branch, so picks and the stream state
+    equal the oracle.  A hub with deg > 10000 and f > deg // 50 would take
+    numpy's partial Fisher-Yates branch: that is reported as a DataError."""
+    n = 1500
+    r = np.random.default_rng(5)
+    key = set()
+    for u in range(n):
+        for v in r.choice(n, 400, replace=False):
+            if u != v:
+                key.add((u, int(v)))
+                key.add((int(v), u))
+    key |= {(u, u) for u in range(n)}
+    key = np.array(sorted(key), np.int64)
+    off = np.zeros(n + 1, np.int64)
+    np.add.at(off, key[:, 0] + 1, 1)
+    off = np.cumsum(off)
+    col = key[:, 1].astype(np.int32)
+    g = fg.CsrGraph(n, off, col)
+    train = np.arange(0, n, 3)
+    fans, bs, seed = (300, 2), 128, 9
+    smp = DeviceSampler(g.to_device(), fans, bs, need_local=True, want_frontier=True)
+    smp.begin_epoch(train, seed)
+    ref, ref_state = sample_batches_oracle(off, col, train, fans, bs, seed, max_batches=2)
+    for bi, rb in enumerate(ref):
+        sb = smp.sample(bi)
+        got = _blocks(smp, sb, len(fans))
+        for li, L in enumerate(rb.layers):
+            assert np.array_equal(got[li][2], L.picks), (bi, li)
+    assert smp.stream_state()["state"]["state"] == ref_state["state"]["state"]
+    smp.check_errors()
+    # hub of degree 12000 with fanout 300 > 12000 // 50: numpy's other branch
+    hub_deg = 12_000
+    n2 = hub_deg + 1
+    off2 = np.concatenate([[0, hub_deg + 1], hub_deg + 1 + 2 * np.arange(1, hub_deg + 1)])
+    col2 = np.concatenate([np.arange(n2), np.stack([np.zeros(hub_deg), np.arange(1, n2)],
+                                                   1).reshape(-1)]).astype(np.int32)
+    g2 = fg.CsrGraph(n2, off2.astype(np.int64), col2)
+    smp2 = DeviceSampler(g2.to_device(), (300,), 4, need_local=False)
+    smp2.begin_epoch(np.array([0]), 1)
+    smp2.sample(0)
+    with pytest.raises(fg.DataError):
+        smp2.check_errors()

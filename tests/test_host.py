@@ -320,36 +320,3 @@ def test_measured_report_semantics_follow_the_reference():
         compare_reports(a, [SimReport("y", 1, 0, 0, 0, 1, 0, 1.0, 0, 1.0, dict(wl, seed=1))])
     with pytest.raises(DataError):
         SimReport.from_dict({"label": "z"})
-
-
-def test_shard_parallel_cpu_baseline_spawns_and_trains(tmp_path):
-    """bench.py's shard-parallel CPU baseline: spawned oracle workers map the
-    host world from .npy files and train disjoint batches (2 workers, tiny
-    SQ world)."""
-    import sys
-    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-    import bench
-    from oracle import codecs as oc
-    r = np.random.default_rng(0)
-    n, d, k = 400, 16, 8
-    a, b = r.integers(0, n, 3000), r.integers(0, n, 3000)
-    key = np.unique(np.concatenate([a * n + b, b * n + a, np.arange(n) * (n + 1)]))
-    rows, cols = key // n, (key % n).astype(np.int32)
-    off = np.zeros(n + 1, np.int64)
-    np.add.at(off, rows + 1, 1)
-    off = np.cumsum(off)
-    x = r.standard_normal((n, d)).astype(np.float32)
-    e_min, e_max = oc.sq_fit(x, k)
-    payload = oc.pack_msb(oc.sq_codes(x, k, e_min, e_max).ravel(), k)
-    p = str(tmp_path)
-    np.save(os.path.join(p, "off.npy"), off)
-    np.save(os.path.join(p, "col.npy"), cols)
-    np.save(os.path.join(p, "labels.npy"), r.integers(0, 3, n).astype(np.int32))
-    np.save(os.path.join(p, "train.npy"), np.arange(0, n, 2))
-    np.save(os.path.join(p, "payload.npy"), np.frombuffer(payload, np.uint8))
-    meta = {"n": n, "d": d, "kind": "sq", "k": k, "e_min": float(e_min), "e_max": float(e_max)}
-    cfg = {"hidden": 16, "classes": 3, "fanouts": (3, 2), "agg": "mean", "batch": 16}
-    out = bench.cpu_parallel_from_dir(p, meta, cfg, nsteps=2, warm=1, workers=2, timeout=300)
-    assert out is not None
-    seeds, wall, workers = out
-    assert seeds == 2 * 2 * 16 and workers == 2 and wall > 0
