@@ -240,7 +240,7 @@ def build_workload(cfg_name, device, seed=0, scale=1.0):
           f"codec ({codec_desc(cfg_name)}) in {t2 - t1:.1f} s, "
           f"{torch.cuda.max_memory_allocated(device) / 2**30:.1f} GiB peak", file=sys.stderr,
           flush=True)
-    return sg, dc, fanouts, bs, hidden
+    return sg, dc, codec_desc(cfg_name), fanouts, bs, hidden
 
 
 def flush_l2(buf):
@@ -259,7 +259,7 @@ def run_ours(args, rank, world, local):
 
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
-    sg, dc, fanouts, bs, hidden = build_workload(args.config, dev, scale=args.scale)
+    sg, dc, _, fanouts, bs, hidden = build_workload(args.config, dev, scale=args.scale)
     pg = dist.group.WORLD if world > 1 else None
     agg_kind = aggregator_of(args.config)
     if agg_kind == "gat":

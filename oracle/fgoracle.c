@@ -318,8 +318,8 @@ int fgo_synth_features(int kind, uint64_t seed, int64_t row0, const int64_t* row
  * reaches j, found with the reference's formula on the host): code =
  * half + #{t_j <= |x|} for x >= 0 (-0.0 included), half - 1 - # otherwise;
  * k = 1: x >= 0.  Packed MSB-first as one continuous stream
- * (bitpack.py:17-36); 8-row groups start on a byte.  Also counts zeros (the
- * caller's fit assumed none, see fgo_sq_world_fit). */
+ * (bitpack.py:17-36); 8-row groups start on a byte.  Also counts the
+ * zero elements met. */
 typedef struct {
   const FeatGen* g;
   int k;
@@ -382,8 +382,8 @@ int64_t fgo_sq_encode_stream(int kind, uint64_t seed, int64_t n, int64_t d, cons
 }
 
 /* Values at flat positions pos[0 .. m) (sorted) of the n x d matrix: the
- * linspace-strided fit sample of sq.py:104-106 when the matrix has no zeros
- * (nonzero rank == flat position). */
+ * linspace-strided fit sample of sq.py:104-106, its nonzero ranks mapped to
+ * positions with the zero list of fgo_find_zeros. */
 typedef struct {
   const FeatGen* g;
   const int64_t* pos;
@@ -418,86 +418,39 @@ int fgo_values_at(int kind, uint64_t seed, int64_t d, const int32_t* labels, int
   return 0;
 }
 
-/* Exact nonzero count per chunk of rows and the values at nonzero ranks
- * (the general fit_sq path, used only when the matrix holds zeros). */
+/* Flat positions of the zero elements of rows [0, n) (fit_sq's
+ * `flat[flat != 0]`, sq.py:99, needs them to map the linspace sample's
+ * nonzero ranks back to positions).  Writes at most cap positions (unsorted
+ * across row chunks) and returns the total count. */
 typedef struct {
   const FeatGen* g;
-  int64_t n, chunk_rows;
-  int64_t* counts;
-  const int64_t *base, *first, *ranks;
-  float* out;
-} NzCtx;
+  int64_t* pos;
+  int64_t cap, count;
+} ZeroCtx;
 
-static void nz_count(int64_t lo, int64_t hi, void* p) {
-  const NzCtx* x = (const NzCtx*)p;
+static void zero_rows(int64_t lo, int64_t hi, void* p) {
+  ZeroCtx* x = (ZeroCtx*)p;
   const int64_t d = x->g->d;
   float* row = (float*)malloc(sizeof(float) * (size_t)d);
-  for (int64_t c = lo; c < hi; ++c) {
-    const int64_t r1 = (c + 1) * x->chunk_rows < x->n ? (c + 1) * x->chunk_rows : x->n;
-    int64_t cnt = 0;
-    for (int64_t i = c * x->chunk_rows; i < r1; ++i) {
-      feature_row(x->g, i, row);
-      for (int64_t j = 0; j < d; ++j) cnt += row[j] != 0.0f;
-    }
-    x->counts[c] = cnt;
-  }
-  free(row);
-}
-
-static void nz_values(int64_t lo_c, int64_t hi_c, void* p) {
-  const NzCtx* x = (const NzCtx*)p;
-  const int64_t d = x->g->d;
-  float* row = (float*)malloc(sizeof(float) * (size_t)d);
-  for (int64_t c = lo_c; c < hi_c; ++c) {
-    const int64_t lo = x->first[c], hi = x->first[c + 1];
-    if (lo >= hi) continue;
-    int64_t rank = x->base[c];
-    const int64_t r1 = (c + 1) * x->chunk_rows < x->n ? (c + 1) * x->chunk_rows : x->n;
-    int64_t q = lo;
-    for (int64_t i = c * x->chunk_rows; i < r1 && q < hi; ++i) {
-      feature_row(x->g, i, row);
-      for (int64_t j = 0; j < d && q < hi; ++j) {
-        if (row[j] == 0.0f) continue;
-        while (q < hi && x->ranks[q] == rank) x->out[q++] = row[j];
-        ++rank;
+  for (int64_t i = lo; i < hi; ++i) {
+    feature_row(x->g, i, row);
+    for (int64_t j = 0; j < d; ++j)
+      if (row[j] == 0.0f) {
+        const int64_t slot = __atomic_fetch_add(&x->count, 1, __ATOMIC_RELAXED);
+        if (slot < x->cap) x->pos[slot] = i * d + j;
       }
-    }
   }
   free(row);
 }
 
-int fgo_count_nonzero_chunks(int kind, uint64_t seed, int64_t n, int64_t d,
-                             const int32_t* labels, int64_t classes, int64_t chunk_rows,
-                             int64_t* counts) {
+int64_t fgo_find_zeros(int kind, uint64_t seed, int64_t n, int64_t d, const int32_t* labels,
+                       int64_t classes, int64_t* pos, int64_t cap) {
+  if (kind == 3 && classes <= 0) return -1;
   FeatGen g = {kind, seed, d, labels, column_table(kind, seed, d, classes)};
-  NzCtx x = {&g, n, chunk_rows, counts, NULL, NULL, NULL, NULL};
-  par_for((n + chunk_rows - 1) / chunk_rows, 1, nz_count, &x);
+  ZeroCtx x = {&g, pos, cap, 0};
+  par_for(n, 256, zero_rows, &x);
   free(g.table);
-  return 0;
-}
-
-int fgo_nonzero_values_at_ranks(int kind, uint64_t seed, int64_t n, int64_t d,
-                                const int32_t* labels, int64_t classes, int64_t chunk_rows,
-                                const int64_t* counts, const int64_t* ranks, int64_t m,
-                                float* out) {
-  const int64_t nchunks = (n + chunk_rows - 1) / chunk_rows;
-  int64_t* base = (int64_t*)malloc(sizeof(int64_t) * (nchunks + 1));
-  int64_t* first = (int64_t*)malloc(sizeof(int64_t) * (nchunks + 1));
-  if (!base || !first) return 3;
-  base[0] = 0;
-  for (int64_t c = 0; c < nchunks; ++c) base[c + 1] = base[c] + counts[c];
-  int64_t t = 0;
-  for (int64_t c = 0; c <= nchunks; ++c) {
-    while (t < m && ranks[t] < base[c]) ++t;
-    first[c] = t;
-  }
-  FeatGen g = {kind, seed, d, labels, column_table(kind, seed, d, classes)};
-  NzCtx x = {&g, n, chunk_rows, (int64_t*)counts, base, first, ranks, out};
-  par_for(nchunks, 1, nz_values, &x);
-  free(g.table);
-  free(base);
-  free(first);
-  return 0;
+  return x.count;
 }
 
 /* --------------------------------------------------------------- graphs */

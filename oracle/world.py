@@ -70,9 +70,7 @@ def lib():
         vp, i64, u64, ci, dbl = C.c_void_p, C.c_int64, C.c_uint64, C.c_int, C.c_double
         sig = {
             "fgo_synth_features": (ci, [ci, u64, i64, vp, i64, i64, vp, i64, vp]),
-            "fgo_count_nonzero_chunks": (ci, [ci, u64, i64, i64, vp, i64, i64, vp]),
-            "fgo_nonzero_values_at_ranks": (ci, [ci, u64, i64, i64, vp, i64, i64, vp, vp, i64,
-                                                 vp]),
+            "fgo_find_zeros": (i64, [ci, u64, i64, i64, vp, i64, vp, i64]),
             "fgo_values_at": (ci, [ci, u64, i64, vp, i64, vp, i64, vp]),
             "fgo_sq_encode_stream": (i64, [ci, u64, i64, i64, vp, i64, ci, vp, vp]),
             "fgo_graph_open": (vp, [u64, i64, i64, dbl, dbl]),
@@ -188,44 +186,40 @@ def _sample_ranks(nnz: int) -> np.ndarray:
     return np.arange(nnz, dtype=np.int64)
 
 
-def fit_sq_exact(n: int, d: int, k: int, *, kind: int = 3, seed: int = 0, labels=None,
-                 clip: float = 0.005, chunk_rows: int = 1 << 14) -> tuple[float, float]:
+def find_zeros(n: int, d: int, *, kind: int = 3, seed: int = 0, labels=None) -> np.ndarray:
+    """Sorted flat positions of the matrix's zero elements (one generation
+    pass; a class-conditional matrix holds ~1 exact zero per 1.6e7 values,
+    from 0.6 m + 0.8 z cancelling in float32)."""
+    lab = None if labels is None else np.ascontiguousarray(labels, dtype=np.int32)
+    cap = 1 << 16
+    while True:
+        pos = np.empty(cap, np.int64)
+        cnt = int(lib().fgo_find_zeros(kind, seed, n, d, _p(lab), _classes(lab), _p(pos), cap))
+        if cnt < 0:
+            raise ValueError("fgo_find_zeros: bad arguments")
+        if cnt <= cap:
+            return np.sort(pos[:cnt])
+        cap = cnt
+
+
+def fit_sq(n: int, d: int, k: int, *, kind: int = 3, seed: int = 0, labels=None,
+           clip: float = 0.005) -> tuple[float, float]:
     """The reference's fit_sq (sq.py:84-111) over the n x d synthetic matrix,
-    which never exists whole: nonzero counts per row chunk, then only the
-    values at the linspace-strided nonzero ranks are regenerated."""
-    lab = np.ascontiguousarray(labels, dtype=np.int32)
-    nch = (n + chunk_rows - 1) // chunk_rows
-    counts = np.empty(nch, np.int64)
-    lib().fgo_count_nonzero_chunks(kind, seed, n, d, _p(lab), _classes(lab), chunk_rows,
-                                   _p(counts))
-    nnz = int(counts.sum())
+    which never exists whole: one pass finds the zeros, then only the values
+    at the linspace-strided nonzero ranks (sq.py:104-106) are regenerated."""
+    lab = None if labels is None else np.ascontiguousarray(labels, dtype=np.int32)
+    zpos = find_zeros(n, d, kind=kind, seed=seed, labels=lab)
+    nnz = n * d - zpos.size
     if nnz == 0:
         if k == 1:
             return 0.0, 0.0
         raise ValueError("cannot fit an exponent range on an all-zero matrix")
     ranks = _sample_ranks(nnz)
-    vals = np.empty(ranks.size, np.float32)
-    lib().fgo_nonzero_values_at_ranks(kind, seed, n, d, _p(lab), _classes(lab), chunk_rows,
-                                      _p(counts), _p(ranks), ranks.size, _p(vals))
-    return _quantiles(vals, clip)
-
-
-def fit_sq_assuming_nonzero(n: int, d: int, *, kind: int = 3, seed: int = 0, labels=None,
-                            clip: float = 0.005) -> tuple[float, float]:
-    """fit_sq when the matrix holds no zero (nonzero rank == flat position):
-    only the 10^7 sampled values are generated.  The assumption is checked by
-    the encode pass (``sq_payload`` returns the zero count); callers fall
-    back to ``fit_sq_exact`` if it fails."""
-    lab = np.ascontiguousarray(labels, dtype=np.int32)
-    pos = _sample_ranks(n * d)
+    # nonzero rank r sits at position r + #{zeros z_i with z_i - i <= r}
+    pos = ranks + np.searchsorted(zpos - np.arange(zpos.size), ranks, side="right")
     vals = np.empty(pos.size, np.float32)
     lib().fgo_values_at(kind, seed, d, _p(lab), _classes(lab), _p(pos), pos.size, _p(vals))
     return _quantiles(vals, clip)
-
-
-def fit_sq(n: int, d: int, k: int, *, kind: int = 3, seed: int = 0, labels=None,
-           clip: float = 0.005) -> tuple[float, float]:
-    return fit_sq_exact(n, d, k, kind=kind, seed=seed, labels=labels, clip=clip)
 
 
 def sq_thresholds(k: int, e_min: float, e_max: float) -> np.ndarray:
@@ -290,16 +284,12 @@ def build_world(path: str, *, n: int, avg_deg: float, classes: int, d: int, trai
     va = max(1, min(n - tr, tr // 5))
     train_ids, _ = split_ids(n, tr, va, seed)
     train_ids.astype(np.int64).tofile(os.path.join(path, "train.bin"))
-    e_min, e_max = fit_sq_assuming_nonzero(n, d, seed=seed, labels=lab)
+    e_min, e_max = fit_sq(n, d, sq_k, seed=seed, labels=lab)
     t2 = time.perf_counter()
-    say(f"fit_sq e_min={e_min:.6g} e_max={e_max:.6g} in {t2 - t1:.1f} s")
+    say(f"fit_sq e_min={e_min:.17g} e_max={e_max:.17g} in {t2 - t1:.1f} s")
     ppath = os.path.join(path, "payload.bin")
     pay = np.memmap(ppath, np.uint8, "w+", shape=((n * d * sq_k + 7) // 8,))
-    _, zeros = sq_payload(n, d, sq_k, e_min, e_max, seed=seed, labels=lab, out=pay,
-                          return_zeros=True)
-    if zeros:  # the matrix holds zeros: the exact two-pass fit, then re-encode
-        e_min, e_max = fit_sq_exact(n, d, sq_k, seed=seed, labels=lab)
-        sq_payload(n, d, sq_k, e_min, e_max, seed=seed, labels=lab, out=pay)
+    sq_payload(n, d, sq_k, e_min, e_max, seed=seed, labels=lab, out=pay)
     pay.flush()
     del pay, lab
     t3 = time.perf_counter()

@@ -703,6 +703,210 @@ k_vq_mean8_fast(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
   if (!waited) bulk_wait(&s_mbar);
 }
 
+// --------------------------------- VQ lane-per-part path (8-bit, bf16)
+// v5 (round 2), for codebooks too large for one SM (MAG240M-shape: 96 parts x
+// 256 x 8 bf16 = 393 KB).  The v4 kernel sliced parts 6 ways with 16 parts
+// (16 B) per slice, so every slice CTA re-read its 16 B out of the row's
+// 32-B sectors (ncu: DRAM read 2x the algorithmic bytes) and its random
+// 16-B codebook lookups from 8 bank groups conflicted (~7.5 wavefronts per
+// warp-wide lookup instead of 4).  Here:
+//  * a slice is one 32-B SECTOR of the code row = 32 parts; CTA b serves
+//    slice b % nslices of every tile, so each sector is read from DRAM by
+//    exactly one CTA and no slice depends on L2 coincidences;
+//  * a warp handles one destination at a time, lane = part: the pick's code
+//    byte comes from a shared-memory copy of its sector and the lane's
+//    lookup hits its own bank group -- part p's entries live at byte offset
+//    (p % PPL) * EB of 128-B lines (PPL = 128 / EB parts per line), so the 8
+//    (W = 8) or 16 (W = 4) lanes of one wavefront never share a bank:
+//    the minimum 4 (2) wavefronts per warp lookup;
+//  * the warp's bf16 output row segment (512 B for W = 8) is one coalesced
+//    store per destination;
+//  * cp.async pipeline over tiles of kTD destinations, one CTA per SM:
+//    indptr slices 3 tiles ahead, source ids 2 ahead, code sectors 1 ahead
+//    (smem rings of 4 / 3 / 2), so the random sector gathers of tile t+1
+//    are in flight while tile t decodes; the codebook slice is filled by
+//    per-entry cp.async into the interleaved layout.
+constexpr int kLaneThreads = 1024;
+constexpr int kLaneWarps = kLaneThreads / 32;
+
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// cp.async the indptr slice of `tile` (entries clamped at max_dst)
+__device__ __forceinline__ void lane_issue_ip(int32_t* dst, const int32_t* __restrict__ indptr,
+                                              int64_t tile, int64_t max_dst) {
+  for (int t = threadIdx.x; t <= kTD; t += blockDim.x)
+    cp_async4(dst + t, indptr + min64(tile * kTD + t, max_dst));
+}
+// cp.async the source ids of a tile whose indptr slice is in smem
+__device__ __forceinline__ void lane_issue_src(int32_t* dst, const int32_t* s_ip,
+                                               const int32_t* __restrict__ src) {
+  const int32_t e0 = s_ip[0], cnt = s_ip[kTD] - e0;
+  if (cnt > kSrcCap) return;  // compute reads them from global
+  for (int t = threadIdx.x; t < cnt; t += blockDim.x) cp_async4(dst + t, src + e0 + t);
+}
+// cp.async the slice's 32-B code sector of every pick of a tile whose source
+// ids are in smem (two 16-B copies per pick)
+__device__ __forceinline__ void lane_issue_codes(uint8_t* dst, const int32_t* s_ip,
+                                                 const int32_t* s_src,
+                                                 const uint8_t* __restrict__ rows,
+                                                 int64_t stride, int sector_off) {
+  const int32_t cnt = s_ip[kTD] - s_ip[0];
+  if (cnt > kSrcCap) return;
+  for (int t = threadIdx.x; t < 2 * cnt; t += blockDim.x) {
+    const int e = t >> 1, h = t & 1;
+    cp_async16(dst + e * 32 + h * 16,
+               rows + (int64_t)s_src[e] * stride + sector_off + h * 16);
+  }
+}
+
+template <int W, bool WT>
+__global__ void __launch_bounds__(kLaneThreads, 1)
+k_vq_mean8_lane(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
+                const __nv_bfloat16* __restrict__ books, int length, int parts,
+                const int32_t* __restrict__ indptr, const int32_t* __restrict__ src,
+                const int64_t* __restrict__ ndst_dev, int64_t max_dst,
+                __nv_bfloat16* __restrict__ out, int64_t ld, int nslices,
+                const float* __restrict__ ew) {
+  constexpr int EB = W * 2;        // bytes per bf16 entry
+  constexpr int PPL = 128 / EB;    // parts per 128-B line
+  extern __shared__ __align__(128) uint8_t s_raw[];
+  const int slice = (int)(blockIdx.x % nslices);
+  const int64_t live = live_dst(ndst_dev, max_dst);
+  const int64_t ntiles = (live + kTD - 1) / kTD;
+  const int64_t tile0 = blockIdx.x / nslices, tstep = gridDim.x / nslices;
+  if (tile0 >= ntiles) return;
+  const int lparts = min(32, parts - slice * 32);
+  // smem: codebook slice | 2 x code sectors | 3 x source ids | 4 x indptr
+  uint8_t* const s_book = s_raw;
+  uint8_t* const s_codes0 = s_book + (size_t)(32 / PPL) * length * 128;
+  int32_t* const s_src0 = reinterpret_cast<int32_t*>(s_codes0 + 2 * kSrcCap * 32);
+  int32_t* const s_ip0 = s_src0 + 3 * kSrcCap;
+  auto IP = [&](int i) { return s_ip0 + i * (kTD + 4); };
+  auto SRC = [&](int i) { return s_src0 + i * kSrcCap; };
+  auto CODES = [&](int i) { return s_codes0 + i * (kSrcCap * 32); };
+  // codebook slice -> interleaved smem lines (group 0, with the first tile's indptr)
+  {
+    const int nent = lparts * length;
+    const __nv_bfloat16* g = books + (int64_t)slice * 32 * length * W;
+    for (int c = threadIdx.x; c < nent; c += blockDim.x) {
+      const int lp = c / length, e = c - lp * length;
+      uint8_t* dst = s_book + ((lp / PPL) * length + e) * 128 + (lp % PPL) * EB;
+      if constexpr (EB == 16) cp_async16(dst, g + (int64_t)c * W);
+      else cp_async8(dst, g + (int64_t)c * W);
+    }
+  }
+  const int sector_off = slice * 32;
+  // prologue: ip(T0) | src(T0), ip(T1) | codes(T0), src(T1), ip(T2)
+  lane_issue_ip(IP(0), indptr, tile0, max_dst);
+  cp_commit();
+  cp_wait_all();
+  __syncthreads();
+  lane_issue_src(SRC(0), IP(0), src);
+  if (tile0 + tstep < ntiles) lane_issue_ip(IP(1), indptr, tile0 + tstep, max_dst);
+  cp_commit();
+  cp_wait_all();
+  __syncthreads();
+  lane_issue_codes(CODES(0), IP(0), SRC(0), rows, stride, sector_off);
+  if (tile0 + tstep < ntiles) lane_issue_src(SRC(1), IP(1), src);
+  if (tile0 + 2 * tstep < ntiles) lane_issue_ip(IP(2), indptr, tile0 + 2 * tstep, max_dst);
+  cp_commit();
+  cp_wait_all();
+  __syncthreads();
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool active = lane < lparts;
+  const uint32_t lbase = smem_addr(s_book) + (uint32_t)((lane / PPL) * length * 128 +
+                                                         (lane % PPL) * EB);
+  const int64_t col0 = (int64_t)(slice * 32 + lane) * W;
+  const bool full_part = col0 + W <= d;
+  int k = 0;
+  for (int64_t tile = tile0; tile < ntiles; tile += tstep, ++k) {
+    // issue: codes(T_{k+1}), src(T_{k+2}), ip(T_{k+3})
+    const int64_t t1 = tile + tstep, t2 = tile + 2 * tstep, t3 = tile + 3 * tstep;
+    if (t1 < ntiles)
+      lane_issue_codes(CODES((k + 1) & 1), IP((k + 1) & 3), SRC((k + 1) % 3), rows, stride,
+                       sector_off);
+    if (t2 < ntiles) lane_issue_src(SRC((k + 2) % 3), IP((k + 2) & 3), src);
+    if (t3 < ntiles) lane_issue_ip(IP((k + 3) & 3), indptr, t3, max_dst);
+    cp_commit();
+    // compute tile T_k
+    const int32_t* s_ip = IP(k & 3);
+    const uint8_t* s_codes = CODES(k & 1);
+    const int32_t e0 = s_ip[0];
+    const bool staged = s_ip[kTD] - e0 <= kSrcCap;
+    for (int vl = warp; vl < kTD; vl += kLaneWarps) {
+      const int64_t v = tile * kTD + vl;
+      if (v >= live) break;
+      const int a = s_ip[vl] - e0;
+      const int cnt = s_ip[vl + 1] - e0 - a;
+      u64 acc[W / 2];
+#pragma unroll
+      for (int j = 0; j < W / 2; ++j) acc[j] = 0ull;
+      for (int u0 = 0; u0 < cnt; u0 += 8) {
+        const int cb = min(cnt - u0, 8);
+        uint32_t code[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (u < cb) {
+            const int e = a + u0 + u;
+            code[u] = staged ? (uint32_t)s_codes[e * 32 + lane]
+                             : (uint32_t)__ldg(rows + (int64_t)__ldg(src + e0 + e) * stride +
+                                               sector_off + lane);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (u < cb) {
+            const uint32_t addr = lbase + code[u] * 128u;
+            const u64 wu = WT ? bcast2(__ldg(ew + e0 + a + u0 + u)) : 0ull;
+            if constexpr (W == 8) {
+              uint32_t x, y, z, w;
+              asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                           : "=r"(x), "=r"(y), "=r"(z), "=r"(w) : "r"(addr));
+              acc[0] = acc2<WT>(acc[0], bf16x2_to_f32x2(x), wu);
+              acc[1] = acc2<WT>(acc[1], bf16x2_to_f32x2(y), wu);
+              acc[2] = acc2<WT>(acc[2], bf16x2_to_f32x2(z), wu);
+              acc[3] = acc2<WT>(acc[3], bf16x2_to_f32x2(w), wu);
+            } else {
+              uint32_t x, y;
+              asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(x), "=r"(y) : "r"(addr));
+              acc[0] = acc2<WT>(acc[0], bf16x2_to_f32x2(x), wu);
+              acc[1] = acc2<WT>(acc[1], bf16x2_to_f32x2(y), wu);
+            }
+          }
+        }
+      }
+      if (active) {
+        const float inv = WT ? 1.0f : (cnt ? 1.0f / (float)cnt : 0.0f);
+        __nv_bfloat16* o = out + v * ld + col0;
+        if (full_part) {
+          store_scaled<W>(o, acc, inv, true);
+        } else {
+#pragma unroll
+          for (int j = 0; j < W; ++j)
+            if (col0 + j < d)
+              o[j] = __float2bfloat16_rn((j & 1 ? hi2(acc[j / 2]) : lo2(acc[j / 2])) * inv);
+        }
+      }
+    }
+    cp_wait_all();
+    __syncthreads();
+  }
+}
+
 // ------------------------------------------------- VQ (any code width)
 template <int W, typename OT>
 __global__ void __launch_bounds__(kThreads, 2)
@@ -1159,6 +1363,28 @@ int launch_vq_w(const fg_codec_desc* c, const int32_t* indptr, const int32_t* sr
   }
   // bf16 output may read the bf16 copy of the codebooks (half the smem bytes)
   const bool lp = std::is_same<OT, __nv_bfloat16>::value && c->table_lp != nullptr && W >= 4;
+  if constexpr (std::is_same<OT, __nv_bfloat16>::value && (W == 4 || W == 8)) {
+    // lane-per-part kernel (v5): sector slices of 32 parts, one CTA per SM.
+    // FG_VQ_LANE=0 keeps the v4 part-sliced kernel (A/B switch).
+    static const int lane_env = [] {
+      const char* e = getenv("FG_VQ_LANE");
+      return e ? atoi(e) : 1;
+    }();
+    const int64_t lane_smem = (int64_t)32 * c->length * W * 2 + 2 * kSrcCap * 32 +
+                              3 * kSrcCap * 4 + 4 * (kTD + 4) * 4;
+    if (lp && lane_env && c->row_stride % 32 == 0 && lane_smem <= 227 * 1024) {
+      const int ns = (int)ceil_div(c->num_parts, 32);
+      auto kern = k_vq_mean8_lane<W, WT>;
+      FG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)lane_smem));
+      const int64_t per_slice = std::max<int64_t>(1, min64(ntiles, sm_count() / ns));
+      kern<<<(int)(per_slice * ns), kLaneThreads, lane_smem, st>>>(
+          c->rows, c->d, c->row_stride, (const __nv_bfloat16*)c->table_lp, c->length,
+          c->num_parts, indptr, src, ndst, max_dst, (__nv_bfloat16*)out, ld, ns, ew);
+      FG_LAUNCH_CHECK();
+      return FG_OK;
+    }
+  }
   if constexpr (std::is_same<OT, __nv_bfloat16>::value && (W == 4 || W == 8)) {
     constexpr int GF = 32 / W;
     constexpr int64_t kFastSmem = 76 * 1024;  // three CTAs per SM (233 KB smem per SM)

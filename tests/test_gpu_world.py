@@ -55,10 +55,9 @@ def test_benchmark_world_bit_identical(shape, k):
     tr, _ = W.split_ids(s["n"], s["train"], max(1, min(s["n"] - s["train"], s["train"] // 5)))
     assert np.array_equal(sg.train_ids, tr)
     dc = build_sq_codec(s["n"], s["d"], k, labels=sg.labels, num_classes=sg.num_classes, seed=0)
-    e = W.fit_sq_assuming_nonzero(s["n"], s["d"], seed=0, labels=lab)
+    e = W.fit_sq(s["n"], s["d"], k, seed=0, labels=lab)
     assert (dc.params.e_min, dc.params.e_max) == e
-    pay, zeros = W.sq_payload(s["n"], s["d"], k, *e, seed=0, labels=lab, return_zeros=True)
-    assert zeros == 0
+    pay = W.sq_payload(s["n"], s["d"], k, *e, seed=0, labels=lab)
     got = dc.to_codec().payload
     assert len(got) == pay.size
     assert np.array_equal(np.frombuffer(got, np.uint8), pay)

@@ -54,9 +54,8 @@ def test_sq_world_matches_reference_fit_and_quantize(k):
     fm = fgr.FeatureMatrix(x)
     p = fgr.fit_sq(fm, k)
     assert W.fit_sq(n, d, k, seed=2, labels=lab) == (p.e_min, p.e_max)
-    assert W.fit_sq_assuming_nonzero(n, d, seed=2, labels=lab) == (p.e_min, p.e_max)
     pay, zeros = W.sq_payload(n, d, k, p.e_min, p.e_max, seed=2, labels=lab, return_zeros=True)
-    assert zeros == 0
+    assert zeros == int((x == 0).sum())
     assert bytes(pay) == fgr.quantize_sq(fm, p).payload
 
 
@@ -68,6 +67,20 @@ def test_sq_world_strided_fit_sample():
     x = W.features(n, d, seed=0, labels=lab)
     p = fgr.fit_sq(fgr.FeatureMatrix(x), 4)
     assert W.fit_sq(n, d, 4, seed=0, labels=lab) == (p.e_min, p.e_max)
+
+
+def test_sq_world_fit_with_exact_zeros():
+    """The class-conditional matrix holds rare exact zeros (0.6 m + 0.8 z
+    cancelling in float32): the fit's nonzero-rank -> position mapping must
+    skip them exactly like the reference's flat[flat != 0] (sq.py:99)."""
+    from oracle import codecs as oc
+    n, d = 300_000, 100
+    lab = W.labels(n, 47, seed=0)
+    x = W.features(n, d, seed=0, labels=lab)
+    zeros = np.flatnonzero(x.reshape(-1) == 0)
+    assert zeros.size >= 1                       # this seed/shape has one
+    assert np.array_equal(W.find_zeros(n, d, seed=0, labels=lab), zeros)
+    assert W.fit_sq(n, d, 8, seed=0, labels=lab) == oc.sq_fit(x, 8)
 
 
 def test_feature_rows_are_row_addressable():
