@@ -21,7 +21,7 @@ is not vendored in /root/reference.  Their published algorithms are:
 * ``permutation(arr)``: Fisher-Yates for ``i = n-1 .. 1`` with the masked
   rejection draw ``random_interval(i)`` on 32-bit draws.
 
-Verified draw-for-draw against numpy in tests/test_oracle_rng.py.
+Verified draw-for-draw against numpy in tests/test_oracle.py (test_pcg_*).
 """
 
 from __future__ import annotations

@@ -832,6 +832,7 @@ k_vq_mean8_lane(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
                                                          (lane % PPL) * EB);
   const int64_t col0 = (int64_t)(slice * 32 + lane) * W;
   const bool full_part = col0 + W <= d;
+  const bool vec_ok = (ld % 8) == 0;  // 16-B aligned bf16 row segments
   int k = 0;
   for (int64_t tile = tile0; tile < ntiles; tile += tstep, ++k) {
     // issue: codes(T_{k+1}), src(T_{k+2}), ip(T_{k+3})
@@ -893,7 +894,7 @@ k_vq_mean8_lane(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
         const float inv = WT ? 1.0f : (cnt ? 1.0f / (float)cnt : 0.0f);
         __nv_bfloat16* o = out + v * ld + col0;
         if (full_part) {
-          store_scaled<W>(o, acc, inv, true);
+          store_scaled<W>(o, acc, inv, vec_ok);
         } else {
 #pragma unroll
           for (int j = 0; j < W; ++j)

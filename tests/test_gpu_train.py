@@ -301,3 +301,57 @@ def test_measured_epoch_breakdown():
         reps.append(r)
     out = compare_reports(reps[0], reps[1:])
     assert len(render_text(out).splitlines()) == 4
+
+
+@pytest.mark.parametrize("codec", [("sq", 8), ("vq", 4, 256)])
+def test_accuracy_parity_config_a(codec):
+    """BASELINE config A at full size: arxiv-shape (169,343 nodes, d=128,
+    40 classes, 90,941 train ids), 2-layer SAGE, fanouts [10,5], 1024-seed
+    batches, hidden 256 -- 8-bit SQ (the config) and VQ w4 L256 (the VQ
+    accuracy run).  The GPU trainer and the CPU fp32 oracle trainer
+    (reference sampler restatement + reference decoders over the same code
+    rows, oracle/trainer.py) start from the same weights and train on the
+    same batches; validation accuracy (18,188 nodes: 0.5 pt = 91 nodes) must
+    agree within 0.5 points after a partial epoch (12 batches: accuracy
+    still far from its plateau) and after a full epoch."""
+    from paper_2207_14696_b200.synth import make_shape
+    sg = make_shape("arxiv", seed=0)
+    dg, labels, C = sg.graph, sg.labels, sg.num_classes
+    n, d = dg.n, 128
+    if codec[0] == "sq":
+        dc = build_sq_codec(n, d, 8, labels=labels, num_classes=C, seed=0)
+        c = dc.to_codec()
+        p = c.params
+
+        def decode_rows(rows):
+            return oc.sq_dequant_rows(c.payload, n, d, 8, p.e_min, p.e_max, rows)
+    else:
+        dc, _ = build_vq_codec(n, d, codec[1], codec[2], labels=labels, num_classes=C, seed=0)
+        codes = dc.rows[:, :dc.num_parts].cpu().numpy().astype(np.int32)
+
+        def decode_rows(rows):
+            return oc.vq_decode(codes, dc.books_host, d, codec[1], rows)
+    fans, bs, hidden, lr = (10, 5), 1024, 256, 3e-3
+    cfg = TrainConfig(fanouts=fans, batch_size=bs, hidden=hidden, lr=lr, seed=0)
+    gpu = SageTrainer(dg, dc, labels, C, cfg)
+    cpu_model = ot.OracleSage(d, hidden, C, len(fans))
+    cpu_model.load_state_dict(gpu.model.reference_state())
+    opt = torch.optim.Adam(cpu_model.parameters(), lr=lr)
+    host = dg.to_host()
+    lab = labels.cpu().numpy()
+    train, val = sg.train_ids, sg.val_ids
+    accs = []
+    for e, nbatch in ((0, 12), (1, None)):
+        nb = gpu.begin_epoch(train, e)
+        for b in range(nb if nbatch is None else nbatch):
+            gpu.step(b)
+        ot.train_epoch(cpu_model, opt, host.row_offsets, host.col_indices, lab, train, fans, bs,
+                       e, decode_rows, max_batches=nbatch)
+        a_gpu = gpu.evaluate(val, seed=777)
+        a_cpu = ot.evaluate(cpu_model, host.row_offsets, host.col_indices, lab, val, fans, bs,
+                            777, decode_rows)
+        accs.append((a_gpu, a_cpu))
+    print("config A accuracy (gpu, cpu oracle):", codec, accs)
+    for a_gpu, a_cpu in accs:
+        assert a_cpu > 1.0 / C * 3
+        assert abs(a_gpu - a_cpu) <= 0.005 + 1e-12, accs

@@ -179,3 +179,27 @@ def test_sampler_pcg_engine_equals_numpy_engine(sampler_golden):
         for lx, ly in zip(x.layers, y.layers):
             assert np.array_equal(lx.picks, ly.picks)
     assert sa["state"]["state"] == sb["state"]["state"]
+
+
+def test_row_source_oracle_equals_array_oracle(sampler_golden):
+    """The row-source restatement (CSR rows served on demand, used for the
+    full-size BASELINE graphs) gives the same batches, blocks and final
+    stream state as the array oracle pinned to the reference above."""
+    from oracle.sampler import HostRows, sample_batches_oracle_rows
+    z = sampler_golden
+    for ci, gname, fans, bs, seed in _configs(z):
+        off = z[f"graph/{gname}/row_offsets"]
+        col = z[f"graph/{gname}/col_indices"]
+        train = z[f"cfg{ci}/train"]
+        a, sa = sample_batches_oracle(off, col, train, fans, bs, seed)
+        b, sb = sample_batches_oracle_rows(HostRows(off, col), off.size - 1, train, fans, bs,
+                                           seed)
+        assert len(a) == len(b)
+        for x, y in zip(a, b):
+            assert np.array_equal(x.seeds, y.seeds) and np.array_equal(x.frontier, y.frontier)
+            assert x.edges_touched == y.edges_touched
+            for lx, ly in zip(x.layers, y.layers):
+                assert np.array_equal(lx.nodes, ly.nodes)
+                assert np.array_equal(lx.counts, ly.counts)
+                assert np.array_equal(lx.picks, ly.picks)
+        assert sa == sb
