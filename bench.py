@@ -565,6 +565,16 @@ def init_dist(backend):
     return rank, world, local
 
 
+def rank_device(local):
+    """GPU of a local rank.  With FG_DIST_BACKEND=gloo (tests: several ranks
+    sharing the sandbox's one GPU) local ranks wrap around the visible
+    devices; NCCL needs one GPU per rank."""
+    import torch
+    if os.environ.get("FG_DIST_BACKEND", "nccl") == "gloo":
+        return local % max(1, torch.cuda.device_count())
+    return local
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -589,9 +599,9 @@ def main():
         world = int(os.environ.get("WORLD_SIZE", "1"))
         run_reference(args, rank, world, int(os.environ.get("LOCAL_RANK", "0")))
         return
-    rank, world, local = init_dist("nccl")
+    rank, world, local = init_dist(os.environ.get("FG_DIST_BACKEND", "nccl"))
     try:
-        run_ours(args, rank, world, local)
+        run_ours(args, rank, world, rank_device(local))
     finally:
         import torch.distributed as dist
         if dist.is_initialized():

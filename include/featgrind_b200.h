@@ -91,6 +91,28 @@ int fg_rows_to_stream(const uint8_t* rows, int64_t n, int64_t row_bits,
                       int64_t row_stride, uint8_t* stream, int64_t stream_bytes,
                       void* cuda_stream);
 
+/* The reference's bitpack module itself (Python facade
+ * paper_2207_14696_b200/bitpack.py, same names and errors):
+ *   fg_bits_pack        <- pack_codes(codes, bits)         bitpack.py:17-36
+ *                          int64 codes -> ceil(count*bits/8) stream bytes;
+ *                          a code < 0 or >= 2^bits sets *err_flag
+ *                          ("codes do not fit in N bits");
+ *   fg_bits_unpack      <- unpack_codes(payload, bits, count, start_bit)
+ *                          bitpack.py:39-55; FG_EDATA when the stream is
+ *                          shorter than start_bit + count*bits;
+ *   fg_bit_rows_gather  <- gather_bit_rows(payload, row_bits, row_ids)
+ *                          bitpack.py:58-83: out[nrows][row_bits] of 0/1
+ *                          bytes; a row past the stream sets *err_flag
+ *                          ("row ids exceed the packed stream").
+ * bits in [1, 32] (else FG_EUSAGE). */
+int fg_bits_pack(const int64_t* codes, int64_t count, int bits, uint8_t* out,
+                 int32_t* err_flag, void* cuda_stream);
+int fg_bits_unpack(const uint8_t* stream, int64_t stream_bytes, int64_t start_bit,
+                   int64_t count, int bits, int64_t* out, void* cuda_stream);
+int fg_bit_rows_gather(const uint8_t* stream, int64_t stream_bytes, int64_t row_bits,
+                       const int64_t* rows, int64_t nrows, uint8_t* out,
+                       int32_t* err_flag, void* cuda_stream);
+
 /* ----------------------------------------------------------------- SQ */
 /* quantize_sq (sq.py:114-129).  `thresholds` (device, float, 2^(k-1)-1
  * entries, ascending) are the smallest |x| whose reference code offset is

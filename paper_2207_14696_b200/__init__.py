@@ -9,7 +9,8 @@ gather-dequantize-mean kernel, and the GraphSAGE trainer (sage.py).
 """
 
 from .errors import DataError, FormatError
-from .graph import CsrGraph, DeviceGraph, FeatureMatrix
+from .graph import (CsrGraph, DeviceGraph, FeatureMatrix, load_features, load_graph,
+                    save_features, save_graph)
 from .sampler import (BatchPlan, DeviceSampler, MiniBatchSample, SampledBatch,
                       SamplerConfig, sample_batches)
 from .sq import (DeviceSqCodec, SqCodec, SqParams, dequantize_sq, fit_sq, load_sq,
@@ -22,6 +23,7 @@ __version__ = "0.1.0"
 __all__ = [
     "DataError", "FormatError",
     "CsrGraph", "DeviceGraph", "FeatureMatrix",
+    "save_features", "load_features", "save_graph", "load_graph",
     "SqParams", "SqCodec", "fit_sq", "quantize_sq", "dequantize_sq",
     "sq_compression_ratio", "save_sq", "load_sq", "DeviceSqCodec",
     "VqParams", "VqCodec", "VqCrReport", "fit_vq", "encode_vq", "decode_vq",

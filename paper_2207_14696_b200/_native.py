@@ -40,6 +40,9 @@ _SIGS = {
     "fg_sm_count": (ci, [C.POINTER(ci)]),
     "fg_stream_to_rows": (ci, [vp, i64, i64, i64, vp, i64, vp]),
     "fg_rows_to_stream": (ci, [vp, i64, i64, i64, vp, i64, vp]),
+    "fg_bits_pack": (ci, [vp, i64, ci, vp, vp, vp]),
+    "fg_bits_unpack": (ci, [vp, i64, i64, i64, ci, vp, vp]),
+    "fg_bit_rows_gather": (ci, [vp, i64, i64, vp, i64, vp, vp, vp]),
     "fg_sq_encode": (ci, [vp, ci, i64, i64, ci, vp, vp, vp, i64, vp]),
     "fg_sq_gather_dequant": (ci, [C.POINTER(CodecDesc), vp, ci, i64, vp, ci, vp, vp]),
     "fg_count_nonzero": (ci, [vp, i64, vp, vp]),

@@ -39,8 +39,11 @@ def agree_num_batches(nb: int, group=None, device=None) -> int:
 def average_flat_(flat: torch.Tensor, group=None) -> torch.Tensor:
     """In-place mean over ranks of a flat gradient buffer (one collective)."""
     if dist.is_initialized() and dist.get_world_size(group) > 1:
-        dist.all_reduce(flat, group=group)
-        flat.div_(dist.get_world_size(group))
+        if dist.get_backend(group) == "nccl":
+            dist.all_reduce(flat, op=dist.ReduceOp.AVG, group=group)  # one NCCL kernel
+        else:
+            dist.all_reduce(flat, group=group)
+            flat.div_(dist.get_world_size(group))
     return flat
 
 

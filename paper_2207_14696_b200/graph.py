@@ -152,3 +152,42 @@ class DeviceGraph:
 
     def nbytes(self) -> int:
         return self.row_offsets.numel() * 8 + self.col_indices.numel() * 4
+
+
+# ------------------------------------------------------- FMAT1 / CSRG1 files
+# graphstore.py:364-426.  Byte-identical files (formats.py); the loaders run
+# the same container validation, with CSR violations re-raised as
+# FormatError.  deviceio.load_csrg_device streams the same CSRG1 file
+# straight into HBM.
+
+def save_features(f: FeatureMatrix, path: str) -> None:
+    """FMAT1: 32-byte header then row-major little-endian payload."""
+    from . import formats
+    formats.write_fmat(path, f.values)
+
+
+def load_features(path: str) -> FeatureMatrix:
+    from . import formats
+    return FeatureMatrix(formats.read_fmat(path))
+
+
+def save_graph(g, path: str) -> None:
+    """CSRG1: header, u64 row offsets, u32 column indices (a DeviceGraph is
+    copied to the host first)."""
+    from . import formats
+    if isinstance(g, DeviceGraph):
+        g = g.to_host()
+    formats.write_csrg(path, g.n, g.row_offsets, g.col_indices, g.has_self_loops)
+
+
+def load_graph(path: str) -> CsrGraph:
+    from . import formats
+    from .errors import FormatError
+    n, off, col, loops = formats.read_csrg(path)
+    try:
+        g = CsrGraph(n, off, col)
+    except DataError as e:
+        raise FormatError(f"{path}: {e}") from e
+    if g.has_self_loops != loops:
+        raise FormatError(f"{path}: self-loop flag does not match contents")
+    return g

@@ -371,6 +371,11 @@ class SageTrainer:
         unchanged by the warm-up (the warm-up steps do update the model)."""
         rng_save = self.sampler.rng.clone()
         nxt = self._next
+        if self.world > 1 and torch.distributed.get_backend(self.pg) != "nccl":
+            # a host-side (gloo) all-reduce cannot live in a CUDA graph: the
+            # step stays eager (NCCL's all-reduce is captured below)
+            self.graphs, self.graph = {}, None
+            return
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s):

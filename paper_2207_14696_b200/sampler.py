@@ -346,6 +346,11 @@ class DeviceSampler:
 
 def sample_batches(g: CsrGraph, train_ids, cfg: SamplerConfig) -> BatchPlan:
     """pipeline.py:185-222 on the device; identical seeds/frontier/edges."""
+    ids = np.unique(np.asarray(train_ids, dtype=np.int64))  # checked before any launch
+    if ids.size == 0:
+        raise DataError("train_ids must be non-empty")
+    if ids.min() < 0 or ids.max() >= g.n:
+        raise DataError("train id out of range")
     dg = g.to_device()
     smp = DeviceSampler(dg, cfg.fanouts, cfg.batch_size, need_local=False, want_frontier=True)
     nb = smp.begin_epoch(train_ids, cfg.seed)

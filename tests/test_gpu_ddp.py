@@ -115,3 +115,25 @@ def test_sharded_preprocessing_matches_single_process():
         p.join(120)
     assert all(o[1] for o in out), "SQ rows differ"
     assert all(o[2] for o in out), "VQ rows/codebooks differ"
+
+
+def test_bench_two_ranks_prints_one_line():
+    """``bench.py --gpus 2`` relaunches itself under torch.distributed.run;
+    both ranks build the world, train (gloo here: the sandbox has one GPU,
+    so the ranks share it and the steps stay eager -- with NCCL the
+    all-reduce is captured in the step graph), and rank 0 alone prints one
+    line with n_gpus 2 and the max-over-ranks timing."""
+    import json
+    import subprocess
+    import sys
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, FG_DIST_BACKEND="gloo")
+    cmd = [sys.executable, os.path.join(repo, "bench.py"), "--gpus", "2", "--config", "products",
+           "--scale", "0.2", "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--no-epoch"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env, cwd=repo)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["parallelism"] == "dp2"
+    assert d["config"]["global_batch"] == 2048 and d["value"] > 0 and d["e2e"]["value"] > 0
