@@ -79,6 +79,13 @@ int fg_version(void);               /* 100 * major + minor */
  * (benchmarks report launches per step from it). */
 int64_t fg_launch_count(void);
 int fg_sm_count(int* out);
+/* Device-wide L2 fetch granularity for global-memory misses
+ * (cudaLimitMaxL2FetchGranularity: 32 / 64 / 128 bytes; 0 = leave as is).
+ * The fused gathers read small random code rows (25-96 B): a wider fetch
+ * than the row wastes DRAM bandwidth.  Set once per process by the Python
+ * facade from FG_L2_FETCH (default: leave the driver's setting). */
+int fg_set_l2_fetch_granularity(int bytes);
+int fg_get_l2_fetch_granularity(int* out);
 
 /* -------------------------------------------------------- code layout */
 /* Continuous reference stream (bitpack.py:17-36 layout, row_bits per row)

@@ -38,6 +38,8 @@ _SIGS = {
     "fg_version": (ci, []),
     "fg_launch_count": (i64, []),
     "fg_sm_count": (ci, [C.POINTER(ci)]),
+    "fg_set_l2_fetch_granularity": (ci, [ci]),
+    "fg_get_l2_fetch_granularity": (ci, [C.POINTER(ci)]),
     "fg_stream_to_rows": (ci, [vp, i64, i64, i64, vp, i64, vp]),
     "fg_rows_to_stream": (ci, [vp, i64, i64, i64, vp, i64, vp]),
     "fg_bits_pack": (ci, [vp, i64, ci, vp, vp, vp]),
@@ -163,9 +165,25 @@ def stream_handle(device=None) -> int:
     return torch.cuda.current_stream(device).cuda_stream
 
 
+_l2_set = False
+
+
 def require_cuda():
+    global _l2_set
     import torch
     if not torch.cuda.is_available():
         raise RuntimeError("featgrind-b200 requires a CUDA device (sm_100a); "
                            "there is no CPU fallback")
     lib()
+    if not _l2_set:
+        _l2_set = True
+        g = int(os.environ.get("FG_L2_FETCH", "0"))
+        if g:
+            torch.cuda.init()
+            call("fg_set_l2_fetch_granularity", g)
+
+
+def l2_fetch_granularity() -> int:
+    v = C.c_int()
+    call("fg_get_l2_fetch_granularity", C.byref(v))
+    return v.value

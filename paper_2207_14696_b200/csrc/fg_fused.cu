@@ -1366,10 +1366,12 @@ int launch_vq_w(const fg_codec_desc* c, const int32_t* indptr, const int32_t* sr
   const bool lp = std::is_same<OT, __nv_bfloat16>::value && c->table_lp != nullptr && W >= 4;
   if constexpr (std::is_same<OT, __nv_bfloat16>::value && (W == 4 || W == 8)) {
     // lane-per-part kernel (v5): sector slices of 32 parts, one CTA per SM.
-    // FG_VQ_LANE=0 keeps the v4 part-sliced kernel (A/B switch).
+    // Off by default (FG_VQ_LANE=1 enables it): measured on the B200 it ties
+    // v4 on MAG240M-shape (131.5 vs 131.1 us) and loses on products-shape
+    // (51.0 vs 36.9 us).
     static const int lane_env = [] {
       const char* e = getenv("FG_VQ_LANE");
-      return e ? atoi(e) : 1;
+      return e ? atoi(e) : 0;
     }();
     const int64_t lane_smem = (int64_t)32 * c->length * W * 2 + 2 * kSrcCap * 32 +
                               3 * kSrcCap * 4 + 4 * (kTD + 4) * 4;

@@ -45,6 +45,22 @@ int fg_version(void) { return 100; }
 
 int64_t fg_launch_count(void) { return (int64_t)__atomic_load_n(&g_launches, __ATOMIC_RELAXED); }
 
+int fg_set_l2_fetch_granularity(int bytes) {
+  FG_CHECK_ARG(bytes == 0 || bytes == 32 || bytes == 64 || bytes == 128,
+               "fg_set_l2_fetch_granularity: 32, 64 or 128 bytes (0 = query only)");
+  if (bytes) FG_CUDA_TRY(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)bytes));
+  size_t v = 0;
+  FG_CUDA_TRY(cudaDeviceGetLimit(&v, cudaLimitMaxL2FetchGranularity));
+  return (int)v == bytes || bytes == 0 ? FG_OK : FG_EUSAGE;
+}
+
+int fg_get_l2_fetch_granularity(int* out) {
+  size_t v = 0;
+  FG_CUDA_TRY(cudaDeviceGetLimit(&v, cudaLimitMaxL2FetchGranularity));
+  *out = (int)v;
+  return FG_OK;
+}
+
 int fg_sm_count(int* out) {
   FG_CHECK_ARG(out != nullptr, "fg_sm_count: null out");
   *out = sm_count();

@@ -25,6 +25,8 @@ def main():
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--check", action="store_true", help="compare against FG_VQ_LANE=0 output "
                     "computed in this process (fp32 kernel as reference)")
+    ap.add_argument("--l2", default="", help="comma list of L2 fetch granularities (bytes) "
+                    "to sweep in this process (fg_set_l2_fetch_granularity); default: as is")
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
     sg, dc, desc, fanouts, bs, hidden = bench.build_workload(a.config, dev)
@@ -34,6 +36,17 @@ def main():
     out = alloc_aggregate(smp.caps[L - 1], dc.d, torch.bfloat16, dev)
     flush = torch.zeros(128 * 1024 * 1024, dtype=torch.float32, device=dev)
     row_bytes = dc.num_parts * dc.bits / 8 if hasattr(dc, "num_parts") else dc.d * dc.params.k / 8
+    from paper_2207_14696_b200 import _native as N
+    grans = [int(x) for x in a.l2.split(",") if x] or [0]
+    base = smp.rng.clone()
+    for g in grans:
+        if g:
+            N.call("fg_set_l2_fetch_granularity", g)
+        smp.rng.copy_(base)
+        run(a, dc, smp, out, flush, row_bytes, L, N.l2_fetch_granularity())
+
+
+def run(a, dc, smp, out, flush, row_bytes, L, gran):
     ts, bts = [], []
     for i in range(a.iters + 3):
         sb = smp.sample(i)
@@ -60,7 +73,8 @@ def main():
     us = sum(ts) / len(ts) * 1e3
     gbs = sum(bts) / len(bts) / (us * 1e-6) / 1e9
     peak, _ = bench.load_peaks()
-    print(json.dumps({"config": a.config, "lane": os.environ.get("FG_VQ_LANE", "1"),
+    print(json.dumps({"config": a.config, "lane": os.environ.get("FG_VQ_LANE", "0"),
+                      "l2_fetch": gran,
                       "avg_us": round(us, 2), "min_us": round(min(ts) * 1e3, 2),
                       "alg_bytes": int(sum(bts) / len(bts)), "GBps": round(gbs, 1),
                       "frac": round(gbs / peak, 4)}))
