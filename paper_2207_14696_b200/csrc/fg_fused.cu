@@ -564,7 +564,12 @@ k_vq_mean8(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
 // count is dispatched once per item to a fully unrolled body, per-part smem
 // base addresses are precomputed, a zero "part" absorbs the lanes of a
 // partial last group, and every lookup is BFE + LEA + LDS + widen + FADD2.
-template <int W, int G, int C, bool WT = false>
+// PR (diagnostic builds selected by FG_FUSED_PROBE, tools/fused_bench.py):
+// bit 0 = no gather (sources from a 1024-row L2-resident set), bit 1 = no
+// decode (codes added as numbers, no shared-memory lookups), bit 2 = no
+// store (outputs kept only when impossible) -- to split the kernel's time
+// between the random row gather, the codebook decode and the output stream.
+template <int W, int G, int C, bool WT = false, int PR = 0>
 __device__ __forceinline__ void vq_fast_body(const uint8_t* __restrict__ rows, int64_t stride,
                                              const int32_t* sids, uint32_t base0,
                                              uint32_t pstride, int p0, u64* acc,
@@ -579,7 +584,10 @@ __device__ __forceinline__ void vq_fast_body(const uint8_t* __restrict__ rows, i
     for (int q = 0; q < G; ++q) {
       const uint32_t code = (cw[u][q >> 2] >> (8 * (q & 3))) & 0xFFu;
       const uint32_t addr = base0 + q * pstride + code * (uint32_t)(W * 2);
-      if constexpr (W == 4) {
+      if constexpr ((PR & 2) != 0) {
+        const float fc = (float)code;
+        acc[q * (W / 2)] = fadd2(acc[q * (W / 2)], pack2(fc, fc));
+      } else if constexpr (W == 4) {
         uint32_t x, y;
         asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(x), "=r"(y) : "r"(addr));
         const u64 wu = WT ? wt[u] : 0ull;
@@ -601,7 +609,7 @@ __device__ __forceinline__ void vq_fast_body(const uint8_t* __restrict__ rows, i
 
 constexpr int kFastThreads = 256;  // 3 CTAs/SM -> 85 registers: 32 fp32 accumulators fit
 
-template <int W, int G, bool WT = false>
+template <int W, int G, bool WT = false, int PR = 0>
 __global__ void __launch_bounds__(kFastThreads, 3)
 k_vq_mean8_fast(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
                 const __nv_bfloat16* __restrict__ books, int length, int parts,
@@ -677,21 +685,23 @@ k_vq_mean8_fast(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
 #pragma unroll
         for (int u = 0; u < 5; ++u)
           if (u < cb) {
-            sids[u] = sp[u];
+            sids[u] = (PR & 1) ? (int32_t)((v * 5 + u) & 1023) : sp[u];
             if constexpr (WT) wt[u] = bcast2(__ldg(ew + e0 + a + base + u));
           }
         switch (cb) {
-          case 1: vq_fast_body<W, G, 1, WT>(rows, stride, sids, base0, pstride, pg, acc, wt); break;
-          case 2: vq_fast_body<W, G, 2, WT>(rows, stride, sids, base0, pstride, pg, acc, wt); break;
-          case 3: vq_fast_body<W, G, 3, WT>(rows, stride, sids, base0, pstride, pg, acc, wt); break;
-          case 4: vq_fast_body<W, G, 4, WT>(rows, stride, sids, base0, pstride, pg, acc, wt); break;
-          default: vq_fast_body<W, G, 5, WT>(rows, stride, sids, base0, pstride, pg, acc, wt); break;
+          case 1: vq_fast_body<W, G, 1, WT, PR>(rows, stride, sids, base0, pstride, pg, acc, wt); break;
+          case 2: vq_fast_body<W, G, 2, WT, PR>(rows, stride, sids, base0, pstride, pg, acc, wt); break;
+          case 3: vq_fast_body<W, G, 3, WT, PR>(rows, stride, sids, base0, pstride, pg, acc, wt); break;
+          case 4: vq_fast_body<W, G, 4, WT, PR>(rows, stride, sids, base0, pstride, pg, acc, wt); break;
+          default: vq_fast_body<W, G, 5, WT, PR>(rows, stride, sids, base0, pstride, pg, acc, wt); break;
         }
       }
       const float inv = WT ? 1.0f : (cnt ? 1.0f / (float)cnt : 0.0f);
       const int64_t col0 = (int64_t)pg * W;
       __nv_bfloat16* o = out + v * ld + col0;
-      if (np == G && col0 + G * W <= d) {
+      if ((PR & 4) && lo2(acc[0]) != -1234.5f) {
+        // diagnostic: no store
+      } else if (np == G && col0 + G * W <= d) {
         store_scaled<G * W>(o, acc, inv, vec_ok);
       } else {
 #pragma unroll
@@ -1062,7 +1072,7 @@ __device__ __forceinline__ void sq_store(OT* o, const u64 (&acc)[8], float inv, 
 // sm_100): one instruction moves 4 code rows of 4 consecutive edges (row
 // indices as coordinates), 4x fewer issue slots than per-row bulk copies,
 // whose operands must be warp-uniform (a 32-step elect loop per warp).
-template <int K, typename OT, bool WT, bool G4 = false>
+template <int K, typename OT, bool WT, bool G4 = false, int PR = 0>
 __global__ void __launch_bounds__(kBulkThreads, 1)
 k_sq_mean_bulk(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
                const float* __restrict__ lut, const int32_t* __restrict__ indptr,
@@ -1125,7 +1135,7 @@ k_sq_mean_bulk(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
       const int e = edge_of(j);
       // G4 pads a partial last group with its last valid row (dummy copies
       // into buffer slack; never read)
-      if (e < ne) sid[j] = __ldg(src + e0 + e);
+      if (e < ne) sid[j] = (PR & 1) ? ((e0 + e) & 1023) : __ldg(src + e0 + e);
       else if (G4 && 4 * tid < ne) sid[j] = sid[j > 0 ? j - 1 : 0];
     }
   };
@@ -1212,8 +1222,14 @@ k_sq_mean_bulk(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
             if constexpr (WT) wt[u] = bcast2(__ldg(ewp + p + u));
           }
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
-            sq_accumulate<K, PAIR, WT>(acc, w[u][0], w[u][1], s_lut, s_lut2, lane, WT ? wt[u] : 0);
+          for (int u = 0; u < 4; ++u) {
+            if constexpr ((PR & 2) != 0) {
+              acc[u] = fadd2(acc[u], w[u][0] ^ w[u][1]);
+            } else {
+              sq_accumulate<K, PAIR, WT>(acc, w[u][0], w[u][1], s_lut, s_lut2, lane,
+                                         WT ? wt[u] : 0);
+            }
+          }
         }
         for (; p < cnt; ++p) {
           uint64_t w0, w1;
@@ -1241,7 +1257,8 @@ k_sq_mean_bulk(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
         }
       }
       const float inv = WT ? 1.0f : (cnt ? 1.0f / (float)cnt : 0.0f);
-      sq_store(out + v * ld + c * 16, acc, inv, c * 16, d, vec_ok);
+      if (!(PR & 4) || lo2(acc[0]) == -1234.5f)
+        sq_store(out + v * ld + c * 16, acc, inv, c * 16, d, vec_ok);
     }
     // slot k+3 (= k-1 mod 4) was last read before the previous barrier; the
     // barrier below publishes it and retires row buffer b for tile k+2
@@ -1301,6 +1318,23 @@ int launch_sq_w(const fg_codec_desc* c, const int32_t* indptr, const int32_t* sr
       const int smem = fixed + 128 + 2 * (g4 ? (row_cap / 4) * gstride : row_cap * rb);
       const int grid = (int)min64(ceil_div(max_dst, td), (int64_t)sm_count());
       auto kern = g4 ? k_sq_mean_bulk<K, OT, WT, true> : k_sq_mean_bulk<K, OT, WT, false>;
+      const int probe = [] {  // read per launch (diagnostic sweeps flip it in-process)  // diagnostics, see vq_fast_body
+        const char* e = getenv("FG_FUSED_PROBE");
+        return e ? atoi(e) : 0;
+      }();
+      if constexpr (!WT && K == 4) {
+        if (g4 && probe) {
+          switch (probe) {
+            case 1: kern = k_sq_mean_bulk<K, OT, WT, true, 1>; break;
+            case 2: kern = k_sq_mean_bulk<K, OT, WT, true, 2>; break;
+            case 3: kern = k_sq_mean_bulk<K, OT, WT, true, 3>; break;
+            case 4: kern = k_sq_mean_bulk<K, OT, WT, true, 4>; break;
+            case 5: kern = k_sq_mean_bulk<K, OT, WT, true, 5>; break;
+            case 6: kern = k_sq_mean_bulk<K, OT, WT, true, 6>; break;
+            default: break;
+          }
+        }
+      }
       FG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       kern<<<grid, kBulkThreads, smem, st>>>(c->rows, c->d, c->row_stride,
                                              (const float*)c->table, indptr, src, ndst, max_dst,
@@ -1406,7 +1440,22 @@ int launch_vq_w(const fg_codec_desc* c, const int32_t* indptr, const int32_t* sr
     if (lp && sp >= GF) {
       const int ns = (int)ceil_div(c->num_parts, sp);
       const int64_t fast_smem = smem_for(sp);
+      const int probe = [] {  // read per launch (diagnostic sweeps flip it in-process)
+        const char* e = getenv("FG_FUSED_PROBE");
+        return e ? atoi(e) : 0;
+      }();
       auto kern = k_vq_mean8_fast<W, GF, WT>;
+      if constexpr (!WT) {
+        switch (probe) {
+          case 1: kern = k_vq_mean8_fast<W, GF, WT, 1>; break;
+          case 2: kern = k_vq_mean8_fast<W, GF, WT, 2>; break;
+          case 3: kern = k_vq_mean8_fast<W, GF, WT, 3>; break;
+          case 4: kern = k_vq_mean8_fast<W, GF, WT, 4>; break;
+          case 5: kern = k_vq_mean8_fast<W, GF, WT, 5>; break;
+          case 6: kern = k_vq_mean8_fast<W, GF, WT, 6>; break;
+          default: break;
+        }
+      }
       FG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)fast_smem));
       // grid: a multiple of the slice count, ~3 CTAs per SM in total

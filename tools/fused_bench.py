@@ -25,6 +25,8 @@ def main():
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--check", action="store_true", help="compare against FG_VQ_LANE=0 output "
                     "computed in this process (fp32 kernel as reference)")
+    ap.add_argument("--probe", default="", help="comma list of FG_FUSED_PROBE diagnostic "
+                    "variants to sweep in this process (1 no gather, 2 no decode, 4 no store)")
     ap.add_argument("--l2", default="", help="comma list of L2 fetch granularities (bytes) "
                     "to sweep in this process (fg_set_l2_fetch_granularity); default: as is")
     a = ap.parse_args()
@@ -39,11 +41,14 @@ def main():
     from paper_2207_14696_b200 import _native as N
     grans = [int(x) for x in a.l2.split(",") if x] or [0]
     base = smp.rng.clone()
+    probes = [x for x in a.probe.split(",") if x] or [os.environ.get("FG_FUSED_PROBE", "0")]
     for g in grans:
         if g:
             N.call("fg_set_l2_fetch_granularity", g)
-        smp.rng.copy_(base)
-        run(a, dc, smp, out, flush, row_bytes, L, N.l2_fetch_granularity())
+        for pr in probes:
+            os.environ["FG_FUSED_PROBE"] = pr
+            smp.rng.copy_(base)
+            run(a, dc, smp, out, flush, row_bytes, L, N.l2_fetch_granularity())
 
 
 def run(a, dc, smp, out, flush, row_bytes, L, gran):
@@ -74,7 +79,7 @@ def run(a, dc, smp, out, flush, row_bytes, L, gran):
     gbs = sum(bts) / len(bts) / (us * 1e-6) / 1e9
     peak, _ = bench.load_peaks()
     print(json.dumps({"config": a.config, "lane": os.environ.get("FG_VQ_LANE", "0"),
-                      "l2_fetch": gran,
+                      "l2_fetch": gran, "probe": os.environ.get("FG_FUSED_PROBE", "0"),
                       "avg_us": round(us, 2), "min_us": round(min(ts) * 1e3, 2),
                       "alg_bytes": int(sum(bts) / len(bts)), "GBps": round(gbs, 1),
                       "frac": round(gbs / peak, 4)}))
