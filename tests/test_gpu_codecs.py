@@ -318,8 +318,8 @@ def test_vq_fit_products_geometry_matches_oracle():
     oracle/world.py), against the oracle fit (vq.py:166-303 restated,
     bit-exact to the reference on the golden cases) on the same rows: the
     k-means++ seeding draws the same numbers, so per-part objectives agree
-    to float64 summation-order noise except where a D^2 draw lands on a
-    prefix-sum boundary; bounded at 2 % either way."""
+    to float64 summation-order noise (a D^2 draw landing exactly on a
+    prefix-sum boundary could pick another point; not the case here)."""
     from oracle import codecs as oc
     from oracle import world as W
     lab = W.labels(2_449_029, 47, seed=0)
@@ -331,5 +331,6 @@ def test_vq_fit_products_geometry_matches_oracle():
     ref = np.array(ref)
     rel = np.abs(got - ref) / np.maximum(ref, 1e-30)
     print("products-geometry fit: per-part relative objective gap", np.sort(rel)[::-1][:5])
-    assert (rel <= 0.02).all(), rel
-    assert (rel <= 1e-6).mean() >= 0.8, rel
+    # measured on the B200: every part within 4e-16 (the same seeding draws
+    # and Lloyd step; only float64 summation order differs)
+    assert (rel <= 1e-9).all(), rel

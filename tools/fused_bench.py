@@ -27,6 +27,9 @@ def main():
                     "computed in this process (fp32 kernel as reference)")
     ap.add_argument("--probe", default="", help="comma list of FG_FUSED_PROBE diagnostic "
                     "variants to sweep in this process (1 no gather, 2 no decode, 4 no store)")
+    ap.add_argument("--flush", default="write", help="comma list of L2 flush modes to sweep: "
+                    "write (512 MB write) | write+read (then a 256 MB read, so the flush's "
+                    "dirty lines are written back before the timed launch)")
     ap.add_argument("--l2", default="", help="comma list of L2 fetch granularities (bytes) "
                     "to sweep in this process (fg_set_l2_fetch_granularity); default: as is")
     a = ap.parse_args()
@@ -37,6 +40,8 @@ def main():
     L = len(fanouts)
     out = alloc_aggregate(smp.caps[L - 1], dc.d, torch.bfloat16, dev)
     flush = torch.zeros(128 * 1024 * 1024, dtype=torch.float32, device=dev)
+    rflush = torch.zeros(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+    sink = torch.zeros(1, dtype=torch.float32, device=dev)
     row_bytes = dc.num_parts * dc.bits / 8 if hasattr(dc, "num_parts") else dc.d * dc.params.k / 8
     from paper_2207_14696_b200 import _native as N
     grans = [int(x) for x in a.l2.split(",") if x] or [0]
@@ -46,19 +51,22 @@ def main():
         if g:
             N.call("fg_set_l2_fetch_granularity", g)
         for pr in probes:
-            os.environ["FG_FUSED_PROBE"] = pr
-            smp.rng.copy_(base)
-            run(a, dc, smp, out, flush, row_bytes, L, N.l2_fetch_granularity())
+            for fm in a.flush.split(","):
+                os.environ["FG_FUSED_PROBE"] = pr
+                smp.rng.copy_(base)
+                fl = (lambda: flush.add_(1)) if fm == "write" else \
+                    (lambda: (flush.add_(1), torch.sum(rflush, dim=0, keepdim=True, out=sink)))
+                run(a, dc, smp, out, fl, row_bytes, L, N.l2_fetch_granularity(), fm)
 
 
-def run(a, dc, smp, out, flush, row_bytes, L, gran):
+def run(a, dc, smp, out, flush, row_bytes, L, gran, fm="write"):
     ts, bts = [], []
     for i in range(a.iters + 3):
         sb = smp.sample(i)
         torch.cuda.synchronize()
         E = int(sb.n_picks[L - 1].item())
         nd = int(sb.n_nodes[L - 1].item())
-        flush.add_(1)
+        flush()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
         gather_dequant_mean(dc, sb.indptr[L - 1], sb.picks[L - 1], sb.n_nodes[L - 1],
@@ -79,7 +87,7 @@ def run(a, dc, smp, out, flush, row_bytes, L, gran):
     gbs = sum(bts) / len(bts) / (us * 1e-6) / 1e9
     peak, _ = bench.load_peaks()
     print(json.dumps({"config": a.config, "lane": os.environ.get("FG_VQ_LANE", "0"),
-                      "l2_fetch": gran, "probe": os.environ.get("FG_FUSED_PROBE", "0"),
+                      "l2_fetch": gran, "flush": fm, "probe": os.environ.get("FG_FUSED_PROBE", "0"),
                       "avg_us": round(us, 2), "min_us": round(min(ts) * 1e3, 2),
                       "alg_bytes": int(sum(bts) / len(bts)), "GBps": round(gbs, 1),
                       "frac": round(gbs / peak, 4)}))
