@@ -70,6 +70,12 @@ typedef struct fg_codec_desc {
   int32_t elem_bits;   /* 32 or 64: decode precision of the table */
   const void* table_lp; /* optional bf16 copy of a VQ table (same layout);
                            used only by bf16-output aggregation, may be NULL */
+  const void* table_h;  /* optional fp16 copy of a VQ table, part p scaled by
+                           2^s_p so its largest |entry| is <= 2048 and every
+                           nonzero entry is a normal fp16 (the bf16-output
+                           mean accumulates it with HADD2 in chunks of <= 8
+                           picks); may be NULL (then table_lp is used) */
+  const float* part_scale; /* [num_parts] 2^-s_p (device), with table_h */
 } fg_codec_desc;
 
 /* ------------------------------------------------------------ library */

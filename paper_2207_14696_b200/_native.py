@@ -30,7 +30,7 @@ class CodecDesc(C.Structure):
     _fields_ = [("kind", i32), ("bits", i32), ("n", i64), ("d", i64),
                 ("row_stride", i64), ("rows", vp), ("table", vp),
                 ("width", i32), ("length", i32), ("num_parts", i32),
-                ("elem_bits", i32), ("table_lp", vp)]
+                ("elem_bits", i32), ("table_lp", vp), ("table_h", vp), ("part_scale", vp)]
 
 
 _SIGS = {

@@ -294,6 +294,284 @@ static int infwd_smem_bytes(int H, int P) {
   return H * P * 2 + kIfRows * P * 2 + 2 * (int)sizeof(Meta) + 8 * 32 * 4 + 8 + 16;
 }
 
+// ---------------------------------------------------------------- v2
+// Warp-specialised version (round 2; ncu of v1 on the papers100M-shape step:
+// 68.6 us, issue 27 %, 0.32 eligible warps, 1 CTA/SM at P = 144: every tile
+// serialised metadata loads -> row gathers -> MMA -> epilogue behind block
+// barriers).  One persistent CTA per SM, 10 warps:
+//   warp 0   producer: tile metadata (indptr window, per-edge source /
+//            destination / flush bits) and the cp.async gather of the edge
+//            sources' X rows into a 3-stage ring (meta + B operand), each
+//            lane's copies completing on the stage's `full` mbarrier
+//            (cp.async.mbarrier.arrive.noinc);
+//   warp 1   MMA issuer: D[acc] = W0 . X^T for 2 halves x P/16 K-steps into
+//            one of TWO TMEM accumulators (2 x H columns), committed to
+//            `acc_full`, so tile k+1's MMA runs under tile k's epilogue;
+//   warps 2-9 epilogue (unchanged math): TMEM -> ReLU -> per-destination
+//            sums -> bf16 rows + ReLU mask bits; they release the TMEM
+//            accumulator (`acc_empty`) and the stage (`empty`).
+constexpr int kIf2Threads = 320;
+constexpr int kIf2Stages = 3;
+
+__device__ __forceinline__ void if_wait(const uint64_t* bar, uint32_t parity) {
+  const uint32_t mb = if_smem(bar);
+  uint32_t done = 0;
+  while (!done)
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done) : "r"(mb), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void if_arrive(const uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(if_smem(bar)) : "memory");
+}
+
+template <bool WT>
+__global__ void __launch_bounds__(kIf2Threads, 1)
+k_input_block_mean_fwd2(const uint16_t* __restrict__ x, int P, const uint16_t* __restrict__ w0,
+                        int H, const int32_t* __restrict__ indptr,
+                        const int32_t* __restrict__ local, const int64_t* __restrict__ ndst_dev,
+                        int64_t max_dst, int D, const float* __restrict__ ew,
+                        uint16_t* __restrict__ out, int64_t out_ld, uint8_t* __restrict__ mbits) {
+  extern __shared__ __align__(1024) uint8_t if_mem[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int PB = P >> 3, HB = H >> 3;
+  uint8_t* sW = if_mem;                                            // W0: H x P (K-major)
+  uint8_t* sX0 = sW + H * P * 2;                                   // [stages] 128 x P
+  Meta* meta = reinterpret_cast<Meta*>(sX0 + kIf2Stages * kIfRows * P * 2);  // [stages]
+  uint32_t* s_bits = reinterpret_cast<uint32_t*>(meta + kIf2Stages);  // [8][32]
+  uint64_t* s_full = reinterpret_cast<uint64_t*>(s_bits + 8 * 32);   // [stages]
+  uint64_t* s_empty = s_full + kIf2Stages;                           // [stages]
+  uint64_t* s_accf = s_empty + kIf2Stages;                           // [2]
+  uint64_t* s_acce = s_accf + 2;                                     // [2]
+  uint64_t* s_wbar = s_acce + 2;                                     // W0 loaded
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(s_wbar + 1);
+
+  const int64_t live = min64(*ndst_dev, max_dst);
+  {  // rows past the live destinations: zeros + the bias column
+    const int64_t och = out_ld >> 3;
+    for (int64_t i = (int64_t)blockIdx.x * kIf2Threads + tid; i < (max_dst - live) * och;
+         i += (int64_t)gridDim.x * kIf2Threads) {
+      const int64_t v = live + i / och, c = i - (i / och) * och;
+      reinterpret_cast<uint4*>(out + v * out_ld)[c] =
+          c < HB ? make_uint4(0u, 0u, 0u, 0u) : make_uint4(0x3F80u, 0u, 0u, 0u);
+    }
+  }
+  const int64_t ntiles = (live + D - 1) / D;
+  if ((int64_t)blockIdx.x >= ntiles) return;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 ::"r"(if_smem(s_tmem)), "r"((uint32_t)(2 * H)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 32) {
+    for (int s = 0; s < kIf2Stages; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 33;" ::"r"(if_smem(s_full + s)));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 8;" ::"r"(if_smem(s_empty + s)));
+    }
+    for (int a = 0; a < 2; ++a) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(if_smem(s_accf + a)));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 8;" ::"r"(if_smem(s_acce + a)));
+    }
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(if_smem(s_wbar)), "r"(kIf2Threads));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *s_tmem;
+  // W0 -> K-major operand by everyone, completion on s_wbar (the MMA waits)
+  for (int i = tid; i < H * PB; i += kIf2Threads) {
+    const int n = i / PB, c = i - n * PB;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;"
+                 ::"r"(if_smem(sW) + if_off(n, c, PB)), "l"(w0 + (int64_t)n * P + c * 8)
+                 : "memory");
+  }
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(if_smem(s_wbar))
+               : "memory");
+  const int halves = H >> 7;
+  const int64_t G = gridDim.x;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    int k = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += G, ++k) {
+      const int s = k % kIf2Stages, use = k / kIf2Stages;
+      if (use > 0) if_wait(s_empty + s, (uint32_t)((use - 1) & 1));
+      Meta& m = meta[s];
+      const int64_t v0 = tile * D;
+      const int nd = (int)min64(D, live - v0);
+      for (int t = lane; t <= nd; t += 32) m.ip[t] = __ldg(indptr + v0 + t);
+      __syncwarp();
+      const int32_t e0 = m.ip[0];
+      const int ne = m.ip[nd] - e0;
+      int32_t lv[kIfRows / 32];
+#pragma unroll
+      for (int q = 0; q < kIfRows / 32; ++q) {
+        const int r = lane + 32 * q;
+        lv[q] = r < ne ? __ldg(local + e0 + r) : -1;
+      }
+#pragma unroll
+      for (int q = 0; q < kIfRows / 32; ++q) {
+        const int r = lane + 32 * q;
+        int j = 0;
+        bool last = false;
+        if (r < ne) {
+          int lo = 0, hi = nd;
+          while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (m.ip[mid] - e0 <= r) lo = mid; else hi = mid;
+          }
+          j = lo;
+          last = r + 1 == m.ip[j + 1] - e0;
+          if (WT) m.w[r] = __ldg(ew + e0 + r);
+        }
+        m.l[r] = lv[q];
+        m.j[r] = j;
+        const unsigned fm = __ballot_sync(0xFFFFFFFFu, last);
+        if (lane == 0) m.fmask[q] = fm;
+        int cnt = 1;
+        if (r < nd) {
+          cnt = m.ip[r + 1] - m.ip[r];
+          m.inv[r] = WT ? 1.f : (cnt ? 1.0f / (float)cnt : 0.f);
+        }
+        const unsigned em = __ballot_sync(0xFFFFFFFFu, cnt == 0);
+        if (lane == 0) m.emask[q] = em;
+      }
+      // B = X rows of the edge sources (dead rows zero-filled)
+      const uint32_t xb = if_smem(sX0) + (uint32_t)(s * kIfRows * P * 2);
+#pragma unroll
+      for (int q = 0; q < kIfRows / 32; ++q) {
+        const int r = lane + 32 * q;
+        const int32_t l = lv[q];
+        const uint16_t* rowp = x + (int64_t)(l >= 0 ? l : 0) * P;
+        for (int c = 0; c < PB; ++c)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;"
+                       ::"r"(xb + if_off(r, c, PB)), "l"(rowp + c * 8), "r"(l >= 0 ? 16 : 0)
+                       : "memory");
+      }
+      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(if_smem(s_full + s))
+                   : "memory");
+      __syncwarp();
+      if (lane == 0) if_arrive(s_full + s);  // releases the metadata stores
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if_wait(s_wbar, 0);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    const uint32_t idesc = if_idesc(kIfRows);
+    const uint32_t lbo = 128, sbo = (uint32_t)PB * 128;
+    int k = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += G, ++k) {
+      const int s = k % kIf2Stages, a = k & 1;
+      if_wait(s_full + s, (uint32_t)((k / kIf2Stages) & 1));
+      if (k >= 2) if_wait(s_acce + a, (uint32_t)(((k >> 1) - 1) & 1));
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      if (lane == 0) {
+        const uint32_t xb = if_smem(sX0) + (uint32_t)(s * kIfRows * P * 2);
+        for (int hf = 0; hf < halves; ++hf) {
+          for (int ks = 0; ks < PB / 2; ++ks) {
+            const uint32_t off = (uint32_t)ks * 256;
+            const uint64_t ad = if_desc(if_smem(sW) + (uint32_t)hf * 16 * sbo + off, lbo, sbo);
+            const uint64_t bd = if_desc(xb + off, lbo, sbo);
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n"
+                ::"r"(tmem + (uint32_t)(a * H + hf * kIfRows)), "l"(ad), "l"(bd), "r"(idesc),
+                  "r"(ks > 0 ? 1u : 0u));
+          }
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                     ::"r"(if_smem(s_accf + a)) : "memory");
+      }
+      __syncwarp();
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int ew_ = warp - 2;                 // 0..7
+    const int half = ew_ >> 2;                // warps 2-5: features 0..127
+    const bool epi = half < halves;
+    const int q4 = warp & 3;                  // TMEM lane quarter of this warp
+    const int fbase = half * 128 + q4 * 32;
+    const int f = fbase + lane;
+    uint32_t* wbits = s_bits + ew_ * 32;
+    int k = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += G, ++k) {
+      const int s = k % kIf2Stages, a = k & 1;
+      if_wait(s_accf + a, (uint32_t)((k >> 1) & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const Meta& m = meta[s];
+      const int64_t v0 = tile * D;
+      const int nd = (int)min64(D, live - v0);
+      const int ne = m.ip[nd] - m.ip[0];
+      if (epi) {
+        uint16_t* orow = out + v0 * out_ld + f;
+        float acc = 0.f;
+        for (int c0 = 0; c0 < ne; c0 += 32) {
+          uint32_t v[32];
+          const uint32_t ta = tmem + ((uint32_t)(q4 * 32) << 16) +
+                              (uint32_t)(a * H + half * kIfRows + c0);
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+              "%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+                "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]),
+                "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]),
+                "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+                "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
+                "=r"(v[30]), "=r"(v[31])
+              : "r"(ta));
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          const uint32_t fmask = m.fmask[c0 >> 5];
+#pragma unroll
+          for (int t = 0; t < 32; ++t) {
+            const float h = __uint_as_float(v[t]);
+            const unsigned mk = __ballot_sync(0xFFFFFFFFu, h > 0.f);
+            if (lane == 0) wbits[t] = mk;
+            if (WT) acc = fmaf(fmaxf(h, 0.f), m.w[c0 + t], acc);
+            else acc += fmaxf(h, 0.f);
+            if ((fmask >> t) & 1u) {
+              const int j = m.j[c0 + t];
+              orow[(int64_t)j * out_ld] = __bfloat16_as_ushort(__float2bfloat16_rn(acc * m.inv[j]));
+              acc = 0.f;
+            }
+          }
+          __syncwarp();
+          if (c0 + lane < ne)
+            *reinterpret_cast<uint32_t*>(mbits + (int64_t)m.l[c0 + lane] * HB + (fbase >> 3)) =
+                wbits[lane];
+          __syncwarp();
+        }
+      }
+      // TMEM accumulator a is drained: the MMA of tile k+2 may overwrite it
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncwarp();
+      if (lane == 0) if_arrive(s_acce + a);
+      if (epi) {
+        uint16_t* orow = out + v0 * out_ld + f;
+        for (int q = 0; q * 32 < nd; ++q)  // destinations without edges
+          for (uint32_t em = m.emask[q]; em; em &= em - 1)
+            orow[(int64_t)(q * 32 + __ffs(em) - 1) * out_ld] = 0;
+      }
+      if (out_ld > H && ew_ == 0)  // bias column block [1, 0, ..., 0]
+        for (int t = lane; t < nd; t += 32)
+          reinterpret_cast<uint4*>(out + (v0 + t) * out_ld + H)[0] = make_uint4(0x3F80u, 0u, 0u, 0u);
+      __syncwarp();
+      if (lane == 0) if_arrive(s_empty + s);  // metadata + B stage free
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"((uint32_t)(2 * H)));
+}
+
+static int infwd2_smem_bytes(int H, int P) {
+  return H * P * 2 + kIf2Stages * kIfRows * P * 2 + kIf2Stages * (int)sizeof(Meta) + 8 * 32 * 4 +
+         (2 * kIf2Stages + 5) * 8 + 16;
+}
+
 }  // namespace fg
 
 using namespace fg;
@@ -319,6 +597,23 @@ extern "C" int fg_input_block_mean_fwd(const uint16_t* x, int64_t P, const uint1
   if (out_ld == 0) out_ld = H;
   FG_CHECK_ARG(out_ld == H || out_ld == H + 8, "out_ld must be H or H + 8 (ones column)");
   if (max_dst == 0) return FG_OK;
+  const int D = (int)min64(kIfRows / fanout, kIfRows - 1);
+  static const int v2_env = [] {  // FG_INFWD_V2=0: the v1 kernel (A/B)
+    const char* e = getenv("FG_INFWD_V2");
+    return e ? atoi(e) : 1;
+  }();
+  const int smem2 = infwd2_smem_bytes((int)H, (int)P);
+  if (v2_env && smem2 <= 227 * 1024) {
+    auto kern2 = edge_w ? k_input_block_mean_fwd2<true> : k_input_block_mean_fwd2<false>;
+    FG_CUDA_TRY(cudaFuncSetAttribute(kern2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2));
+    const int64_t tiles = (max_dst + D - 1) / D;
+    const int grid = (int)max64(1, min64(tiles, (int64_t)sm_count()));
+    kern2<<<grid, kIf2Threads, smem2, as_stream(s)>>>(
+        x, (int)P, w0, (int)H, indptr, local, n_dst_dev, max_dst, D, edge_w, out, out_ld,
+        relu_bits);
+    FG_LAUNCH_CHECK();
+    return FG_OK;
+  }
   const int smem = infwd_smem_bytes((int)H, (int)P);
   auto kern = edge_w ? k_input_block_mean_fwd<true> : k_input_block_mean_fwd<false>;
   FG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -332,7 +627,6 @@ extern "C" int fg_input_block_mean_fwd(const uint16_t* x, int64_t P, const uint1
   int per_sm = smem_sm / (smem + 1024);
   per_sm = per_sm < 1 ? 1 : (per_sm > 512 / (int)H ? 512 / (int)H : per_sm);
   // s_ip holds D + 1 <= 128 entries
-  const int D = (int)min64(kIfRows / fanout, kIfRows - 1);
   const int64_t tiles = (max_dst + D - 1) / D;
   static const int ctas_env = [] {  // FG_INFWD_CTAS: grid override (tests, probes)
     const char* e = getenv("FG_INFWD_CTAS");
