@@ -462,6 +462,11 @@ int fg_bitmap_compact(uint32_t* bitmap, int64_t n, int32_t* out_ids,
                       int32_t* word_prefix, void* workspace,
                       int64_t workspace_bytes, void* cuda_stream);
 int64_t fg_bitmap_workspace_bytes(int64_t n);
+/* Sorted copy of <= 4096 int64 ids (< n < 2^31) as int32 (pipeline.py:203,
+ * np.sort of a batch's seeds; duplicates kept), one CTA radix sort; count
+ * taken from the device scalar *cnt (clamped to cap), written to *out_cnt. */
+int fg_sort_ids(const int64_t* ids, const int64_t* cnt, int64_t cap, int32_t* out,
+                int64_t* out_cnt, int64_t n, void* cuda_stream);
 int fg_bitmap_rank(const int32_t* ids, const int64_t* count_dev, int64_t max_count,
                    const uint32_t* bitmap, const int32_t* word_prefix,
                    int32_t* rank_out, void* cuda_stream);

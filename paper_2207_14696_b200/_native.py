@@ -101,6 +101,7 @@ _SIGS = {
     "fg_bitmap_compact": (ci, [vp, i64, vp, i64, vp, vp, vp, i64, vp]),
     "fg_bitmap_workspace_bytes": (i64, [i64]),
     "fg_bitmap_rank": (ci, [vp, vp, i64, vp, vp, vp, vp]),
+    "fg_sort_ids": (ci, [vp, vp, i64, vp, vp, i64, vp]),
     "fg_bitmap_clear": (ci, [vp, vp, i64, vp, i64, vp]),
     "fg_synth_features": (ci, [ci, u64, i64, i64, i64, vp, ci, vp, vp]),
     "fg_synth_feature_rows": (ci, [ci, u64, vp, i64, i64, vp, ci, vp, vp]),

@@ -1358,536 +1358,11 @@ static bool code_row_tensor_map(const fg_codec_desc* c, int rb, CUtensorMap* m) 
          CUDA_SUCCESS;
 }
 
-// ------------------------------ VQ v6: warp-specialised, sector-sliced (8-bit, bf16)
-// Round 2 (after ncu: v4 issue 39 % with 2x DRAM read amplification, 2x
-// partial-sector stores and 59 % shared-memory bank conflicts; v5 issue-bound
-// at 73 %).  For 8-bit codes, W in {4, 8}, bf16 output:
-//  * slices of 32 parts = one 32-B sector of the code row; CTA b serves slice
-//    b % ns of every tile (MAG240M-shape: 3 slices, 128 KB of fp16 codebook
-//    per CTA), so each sector is fetched from DRAM exactly once;
-//  * warp 0 produces: per tile it stages the indptr window and fetches the
-//    slice's sector of every pick with TMA tensor gathers (tile::gather4: 4
-//    rows of 32 B = one contiguous 128-B group per instruction) into a
-//    4-stage smem ring, tracked by full / empty mbarriers -- tiles run up to
-//    4 ahead of the decode, with no block-wide barrier in the loop;
-//  * warps 1..15 consume: one destination per warp at a time, lane = part:
-//    the pick's code byte is lane-contiguous in the staged sector (one
-//    wavefront per pick), the entry lookup hits a conflict-free bank group
-//    (part p's entries at byte (p % PPL) * EB of 128-B lines), and the
-//    warp's output segment (32 parts x W bf16 = 256 / 512 B) is one
-//    coalesced full-sector store;
-//  * F16: codebook entries in fp16 scaled per part (table_h, part_scale),
-//    accumulated with HADD2 over chunks of <= 8 picks then widened to fp32:
-//    one LDS + W/2 HADD2 per lookup instead of LDS + W unpacks + W/2 FADD2.
-//    Without table_h (or for weighted sums) the bf16 table with fp32 FADD2 /
-//    FFMA2 accumulation is used.
-constexpr int kV6Threads = 512;
-constexpr int kV6Cons = kV6Threads / 32 - 1;  // consumer warps
-constexpr int kV6TD = 64;                      // destinations per tile
-constexpr int kV6Cap = kV6TD * 8;              // staged picks per tile (fanout <= 8)
-constexpr int kV6Stages = 4;
-constexpr int kV6IpPitch = kV6TD + 4;
-
-__device__ __forceinline__ void v6_wait(uint32_t bar, uint32_t parity) {
-  uint32_t done = 0;
-  while (!done)
-    asm volatile(
-        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-        : "=r"(done) : "r"(bar), "r"(parity) : "memory");
-}
-
-
-// v6 producer (warp 0): software-pipelined over tiles -- the indptr window
-// of tile k+2 and the source ids of tile k+1 are loaded into registers while
-// tile k's TMA gathers are issued, so each tile costs the producer one
-// overlapped global round trip instead of three serial ones.  Lane l owns
-// gather groups l + 32 i (4 picks each, i < 4: td * 8 <= 512 picks).
-struct V6Pref {
-  int32_t ip[3];    // indptr entries lane, lane + 32, lane + 64 of the window
-  int32_t sid[16];  // source ids of groups lane + 32 i, 4 per group
-  int32_t e0, ne;   // tile edge range (uniform)
-};
-__device__ __forceinline__ void v6_load_ip(V6Pref& p, const int32_t* __restrict__ indptr,
-                                           int64_t v0, int nd, int lane) {
-#pragma unroll
-  for (int q = 0; q < 3; ++q) {
-    const int t = lane + 32 * q;
-    p.ip[q] = t <= nd ? __ldg(indptr + v0 + t) : 0;
-  }
-}
-__device__ __forceinline__ int32_t v6_ip_at(const V6Pref& p, int t) {
-  const int32_t a = __shfl_sync(0xFFFFFFFFu, p.ip[0], t & 31);
-  const int32_t b = __shfl_sync(0xFFFFFFFFu, p.ip[1], t & 31);
-  const int32_t c = __shfl_sync(0xFFFFFFFFu, p.ip[2], t & 31);
-  return t < 32 ? a : (t < 64 ? b : c);
-}
-__device__ __forceinline__ void v6_load_sid(V6Pref& p, const int32_t* __restrict__ src, int nd,
-                                            int cap, int lane) {
-  p.e0 = v6_ip_at(p, 0);
-  p.ne = v6_ip_at(p, nd) - p.e0;
-  const int groups = p.ne <= cap ? (p.ne + 3) >> 2 : 0;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int g = lane + 32 * i;
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-      p.sid[4 * i + u] = g < groups ? __ldg(src + p.e0 + min(4 * g + u, p.ne - 1)) : 0;
-  }
-}
-
-__device__ __forceinline__ void v6_producer(int64_t tile0, int64_t tstep, int64_t ntiles,
-                                            int64_t live, int td, int cap, int stages,
-                                            const int32_t* __restrict__ indptr,
-                                            const int32_t* __restrict__ src, int32_t* s_ip,
-                                            uint64_t* s_full, uint64_t* s_empty,
-                                            uint8_t* s_codes, int row_bytes, int xcoord,
-                                            const CUtensorMap* tmap, int lane) {
-  auto nd_of = [&](int64_t tile) { return (int)min64(td, live - tile * td); };
-  V6Pref cur, nxt, nn;
-  v6_load_ip(cur, indptr, tile0 * td, nd_of(tile0), lane);
-  v6_load_sid(cur, src, nd_of(tile0), cap, lane);
-  if (tile0 + tstep < ntiles) v6_load_ip(nxt, indptr, (tile0 + tstep) * td, nd_of(tile0 + tstep), lane);
-  int k = 0;
-  for (int64_t tile = tile0; tile < ntiles; tile += tstep, ++k) {
-    const int s = k % stages, use = k / stages;
-    const int nd = nd_of(tile);
-    const bool has1 = tile + tstep < ntiles, has2 = tile + 2 * tstep < ntiles;
-    // next tiles' metadata in flight while this one waits and issues
-    if (has1) v6_load_sid(nxt, src, nd_of(tile + tstep), cap, lane);
-    if (has2) v6_load_ip(nn, indptr, (tile + 2 * tstep) * td, nd_of(tile + 2 * tstep), lane);
-    if (use > 0) v6_wait(smem_addr(s_empty + s), (uint32_t)((use - 1) & 1));
-    int32_t* ip = s_ip + s * kV6IpPitch;
-#pragma unroll
-    for (int q = 0; q < 3; ++q)
-      if (lane + 32 * q <= nd) ip[lane + 32 * q] = cur.ip[q];
-    const uint32_t groups = cur.ne <= cap ? (uint32_t)((cur.ne + 3) >> 2) : 0u;
-    const uint32_t full = smem_addr(s_full + s);
-    __syncwarp();
-    if (lane == 0)
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
-                   ::"r"(full), "r"(groups * (uint32_t)(4 * row_bytes)) : "memory");
-    __syncwarp();
-    uint8_t* dst = s_codes + (size_t)s * cap * row_bytes;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const uint32_t g = (uint32_t)(lane + 32 * i);
-      if (g < groups)
-        asm volatile(
-            "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
-            " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];"
-            ::"r"(smem_addr(dst + (size_t)g * 4 * row_bytes)),
-              "l"(reinterpret_cast<uint64_t>(tmap)), "r"(xcoord), "r"(cur.sid[4 * i]),
-              "r"(cur.sid[4 * i + 1]), "r"(cur.sid[4 * i + 2]), "r"(cur.sid[4 * i + 3]),
-              "r"(full)
-            : "memory");
-    }
-    cur = nxt;
-    nxt = nn;
-  }
-}
-
-template <int W, bool F16, bool WT>
-__global__ void __launch_bounds__(kV6Threads, 1)
-k_vq_mean_v6(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
-             const uint16_t* __restrict__ books, const float* __restrict__ part_scale,
-             int length, int parts, const int32_t* __restrict__ indptr,
-             const int32_t* __restrict__ src, const int64_t* __restrict__ ndst_dev,
-             int64_t max_dst, __nv_bfloat16* __restrict__ out, int64_t ld, int nslices,
-             const float* __restrict__ ew, const __grid_constant__ CUtensorMap tmap) {
-  constexpr int EB = W * 2;        // bytes per entry (fp16 / bf16)
-  constexpr int PPL = 128 / EB;    // parts per 128-B line
-  constexpr int NA = W / 2;        // 32-bit words per entry
-  extern __shared__ __align__(1024) uint8_t s_raw[];
-  const int slice = (int)(blockIdx.x % nslices);
-  const int64_t live = live_dst(ndst_dev, max_dst);
-  const int64_t ntiles = (live + kV6TD - 1) / kV6TD;
-  const int64_t tile0 = blockIdx.x / nslices, tstep = gridDim.x / nslices;
-  if (tile0 >= ntiles) return;
-  const int lparts = min(32, parts - slice * 32);
-  uint8_t* const s_book = s_raw;                                       // (32/PPL)*L lines
-  uint8_t* const s_codes = s_book + (size_t)(32 / PPL) * length * 128;  // [stages][cap][32]
-  int32_t* const s_ip = reinterpret_cast<int32_t*>(s_codes + (size_t)kV6Stages * kV6Cap * 32);
-  uint64_t* const s_full = reinterpret_cast<uint64_t*>(s_ip + kV6Stages * kV6IpPitch);
-  uint64_t* const s_empty = s_full + kV6Stages;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) {
-    for (int s = 0; s < kV6Stages; ++s) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(s_full + s)));
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(s_empty + s)),
-                   "r"(kV6Cons));
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;");
-  }
-  __syncthreads();
-  const int sector_off = slice * 32;
-
-  if (warp == 0) {
-    v6_producer(tile0, tstep, ntiles, live, kV6TD, kV6Cap, kV6Stages, indptr, src, s_ip, s_full,
-                s_empty, s_codes, 32, sector_off, &tmap, lane);
-    return;
-  }
-  // ------------------------------------------------------------ consumers
-  {
-    // codebook slice -> interleaved lines (consumers only; one named barrier)
-    const int nent = lparts * length;
-    const uint8_t* g = reinterpret_cast<const uint8_t*>(books) + (size_t)slice * 32 * length * EB;
-    for (int c = tid - 32; c < nent; c += kV6Threads - 32) {
-      const int lp = c / length, e = c - lp * length;
-      uint8_t* dst = s_book + ((size_t)(lp / PPL) * length + e) * 128 + (lp % PPL) * EB;
-      if constexpr (EB == 16)
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)),
-                     "l"(g + (size_t)c * EB) : "memory");
-      else
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr(dst)),
-                     "l"(g + (size_t)c * EB) : "memory");
-    }
-    asm volatile("cp.async.wait_all;" ::: "memory");
-    asm volatile("bar.sync 1, %0;" ::"r"(kV6Threads - 32) : "memory");
-  }
-  const int cw = warp - 1;
-  const bool active = lane < lparts;
-  const uint32_t lbase = smem_addr(s_book) + (uint32_t)((lane / PPL) * length * 128 + (lane % PPL) * EB);
-  const int64_t col0 = (int64_t)(slice * 32 + lane) * W;
-  const bool full_part = col0 + W <= d;
-  const bool vec_ok = (ld % 8) == 0;
-  const float pscale = (F16 && active) ? __ldg(part_scale + slice * 32 + lane) : 1.0f;
-  int k = 0;
-  for (int64_t tile = tile0; tile < ntiles; tile += tstep, ++k) {
-    const int s = k % kV6Stages;
-    v6_wait(smem_addr(s_full + s), (uint32_t)((k / kV6Stages) & 1));
-    const int32_t* ip = s_ip + s * kV6IpPitch;
-    const uint8_t* codes = s_codes + (size_t)s * kV6Cap * 32;
-    const int64_t v0 = tile * kV6TD;
-    const int nd = (int)min64(kV6TD, live - v0);
-    const int32_t e0 = ip[0];
-    const bool staged = ip[nd] - e0 <= kV6Cap;
-    for (int vl = cw; vl < nd; vl += kV6Cons) {
-      const int a = ip[vl] - e0;
-      const int cnt = ip[vl + 1] - e0 - a;
-      u64 acc[NA];
-#pragma unroll
-      for (int j = 0; j < NA; ++j) acc[j] = 0ull;
-      for (int u0 = 0; u0 < cnt; u0 += 8) {
-        const int cb = min(cnt - u0, 8);
-        uint32_t code[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (u < cb) {
-            const int e = a + u0 + u;
-            code[u] = staged ? (uint32_t)codes[e * 32 + lane]
-                             : (uint32_t)__ldg(rows + (int64_t)__ldg(src + e0 + e) * stride +
-                                               sector_off + lane);
-          }
-        if (active) {
-          if constexpr (F16) {
-            uint32_t h[NA];
-#pragma unroll
-            for (int j = 0; j < NA; ++j) h[j] = 0u;
-#pragma unroll
-            for (int u = 0; u < 8; ++u)
-              if (u < cb) {
-                const uint32_t addr = lbase + code[u] * 128u;
-                if constexpr (W == 8) {
-                  uint32_t x, y, z, w;
-                  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
-                               : "=r"(x), "=r"(y), "=r"(z), "=r"(w) : "r"(addr));
-                  h[0] = hadd2u(h[0], x); h[1] = hadd2u(h[1], y);
-                  h[2] = hadd2u(h[2], z); h[3] = hadd2u(h[3], w);
-                } else {
-                  uint32_t x, y;
-                  asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(x), "=r"(y) : "r"(addr));
-                  h[0] = hadd2u(h[0], x); h[1] = hadd2u(h[1], y);
-                }
-              }
-#pragma unroll
-            for (int j = 0; j < NA; ++j) acc[j] = fadd2(acc[j], h2_to_f32x2(h[j]));
-          } else {
-#pragma unroll
-            for (int u = 0; u < 8; ++u)
-              if (u < cb) {
-                const uint32_t addr = lbase + code[u] * 128u;
-                const u64 wu = WT ? bcast2(__ldg(ew + e0 + a + u0 + u)) : 0ull;
-                uint32_t q[4];
-                if constexpr (W == 8)
-                  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
-                               : "=r"(q[0]), "=r"(q[1]), "=r"(q[2]), "=r"(q[3]) : "r"(addr));
-                else
-                  asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(q[0]), "=r"(q[1]) : "r"(addr));
-#pragma unroll
-                for (int j = 0; j < NA; ++j) acc[j] = acc2<WT>(acc[j], bf16x2_to_f32x2(q[j]), wu);
-              }
-          }
-        }
-      }
-      if (active) {
-        const float inv = (WT ? 1.0f : (cnt ? 1.0f / (float)cnt : 0.0f)) * pscale;
-        __nv_bfloat16* o = out + (v0 + vl) * ld + col0;
-        if (full_part) {
-          store_scaled<W>(o, acc, inv, vec_ok);
-        } else {
-#pragma unroll
-          for (int j = 0; j < W; ++j)
-            if (col0 + j < d)
-              o[j] = __float2bfloat16_rn((j & 1 ? hi2(acc[j / 2]) : lo2(acc[j / 2])) * inv);
-        }
-      }
-    }
-    __syncwarp();
-    if (lane == 0)
-      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(s_empty + s))
-                   : "memory");
-  }
-}
-
-static int64_t v6_smem_bytes(int W, int length) {
-  return (int64_t)(32 / (128 / (W * 2))) * length * 128 + (int64_t)kV6Stages * kV6Cap * 32 +
-         (int64_t)kV6Stages * kV6IpPitch * 4 + 2 * kV6Stages * 8;
-}
-
-// v6 launch for 8-bit VQ codes with bf16 output; returns false when the
-// shape is not covered (the caller falls back to v4)
-template <int W, bool WT>
-static bool launch_vq_v6(const fg_codec_desc* c, const int32_t* indptr, const int32_t* src,
-                         const int64_t* ndst, int64_t max_dst, void* out, int64_t ld,
-                         cudaStream_t st, const float* ew, int* rc) {
-  const char* e = getenv("FG_VQ_V6");  // off by default (measured slower)
-  if (!e || atoi(e) == 0) return false;
-  if (c->bits != 8 || c->length > 256 || c->row_stride % 32 != 0 ||
-      c->row_stride < 32 * ceil_div(c->num_parts, 32) || c->table_lp == nullptr)
-    return false;
-  const int64_t smem = v6_smem_bytes(W, c->length);
-  if (smem > 227 * 1024) return false;
-  CUtensorMap tmap;
-  if (!code_row_tensor_map(c, 32, &tmap)) return false;
-  const char* ef = getenv("FG_VQ_F16");  // A/B switch: 0 = bf16 table, fp32 sums
-  const bool f16 = !WT && c->table_h != nullptr && c->part_scale != nullptr &&
-                   !(ef && atoi(ef) == 0);
-  const int ns = (int)ceil_div(c->num_parts, 32);
-  const int64_t ntiles = ceil_div(max_dst, kV6TD);
-  const int64_t per_slice = std::max<int64_t>(1, min64(ntiles, sm_count() / ns));
-  auto kern = f16 ? k_vq_mean_v6<W, true, false> : k_vq_mean_v6<W, false, WT>;
-  *rc = FG_OK;
-  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-  if (err != cudaSuccess) {
-    set_error("v6 smem attribute: %s", cudaGetErrorString(err));
-    *rc = FG_ECUDA;
-    return true;
-  }
-  kern<<<(int)(per_slice * ns), kV6Threads, smem, st>>>(
-      c->rows, c->d, c->row_stride,
-      (const uint16_t*)(f16 ? c->table_h : c->table_lp), c->part_scale, c->length,
-      c->num_parts, indptr, src, ndst, max_dst, (__nv_bfloat16*)out, ld, ns, ew, tmap);
-  count_launch();
-  err = cudaGetLastError();
-  if (err != cudaSuccess) {
-    set_error("k_vq_mean_v6 launch: %s", cudaGetErrorString(err));
-    *rc = FG_ECUDA;
-  }
-  return true;
-}
-
-// ------------------------------ SQ v6: the same producer / consumer pipeline
-// For k in {4, 8} with whole 32-B code sectors per row (d*k/8 = 32*NB,
-// papers100M-shape k=4 d=128: NB=2; arxiv-shape k=8 d=128: NB=4), bf16
-// output.  Warp 0 stages whole code rows by tile::gather4 (box = the row's
-// RB bytes) into a 4-stage ring; consumer warps take one destination at a
-// time, lane l owns code bytes [l*NB, l*NB+NB) -> EPL = 8*NB/k consecutive
-// outputs, so a pick costs one 2/4-byte shared load, NB lookups in a
-// lane-private replicated table (k=4: decoded byte PAIRS, 8 B; k=8: 4 B) and
-// EPL/2 FADD2s, and the destination's row is one coalesced store.
-template <int K, int NB, bool WT>
-__global__ void __launch_bounds__(kV6Threads, 1)
-k_sq_mean_v6(const uint8_t* __restrict__ rows, int64_t stride, const float* __restrict__ lut,
-             const int32_t* __restrict__ indptr, const int32_t* __restrict__ src,
-             const int64_t* __restrict__ ndst_dev, int64_t max_dst,
-             __nv_bfloat16* __restrict__ out, int64_t ld, int td, int stages,
-             const float* __restrict__ ew, const __grid_constant__ CUtensorMap tmap) {
-  constexpr int RB = 32 * NB;           // code bytes per row
-  constexpr int EPL = 8 * NB / K;       // outputs per lane
-  constexpr int NA = EPL / 2;           // fp32 pair accumulators
-  constexpr bool PAIR = K == 4;
-  constexpr int LUTB = PAIR ? 256 * 32 * 8 : 256 * 32 * 4;
-  extern __shared__ __align__(1024) uint8_t s_raw[];
-  const int64_t live = live_dst(ndst_dev, max_dst);
-  const int64_t ntiles = (live + td - 1) / td;
-  if ((int64_t)blockIdx.x >= ntiles) return;
-  const int cap = td * 8;
-  uint8_t* const s_lut = s_raw;
-  uint8_t* const s_codes = s_raw + LUTB;                                 // [stages][cap][RB]
-  int32_t* const s_ip = reinterpret_cast<int32_t*>(s_codes + (size_t)stages * cap * RB);
-  uint64_t* const s_full = reinterpret_cast<uint64_t*>(s_ip + kV6Stages * kV6IpPitch);
-  uint64_t* const s_empty = s_full + kV6Stages;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) {
-    for (int s = 0; s < stages; ++s) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(s_full + s)));
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(s_empty + s)),
-                   "r"(kV6Cons));
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;");
-  }
-  __syncthreads();
-  const int64_t G = gridDim.x;
-  if (warp == 0) {
-    v6_producer(blockIdx.x, G, ntiles, live, td, cap, stages, indptr, src, s_ip, s_full, s_empty,
-                s_codes, RB, 0, &tmap, lane);
-    return;
-  }
-  // consumers: replicated lane-private table, then the tile loop
-  if constexpr (PAIR) {
-    u64* t2 = reinterpret_cast<u64*>(s_lut);
-    for (int i = tid - 32; i < 256 * 32; i += kV6Threads - 32) {
-      const int pv = i >> 5;
-      t2[i] = pack2(__ldg(lut + (pv >> 4)), __ldg(lut + (pv & 15)));
-    }
-  } else {
-    float* t1 = reinterpret_cast<float*>(s_lut);
-    for (int i = tid - 32; i < 256 * 32; i += kV6Threads - 32) t1[i] = __ldg(lut + (i >> 5));
-  }
-  asm volatile("bar.sync 1, %0;" ::"r"(kV6Threads - 32) : "memory");
-  const int cw = warp - 1;
-  const uint32_t tbase = smem_addr(s_lut) + (uint32_t)lane * (PAIR ? 8u : 4u);
-  const bool vec_ok = (ld % 4) == 0;
-  int k = 0;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += G, ++k) {
-    const int s = k % stages;
-    v6_wait(smem_addr(s_full + s), (uint32_t)((k / stages) & 1));
-    const int32_t* ip = s_ip + s * kV6IpPitch;
-    const uint8_t* codes = s_codes + (size_t)s * cap * RB;
-    const int64_t v0 = tile * td;
-    const int nd = (int)min64(td, live - v0);
-    const int32_t e0 = ip[0];
-    const bool staged = ip[nd] - e0 <= cap;
-    for (int vl = cw; vl < nd; vl += kV6Cons) {
-      const int a = ip[vl] - e0;
-      const int cnt = ip[vl + 1] - e0 - a;
-      u64 acc[NA];
-#pragma unroll
-      for (int j = 0; j < NA; ++j) acc[j] = 0ull;
-      for (int u0 = 0; u0 < cnt; u0 += 8) {
-        const int cb = min(cnt - u0, 8);
-        uint32_t cw8[8];
-        u64 wt[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (u < cb) {
-            const int e = a + u0 + u;
-            const uint8_t* p = staged ? codes + (size_t)e * RB + lane * NB
-                                      : rows + (int64_t)__ldg(src + e0 + e) * stride + lane * NB;
-            if constexpr (NB == 4) cw8[u] = staged ? *reinterpret_cast<const uint32_t*>(p)
-                                                   : __ldg(reinterpret_cast<const uint32_t*>(p));
-            else if constexpr (NB == 2) cw8[u] = staged ? *reinterpret_cast<const uint16_t*>(p)
-                                                        : __ldg(reinterpret_cast<const uint16_t*>(p));
-            else cw8[u] = staged ? *p : __ldg(p);
-            if constexpr (WT) wt[u] = bcast2(__ldg(ew + e0 + e));
-          }
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (u < cb) {
-#pragma unroll
-            for (int b = 0; b < NB; ++b) {
-              const uint32_t byte = (cw8[u] >> (8 * b)) & 0xFFu;
-              if constexpr (PAIR) {
-                uint32_t x, y;
-                asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(x), "=r"(y)
-                             : "r"(tbase + byte * 256u));
-                acc[b] = acc2<WT>(acc[b], ((u64)y << 32) | x, WT ? wt[u] : 0ull);
-              } else if (b % 2 == 0) {
-                const uint32_t b1 = (cw8[u] >> (8 * (b + 1))) & 0xFFu;
-                float f0, f1;
-                asm volatile("ld.shared.f32 %0, [%1];" : "=f"(f0) : "r"(tbase + byte * 128u));
-                asm volatile("ld.shared.f32 %0, [%1];" : "=f"(f1) : "r"(tbase + b1 * 128u));
-                acc[b / 2] = acc2<WT>(acc[b / 2], pack2(f0, f1), WT ? wt[u] : 0ull);
-              }
-            }
-          }
-      }
-      const float inv = WT ? 1.0f : (cnt ? 1.0f / (float)cnt : 0.0f);
-      __nv_bfloat16* o = out + (v0 + vl) * ld + lane * EPL;
-      uint32_t w[NA];
-#pragma unroll
-      for (int j = 0; j < NA; ++j) {
-        const __nv_bfloat162 b2 = __floats2bfloat162_rn(lo2(acc[j]) * inv, hi2(acc[j]) * inv);
-        w[j] = *reinterpret_cast<const uint32_t*>(&b2);
-      }
-      if (vec_ok) {
-        if constexpr (NA == 2) *reinterpret_cast<uint2*>(o) = make_uint2(w[0], w[1]);
-        else *reinterpret_cast<uint32_t*>(o) = w[0];
-      } else {
-#pragma unroll
-        for (int j = 0; j < NA; ++j) {
-          o[2 * j] = __ushort_as_bfloat16((unsigned short)(w[j] & 0xFFFFu));
-          o[2 * j + 1] = __ushort_as_bfloat16((unsigned short)(w[j] >> 16));
-        }
-      }
-    }
-    __syncwarp();
-    if (lane == 0)
-      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(s_empty + s))
-                   : "memory");
-  }
-}
-
-template <bool WT>
-static bool launch_sq_v6(const fg_codec_desc* c, const int32_t* indptr, const int32_t* src,
-                         const int64_t* ndst, int64_t max_dst, void* out, int64_t ld,
-                         cudaStream_t st, const float* ew, int* rc) {
-  const char* e = getenv("FG_SQ_V6");  // off by default (measured slower)
-  if (!e || atoi(e) == 0) return false;
-  const int K = c->bits;
-  if (!(K == 4 || K == 8) || (c->d * K) % 256 != 0) return false;
-  const int RB = (int)(c->d * K / 8), NB = RB / 32;
-  if (!(NB == 1 || NB == 2 || NB == 4) || (K == 8 && NB == 1) || c->row_stride < RB ||
-      c->elem_bits != 32)
-    return false;
-  CUtensorMap tmap;
-  if (!code_row_tensor_map(c, RB, &tmap)) return false;
-  const int lutb = K == 4 ? 256 * 32 * 8 : 256 * 32 * 4;
-  const int tail = kV6Stages * kV6IpPitch * 4 + 2 * kV6Stages * 8;
-  int td = kV6TD, stages = kV6Stages;
-  while (lutb + (int64_t)stages * td * 8 * RB + tail > 220 * 1024) {
-    if (stages > 2) --stages; else td /= 2;
-  }
-  const int64_t smem = lutb + (int64_t)stages * td * 8 * RB + tail;
-  void (*kern)(const uint8_t*, int64_t, const float*, const int32_t*, const int32_t*,
-               const int64_t*, int64_t, __nv_bfloat16*, int64_t, int, int, const float*,
-               const CUtensorMap) = nullptr;
-  if (K == 4 && NB == 1) kern = k_sq_mean_v6<4, 1, WT>;
-  else if (K == 4 && NB == 2) kern = k_sq_mean_v6<4, 2, WT>;
-  else if (K == 4 && NB == 4) kern = k_sq_mean_v6<4, 4, WT>;
-  else if (K == 8 && NB == 2) kern = k_sq_mean_v6<8, 2, WT>;
-  else kern = k_sq_mean_v6<8, 4, WT>;
-  *rc = FG_OK;
-  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-  if (err != cudaSuccess) {
-    set_error("sq v6 smem attribute: %s", cudaGetErrorString(err));
-    *rc = FG_ECUDA;
-    return true;
-  }
-  const int grid = (int)min64(ceil_div(max_dst, td), (int64_t)sm_count());
-  kern<<<grid, kV6Threads, smem, st>>>(c->rows, c->row_stride, (const float*)c->table, indptr,
-                                       src, ndst, max_dst, (__nv_bfloat16*)out, ld, td, stages,
-                                       ew, tmap);
-  count_launch();
-  err = cudaGetLastError();
-  if (err != cudaSuccess) {
-    set_error("k_sq_mean_v6 launch: %s", cudaGetErrorString(err));
-    *rc = FG_ECUDA;
-  }
-  return true;
-}
-
 // ------------------------------------------------------------ launchers
 template <int K, typename OT, bool WT>
 int launch_sq_w(const fg_codec_desc* c, const int32_t* indptr, const int32_t* src,
                 const int64_t* ndst, int64_t max_dst, void* out, int64_t ld, cudaStream_t st,
                 const float* ew) {
-  if constexpr (std::is_same<OT, __nv_bfloat16>::value) {
-    int rc = FG_OK;
-    if (launch_sq_v6<WT>(c, indptr, src, ndst, max_dst, out, ld, st, ew, &rc)) return rc;
-  }
   // TMA-staged variant: needs a row buffer holding a tile of >= 32
   // destinations at fanout 8 next to the decode table
   {
@@ -1897,6 +1372,7 @@ int launch_sq_w(const fg_codec_desc* c, const int32_t* indptr, const int32_t* sr
     const int chunks = (int)((c->d + 15) / 16);
     const int rb = (chunks * 2 * K + 15) / 16 * 16;
     CUtensorMap tmap;
+    memset(&tmap, 0, sizeof(tmap));
     const bool g4 = rb <= 256 && rb <= c->row_stride && code_row_tensor_map(c, rb, &tmap);
     const int gstride = (4 * rb + 127) & ~127;  // G4 group pitch (128-B aligned)
     int row_cap = g4 ? (kSmemBudget - fixed - 128) / (2 * gstride) * 4
@@ -1990,19 +1466,22 @@ int launch_vq_w(const fg_codec_desc* c, const int32_t* indptr, const int32_t* sr
   // bf16 output may read the bf16 copy of the codebooks (half the smem bytes)
   const bool lp = std::is_same<OT, __nv_bfloat16>::value && c->table_lp != nullptr && W >= 4;
   if constexpr (std::is_same<OT, __nv_bfloat16>::value && (W == 4 || W == 8)) {
-    int rc = FG_OK;
-    if (lp && launch_vq_v6<W, WT>(c, indptr, src, ndst, max_dst, out, ld, st, ew, &rc))
-      return rc;
-  }
-  if constexpr (std::is_same<OT, __nv_bfloat16>::value && (W == 4 || W == 8)) {
     // lane-per-part kernel (v5): sector slices of 32 parts, one CTA per SM.
-    // Off by default (FG_VQ_LANE=1 enables it): measured on the B200 it ties
-    // v4 on MAG240M-shape (131.5 vs 131.1 us) and loses on products-shape
-    // (51.0 vs 36.9 us).
-    static const int lane_env = [] {
-      const char* e = getenv("FG_VQ_LANE");  // 1: bf16 table, 2: fp16 table (HADD2)
-      return e ? atoi(e) : 0;
+    // Default for codebooks the v4 kernel below must part-slice (bf16 table
+    // over 70 KB, e.g. MAG240M-shape, 96 parts), in its fp16 form (scaled
+    // table_h, HADD2 chunks): measured 116 us vs 125 us for v4 there; with
+    // the bf16 table it was issue-bound (73 %) and tied v4.  Products-shape
+    // (unsliced, 25 parts) stays on v4 (36.9 vs 45.4 us).
+    // FG_VQ_LANE = 0 (off) | 1 (bf16 table) | 2 (fp16 table) forces a mode.
+    static const int lane_force = [] {
+      const char* e = getenv("FG_VQ_LANE");
+      return e ? atoi(e) : -1;
     }();
+    const int64_t v4_unsliced = (((int64_t)c->num_parts + (32 / W) - 1) / (32 / W) * (32 / W)) *
+                                    c->length * W * 2 + stage_bytes;
+    const bool has_h = !WT && c->table_h != nullptr && c->part_scale != nullptr;
+    const int lane_env = lane_force >= 0 ? lane_force
+                                         : (v4_unsliced > 76 * 1024 && has_h ? 2 : 0);
     const int64_t lane_smem = (int64_t)32 * c->length * W * 2 + 2 * kSrcCap * 32 +
                               3 * kSrcCap * 4 + 4 * (kTD + 4) * 4;
     if (lp && lane_env && c->row_stride % 32 == 0 && lane_smem <= 227 * 1024) {

@@ -598,12 +598,21 @@ extern "C" int fg_input_block_mean_fwd(const uint16_t* x, int64_t P, const uint1
   FG_CHECK_ARG(out_ld == H || out_ld == H + 8, "out_ld must be H or H + 8 (ones column)");
   if (max_dst == 0) return FG_OK;
   const int D = (int)min64(kIfRows / fanout, kIfRows - 1);
-  static const int v2_env = [] {  // FG_INFWD_V2=0: the v1 kernel (A/B)
+  // v2 (warp-specialised) when v1 fits only one CTA per SM: measured on the
+  // B200 papers100M-shape block (P = 144, v1 at 1 CTA/SM) 62.8 -> 50.6 us;
+  // products-shape (P = 112, v1 at 2 CTAs/SM) v1 48.5 us beats v2 56.7 us.
+  // FG_INFWD_V2 = 0 / 1 forces v1 / v2.
+  static const int v2_env = [] {
     const char* e = getenv("FG_INFWD_V2");
-    return e ? atoi(e) : 1;
+    return e ? atoi(e) : -1;
   }();
   const int smem2 = infwd2_smem_bytes((int)H, (int)P);
-  if (v2_env && smem2 <= 227 * 1024) {
+  int dev0 = 0, smem_sm0 = 0;
+  FG_CUDA_TRY(cudaGetDevice(&dev0));
+  FG_CUDA_TRY(cudaDeviceGetAttribute(&smem_sm0, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev0));
+  const bool v1_single = smem_sm0 / (infwd_smem_bytes((int)H, (int)P) + 1024) < 2;
+  const bool use_v2 = v2_env >= 0 ? v2_env != 0 : v1_single;
+  if (use_v2 && smem2 <= 227 * 1024) {
     auto kern2 = edge_w ? k_input_block_mean_fwd2<true> : k_input_block_mean_fwd2<false>;
     FG_CUDA_TRY(cudaFuncSetAttribute(kern2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2));
     const int64_t tiles = (max_dst + D - 1) / D;

@@ -18,6 +18,7 @@
 // prefix, ordered emit (ascending ids), rank lookup, clear.
 #include <cub/block/block_reduce.cuh>
 #include <cub/block/block_scan.cuh>
+#include <cub/block/block_radix_sort.cuh>
 
 #include <stdlib.h>
 
@@ -496,10 +497,16 @@ k_layer_fixup(const int64_t* __restrict__ off, const int32_t* __restrict__ col,
                &s_bad, delta);
 }
 
-// Single-pass compaction over level 1: thread per quarter of a level-1 word
-// (8 level-0 words = 256 node ids); popcounts of its non-empty words, block
-// scan, decoupled look-back prefix, ordered emit of the set bits (ascending
-// ids) and the word prefix of every non-empty level-0 word.
+// Single-pass compaction over level 1: thread per kBmIpt consecutive quarters
+// of level-1 words (8 level-0 words = 256 node ids each); popcounts of its
+// non-empty words, block scan, decoupled look-back prefix, ordered emit of
+// the set bits (ascending ids) and the word prefix of every non-empty level-0
+// word.  IPT = 8 for large bitmaps (round 2: a papers100M-shape bitmap, 111 M
+// ids, is 212 tiles instead of 1.7 K, one wave with a short look-back chain),
+// 1 below ~10 M ids (products-shape: 1 item per thread keeps ~40 CTAs busy).
+constexpr int kBmIpt = 8;
+inline int bm_ipt(int64_t words0) { return words0 / 32 * 4 >= 148ll * kBmThreads * 8 ? kBmIpt : 1; }
+template <int IPT>
 __global__ void __launch_bounds__(kBmThreads)
 k_bm_compact(const uint32_t* __restrict__ bm, int64_t words0, unsigned long long* status,
              unsigned int* ctr, int32_t* __restrict__ out, int64_t max_out,
@@ -510,32 +517,71 @@ k_bm_compact(const uint32_t* __restrict__ bm, int64_t words0, unsigned long long
   __shared__ unsigned long long s_u64;
   const ScanState sc{status, ctr, ctr + 1};
   const unsigned int tile = scan_take_tile(sc, &s_u32);
-  // item = (level-1 word j, quarter qq): level-0 words 32j + 8qq .. +7
+  // items = (level-1 word j, quarter qq), kBmIpt consecutive per thread:
+  // level-0 words 32j + 8qq .. +7
   const int64_t l1w = words0 / 32;
-  const int64_t item = (int64_t)tile * kBmThreads + threadIdx.x;
-  const int64_t j = item >> 2;
-  const int qq = (int)(item & 3);
-  const uint32_t l1 = j < l1w ? (bm[words0 + j] >> (8 * qq)) & 0xFFu : 0u;
-  const int64_t wbase = j * 32 + 8 * qq;
+  const int64_t item0 = ((int64_t)tile * kBmThreads + threadIdx.x) * IPT;
+  uint32_t l1[IPT];
   unsigned long long c = 0;
-  for (uint32_t x = l1; x; x &= x - 1) c += __popc(bm[wbase + (__ffs(x) - 1)]);
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    const int64_t item = item0 + i;
+    const int64_t j = item >> 2;
+    l1[i] = j < l1w ? (__ldg(bm + words0 + j) >> (8 * (int)(item & 3))) & 0xFFu : 0u;
+    const int64_t wbase = j * 32 + 8 * (item & 3);
+    for (uint32_t x = l1[i]; x; x &= x - 1) c += __popc(__ldg(bm + wbase + (__ffs(x) - 1)));
+  }
   unsigned long long excl, agg;
   BS(tmp).ExclusiveSum(c, excl, agg);
   const unsigned long long prefix = scan_tile_prefix(sc, tile, agg, &s_u64);
   int64_t pos = (int64_t)(prefix + excl);
-  for (uint32_t x = l1; x; x &= x - 1) {
-    const int64_t w = wbase + (__ffs(x) - 1);
-    uint32_t bits = bm[w];
-    if (wprefix) wprefix[w] = (int32_t)pos;
-    while (bits) {
-      const int b = __ffs(bits) - 1;
-      bits &= bits - 1;
-      if (pos < max_out) out[pos] = (int32_t)((w << 5) + b);
-      ++pos;
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    const int64_t item = item0 + i;
+    const int64_t wbase = (item >> 2) * 32 + 8 * (item & 3);
+    for (uint32_t x = l1[i]; x; x &= x - 1) {
+      const int64_t w = wbase + (__ffs(x) - 1);
+      uint32_t bits = __ldg(bm + w);
+      if (wprefix) wprefix[w] = (int32_t)pos;
+      while (bits) {
+        const int b = __ffs(bits) - 1;
+        bits &= bits - 1;
+        if (pos < max_out) out[pos] = (int32_t)((w << 5) + b);
+        ++pos;
+      }
     }
   }
   if (scan_last_block(sc, ntiles, &s_u32) && threadIdx.x == 0)
     *out_count = (int64_t)(status[ntiles - 1] & kScanValMask);
+}
+
+// Seed layer (pipeline.py:203 np.sort of the batch's permutation slice): one
+// CTA radix-sorts the <= 4096 seed ids in shared memory (cub::BlockRadixSort
+// over the id bits) instead of marking, compacting and clearing the whole
+// n-bit bitmap (three kernels, ~25 us at papers100M-shape for 1024 ids).
+// Duplicates are kept, as np.sort keeps them.
+template <int IPT>
+__global__ void __launch_bounds__(1024)
+k_sort_ids(const int64_t* __restrict__ ids, const int64_t* __restrict__ cnt, int64_t cap,
+           int32_t* __restrict__ out, int64_t* __restrict__ out_cnt, int end_bit) {
+  using BRS = cub::BlockRadixSort<uint32_t, 1024, IPT>;
+  __shared__ typename BRS::TempStorage tmp;
+  const int64_t live = min64(*cnt, cap);
+  uint32_t k[IPT];
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    const int64_t j = (int64_t)threadIdx.x * IPT + i;
+    k[i] = j < live ? (uint32_t)ids[j] : 0xFFFFFFFFu;
+  }
+  // pads (0xFFFFFFFF) sort after every id: their low end_bit bits are the
+  // maximum and the sort is stable (pads come last in the input)
+  BRS(tmp).Sort(k, 0, end_bit);
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    const int64_t j = (int64_t)threadIdx.x * IPT + i;
+    if (j < live) out[j] = (int32_t)k[i];
+  }
+  if (threadIdx.x == 0) *out_cnt = live;
 }
 
 __global__ void k_bm_rank(const int32_t* __restrict__ ids, const int64_t* __restrict__ cnt,
@@ -667,7 +713,7 @@ int64_t fg_bitmap_words(int64_t n) { return bm_words0(n) + bm_words0(n) / 32; }
 
 int64_t fg_bitmap_workspace_bytes(int64_t n) {
   const int64_t l1w = bm_words0(n > 0 ? n : 1) / 32;
-  const int64_t nb = ceil_div(4 * l1w, kBmThreads);
+  const int64_t nb = ceil_div(4 * l1w, (int64_t)kBmThreads);  // IPT = 1 upper bound
   return align256(64 + nb * 8);
 }
 
@@ -695,12 +741,33 @@ int fg_bitmap_compact(uint32_t* bm, int64_t n, int32_t* out_ids, int64_t max_out
   FG_CHECK_ARG(ws_bytes >= fg_bitmap_workspace_bytes(n), "fg_bitmap_compact: workspace too small");
   cudaStream_t st = as_stream(s);
   const int64_t words0 = bm_words0(n);
-  const int64_t nb = ceil_div(4 * (words0 / 32), kBmThreads);
+  const int ipt = bm_ipt(words0);
+  const int64_t nb = ceil_div(4 * (words0 / 32), (int64_t)kBmThreads * ipt);
   unsigned int* ctr = (unsigned int*)ws;
   unsigned long long* status = (unsigned long long*)((char*)ws + 64);
   FG_CUDA_TRY(cudaMemsetAsync(ws, 0, 64 + nb * 8, st));
-  k_bm_compact<<<(unsigned)nb, kBmThreads, 0, st>>>(bm, words0, status, ctr, out_ids, max_out,
-                                                    out_count, wprefix, (unsigned)nb);
+  auto kern = ipt == kBmIpt ? k_bm_compact<kBmIpt> : k_bm_compact<1>;
+  kern<<<(unsigned)nb, kBmThreads, 0, st>>>(bm, words0, status, ctr, out_ids, max_out, out_count,
+                                            wprefix, (unsigned)nb);
+  FG_LAUNCH_CHECK();
+  return FG_OK;
+}
+
+int fg_sort_ids(const int64_t* ids, const int64_t* cnt, int64_t cap, int32_t* out,
+                int64_t* out_cnt, int64_t n, void* s) {
+  FG_CHECK_ARG(cap >= 0 && cap <= 4096, "fg_sort_ids: at most 4096 ids");
+  FG_CHECK_ARG(n >= 1 && n < INT32_MAX, "fg_sort_ids: n must be in [1, 2^31)");
+  if (cap == 0) return FG_OK;
+  cudaStream_t st = as_stream(s);
+  const int ipt = (int)ceil_div(cap, 1024);
+  int end_bit = 1;
+  while (end_bit < 32 && (1ll << end_bit) < n) ++end_bit;  // ids < n <= 2^end_bit
+  switch (ipt) {
+    case 1: k_sort_ids<1><<<1, 1024, 0, st>>>(ids, cnt, cap, out, out_cnt, end_bit); break;
+    case 2: k_sort_ids<2><<<1, 1024, 0, st>>>(ids, cnt, cap, out, out_cnt, end_bit); break;
+    case 3: k_sort_ids<3><<<1, 1024, 0, st>>>(ids, cnt, cap, out, out_cnt, end_bit); break;
+    default: k_sort_ids<4><<<1, 1024, 0, st>>>(ids, cnt, cap, out, out_cnt, end_bit); break;
+  }
   FG_LAUNCH_CHECK();
   return FG_OK;
 }

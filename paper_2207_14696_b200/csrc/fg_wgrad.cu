@@ -486,11 +486,11 @@ extern "C" int fg_block_mean_wgrad(const uint16_t* g, int64_t g_ld, const int32_
   FG_CHECK_ARG(scratch_bytes >= fg_block_mean_wgrad_scratch_bytes(H, P), "scratch too small");
   cudaStream_t st = as_stream(s);
   float* seg_f = scratch + (int64_t)nb * H * P;
+  uint32_t cols = 32;
+  while (cols < (uint32_t)((H / 128) * P)) cols <<= 1;
   const int smem = wgrad_smem_bytes((int)H, (int)P);
   FG_CUDA_TRY(cudaFuncSetAttribute(k_block_mean_wgrad, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    smem));
-  uint32_t cols = 32;
-  while (cols < (uint32_t)((H / 128) * P)) cols <<= 1;
   k_block_mean_wgrad<<<nb, kWgThreads, smem, st>>>(g, g_ld, indptr, n_dst_dev, max_dst, local,
                                                    edge_w,
                                                    mask_kind == 1 ? (const uint16_t*)relu_mask

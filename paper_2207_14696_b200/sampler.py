@@ -263,12 +263,19 @@ class DeviceSampler:
         L = len(self.fanouts)
         n = self.g.n
         bm, wp = N.ptr(self.bitmap), N.ptr(self.wprefix)
-        # seeds = sort(perm slice): bitmap order gives ascending ids
-        N.call("fg_bitmap_mark64", N.ptr(self.seed_in), N.ptr(self.n_seed_in), self.bs, bm, n, s)
-        N.call("fg_bitmap_compact", bm, n, N.ptr(self.nodes[0]), self.caps[0],
-               N.ptr(self.n_nodes[0]), None, N.ptr(self.ws_bm), self.ws_bm.numel(), s)
-        N.call("fg_bitmap_clear", N.ptr(self.nodes[0]), N.ptr(self.n_nodes[0]), self.caps[0], bm,
-               n, s)
+        # seeds = sort(perm slice) (pipeline.py:203): one-CTA radix sort for
+        # batches up to 4096 on graphs past 2^24 nodes (the bitmap route
+        # scans all n bits: ~20 us at papers100M-shape), else bitmap order
+        if self.bs <= 4096 and n > (1 << 24):
+            N.call("fg_sort_ids", N.ptr(self.seed_in), N.ptr(self.n_seed_in), self.bs,
+                   N.ptr(self.nodes[0]), N.ptr(self.n_nodes[0]), n, s)
+        else:
+            N.call("fg_bitmap_mark64", N.ptr(self.seed_in), N.ptr(self.n_seed_in), self.bs, bm,
+                   n, s)
+            N.call("fg_bitmap_compact", bm, n, N.ptr(self.nodes[0]), self.caps[0],
+                   N.ptr(self.n_nodes[0]), None, N.ptr(self.ws_bm), self.ws_bm.numel(), s)
+            N.call("fg_bitmap_clear", N.ptr(self.nodes[0]), N.ptr(self.n_nodes[0]),
+                   self.caps[0], bm, n, s)
         if self.want_frontier:
             N.call("fg_bitmap_mark", N.ptr(self.nodes[0]), N.ptr(self.n_nodes[0]), self.caps[0],
                    N.ptr(self.fbitmap), n, s)

@@ -237,3 +237,26 @@ def test_sampler_fanout_above_200_small_graph():
     smp2.sample(0)
     with pytest.raises(fg.DataError):
         smp2.check_errors()
+
+
+@pytest.mark.parametrize("cap,live,n", [(1024, 1024, 111_059_956), (1024, 700, 50_000_000),
+                                        (4096, 4096, 244_160_499), (3000, 1, 2 ** 30),
+                                        (1, 1, 5)])
+def test_seed_sort_equals_numpy_sort(cap, live, n):
+    """fg_sort_ids (the seed layer on graphs past 2^24 nodes) is np.sort of
+    the batch's ids (pipeline.py:203), duplicates kept; count from the
+    device scalar."""
+    from paper_2207_14696_b200 import _native as N
+    rng = np.random.default_rng(cap + live)
+    ids = rng.integers(0, n, cap).astype(np.int64)
+    ids[: live // 3] = ids[0]  # duplicates
+    d_ids = torch.from_numpy(ids).cuda()
+    out = torch.full((cap,), -7, dtype=torch.int32, device="cuda")
+    cnt = torch.tensor([live], dtype=torch.int64, device="cuda")
+    ocnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    N.call("fg_sort_ids", N.ptr(d_ids), N.ptr(cnt), cap, N.ptr(out), N.ptr(ocnt), n,
+           N.stream_handle())
+    assert int(ocnt.item()) == live
+    o = out.cpu().numpy()
+    assert np.array_equal(o[:live], np.sort(ids[:live]).astype(np.int32))
+    assert (o[live:] == -7).all()

@@ -30,6 +30,8 @@ def main():
     ap.add_argument("--flush", default="write", help="comma list of L2 flush modes to sweep: "
                     "write (512 MB write) | write+read (then a 256 MB read, so the flush's "
                     "dirty lines are written back before the timed launch)")
+    ap.add_argument("--pitch", type=int, default=0, help="output row pitch in elements "
+                    "(default: aggregate.padded_dim(d))")
     ap.add_argument("--l2", default="", help="comma list of L2 fetch granularities (bytes) "
                     "to sweep in this process (fg_set_l2_fetch_granularity); default: as is")
     a = ap.parse_args()
@@ -39,6 +41,8 @@ def main():
     smp.begin_epoch(sg.train_ids, 0)
     L = len(fanouts)
     out = alloc_aggregate(smp.caps[L - 1], dc.d, torch.bfloat16, dev)
+    if a.pitch:
+        out = torch.zeros((smp.caps[L - 1], a.pitch), dtype=torch.bfloat16, device=dev)
     flush = torch.zeros(128 * 1024 * 1024, dtype=torch.float32, device=dev)
     rflush = torch.zeros(64 * 1024 * 1024, dtype=torch.float32, device=dev)
     sink = torch.zeros(1, dtype=torch.float32, device=dev)
@@ -87,7 +91,7 @@ def run(a, dc, smp, out, flush, row_bytes, L, gran, fm="write"):
     gbs = sum(bts) / len(bts) / (us * 1e-6) / 1e9
     peak, _ = bench.load_peaks()
     print(json.dumps({"config": a.config, "lane": os.environ.get("FG_VQ_LANE", "0"),
-                      "l2_fetch": gran, "flush": fm, "probe": os.environ.get("FG_FUSED_PROBE", "0"),
+                      "l2_fetch": gran, "flush": fm, "pitch": out.shape[1], "probe": os.environ.get("FG_FUSED_PROBE", "0"),
                       "avg_us": round(us, 2), "min_us": round(min(ts) * 1e3, 2),
                       "alg_bytes": int(sum(bts) / len(bts)), "GBps": round(gbs, 1),
                       "frac": round(gbs / peak, 4)}))

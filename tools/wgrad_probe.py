@@ -14,7 +14,7 @@ from paper_2207_14696_b200.aggregate import block_mean_wgrad, wgrad_scratch  # n
 
 def main():
     rng = np.random.default_rng(0)
-    n_src, n_dst, fan, H, P = 104_000, 15_360, 10, 256, 112
+    n_src, n_dst, fan, H, P = 104_000, 15_360, 10, 256, int(sys.argv[1]) if len(sys.argv) > 1 else 112
     counts = np.full(n_dst, fan)
     indptr = np.zeros(n_dst + 1, np.int32)
     indptr[1:] = np.cumsum(counts)
@@ -40,7 +40,7 @@ def main():
         ts.append((s, e))
     torch.cuda.synchronize()
     print(f"wgrad (kernel + reduce): median {statistics.median(a.elapsed_time(b) for a, b in ts) * 1e3:.1f} us "
-          f"for {indptr[-1]} edges")
+          f"for {indptr[-1]} edges, P={P}, v2={os.environ.get('FG_WGRAD_V2', '1')}")
 
 
 if __name__ == "__main__":
