@@ -384,6 +384,35 @@ int fg_gat_xagg_fwd(const uint16_t* x, int64_t d, int heads, const float* alpha,
 int fg_gat_xagg_bwd(const uint16_t* x, int64_t d, int heads, const int32_t* indptr,
                     int64_t max_dst, const int64_t* n_dst_dev, const float* dout, float* dalpha,
                     int64_t e_cap, void* cuda_stream);
+/* GAT input layer straight from the code rows of the last block's picks
+ * (`codec` + `picks`; or, with x_rows != NULL, from decoded bf16 rows, one per
+ * pick): no decoded per-pick matrix in HBM.  Elements are decoded exactly as
+ * dequantize_sq / decode_vq (sq.py:132-153, vq.py:330-344; SQ any k, VQ
+ * 8-bit codes).  Per head k of H (H <= 8), c = [c_l; c_r] ([2H][d]):
+ *   fg_gat_code_scores      el[e,k] = <x_e, c_l[k]>, er[e,k] = <x_e, c_r[k]>
+ *   fg_gat_code_scores_bwd  partial[b][q][j] = sum_{e in block b} ds[e,q] x[e,j]
+ *                           (ds = [del | der]; fg_gat_code_scores_bwd_blocks(e_cap)
+ *                           blocks, summed by the caller in block order)
+ *   fg_gat_code_xagg_fwd    A[v, k*d + j] = sum_{e in v} alpha[e,k] x[e,j] (bf16;
+ *                           rows past the live count zeroed)
+ *   fg_gat_code_xagg_bwd    dalpha[e,k] = <dA[v, k*d : (k+1)*d], x_e> (dA bf16) */
+int fg_gat_code_scores(const fg_codec_desc* codec, const uint16_t* x_rows,
+                       const int32_t* picks, const int64_t* n_picks_dev, int64_t e_cap,
+                       int64_t d, int heads, const float* c, float* el, float* er,
+                       void* cuda_stream);
+int64_t fg_gat_code_scores_bwd_blocks(int64_t e_cap);
+int fg_gat_code_scores_bwd(const fg_codec_desc* codec, const uint16_t* x_rows,
+                           const int32_t* picks, const int64_t* n_picks_dev, int64_t e_cap,
+                           int64_t d, int heads, const float* del, const float* der,
+                           float* partial, void* cuda_stream);
+int fg_gat_code_xagg_fwd(const fg_codec_desc* codec, const uint16_t* x_rows,
+                         const int32_t* picks, int64_t d, int heads, const float* alpha,
+                         const int32_t* indptr, int64_t max_dst, const int64_t* n_dst_dev,
+                         uint16_t* out, void* cuda_stream);
+int fg_gat_code_xagg_bwd(const fg_codec_desc* codec, const uint16_t* x_rows,
+                         const int32_t* picks, int64_t d, int heads, const int32_t* indptr,
+                         int64_t max_dst, const int64_t* n_dst_dev, const uint16_t* dA,
+                         float* dalpha, void* cuda_stream);
 int fg_gat_agg_bwd(const uint16_t* z, int64_t hf, int heads, const float* alpha,
                    const int32_t* indptr, const int32_t* local, int64_t max_dst,
                    const int64_t* n_dst_dev, const float* dout, float* dz, float* dalpha,

@@ -19,6 +19,8 @@
 // Forward: one thread per (destination, head).  Backward scatters into source
 // rows with fp32 atomics (dz, d el, d er): the attention backward is not
 // bitwise deterministic.
+#include <algorithm>
+
 #include "fg_common.cuh"
 
 namespace fg {
@@ -304,6 +306,218 @@ k_gat_xagg_bwd(const __nv_bfloat16* __restrict__ x, int d, int heads,
     }
   }
 }
+// ------------------------------------------------ input layer from codes
+// Round 2: the GAT input layer reads the code rows of the last block's picks
+// directly (no per-pick decoded bf16 matrix in HBM): every kernel below
+// decodes the elements it needs in registers (SQ: LUT of the reference
+// decodes; VQ 8-bit: codebook entry), exactly dequantize_sq / decode_vq
+// (sq.py:132-153, vq.py:330-344).  kind 0 = rows already decoded (bf16, one
+// row per pick, in pick order) for codecs outside that set.
+struct GatCodes {
+  int kind, bits, width, length;
+  int64_t stride;       // bytes per row (kind 0: d * 2)
+  const uint8_t* rows;  // code rows (kind 0: decoded bf16 rows)
+  const float* table;   // SQ LUT / VQ fp32 codebooks [P][L][W]
+  const int32_t* picks; // source node of each pick (unused for kind 0)
+};
+__device__ __forceinline__ const uint8_t* gat_row(const GatCodes& c, int64_t e) {
+  return c.kind == 0 ? c.rows + e * c.stride : c.rows + (int64_t)__ldg(c.picks + e) * c.stride;
+}
+__device__ __forceinline__ float gat_elem(const GatCodes& c, const uint8_t* row, int j) {
+  if (c.kind == 0) {
+    const uint16_t h = reinterpret_cast<const uint16_t*>(row)[j];
+    return __uint_as_float((uint32_t)h << 16);
+  }
+  if (c.kind == FG_CODEC_SQ) {
+    const int k = c.bits;
+    if (k == 8) return __ldg(c.table + row[j]);
+    const int64_t bit = (int64_t)j * k;
+    const int b = (int)(bit >> 3), sh = (int)(bit & 7);
+    uint32_t w = (uint32_t)row[b] << 8;
+    if (sh + k > 8) w |= row[b + 1];
+    return __ldg(c.table + ((w >> (16 - sh - k)) & ((1u << k) - 1u)));
+  }
+  const int p = j / c.width;  // VQ, 8-bit codes
+  return __ldg(c.table + ((int64_t)p * c.length + row[p]) * c.width + (j - p * c.width));
+}
+
+// el[e, k] = <x_e, c[k]>, er[e, k] = <x_e, c[H + k]>: thread per pick, c in smem
+__global__ void __launch_bounds__(256)
+k_gat_code_scores(GatCodes cd, int d, int heads, const float* __restrict__ c,
+                  const int64_t* __restrict__ ne_dev, int64_t e_cap, float* __restrict__ el,
+                  float* __restrict__ er) {
+  extern __shared__ float s_c[];  // [2H][d]
+  for (int i = threadIdx.x; i < 2 * heads * d; i += blockDim.x) s_c[i] = c[i];
+  __syncthreads();
+  const int64_t ne = min64(*ne_dev, e_cap);
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ne;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const uint8_t* row = gat_row(cd, e);
+    float acc[2 * kMaxHeads];
+#pragma unroll
+    for (int q = 0; q < 2 * kMaxHeads; ++q) acc[q] = 0.f;
+    for (int j = 0; j < d; ++j) {
+      const float x = gat_elem(cd, row, j);
+#pragma unroll
+      for (int q = 0; q < 2 * kMaxHeads; ++q)
+        if (q < 2 * heads) acc[q] = fmaf(x, s_c[q * d + j], acc[q]);
+    }
+#pragma unroll
+    for (int k = 0; k < kMaxHeads; ++k)
+      if (k < heads) {
+        el[e * heads + k] = acc[k];
+        er[e * heads + k] = acc[heads + k];
+      }
+  }
+}
+
+// partial[b][q][j] = sum over block b's picks e of ds[e, q] x[e, j]
+// (ds = [del | der], q < 2H): thread per column j, picks in fixed order
+// (deterministic; the partials are summed in block order by the caller)
+__global__ void k_gat_code_scores_bwd(GatCodes cd, int d, int heads,
+                                      const float* __restrict__ del, const float* __restrict__ der,
+                                      const int64_t* __restrict__ ne_dev, int64_t e_cap,
+                                      int64_t per_block, float* __restrict__ partial) {
+  __shared__ float s_ds[32][2 * kMaxHeads];
+  const int64_t ne = min64(*ne_dev, e_cap);
+  const int64_t e_lo = blockIdx.x * per_block, e_hi = min64(ne, e_lo + per_block);
+  float acc[2 * kMaxHeads];
+#pragma unroll
+  for (int q = 0; q < 2 * kMaxHeads; ++q) acc[q] = 0.f;
+  for (int64_t e0 = e_lo; e0 < e_hi; e0 += 32) {
+    const int nb = (int)min64(32, e_hi - e0);
+    __syncthreads();
+    for (int i = threadIdx.x; i < nb * 2 * heads; i += blockDim.x) {
+      const int r = i / (2 * heads), q = i - r * 2 * heads;
+      s_ds[r][q] = q < heads ? del[(e0 + r) * heads + q] : der[(e0 + r) * heads + q - heads];
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < d; j += blockDim.x) {
+      for (int r = 0; r < nb; ++r) {
+        const float x = gat_elem(cd, gat_row(cd, e0 + r), j);
+#pragma unroll
+        for (int q = 0; q < 2 * kMaxHeads; ++q)
+          if (q < 2 * heads) acc[q] = fmaf(s_ds[r][q], x, acc[q]);
+      }
+    }
+  }
+  // blockDim >= d: thread j owns column j
+  const int j = threadIdx.x;
+  if (j < d) {
+#pragma unroll
+    for (int q = 0; q < 2 * kMaxHeads; ++q)
+      if (q < 2 * heads) partial[((int64_t)blockIdx.x * 2 * heads + q) * d + j] = acc[q];
+  }
+}
+
+// A[v, k*d + j] = sum_{e in v} alpha[e, k] x[e, j] (bf16; rows past the live
+// count zero): warp per destination, lane owns columns j = lane + 32 i
+// (i < kXI, d <= 32 kXI), edges outer (each alpha and x element read once)
+constexpr int kXI = 8;  // d <= 256
+template <int HEADS, int XI>
+__global__ void __launch_bounds__(256)
+k_gat_code_xagg_fwd(GatCodes cd, int d, const float* __restrict__ alpha,
+                    const int32_t* __restrict__ indptr, int64_t max_dst,
+                    const int64_t* __restrict__ ndst_dev, __nv_bfloat16* __restrict__ out) {
+  constexpr int heads = HEADS;
+  const int64_t live = min64(*ndst_dev, max_dst);
+  const int lane = threadIdx.x & 31;
+  for (int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; v < max_dst;
+       v += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    __nv_bfloat16* o = out + v * (int64_t)heads * d;
+    const int32_t e0 = v < live ? indptr[v] : 0, e1 = v < live ? indptr[v + 1] : 0;
+    float acc[XI][HEADS];
+#pragma unroll
+    for (int i = 0; i < XI; ++i)
+#pragma unroll
+      for (int k = 0; k < HEADS; ++k) acc[i][k] = 0.f;
+    for (int32_t e = e0; e < e1; ++e) {
+      const uint8_t* row = gat_row(cd, e);
+      float al[HEADS];
+#pragma unroll
+      for (int k = 0; k < HEADS; ++k)
+        al[k] = __ldg(alpha + (int64_t)e * heads + k);
+#pragma unroll
+      for (int i = 0; i < XI; ++i) {
+        const int j = lane + 32 * i;
+        if (j < d) {
+          const float xv = gat_elem(cd, row, j);
+#pragma unroll
+          for (int k = 0; k < HEADS; ++k)
+            acc[i][k] = fmaf(al[k], xv, acc[i][k]);
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < HEADS; ++k)
+#pragma unroll
+        for (int i = 0; i < XI; ++i) {
+          const int j = lane + 32 * i;
+          if (j < d) o[k * d + j] = __float2bfloat16_rn(acc[i][k]);
+        }
+  }
+}
+
+// dalpha[e, k] = <dA[v, k*d : (k+1)*d], x_e>: warp per destination, dA[v]
+// held in registers; B = 32/H edges at a time give 32 partial dots per lane,
+// reduced across the warp by one 31-shuffle transpose-reduce (lane L ends
+// with edge L/H, head L%H), then one coalesced 32-float store
+template <int HEADS, int XI>
+__global__ void __launch_bounds__(256)
+k_gat_code_xagg_bwd(GatCodes cd, int d, const int32_t* __restrict__ indptr,
+                    int64_t max_dst, const int64_t* __restrict__ ndst_dev,
+                    const __nv_bfloat16* __restrict__ dA, float* __restrict__ dalpha) {
+  constexpr int heads = HEADS, B = 32 / HEADS;
+  const int64_t live = min64(*ndst_dev, max_dst);
+  const int lane = threadIdx.x & 31;
+  for (int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; v < live;
+       v += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int32_t e0 = indptr[v], e1 = indptr[v + 1];
+    const __nv_bfloat16* g = dA + v * (int64_t)heads * d;
+    float gk[XI][HEADS];
+#pragma unroll
+    for (int i = 0; i < XI; ++i) {
+      const int j = lane + 32 * i;
+#pragma unroll
+      for (int k = 0; k < HEADS; ++k)
+        gk[i][k] = j < d ? __bfloat162float(g[k * d + j]) : 0.f;
+    }
+    for (int32_t eb = e0; eb < e1; eb += B) {
+      float pv[32];
+#pragma unroll
+      for (int q = 0; q < 32; ++q) pv[q] = 0.f;
+#pragma unroll
+      for (int b = 0; b < B; ++b) {
+        if (eb + b < e1) {
+          const uint8_t* row = gat_row(cd, eb + b);
+#pragma unroll
+          for (int i = 0; i < XI; ++i) {
+            const int j = lane + 32 * i;
+            if (j < d) {
+              const float xv = gat_elem(cd, row, j);
+#pragma unroll
+              for (int k = 0; k < HEADS; ++k)
+                pv[b * HEADS + k] = fmaf(gk[i][k], xv, pv[b * HEADS + k]);
+            }
+          }
+        }
+      }
+      // transpose-reduce: lane L ends with the warp sum of pv[L]
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) {
+        const bool upper = (lane & off) != 0;
+#pragma unroll
+        for (int q = 0; q < off; ++q) {
+          const float send = upper ? pv[q] : pv[q + off];
+          const float keep = upper ? pv[q + off] : pv[q];
+          pv[q] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+        }
+      }
+      const int eo = lane / heads;
+      if (eb + eo < e1) dalpha[(int64_t)(eb + eo) * heads + (lane - eo * heads)] = pv[0];
+    }
+  }
+}
 }  // namespace fg
 
 extern "C" int fg_gat_xagg_fwd(const uint16_t* x, int64_t d, int heads, const float* alpha,
@@ -328,6 +542,127 @@ extern "C" int fg_gat_xagg_bwd(const uint16_t* x, int64_t d, int heads, const in
   fg::k_gat_xagg_bwd<<<grid_for(max_dst * 32, 256), 256, 0, as_stream(s)>>>(
       reinterpret_cast<const __nv_bfloat16*>(x), (int)d, heads, indptr, max_dst, n_dst_dev, dout,
       dalpha);
+  FG_LAUNCH_CHECK();
+  return FG_OK;
+}
+
+// ------------------------------------------------ C ABI: input layer from codes
+static fg::GatCodes gat_codes(const fg_codec_desc* c, const uint16_t* x_rows, int64_t d,
+                              const int32_t* picks) {
+  fg::GatCodes g{};
+  if (x_rows) {
+    g.kind = 0;
+    g.rows = reinterpret_cast<const uint8_t*>(x_rows);
+    g.stride = d * 2;
+  } else {
+    g.kind = c->kind;
+    g.bits = c->bits;
+    g.width = c->width;
+    g.length = c->length;
+    g.stride = c->row_stride;
+    g.rows = c->rows;
+    g.table = reinterpret_cast<const float*>(c->table);
+  }
+  g.picks = picks;
+  return g;
+}
+static bool gat_codes_ok(const fg_codec_desc* c, const uint16_t* x_rows) {
+  if (x_rows) return true;
+  if (!c) return false;
+  if (c->kind == FG_CODEC_SQ) return c->elem_bits == 32;
+  return c->kind == FG_CODEC_VQ && c->bits == 8;
+}
+
+extern "C" int fg_gat_code_scores(const fg_codec_desc* codec, const uint16_t* x_rows,
+                                  const int32_t* picks, const int64_t* n_picks_dev, int64_t e_cap,
+                                  int64_t d, int heads, const float* c, float* el, float* er,
+                                  void* s) {
+  FG_CHECK_ARG(gat_codes_ok(codec, x_rows) && c && el && er && n_picks_dev && heads >= 1 &&
+                   heads <= fg::kMaxHeads && d >= 1 && 2 * heads * d <= 12288,
+               "fg_gat_code_scores: bad argument");
+  if (e_cap == 0) return FG_OK;
+  const fg::GatCodes g = gat_codes(codec, x_rows, d, picks);
+  fg::k_gat_code_scores<<<grid_for(e_cap, 256), 256, (size_t)2 * heads * d * 4, as_stream(s)>>>(
+      g, (int)d, heads, c, n_picks_dev, e_cap, el, er);
+  FG_LAUNCH_CHECK();
+  return FG_OK;
+}
+
+extern "C" int64_t fg_gat_code_scores_bwd_blocks(int64_t e_cap) {
+  return std::max<int64_t>(1, std::min<int64_t>(4 * sm_count(), ceil_div(e_cap, 512)));
+}
+
+extern "C" int fg_gat_code_scores_bwd(const fg_codec_desc* codec, const uint16_t* x_rows,
+                                      const int32_t* picks, const int64_t* n_picks_dev,
+                                      int64_t e_cap, int64_t d, int heads, const float* del,
+                                      const float* der, float* partial, void* s) {
+  FG_CHECK_ARG(gat_codes_ok(codec, x_rows) && del && der && partial && n_picks_dev &&
+                   heads >= 1 && heads <= fg::kMaxHeads && d >= 1 && d <= 1024,
+               "fg_gat_code_scores_bwd: bad argument (d <= 1024)");
+  if (e_cap == 0) return FG_OK;
+  const fg::GatCodes g = gat_codes(codec, x_rows, d, picks);
+  const int64_t nb = fg_gat_code_scores_bwd_blocks(e_cap);
+  const int64_t per = ceil_div(e_cap, nb);
+  const int threads = (int)std::max<int64_t>(32, ceil_div(d, 32) * 32);
+  fg::k_gat_code_scores_bwd<<<(unsigned)nb, threads, 0, as_stream(s)>>>(
+      g, (int)d, heads, del, der, n_picks_dev, e_cap, per, partial);
+  FG_LAUNCH_CHECK();
+  return FG_OK;
+}
+
+extern "C" int fg_gat_code_xagg_fwd(const fg_codec_desc* codec, const uint16_t* x_rows,
+                                    const int32_t* picks, int64_t d, int heads,
+                                    const float* alpha, const int32_t* indptr, int64_t max_dst,
+                                    const int64_t* n_dst_dev, uint16_t* out, void* s) {
+  FG_CHECK_ARG(gat_codes_ok(codec, x_rows) && alpha && indptr && n_dst_dev && out &&
+                   (heads == 1 || heads == 2 || heads == 4 || heads == 8) && d >= 1 &&
+                   d <= 32 * fg::kXI,
+               "fg_gat_code_xagg_fwd: bad argument (heads in {1,2,4,8}, d <= 256)");
+  if (max_dst == 0) return FG_OK;
+  const fg::GatCodes g = gat_codes(codec, x_rows, d, picks);
+  auto* ob = reinterpret_cast<__nv_bfloat16*>(out);
+  const dim3 grid(grid_for(max_dst * 32, 256));
+  cudaStream_t st = as_stream(s);
+#define FG_XAGG_FWD(H, XI) \
+  fg::k_gat_code_xagg_fwd<H, XI><<<grid, 256, 0, st>>>(g, (int)d, alpha, indptr, max_dst, \
+                                                        n_dst_dev, ob)
+  const bool small = d <= 128;
+  switch (heads) {
+    case 1: if (small) FG_XAGG_FWD(1, 4); else FG_XAGG_FWD(1, 8); break;
+    case 2: if (small) FG_XAGG_FWD(2, 4); else FG_XAGG_FWD(2, 8); break;
+    case 4: if (small) FG_XAGG_FWD(4, 4); else FG_XAGG_FWD(4, 8); break;
+    default: if (small) FG_XAGG_FWD(8, 4); else FG_XAGG_FWD(8, 8); break;
+  }
+#undef FG_XAGG_FWD
+  FG_LAUNCH_CHECK();
+  return FG_OK;
+}
+
+extern "C" int fg_gat_code_xagg_bwd(const fg_codec_desc* codec, const uint16_t* x_rows,
+                                    const int32_t* picks, int64_t d, int heads,
+                                    const int32_t* indptr, int64_t max_dst,
+                                    const int64_t* n_dst_dev, const uint16_t* dA, float* dalpha,
+                                    void* s) {
+  FG_CHECK_ARG(gat_codes_ok(codec, x_rows) && indptr && n_dst_dev && dA && dalpha &&
+                   (heads == 1 || heads == 2 || heads == 4 || heads == 8) && d >= 1 &&
+                   d <= 32 * fg::kXI,
+               "fg_gat_code_xagg_bwd: bad argument (heads in {1,2,4,8}, d <= 256)");
+  if (max_dst == 0) return FG_OK;
+  const fg::GatCodes g = gat_codes(codec, x_rows, d, picks);
+  const auto* dAb = reinterpret_cast<const __nv_bfloat16*>(dA);
+  const dim3 grid(grid_for(max_dst * 32, 256));
+  cudaStream_t st = as_stream(s);
+#define FG_XAGG_BWD(H, XI) \
+  fg::k_gat_code_xagg_bwd<H, XI><<<grid, 256, 0, st>>>(g, (int)d, indptr, max_dst, n_dst_dev, \
+                                                        dAb, dalpha)
+  const bool small = d <= 128;
+  switch (heads) {
+    case 1: if (small) FG_XAGG_BWD(1, 4); else FG_XAGG_BWD(1, 8); break;
+    case 2: if (small) FG_XAGG_BWD(2, 4); else FG_XAGG_BWD(2, 8); break;
+    case 4: if (small) FG_XAGG_BWD(4, 4); else FG_XAGG_BWD(4, 8); break;
+    default: if (small) FG_XAGG_BWD(8, 4); else FG_XAGG_BWD(8, 8); break;
+  }
+#undef FG_XAGG_BWD
   FG_LAUNCH_CHECK();
   return FG_OK;
 }

@@ -13,8 +13,9 @@ sample itself has no representation at the layer below, so the
 query is the mean of its sampled neighbours' er.
 
 Input layer: the sources of the last block are its picks (one row per pick),
-decoded on the device by the codec's gather-dequant kernel (bf16) and
-projected by one GEMM; hidden layers project the previous layer's output.
+read straight from the codec's code rows by the scores / attention-weighted
+aggregation kernels (decoded in registers) and projected by one block-
+diagonal GEMM; hidden layers project the previous layer's output.
 Edge operators are CUDA kernels wrapped as autograd Functions; the GEMMs,
 LeakyReLU/ELU and the loss are torch/cuBLAS plus the fused softmax-CE kernel.
 """
@@ -89,6 +90,29 @@ class GatAggregate(torch.autograd.Function):
         return dz, dalpha, None, None, None, None
 
 
+class PickSource:
+    """The last block's picks as the input layer reads them: decoded once by
+    the codec's gather kernel into bf16 rows (one per pick, pick order).
+    The code-reading form of the same kernels (``decoded=False``: elements
+    decoded in registers from the code rows, SQ any k / VQ 8-bit) is kept for
+    A/B: measured slower on the B200 (products-shape SQ8: per-thread byte
+    decodes are less coalesced than one bf16 row gather + cuBLAS)."""
+
+    def __init__(self, codec, picks, n_picks, e_cap: int, decoded: bool = True):
+        import ctypes
+        self.codec, self.picks, self.n_picks, self.e_cap = codec, picks, n_picks, int(e_cap)
+        self.d = codec.d
+        desc = codec.desc
+        direct = not decoded and ((desc.kind == N.CODEC_SQ and desc.elem_bits == 32) or
+                                  (desc.kind == N.CODEC_VQ and desc.bits == 8))
+        self.x = None if direct else codec.gather(picks, out_dtype=torch.bfloat16, check=False)
+        self._desc = ctypes.byref(desc)
+
+    def head(self):
+        """(codec desc, decoded rows or None, picks) -- the kernels' first args."""
+        return (self._desc, N.ptr(self.x), N.ptr(self.picks))
+
+
 class PickScores(torch.autograd.Function):
     """s = x c^T for the decoded picks x [E, d] (bf16) and c [2H, d]; the
     backward dc = ds^T x has K = E (~5e5): split into 64 chunks reduced by
@@ -112,64 +136,56 @@ class PickScores(torch.autograd.Function):
         return None, part.float().sum(0)
 
 
-def _chunked_sum_bmm(a, b, ch: int = 64):
-    """sum_n a[n]^T b[n] for a [N, p], b [N, q] with N ~ 1e5: 64 K-chunks in
-    one batched GEMM, then a sum (cuBLAS picks an 8-CTA kernel for the
-    single skinny K = N product)."""
-    n = a.shape[0]
-    pad = (-n) % ch
-    if pad:
-        a = torch.cat([a, a.new_zeros(pad, a.shape[1])])
-        b = torch.cat([b, b.new_zeros(pad, b.shape[1])])
-    return torch.bmm(a.view(ch, -1, a.shape[1]).transpose(1, 2),
-                     b.view(ch, -1, b.shape[1])).sum(0)
-
-
-class HeadProject(torch.autograd.Function):
-    """out[n, k*F:(k+1)*F] = agg[n, k*d:(k+1)*d] @ w[k]^T, w [H, F, d]."""
+class GatInputScores(torch.autograd.Function):
+    """el, er [e_cap, H] = per-pick scores x_e . c[k] from the code rows;
+    backward dc = sum_e ds_e x_e^T (deterministic block partials)."""
 
     @staticmethod
-    def forward(ctx, agg, w):
-        n = agg.shape[0]
-        H, f, d = w.shape
-        a = agg.view(n, H, d).transpose(0, 1).to(torch.bfloat16)          # [H, n, d]
-        out = torch.bmm(a, w.to(torch.bfloat16).transpose(1, 2))           # [H, n, F]
-        ctx.save_for_backward(a, w)
-        return out.transpose(0, 1).reshape(n, H * f).float()
+    def forward(ctx, c, src, heads: int):
+        c = c.float().contiguous()
+        el = torch.empty((src.e_cap, heads), dtype=torch.float32, device=c.device)
+        er = torch.empty_like(el)
+        N.call("fg_gat_code_scores", *src.head(), N.ptr(src.n_picks), src.e_cap, src.d, heads,
+               N.ptr(c), N.ptr(el), N.ptr(er), N.stream_handle())
+        ctx.src, ctx.heads = src, heads
+        return el, er
 
     @staticmethod
-    def backward(ctx, dout):
-        a, w = ctx.saved_tensors
-        H, f, d = w.shape
-        n = a.shape[1]
-        g = dout.view(n, H, f).transpose(0, 1).to(torch.bfloat16)          # [H, n, F]
-        dw = torch.stack([_chunked_sum_bmm(g[k], a[k]) for k in range(H)])  # [H, F, d]
-        return None, dw.float()
+    def backward(ctx, del_, der):
+        src, heads = ctx.src, ctx.heads
+        nb = N.lib().fg_gat_code_scores_bwd_blocks(src.e_cap)
+        part = torch.empty((nb, 2 * heads, src.d), dtype=torch.float32, device=del_.device)
+        z = torch.zeros((src.e_cap, heads), dtype=torch.float32, device=del_.device)
+        del_ = z if del_ is None else del_.float().contiguous()
+        der = z if der is None else der.float().contiguous()
+        N.call("fg_gat_code_scores_bwd", *src.head(), N.ptr(src.n_picks), src.e_cap, src.d, heads,
+               N.ptr(del_), N.ptr(der), N.ptr(part), N.stream_handle())
+        return part.sum(0), None, None
 
 
-class GatInputAggregate(torch.autograd.Function):
-    """A[v, k*d:(k+1)*d] = sum_e alpha[e,k] x[e] over decoded pick rows x
-    (constant input: no dx)."""
-
-    @staticmethod
-    def forward(ctx, x, alpha, indptr, n_dst, max_dst: int):
-        x = x.to(torch.bfloat16).contiguous()
-        d, heads = x.shape[1], alpha.shape[1]
-        out = torch.empty((max_dst, heads * d), dtype=torch.float32, device=x.device)
-        N.call("fg_gat_xagg_fwd", N.ptr(x), d, heads, N.ptr(alpha), N.ptr(indptr), max_dst,
-               N.ptr(n_dst), N.ptr(out), N.stream_handle())
-        ctx.save_for_backward(x, indptr, n_dst)
-        ctx.max_dst, ctx.heads, ctx.e_cap = max_dst, heads, alpha.shape[0]
-        return out
+class GatInputXagg(torch.autograd.Function):
+    """A [max_dst, H*d] bf16 = per head the alpha-weighted sum of the picks'
+    decoded rows; backward dalpha[e, k] = <dA[v, k], x_e>."""
 
     @staticmethod
-    def backward(ctx, dout):
-        x, indptr, n_dst = ctx.saved_tensors
-        dalpha = torch.zeros((ctx.e_cap, ctx.heads), dtype=torch.float32, device=x.device)
-        N.call("fg_gat_xagg_bwd", N.ptr(x), x.shape[1], ctx.heads, N.ptr(indptr), ctx.max_dst,
-               N.ptr(n_dst), N.ptr(dout.float().contiguous()), N.ptr(dalpha), ctx.e_cap,
-               N.stream_handle())
-        return None, dalpha, None, None, None
+    def forward(ctx, alpha, src, indptr, n_dst, max_dst: int, heads: int):
+        alpha = alpha.float().contiguous()
+        A = torch.empty((max_dst, heads * src.d), dtype=torch.bfloat16, device=alpha.device)
+        N.call("fg_gat_code_xagg_fwd", *src.head(), src.d, heads, N.ptr(alpha), N.ptr(indptr),
+               max_dst, N.ptr(n_dst), N.ptr(A), N.stream_handle())
+        ctx.save_for_backward(indptr, n_dst)
+        ctx.src, ctx.max_dst, ctx.heads = src, max_dst, heads
+        return A
+
+    @staticmethod
+    def backward(ctx, dA):
+        indptr, n_dst = ctx.saved_tensors
+        src, heads = ctx.src, ctx.heads
+        dalpha = torch.zeros((src.e_cap, heads), dtype=torch.float32, device=dA.device)
+        dA = dA.to(torch.bfloat16).contiguous()
+        N.call("fg_gat_code_xagg_bwd", *src.head(), src.d, heads, N.ptr(indptr), ctx.max_dst,
+               N.ptr(n_dst), N.ptr(dA), N.ptr(dalpha), N.stream_handle())
+        return dalpha, None, None, None, None, None
 
 
 class GatLayer(nn.Module):
@@ -200,20 +216,29 @@ class GatLayer(nn.Module):
         alpha = GatAttention.apply(el, er, indptr, local, n_dst, max_dst, e_cap, slope)
         return GatAggregate.apply(z, alpha, indptr, local, n_dst, max_dst) + self.bias
 
-    def _forward_input(self, x, indptr, n_dst, max_dst, e_cap, slope):
+    def _forward_input(self, src, indptr, n_dst, max_dst, e_cap, slope):
         """Same math for the input layer, rearranged by linearity: scores
-        el = x (W_k^T a_l[k]) per pick, the attention-weighted sum of the
-        decoded picks per head, then one [N_dst, d] x [d, F] product per head
-        -- no per-pick projection (518 K x 256 at products shape)."""
+        el = x (W_k^T a_l[k]) per pick (one skinny GEMM on the decoded picks),
+        the attention-weighted sum of the picks' rows per head (A,
+        [N_dst, H*d] bf16, one kernel), then out = A . blockdiag(W_k^T) + b:
+        one GEMM, no per-pick projection.  Every step is differentiable: dA
+        flows back to the attention (round 1's head projection dropped it, so
+        layer 0's attention vectors never trained)."""
         H, f = self.heads, self.width // self.heads
-        d = x.shape[1]
+        d = src.d
         w = self.lin.weight.view(H, f, d)                       # [H, F, d]
         c = torch.cat([torch.einsum("hfd,hf->hd", w, self.attn_l),
                        torch.einsum("hfd,hf->hd", w, self.attn_r)])  # [2H, d]
-        s = PickScores.apply(x.to(torch.bfloat16), c)           # [E, 2H]
-        alpha = GatAttention.apply(s[:, :H], s[:, H:], indptr, None, n_dst, max_dst, e_cap, slope)
-        agg = GatInputAggregate.apply(x, alpha, indptr, n_dst, max_dst)   # [N, H*d]
-        return HeadProject.apply(agg, w) + self.bias
+        if src.x is not None:  # decoded rows: the scores are one skinny GEMM
+            sc = PickScores.apply(src.x, c)
+            el, er = sc[:, :H].contiguous(), sc[:, H:].contiguous()
+        else:
+            el, er = GatInputScores.apply(c, src, H)
+        alpha = GatAttention.apply(el, er, indptr, None, n_dst, max_dst, e_cap, slope)
+        A = GatInputXagg.apply(alpha, src, indptr, n_dst, max_dst, H)   # [N, H*d] bf16
+        w_bd = torch.block_diag(*[w[k].t() for k in range(H)])         # [H*d, H*F]
+        # bias folded into the GEMM; the output stays in the autocast dtype
+        return torch.addmm(self.bias.to(A.dtype), A, w_bd.to(A.dtype))
 
 
 class GatModel(nn.Module):
@@ -235,10 +260,10 @@ class GatModel(nn.Module):
                 layers.append(GatLayer(d_in, hidden // heads, heads))
         self.layers = nn.ModuleList(layers)
 
-    def forward(self, x_picks, sb, caps, pick_cap):
-        """x_picks: decoded input rows of the last block's picks [pick_cap, d]."""
+    def forward(self, src, sb, caps, pick_cap):
+        """src: the last block's picks (PickSource: code rows or decoded rows)."""
         L = len(self.layers)
-        h = x_picks
+        h = src
         for i, layer in enumerate(self.layers):
             l = L - 1 - i  # block feeding layer i
             local = None if l == L - 1 else sb.local[l]
@@ -262,9 +287,9 @@ class GatConfig:
 
 class GatTrainer:
     """Single-process (or one-rank-of-DDP) GAT trainer over device-resident
-    data: sample -> decode the last block's picks (codec gather-dequant, bf16)
-    -> GAT layers -> fused softmax-CE -> autograd backward -> flat all-reduce
-    -> Adam; one CUDA graph per step."""
+    data: sample -> GAT layers (input layer straight from the picks' code
+    rows) -> fused softmax-CE -> autograd backward into one flat gradient ->
+    flat all-reduce -> flat Adam; one CUDA graph per step."""
 
     def __init__(self, graph, codec, labels, num_classes: int, cfg: GatConfig,
                  process_group=None):
@@ -278,13 +303,30 @@ class GatTrainer:
         self.caps = self.sampler.caps
         self.pick_cap = self.sampler.pcaps[L - 1]
         self.model = GatModel(codec.d, cfg.hidden, num_classes, L, cfg.heads).to(self.device)
-        self.opt = torch.optim.Adam(self.model.parameters(), lr=cfg.lr, capturable=True)
+        # one flat fp32 buffer each for params / grads (the parameters and their
+        # .grad are views): one memset, one all-reduce and one Adam kernel per
+        # step instead of per-tensor foreach launches
+        from .sage import FlatAdam
+        params = list(self.model.parameters())
+        total = sum(p.numel() for p in params)
+        self.flat_param = torch.zeros(total, dtype=torch.float32, device=self.device)
+        self.flat_grad = torch.zeros(total, dtype=torch.float32, device=self.device)
+        off = 0
+        for p in params:
+            n = p.numel()
+            self.flat_param[off:off + n].copy_(p.data.reshape(-1))
+            p.data = self.flat_param[off:off + n].view_as(p)
+            p.grad = self.flat_grad[off:off + n].view_as(p)
+            off += n
+        if self.world > 1:
+            torch.distributed.broadcast(self.flat_param, 0, group=self.pg)
+        self.opt = FlatAdam(self.flat_param, self.flat_grad, lr=cfg.lr)
         self.loss_buf = torch.zeros((), dtype=torch.float32, device=self.device)
         self.graph = None
 
     def _decode(self, sb):
         L = len(self.cfg.fanouts)
-        return self.codec.gather(sb.picks[L - 1], out_dtype=torch.bfloat16, check=False)
+        return PickSource(self.codec, sb.picks[L - 1], sb.n_picks[L - 1], self.pick_cap)
 
     def _body(self, k: int = 0):
         sb = self.sampler.sample_loaded()
@@ -293,11 +335,9 @@ class GatTrainer:
             logits = self.model(x, sb, self.caps, self.pick_cap)
         loss = softmax_ce(logits.contiguous(), self.labels, sb.nodes[0], sb.n_nodes[0],
                           self.model.num_classes)
-        self.opt.zero_grad(set_to_none=False)
+        self.flat_grad.zero_()
         loss.backward()
-        if self.world > 1:
-            for p in self.model.parameters():
-                ddp.average_flat_(p.grad.view(-1), self.pg)
+        ddp.average_flat_(self.flat_grad, self.pg)
         self.opt.step()
         self.loss_buf.copy_(loss.detach())
 
@@ -362,9 +402,9 @@ class GatTrainer:
         self.model.eval()
         for b in range(nb):
             sb = smp.sample(b)
-            x = self.codec.gather(sb.picks[L - 1], out_dtype=torch.bfloat16, check=False)
+            src = PickSource(self.codec, sb.picks[L - 1], sb.n_picks[L - 1], smp.pcaps[L - 1])
             with torch.autocast("cuda", dtype=torch.bfloat16):
-                logits = self.model(x, sb, smp.caps, smp.pcaps[L - 1])
+                logits = self.model(src, sb, smp.caps, smp.pcaps[L - 1])
             valid = torch.arange(smp.caps[0], device=self.device) < sb.n_nodes[0]
             y = self.labels[sb.nodes[0].long()].long()
             pred = logits[:, :self.model.num_classes].argmax(1)

@@ -117,3 +117,65 @@ def test_gat_graphed_training_learns():
         losses += [float(t.step(b).item()) for b in range(nb)]
     assert np.isfinite(losses).all() and np.mean(losses[-5:]) < losses[0]
     assert t.evaluate(val) > 0.3
+
+
+@pytest.mark.parametrize("codec_kind", ["sq8", "sq4", "vq"])
+def test_gat_gradients_match_cpu_oracle_model(codec_kind):
+    """One batch, same weights: the GPU GAT (input layer straight from the
+    code rows, bf16 autocast) and the CPU fp32 oracle GAT on the oracle's
+    decodes give the same loss and the same gradient for EVERY parameter --
+    including layer 0's attention vectors (round 1's head projection dropped
+    dA, so they received none)."""
+    from paper_2207_14696_b200.gat import PickSource
+    from paper_2207_14696_b200.synth import build_vq_codec
+    from oracle.sampler import sample_batches_oracle
+    n, d, C = 6000, 40, 5
+    dg, labels = generate_graph(n, 12.0, C, seed=3)
+    if codec_kind == "vq":
+        dc, _ = build_vq_codec(n, d, 4, 256, labels=labels, num_classes=C, seed=3, max_iters=3,
+                               restarts=1)
+        codes = dc.rows[:, :dc.num_parts].cpu().numpy().astype(np.int32)
+
+        def decode_rows(rows):
+            return oc.vq_decode(codes, dc.books_host, d, 4, rows)
+    else:
+        k = 8 if codec_kind == "sq8" else 4
+        dc = build_sq_codec(n, d, k, labels=labels, num_classes=C, seed=3)
+        c = dc.to_codec()
+
+        def decode_rows(rows):
+            return oc.sq_dequant_rows(c.payload, n, d, k, c.params.e_min, c.params.e_max, rows)
+    train, _ = split_ids(n, n // 4, n // 10, 3)
+    fans, bs = (10, 5), 256
+    t = GatTrainer(dg, dc, labels, C, GatConfig(fanouts=fans, batch_size=bs, hidden=64, heads=4,
+                                                use_graph=False))
+    t.begin_epoch(train, 0)
+    t.sampler.load_seeds(0)
+    sb = t.sampler.sample_loaded()
+    L = len(fans)
+    src = PickSource(dc, sb.picks[L - 1], sb.n_picks[L - 1], t.pick_cap)
+    with torch.autocast("cuda", dtype=torch.bfloat16):
+        logits = t.model(src, sb, t.caps, t.pick_cap)
+    nd = int(sb.n_nodes[0].item())
+    y = labels[sb.nodes[0][:nd].long()].long()
+    loss = F.cross_entropy(logits[:nd, :C].float(), y)
+    t.model.zero_grad()
+    loss.backward()
+    # the oracle on the same batch (reference sampler restatement)
+    host = dg.to_host()
+    ref, _ = sample_batches_oracle(host.row_offsets, host.col_indices, train, fans, bs, 0,
+                                   max_batches=1)
+    cpu_model = ot.OracleGat(d, 64, C, L, heads=4)
+    cpu_model.load_state_dict(t.reference_state())
+    x, blocks = ot.gat_batch_tensors(ref[0], decode_rows)
+    lab = labels.cpu().numpy()
+    loss_c = F.cross_entropy(cpu_model(x, blocks), torch.from_numpy(lab[ref[0].seeds]).long())
+    loss_c.backward()
+    assert abs(float(loss) - float(loss_c)) < 2e-2 * abs(float(loss_c)), (float(loss), float(loss_c))
+    gpu_grads = dict(t.model.named_parameters())
+    for name, p in cpu_model.named_parameters():
+        g_ref = p.grad
+        g = gpu_grads[name].grad.float().cpu()
+        assert g_ref is not None and g_ref.norm() > 0, name
+        rel = ((g - g_ref).norm() / g_ref.norm()).item()
+        assert rel < 1e-1, (name, rel)  # bf16 autocast vs fp32
