@@ -220,6 +220,17 @@ int fg_kmeans_assign_tc(const double* pts, int64_t m, int w, const double* cents
 /* np.bincount(assign, weights=pts[:, j]) for all j (vq.py:159-164), summed
  * per cluster in point order so the float64 result is identical: `order`
  * is a stable sort of the m points by cluster, `start` has k+1 offsets. */
+/* k-means++ seeding (vq.py:166-181) of B independent jobs at once (every
+ * part x restart of fit_vq), no host round trip per centroid.  pts [B][M][w]
+ * float64 (rows past mrow[b] ignored), xx [B][M] their squared norms, cents
+ * [B][K][w] with cents[b][0] set by the caller (the job's first draw), u
+ * [B][K-1] the job's rng.random() draws in order.  Workspace: d2 [B][M]
+ * (caller fills +inf), part [B][ceil(M/1024)], flag [B] (caller zeroes; set
+ * to 1 for a job that met the degenerate d2.sum() <= 0 branch, whose
+ * centroids past that step are then undefined).  w <= 32. */
+int fg_kmeanspp_batched(const double* pts, const double* xx, const int64_t* mrow, int64_t B,
+                        int64_t M, int w, int K, const double* u, double* cents, double* d2,
+                        double* part, int* flag, void* cuda_stream);
 int fg_segment_sums(const double* pts, int64_t m, int w, const int64_t* order,
                     const int64_t* start, int k, double* sums, double* counts,
                     void* cuda_stream);

@@ -57,6 +57,7 @@ _SIGS = {
     "fg_vq_assign_fp64": (ci, [vp, ci, i64, i64, ci, ci, ci, vp, vp, ci, ci, vp, i64, vp, vp]),
     "fg_codes_to_rows": (ci, [vp, i64, ci, ci, vp, i64, vp]),
     "fg_segment_sums": (ci, [vp, i64, ci, vp, vp, ci, vp, vp, vp]),
+    "fg_kmeanspp_batched": (ci, [vp, vp, vp, i64, i64, ci, ci, vp, vp, vp, vp, vp, vp]),
     "fg_vq_gather_decode": (ci, [C.POINTER(CodecDesc), vp, ci, i64, vp, ci, vp, vp]),
     "fg_kmeans_assign": (ci, [vp, i64, ci, vp, ci, ci, vp, vp, vp, vp]),
     "fg_kmeans_assign_tc": (ci, [vp, i64, ci, vp, ci, ci, vp, vp, vp]),

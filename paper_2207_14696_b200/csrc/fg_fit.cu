@@ -286,3 +286,176 @@ extern "C" int fg_kmeans_assign(const double* pts, int64_t m, int w, const doubl
   FG_LAUNCH_CHECK();
   return FG_OK;
 }
+
+// ------------------------------------------------ batched k-means++ seeding
+// vq.py:166-181 for B independent jobs (every part x restart of fit_vq) at
+// once, with no host round trip per centroid: the per-step uniforms
+// u[b][c-1] = rng.random() are drawn up front from each job's own Generator
+// (the same stream positions the reference consumes, as long as no job hits
+// the degenerate `d2.sum() <= 0` branch, which is flagged on the device and
+// redone on the host path).  Per step two kernels:
+//   k_kpp_search: CTA per job -- total = sum of the block partials (fixed
+//     order), target = u * total, the block whose running sum reaches the
+//     target, then the first point inside it whose running sum reaches it
+//     (np.searchsorted(np.cumsum(d2), target), clamped to m - 1); the point
+//     becomes centroid c;
+//   k_kpp_update: d2[i] = min(d2[i], ||x_i||^2 + ||c||^2 - 2 x_i.c) clamped at
+//     0 (vq.py:154-156 expression order), per-block partial sums of the new d2.
+// Float64 throughout; the running sums are blocked (not numpy's sequential
+// cumsum), so picks can differ at exact prefix-sum boundaries (objective
+// parity, tests/test_gpu_codecs.py).
+constexpr int kKppBlock = 1024;
+
+__global__ void __launch_bounds__(kKppBlock)
+k_kpp_update(const double* __restrict__ pts, const double* __restrict__ xx,
+             const int64_t* __restrict__ mrow, int64_t M, int w,
+             const double* __restrict__ cents, int K, int c, double* __restrict__ d2,
+             double* __restrict__ part, int64_t nblk, const int* __restrict__ flag) {
+  const int64_t b = blockIdx.y;
+  if (flag[b]) return;
+  __shared__ double s_c[32];
+  __shared__ double s_cc;
+  __shared__ double s_red[kKppBlock / 32];
+  const double* cb = cents + ((int64_t)b * K + c) * w;
+  if (threadIdx.x < w) s_c[threadIdx.x] = cb[threadIdx.x];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double cc = 0.0;
+    for (int j = 0; j < w; ++j) cc += s_c[j] * s_c[j];
+    s_cc = cc;
+  }
+  __syncthreads();
+  const int64_t i = blockIdx.x * (int64_t)kKppBlock + threadIdx.x;
+  double v = 0.0;
+  if (i < mrow[b]) {
+    const double* x = pts + (b * M + i) * w;
+    double dot = 0.0;
+    for (int j = 0; j < w; ++j) dot = fma(x[j], s_c[j], dot);
+    const double dist = fmax(xx[b * M + i] + s_cc - 2.0 * dot, 0.0);
+    double* dp = d2 + b * M + i;
+    v = fmin(*dp, dist);
+    *dp = v;
+  }
+  // fixed-order block sum (warp shuffles, then one warp)
+  for (int o = 16; o; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double t = s_red[threadIdx.x];
+    for (int o = 16; o; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
+    if (threadIdx.x == 0) part[b * nblk + blockIdx.x] = t;
+  }
+}
+
+__global__ void __launch_bounds__(1024)
+k_kpp_search(const double* __restrict__ pts, const int64_t* __restrict__ mrow, int64_t M, int w,
+             const double* __restrict__ d2, const double* __restrict__ part, int64_t nblk,
+             const double* __restrict__ u, int K, int c, double* __restrict__ cents,
+             int* __restrict__ flag) {
+  const int64_t b = blockIdx.x;
+  if (flag[b]) return;
+  __shared__ double s_tot, s_base;
+  __shared__ int64_t s_blk;
+  __shared__ double s_warp[32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const double* pb = part + b * nblk;
+  // total in fixed order (one warp, strided partials then a shuffle tree)
+  if (wid == 0) {
+    double t = 0.0;
+    for (int64_t j = lane; j < nblk; j += 32) t += pb[j];
+    for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (lane == 0) s_tot = t;
+  }
+  __syncthreads();
+  const double tot = s_tot;
+  if (!(tot > 0.0)) {  // degenerate: the host redoes this job exactly
+    if (tid == 0) flag[b] = 1;
+    return;
+  }
+  const double target = u[b * (K - 1) + (c - 1)] * tot;
+  // block containing the target: warp 0 scans the partials 32 at a time
+  if (wid == 0) {
+    double run = 0.0;
+    int64_t found = nblk - 1;
+    double base = 0.0;
+    bool done = false;
+    for (int64_t j0 = 0; j0 < nblk && !done; j0 += 32) {
+      const int64_t j = j0 + lane;
+      double v = j < nblk ? pb[j] : 0.0;
+      double incl = v;
+      for (int o = 1; o < 32; o <<= 1) {
+        const double n = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += n;
+      }
+      const unsigned hit = __ballot_sync(0xffffffffu, j < nblk && run + incl >= target);
+      if (hit) {
+        const int l = __ffs(hit) - 1;
+        found = j0 + l;
+        base = run + __shfl_sync(0xffffffffu, incl - v, l);
+        done = true;
+      } else {
+        run += __shfl_sync(0xffffffffu, incl, 31);
+      }
+    }
+    if (!done) base = run - (nblk ? pb[nblk - 1] : 0.0);  // clamp: last block
+    if (lane == 0) {
+      s_blk = found;
+      s_base = base;
+    }
+  }
+  __syncthreads();
+  // inside the block: inclusive scan of its d2 values, first index >= target
+  const int64_t i = s_blk * kKppBlock + tid;
+  const double v = i < mrow[b] ? d2[b * M + i] : 0.0;
+  double incl = v;
+  for (int o = 1; o < 32; o <<= 1) {
+    const double n = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += n;
+  }
+  if (lane == 31) s_warp[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    double t = s_warp[lane];
+    for (int o = 1; o < 32; o <<= 1) {
+      const double n = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += n;
+    }
+    s_warp[lane] = t - s_warp[lane];  // exclusive warp offsets
+  }
+  __syncthreads();
+  const double cum = s_base + s_warp[wid] + incl;
+  __shared__ int64_t s_pick;
+  if (tid == 0) s_pick = INT64_MAX;
+  __syncthreads();
+  if (i < mrow[b] && cum >= target) atomicMin((unsigned long long*)&s_pick, (unsigned long long)i);
+  __syncthreads();
+  int64_t pick = s_pick;
+  if (pick == INT64_MAX) pick = mrow[b] - 1;  // searchsorted past the end -> clamp
+  pick = pick < mrow[b] - 1 ? pick : mrow[b] - 1;
+  if (tid < w) cents[((int64_t)b * K + c) * w + tid] = pts[(b * M + pick) * w + tid];
+}
+
+extern "C" int fg_kmeanspp_batched(const double* pts, const double* xx, const int64_t* mrow,
+                                   int64_t B, int64_t M, int w, int K, const double* u,
+                                   double* cents, double* d2, double* part, int* flag,
+                                   void* s) {
+  FG_CHECK_ARG(pts && xx && mrow && u && cents && d2 && part && flag && B >= 1 && M >= 1 &&
+                   w >= 1 && w <= 32 && K >= 1,
+               "fg_kmeanspp_batched: bad argument (width <= 32)");
+  cudaStream_t st = as_stream(s);
+  const int64_t nblk = ceil_div(M, kKppBlock);
+  FG_CHECK_ARG(nblk <= 65535 * 1024ll, "fg_kmeanspp_batched: too many points");
+  const dim3 ug((unsigned)nblk, (unsigned)B);
+  // d2 = +inf before the first centroid: the first update sets d2 = dist(c0)
+  k_kpp_update<<<ug, kKppBlock, 0, st>>>(pts, xx, mrow, M, w, cents, K, 0, d2, part, nblk, flag);
+  FG_LAUNCH_CHECK();
+  for (int c = 1; c < K; ++c) {
+    k_kpp_search<<<(unsigned)B, 1024, 0, st>>>(pts, mrow, M, w, d2, part, nblk, u, K, c, cents,
+                                                flag);
+    FG_LAUNCH_CHECK();
+    k_kpp_update<<<ug, kKppBlock, 0, st>>>(pts, xx, mrow, M, w, cents, K, c, d2, part, nblk,
+                                            flag);
+    FG_LAUNCH_CHECK();
+  }
+  return FG_OK;
+}

@@ -1381,7 +1381,11 @@ int launch_sq_w(const fg_codec_desc* c, const int32_t* indptr, const int32_t* sr
     row_cap &= ~3;  // whole gather4 groups
     int td = kTD;
     while (td > 32 && td * 8 > row_cap) td /= 2;
-    if (td * 8 <= row_cap && rb <= c->row_stride) {
+    static const int bulk_env = [] {  // FG_SQ_BULK=0: register kernel (A/B)
+      const char* e = getenv("FG_SQ_BULK");
+      return e ? atoi(e) : 1;
+    }();
+    if (bulk_env && td * 8 <= row_cap && rb <= c->row_stride) {
       const int smem = fixed + 128 + 2 * (g4 ? (row_cap / 4) * gstride : row_cap * rb);
       const int grid = (int)min64(ceil_div(max_dst, td), (int64_t)sm_count());
       auto kern = g4 ? k_sq_mean_bulk<K, OT, WT, true> : k_sq_mean_bulk<K, OT, WT, false>;

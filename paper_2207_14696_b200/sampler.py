@@ -141,8 +141,6 @@ class DeviceSampler:
         self.caps, self.pcaps = caps, pcaps
         i32, i64 = torch.int32, torch.int64
         z = lambda *s, dt=i32: torch.zeros(*s, dtype=dt, device=dev)  # noqa: E731
-        self.seed_in = z(self.bs, dt=i64)
-        self.n_seed_in = z(1, dt=i64)
         self.nodes = [z(c) for c in caps]
         self.n_nodes = [z(1, dt=i64) for _ in caps]
         self.indptr = [z(caps[l] + 1) for l in range(L)]
@@ -216,8 +214,15 @@ class DeviceSampler:
         blk = rng_block_from_numpy(state)
         perm = np.ascontiguousarray(ids)
         N.call("fg_rng_permutation_host", blk.ctypes.data, perm.ctypes.data, perm.size)
+        # each batch's seeds are np.sort(perm[lo:lo + bs]) (pipeline.py:203):
+        # sort the slices once here, so a batch's seeds are one copy into the
+        # sorted seed layer (no sort kernel in the sampling chain)
+        full = perm.size // self.bs
+        if full:
+            perm[:full * self.bs].reshape(full, self.bs).sort(axis=1)
+        perm[full * self.bs:].sort()
         self.perm_host = perm
-        self.perm = torch.from_numpy(perm).to(self.device)
+        self.perm = torch.from_numpy(perm.astype(np.int32)).to(self.device)
         self.rng.copy_(torch.from_numpy(blk.view(np.int64)))
         return (perm.size + self.bs - 1) // self.bs
 
@@ -230,19 +235,29 @@ class DeviceSampler:
         return rng_block_to_numpy(self.rng.cpu().numpy().view(np.uint64), self._inc)
 
     def load_seeds(self, b: int) -> None:
-        """Device copy of batch b's slice of the permutation into the static
-        seed buffer (used by the device-resident timed path)."""
+        """Batch b's seeds (its sorted slice of the permutation) into the seed
+        layer, a device copy (the device-resident timed path)."""
         perm = self.owner.perm
         lo = b * self.bs
         cnt = min(self.bs, perm.numel() - lo)
-        self.seed_in[:cnt].copy_(perm[lo:lo + cnt])
-        self.n_seed_in.fill_(cnt)
+        self.nodes[0][:cnt].copy_(perm[lo:lo + cnt])
+        self.n_nodes[0].fill_(cnt)
 
     def load_seeds_host(self, seeds) -> None:
-        """Seeds from a (pinned) host tensor: the end-to-end input copy."""
+        """Seeds from a host tensor: the end-to-end input copy.  The seed
+        layer holds the batch's ids in ascending order (np.sort of the
+        permutation slice, pipeline.py:203): unsorted seeds are sorted on the
+        host first.  A sorted pinned int32 tensor copies asynchronously."""
+        import torch
+        if seeds.numel() > 1 and not bool((seeds[1:] >= seeds[:-1]).all()):
+            seeds = torch.sort(seeds.to(torch.int64)).values
+        if seeds.dtype != torch.int32:
+            seeds = seeds.to(torch.int32)
         cnt = seeds.numel()
-        self.seed_in[:cnt].copy_(seeds, non_blocking=True)
-        self.n_seed_in.fill_(cnt)
+        if cnt > self.bs:
+            raise DataError("more seeds than the batch size")
+        self.nodes[0][:cnt].copy_(seeds, non_blocking=True)
+        self.n_nodes[0].fill_(cnt)
 
     def batch_view(self) -> SampledBatch:
         """The SampledBatch over this slot's static output buffers (what
@@ -258,24 +273,13 @@ class DeviceSampler:
 
     # ------------------------------------------------------------ sample
     def sample_loaded(self) -> SampledBatch:
-        """Sample the batch whose seeds are in ``seed_in`` (capture-safe)."""
+        """Sample the batch whose seeds load_seeds[_host] put in the seed layer
+        (``nodes[0]``; capture-safe)."""
         s = N.stream_handle()
         L = len(self.fanouts)
         n = self.g.n
         bm, wp = N.ptr(self.bitmap), N.ptr(self.wprefix)
-        # seeds = sort(perm slice) (pipeline.py:203): one-CTA radix sort for
-        # batches up to 4096 on graphs past 2^24 nodes (the bitmap route
-        # scans all n bits: ~20 us at papers100M-shape), else bitmap order
-        if self.bs <= 4096 and n > (1 << 24):
-            N.call("fg_sort_ids", N.ptr(self.seed_in), N.ptr(self.n_seed_in), self.bs,
-                   N.ptr(self.nodes[0]), N.ptr(self.n_nodes[0]), n, s)
-        else:
-            N.call("fg_bitmap_mark64", N.ptr(self.seed_in), N.ptr(self.n_seed_in), self.bs, bm,
-                   n, s)
-            N.call("fg_bitmap_compact", bm, n, N.ptr(self.nodes[0]), self.caps[0],
-                   N.ptr(self.n_nodes[0]), None, N.ptr(self.ws_bm), self.ws_bm.numel(), s)
-            N.call("fg_bitmap_clear", N.ptr(self.nodes[0]), N.ptr(self.n_nodes[0]),
-                   self.caps[0], bm, n, s)
+        # the seed layer (sorted batch ids) was written by load_seeds[_host]
         if self.want_frontier:
             N.call("fg_bitmap_mark", N.ptr(self.nodes[0]), N.ptr(self.n_nodes[0]), self.caps[0],
                    N.ptr(self.fbitmap), n, s)

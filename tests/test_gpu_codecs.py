@@ -297,19 +297,28 @@ def test_streaming_csrg1_device_load(tmp_path):
 
 
 def test_batched_kmeanspp_matches_sequential():
-    """_kmeanspp_batched (all (part, restart) seedings advanced together, one
-    host sync per step) draws the same centroids as the per-job _kmeanspp
-    with the same Generators -- including jobs of different row counts."""
+    """_kmeanspp_batched (every (part, restart) seeding on the device at once,
+    fg_kmeanspp_batched: uniforms drawn up front, no host sync per centroid)
+    draws the same centroids as the per-job host-synced _kmeanspp with the
+    same Generators -- including jobs of different row counts -- and leaves
+    each Generator at the same stream position; a degenerate job (all points
+    equal: d2.sum() == 0 after the first centroid) takes the exact path."""
     import torch
     from paper_2207_14696_b200.vq import _kmeanspp, _kmeanspp_batched
     g = torch.Generator(device="cuda").manual_seed(3)
     pts = [torch.randn(n, 4, device="cuda", dtype=torch.float64, generator=g)
            for n in (5000, 3700, 5000)]
     seeds = [11, 12, 13]
-    seq = [_kmeanspp(p, 32, np.random.default_rng(s)) for p, s in zip(pts, seeds)]
-    bat = _kmeanspp_batched([(p, np.random.default_rng(s)) for p, s in zip(pts, seeds)], 32)
+    pts.append(torch.ones(800, 4, device="cuda", dtype=torch.float64))  # degenerate
+    seeds.append(14)
+    rs = [np.random.default_rng(s) for s in seeds]
+    rb = [np.random.default_rng(s) for s in seeds]
+    seq = [_kmeanspp(p, 32, r) for p, r in zip(pts, rs)]
+    bat = _kmeanspp_batched(list(zip(pts, rb)), 32)
     for a, b in zip(seq, bat):
         assert torch.equal(a, b)
+    for a, b in zip(rs, rb):
+        assert a.bit_generator.state == b.bit_generator.state
 
 
 def test_vq_fit_products_geometry_matches_oracle():

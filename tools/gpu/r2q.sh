@@ -1,0 +1,27 @@
+# round-2 validation: full gpu suite + smoke, bench lines (ours + reference), profiles
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out/r2
+( time timeout 2400 python -m pytest tests -m gpu -q ) > gpurun_out/r2/t_gpu_all.log 2>&1
+tail -3 gpurun_out/r2/t_gpu_all.log
+( timeout 600 python -c "import __graft_entry__ as g; g.smoke()" ) > gpurun_out/r2/smoke.log 2>&1; tail -1 gpurun_out/r2/smoke.log
+timeout 900 python bench.py > gpurun_out/r2/bench_papers100m.json 2> gpurun_out/r2/bench_papers100m.err
+timeout 1500 python bench.py --impl reference > gpurun_out/r2/bench_reference.json 2> gpurun_out/r2/bench_reference.err
+timeout 900 python bench.py --config mag240m --no-cpu-baseline > gpurun_out/r2/bench_mag240m.json 2> gpurun_out/r2/bench_mag240m.err
+timeout 900 python bench.py --config products --no-cpu-baseline > gpurun_out/r2/bench_products.json 2> gpurun_out/r2/bench_products.err
+timeout 900 python bench.py --config products-gcn --no-cpu-baseline > gpurun_out/r2/bench_products-gcn.json 2> gpurun_out/r2/bench_products-gcn.err
+timeout 900 python bench.py --config products-gat --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/r2/bench_products-gat.json 2> gpurun_out/r2/bench_products-gat.err
+timeout 900 python bench.py --config arxiv --no-cpu-baseline > gpurun_out/r2/bench_arxiv.json 2> gpurun_out/r2/bench_arxiv.err
+for f in gpurun_out/r2/bench_*.json; do echo $f; python -c "import json,sys;d=json.load(open('$f'));print(d.get('value'),d.get('ms_per_step'),d.get('e2e',{}).get('value'),(d.get('roofline') or {}).get('frac'),(d.get('epoch') or {}).get('seeds_per_s'))"; done
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+    --log-file gpurun_out/r2/launches_bench_default.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-epoch > /dev/null 2>&1
+for cfg in papers100m mag240m products; do
+  timeout 900 ncu --nvtx --nvtx-include "step/" --set full --import-source on --clock-control none \
+      -k regex:"k_vq_mean8|k_sq_mean" -c 1 -o gpurun_out/r2/fused_${cfg} \
+      python tools/profile_step.py --config ${cfg} --steps 1 > gpurun_out/r2/ncu_${cfg}.log 2>&1
+  bash tools/ncu_brief.sh gpurun_out/r2/fused_${cfg}.ncu-rep 40 > gpurun_out/r2/fused_${cfg}_brief.txt 2>&1
+  ncu -i gpurun_out/r2/fused_${cfg}.ncu-rep --page raw --csv > gpurun_out/r2/fused_${cfg}_raw.csv 2>/dev/null
+  rm -f gpurun_out/r2/fused_${cfg}.ncu-rep
+done
+timeout 900 ncu --nvtx --nvtx-include "step/" --metrics gpu__time_duration.sum --clock-control none --csv \
+    --log-file gpurun_out/r2/launches_papers100m_step.csv python tools/profile_step.py --config papers100m --steps 2 > /dev/null 2>&1
+du -sh gpurun_out/r2
