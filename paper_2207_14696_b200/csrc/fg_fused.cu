@@ -822,6 +822,47 @@ __device__ __forceinline__ void lane_issue_codes(uint8_t* dst, const int32_t* s_
   }
 }
 
+// fp16 lane body, C staged picks (compile-time count: no per-pick
+// predication): C code bytes (lane-contiguous), C conflict-free 16/8-byte
+// lookups, W/2 HADD2 each.  ncu of the generic loop: 84.5 M instructions for
+// a MAG240M-shape launch, 71 % issue -- the per-destination predication and
+// staged/global selects, not the lookups, were the cost.
+template <int C, int W>
+__device__ __forceinline__ void lane_f16_body(const uint8_t* cp, uint32_t lbase, uint32_t* h) {
+  uint32_t code[C];
+#pragma unroll
+  for (int u = 0; u < C; ++u) code[u] = cp[u * 32];
+#pragma unroll
+  for (int u = 0; u < C; ++u) {
+    const uint32_t addr = lbase + code[u] * 128u;
+    if constexpr (W == 8) {
+      uint32_t x, y, z, w;
+      asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(x), "=r"(y), "=r"(z), "=r"(w) : "r"(addr));
+      h[0] = hadd2u(h[0], x); h[1] = hadd2u(h[1], y);
+      h[2] = hadd2u(h[2], z); h[3] = hadd2u(h[3], w);
+    } else {
+      uint32_t x, y;
+      asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(x), "=r"(y) : "r"(addr));
+      h[0] = hadd2u(h[0], x); h[1] = hadd2u(h[1], y);
+    }
+  }
+}
+template <int W>
+__device__ __forceinline__ void lane_f16_chunk(const uint8_t* cp, int cb, uint32_t lbase,
+                                               uint32_t* h) {
+  switch (cb) {
+    case 1: lane_f16_body<1, W>(cp, lbase, h); break;
+    case 2: lane_f16_body<2, W>(cp, lbase, h); break;
+    case 3: lane_f16_body<3, W>(cp, lbase, h); break;
+    case 4: lane_f16_body<4, W>(cp, lbase, h); break;
+    case 5: lane_f16_body<5, W>(cp, lbase, h); break;
+    case 6: lane_f16_body<6, W>(cp, lbase, h); break;
+    case 7: lane_f16_body<7, W>(cp, lbase, h); break;
+    default: lane_f16_body<8, W>(cp, lbase, h); break;
+  }
+}
+
 template <int W, bool WT, bool F16 = false>
 __global__ void __launch_bounds__(kLaneThreads, 1)
 k_vq_mean8_lane(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
@@ -883,6 +924,7 @@ k_vq_mean8_lane(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
   const int64_t col0 = (int64_t)(slice * 32 + lane) * W;
   const bool full_part = col0 + W <= d;
   const bool vec_ok = (ld % 8) == 0;  // 16-B aligned bf16 row segments
+  const float pscale = (F16 && active) ? __ldg(part_scale + slice * 32 + lane) : 1.0f;
   int k = 0;
   for (int64_t tile = tile0; tile < ntiles; tile += tstep, ++k) {
     // issue: codes(T_{k+1}), src(T_{k+2}), ip(T_{k+3})
@@ -903,6 +945,37 @@ k_vq_mean8_lane(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
       if (v >= live) break;
       const int a = s_ip[vl] - e0;
       const int cnt = s_ip[vl + 1] - e0 - a;
+      if constexpr (F16) {
+        if (staged && cnt <= 8) {  // the common case: one HADD2 chunk, no fp32 pass
+          uint32_t h[W / 2];
+#pragma unroll
+          for (int j = 0; j < W / 2; ++j) h[j] = 0u;
+          if (cnt) lane_f16_chunk<W>(s_codes + a * 32 + lane, cnt, lbase, h);
+          if (active) {
+            const float inv = (cnt ? __fdividef(1.0f, (float)cnt) : 0.0f) * pscale;
+            uint32_t wv[W / 2];
+#pragma unroll
+            for (int j = 0; j < W / 2; ++j) {
+              const u64 f = h2_to_f32x2(h[j]);
+              const __nv_bfloat162 b2 = __floats2bfloat162_rn(lo2(f) * inv, hi2(f) * inv);
+              wv[j] = *reinterpret_cast<const uint32_t*>(&b2);
+            }
+            __nv_bfloat16* o = out + v * ld + col0;
+            if (full_part && vec_ok) {
+              if constexpr (W == 8)
+                *reinterpret_cast<uint4*>(o) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+              else
+                *reinterpret_cast<uint2*>(o) = make_uint2(wv[0], wv[1]);
+            } else {
+#pragma unroll
+              for (int j = 0; j < W; ++j)
+                if (col0 + j < d)
+                  o[j] = __ushort_as_bfloat16((unsigned short)(wv[j / 2] >> (16 * (j & 1))));
+            }
+          }
+          continue;
+        }
+      }
       u64 acc[W / 2];
 #pragma unroll
       for (int j = 0; j < W / 2; ++j) acc[j] = 0ull;
@@ -966,8 +1039,7 @@ k_vq_mean8_lane(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
         }
       }
       if (active) {
-        const float inv = (WT ? 1.0f : (cnt ? 1.0f / (float)cnt : 0.0f)) *
-                          (F16 ? __ldg(part_scale + slice * 32 + lane) : 1.0f);
+        const float inv = (WT ? 1.0f : (cnt ? 1.0f / (float)cnt : 0.0f)) * pscale;
         __nv_bfloat16* o = out + v * ld + col0;
         if (full_part) {
           store_scaled<W>(o, acc, inv, vec_ok);
@@ -1471,11 +1543,11 @@ int launch_vq_w(const fg_codec_desc* c, const int32_t* indptr, const int32_t* sr
   const bool lp = std::is_same<OT, __nv_bfloat16>::value && c->table_lp != nullptr && W >= 4;
   if constexpr (std::is_same<OT, __nv_bfloat16>::value && (W == 4 || W == 8)) {
     // lane-per-part kernel (v5): sector slices of 32 parts, one CTA per SM.
-    // Default for codebooks the v4 kernel below must part-slice (bf16 table
-    // over 70 KB, e.g. MAG240M-shape, 96 parts), in its fp16 form (scaled
-    // table_h, HADD2 chunks): measured 116 us vs 125 us for v4 there; with
-    // the bf16 table it was issue-bound (73 %) and tied v4.  Products-shape
-    // (unsliced, 25 parts) stays on v4 (36.9 vs 45.4 us).
+    // Default whenever the fp16 copy of the codebook exists (scaled table_h,
+    // HADD2 chunks) -- with the unpredicated C-pick bodies (lane_f16_body):
+    // MAG240M-shape 125 (v4) -> 116.6 -> 76.9 us, products-shape 36.9 (v4)
+    // -> 33.8 us.  With the bf16 table it was issue-bound (73 %) and tied v4,
+    // so codecs without table_h stay on v4.
     // FG_VQ_LANE = 0 (off) | 1 (bf16 table) | 2 (fp16 table) forces a mode.
     static const int lane_force = [] {
       const char* e = getenv("FG_VQ_LANE");
@@ -1484,8 +1556,8 @@ int launch_vq_w(const fg_codec_desc* c, const int32_t* indptr, const int32_t* sr
     const int64_t v4_unsliced = (((int64_t)c->num_parts + (32 / W) - 1) / (32 / W) * (32 / W)) *
                                     c->length * W * 2 + stage_bytes;
     const bool has_h = !WT && c->table_h != nullptr && c->part_scale != nullptr;
-    const int lane_env = lane_force >= 0 ? lane_force
-                                         : (v4_unsliced > 76 * 1024 && has_h ? 2 : 0);
+    (void)v4_unsliced;
+    const int lane_env = lane_force >= 0 ? lane_force : (has_h ? 2 : 0);
     const int64_t lane_smem = (int64_t)32 * c->length * W * 2 + 2 * kSrcCap * 32 +
                               3 * kSrcCap * 4 + 4 * (kTD + 4) * 4;
     if (lp && lane_env && c->row_stride % 32 == 0 && lane_smem <= 227 * 1024) {

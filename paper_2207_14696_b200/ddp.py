@@ -18,9 +18,11 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
+from .graph import sorted_unique_ids
+
 
 def shard_ids(train_ids, rank: int, world: int) -> np.ndarray:
-    ids = np.unique(np.asarray(train_ids, dtype=np.int64))
+    ids = sorted_unique_ids(train_ids)
     return ids[rank::world]
 
 

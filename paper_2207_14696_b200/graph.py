@@ -154,6 +154,16 @@ class DeviceGraph:
         return self.row_offsets.numel() * 8 + self.col_indices.numel() * 4
 
 
+def sorted_unique_ids(a) -> np.ndarray:
+    """np.unique(a) as int64 (pipeline.py:194), with a linear-time fast path
+    for ids that are already strictly increasing (train splits usually are):
+    numpy's unique sorts (~0.5 s for 1.1 M ids on the bench host)."""
+    a = np.asarray(a, dtype=np.int64).reshape(-1)
+    if a.size < 2 or bool(np.all(a[1:] > a[:-1])):
+        return np.ascontiguousarray(a)
+    return np.unique(a)
+
+
 # ------------------------------------------------------- FMAT1 / CSRG1 files
 # graphstore.py:364-426.  Byte-identical files (formats.py); the loaders run
 # the same container validation, with CSR violations re-raised as

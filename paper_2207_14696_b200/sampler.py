@@ -27,7 +27,7 @@ import numpy as np
 from . import _native as N
 from .aggregate import AGGREGATORS
 from .errors import DataError
-from .graph import CsrGraph, DeviceGraph
+from .graph import CsrGraph, DeviceGraph, sorted_unique_ids
 
 __all__ = ["SamplerConfig", "MiniBatchSample", "BatchPlan", "sample_batches",
            "DeviceSampler", "SampledBatch", "rng_block_from_numpy"]
@@ -204,7 +204,7 @@ class DeviceSampler:
         Uploads the permutation and the post-permutation stream state;
         returns the number of batches."""
         import torch
-        ids = np.unique(np.asarray(train_ids, dtype=np.int64))
+        ids = sorted_unique_ids(train_ids)
         if ids.size == 0:
             raise DataError("train_ids must be non-empty")
         if ids.min() < 0 or ids.max() >= self.g.n:
@@ -357,7 +357,7 @@ class DeviceSampler:
 
 def sample_batches(g: CsrGraph, train_ids, cfg: SamplerConfig) -> BatchPlan:
     """pipeline.py:185-222 on the device; identical seeds/frontier/edges."""
-    ids = np.unique(np.asarray(train_ids, dtype=np.int64))  # checked before any launch
+    ids = sorted_unique_ids(train_ids)  # checked before any launch
     if ids.size == 0:
         raise DataError("train_ids must be non-empty")
     if ids.min() < 0 or ids.max() >= g.n:
