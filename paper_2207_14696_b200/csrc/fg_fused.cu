@@ -833,24 +833,39 @@ __device__ __forceinline__ void lane_f16_body(const uint8_t* cp, uint32_t lbase,
 #pragma unroll
   for (int u = 0; u < C; ++u) code[u] = cp[u * 32];
 #pragma unroll
-  for (int u = 0; u < C; ++u) {
+  for (int u = 0; u < C; ++u) {  // the first pick initialises the sums
     const uint32_t addr = lbase + code[u] * 128u;
     if constexpr (W == 8) {
       uint32_t x, y, z, w;
       asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
                    : "=r"(x), "=r"(y), "=r"(z), "=r"(w) : "r"(addr));
-      h[0] = hadd2u(h[0], x); h[1] = hadd2u(h[1], y);
-      h[2] = hadd2u(h[2], z); h[3] = hadd2u(h[3], w);
+      if (u == 0) {
+        h[0] = x; h[1] = y; h[2] = z; h[3] = w;
+      } else {
+        h[0] = hadd2u(h[0], x); h[1] = hadd2u(h[1], y);
+        h[2] = hadd2u(h[2], z); h[3] = hadd2u(h[3], w);
+      }
     } else {
       uint32_t x, y;
       asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(x), "=r"(y) : "r"(addr));
-      h[0] = hadd2u(h[0], x); h[1] = hadd2u(h[1], y);
+      if (u == 0) {
+        h[0] = x; h[1] = y;
+      } else {
+        h[0] = hadd2u(h[0], x); h[1] = hadd2u(h[1], y);
+      }
     }
   }
 }
+// 1/cnt for the <= 8-pick fast path (cnt = 0 -> 0)
+__constant__ float kInvCnt[9] = {0.f, 1.f, 1.f / 2, 1.f / 3, 1.f / 4, 1.f / 5, 1.f / 6, 1.f / 7,
+                                 1.f / 8};
 template <int W>
 __device__ __forceinline__ void lane_f16_chunk(const uint8_t* cp, int cb, uint32_t lbase,
                                                uint32_t* h) {
+  if (cb == 5) {  // the fanout-5 input layer of every BASELINE config: one compare
+    lane_f16_body<5, W>(cp, lbase, h);
+    return;
+  }
   switch (cb) {
     case 1: lane_f16_body<1, W>(cp, lbase, h); break;
     case 2: lane_f16_body<2, W>(cp, lbase, h); break;
@@ -952,7 +967,7 @@ k_vq_mean8_lane(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
           for (int j = 0; j < W / 2; ++j) h[j] = 0u;
           if (cnt) lane_f16_chunk<W>(s_codes + a * 32 + lane, cnt, lbase, h);
           if (active) {
-            const float inv = (cnt ? __fdividef(1.0f, (float)cnt) : 0.0f) * pscale;
+            const float inv = kInvCnt[cnt] * pscale;
             uint32_t wv[W / 2];
 #pragma unroll
             for (int j = 0; j < W / 2; ++j) {

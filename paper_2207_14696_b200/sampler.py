@@ -203,7 +203,10 @@ class DeviceSampler:
         """unique -> default_rng(seed) -> permutation (pipeline.py:194-200).
         Uploads the permutation and the post-permutation stream state;
         returns the number of batches."""
+        import time
+
         import torch
+        t0 = time.perf_counter()
         ids = sorted_unique_ids(train_ids)
         if ids.size == 0:
             raise DataError("train_ids must be non-empty")
@@ -213,7 +216,9 @@ class DeviceSampler:
         self._inc = int(state["state"]["inc"])
         blk = rng_block_from_numpy(state)
         perm = np.ascontiguousarray(ids)
+        t1 = time.perf_counter()
         N.call("fg_rng_permutation_host", blk.ctypes.data, perm.ctypes.data, perm.size)
+        t2 = time.perf_counter()
         # each batch's seeds are np.sort(perm[lo:lo + bs]) (pipeline.py:203):
         # sort the slices once here, so a batch's seeds are one copy into the
         # sorted seed layer (no sort kernel in the sampling chain)
@@ -222,8 +227,13 @@ class DeviceSampler:
             perm[:full * self.bs].reshape(full, self.bs).sort(axis=1)
         perm[full * self.bs:].sort()
         self.perm_host = perm
+        t3 = time.perf_counter()
         self.perm = torch.from_numpy(perm.astype(np.int32)).to(self.device)
         self.rng.copy_(torch.from_numpy(blk.view(np.int64)))
+        # host-side cost breakdown of the last begin_epoch (bench.py reports it)
+        self.begin_epoch_timing = {"unique_s": t1 - t0, "permutation_s": t2 - t1,
+                                   "batch_sort_s": t3 - t2,
+                                   "upload_s": time.perf_counter() - t3}
         return (perm.size + self.bs - 1) // self.bs
 
     def set_stream_state(self, state: dict) -> None:
