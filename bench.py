@@ -358,7 +358,9 @@ def run_ours(args, rank, world, local):
         epoch = {"seeds_per_s": round(nb1 * bs * world / ep_s, 1), "wall_s": round(ep_s, 4),
                  "begin_epoch_s": round(t1 - t0, 4), "enqueue_s": round(t2 - t1, 4),
                  "begin_epoch_parts_s": {k: round(v, 4) for k, v in
-                                         getattr(tr.sampler, "begin_epoch_timing", {}).items()},
+                                         {**getattr(tr, "begin_epoch_timing", {}),
+                                          **getattr(tr.sampler, "begin_epoch_timing",
+                                                    {})}.items()},
                  "batches_per_rank": nb1, "includes": "begin_epoch (host permutation + "
                  "upload) + every batch of the epoch, wall clock, max over ranks"}
     # ---- roofline: the fused gather-dequant-mean kernel, timed alone

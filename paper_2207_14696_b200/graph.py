@@ -160,7 +160,7 @@ def sorted_unique_ids(a) -> np.ndarray:
     numpy's unique sorts (~0.5 s for 1.1 M ids on the bench host)."""
     a = np.asarray(a, dtype=np.int64).reshape(-1)
     if a.size < 2 or bool(np.all(a[1:] > a[:-1])):
-        return np.ascontiguousarray(a)
+        return a.copy()  # always a fresh array, like np.unique (callers permute it)
     return np.unique(a)
 
 

@@ -397,12 +397,18 @@ class SageTrainer:
     def begin_epoch(self, train_ids, epoch: int = 0) -> int:
         """Seeds are sharded like DDP: rank r takes ids[r::W] with seed
         seed*W + r + epoch."""
+        import time
+        t0 = time.perf_counter()
         r = torch.distributed.get_rank(self.pg) if self.world > 1 else 0
         shard = ddp.shard_ids(train_ids, r, self.world)
+        t1 = time.perf_counter()
         self._nb = self.sampler.begin_epoch(shard, ddp.rank_seed(self.cfg.seed, epoch, r,
                                                                  self.world))
+        t2 = time.perf_counter()
         self._nb = ddp.agree_num_batches(self._nb, self.pg, self.device)
         self._primed, self._next = False, 0
+        self.begin_epoch_timing = {"shard_s": t1 - t0, "sampler_s": t2 - t1,
+                                   "agree_s": time.perf_counter() - t2}
         return self._nb
 
     def prepare(self, b: int, seeds_host: torch.Tensor | None = None) -> None:

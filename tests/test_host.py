@@ -320,3 +320,14 @@ def test_measured_report_semantics_follow_the_reference():
         compare_reports(a, [SimReport("y", 1, 0, 0, 0, 1, 0, 1.0, 0, 1.0, dict(wl, seed=1))])
     with pytest.raises(DataError):
         SimReport.from_dict({"label": "z"})
+
+
+def test_sorted_unique_ids_never_aliases_the_input():
+    """The fast path (already strictly increasing ids) must copy: the sampler
+    permutes the returned array in place (fg_rng_permutation_host)."""
+    from paper_2207_14696_b200.graph import sorted_unique_ids
+    a = np.arange(10, dtype=np.int64)
+    out = sorted_unique_ids(a)
+    out[:] = 0
+    assert np.array_equal(a, np.arange(10))
+    assert np.array_equal(sorted_unique_ids(np.array([5, 3, 3, 9])), [3, 5, 9])
