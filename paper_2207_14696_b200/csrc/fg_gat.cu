@@ -320,11 +320,14 @@ struct GatCodes {
   const float* table;   // SQ LUT / VQ fp32 codebooks [P][L][W]
   const int32_t* picks; // source node of each pick (unused for kind 0)
 };
+template <int KIND = -1>
 __device__ __forceinline__ const uint8_t* gat_row(const GatCodes& c, int64_t e) {
-  return c.kind == 0 ? c.rows + e * c.stride : c.rows + (int64_t)__ldg(c.picks + e) * c.stride;
+  return (KIND == 0 || c.kind == 0) ? c.rows + e * c.stride
+                                    : c.rows + (int64_t)__ldg(c.picks + e) * c.stride;
 }
+template <int KIND = -1>  // 0: decoded bf16 rows (compile-time), -1: runtime kind
 __device__ __forceinline__ float gat_elem(const GatCodes& c, const uint8_t* row, int j) {
-  if (c.kind == 0) {
+  if (KIND == 0 || c.kind == 0) {
     const uint16_t h = reinterpret_cast<const uint16_t*>(row)[j];
     return __uint_as_float((uint32_t)h << 16);
   }
@@ -414,7 +417,7 @@ __global__ void k_gat_code_scores_bwd(GatCodes cd, int d, int heads,
 // count zero): warp per destination, lane owns columns j = lane + 32 i
 // (i < kXI, d <= 32 kXI), edges outer (each alpha and x element read once)
 constexpr int kXI = 8;  // d <= 256
-template <int HEADS, int XI>
+template <int HEADS, int XI, int KIND>
 __global__ void __launch_bounds__(256)
 k_gat_code_xagg_fwd(GatCodes cd, int d, const float* __restrict__ alpha,
                     const int32_t* __restrict__ indptr, int64_t max_dst,
@@ -432,7 +435,7 @@ k_gat_code_xagg_fwd(GatCodes cd, int d, const float* __restrict__ alpha,
 #pragma unroll
       for (int k = 0; k < HEADS; ++k) acc[i][k] = 0.f;
     for (int32_t e = e0; e < e1; ++e) {
-      const uint8_t* row = gat_row(cd, e);
+      const uint8_t* row = gat_row<KIND>(cd, e);
       float al[HEADS];
 #pragma unroll
       for (int k = 0; k < HEADS; ++k)
@@ -441,7 +444,7 @@ k_gat_code_xagg_fwd(GatCodes cd, int d, const float* __restrict__ alpha,
       for (int i = 0; i < XI; ++i) {
         const int j = lane + 32 * i;
         if (j < d) {
-          const float xv = gat_elem(cd, row, j);
+          const float xv = gat_elem<KIND>(cd, row, j);
 #pragma unroll
           for (int k = 0; k < HEADS; ++k)
             acc[i][k] = fmaf(al[k], xv, acc[i][k]);
@@ -462,7 +465,7 @@ k_gat_code_xagg_fwd(GatCodes cd, int d, const float* __restrict__ alpha,
 // held in registers; B = 32/H edges at a time give 32 partial dots per lane,
 // reduced across the warp by one 31-shuffle transpose-reduce (lane L ends
 // with edge L/H, head L%H), then one coalesced 32-float store
-template <int HEADS, int XI>
+template <int HEADS, int XI, int KIND>
 __global__ void __launch_bounds__(256)
 k_gat_code_xagg_bwd(GatCodes cd, int d, const int32_t* __restrict__ indptr,
                     int64_t max_dst, const int64_t* __restrict__ ndst_dev,
@@ -489,12 +492,12 @@ k_gat_code_xagg_bwd(GatCodes cd, int d, const int32_t* __restrict__ indptr,
 #pragma unroll
       for (int b = 0; b < B; ++b) {
         if (eb + b < e1) {
-          const uint8_t* row = gat_row(cd, eb + b);
+          const uint8_t* row = gat_row<KIND>(cd, eb + b);
 #pragma unroll
           for (int i = 0; i < XI; ++i) {
             const int j = lane + 32 * i;
             if (j < d) {
-              const float xv = gat_elem(cd, row, j);
+              const float xv = gat_elem<KIND>(cd, row, j);
 #pragma unroll
               for (int k = 0; k < HEADS; ++k)
                 pv[b * HEADS + k] = fmaf(gk[i][k], xv, pv[b * HEADS + k]);
@@ -623,9 +626,15 @@ extern "C" int fg_gat_code_xagg_fwd(const fg_codec_desc* codec, const uint16_t* 
   auto* ob = reinterpret_cast<__nv_bfloat16*>(out);
   const dim3 grid(grid_for(max_dst * 32, 256));
   cudaStream_t st = as_stream(s);
-#define FG_XAGG_FWD(H, XI) \
-  fg::k_gat_code_xagg_fwd<H, XI><<<grid, 256, 0, st>>>(g, (int)d, alpha, indptr, max_dst, \
-                                                        n_dst_dev, ob)
+#define FG_XAGG_FWD(H, XI)                                                                \
+  do {                                                                                    \
+    if (g.kind == 0)                                                                      \
+      fg::k_gat_code_xagg_fwd<H, XI, 0><<<grid, 256, 0, st>>>(g, (int)d, alpha, indptr,   \
+                                                              max_dst, n_dst_dev, ob);    \
+    else                                                                                  \
+      fg::k_gat_code_xagg_fwd<H, XI, -1><<<grid, 256, 0, st>>>(g, (int)d, alpha, indptr,  \
+                                                               max_dst, n_dst_dev, ob);   \
+  } while (0)
   const bool small = d <= 128;
   switch (heads) {
     case 1: if (small) FG_XAGG_FWD(1, 4); else FG_XAGG_FWD(1, 8); break;
@@ -652,9 +661,15 @@ extern "C" int fg_gat_code_xagg_bwd(const fg_codec_desc* codec, const uint16_t* 
   const auto* dAb = reinterpret_cast<const __nv_bfloat16*>(dA);
   const dim3 grid(grid_for(max_dst * 32, 256));
   cudaStream_t st = as_stream(s);
-#define FG_XAGG_BWD(H, XI) \
-  fg::k_gat_code_xagg_bwd<H, XI><<<grid, 256, 0, st>>>(g, (int)d, indptr, max_dst, n_dst_dev, \
-                                                        dAb, dalpha)
+#define FG_XAGG_BWD(H, XI)                                                                \
+  do {                                                                                    \
+    if (g.kind == 0)                                                                      \
+      fg::k_gat_code_xagg_bwd<H, XI, 0><<<grid, 256, 0, st>>>(g, (int)d, indptr, max_dst,  \
+                                                              n_dst_dev, dAb, dalpha);    \
+    else                                                                                  \
+      fg::k_gat_code_xagg_bwd<H, XI, -1><<<grid, 256, 0, st>>>(g, (int)d, indptr, max_dst, \
+                                                               n_dst_dev, dAb, dalpha);   \
+  } while (0)
   const bool small = d <= 128;
   switch (heads) {
     case 1: if (small) FG_XAGG_BWD(1, 4); else FG_XAGG_BWD(1, 8); break;

@@ -119,13 +119,15 @@ def test_gat_graphed_training_learns():
     assert t.evaluate(val) > 0.3
 
 
-@pytest.mark.parametrize("codec_kind", ["sq8", "sq4", "vq"])
-def test_gat_gradients_match_cpu_oracle_model(codec_kind):
+@pytest.mark.parametrize("codec_kind,decoded", [("sq8", True), ("sq4", True), ("vq", True),
+                                                ("sq8", False), ("sq4", False), ("vq", False)])
+def test_gat_gradients_match_cpu_oracle_model(codec_kind, decoded):
     """One batch, same weights: the GPU GAT (input layer straight from the
     code rows, bf16 autocast) and the CPU fp32 oracle GAT on the oracle's
     decodes give the same loss and the same gradient for EVERY parameter --
     including layer 0's attention vectors (round 1's head projection dropped
-    dA, so they received none)."""
+    dA, so they received none) -- for both input forms: decoded bf16 pick
+    rows and the code-reading kernels (fg_gat_code_*)."""
     from paper_2207_14696_b200.gat import PickSource
     from paper_2207_14696_b200.synth import build_vq_codec
     from oracle.sampler import sample_batches_oracle
@@ -153,7 +155,9 @@ def test_gat_gradients_match_cpu_oracle_model(codec_kind):
     t.sampler.load_seeds(0)
     sb = t.sampler.sample_loaded()
     L = len(fans)
-    src = PickSource(dc, sb.picks[L - 1], sb.n_picks[L - 1], t.pick_cap)
+    # decoded=False: the input layer's kernels read the code rows directly
+    src = PickSource(dc, sb.picks[L - 1], sb.n_picks[L - 1], t.pick_cap, decoded=decoded)
+    assert (src.x is None) == (not decoded)
     with torch.autocast("cuda", dtype=torch.bfloat16):
         logits = t.model(src, sb, t.caps, t.pick_cap)
     nd = int(sb.n_nodes[0].item())
