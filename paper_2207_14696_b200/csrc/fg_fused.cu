@@ -1091,186 +1091,6 @@ k_vq_mean8_lane(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
   }
 }
 
-// --------------------------- VQ half-warp-per-destination path (8-bit, W=8, fp16)
-// v7 (round 2).  MAG240M-shape after the lane kernel's unpredicated bodies:
-// 74 us at 66 % issue, ~40 % of it per-destination bookkeeping paid once per
-// (destination, slice).  Here a warp takes TWO destinations per pass: lane l
-// serves destination 2*pass + (l >> 4) and the slice's parts 2(l & 15) and
-// 2(l & 15) + 1, so the loop / dispatch / index work is shared by two
-// destinations, a pick's two code bytes are one 2-byte load, and the lane's
-// output (2 parts x 8 bf16 = 32 B) is one full-sector 256-bit store.
-// Codebook lines are interleaved by pair half: part p lives at line
-// ((p & 1) * 2 + ((p >> 1) >> 3)) * L + e, byte ((p >> 1) & 7) * 16, so the
-// 8 lanes of a wavefront hit 8 different bank groups in both lookups.
-__device__ __forceinline__ void pair_f16_pick(const uint8_t* cp, uint32_t la, uint32_t lb,
-                                              uint32_t* ha, uint32_t* hb, bool first) {
-  const uint32_t c = *reinterpret_cast<const uint16_t*>(cp);
-  const uint32_t aa = la + (c & 0xFFu) * 128u, ab = lb + (c >> 8) * 128u;
-  uint32_t x0, x1, x2, x3, y0, y1, y2, y3;
-  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(x0), "=r"(x1), "=r"(x2), "=r"(x3) : "r"(aa));
-  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(y0), "=r"(y1), "=r"(y2), "=r"(y3) : "r"(ab));
-  if (first) {
-    ha[0] = x0; ha[1] = x1; ha[2] = x2; ha[3] = x3;
-    hb[0] = y0; hb[1] = y1; hb[2] = y2; hb[3] = y3;
-  } else {
-    ha[0] = hadd2u(ha[0], x0); ha[1] = hadd2u(ha[1], x1);
-    ha[2] = hadd2u(ha[2], x2); ha[3] = hadd2u(ha[3], x3);
-    hb[0] = hadd2u(hb[0], y0); hb[1] = hadd2u(hb[1], y1);
-    hb[2] = hadd2u(hb[2], y2); hb[3] = hadd2u(hb[3], y3);
-  }
-}
-
-__global__ void __launch_bounds__(kLaneThreads, 1)
-k_vq_mean8_pair(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
-                const __nv_bfloat16* __restrict__ books, int length, int parts,
-                const int32_t* __restrict__ indptr, const int32_t* __restrict__ src,
-                const int64_t* __restrict__ ndst_dev, int64_t max_dst,
-                __nv_bfloat16* __restrict__ out, int64_t ld, int nslices,
-                const float* __restrict__ part_scale) {
-  constexpr int W = 8;
-  extern __shared__ __align__(128) uint8_t s_raw[];
-  const int slice = (int)(blockIdx.x % nslices);
-  const int64_t live = live_dst(ndst_dev, max_dst);
-  const int64_t ntiles = (live + kTD - 1) / kTD;
-  const int64_t tile0 = blockIdx.x / nslices, tstep = gridDim.x / nslices;
-  if (tile0 >= ntiles) return;
-  const int lparts = min(32, parts - slice * 32);
-  uint8_t* const s_book = s_raw;                                   // 4 groups x L lines
-  uint8_t* const s_codes0 = s_book + (size_t)4 * length * 128;
-  int32_t* const s_src0 = reinterpret_cast<int32_t*>(s_codes0 + 2 * kSrcCap * 32);
-  int32_t* const s_ip0 = s_src0 + 3 * kSrcCap;
-  auto IP = [&](int i) { return s_ip0 + i * (kTD + 4); };
-  auto SRC = [&](int i) { return s_src0 + i * kSrcCap; };
-  auto CODES = [&](int i) { return s_codes0 + i * (kSrcCap * 32); };
-  {
-    const int nent = lparts * length;
-    const __nv_bfloat16* g = books + (int64_t)slice * 32 * length * W;
-    for (int c = threadIdx.x; c < nent; c += blockDim.x) {
-      const int lp = c / length, e = c - lp * length;
-      uint8_t* dst = s_book + ((size_t)((lp & 1) * 2 + ((lp >> 1) >> 3)) * length + e) * 128 +
-                     ((lp >> 1) & 7) * 16;
-      cp_async16(dst, g + (int64_t)c * W);
-    }
-  }
-  const int sector_off = slice * 32;
-  lane_issue_ip(IP(0), indptr, tile0, max_dst);
-  cp_commit();
-  cp_wait_all();
-  __syncthreads();
-  lane_issue_src(SRC(0), IP(0), src);
-  if (tile0 + tstep < ntiles) lane_issue_ip(IP(1), indptr, tile0 + tstep, max_dst);
-  cp_commit();
-  cp_wait_all();
-  __syncthreads();
-  lane_issue_codes(CODES(0), IP(0), SRC(0), rows, stride, sector_off);
-  if (tile0 + tstep < ntiles) lane_issue_src(SRC(1), IP(1), src);
-  if (tile0 + 2 * tstep < ntiles) lane_issue_ip(IP(2), indptr, tile0 + 2 * tstep, max_dst);
-  cp_commit();
-  cp_wait_all();
-  __syncthreads();
-
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int half = lane >> 4, pl = lane & 15;
-  const int pa = 2 * pl, pb = 2 * pl + 1;  // slice-local parts of this lane
-  const bool act_a = pa < lparts, act_b = pb < lparts;
-  const uint32_t sb = smem_addr(s_book);
-  const uint32_t la = sb + (uint32_t)((0 * 2 + (pl >> 3)) * length * 128 + (pl & 7) * 16);
-  const uint32_t lb = sb + (uint32_t)((1 * 2 + (pl >> 3)) * length * 128 + (pl & 7) * 16);
-  const int64_t col0 = (int64_t)(slice * 32 + pa) * W;
-  const bool full = col0 + 2 * W <= d;
-  const bool vec_ok = (ld % 16) == 0;  // 32-B aligned row segments
-  const float sa = act_a ? __ldg(part_scale + slice * 32 + pa) : 0.f;
-  const float sbs = act_b ? __ldg(part_scale + slice * 32 + pb) : 0.f;
-  int k = 0;
-  for (int64_t tile = tile0; tile < ntiles; tile += tstep, ++k) {
-    const int64_t t1 = tile + tstep, t2 = tile + 2 * tstep, t3 = tile + 3 * tstep;
-    if (t1 < ntiles)
-      lane_issue_codes(CODES((k + 1) & 1), IP((k + 1) & 3), SRC((k + 1) % 3), rows, stride,
-                       sector_off);
-    if (t2 < ntiles) lane_issue_src(SRC((k + 2) % 3), IP((k + 2) & 3), src);
-    if (t3 < ntiles) lane_issue_ip(IP((k + 3) & 3), indptr, t3, max_dst);
-    cp_commit();
-    const int32_t* s_ip = IP(k & 3);
-    const uint8_t* s_codes = CODES(k & 1);
-    const int32_t e0 = s_ip[0];
-    const bool staged = s_ip[kTD] - e0 <= kSrcCap;
-    for (int vp = warp; 2 * vp < kTD; vp += kLaneWarps) {
-      const int vl = 2 * vp + half;
-      const int64_t v = tile * kTD + vl;
-      const bool valid = v < live;
-      if (!__any_sync(0xFFFFFFFFu, valid)) break;
-      const int a = valid ? s_ip[vl] - e0 : 0;
-      const int cnt = valid ? s_ip[vl + 1] - e0 - a : 0;
-      uint32_t ha[4] = {0u, 0u, 0u, 0u}, hb[4] = {0u, 0u, 0u, 0u};
-      u64 fa[4] = {0ull, 0ull, 0ull, 0ull}, fb[4] = {0ull, 0ull, 0ull, 0ull};
-      bool wide = false;  // sums in fa/fb (fp32) instead of ha/hb
-      if (staged && __all_sync(0xFFFFFFFFu, cnt == 5)) {  // both halves: 5 picks
-        const uint8_t* cp = s_codes + a * 32 + 2 * pl;
-#pragma unroll
-        for (int u = 0; u < 5; ++u) pair_f16_pick(cp + u * 32, la, lb, ha, hb, u == 0);
-      } else {  // general: per-lane pick loop, fp16 chunks of <= 8 widened to fp32
-        wide = true;
-        for (int u0 = 0; u0 < cnt; u0 += 8) {
-          const int cb = min(cnt - u0, 8);
-          for (int u = 0; u < cb; ++u) {
-            const int e = a + u0 + u;
-            uint32_t c;
-            if (staged) {
-              c = *reinterpret_cast<const uint16_t*>(s_codes + e * 32 + 2 * pl);
-            } else {
-              const uint8_t* rp = rows + (int64_t)__ldg(src + e0 + e) * stride + sector_off + 2 * pl;
-              c = (uint32_t)__ldg(rp) | ((uint32_t)__ldg(rp + 1) << 8);
-            }
-            uint32_t x[4], y[4];
-            const uint32_t aa = la + (c & 0xFFu) * 128u, ab = lb + (c >> 8) * 128u;
-            asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
-                         : "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3]) : "r"(aa));
-            asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
-                         : "=r"(y[0]), "=r"(y[1]), "=r"(y[2]), "=r"(y[3]) : "r"(ab));
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              ha[j] = u == 0 ? x[j] : hadd2u(ha[j], x[j]);
-              hb[j] = u == 0 ? y[j] : hadd2u(hb[j], y[j]);
-            }
-          }
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            fa[j] = fadd2(fa[j], cb ? h2_to_f32x2(ha[j]) : 0ull);
-            fb[j] = fadd2(fb[j], cb ? h2_to_f32x2(hb[j]) : 0ull);
-          }
-        }
-      }
-      if (valid && act_a) {
-        const float inv = cnt ? (cnt <= 8 ? kInvCnt[cnt] : 1.0f / (float)cnt) : 0.0f;
-        const float ia = inv * sa, ib = inv * sbs;
-        uint32_t w[8];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const u64 xa = wide ? fa[j] : h2_to_f32x2(ha[j]);
-          const u64 xb = wide ? fb[j] : h2_to_f32x2(hb[j]);
-          const __nv_bfloat162 b0 = __floats2bfloat162_rn(lo2(xa) * ia, hi2(xa) * ia);
-          const __nv_bfloat162 b1 = __floats2bfloat162_rn(lo2(xb) * ib, hi2(xb) * ib);
-          w[j] = *reinterpret_cast<const uint32_t*>(&b0);
-          w[4 + j] = *reinterpret_cast<const uint32_t*>(&b1);
-        }
-        __nv_bfloat16* o = out + v * ld + col0;
-        if (full && act_b && vec_ok && aligned32(o)) {
-          stg256(o, w);
-        } else {
-#pragma unroll
-          for (int j = 0; j < 2 * W; ++j)
-            if (col0 + j < d && (j < W || act_b))
-              o[j] = __ushort_as_bfloat16((unsigned short)(w[j / 2] >> (16 * (j & 1))));
-        }
-      }
-    }
-    cp_wait_all();
-    __syncthreads();
-  }
-}
-
 // ------------------------------------------------- VQ (any code width)
 template <int W, typename OT>
 __global__ void __launch_bounds__(kThreads, 2)
@@ -1777,24 +1597,6 @@ int launch_vq_w(const fg_codec_desc* c, const int32_t* indptr, const int32_t* sr
                               3 * kSrcCap * 4 + 4 * (kTD + 4) * 4;
     if (lp && lane_env && c->row_stride % 32 == 0 && lane_smem <= 227 * 1024) {
       const int ns = (int)ceil_div(c->num_parts, 32);
-      if constexpr (W == 8 && !WT) {
-        static const int pair_env = [] {  // FG_VQ_PAIR=0: the one-destination lane kernel
-          const char* e = getenv("FG_VQ_PAIR");
-          return e ? atoi(e) : 1;
-        }();
-        if (pair_env && lane_env == 2 && has_h) {
-          FG_CUDA_TRY(cudaFuncSetAttribute(k_vq_mean8_pair,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)lane_smem));
-          const int64_t per_slice = std::max<int64_t>(1, min64(ntiles, sm_count() / ns));
-          k_vq_mean8_pair<<<(int)(per_slice * ns), kLaneThreads, lane_smem, st>>>(
-              c->rows, c->d, c->row_stride, (const __nv_bfloat16*)c->table_h, c->length,
-              c->num_parts, indptr, src, ndst, max_dst, (__nv_bfloat16*)out, ld, ns,
-              c->part_scale);
-          FG_LAUNCH_CHECK();
-          return FG_OK;
-        }
-      }
       const bool f16 = !WT && c->table_h != nullptr && c->part_scale != nullptr && lane_env == 2;
       auto kern = f16 ? k_vq_mean8_lane<W, false, true> : k_vq_mean8_lane<W, WT, false>;
       FG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
