@@ -1091,6 +1091,232 @@ k_vq_mean8_lane(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
   }
 }
 
+// ------------------------------------ SQ lane-per-byte-group path (k in {4, 8}, bf16)
+// Round 2, the lane kernel's structure for SQ rows whose code bytes are a
+// multiple of 32 (papers100M-shape k=4 d=128: 64 B; arxiv-shape k=8 d=128:
+// 128 B): a warp takes one destination at a time, lane l owns code bytes
+// [l*NB, l*NB + NB) and the 8*NB/k outputs they decode to; whole code rows
+// are staged one tile ahead by per-thread 16-byte cp.async (no TMA unit in
+// the row path), the decode table is replicated per lane (k=4: decoded byte
+// PAIRS, 8 B; k=8: 4 B: conflict-free), pick counts up to 8 run unpredicated
+// bodies, and the destination's row is one coalesced store.
+template <int RB>
+__device__ __forceinline__ void sq_lane_issue_rows(uint8_t* dst, const int32_t* s_ip,
+                                                   const int32_t* s_src,
+                                                   const uint8_t* __restrict__ rows,
+                                                   int64_t stride, int cap) {
+  constexpr int CH = RB / 16;
+  const int32_t cnt = s_ip[kTD] - s_ip[0];
+  if (cnt > cap) return;
+  for (int t = threadIdx.x; t < CH * cnt; t += blockDim.x) {
+    const int e = t / CH, h = t - e * CH;
+    cp_async16(dst + e * RB + h * 16, rows + (int64_t)s_src[e] * stride + h * 16);
+  }
+}
+
+template <int K, int NB, int C>
+__device__ __forceinline__ void sq_lane_body(const uint8_t* cp, uint32_t tb, u64* acc) {
+  constexpr int RB = 32 * NB;
+  uint32_t cw[C];
+#pragma unroll
+  for (int u = 0; u < C; ++u) {
+    if constexpr (NB == 4) cw[u] = *reinterpret_cast<const uint32_t*>(cp + u * RB);
+    else if constexpr (NB == 2) cw[u] = *reinterpret_cast<const uint16_t*>(cp + u * RB);
+    else cw[u] = cp[u * RB];
+  }
+#pragma unroll
+  for (int u = 0; u < C; ++u) {
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const uint32_t byte = (cw[u] >> (8 * b)) & 0xFFu;
+      if constexpr (K == 4) {
+        uint32_t x, y;
+        asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(x), "=r"(y) : "r"(tb + byte * 256u));
+        acc[b] = fadd2(acc[b], ((u64)y << 32) | x);
+      } else if (b % 2 == 0) {
+        const uint32_t b1 = (cw[u] >> (8 * (b + 1))) & 0xFFu;
+        float f0, f1;
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(f0) : "r"(tb + byte * 128u));
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(f1) : "r"(tb + b1 * 128u));
+        acc[b / 2] = fadd2(acc[b / 2], pack2(f0, f1));
+      }
+    }
+  }
+}
+
+template <int K, int NB>
+__global__ void __launch_bounds__(kLaneThreads, 1)
+k_sq_mean_lane(const uint8_t* __restrict__ rows, int64_t stride, const float* __restrict__ lut,
+               const int32_t* __restrict__ indptr, const int32_t* __restrict__ src,
+               const int64_t* __restrict__ ndst_dev, int64_t max_dst,
+               __nv_bfloat16* __restrict__ out, int64_t ld, int cap) {
+  constexpr int RB = 32 * NB;        // code bytes per row
+  constexpr int EPL = 8 * NB / K;    // outputs per lane
+  constexpr int NA = EPL / 2;
+  constexpr bool PAIR = K == 4;
+  constexpr int LUTB = PAIR ? 256 * 32 * 8 : 256 * 32 * 4;
+  extern __shared__ __align__(128) uint8_t s_raw[];
+  const int64_t live = live_dst(ndst_dev, max_dst);
+  const int64_t ntiles = (live + kTD - 1) / kTD;
+  const int64_t tile0 = blockIdx.x, tstep = gridDim.x;
+  if (tile0 >= ntiles) return;
+  uint8_t* const s_lut = s_raw;
+  uint8_t* const s_rows0 = s_raw + LUTB;                                  // [2][cap][RB]
+  int32_t* const s_src0 = reinterpret_cast<int32_t*>(s_rows0 + 2 * (size_t)cap * RB);  // [3][cap]
+  int32_t* const s_ip0 = s_src0 + 3 * cap;                                // [4][kTD + 4]
+  auto IP = [&](int i) { return s_ip0 + i * (kTD + 4); };
+  auto SRC = [&](int i) { return s_src0 + i * cap; };
+  auto ROWS = [&](int i) { return s_rows0 + (size_t)i * cap * RB; };
+  if constexpr (PAIR) {
+    u64* t2 = reinterpret_cast<u64*>(s_lut);
+    for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) {
+      const int pv = i >> 5;
+      t2[i] = pack2(__ldg(lut + (pv >> 4)), __ldg(lut + (pv & 15)));
+    }
+  } else {
+    float* t1 = reinterpret_cast<float*>(s_lut);
+    for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) t1[i] = __ldg(lut + (i >> 5));
+  }
+  auto issue_src = [&](int32_t* dst, const int32_t* ip) {
+    const int32_t e0 = ip[0], c = ip[kTD] - e0;
+    if (c > cap) return;
+    for (int t = threadIdx.x; t < c; t += blockDim.x) cp_async4(dst + t, src + e0 + t);
+  };
+  lane_issue_ip(IP(0), indptr, tile0, max_dst);
+  cp_commit();
+  cp_wait_all();
+  __syncthreads();
+  issue_src(SRC(0), IP(0));
+  if (tile0 + tstep < ntiles) lane_issue_ip(IP(1), indptr, tile0 + tstep, max_dst);
+  cp_commit();
+  cp_wait_all();
+  __syncthreads();
+  sq_lane_issue_rows<RB>(ROWS(0), IP(0), SRC(0), rows, stride, cap);
+  if (tile0 + tstep < ntiles) issue_src(SRC(1), IP(1));
+  if (tile0 + 2 * tstep < ntiles) lane_issue_ip(IP(2), indptr, tile0 + 2 * tstep, max_dst);
+  cp_commit();
+  cp_wait_all();
+  __syncthreads();
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t tb = smem_addr(s_lut) + (uint32_t)lane * (PAIR ? 8u : 4u);
+  const bool vec_ok = (ld % 4) == 0;
+  int k = 0;
+  for (int64_t tile = tile0; tile < ntiles; tile += tstep, ++k) {
+    const int64_t t1 = tile + tstep, t2 = tile + 2 * tstep, t3 = tile + 3 * tstep;
+    if (t1 < ntiles) sq_lane_issue_rows<RB>(ROWS((k + 1) & 1), IP((k + 1) & 3), SRC((k + 1) % 3),
+                                            rows, stride, cap);
+    if (t2 < ntiles) issue_src(SRC((k + 2) % 3), IP((k + 2) & 3));
+    if (t3 < ntiles) lane_issue_ip(IP((k + 3) & 3), indptr, t3, max_dst);
+    cp_commit();
+    const int32_t* s_ip = IP(k & 3);
+    const uint8_t* s_rw = ROWS(k & 1);
+    const int32_t e0 = s_ip[0];
+    const bool staged = s_ip[kTD] - e0 <= cap;
+    for (int vl = warp; vl < kTD; vl += kLaneWarps) {
+      const int64_t v = tile * kTD + vl;
+      if (v >= live) break;
+      const int a = s_ip[vl] - e0;
+      const int cnt = s_ip[vl + 1] - e0 - a;
+      u64 acc[NA];
+#pragma unroll
+      for (int j = 0; j < NA; ++j) acc[j] = 0ull;
+      if (staged) {
+        const uint8_t* cp = s_rw + (size_t)a * RB + lane * NB;
+        int u0 = 0;
+        for (; u0 + 8 <= cnt; u0 += 8) sq_lane_body<K, NB, 8>(cp + (size_t)u0 * RB, tb, acc);
+        switch (cnt - u0) {
+          case 1: sq_lane_body<K, NB, 1>(cp + (size_t)u0 * RB, tb, acc); break;
+          case 2: sq_lane_body<K, NB, 2>(cp + (size_t)u0 * RB, tb, acc); break;
+          case 3: sq_lane_body<K, NB, 3>(cp + (size_t)u0 * RB, tb, acc); break;
+          case 4: sq_lane_body<K, NB, 4>(cp + (size_t)u0 * RB, tb, acc); break;
+          case 5: sq_lane_body<K, NB, 5>(cp + (size_t)u0 * RB, tb, acc); break;
+          case 6: sq_lane_body<K, NB, 6>(cp + (size_t)u0 * RB, tb, acc); break;
+          case 7: sq_lane_body<K, NB, 7>(cp + (size_t)u0 * RB, tb, acc); break;
+          default: break;
+        }
+      } else {  // tile larger than the staging buffer: codes from global
+        for (int u = 0; u < cnt; ++u) {
+          const uint8_t* rp = rows + (int64_t)__ldg(src + e0 + a + u) * stride + lane * NB;
+          uint32_t tw = 0;
+#pragma unroll
+          for (int b = 0; b < NB; ++b) tw |= (uint32_t)__ldg(rp + b) << (8 * b);
+          sq_lane_body<K, NB, 1>(reinterpret_cast<const uint8_t*>(&tw), tb, acc);
+        }
+      }
+      const float inv = cnt ? (cnt <= 8 ? kInvCnt[cnt] : 1.0f / (float)cnt) : 0.0f;
+      uint32_t w[NA];
+#pragma unroll
+      for (int j = 0; j < NA; ++j) {
+        const __nv_bfloat162 b2 = __floats2bfloat162_rn(lo2(acc[j]) * inv, hi2(acc[j]) * inv);
+        w[j] = *reinterpret_cast<const uint32_t*>(&b2);
+      }
+      __nv_bfloat16* o = out + v * ld + lane * EPL;
+      if (vec_ok) {
+        if constexpr (NA == 2) *reinterpret_cast<uint2*>(o) = make_uint2(w[0], w[1]);
+        else if constexpr (NA == 4) *reinterpret_cast<uint4*>(o) = make_uint4(w[0], w[1], w[2], w[3]);
+        else *reinterpret_cast<uint32_t*>(o) = w[0];
+      } else {
+#pragma unroll
+        for (int j = 0; j < NA; ++j) {
+          o[2 * j] = __ushort_as_bfloat16((unsigned short)(w[j] & 0xFFFFu));
+          o[2 * j + 1] = __ushort_as_bfloat16((unsigned short)(w[j] >> 16));
+        }
+      }
+    }
+    cp_wait_all();
+    __syncthreads();
+  }
+}
+
+// SQ lane launch for bf16 output, mean, k in {4, 8}, d*k/8 a multiple of 32;
+// false when not covered (FG_SQ_LANE=0 also disables it)
+template <bool WT>
+static bool launch_sq_lane(const fg_codec_desc* c, const int32_t* indptr, const int32_t* src,
+                           const int64_t* ndst, int64_t max_dst, void* out, int64_t ld,
+                           cudaStream_t st, int* rc) {
+  if constexpr (WT) {
+    return false;
+  } else {
+    static const int env = [] {
+      const char* e = getenv("FG_SQ_LANE");
+      return e ? atoi(e) : 1;
+    }();
+    const int K = c->bits;
+    if (!env || !(K == 4 || K == 8) || (c->d * K) % 256 != 0 || c->elem_bits != 32) return false;
+    const int RB = (int)(c->d * K / 8), NB = RB / 32;
+    if (!(NB == 2 || NB == 4) || c->row_stride < RB || c->row_stride % 16 != 0) return false;
+    const int lutb = K == 4 ? 256 * 32 * 8 : 256 * 32 * 4;
+    const int tail = 4 * (kTD + 4) * 4;
+    int cap = kSrcCap;
+    while (cap > kTD && lutb + 2 * (int64_t)cap * RB + 3 * (int64_t)cap * 4 + tail > 220 * 1024)
+      cap -= kTD;
+    const int64_t smem = lutb + 2 * (int64_t)cap * RB + 3 * (int64_t)cap * 4 + tail;
+    void (*kern)(const uint8_t*, int64_t, const float*, const int32_t*, const int32_t*,
+                 const int64_t*, int64_t, __nv_bfloat16*, int64_t, int) =
+        K == 4 ? (NB == 2 ? k_sq_mean_lane<4, 2> : k_sq_mean_lane<4, 4>)
+               : (NB == 2 ? k_sq_mean_lane<8, 2> : k_sq_mean_lane<8, 4>);
+    *rc = FG_OK;
+    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem);
+    if (err != cudaSuccess) {
+      set_error("sq lane smem attribute: %s", cudaGetErrorString(err));
+      *rc = FG_ECUDA;
+      return true;
+    }
+    const int grid = (int)min64(ceil_div(max_dst, kTD), (int64_t)sm_count());
+    kern<<<grid, kLaneThreads, smem, st>>>(c->rows, c->row_stride, (const float*)c->table, indptr,
+                                           src, ndst, max_dst, (__nv_bfloat16*)out, ld, cap);
+    count_launch();
+    err = cudaGetLastError();
+    if (err != cudaSuccess) {
+      set_error("k_sq_mean_lane launch: %s", cudaGetErrorString(err));
+      *rc = FG_ECUDA;
+    }
+    return true;
+  }
+}
+
 // ------------------------------------------------- VQ (any code width)
 template <int W, typename OT>
 __global__ void __launch_bounds__(kThreads, 2)
@@ -1470,6 +1696,10 @@ template <int K, typename OT, bool WT>
 int launch_sq_w(const fg_codec_desc* c, const int32_t* indptr, const int32_t* src,
                 const int64_t* ndst, int64_t max_dst, void* out, int64_t ld, cudaStream_t st,
                 const float* ew) {
+  if constexpr (std::is_same<OT, __nv_bfloat16>::value) {
+    int rc = FG_OK;
+    if (launch_sq_lane<WT>(c, indptr, src, ndst, max_dst, out, ld, st, &rc)) return rc;
+  }
   // TMA-staged variant: needs a row buffer holding a tile of >= 32
   // destinations at fanout 8 next to the decode table
   {
