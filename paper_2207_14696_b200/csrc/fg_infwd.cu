@@ -310,7 +310,7 @@ static int infwd_smem_bytes(int H, int P) {
 //   warps 2-9 epilogue (unchanged math): TMEM -> ReLU -> per-destination
 //            sums -> bf16 rows + ReLU mask bits; they release the TMEM
 //            accumulator (`acc_empty`) and the stage (`empty`).
-constexpr int kIf2Threads = 320;
+constexpr int kIf2Threads = 576;  // producer, MMA issuer, 2 x 8 epilogue warps
 constexpr int kIf2Stages = 3;
 
 __device__ __forceinline__ void if_wait(const uint64_t* bar, uint32_t parity) {
@@ -338,8 +338,8 @@ k_input_block_mean_fwd2(const uint16_t* __restrict__ x, int P, const uint16_t* _
   uint8_t* sW = if_mem;                                            // W0: H x P (K-major)
   uint8_t* sX0 = sW + H * P * 2;                                   // [stages] 128 x P
   Meta* meta = reinterpret_cast<Meta*>(sX0 + kIf2Stages * kIfRows * P * 2);  // [stages]
-  uint32_t* s_bits = reinterpret_cast<uint32_t*>(meta + kIf2Stages);  // [8][32]
-  uint64_t* s_full = reinterpret_cast<uint64_t*>(s_bits + 8 * 32);   // [stages]
+  uint32_t* s_bits = reinterpret_cast<uint32_t*>(meta + kIf2Stages);  // [16][32]
+  uint64_t* s_full = reinterpret_cast<uint64_t*>(s_bits + 16 * 32);  // [stages]
   uint64_t* s_empty = s_full + kIf2Stages;                           // [stages]
   uint64_t* s_accf = s_empty + kIf2Stages;                           // [2]
   uint64_t* s_acce = s_accf + 2;                                     // [2]
@@ -393,23 +393,65 @@ k_input_block_mean_fwd2(const uint16_t* __restrict__ x, int P, const uint16_t* _
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
+    // software-pipelined: the indptr window of tile k+2 and the edge sources
+    // of tile k+1 are loaded into registers while tile k's metadata and row
+    // copies are issued (ncu of the unpipelined producer: 3 serial global
+    // round trips per tile, the consumers spinning on `full`)
+    constexpr int kIpq = (kIfRows + 31) / 32;  // indptr window entries per lane (D + 1 <= 128)
+    auto nd_of = [&](int64_t t) { return (int)min64(D, live - t * D); };
+    auto load_ip = [&](int64_t t, int32_t* r) {
+      const int nd = nd_of(t);
+#pragma unroll
+      for (int q = 0; q < kIpq; ++q) {
+        const int i = lane + 32 * q;
+        r[q] = i <= nd ? __ldg(indptr + t * D + i) : 0;
+      }
+    };
+    auto ip_at = [&](const int32_t* r, int i) {  // window entry i (uniform)
+      int32_t v = 0;
+#pragma unroll
+      for (int q = 0; q < kIpq; ++q) {
+        const int32_t x = __shfl_sync(0xFFFFFFFFu, r[q], i & 31);
+        if ((i >> 5) == q) v = x;
+      }
+      return v;
+    };
+    auto load_l = [&](int64_t t, const int32_t* r, int32_t* lv) {
+      const int32_t e0 = ip_at(r, 0), ne = ip_at(r, nd_of(t)) - e0;
+#pragma unroll
+      for (int q = 0; q < kIfRows / 32; ++q) {
+        const int i = lane + 32 * q;
+        lv[q] = i < ne ? __ldg(local + e0 + i) : -1;
+      }
+    };
+    int32_t ip_c[kIpq], ip_n[kIpq], lv_c[kIfRows / 32];
+    {
+      const int64_t t0 = blockIdx.x;
+      load_ip(t0, ip_c);
+      load_l(t0, ip_c, lv_c);
+      if (t0 + G < ntiles) load_ip(t0 + G, ip_n);
+    }
     int k = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += G, ++k) {
       const int s = k % kIf2Stages, use = k / kIf2Stages;
       if (use > 0) if_wait(s_empty + s, (uint32_t)((use - 1) & 1));
       Meta& m = meta[s];
-      const int64_t v0 = tile * D;
-      const int nd = (int)min64(D, live - v0);
-      for (int t = lane; t <= nd; t += 32) m.ip[t] = __ldg(indptr + v0 + t);
+      const int nd = nd_of(tile);
+#pragma unroll
+      for (int q = 0; q < kIpq; ++q)
+        if (lane + 32 * q <= nd) m.ip[lane + 32 * q] = ip_c[q];
+      int32_t lv[kIfRows / 32];
+#pragma unroll
+      for (int q = 0; q < kIfRows / 32; ++q) lv[q] = lv_c[q];
       __syncwarp();
       const int32_t e0 = m.ip[0];
       const int ne = m.ip[nd] - e0;
-      int32_t lv[kIfRows / 32];
+      // next tiles' loads in flight while this tile is issued
+      const bool has1 = tile + G < ntiles, has2 = tile + 2 * G < ntiles;
+      if (has1) load_l(tile + G, ip_n, lv_c);
 #pragma unroll
-      for (int q = 0; q < kIfRows / 32; ++q) {
-        const int r = lane + 32 * q;
-        lv[q] = r < ne ? __ldg(local + e0 + r) : -1;
-      }
+      for (int q = 0; q < kIpq; ++q) ip_c[q] = ip_n[q];
+      if (has2) load_ip(tile + 2 * G, ip_n);
 #pragma unroll
       for (int q = 0; q < kIfRows / 32; ++q) {
         const int r = lane + 32 * q;
@@ -488,15 +530,22 @@ k_input_block_mean_fwd2(const uint16_t* __restrict__ x, int P, const uint16_t* _
     }
   } else {
     // ------------------------------------------------------------ epilogue
-    const int ew_ = warp - 2;                 // 0..7
-    const int half = ew_ >> 2;                // warps 2-5: features 0..127
+    // two groups of 8 warps take alternate tiles (group g: tiles k = g mod 2,
+    // TMEM accumulator g), so two epilogues run at once -- ncu: the per-edge
+    // ReLU / ballot / running-sum chain of one 8-warp group bounded the
+    // kernel (~4 us per tile)
+    const int ew_all = warp - 2;              // 0..15
+    const int grp = ew_all >> 3;
+    const int ew_ = ew_all & 7;               // 0..7 within the group
+    const int half = ew_ >> 2;                // warps 0-3 of a group: features 0..127
     const bool epi = half < halves;
     const int q4 = warp & 3;                  // TMEM lane quarter of this warp
     const int fbase = half * 128 + q4 * 32;
     const int f = fbase + lane;
-    uint32_t* wbits = s_bits + ew_ * 32;
+    uint32_t* wbits = s_bits + ew_all * 32;
     int k = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += G, ++k) {
+      if ((k & 1) != grp) continue;
       const int s = k % kIf2Stages, a = k & 1;
       if_wait(s_accf + a, (uint32_t)((k >> 1) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;");
@@ -553,7 +602,7 @@ k_input_block_mean_fwd2(const uint16_t* __restrict__ x, int P, const uint16_t* _
           for (uint32_t em = m.emask[q]; em; em &= em - 1)
             orow[(int64_t)(q * 32 + __ffs(em) - 1) * out_ld] = 0;
       }
-      if (out_ld > H && ew_ == 0)  // bias column block [1, 0, ..., 0]
+      if (out_ld > H && ew_ == 0)  // bias column block [1, 0, ..., 0] (the group's warp 0)
         for (int t = lane; t < nd; t += 32)
           reinterpret_cast<uint4*>(out + (v0 + t) * out_ld + H)[0] = make_uint4(0x3F80u, 0u, 0u, 0u);
       __syncwarp();
@@ -568,7 +617,7 @@ k_input_block_mean_fwd2(const uint16_t* __restrict__ x, int P, const uint16_t* _
 }
 
 static int infwd2_smem_bytes(int H, int P) {
-  return H * P * 2 + kIf2Stages * kIfRows * P * 2 + kIf2Stages * (int)sizeof(Meta) + 8 * 32 * 4 +
+  return H * P * 2 + kIf2Stages * kIfRows * P * 2 + kIf2Stages * (int)sizeof(Meta) + 16 * 32 * 4 +
          (2 * kIf2Stages + 5) * 8 + 16;
 }
 
@@ -598,10 +647,12 @@ extern "C" int fg_input_block_mean_fwd(const uint16_t* x, int64_t P, const uint1
   FG_CHECK_ARG(out_ld == H || out_ld == H + 8, "out_ld must be H or H + 8 (ones column)");
   if (max_dst == 0) return FG_OK;
   const int D = (int)min64(kIfRows / fanout, kIfRows - 1);
-  // v2 (warp-specialised) when v1 fits only one CTA per SM: measured on the
-  // B200 papers100M-shape block (P = 144, v1 at 1 CTA/SM) 62.8 -> 50.6 us;
-  // products-shape (P = 112, v1 at 2 CTAs/SM) v1 48.5 us beats v2 56.7 us.
-  // FG_INFWD_V2 = 0 / 1 forces v1 / v2.
+  // v2 (warp-specialised, two epilogue warp groups) where v1 fits only one
+  // CTA per SM: papers100M-shape block (P = 144) 62.8 (v1) -> 44.5 us.  At
+  // products shape (P = 112, v1 at 2 CTAs/SM) v2 is faster alone (46.5 vs
+  // 48.5 us) but the step is slower (0.248 vs 0.238 ms: one 576-thread CTA
+  // on every SM crowds out the overlapped sampler).  FG_INFWD_V2 = 0 / 1
+  // forces v1 / v2.
   static const int v2_env = [] {
     const char* e = getenv("FG_INFWD_V2");
     return e ? atoi(e) : -1;
