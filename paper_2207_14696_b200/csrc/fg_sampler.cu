@@ -505,7 +505,14 @@ k_layer_fixup(const int64_t* __restrict__ off, const int32_t* __restrict__ col,
 // ids, is 212 tiles instead of 1.7 K, one wave with a short look-back chain),
 // 1 below ~10 M ids (products-shape: 1 item per thread keeps ~40 CTAs busy).
 constexpr int kBmIpt = 8;
-inline int bm_ipt(int64_t words0) { return words0 / 32 * 4 >= 148ll * kBmThreads * 8 ? kBmIpt : 1; }
+inline int bm_ipt(int64_t words0) {
+  static const int env = [] {  // FG_BM_IPT: force 1 / 2 / 4 / 8 / 16 items per thread
+    const char* e = getenv("FG_BM_IPT");
+    return e ? atoi(e) : 0;
+  }();
+  if (env == 1 || env == 2 || env == 4 || env == 8 || env == 16) return env;
+  return words0 / 32 * 4 >= 148ll * kBmThreads * 8 ? kBmIpt : 1;
+}
 template <int IPT>
 __global__ void __launch_bounds__(kBmThreads)
 k_bm_compact(const uint32_t* __restrict__ bm, int64_t words0, unsigned long long* status,
@@ -746,7 +753,8 @@ int fg_bitmap_compact(uint32_t* bm, int64_t n, int32_t* out_ids, int64_t max_out
   unsigned int* ctr = (unsigned int*)ws;
   unsigned long long* status = (unsigned long long*)((char*)ws + 64);
   FG_CUDA_TRY(cudaMemsetAsync(ws, 0, 64 + nb * 8, st));
-  auto kern = ipt == kBmIpt ? k_bm_compact<kBmIpt> : k_bm_compact<1>;
+  auto kern = ipt == 16 ? k_bm_compact<16> : ipt == 8 ? k_bm_compact<8> : ipt == 4 ? k_bm_compact<4>
+            : ipt == 2 ? k_bm_compact<2> : k_bm_compact<1>;
   kern<<<(unsigned)nb, kBmThreads, 0, st>>>(bm, words0, status, ctr, out_ids, max_out, out_count,
                                             wprefix, (unsigned)nb);
   FG_LAUNCH_CHECK();
