@@ -337,6 +337,13 @@ int fg_block_mean_bwd_t(const uint16_t* grad_out, int64_t h_dim, int64_t g_ld,
                         const int32_t* t_indptr, const int32_t* t_dst,
                         const float* t_w, const int64_t* n_src_dev, int64_t cap_src,
                         const uint16_t* relu_mask, uint16_t* out, void* cuda_stream);
+/* Same, with the ReLU mask as packed bits (h_dim/8 bytes per source row, bit
+ * t of byte c = feature 8c + t, as fg_block_mean_fwd_bits writes them): the
+ * backward reads 1/16 of the bytes of the bf16 h mask. */
+int fg_block_mean_bwd_t_bits(const uint16_t* grad_out, int64_t h_dim, int64_t g_ld,
+                             const int32_t* t_indptr, const int32_t* t_dst,
+                             const float* t_w, const int64_t* n_src_dev, int64_t cap_src,
+                             const uint8_t* relu_bits, uint16_t* out, void* cuda_stream);
 
 /* Fused block-mean backward + input-layer weight gradient (tcgen05/TMEM).
  * For the SAGE input layer h = x W^T (x: [cap_src, p_dim] bf16 rows with a
@@ -375,13 +382,17 @@ int fg_relu_mask_bits(const uint16_t* h, int64_t rows, int64_t h_dim, uint8_t* o
  * picks).  el/er/q/alpha fp32 [rows, heads]; z bf16 [src rows, hf]
  * (hf / heads a multiple of 8); out/dout/dz fp32.  Backward accumulates into
  * del/der/dz/dalpha with atomics (callers zero them). */
-int fg_gat_softmax_fwd(const float* el, const float* er, const int32_t* indptr,
-                       const int32_t* local, int64_t max_dst, const int64_t* n_dst_dev,
-                       int heads, float slope, float* alpha, float* q, void* cuda_stream);
-int fg_gat_softmax_bwd(const float* el, const float* q, const float* alpha, const float* dalpha,
+/* el / er / del / der rows have pitch score_ld floats (0 = heads): the
+ * scores of one GEMM [rows, 2 heads] are passed as el = s, er = s + heads,
+ * score_ld = 2 heads. */
+int fg_gat_softmax_fwd(const float* el, const float* er, int64_t score_ld,
                        const int32_t* indptr, const int32_t* local, int64_t max_dst,
-                       const int64_t* n_dst_dev, int heads, float slope, float* del,
-                       float* der, void* cuda_stream);
+                       const int64_t* n_dst_dev, int heads, float slope, float* alpha, float* q,
+                       void* cuda_stream);
+int fg_gat_softmax_bwd(const float* el, int64_t score_ld, const float* q, const float* alpha,
+                       const float* dalpha, const int32_t* indptr, const int32_t* local,
+                       int64_t max_dst, const int64_t* n_dst_dev, int heads, float slope,
+                       float* del, float* der, void* cuda_stream);
 int fg_gat_agg_fwd(const uint16_t* z, int64_t hf, int heads, const float* alpha,
                    const int32_t* indptr, const int32_t* local, int64_t max_dst,
                    const int64_t* n_dst_dev, float* out, void* cuda_stream);
@@ -415,7 +426,7 @@ int64_t fg_gat_code_scores_bwd_blocks(int64_t e_cap);
 int fg_gat_code_scores_bwd(const fg_codec_desc* codec, const uint16_t* x_rows,
                            const int32_t* picks, const int64_t* n_picks_dev, int64_t e_cap,
                            int64_t d, int heads, const float* del, const float* der,
-                           float* partial, void* cuda_stream);
+                           int64_t score_ld, float* partial, void* cuda_stream);
 int fg_gat_code_xagg_fwd(const fg_codec_desc* codec, const uint16_t* x_rows,
                          const int32_t* picks, int64_t d, int heads, const float* alpha,
                          const int32_t* indptr, int64_t max_dst, const int64_t* n_dst_dev,

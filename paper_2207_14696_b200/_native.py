@@ -75,21 +75,22 @@ _SIGS = {
     "fg_block_transpose_scratch_bytes": (i64, [i64]),
     "fg_block_transpose": (ci, [vp, vp, i64, vp, vp, i64, ci, i64, vp, vp, vp, vp, vp, i64, vp]),
     "fg_block_mean_bwd_t": (ci, [vp, i64, i64, vp, vp, vp, vp, i64, vp, vp, vp]),
+    "fg_block_mean_bwd_t_bits": (ci, [vp, i64, i64, vp, vp, vp, vp, i64, vp, vp, vp]),
     "fg_block_mean_wgrad_supported": (ci, [i64, i64]),
     "fg_block_mean_wgrad_scratch_bytes": (i64, [i64, i64]),
     "fg_block_mean_wgrad": (ci, [vp, i64, vp, vp, vp, i64, vp, vp, ci, i64, vp, i64, vp, vp,
                                  i64, vp]),
     "fg_relu_mask_bits": (ci, [vp, i64, i64, vp, vp]),
-    "fg_gat_softmax_fwd": (ci, [vp, vp, vp, vp, i64, vp, ci, C.c_float, vp, vp, vp]),
-    "fg_gat_softmax_bwd": (ci, [vp, vp, vp, vp, vp, vp, i64, vp, ci, C.c_float, vp, vp, vp]),
+    "fg_gat_softmax_fwd": (ci, [vp, vp, i64, vp, vp, i64, vp, ci, C.c_float, vp, vp, vp]),
+    "fg_gat_softmax_bwd": (ci, [vp, i64, vp, vp, vp, vp, vp, i64, vp, ci, C.c_float, vp, vp, vp]),
     "fg_gat_agg_fwd": (ci, [vp, i64, ci, vp, vp, vp, i64, vp, vp, vp]),
     "fg_gat_agg_bwd": (ci, [vp, i64, ci, vp, vp, vp, i64, vp, vp, vp, vp, vp]),
     "fg_gat_xagg_fwd": (ci, [vp, i64, ci, vp, vp, i64, vp, vp, vp]),
     "fg_gat_xagg_bwd": (ci, [vp, i64, ci, vp, i64, vp, vp, vp, i64, vp]),
     "fg_gat_code_scores": (ci, [C.POINTER(CodecDesc), vp, vp, vp, i64, i64, ci, vp, vp, vp, vp]),
     "fg_gat_code_scores_bwd_blocks": (i64, [i64]),
-    "fg_gat_code_scores_bwd": (ci, [C.POINTER(CodecDesc), vp, vp, vp, i64, i64, ci, vp, vp, vp,
-                                    vp]),
+    "fg_gat_code_scores_bwd": (ci, [C.POINTER(CodecDesc), vp, vp, vp, i64, i64, ci, vp, vp, i64,
+                                    vp, vp]),
     "fg_gat_code_xagg_fwd": (ci, [C.POINTER(CodecDesc), vp, vp, i64, ci, vp, vp, i64, vp, vp,
                                   vp]),
     "fg_gat_code_xagg_bwd": (ci, [C.POINTER(CodecDesc), vp, vp, i64, ci, vp, i64, vp, vp, vp,

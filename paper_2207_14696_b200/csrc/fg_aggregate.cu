@@ -321,13 +321,17 @@ __device__ __forceinline__ uint2 f32_to_bf16x4(const float* f) {
   return make_uint2(*reinterpret_cast<const uint32_t*>(&a), *reinterpret_cast<const uint32_t*>(&b));
 }
 
-template <bool RELU, int R>
+// RELU: 0 none, 1 mask = the forward's bf16 h rows (relu' = h > 0), 2 mask =
+// packed ReLU bits (H/8 bytes per row, bit t of byte c = feature 8c + t, as
+// fg_block_mean_fwd_bits / fg_input_block_mean_fwd write them)
+template <int RELU, int R>
 __global__ void __launch_bounds__(256, 3)
 k_block_mean_bwd_t(const uint16_t* __restrict__ g, int64_t H, int64_t g_ld,
                    const int32_t* __restrict__ t_indptr,
                    const int32_t* __restrict__ t_dst, const float* __restrict__ t_w,
                    const int64_t* __restrict__ nsrc_dev, int64_t cap_src,
-                   const uint16_t* __restrict__ mask, uint16_t* __restrict__ out) {
+                   const uint16_t* __restrict__ mask, const uint8_t* __restrict__ mbits,
+                   uint16_t* __restrict__ out) {
   const int64_t chunks = H >> 2;
   const int64_t ngroups = (cap_src + R - 1) / R;
   const int64_t total = ngroups * chunks;
@@ -351,10 +355,13 @@ k_block_mean_bwd_t(const uint16_t* __restrict__ g, int64_t H, int64_t g_ld,
     for (int u = 0; u < R; ++u)
       if (i0[u] < i1[u]) { v[u] = t_dst[i0[u]]; w[u] = t_w[i0[u]]; }
     uint2 q[R], mq[R];
+    uint32_t mb[R];
 #pragma unroll
     for (int u = 0; u < R; ++u) {
       mq[u] = make_uint2(0u, 0u);
-      if (RELU && r0 + u < live) mq[u] = __ldg(reinterpret_cast<const uint2*>(mask + (r0 + u) * H) + c);
+      mb[u] = 0u;
+      if (RELU == 1 && r0 + u < live) mq[u] = __ldg(reinterpret_cast<const uint2*>(mask + (r0 + u) * H) + c);
+      if (RELU == 2 && r0 + u < live) mb[u] = __ldg(mbits + (r0 + u) * (H >> 3) + (c >> 1));
       if (i0[u] < i1[u]) q[u] = __ldg(reinterpret_cast<const uint2*>(g + (int64_t)v[u] * g_ld) + c);
     }
 #pragma unroll
@@ -387,11 +394,16 @@ k_block_mean_bwd_t(const uint16_t* __restrict__ g, int64_t H, int64_t g_ld,
             for (int j = 0; j < 4; ++j) acc[j] = fmaf(f[j], sc[k], acc[j]);
           }
       }
-      if (RELU) {
+      if (RELU == 1) {
         float m[4];
         bf16x4_to_f32(mq[u], m);
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[j] = m[j] > 0.f ? acc[j] : 0.f;
+      }
+      if (RELU == 2) {
+        const uint32_t nib = mb[u] >> ((c & 1) * 4);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[j] = (nib >> j) & 1u ? acc[j] : 0.f;
       }
       // padded source rows (r >= live) get a zero gradient
       reinterpret_cast<uint2*>(out + r * H)[c] = f32_to_bf16x4(acc);
@@ -481,24 +493,45 @@ extern "C" int fg_block_transpose(const int32_t* local, const int64_t* n_edges_d
   return FG_OK;
 }
 
-extern "C" int fg_block_mean_bwd_t(const uint16_t* g, int64_t H, int64_t g_ld,
-                                   const int32_t* t_indptr, const int32_t* t_dst,
-                                   const float* t_w, const int64_t* n_src_dev, int64_t cap_src,
-                                   const uint16_t* relu_mask, uint16_t* out, void* s) {
+static int block_mean_bwd_t(const uint16_t* g, int64_t H, int64_t g_ld, const int32_t* t_indptr,
+                            const int32_t* t_dst, const float* t_w, const int64_t* n_src_dev,
+                            int64_t cap_src, const uint16_t* relu_mask, const uint8_t* relu_bits,
+                            uint16_t* out, void* s) {
   FG_CHECK_ARG(H % 8 == 0, "hidden dim must be a multiple of 8");
   if (g_ld == 0) g_ld = H;
   FG_CHECK_ARG(g_ld % 8 == 0 && g_ld >= H, "bad g_ld");
   if (cap_src == 0) return FG_OK;
   constexpr int R = 4;
   const int64_t total = (cap_src + R - 1) / R * (H / 4);
-  if (relu_mask)
-    fg::k_block_mean_bwd_t<true, R><<<grid_for(total, 256, 3), 256, 0, as_stream(s)>>>(
-        g, H, g_ld, t_indptr, t_dst, t_w, n_src_dev, cap_src, relu_mask, out);
+  if (relu_bits)
+    fg::k_block_mean_bwd_t<2, R><<<grid_for(total, 256, 3), 256, 0, as_stream(s)>>>(
+        g, H, g_ld, t_indptr, t_dst, t_w, n_src_dev, cap_src, nullptr, relu_bits, out);
+  else if (relu_mask)
+    fg::k_block_mean_bwd_t<1, R><<<grid_for(total, 256, 3), 256, 0, as_stream(s)>>>(
+        g, H, g_ld, t_indptr, t_dst, t_w, n_src_dev, cap_src, relu_mask, nullptr, out);
   else
-    fg::k_block_mean_bwd_t<false, R><<<grid_for(total, 256, 3), 256, 0, as_stream(s)>>>(
-        g, H, g_ld, t_indptr, t_dst, t_w, n_src_dev, cap_src, nullptr, out);
+    fg::k_block_mean_bwd_t<0, R><<<grid_for(total, 256, 3), 256, 0, as_stream(s)>>>(
+        g, H, g_ld, t_indptr, t_dst, t_w, n_src_dev, cap_src, nullptr, nullptr, out);
   FG_LAUNCH_CHECK();
   return FG_OK;
+}
+
+extern "C" int fg_block_mean_bwd_t(const uint16_t* g, int64_t H, int64_t g_ld,
+                                   const int32_t* t_indptr, const int32_t* t_dst,
+                                   const float* t_w, const int64_t* n_src_dev, int64_t cap_src,
+                                   const uint16_t* relu_mask, uint16_t* out, void* s) {
+  return block_mean_bwd_t(g, H, g_ld, t_indptr, t_dst, t_w, n_src_dev, cap_src, relu_mask,
+                          nullptr, out, s);
+}
+
+extern "C" int fg_block_mean_bwd_t_bits(const uint16_t* g, int64_t H, int64_t g_ld,
+                                        const int32_t* t_indptr, const int32_t* t_dst,
+                                        const float* t_w, const int64_t* n_src_dev,
+                                        int64_t cap_src, const uint8_t* relu_bits,
+                                        uint16_t* out, void* s) {
+  FG_CHECK_ARG(relu_bits != nullptr, "relu_bits is required");
+  return block_mean_bwd_t(g, H, g_ld, t_indptr, t_dst, t_w, n_src_dev, cap_src, nullptr,
+                          relu_bits, out, s);
 }
 
 extern "C" int fg_adam_step(float* params, const float* grads, float* m, float* v, int64_t n,

@@ -29,7 +29,7 @@ __device__ __forceinline__ float leaky(float x, float s) { return x > 0.f ? x : 
 
 // alpha[e, k], q[v, k]
 __global__ void k_gat_softmax_fwd(const float* __restrict__ el, const float* __restrict__ er,
-                                  const int32_t* __restrict__ indptr,
+                                  int64_t ld, const int32_t* __restrict__ indptr,
                                   const int32_t* __restrict__ local, int64_t ndst_live_cap,
                                   const int64_t* __restrict__ ndst_dev, int heads, float slope,
                                   float* __restrict__ alpha, float* __restrict__ q) {
@@ -46,19 +46,19 @@ __global__ void k_gat_softmax_fwd(const float* __restrict__ el, const float* __r
     float qs = 0.f;
     for (int32_t e = e0; e < e1; ++e) {
       const int64_t u = local ? local[e] : e;
-      qs += er[u * heads + k];
+      qs += er[u * ld + k];
     }
     const float qv = qs / (float)(e1 - e0);
     q[t] = qv;
     float mx = -INFINITY;
     for (int32_t e = e0; e < e1; ++e) {
       const int64_t u = local ? local[e] : e;
-      mx = fmaxf(mx, leaky(el[u * heads + k] + qv, slope));
+      mx = fmaxf(mx, leaky(el[u * ld + k] + qv, slope));
     }
     float den = 0.f;
     for (int32_t e = e0; e < e1; ++e) {
       const int64_t u = local ? local[e] : e;
-      const float p = __expf(leaky(el[u * heads + k] + qv, slope) - mx);
+      const float p = __expf(leaky(el[u * ld + k] + qv, slope) - mx);
       alpha[(int64_t)e * heads + k] = p;
       den += p;
     }
@@ -68,7 +68,8 @@ __global__ void k_gat_softmax_fwd(const float* __restrict__ el, const float* __r
 }
 
 // d el[u,k] += dpre_e ; d er[u,k] += (sum_e' dpre_e') / cnt_v
-__global__ void k_gat_softmax_bwd(const float* __restrict__ el, const float* __restrict__ q,
+__global__ void k_gat_softmax_bwd(const float* __restrict__ el, int64_t ld,
+                                  const float* __restrict__ q,
                                   const float* __restrict__ alpha, const float* __restrict__ dalpha,
                                   const int32_t* __restrict__ indptr,
                                   const int32_t* __restrict__ local, int64_t ndst_cap,
@@ -90,15 +91,15 @@ __global__ void k_gat_softmax_bwd(const float* __restrict__ el, const float* __r
       const int64_t u = local ? local[e] : e;
       const float a = alpha[(int64_t)e * heads + k];
       const float ds = a * (dalpha[(int64_t)e * heads + k] - dot);
-      const float pre = el[u * heads + k] + qv;
+      const float pre = el[u * ld + k] + qv;
       const float dpre = pre > 0.f ? ds : slope * ds;
-      atomicAdd(del + u * heads + k, dpre);
+      atomicAdd(del + u * ld + k, dpre);
       dq += dpre;
     }
     const float share = dq / (float)(e1 - e0);
     for (int32_t e = e0; e < e1; ++e) {
       const int64_t u = local ? local[e] : e;
-      atomicAdd(der + u * heads + k, share);
+      atomicAdd(der + u * ld + k, share);
     }
   }
 }
@@ -179,26 +180,31 @@ __global__ void k_gat_agg_bwd(const __nv_bfloat16* __restrict__ z, int64_t hf, i
 
 using namespace fg;
 
-extern "C" int fg_gat_softmax_fwd(const float* el, const float* er, const int32_t* indptr,
-                                  const int32_t* local, int64_t max_dst, const int64_t* n_dst_dev,
-                                  int heads, float slope, float* alpha, float* q, void* s) {
+extern "C" int fg_gat_softmax_fwd(const float* el, const float* er, int64_t ld,
+                                  const int32_t* indptr, const int32_t* local, int64_t max_dst,
+                                  const int64_t* n_dst_dev, int heads, float slope, float* alpha,
+                                  float* q, void* s) {
   FG_CHECK_ARG(el && er && indptr && n_dst_dev && alpha && q && heads >= 1, "null argument");
+  if (ld == 0) ld = heads;
+  FG_CHECK_ARG(ld >= heads, "fg_gat_softmax_fwd: ld < heads");
   if (max_dst == 0) return FG_OK;
   k_gat_softmax_fwd<<<grid_for(max_dst * heads, 256), 256, 0, as_stream(s)>>>(
-      el, er, indptr, local, max_dst, n_dst_dev, heads, slope, alpha, q);
+      el, er, ld, indptr, local, max_dst, n_dst_dev, heads, slope, alpha, q);
   FG_LAUNCH_CHECK();
   return FG_OK;
 }
 
-extern "C" int fg_gat_softmax_bwd(const float* el, const float* q, const float* alpha,
-                                  const float* dalpha, const int32_t* indptr,
+extern "C" int fg_gat_softmax_bwd(const float* el, int64_t ld, const float* q,
+                                  const float* alpha, const float* dalpha, const int32_t* indptr,
                                   const int32_t* local, int64_t max_dst,
                                   const int64_t* n_dst_dev, int heads, float slope, float* del,
                                   float* der, void* s) {
   FG_CHECK_ARG(el && q && alpha && dalpha && indptr && n_dst_dev && del && der, "null argument");
+  if (ld == 0) ld = heads;
+  FG_CHECK_ARG(ld >= heads, "fg_gat_softmax_bwd: ld < heads");
   if (max_dst == 0) return FG_OK;
   k_gat_softmax_bwd<<<grid_for(max_dst * heads, 256), 256, 0, as_stream(s)>>>(
-      el, q, alpha, dalpha, indptr, local, max_dst, n_dst_dev, heads, slope, del, der);
+      el, ld, q, alpha, dalpha, indptr, local, max_dst, n_dst_dev, heads, slope, del, der);
   FG_LAUNCH_CHECK();
   return FG_OK;
 }
@@ -379,6 +385,7 @@ k_gat_code_scores(GatCodes cd, int d, int heads, const float* __restrict__ c,
 // (deterministic; the partials are summed in block order by the caller)
 __global__ void k_gat_code_scores_bwd(GatCodes cd, int d, int heads,
                                       const float* __restrict__ del, const float* __restrict__ der,
+                                      int64_t ld,
                                       const int64_t* __restrict__ ne_dev, int64_t e_cap,
                                       int64_t per_block, float* __restrict__ partial) {
   __shared__ float s_ds[32][2 * kMaxHeads];
@@ -392,7 +399,7 @@ __global__ void k_gat_code_scores_bwd(GatCodes cd, int d, int heads,
     __syncthreads();
     for (int i = threadIdx.x; i < nb * 2 * heads; i += blockDim.x) {
       const int r = i / (2 * heads), q = i - r * 2 * heads;
-      s_ds[r][q] = q < heads ? del[(e0 + r) * heads + q] : der[(e0 + r) * heads + q - heads];
+      s_ds[r][q] = q < heads ? del[(e0 + r) * ld + q] : der[(e0 + r) * ld + q - heads];
     }
     __syncthreads();
     for (int j = threadIdx.x; j < d; j += blockDim.x) {
@@ -598,17 +605,19 @@ extern "C" int64_t fg_gat_code_scores_bwd_blocks(int64_t e_cap) {
 extern "C" int fg_gat_code_scores_bwd(const fg_codec_desc* codec, const uint16_t* x_rows,
                                       const int32_t* picks, const int64_t* n_picks_dev,
                                       int64_t e_cap, int64_t d, int heads, const float* del,
-                                      const float* der, float* partial, void* s) {
+                                      const float* der, int64_t ld, float* partial, void* s) {
   FG_CHECK_ARG(gat_codes_ok(codec, x_rows) && del && der && partial && n_picks_dev &&
                    heads >= 1 && heads <= fg::kMaxHeads && d >= 1 && d <= 1024,
                "fg_gat_code_scores_bwd: bad argument (d <= 1024)");
+  if (ld == 0) ld = heads;
+  FG_CHECK_ARG(ld >= heads, "fg_gat_code_scores_bwd: ld < heads");
   if (e_cap == 0) return FG_OK;
   const fg::GatCodes g = gat_codes(codec, x_rows, d, picks);
   const int64_t nb = fg_gat_code_scores_bwd_blocks(e_cap);
   const int64_t per = ceil_div(e_cap, nb);
   const int threads = (int)std::max<int64_t>(32, ceil_div(d, 32) * 32);
   fg::k_gat_code_scores_bwd<<<(unsigned)nb, threads, 0, as_stream(s)>>>(
-      g, (int)d, heads, del, der, n_picks_dev, e_cap, per, partial);
+      g, (int)d, heads, del, der, ld, n_picks_dev, e_cap, per, partial);
   FG_LAUNCH_CHECK();
   return FG_OK;
 }

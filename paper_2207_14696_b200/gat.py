@@ -22,6 +22,7 @@ LeakyReLU/ELU and the loss are torch/cuBLAS plus the fused softmax-CE kernel.
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -44,8 +45,8 @@ class GatAttention(torch.autograd.Function):
         el, er = el.float().contiguous(), er.float().contiguous()
         alpha = torch.zeros((e_cap, heads), dtype=torch.float32, device=el.device)
         q = torch.empty((max_dst, heads), dtype=torch.float32, device=el.device)
-        N.call("fg_gat_softmax_fwd", N.ptr(el), N.ptr(er), N.ptr(indptr), N.ptr(local), max_dst,
-               N.ptr(n_dst), heads, slope, N.ptr(alpha), N.ptr(q), N.stream_handle())
+        N.call("fg_gat_softmax_fwd", N.ptr(el), N.ptr(er), heads, N.ptr(indptr), N.ptr(local),
+               max_dst, N.ptr(n_dst), heads, slope, N.ptr(alpha), N.ptr(q), N.stream_handle())
         ctx.save_for_backward(el, q, alpha, indptr, local if local is not None else indptr, n_dst)
         ctx.has_local, ctx.max_dst, ctx.slope = local is not None, max_dst, slope
         return alpha
@@ -57,7 +58,7 @@ class GatAttention(torch.autograd.Function):
         heads = el.shape[1]
         del_ = torch.zeros_like(el)
         der = torch.zeros_like(el)
-        N.call("fg_gat_softmax_bwd", N.ptr(el), N.ptr(q), N.ptr(alpha),
+        N.call("fg_gat_softmax_bwd", N.ptr(el), heads, N.ptr(q), N.ptr(alpha),
                N.ptr(dalpha.float().contiguous()), N.ptr(indptr), N.ptr(local), ctx.max_dst,
                N.ptr(n_dst), heads, ctx.slope, N.ptr(del_), N.ptr(der), N.stream_handle())
         return del_, der, None, None, None, None, None, None
@@ -159,7 +160,7 @@ class GatInputScores(torch.autograd.Function):
         del_ = z if del_ is None else del_.float().contiguous()
         der = z if der is None else der.float().contiguous()
         N.call("fg_gat_code_scores_bwd", *src.head(), N.ptr(src.n_picks), src.e_cap, src.d, heads,
-               N.ptr(del_), N.ptr(der), N.ptr(part), N.stream_handle())
+               N.ptr(del_), N.ptr(der), heads, N.ptr(part), N.stream_handle())
         return part.sum(0), None, None
 
 
@@ -274,6 +275,45 @@ class GatModel(nn.Module):
         return h
 
 
+class _LayerViews:
+    """One GatLayer's parameters as views of the trainer's flat fp32 / bf16
+    parameter buffers and flat gradient (attn_l, attn_r adjacent: one [2,
+    heads, F] view each), plus the input layer's persistent block-diagonal
+    bf16 weight (zero off the diagonal; the diagonal blocks are refreshed
+    from the bf16 shadow every step)."""
+
+    def __init__(self, layer, flat, grad, flat_bf16):
+        def off(p):
+            return (p.data_ptr() - flat.data_ptr()) // flat.element_size()
+
+        self.heads = layer.heads
+        self.width = layer.width
+        self.F = layer.width // layer.heads
+        self.D = layer.lin.weight.shape[1]
+        w, al, ar, b = layer.lin.weight, layer.attn_l, layer.attn_r, layer.bias
+        assert off(ar) == off(al) + al.numel(), "attn_l / attn_r must be adjacent"
+        ow, oa, ob = off(w), off(al), off(b)
+        na, nw, nb = 2 * al.numel(), w.numel(), b.numel()
+        shp_a = (2, self.heads, self.F)
+        self.W = flat[ow:ow + nw].view(w.shape)
+        self.Wb = flat_bf16[ow:ow + nw].view(w.shape)
+        self.attn = flat[oa:oa + na].view(shp_a)
+        self.b = flat[ob:ob + nb]
+        self.bb = flat_bf16[ob:ob + nb]
+        self.dW = grad[ow:ow + nw].view(w.shape)
+        self.dattn = grad[oa:oa + na].view(shp_a)
+        self.db = grad[ob:ob + nb]
+        self.wbd = None
+
+    def refresh_block_diag(self):
+        Hh, F, D = self.heads, self.F, self.D
+        if self.wbd is None:
+            self.wbd = torch.zeros((Hh * D, Hh * F), dtype=torch.bfloat16, device=self.W.device)
+        # wbd[k*D + j, k*F + f] = W[k*F + f, j]
+        self.wbd.view(Hh, D, Hh, F).diagonal(dim1=0, dim2=2).copy_(
+            self.Wb.view(Hh, F, D).permute(2, 1, 0))
+
+
 @dataclass
 class GatConfig:
     fanouts: tuple = (15, 10, 5)
@@ -283,6 +323,7 @@ class GatConfig:
     lr: float = 3e-3
     seed: int = 0
     use_graph: bool = True
+    explicit: bool = True
 
 
 class GatTrainer:
@@ -320,8 +361,18 @@ class GatTrainer:
             off += n
         if self.world > 1:
             torch.distributed.broadcast(self.flat_param, 0, group=self.pg)
-        self.opt = FlatAdam(self.flat_param, self.flat_grad, lr=cfg.lr)
+        # bf16 shadow of the parameters (written by the Adam kernel): the
+        # explicit step's GEMM operands
+        self.flat_bf16 = torch.zeros(total, dtype=torch.bfloat16, device=self.device)
+        self.opt = FlatAdam(self.flat_param, self.flat_grad, lr=cfg.lr, param_bf16=self.flat_bf16)
         self.loss_buf = torch.zeros((), dtype=torch.float32, device=self.device)
+        self.ce_ctr = torch.zeros(1, dtype=torch.int32, device=self.device)
+        # explicit forward/backward (no autograd/autocast glue); FG_GAT_EXPLICIT=0
+        # keeps the autograd model step (A/B and the gradient tests' reference)
+        self.explicit = (cfg.explicit and L > 1
+                         and os.environ.get("FG_GAT_EXPLICIT", "1") != "0")
+        self._views = [_LayerViews(layer, self.flat_param, self.flat_grad, self.flat_bf16)
+                       for layer in self.model.layers]
         self.graph = None
 
     def _decode(self, sb):
@@ -330,16 +381,130 @@ class GatTrainer:
 
     def _body(self, k: int = 0):
         sb = self.sampler.sample_loaded()
-        x = self._decode(sb)
-        with torch.autocast("cuda", dtype=torch.bfloat16):
-            logits = self.model(x, sb, self.caps, self.pick_cap)
-        loss = softmax_ce(logits.contiguous(), self.labels, sb.nodes[0], sb.n_nodes[0],
-                          self.model.num_classes)
-        self.flat_grad.zero_()
-        loss.backward()
+        if self.explicit:
+            self.forward_backward(sb)
+        else:
+            x = self._decode(sb)
+            with torch.autocast("cuda", dtype=torch.bfloat16):
+                logits = self.model(x, sb, self.caps, self.pick_cap)
+            loss = softmax_ce(logits.contiguous(), self.labels, sb.nodes[0], sb.n_nodes[0],
+                              self.model.num_classes)
+            self.flat_grad.zero_()
+            loss.backward()
+            self.loss_buf.copy_(loss.detach())
         ddp.average_flat_(self.flat_grad, self.pg)
         self.opt.step()
-        self.loss_buf.copy_(loss.detach())
+
+    def forward_backward(self, sb) -> None:
+        """GatModel's loss and every parameter gradient for batch sb, written
+        out (same math as the autograd model, bf16 GEMM operands from the
+        Adam kernel's shadow, fp32 scores / attention / gradients): loss ->
+        loss_buf, gradients -> flat_grad (every element written: no zero
+        fill).  Layer i reads block l = L-1-i; the input layer's sources are
+        the decoded picks (one row per pick).
+
+        forward   c = [a_l . W_k ; a_r . W_k]  (scores el|er = src c^T, one GEMM)
+                  alpha = softmax_v LeakyReLU(el[l_e] + mean_e er[l_e])
+                  input: A = sum_e alpha x_e per head, o = A blockdiag(W_k^T) + b
+                  other: o = sum_e alpha z[l_e] + b,  z = h W^T
+                  h_next = ELU(o); logits = o of the last layer
+        backward  dz, dalpha (agg), ds = [del|der] (softmax), dW = dz^T h
+                  (input: the diagonal blocks of do^T A), dc = ds^T src,
+                  dW += a . dc, d[a_l|a_r] = W . dc, dh = dz W + ds c,
+                  do_prev = ELU'(h) dh"""
+        L = len(self.cfg.fanouts)
+        s = N.stream_handle()
+        dev = self.device
+        f32, bf16 = torch.float32, torch.bfloat16
+        x = self._decode(sb).x  # [pick_cap, d] bf16, pick order
+        saved = []
+        h = x
+        for i, v in enumerate(self._views):
+            l = L - 1 - i
+            Hh, Fh, D = v.heads, v.F, v.D
+            c = torch.bmm(v.attn.permute(1, 0, 2), v.W.view(Hh, Fh, D))     # [Hh, 2, D]
+            c = c.permute(1, 0, 2).reshape(2 * Hh, D)                       # [el | er] rows
+            cb = c.to(bf16)
+            sc = torch.mm(h, cb.t(), out_dtype=f32)                         # [src rows, 2Hh]
+            first = i == 0
+            local = None if first else sb.local[l]
+            e_cap = self.pick_cap if first else sb.local[l].numel()
+            alpha = torch.empty((e_cap, Hh), dtype=f32, device=dev)
+            q = torch.empty((self.caps[l], Hh), dtype=f32, device=dev)
+            N.call("fg_gat_softmax_fwd", N.ptr(sc), N.ptr(sc[:, Hh:]), 2 * Hh,
+                   N.ptr(sb.indptr[l]), N.ptr(local), self.caps[l], N.ptr(sb.n_nodes[l]), Hh,
+                   0.2, N.ptr(alpha), N.ptr(q), s)
+            if first:
+                A = torch.empty((self.caps[l], Hh * D), dtype=bf16, device=dev)
+                N.call("fg_gat_code_xagg_fwd", None, N.ptr(h), None, D, Hh, N.ptr(alpha),
+                       N.ptr(sb.indptr[l]), self.caps[l], N.ptr(sb.n_nodes[l]), N.ptr(A), s)
+                v.refresh_block_diag()
+                o = torch.addmm(v.bb, A, v.wbd)                                # bf16
+                z = A
+            else:
+                z = torch.mm(h, v.Wb.t())                                       # [src rows, Wd]
+                o = torch.empty((self.caps[l], v.width), dtype=f32, device=dev)
+                N.call("fg_gat_agg_fwd", N.ptr(z), v.width, Hh, N.ptr(alpha), N.ptr(sb.indptr[l]),
+                       N.ptr(local), self.caps[l], N.ptr(sb.n_nodes[l]), N.ptr(o), s)
+                o += v.b
+            saved.append((h, c, cb, sc, alpha, q, z, local, e_cap))
+            h = F.elu(o).to(bf16) if i < L - 1 else o
+        logits = h
+        C, ld = self.model.num_classes, logits.shape[1]
+        do = torch.empty_like(logits)
+        row_loss = torch.empty(logits.shape[0], dtype=f32, device=dev)
+        N.call("fg_softmax_ce", N.ptr(logits), 0, C, ld, logits.shape[0], N.ptr(sb.n_nodes[0]),
+               N.ptr(self.labels), N.ptr(sb.nodes[0]), N.ptr(do), N.ptr(row_loss),
+               N.ptr(self.loss_buf), N.ptr(self.ce_ctr), s)
+        # ---- backward
+        for i in range(L - 1, -1, -1):
+            v = self._views[i]
+            l = L - 1 - i
+            Hh, Fh, D = v.heads, v.F, v.D
+            h, c, cb, sc, alpha, q, z, local, e_cap = saved[i]
+            torch.sum(do, 0, dtype=f32, out=v.db)
+            ds = torch.zeros((h.shape[0], 2 * Hh), dtype=f32, device=dev)
+            if i == 0:
+                A = z
+                dA = torch.mm(do, v.wbd.t())                                    # [N, Hh*D] bf16
+                # dW_k = do_k^T A_k: the diagonal blocks only (strided batched GEMM)
+                dWk = torch.bmm(do.view(-1, Hh, Fh).permute(1, 2, 0),
+                                A.view(-1, Hh, D).permute(1, 0, 2))
+                v.dW.view(Hh, Fh, D).copy_(dWk)
+                dalpha = torch.empty((e_cap, Hh), dtype=f32, device=dev)
+                N.call("fg_gat_code_xagg_bwd", None, N.ptr(h), None, D, Hh, N.ptr(sb.indptr[l]),
+                       self.caps[l], N.ptr(sb.n_nodes[l]), N.ptr(dA), N.ptr(dalpha), s)
+                N.call("fg_gat_softmax_bwd", N.ptr(sc), 2 * Hh, N.ptr(q), N.ptr(alpha),
+                       N.ptr(dalpha), N.ptr(sb.indptr[l]), None, self.caps[l],
+                       N.ptr(sb.n_nodes[l]), Hh, 0.2, N.ptr(ds), N.ptr(ds[:, Hh:]), s)
+                nb = N.lib().fg_gat_code_scores_bwd_blocks(e_cap)
+                part = torch.empty((nb, 2 * Hh, D), dtype=f32, device=dev)
+                N.call("fg_gat_code_scores_bwd", None, N.ptr(h), None, N.ptr(sb.n_picks[l]), e_cap,
+                       D, Hh, N.ptr(ds), N.ptr(ds[:, Hh:]), 2 * Hh, N.ptr(part), s)
+                dc = part.sum(0)
+            else:
+                dz = torch.zeros((h.shape[0], v.width), dtype=f32, device=dev)
+                dalpha = torch.zeros((e_cap, Hh), dtype=f32, device=dev)
+                N.call("fg_gat_agg_bwd", N.ptr(z), v.width, Hh, N.ptr(alpha), N.ptr(sb.indptr[l]),
+                       N.ptr(local), self.caps[l], N.ptr(sb.n_nodes[l]), N.ptr(do), N.ptr(dz),
+                       N.ptr(dalpha), s)
+                N.call("fg_gat_softmax_bwd", N.ptr(sc), 2 * Hh, N.ptr(q), N.ptr(alpha),
+                       N.ptr(dalpha), N.ptr(sb.indptr[l]), N.ptr(local), self.caps[l],
+                       N.ptr(sb.n_nodes[l]), Hh, 0.2, N.ptr(ds), N.ptr(ds[:, Hh:]), s)
+                dzb, dsb = dz.to(bf16), ds.to(bf16)
+                torch.mm(dzb.t(), h, out_dtype=f32, out=v.dW)
+                dc = torch.mm(dsb.t(), h, out_dtype=f32)                      # [2Hh, D]
+            dcv = dc.view(2, Hh, D).permute(1, 0, 2)                            # [Hh, 2, D]
+            # d[a_l | a_r][k, f] = <W[kF+f], dc[el|er row k]>;  dW += a . dc
+            v.dattn.copy_(torch.bmm(v.W.view(Hh, Fh, D), dcv.transpose(1, 2)).permute(2, 0, 1))
+            v.dW.view(Hh, Fh, D).baddbmm_(v.attn.permute(1, 2, 0), dcv)
+            if i == 0:
+                break
+            dh = torch.addmm(torch.mm(dzb, v.Wb), dsb, cb)                      # [src rows, D] bf16
+            # ELU'(o) from its output h: 1 where h > 0, h + 1 elsewhere
+            do = torch.ops.aten.elu_backward(dh, 1.0, 1.0, 1.0, True, h)
+            if i - 1 > 0:
+                do = do.float()
 
     def begin_epoch(self, train_ids, epoch: int = 0) -> int:
         r = torch.distributed.get_rank(self.pg) if self.world > 1 else 0

@@ -229,11 +229,14 @@ class SageTrainer:
         self.relu_bits = None
         if fused:
             self.wgrad_scratch = wgrad_scratch(w0.shape[0], w0.shape[1], self.device)
-            # h0's packed ReLU mask, written by the first block mean's forward
-            # (FG_RELU_BITS=0: the wgrad kernel reads h0 itself)
-            if os.environ.get("FG_RELU_BITS", "1") != "0":
-                self.relu_bits = torch.empty((self.caps[L - 1], w0.shape[0] // 8),
-                                             dtype=torch.uint8, device=self.device)
+        # h0's packed ReLU mask, written by the first block mean's forward and
+        # read by the dW0 kernel or, on the GEMM path (MAG: P > 256), by the
+        # block-mean backward instead of the bf16 h0 rows (FG_RELU_BITS=0:
+        # the backward reads h0 itself)
+        if (self.explicit and L > 1 and w0.shape[0] % 8 == 0
+                and os.environ.get("FG_RELU_BITS", "1") != "0"):
+            self.relu_bits = torch.empty((self.caps[L - 1], w0.shape[0] // 8),
+                                         dtype=torch.uint8, device=self.device)
         # forward: input projection fused with the first block mean
         # (fg_infwd.cu) when the shape allows -- mean aggregator only (products
         # step 0.258 -> 0.247 ms; GCN's weighted variant measured no gain);
@@ -310,7 +313,7 @@ class SageTrainer:
                 l = L - 2 - i  # block feeding layer i+1
                 H = h.shape[1]
                 a = torch.empty((caps[l], H + 8), dtype=torch.bfloat16, device=self.device)
-                if fused and i == 0 and self.relu_bits is not None:
+                if i == 0 and self.relu_bits is not None:
                     # h0's ReLU mask as bits for the edge-tiled dW0 (mask_kind 2)
                     N.call("fg_block_mean_fwd_bits", N.ptr(h), H, N.ptr(sb.indptr[l]),
                            N.ptr(sb.local[l]), N.ptr(sb.n_nodes[l]), caps[l], N.ptr(a), H + 8,
@@ -344,8 +347,13 @@ class SageTrainer:
                 break
             t_indptr, t_dst, t_w, n_src = sb.trans[l]
             dh = torch.empty_like(hs[i - 1])
-            N.call("fg_block_mean_bwd_t", N.ptr(din), H, H, N.ptr(t_indptr), N.ptr(t_dst),
-                   N.ptr(t_w), N.ptr(n_src), dh.shape[0], N.ptr(hs[i - 1]), N.ptr(dh), s)
+            if i == 1 and self.relu_bits is not None:
+                N.call("fg_block_mean_bwd_t_bits", N.ptr(din), H, H, N.ptr(t_indptr),
+                       N.ptr(t_dst), N.ptr(t_w), N.ptr(n_src), dh.shape[0],
+                       N.ptr(self.relu_bits), N.ptr(dh), s)
+            else:
+                N.call("fg_block_mean_bwd_t", N.ptr(din), H, H, N.ptr(t_indptr), N.ptr(t_dst),
+                       N.ptr(t_w), N.ptr(n_src), dh.shape[0], N.ptr(hs[i - 1]), N.ptr(dh), s)
         ddp.average_flat_(self.flat_grad, self.pg)
         self.opt.step()
 

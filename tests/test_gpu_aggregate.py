@@ -188,6 +188,34 @@ def test_hidden_block_mean_gather_backward(relu):
     assert torch.allclose(h.grad.float(), hf.grad, atol=2e-2, rtol=1e-2)
 
 
+@pytest.mark.parametrize("H", [64, 256])
+def test_block_mean_bwd_t_relu_bits_matches_h_mask(H):
+    """fg_block_mean_bwd_t_bits (packed ReLU bits, the MAG GEMM path's dh0)
+    equals fg_block_mean_bwd_t with the bf16 h rows as the mask, bit for bit."""
+    from paper_2207_14696_b200 import _native as N
+    from paper_2207_14696_b200.aggregate import relu_mask_bits
+    rng = np.random.default_rng(H)
+    n_src, n_dst, max_dst = 4000, 900, 1000
+    counts, indptr, src = _block(n_src, n_dst, max_dst, 9, rng)
+    ti, td, tw = _transpose_np(indptr, src, n_dst, n_src)
+    dev = "cuda"
+    h = torch.randn(n_src, H, device=dev).to(torch.bfloat16)
+    g = torch.randn(max_dst, H, device=dev).to(torch.bfloat16)
+    bits = relu_mask_bits(h)
+    t = [torch.from_numpy(x).to(dev) for x in (ti, td, tw)]
+    ns = torch.tensor([n_src - 7], device=dev)   # padded rows past the live sources
+    a = torch.full((n_src, H), 7.0, device=dev).to(torch.bfloat16)
+    b = torch.full_like(a, -7.0)
+    s = N.stream_handle()
+    N.call("fg_block_mean_bwd_t", N.ptr(g), H, H, N.ptr(t[0]), N.ptr(t[1]), N.ptr(t[2]),
+           N.ptr(ns), n_src, N.ptr(h), N.ptr(a), s)
+    N.call("fg_block_mean_bwd_t_bits", N.ptr(g), H, H, N.ptr(t[0]), N.ptr(t[1]), N.ptr(t[2]),
+           N.ptr(ns), n_src, N.ptr(bits), N.ptr(b), s)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    assert (a[n_src - 7:] == 0).all()
+
+
 def test_block_transpose_kernel():
     from paper_2207_14696_b200 import _native as N
     rng = np.random.default_rng(8)

@@ -183,3 +183,17 @@ def test_gat_gradients_match_cpu_oracle_model(codec_kind, decoded):
         assert g_ref is not None and g_ref.norm() > 0, name
         rel = ((g - g_ref).norm() / g_ref.norm()).item()
         assert rel < 1e-1, (name, rel)  # bf16 autocast vs fp32
+    if decoded:
+        # the trainer's explicit step (no autograd) on the same batch: same
+        # loss, same gradient for every parameter, written into flat_grad
+        t.flat_grad.fill_(float("nan"))   # every element must be written
+        t.forward_backward(sb)
+        torch.cuda.synchronize()
+        assert abs(float(t.loss_buf) - float(loss_c)) < 2e-2 * abs(float(loss_c))
+        assert torch.isfinite(t.flat_grad).all()
+        for name, p in cpu_model.named_parameters():
+            q = gpu_grads[name]
+            off = (q.data_ptr() - t.flat_param.data_ptr()) // 4
+            g = t.flat_grad[off:off + q.numel()].view(q.shape).cpu()
+            rel = ((g - p.grad).norm() / p.grad.norm()).item()
+            assert rel < 5e-2, ("explicit", name, rel)
