@@ -427,10 +427,43 @@ int fg_gat_code_scores_bwd(const fg_codec_desc* codec, const uint16_t* x_rows,
                            const int32_t* picks, const int64_t* n_picks_dev, int64_t e_cap,
                            int64_t d, int heads, const float* del, const float* der,
                            int64_t score_ld, float* partial, void* cuda_stream);
+/* out row pitch out_ld (0 = heads*d); columns heads*d .. out_ld-1 get
+ * [1, 0, ...]: a ones column that carries the projection's bias (a bias row
+ * in the weight) and yields the bias gradient from the weight-gradient GEMM */
 int fg_gat_code_xagg_fwd(const fg_codec_desc* codec, const uint16_t* x_rows,
                          const int32_t* picks, int64_t d, int heads, const float* alpha,
                          const int32_t* indptr, int64_t max_dst, const int64_t* n_dst_dev,
-                         uint16_t* out, void* cuda_stream);
+                         uint16_t* out, int64_t out_ld, void* cuda_stream);
+/* Fused GAT input layer over the decoded picks x [E, d] (bf16, row e = pick
+ * e; each pick belongs to one destination), heads in {1, 2, 4, 8}, d <= 256,
+ * c = [a_l . W_k ; a_r . W_k] fp32 [2 heads, d]:
+ *   fg_gat_input_attn_fwd  scores[e] = [el | er] = x_e c^T (fp32 [E, 2 heads]),
+ *                          q, alpha as fg_gat_softmax_fwd, and
+ *                          out[v, k*d + j] = sum_e alpha[e,k] x[e,j] (bf16, row
+ *                          pitch out_ld, columns past heads*d = [1, 0..]; rows
+ *                          max_dst..rows-1 zero) -- one pass over x;
+ *   fg_gat_input_attn_bwd  from dA (bf16 [max_dst, heads*d]): dalpha (scratch
+ *                          [E, heads]), the softmax backward and
+ *                          partial[b] = sum_{e in CTA b} [del | der]_e x_e
+ *                          (fp32 [fg_gat_input_attn_bwd_blocks()][2 heads][d],
+ *                          summed by the caller; deterministic). */
+int fg_gat_input_attn_fwd(const uint16_t* x, int64_t d, int heads, const float* c,
+                          const int32_t* indptr, int64_t max_dst, int64_t rows,
+                          const int64_t* n_dst_dev, float slope, float* scores, float* alpha,
+                          float* q, uint16_t* out, int64_t out_ld, void* cuda_stream);
+int64_t fg_gat_input_attn_bwd_blocks(void);
+int fg_gat_input_attn_bwd(const uint16_t* x, int64_t d, int heads, const float* scores,
+                          const float* alpha, const float* q, const uint16_t* dA,
+                          const int32_t* indptr, int64_t max_dst, const int64_t* n_dst_dev,
+                          float slope, float* dalpha, float* partial, void* cuda_stream);
+/* ELU between GAT layers: h = bf16(ELU(in + bias)) for in fp32 (in_f32 = 1)
+ * or bf16 rows of pitch ld_in, bias fp32 [cols] or NULL (cols % 8 == 0); and
+ * out = dh * ELU'(.) from the forward's output h (1 where h > 0, h + 1
+ * elsewhere), n elements (n % 8 == 0), fp32 (out_f32 = 1) or bf16 out. */
+int fg_gat_elu_fwd(const void* in, int in_f32, int64_t ld_in, const float* bias, int64_t rows,
+                   int64_t cols, uint16_t* out, void* cuda_stream);
+int fg_gat_elu_bwd(const uint16_t* dh, const uint16_t* h, int64_t n, void* out, int out_f32,
+                   void* cuda_stream);
 int fg_gat_code_xagg_bwd(const fg_codec_desc* codec, const uint16_t* x_rows,
                          const int32_t* picks, int64_t d, int heads, const int32_t* indptr,
                          int64_t max_dst, const int64_t* n_dst_dev, const uint16_t* dA,

@@ -428,13 +428,18 @@ template <int HEADS, int XI, int KIND>
 __global__ void __launch_bounds__(256)
 k_gat_code_xagg_fwd(GatCodes cd, int d, const float* __restrict__ alpha,
                     const int32_t* __restrict__ indptr, int64_t max_dst,
-                    const int64_t* __restrict__ ndst_dev, __nv_bfloat16* __restrict__ out) {
+                    const int64_t* __restrict__ ndst_dev, __nv_bfloat16* __restrict__ out,
+                    int64_t out_ld) {
   constexpr int heads = HEADS;
   const int64_t live = min64(*ndst_dev, max_dst);
   const int lane = threadIdx.x & 31;
   for (int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; v < max_dst;
        v += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    __nv_bfloat16* o = out + v * (int64_t)heads * d;
+    __nv_bfloat16* o = out + v * out_ld;
+    // columns past heads*d: [1, 0, ...] (the projection's bias row / the
+    // weight gradient's bias column)
+    for (int64_t j = (int64_t)heads * d + lane; j < out_ld; j += 32)
+      o[j] = __float2bfloat16_rn(j == (int64_t)heads * d ? 1.f : 0.f);
     const int32_t e0 = v < live ? indptr[v] : 0, e1 = v < live ? indptr[v + 1] : 0;
     float acc[XI][HEADS];
 #pragma unroll
@@ -625,7 +630,10 @@ extern "C" int fg_gat_code_scores_bwd(const fg_codec_desc* codec, const uint16_t
 extern "C" int fg_gat_code_xagg_fwd(const fg_codec_desc* codec, const uint16_t* x_rows,
                                     const int32_t* picks, int64_t d, int heads,
                                     const float* alpha, const int32_t* indptr, int64_t max_dst,
-                                    const int64_t* n_dst_dev, uint16_t* out, void* s) {
+                                    const int64_t* n_dst_dev, uint16_t* out, int64_t out_ld,
+                                    void* s) {
+  if (out_ld == 0) out_ld = heads * d;
+  FG_CHECK_ARG(out_ld >= heads * d, "fg_gat_code_xagg_fwd: out_ld < heads * d");
   FG_CHECK_ARG(gat_codes_ok(codec, x_rows) && alpha && indptr && n_dst_dev && out &&
                    (heads == 1 || heads == 2 || heads == 4 || heads == 8) && d >= 1 &&
                    d <= 32 * fg::kXI,
@@ -639,10 +647,12 @@ extern "C" int fg_gat_code_xagg_fwd(const fg_codec_desc* codec, const uint16_t* 
   do {                                                                                    \
     if (g.kind == 0)                                                                      \
       fg::k_gat_code_xagg_fwd<H, XI, 0><<<grid, 256, 0, st>>>(g, (int)d, alpha, indptr,   \
-                                                              max_dst, n_dst_dev, ob);    \
+                                                              max_dst, n_dst_dev, ob,     \
+                                                              out_ld);                    \
     else                                                                                  \
       fg::k_gat_code_xagg_fwd<H, XI, -1><<<grid, 256, 0, st>>>(g, (int)d, alpha, indptr,  \
-                                                               max_dst, n_dst_dev, ob);   \
+                                                               max_dst, n_dst_dev, ob,    \
+                                                               out_ld);                   \
   } while (0)
   const bool small = d <= 128;
   switch (heads) {
@@ -687,6 +697,424 @@ extern "C" int fg_gat_code_xagg_bwd(const fg_codec_desc* codec, const uint16_t* 
     default: if (small) FG_XAGG_BWD(8, 4); else FG_XAGG_BWD(8, 8); break;
   }
 #undef FG_XAGG_BWD
+  FG_LAUNCH_CHECK();
+  return FG_OK;
+}
+
+// ------------------------------------------------ ELU between GAT layers
+// forward: h = bf16(ELU(o + bias)) (o fp32 or bf16, row pitch ld_in; bias
+// fp32 [cols] or NULL); backward: do = dh * ELU'(.) computed from the
+// output h (1 where h > 0, h + 1 elsewhere), fp32 or bf16 out.  8 columns
+// per thread (cols % 8 == 0).
+namespace fg {
+template <bool IN_F32>
+__global__ void k_gat_elu_fwd(const void* __restrict__ in, int64_t ld_in,
+                              const float* __restrict__ bias, int64_t rows, int64_t cols,
+                              uint16_t* __restrict__ out) {
+  const int64_t ch = cols >> 3;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < rows * ch;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = t / ch, c = (t - r * ch) * 8;
+    float f[8];
+    if (IN_F32) {
+      const float4* p = reinterpret_cast<const float4*>(static_cast<const float*>(in) + r * ld_in + c);
+      const float4 a = p[0], b = p[1];
+      f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+    } else {
+      ld8(static_cast<const __nv_bfloat16*>(in) + r * ld_in + c, f);
+    }
+    if (bias) {
+      const float4 a = reinterpret_cast<const float4*>(bias + c)[0];
+      const float4 b = reinterpret_cast<const float4*>(bias + c)[1];
+      f[0] += a.x; f[1] += a.y; f[2] += a.z; f[3] += a.w;
+      f[4] += b.x; f[5] += b.y; f[6] += b.z; f[7] += b.w;
+    }
+    uint32_t w[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float x0 = f[2 * i] > 0.f ? f[2 * i] : expm1f(f[2 * i]);
+      const float x1 = f[2 * i + 1] > 0.f ? f[2 * i + 1] : expm1f(f[2 * i + 1]);
+      const __nv_bfloat162 h = __floats2bfloat162_rn(x0, x1);
+      w[i] = *reinterpret_cast<const uint32_t*>(&h);
+    }
+    reinterpret_cast<uint4*>(out + r * cols + c)[0] = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+template <bool OUT_F32>
+__global__ void k_gat_elu_bwd(const __nv_bfloat16* __restrict__ dh,
+                              const __nv_bfloat16* __restrict__ h, int64_t n8,
+                              void* __restrict__ out) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n8;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    float g[8], y[8];
+    ld8(dh + t * 8, g);
+    ld8(h + t * 8, y);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) g[i] = y[i] > 0.f ? g[i] : g[i] * (y[i] + 1.f);
+    if (OUT_F32) {
+      float4* o = reinterpret_cast<float4*>(static_cast<float*>(out) + t * 8);
+      o[0] = make_float4(g[0], g[1], g[2], g[3]);
+      o[1] = make_float4(g[4], g[5], g[6], g[7]);
+    } else {
+      uint32_t w[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const __nv_bfloat162 b = __floats2bfloat162_rn(g[2 * i], g[2 * i + 1]);
+        w[i] = *reinterpret_cast<const uint32_t*>(&b);
+      }
+      reinterpret_cast<uint4*>(static_cast<uint16_t*>(out) + t * 8)[0] =
+          make_uint4(w[0], w[1], w[2], w[3]);
+    }
+  }
+}
+}  // namespace fg
+
+extern "C" int fg_gat_elu_fwd(const void* in, int in_f32, int64_t ld_in, const float* bias,
+                              int64_t rows, int64_t cols, uint16_t* out, void* s) {
+  FG_CHECK_ARG(in && out && cols % 8 == 0 && ld_in >= cols && ld_in % 8 == 0,
+               "fg_gat_elu_fwd: bad argument (cols, ld_in multiples of 8)");
+  FG_CHECK_ARG((uintptr_t)in % 16 == 0 && (uintptr_t)out % 16 == 0 &&
+                   (uintptr_t)bias % 16 == 0, "fg_gat_elu_fwd: pointers must be 16-byte aligned");
+  if (rows == 0) return FG_OK;
+  const int64_t total = rows * (cols / 8);
+  if (in_f32)
+    fg::k_gat_elu_fwd<true><<<grid_for(total, 256), 256, 0, as_stream(s)>>>(
+        in, ld_in, bias, rows, cols, out);
+  else
+    fg::k_gat_elu_fwd<false><<<grid_for(total, 256), 256, 0, as_stream(s)>>>(
+        in, ld_in, bias, rows, cols, out);
+  FG_LAUNCH_CHECK();
+  return FG_OK;
+}
+
+extern "C" int fg_gat_elu_bwd(const uint16_t* dh, const uint16_t* h, int64_t n, void* out,
+                              int out_f32, void* s) {
+  FG_CHECK_ARG(dh && h && out && n % 8 == 0, "fg_gat_elu_bwd: bad argument (n % 8)");
+  FG_CHECK_ARG((uintptr_t)dh % 16 == 0 && (uintptr_t)h % 16 == 0 && (uintptr_t)out % 16 == 0,
+               "fg_gat_elu_bwd: pointers must be 16-byte aligned");
+  if (n == 0) return FG_OK;
+  const auto* dhb = reinterpret_cast<const __nv_bfloat16*>(dh);
+  const auto* hb = reinterpret_cast<const __nv_bfloat16*>(h);
+  if (out_f32)
+    fg::k_gat_elu_bwd<true><<<grid_for(n / 8, 256), 256, 0, as_stream(s)>>>(dhb, hb, n / 8, out);
+  else
+    fg::k_gat_elu_bwd<false><<<grid_for(n / 8, 256), 256, 0, as_stream(s)>>>(dhb, hb, n / 8, out);
+  FG_LAUNCH_CHECK();
+  return FG_OK;
+}
+
+// ------------------------------------------------ fused input-layer attention
+// The input layer's sources are the decoded picks (row e = pick e, each pick
+// belongs to exactly one destination), so a warp that owns destination v owns
+// every row its attention touches.  Forward: per pick the 2H scores
+// x_e . c[q] (one 9-shuffle transpose-reduce for 2H = 8), q = mean er, the
+// per-head softmax of LeakyReLU(el + q), and A[v] = sum_e alpha x_e -- one
+// pass over x instead of a score GEMM + softmax + aggregation (three).
+// Backward: dalpha = <dA[v, head], x_e>, the softmax backward within the
+// warp, and dc = sum_e [del | der]_e x_e accumulated in registers (per-CTA
+// partials in fixed warp order; deterministic).
+namespace fg {
+// After tr_reduce<V>, lane L holds the warp total of pv[tr_index<V>(L)]
+// (V a power of two <= 32): log2(V) halving exchanges at offsets 16, 8, ...,
+// then a plain butterfly over the remaining offsets.
+template <int V>
+__device__ __forceinline__ float tr_reduce(float (&pv)[V], int lane) {
+  int off = 16;
+#pragma unroll
+  for (int n = V; n > 1; n >>= 1, off >>= 1) {
+    const bool upper = (lane & off) != 0;
+#pragma unroll
+    for (int i = 0; i < n / 2; ++i) {
+      const float send = upper ? pv[i] : pv[i + n / 2];
+      const float keep = upper ? pv[i + n / 2] : pv[i];
+      pv[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+  float r = pv[0];
+#pragma unroll
+  for (; off >= 1; off >>= 1) r += __shfl_xor_sync(0xffffffffu, r, off);
+  return r;
+}
+template <int V>
+__device__ __forceinline__ int tr_index(int lane) {
+  int idx = 0, off = 16;
+#pragma unroll
+  for (int n = V; n > 1; n >>= 1, off >>= 1) idx = (idx << 1) | ((lane & off) ? 1 : 0);
+  return idx;
+}
+template <int V>
+__device__ __forceinline__ int tr_lane(int idx) {  // the lowest lane holding idx
+  int lane = 0, off = 16, b = 0;
+  for (int n = V; n > 2; n >>= 1) ++b;  // b = log2(V) - 1
+#pragma unroll
+  for (int n = V; n > 1; n >>= 1, off >>= 1, --b)
+    if ((idx >> b) & 1) lane |= off;
+  return lane;
+}
+
+template <int XI>
+__device__ __forceinline__ void load_row(const __nv_bfloat16* __restrict__ xr, int d, int lane,
+                                         float (&xv)[XI]) {
+#pragma unroll
+  for (int i = 0; i < XI; ++i) {
+    const int j = lane + 32 * i;
+    xv[i] = j < d ? __bfloat162float(xr[j]) : 0.f;
+  }
+}
+
+template <int HEADS, int XI>
+__global__ void __launch_bounds__(256)
+k_gat_input_attn_fwd(const __nv_bfloat16* __restrict__ x, int d, const float* __restrict__ c,
+                     const int32_t* __restrict__ indptr, int64_t max_dst, int64_t rows,
+                     const int64_t* __restrict__ ndst_dev, float slope, float* __restrict__ sc,
+                     float* __restrict__ alpha, float* __restrict__ q,
+                     __nv_bfloat16* __restrict__ out, int64_t out_ld) {
+  constexpr int V = 2 * HEADS;
+  const int64_t live = min64(*ndst_dev, max_dst);
+  const int lane = threadIdx.x & 31;
+  const int my = tr_index<V>(lane);
+  const bool writer = (lane & (32 / V - 1)) == 0;
+  float cr[V][XI];
+#pragma unroll
+  for (int s = 0; s < V; ++s)
+#pragma unroll
+    for (int i = 0; i < XI; ++i) {
+      const int j = lane + 32 * i;
+      cr[s][i] = j < d ? __ldg(c + s * d + j) : 0.f;
+    }
+  for (int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; v < rows;
+       v += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    __nv_bfloat16* o = out + v * out_ld;
+    for (int64_t j = (int64_t)HEADS * d + lane; j < out_ld; j += 32)
+      o[j] = __float2bfloat16_rn(j == (int64_t)HEADS * d ? 1.f : 0.f);
+    const int32_t e0 = v < live ? indptr[v] : 0, e1 = v < live ? indptr[v + 1] : 0;
+    float acc[XI][HEADS];
+#pragma unroll
+    for (int i = 0; i < XI; ++i)
+#pragma unroll
+      for (int k = 0; k < HEADS; ++k) acc[i][k] = 0.f;
+    if (e1 > e0) {
+      // pass 1: scores [el | er] per pick, er summed for the query
+      float qacc = 0.f;
+      for (int32_t e = e0; e < e1; ++e) {
+        float xv[XI], pv[V];
+        load_row<XI>(x + (int64_t)e * d, d, lane, xv);
+#pragma unroll
+        for (int s = 0; s < V; ++s) {
+          float t = 0.f;
+#pragma unroll
+          for (int i = 0; i < XI; ++i) t = fmaf(xv[i], cr[s][i], t);
+          pv[s] = t;
+        }
+        const float r = tr_reduce<V>(pv, lane);
+        if (writer) sc[(int64_t)e * V + my] = r;
+        if (my >= HEADS) qacc += r;
+      }
+      __syncwarp();
+      const float rc = 1.f / (float)(e1 - e0);
+      float qk[HEADS], mx[HEADS], inv[HEADS];
+#pragma unroll
+      for (int k = 0; k < HEADS; ++k) {
+        qk[k] = __shfl_sync(0xffffffffu, qacc, tr_lane<V>(HEADS + k)) * rc;
+        mx[k] = -INFINITY;
+        inv[k] = 0.f;
+      }
+      for (int32_t e = e0; e < e1; ++e)
+#pragma unroll
+        for (int k = 0; k < HEADS; ++k)
+          mx[k] = fmaxf(mx[k], leaky(sc[(int64_t)e * V + k] + qk[k], slope));
+      for (int32_t e = e0; e < e1; ++e)
+#pragma unroll
+        for (int k = 0; k < HEADS; ++k)
+          inv[k] += __expf(leaky(sc[(int64_t)e * V + k] + qk[k], slope) - mx[k]);
+#pragma unroll
+      for (int k = 0; k < HEADS; ++k) {
+        inv[k] = 1.f / inv[k];
+        if (lane == k) q[v * HEADS + k] = qk[k];
+      }
+      // pass 2: alpha and the per-head weighted sums of the pick rows
+      for (int32_t e = e0; e < e1; ++e) {
+        float al[HEADS], xv[XI];
+#pragma unroll
+        for (int k = 0; k < HEADS; ++k) {
+          al[k] = __expf(leaky(sc[(int64_t)e * V + k] + qk[k], slope) - mx[k]) * inv[k];
+          if (lane == k) alpha[(int64_t)e * HEADS + k] = al[k];
+        }
+        load_row<XI>(x + (int64_t)e * d, d, lane, xv);
+#pragma unroll
+        for (int i = 0; i < XI; ++i)
+#pragma unroll
+          for (int k = 0; k < HEADS; ++k) acc[i][k] = fmaf(al[k], xv[i], acc[i][k]);
+      }
+    } else if (v < max_dst && lane < HEADS) {
+      q[v * HEADS + lane] = 0.f;
+    }
+#pragma unroll
+    for (int k = 0; k < HEADS; ++k)
+#pragma unroll
+      for (int i = 0; i < XI; ++i) {
+        const int j = lane + 32 * i;
+        if (j < d) o[k * d + j] = __float2bfloat16_rn(acc[i][k]);
+      }
+  }
+}
+
+template <int HEADS, int XI>
+__global__ void __launch_bounds__(256)
+k_gat_input_attn_bwd(const __nv_bfloat16* __restrict__ x, int d, const float* __restrict__ sc,
+                     const float* __restrict__ alpha, const float* __restrict__ q,
+                     const __nv_bfloat16* __restrict__ dA, const int32_t* __restrict__ indptr,
+                     int64_t max_dst, const int64_t* __restrict__ ndst_dev, float slope,
+                     float* __restrict__ dalpha, float* __restrict__ partial) {
+  constexpr int V = 2 * HEADS;
+  extern __shared__ float s_dc[];  // [V][d]
+  const int64_t live = min64(*ndst_dev, max_dst);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int my = tr_index<HEADS>(lane);
+  const bool writer = (lane & (32 / HEADS - 1)) == 0;
+  float dc[V][XI];
+#pragma unroll
+  for (int s = 0; s < V; ++s)
+#pragma unroll
+    for (int i = 0; i < XI; ++i) dc[s][i] = 0.f;
+  for (int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; v < live;
+       v += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int32_t e0 = indptr[v], e1 = indptr[v + 1];
+    if (e1 == e0) continue;
+    float g[HEADS][XI];
+#pragma unroll
+    for (int k = 0; k < HEADS; ++k)
+#pragma unroll
+      for (int i = 0; i < XI; ++i) {
+        const int j = lane + 32 * i;
+        g[k][i] = j < d ? __bfloat162float(dA[(v * HEADS + k) * (int64_t)d + j]) : 0.f;
+      }
+    for (int32_t e = e0; e < e1; ++e) {  // dalpha[e, k] = <dA[v, k], x_e>
+      float xv[XI], pv[HEADS];
+      load_row<XI>(x + (int64_t)e * d, d, lane, xv);
+#pragma unroll
+      for (int k = 0; k < HEADS; ++k) {
+        float t = 0.f;
+#pragma unroll
+        for (int i = 0; i < XI; ++i) t = fmaf(g[k][i], xv[i], t);
+        pv[k] = t;
+      }
+      const float r = tr_reduce<HEADS>(pv, lane);
+      if (writer) dalpha[(int64_t)e * HEADS + my] = r;
+    }
+    __syncwarp();
+    float qk[HEADS], dot[HEADS], share[HEADS];
+#pragma unroll
+    for (int k = 0; k < HEADS; ++k) {
+      qk[k] = q[v * HEADS + k];
+      dot[k] = 0.f;
+      share[k] = 0.f;
+    }
+    for (int32_t e = e0; e < e1; ++e)
+#pragma unroll
+      for (int k = 0; k < HEADS; ++k)
+        dot[k] = fmaf(alpha[(int64_t)e * HEADS + k], dalpha[(int64_t)e * HEADS + k], dot[k]);
+    for (int32_t e = e0; e < e1; ++e)
+#pragma unroll
+      for (int k = 0; k < HEADS; ++k) {
+        const float ds = alpha[(int64_t)e * HEADS + k] * (dalpha[(int64_t)e * HEADS + k] - dot[k]);
+        share[k] += sc[(int64_t)e * V + k] + qk[k] > 0.f ? ds : slope * ds;
+      }
+    const float rc = 1.f / (float)(e1 - e0);
+#pragma unroll
+    for (int k = 0; k < HEADS; ++k) share[k] *= rc;
+    for (int32_t e = e0; e < e1; ++e) {  // dc += [del | der]_e x_e
+      float xv[XI], dl[HEADS];
+#pragma unroll
+      for (int k = 0; k < HEADS; ++k) {
+        const float ds = alpha[(int64_t)e * HEADS + k] * (dalpha[(int64_t)e * HEADS + k] - dot[k]);
+        dl[k] = sc[(int64_t)e * V + k] + qk[k] > 0.f ? ds : slope * ds;
+      }
+      load_row<XI>(x + (int64_t)e * d, d, lane, xv);
+#pragma unroll
+      for (int i = 0; i < XI; ++i)
+#pragma unroll
+        for (int k = 0; k < HEADS; ++k) {
+          dc[k][i] = fmaf(dl[k], xv[i], dc[k][i]);
+          dc[HEADS + k][i] = fmaf(share[k], xv[i], dc[HEADS + k][i]);
+        }
+    }
+  }
+  // CTA partial in fixed warp order
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+    if (warp == w)
+#pragma unroll
+      for (int s = 0; s < V; ++s)
+#pragma unroll
+        for (int i = 0; i < XI; ++i) {
+          const int j = lane + 32 * i;
+          if (j < d) s_dc[s * d + j] = (w == 0 ? 0.f : s_dc[s * d + j]) + dc[s][i];
+        }
+    __syncthreads();
+  }
+  for (int t = threadIdx.x; t < V * d; t += blockDim.x)
+    partial[(int64_t)blockIdx.x * V * d + t] = s_dc[t];
+}
+}  // namespace fg
+
+extern "C" int64_t fg_gat_input_attn_bwd_blocks(void) { return 2 * sm_count(); }
+
+extern "C" int fg_gat_input_attn_fwd(const uint16_t* x, int64_t d, int heads, const float* c,
+                                     const int32_t* indptr, int64_t max_dst, int64_t rows,
+                                     const int64_t* n_dst_dev, float slope, float* scores,
+                                     float* alpha, float* q, uint16_t* out, int64_t out_ld,
+                                     void* s) {
+  FG_CHECK_ARG(x && c && indptr && n_dst_dev && scores && alpha && q && out && rows >= max_dst &&
+                   (heads == 1 || heads == 2 || heads == 4 || heads == 8) && d >= 1 && d <= 256,
+               "fg_gat_input_attn_fwd: bad argument (heads in {1,2,4,8}, d <= 256)");
+  if (out_ld == 0) out_ld = heads * d;
+  FG_CHECK_ARG(out_ld >= heads * d, "fg_gat_input_attn_fwd: out_ld < heads * d");
+  if (rows == 0) return FG_OK;
+  const auto* xb = reinterpret_cast<const __nv_bfloat16*>(x);
+  auto* ob = reinterpret_cast<__nv_bfloat16*>(out);
+  const dim3 grid(grid_for(rows * 32, 256));
+  cudaStream_t st = as_stream(s);
+#define FG_IA_FWD(H, XI)                                                                   \
+  fg::k_gat_input_attn_fwd<H, XI><<<grid, 256, 0, st>>>(xb, (int)d, c, indptr, max_dst, rows, \
+                                                        n_dst_dev, slope, scores, alpha, q,  \
+                                                        ob, out_ld)
+  const bool small = d <= 128;
+  switch (heads) {
+    case 1: if (small) FG_IA_FWD(1, 4); else FG_IA_FWD(1, 8); break;
+    case 2: if (small) FG_IA_FWD(2, 4); else FG_IA_FWD(2, 8); break;
+    case 4: if (small) FG_IA_FWD(4, 4); else FG_IA_FWD(4, 8); break;
+    default: if (small) FG_IA_FWD(8, 4); else FG_IA_FWD(8, 8); break;
+  }
+#undef FG_IA_FWD
+  FG_LAUNCH_CHECK();
+  return FG_OK;
+}
+
+extern "C" int fg_gat_input_attn_bwd(const uint16_t* x, int64_t d, int heads,
+                                     const float* scores, const float* alpha, const float* q,
+                                     const uint16_t* dA, const int32_t* indptr, int64_t max_dst,
+                                     const int64_t* n_dst_dev, float slope, float* dalpha,
+                                     float* partial, void* s) {
+  FG_CHECK_ARG(x && scores && alpha && q && dA && indptr && n_dst_dev && dalpha && partial &&
+                   (heads == 1 || heads == 2 || heads == 4 || heads == 8) && d >= 1 && d <= 256,
+               "fg_gat_input_attn_bwd: bad argument (heads in {1,2,4,8}, d <= 256)");
+  const auto* xb = reinterpret_cast<const __nv_bfloat16*>(x);
+  const auto* gb = reinterpret_cast<const __nv_bfloat16*>(dA);
+  const dim3 grid((unsigned)fg_gat_input_attn_bwd_blocks());
+  const size_t smem = (size_t)2 * heads * d * sizeof(float);
+  cudaStream_t st = as_stream(s);
+#define FG_IA_BWD(H, XI)                                                                  \
+  fg::k_gat_input_attn_bwd<H, XI><<<grid, 256, smem, st>>>(xb, (int)d, scores, alpha, q, gb, \
+                                                           indptr, max_dst, n_dst_dev, slope, \
+                                                           dalpha, partial)
+  const bool small = d <= 128;
+  switch (heads) {
+    case 1: if (small) FG_IA_BWD(1, 4); else FG_IA_BWD(1, 8); break;
+    case 2: if (small) FG_IA_BWD(2, 4); else FG_IA_BWD(2, 8); break;
+    case 4: if (small) FG_IA_BWD(4, 4); else FG_IA_BWD(4, 8); break;
+    default: if (small) FG_IA_BWD(8, 4); else FG_IA_BWD(8, 8); break;
+  }
+#undef FG_IA_BWD
   FG_LAUNCH_CHECK();
   return FG_OK;
 }

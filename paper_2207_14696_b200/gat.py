@@ -173,7 +173,7 @@ class GatInputXagg(torch.autograd.Function):
         alpha = alpha.float().contiguous()
         A = torch.empty((max_dst, heads * src.d), dtype=torch.bfloat16, device=alpha.device)
         N.call("fg_gat_code_xagg_fwd", *src.head(), src.d, heads, N.ptr(alpha), N.ptr(indptr),
-               max_dst, N.ptr(n_dst), N.ptr(A), N.stream_handle())
+               max_dst, N.ptr(n_dst), N.ptr(A), 0, N.stream_handle())
         ctx.save_for_backward(indptr, n_dst)
         ctx.src, ctx.max_dst, ctx.heads = src, max_dst, heads
         return A
@@ -275,6 +275,28 @@ class GatModel(nn.Module):
         return h
 
 
+def _round_up(n: int, m: int) -> int:
+    return (n + m - 1) // m * m
+
+
+def _kgemm(a, b, out, chunks: int = 64, min_k: int = 32768):
+    """out [M, N] fp32 = a^T b for bf16 a [K, M], b [K, N].  Past min_k rows
+    K is cut into `chunks` slices multiplied by one batched GEMM (fp32 out)
+    and summed: for K ~ 1e5 with M, N <= 400 cuBLAS's single-GEMM choice (no
+    split-K) runs several times slower.  A K % chunks tail is one more GEMM."""
+    K = a.shape[0]
+    if K < min_k:
+        return torch.mm(a.t(), b, out_dtype=torch.float32, out=out)
+    kc = K // chunks
+    Kc = kc * chunks
+    part = torch.bmm(a[:Kc].view(chunks, kc, -1).transpose(1, 2), b[:Kc].view(chunks, kc, -1),
+                     out_dtype=torch.float32)
+    torch.sum(part, 0, out=out)
+    if Kc < K:
+        out += torch.mm(a[Kc:].t(), b[Kc:], out_dtype=torch.float32)
+    return out
+
+
 class _LayerViews:
     """One GatLayer's parameters as views of the trainer's flat fp32 / bf16
     parameter buffers and flat gradient (attn_l, attn_r adjacent: one [2,
@@ -306,12 +328,15 @@ class _LayerViews:
         self.wbd = None
 
     def refresh_block_diag(self):
+        """wbd [Hh*D + 8, Hh*F]: wbd[k*D + j, k*F + f] = W[k*F + f, j], row
+        Hh*D = the bias (the input's ones column), zeros elsewhere."""
         Hh, F, D = self.heads, self.F, self.D
         if self.wbd is None:
-            self.wbd = torch.zeros((Hh * D, Hh * F), dtype=torch.bfloat16, device=self.W.device)
-        # wbd[k*D + j, k*F + f] = W[k*F + f, j]
-        self.wbd.view(Hh, D, Hh, F).diagonal(dim1=0, dim2=2).copy_(
+            self.wbd = torch.zeros((Hh * D + 8, Hh * F), dtype=torch.bfloat16,
+                                   device=self.W.device)
+        self.wbd[:Hh * D].view(Hh, D, Hh, F).diagonal(dim1=0, dim2=2).copy_(
             self.Wb.view(Hh, F, D).permute(2, 1, 0))
+        self.wbd[Hh * D].copy_(self.bb)
 
 
 @dataclass
@@ -324,13 +349,14 @@ class GatConfig:
     seed: int = 0
     use_graph: bool = True
     explicit: bool = True
+    pipeline: bool = True
 
 
 class GatTrainer:
     """Single-process (or one-rank-of-DDP) GAT trainer over device-resident
-    data: sample -> GAT layers (input layer straight from the picks' code
-    rows) -> fused softmax-CE -> autograd backward into one flat gradient ->
-    flat all-reduce -> flat Adam; one CUDA graph per step."""
+    data: sample (pipelined on a side stream) -> GAT layers (input layer over
+    the decoded picks) -> fused softmax-CE -> explicit backward into one flat
+    gradient -> flat all-reduce -> flat Adam; one CUDA graph per sampler slot."""
 
     def __init__(self, graph, codec, labels, num_classes: int, cfg: GatConfig,
                  process_group=None):
@@ -341,6 +367,18 @@ class GatTrainer:
         torch.manual_seed(cfg.seed)
         L = len(cfg.fanouts)
         self.sampler = DeviceSampler(graph, cfg.fanouts, cfg.batch_size, need_local=True)
+        # pipelined like SageTrainer: batch b+1 is sampled into the other slot
+        # on a side stream while batch b trains (one shared PCG64 stream)
+        self.samplers = [self.sampler]
+        self.pipeline = cfg.pipeline
+        if self.pipeline:
+            self.samplers.append(DeviceSampler(graph, cfg.fanouts, cfg.batch_size,
+                                               need_local=True, share=self.sampler))
+            self.side = torch.cuda.Stream(self.device,
+                                          priority=int(os.environ.get("FG_SIDE_PRIORITY", "-1")))
+        self.graphs = {}
+        self._primed, self._next = False, 0
+        self.steps_run = 0
         self.caps = self.sampler.caps
         self.pick_cap = self.sampler.pcaps[L - 1]
         self.model = GatModel(codec.d, cfg.hidden, num_classes, L, cfg.heads).to(self.device)
@@ -373,6 +411,7 @@ class GatTrainer:
                          and os.environ.get("FG_GAT_EXPLICIT", "1") != "0")
         self._views = [_LayerViews(layer, self.flat_param, self.flat_grad, self.flat_bf16)
                        for layer in self.model.layers]
+        self._ones = torch.ones(max(self.caps), dtype=torch.float32, device=self.device)
         self.graph = None
 
     def _decode(self, sb):
@@ -380,7 +419,19 @@ class GatTrainer:
         return PickSource(self.codec, sb.picks[L - 1], sb.n_picks[L - 1], self.pick_cap)
 
     def _body(self, k: int = 0):
-        sb = self.sampler.sample_loaded()
+        """One step.  Serial: sample slot 0's loaded seeds, then train.
+        Pipelined: train the batch already in slot k while the side stream
+        samples the next batch (seeds already loaded) into slot 1-k."""
+        if not self.pipeline:
+            return self._train(self.sampler.sample_loaded())
+        cur = torch.cuda.current_stream()
+        self.side.wait_stream(cur)
+        with torch.cuda.stream(self.side):
+            self.samplers[1 - k].sample_loaded()
+        self._train(self.samplers[k].batch_view())
+        cur.wait_stream(self.side)
+
+    def _train(self, sb):
         if self.explicit:
             self.forward_backward(sb)
         else:
@@ -422,33 +473,46 @@ class GatTrainer:
         for i, v in enumerate(self._views):
             l = L - 1 - i
             Hh, Fh, D = v.heads, v.F, v.D
-            c = torch.bmm(v.attn.permute(1, 0, 2), v.W.view(Hh, Fh, D))     # [Hh, 2, D]
+            c = torch.bmm(v.attn.permute(1, 0, 2), v.W.view(Hh, Fh, D))    # [Hh, 2, D]
             c = c.permute(1, 0, 2).reshape(2 * Hh, D)                       # [el | er] rows
             cb = c.to(bf16)
-            sc = torch.mm(h, cb.t(), out_dtype=f32)                         # [src rows, 2Hh]
             first = i == 0
             local = None if first else sb.local[l]
             e_cap = self.pick_cap if first else sb.local[l].numel()
             alpha = torch.empty((e_cap, Hh), dtype=f32, device=dev)
             q = torch.empty((self.caps[l], Hh), dtype=f32, device=dev)
-            N.call("fg_gat_softmax_fwd", N.ptr(sc), N.ptr(sc[:, Hh:]), 2 * Hh,
-                   N.ptr(sb.indptr[l]), N.ptr(local), self.caps[l], N.ptr(sb.n_nodes[l]), Hh,
-                   0.2, N.ptr(alpha), N.ptr(q), s)
             if first:
-                A = torch.empty((self.caps[l], Hh * D), dtype=bf16, device=dev)
-                N.call("fg_gat_code_xagg_fwd", None, N.ptr(h), None, D, Hh, N.ptr(alpha),
-                       N.ptr(sb.indptr[l]), self.caps[l], N.ptr(sb.n_nodes[l]), N.ptr(A), s)
+                # one pass over the picks (fg_gat_input_attn_fwd): scores,
+                # softmax and A = [per-head alpha-weighted pick sums | 1 0..0],
+                # rows padded to a multiple of 64 (zero rows) for the chunked
+                # K-GEMMs; o = A [blockdiag(W_k^T); b; 0] (bias via the ones column)
+                sc = torch.empty((e_cap, 2 * Hh), dtype=f32, device=dev)
+                rows = _round_up(self.caps[l], 64)
+                A = torch.empty((rows, Hh * D + 8), dtype=bf16, device=dev)
+                N.call("fg_gat_input_attn_fwd", N.ptr(h), D, Hh, N.ptr(c), N.ptr(sb.indptr[l]),
+                       self.caps[l], rows, N.ptr(sb.n_nodes[l]), 0.2, N.ptr(sc), N.ptr(alpha),
+                       N.ptr(q), N.ptr(A), Hh * D + 8, s)
                 v.refresh_block_diag()
-                o = torch.addmm(v.bb, A, v.wbd)                                # bf16
+                o = torch.mm(A, v.wbd)                                          # bf16
                 z = A
+                bias, in_f32 = None, 0
             else:
+                sc = torch.mm(h, cb.t(), out_dtype=f32)                     # [src rows, 2Hh]
+                N.call("fg_gat_softmax_fwd", N.ptr(sc), N.ptr(sc[:, Hh:]), 2 * Hh,
+                       N.ptr(sb.indptr[l]), N.ptr(local), self.caps[l], N.ptr(sb.n_nodes[l]),
+                       Hh, 0.2, N.ptr(alpha), N.ptr(q), s)
                 z = torch.mm(h, v.Wb.t())                                       # [src rows, Wd]
                 o = torch.empty((self.caps[l], v.width), dtype=f32, device=dev)
                 N.call("fg_gat_agg_fwd", N.ptr(z), v.width, Hh, N.ptr(alpha), N.ptr(sb.indptr[l]),
                        N.ptr(local), self.caps[l], N.ptr(sb.n_nodes[l]), N.ptr(o), s)
-                o += v.b
+                bias, in_f32 = v.b, 1
             saved.append((h, c, cb, sc, alpha, q, z, local, e_cap))
-            h = F.elu(o).to(bf16) if i < L - 1 else o
+            if i < L - 1:
+                h = torch.empty(o.shape, dtype=bf16, device=dev)
+                N.call("fg_gat_elu_fwd", N.ptr(o), in_f32, o.shape[1], N.ptr(bias), o.shape[0],
+                       o.shape[1], N.ptr(h), s)
+            else:
+                h = o.add_(v.b)
         logits = h
         C, ld = self.model.num_classes, logits.shape[1]
         do = torch.empty_like(logits)
@@ -462,27 +526,26 @@ class GatTrainer:
             l = L - 1 - i
             Hh, Fh, D = v.heads, v.F, v.D
             h, c, cb, sc, alpha, q, z, local, e_cap = saved[i]
-            torch.sum(do, 0, dtype=f32, out=v.db)
-            ds = torch.zeros((h.shape[0], 2 * Hh), dtype=f32, device=dev)
             if i == 0:
                 A = z
-                dA = torch.mm(do, v.wbd.t())                                    # [N, Hh*D] bf16
-                # dW_k = do_k^T A_k: the diagonal blocks only (strided batched GEMM)
-                dWk = torch.bmm(do.view(-1, Hh, Fh).permute(1, 2, 0),
-                                A.view(-1, Hh, D).permute(1, 0, 2))
-                v.dW.view(Hh, Fh, D).copy_(dWk)
+                dA = torch.mm(do, v.wbd[:Hh * D].t())                          # [rows, Hh*D]
+                # do^T A: the diagonal blocks are dW_k, the ones column db
+                full = _kgemm(do, A, torch.empty((v.width, A.shape[1]), dtype=f32, device=dev))
+                v.dW.view(Hh, Fh, D).copy_(
+                    full[:, :Hh * D].view(Hh, Fh, Hh, D).diagonal(dim1=0, dim2=2).permute(2, 0, 1))
+                v.db.copy_(full[:, Hh * D])
+                # dalpha, the softmax backward and dc = [del|der]^T x in one
+                # pass over the picks (fg_gat_input_attn_bwd)
                 dalpha = torch.empty((e_cap, Hh), dtype=f32, device=dev)
-                N.call("fg_gat_code_xagg_bwd", None, N.ptr(h), None, D, Hh, N.ptr(sb.indptr[l]),
-                       self.caps[l], N.ptr(sb.n_nodes[l]), N.ptr(dA), N.ptr(dalpha), s)
-                N.call("fg_gat_softmax_bwd", N.ptr(sc), 2 * Hh, N.ptr(q), N.ptr(alpha),
-                       N.ptr(dalpha), N.ptr(sb.indptr[l]), None, self.caps[l],
-                       N.ptr(sb.n_nodes[l]), Hh, 0.2, N.ptr(ds), N.ptr(ds[:, Hh:]), s)
-                nb = N.lib().fg_gat_code_scores_bwd_blocks(e_cap)
-                part = torch.empty((nb, 2 * Hh, D), dtype=f32, device=dev)
-                N.call("fg_gat_code_scores_bwd", None, N.ptr(h), None, N.ptr(sb.n_picks[l]), e_cap,
-                       D, Hh, N.ptr(ds), N.ptr(ds[:, Hh:]), 2 * Hh, N.ptr(part), s)
+                part = torch.empty((N.lib().fg_gat_input_attn_bwd_blocks(), 2 * Hh, D),
+                                   dtype=f32, device=dev)
+                N.call("fg_gat_input_attn_bwd", N.ptr(h), D, Hh, N.ptr(sc), N.ptr(alpha), N.ptr(q),
+                       N.ptr(dA), N.ptr(sb.indptr[l]), self.caps[l], N.ptr(sb.n_nodes[l]), 0.2,
+                       N.ptr(dalpha), N.ptr(part), s)
                 dc = part.sum(0)
             else:
+                ds = torch.zeros((h.shape[0], 2 * Hh), dtype=f32, device=dev)
+                torch.mv(do.t(), self._ones[:do.shape[0]], out=v.db)
                 dz = torch.zeros((h.shape[0], v.width), dtype=f32, device=dev)
                 dalpha = torch.zeros((e_cap, Hh), dtype=f32, device=dev)
                 N.call("fg_gat_agg_bwd", N.ptr(z), v.width, Hh, N.ptr(alpha), N.ptr(sb.indptr[l]),
@@ -492,8 +555,8 @@ class GatTrainer:
                        N.ptr(dalpha), N.ptr(sb.indptr[l]), N.ptr(local), self.caps[l],
                        N.ptr(sb.n_nodes[l]), Hh, 0.2, N.ptr(ds), N.ptr(ds[:, Hh:]), s)
                 dzb, dsb = dz.to(bf16), ds.to(bf16)
-                torch.mm(dzb.t(), h, out_dtype=f32, out=v.dW)
-                dc = torch.mm(dsb.t(), h, out_dtype=f32)                      # [2Hh, D]
+                _kgemm(dzb, h, v.dW)
+                dc = _kgemm(dsb, h, torch.empty((2 * Hh, D), dtype=f32, device=dev))
             dcv = dc.view(2, Hh, D).permute(1, 0, 2)                            # [Hh, 2, D]
             # d[a_l | a_r][k, f] = <W[kF+f], dc[el|er row k]>;  dW += a . dc
             v.dattn.copy_(torch.bmm(v.W.view(Hh, Fh, D), dcv.transpose(1, 2)).permute(2, 0, 1))
@@ -501,58 +564,22 @@ class GatTrainer:
             if i == 0:
                 break
             dh = torch.addmm(torch.mm(dzb, v.Wb), dsb, cb)                      # [src rows, D] bf16
-            # ELU'(o) from its output h: 1 where h > 0, h + 1 elsewhere
-            do = torch.ops.aten.elu_backward(dh, 1.0, 1.0, 1.0, True, h)
-            if i - 1 > 0:
-                do = do.float()
+            # ELU'(o) from its output h; fp32 for a hidden layer's aggregation
+            # backward, bf16 for the input layer's GEMMs
+            nxt = torch.empty(dh.shape, dtype=f32 if i - 1 > 0 else bf16, device=dev)
+            N.call("fg_gat_elu_bwd", N.ptr(dh), N.ptr(h), dh.numel(), N.ptr(nxt),
+                   int(i - 1 > 0), s)
+            do = nxt
 
-    def begin_epoch(self, train_ids, epoch: int = 0) -> int:
-        r = torch.distributed.get_rank(self.pg) if self.world > 1 else 0
-        shard = ddp.shard_ids(train_ids, r, self.world)
-        self._nb = self.sampler.begin_epoch(shard, ddp.rank_seed(self.cfg.seed, epoch, r,
-                                                                 self.world))
-        self._nb = ddp.agree_num_batches(self._nb, self.pg, self.device)
-        return self._nb
-
-    def capture(self, warmup_batches: int = 3):
-        rng_save = self.sampler.rng.clone()
-        s = torch.cuda.Stream()
-        s.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(s):
-            for b in range(warmup_batches):
-                self.sampler.load_seeds(b % self._nb)
-                self._body()
-        torch.cuda.current_stream().wait_stream(s)
-        torch.cuda.synchronize()
-        self.graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(self.graph):
-            self._body()
-        torch.cuda.synchronize()
-        self.sampler.rng.copy_(rng_save)
-
-    # same step API as SageTrainer (serial sampling: one slot)
-    pipeline = False
-
-    @property
-    def samplers(self):
-        return [self.sampler]
-
-    def prepare(self, b: int, seeds_host=None) -> None:
-        if seeds_host is not None:
-            self.sampler.load_seeds_host(seeds_host)
-        else:
-            self.sampler.load_seeds(b)
-
-    def replay(self, b: int):
-        if self.graph is not None:
-            self.graph.replay()
-        else:
-            self._body()
-        return self.loss_buf
-
-    def step(self, b: int, seeds_host=None):
-        self.prepare(b, seeds_host)
-        return self.replay(b)
+    # epoch / step API and CUDA-graph capture: SageTrainer's (same slot
+    # logic, same attribute names; one graph per sampler slot)
+    from .sage import SageTrainer as _S
+    begin_epoch = _S.begin_epoch
+    prepare = _S.prepare
+    replay = _S.replay
+    step = _S.step
+    capture = _S.capture
+    del _S
 
     @torch.no_grad()
     def evaluate(self, ids, seed: int = 12345, max_batches: int | None = None) -> float:

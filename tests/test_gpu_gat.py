@@ -197,3 +197,28 @@ def test_gat_gradients_match_cpu_oracle_model(codec_kind, decoded):
             g = t.flat_grad[off:off + q.numel()].view(q.shape).cpu()
             rel = ((g - p.grad).norm() / p.grad.norm()).item()
             assert rel < 5e-2, ("explicit", name, rel)
+
+
+@pytest.mark.parametrize("in_f32", [0, 1])
+def test_gat_elu_kernels_match_torch(in_f32):
+    """fg_gat_elu_fwd (bias + ELU -> bf16) and fg_gat_elu_bwd (ELU' from the
+    output) against torch on the same values."""
+    from paper_2207_14696_b200 import _native as N
+    dev = "cuda"
+    rows, cols = 1000, 264
+    o = torch.randn(rows, cols, device=dev) * 3
+    o = o if in_f32 else o.to(torch.bfloat16)
+    b = torch.randn(cols, device=dev)
+    h = torch.empty((rows, cols), dtype=torch.bfloat16, device=dev)
+    s = N.stream_handle()
+    N.call("fg_gat_elu_fwd", N.ptr(o), in_f32, cols, N.ptr(b), rows, cols, N.ptr(h), s)
+    ref = F.elu(o.float() + b).to(torch.bfloat16)
+    torch.cuda.synchronize()
+    assert (h.float() - ref.float()).abs().max().item() <= 1e-2
+    dh = torch.randn(rows, cols, device=dev).to(torch.bfloat16)
+    out = torch.empty((rows, cols), dtype=torch.float32 if in_f32 else torch.bfloat16, device=dev)
+    N.call("fg_gat_elu_bwd", N.ptr(dh), N.ptr(h), dh.numel(), N.ptr(out), in_f32, s)
+    hf = h.float()
+    want = torch.where(hf > 0, dh.float(), dh.float() * (hf + 1))
+    torch.cuda.synchronize()
+    assert (out.float() - want).abs().max().item() <= (0 if in_f32 else 2e-2)
