@@ -852,18 +852,150 @@ __device__ __forceinline__ int tr_lane(int idx) {  // the lowest lane holding id
   return lane;
 }
 
-template <int XI>
-__device__ __forceinline__ void load_row(const __nv_bfloat16* __restrict__ xr, int d, int lane,
-                                         float (&xv)[XI]) {
+// lane owns column pairs (2p, 2p+1), p = lane + 32 i (d even)
+template <int XP>
+__device__ __forceinline__ void load_row2(const __nv_bfloat16* __restrict__ xr, int d, int lane,
+                                          float2 (&xv)[XP]) {
 #pragma unroll
-  for (int i = 0; i < XI; ++i) {
-    const int j = lane + 32 * i;
-    xv[i] = j < d ? __bfloat162float(xr[j]) : 0.f;
+  for (int i = 0; i < XP; ++i) {
+    const int j = 2 * (lane + 32 * i);
+    xv[i] = j < d ? __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(xr + j))
+                  : make_float2(0.f, 0.f);
   }
 }
 
-template <int HEADS, int XI>
-__global__ void __launch_bounds__(256)
+// Destinations with C <= kIaMaxP picks run a body specialised on C (rows,
+// scores and attention in registers, no per-pick branches: the counts are
+// warp-uniform, one switch per destination); larger ones take the general
+// path through the scores / alpha / dalpha buffers.
+constexpr int kIaMaxP = 6;
+
+template <int HEADS, int XP>
+struct IaFwd {
+  static constexpr int V = 2 * HEADS;
+  const __nv_bfloat16* __restrict__ x;
+  int d, lane, my;
+  bool writer;
+  float slope;
+  float* __restrict__ sc;
+  float* __restrict__ alpha;
+  float2 cr[V][XP];
+
+  __device__ __forceinline__ float scores(const float2 (&xv)[XP]) const {
+    float pv[V];
+#pragma unroll
+    for (int s = 0; s < V; ++s) {
+      float t = 0.f;
+#pragma unroll
+      for (int i = 0; i < XP; ++i) t = fmaf(xv[i].x, cr[s][i].x, fmaf(xv[i].y, cr[s][i].y, t));
+      pv[s] = t;
+    }
+    return tr_reduce<V>(pv, lane);
+  }
+  __device__ __forceinline__ void accum(float2 (&acc)[XP][HEADS], const float (&al)[HEADS],
+                                        const float2 (&xv)[XP]) const {
+#pragma unroll
+    for (int k = 0; k < HEADS; ++k)
+#pragma unroll
+      for (int i = 0; i < XP; ++i) {
+        acc[i][k].x = fmaf(al[k], xv[i].x, acc[i][k].x);
+        acc[i][k].y = fmaf(al[k], xv[i].y, acc[i][k].y);
+      }
+  }
+  template <int C>
+  __device__ __forceinline__ void body(int32_t e0, float* __restrict__ qv,
+                                       float2 (&acc)[XP][HEADS]) const {
+    float2 xr[C][XP];
+    float rs[C];
+#pragma unroll
+    for (int e = 0; e < C; ++e) load_row2<XP>(x + (int64_t)(e0 + e) * d, d, lane, xr[e]);
+    float qacc = 0.f;
+#pragma unroll
+    for (int e = 0; e < C; ++e) {
+      rs[e] = scores(xr[e]);
+      if (writer) sc[(int64_t)(e0 + e) * V + my] = rs[e];
+      qacc += my >= HEADS ? rs[e] : 0.f;
+    }
+    float qk[HEADS], mx[HEADS], den[HEADS], sl[C][HEADS];
+#pragma unroll
+    for (int k = 0; k < HEADS; ++k) {
+      qk[k] = __shfl_sync(0xffffffffu, qacc, tr_lane<V>(HEADS + k)) * (1.f / C);
+      if (lane == k) qv[k] = qk[k];
+    }
+#pragma unroll
+    for (int e = 0; e < C; ++e)
+#pragma unroll
+      for (int k = 0; k < HEADS; ++k) {
+        sl[e][k] = leaky(__shfl_sync(0xffffffffu, rs[e], tr_lane<V>(k)) + qk[k], slope);
+        mx[k] = e ? fmaxf(mx[k], sl[e][k]) : sl[e][k];
+      }
+#pragma unroll
+    for (int e = 0; e < C; ++e)
+#pragma unroll
+      for (int k = 0; k < HEADS; ++k) {
+        sl[e][k] = __expf(sl[e][k] - mx[k]);
+        den[k] = e ? den[k] + sl[e][k] : sl[e][k];
+      }
+#pragma unroll
+    for (int k = 0; k < HEADS; ++k) den[k] = 1.f / den[k];
+#pragma unroll
+    for (int e = 0; e < C; ++e) {
+      float al[HEADS];
+#pragma unroll
+      for (int k = 0; k < HEADS; ++k) {
+        al[k] = sl[e][k] * den[k];
+        if (lane == k) alpha[(int64_t)(e0 + e) * HEADS + k] = al[k];
+      }
+      accum(acc, al, xr[e]);
+    }
+  }
+  // general path: scores through sc, rows re-read
+  __device__ void general(int32_t e0, int32_t e1, float* __restrict__ qv,
+                          float2 (&acc)[XP][HEADS]) const {
+    float qacc = 0.f;
+    for (int32_t e = e0; e < e1; ++e) {
+      float2 xv[XP];
+      load_row2<XP>(x + (int64_t)e * d, d, lane, xv);
+      const float r = scores(xv);
+      if (writer) sc[(int64_t)e * V + my] = r;
+      if (my >= HEADS) qacc += r;
+    }
+    __syncwarp();
+    const float rc = 1.f / (float)(e1 - e0);
+    float qk[HEADS], mx[HEADS], inv[HEADS];
+#pragma unroll
+    for (int k = 0; k < HEADS; ++k) {
+      qk[k] = __shfl_sync(0xffffffffu, qacc, tr_lane<V>(HEADS + k)) * rc;
+      mx[k] = -INFINITY;
+      inv[k] = 0.f;
+      if (lane == k) qv[k] = qk[k];
+    }
+    for (int32_t e = e0; e < e1; ++e)
+#pragma unroll
+      for (int k = 0; k < HEADS; ++k)
+        mx[k] = fmaxf(mx[k], leaky(sc[(int64_t)e * V + k] + qk[k], slope));
+    for (int32_t e = e0; e < e1; ++e)
+#pragma unroll
+      for (int k = 0; k < HEADS; ++k)
+        inv[k] += __expf(leaky(sc[(int64_t)e * V + k] + qk[k], slope) - mx[k]);
+#pragma unroll
+    for (int k = 0; k < HEADS; ++k) inv[k] = 1.f / inv[k];
+    for (int32_t e = e0; e < e1; ++e) {
+      float2 xv[XP];
+      float al[HEADS];
+      load_row2<XP>(x + (int64_t)e * d, d, lane, xv);
+#pragma unroll
+      for (int k = 0; k < HEADS; ++k) {
+        al[k] = __expf(leaky(sc[(int64_t)e * V + k] + qk[k], slope) - mx[k]) * inv[k];
+        if (lane == k) alpha[(int64_t)e * HEADS + k] = al[k];
+      }
+      accum(acc, al, xv);
+    }
+  }
+};
+
+template <int HEADS, int XP>
+__global__ void __launch_bounds__(256, 2)
 k_gat_input_attn_fwd(const __nv_bfloat16* __restrict__ x, int d, const float* __restrict__ c,
                      const int32_t* __restrict__ indptr, int64_t max_dst, int64_t rows,
                      const int64_t* __restrict__ ndst_dev, float slope, float* __restrict__ sc,
@@ -871,16 +1003,23 @@ k_gat_input_attn_fwd(const __nv_bfloat16* __restrict__ x, int d, const float* __
                      __nv_bfloat16* __restrict__ out, int64_t out_ld) {
   constexpr int V = 2 * HEADS;
   const int64_t live = min64(*ndst_dev, max_dst);
-  const int lane = threadIdx.x & 31;
-  const int my = tr_index<V>(lane);
-  const bool writer = (lane & (32 / V - 1)) == 0;
-  float cr[V][XI];
+  IaFwd<HEADS, XP> f;
+  f.x = x;
+  f.d = d;
+  f.lane = threadIdx.x & 31;
+  f.my = tr_index<V>(f.lane);
+  f.writer = (f.lane & (32 / V - 1)) == 0;
+  f.slope = slope;
+  f.sc = sc;
+  f.alpha = alpha;
+  const int lane = f.lane;
 #pragma unroll
   for (int s = 0; s < V; ++s)
 #pragma unroll
-    for (int i = 0; i < XI; ++i) {
-      const int j = lane + 32 * i;
-      cr[s][i] = j < d ? __ldg(c + s * d + j) : 0.f;
+    for (int i = 0; i < XP; ++i) {
+      const int j = 2 * (lane + 32 * i);
+      f.cr[s][i] = j < d ? make_float2(__ldg(c + s * d + j), __ldg(c + s * d + j + 1))
+                         : make_float2(0.f, 0.f);
     }
   for (int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; v < rows;
        v += ((int64_t)gridDim.x * blockDim.x) >> 5) {
@@ -888,79 +1027,142 @@ k_gat_input_attn_fwd(const __nv_bfloat16* __restrict__ x, int d, const float* __
     for (int64_t j = (int64_t)HEADS * d + lane; j < out_ld; j += 32)
       o[j] = __float2bfloat16_rn(j == (int64_t)HEADS * d ? 1.f : 0.f);
     const int32_t e0 = v < live ? indptr[v] : 0, e1 = v < live ? indptr[v + 1] : 0;
-    float acc[XI][HEADS];
+    float2 acc[XP][HEADS];
 #pragma unroll
-    for (int i = 0; i < XI; ++i)
+    for (int i = 0; i < XP; ++i)
 #pragma unroll
-      for (int k = 0; k < HEADS; ++k) acc[i][k] = 0.f;
-    if (e1 > e0) {
-      // pass 1: scores [el | er] per pick, er summed for the query
-      float qacc = 0.f;
-      for (int32_t e = e0; e < e1; ++e) {
-        float xv[XI], pv[V];
-        load_row<XI>(x + (int64_t)e * d, d, lane, xv);
-#pragma unroll
-        for (int s = 0; s < V; ++s) {
-          float t = 0.f;
-#pragma unroll
-          for (int i = 0; i < XI; ++i) t = fmaf(xv[i], cr[s][i], t);
-          pv[s] = t;
-        }
-        const float r = tr_reduce<V>(pv, lane);
-        if (writer) sc[(int64_t)e * V + my] = r;
-        if (my >= HEADS) qacc += r;
-      }
-      __syncwarp();
-      const float rc = 1.f / (float)(e1 - e0);
-      float qk[HEADS], mx[HEADS], inv[HEADS];
-#pragma unroll
-      for (int k = 0; k < HEADS; ++k) {
-        qk[k] = __shfl_sync(0xffffffffu, qacc, tr_lane<V>(HEADS + k)) * rc;
-        mx[k] = -INFINITY;
-        inv[k] = 0.f;
-      }
-      for (int32_t e = e0; e < e1; ++e)
-#pragma unroll
-        for (int k = 0; k < HEADS; ++k)
-          mx[k] = fmaxf(mx[k], leaky(sc[(int64_t)e * V + k] + qk[k], slope));
-      for (int32_t e = e0; e < e1; ++e)
-#pragma unroll
-        for (int k = 0; k < HEADS; ++k)
-          inv[k] += __expf(leaky(sc[(int64_t)e * V + k] + qk[k], slope) - mx[k]);
-#pragma unroll
-      for (int k = 0; k < HEADS; ++k) {
-        inv[k] = 1.f / inv[k];
-        if (lane == k) q[v * HEADS + k] = qk[k];
-      }
-      // pass 2: alpha and the per-head weighted sums of the pick rows
-      for (int32_t e = e0; e < e1; ++e) {
-        float al[HEADS], xv[XI];
-#pragma unroll
-        for (int k = 0; k < HEADS; ++k) {
-          al[k] = __expf(leaky(sc[(int64_t)e * V + k] + qk[k], slope) - mx[k]) * inv[k];
-          if (lane == k) alpha[(int64_t)e * HEADS + k] = al[k];
-        }
-        load_row<XI>(x + (int64_t)e * d, d, lane, xv);
-#pragma unroll
-        for (int i = 0; i < XI; ++i)
-#pragma unroll
-          for (int k = 0; k < HEADS; ++k) acc[i][k] = fmaf(al[k], xv[i], acc[i][k]);
-      }
-    } else if (v < max_dst && lane < HEADS) {
-      q[v * HEADS + lane] = 0.f;
+      for (int k = 0; k < HEADS; ++k) acc[i][k] = make_float2(0.f, 0.f);
+    float* qv = q + v * HEADS;
+    switch (e1 - e0) {
+      case 0: if (v < max_dst && lane < HEADS) qv[lane] = 0.f; break;
+      case 1: f.template body<1>(e0, qv, acc); break;
+      case 2: f.template body<2>(e0, qv, acc); break;
+      case 3: f.template body<3>(e0, qv, acc); break;
+      case 4: f.template body<4>(e0, qv, acc); break;
+      case 5: f.template body<5>(e0, qv, acc); break;
+      case 6: f.template body<6>(e0, qv, acc); break;
+      default: f.general(e0, e1, qv, acc); break;
     }
 #pragma unroll
     for (int k = 0; k < HEADS; ++k)
 #pragma unroll
-      for (int i = 0; i < XI; ++i) {
-        const int j = lane + 32 * i;
-        if (j < d) o[k * d + j] = __float2bfloat16_rn(acc[i][k]);
+      for (int i = 0; i < XP; ++i) {
+        const int j = 2 * (lane + 32 * i);
+        if (j < d)
+          *reinterpret_cast<__nv_bfloat162*>(o + k * d + j) =
+              __floats2bfloat162_rn(acc[i][k].x, acc[i][k].y);
       }
   }
 }
 
-template <int HEADS, int XI>
-__global__ void __launch_bounds__(256)
+template <int HEADS, int XP>
+struct IaBwd {
+  static constexpr int V = 2 * HEADS;
+  const __nv_bfloat16* __restrict__ x;
+  const float* __restrict__ sc;
+  const float* __restrict__ alpha;
+  float* __restrict__ dalpha;
+  int d, lane, my;
+  bool writer;
+  float slope;
+  float2 g[HEADS][XP];
+  float2 dc[V][XP];
+
+  __device__ __forceinline__ float dots(const float2 (&xv)[XP]) const {
+    float pv[HEADS];
+#pragma unroll
+    for (int k = 0; k < HEADS; ++k) {
+      float t = 0.f;
+#pragma unroll
+      for (int i = 0; i < XP; ++i) t = fmaf(g[k][i].x, xv[i].x, fmaf(g[k][i].y, xv[i].y, t));
+      pv[k] = t;
+    }
+    return tr_reduce<HEADS>(pv, lane);
+  }
+  __device__ __forceinline__ void accum(const float2 (&xv)[XP], const float (&dl)[HEADS],
+                                        const float (&sh)[HEADS]) {
+#pragma unroll
+    for (int k = 0; k < HEADS; ++k)
+#pragma unroll
+      for (int i = 0; i < XP; ++i) {
+        dc[k][i].x = fmaf(dl[k], xv[i].x, dc[k][i].x);
+        dc[k][i].y = fmaf(dl[k], xv[i].y, dc[k][i].y);
+        dc[HEADS + k][i].x = fmaf(sh[k], xv[i].x, dc[HEADS + k][i].x);
+        dc[HEADS + k][i].y = fmaf(sh[k], xv[i].y, dc[HEADS + k][i].y);
+      }
+  }
+  template <int C>
+  __device__ __forceinline__ void body(int32_t e0, const float (&qk)[HEADS]) {
+    float2 xr[C][XP];
+    float al[C][HEADS], dl[C][HEADS], dot[HEADS], sh[HEADS];
+#pragma unroll
+    for (int e = 0; e < C; ++e) {
+      load_row2<XP>(x + (int64_t)(e0 + e) * d, d, lane, xr[e]);
+#pragma unroll
+      for (int k = 0; k < HEADS; ++k) al[e][k] = alpha[(int64_t)(e0 + e) * HEADS + k];
+    }
+#pragma unroll
+    for (int e = 0; e < C; ++e) {
+      const float r = dots(xr[e]);
+#pragma unroll
+      for (int k = 0; k < HEADS; ++k) {
+        dl[e][k] = __shfl_sync(0xffffffffu, r, tr_lane<HEADS>(k));  // dalpha
+        dot[k] = e ? fmaf(al[e][k], dl[e][k], dot[k]) : al[e][k] * dl[e][k];
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < C; ++e)
+#pragma unroll
+      for (int k = 0; k < HEADS; ++k) {
+        const float ds = al[e][k] * (dl[e][k] - dot[k]);
+        dl[e][k] = sc[(int64_t)(e0 + e) * V + k] + qk[k] > 0.f ? ds : slope * ds;
+        sh[k] = e ? sh[k] + dl[e][k] : dl[e][k];
+      }
+#pragma unroll
+    for (int k = 0; k < HEADS; ++k) sh[k] *= 1.f / C;
+#pragma unroll
+    for (int e = 0; e < C; ++e) accum(xr[e], dl[e], sh);
+  }
+  __device__ void general(int32_t e0, int32_t e1, const float (&qk)[HEADS]) {
+    float dot[HEADS], sh[HEADS];
+#pragma unroll
+    for (int k = 0; k < HEADS; ++k) dot[k] = sh[k] = 0.f;
+    for (int32_t e = e0; e < e1; ++e) {  // dalpha[e, k] = <dA[v, k], x_e>
+      float2 xv[XP];
+      load_row2<XP>(x + (int64_t)e * d, d, lane, xv);
+      const float r = dots(xv);
+      if (writer) dalpha[(int64_t)e * HEADS + my] = r;
+    }
+    __syncwarp();
+    for (int32_t e = e0; e < e1; ++e)
+#pragma unroll
+      for (int k = 0; k < HEADS; ++k)
+        dot[k] = fmaf(alpha[(int64_t)e * HEADS + k], dalpha[(int64_t)e * HEADS + k], dot[k]);
+    for (int32_t e = e0; e < e1; ++e)
+#pragma unroll
+      for (int k = 0; k < HEADS; ++k) {
+        const float ds = alpha[(int64_t)e * HEADS + k] * (dalpha[(int64_t)e * HEADS + k] - dot[k]);
+        sh[k] += sc[(int64_t)e * V + k] + qk[k] > 0.f ? ds : slope * ds;
+      }
+    const float rc = 1.f / (float)(e1 - e0);
+#pragma unroll
+    for (int k = 0; k < HEADS; ++k) sh[k] *= rc;
+    for (int32_t e = e0; e < e1; ++e) {  // dc += [del | der]_e x_e
+      float2 xv[XP];
+      float dl[HEADS];
+#pragma unroll
+      for (int k = 0; k < HEADS; ++k) {
+        const float ds = alpha[(int64_t)e * HEADS + k] * (dalpha[(int64_t)e * HEADS + k] - dot[k]);
+        dl[k] = sc[(int64_t)e * V + k] + qk[k] > 0.f ? ds : slope * ds;
+      }
+      load_row2<XP>(x + (int64_t)e * d, d, lane, xv);
+      accum(xv, dl, sh);
+    }
+  }
+};
+
+template <int HEADS, int XP>
+__global__ void __launch_bounds__(256, 2)
 k_gat_input_attn_bwd(const __nv_bfloat16* __restrict__ x, int d, const float* __restrict__ sc,
                      const float* __restrict__ alpha, const float* __restrict__ q,
                      const __nv_bfloat16* __restrict__ dA, const int32_t* __restrict__ indptr,
@@ -970,74 +1172,44 @@ k_gat_input_attn_bwd(const __nv_bfloat16* __restrict__ x, int d, const float* __
   extern __shared__ float s_dc[];  // [V][d]
   const int64_t live = min64(*ndst_dev, max_dst);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int my = tr_index<HEADS>(lane);
-  const bool writer = (lane & (32 / HEADS - 1)) == 0;
-  float dc[V][XI];
+  IaBwd<HEADS, XP> b;
+  b.x = x;
+  b.sc = sc;
+  b.alpha = alpha;
+  b.dalpha = dalpha;
+  b.d = d;
+  b.lane = lane;
+  b.my = tr_index<HEADS>(lane);
+  b.writer = (lane & (32 / HEADS - 1)) == 0;
+  b.slope = slope;
 #pragma unroll
   for (int s = 0; s < V; ++s)
 #pragma unroll
-    for (int i = 0; i < XI; ++i) dc[s][i] = 0.f;
+    for (int i = 0; i < XP; ++i) b.dc[s][i] = make_float2(0.f, 0.f);
   for (int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; v < live;
        v += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     const int32_t e0 = indptr[v], e1 = indptr[v + 1];
     if (e1 == e0) continue;
-    float g[HEADS][XI];
 #pragma unroll
     for (int k = 0; k < HEADS; ++k)
 #pragma unroll
-      for (int i = 0; i < XI; ++i) {
-        const int j = lane + 32 * i;
-        g[k][i] = j < d ? __bfloat162float(dA[(v * HEADS + k) * (int64_t)d + j]) : 0.f;
+      for (int i = 0; i < XP; ++i) {
+        const int j = 2 * (lane + 32 * i);
+        b.g[k][i] = j < d ? __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(
+                                dA + (v * HEADS + k) * (int64_t)d + j))
+                          : make_float2(0.f, 0.f);
       }
-    for (int32_t e = e0; e < e1; ++e) {  // dalpha[e, k] = <dA[v, k], x_e>
-      float xv[XI], pv[HEADS];
-      load_row<XI>(x + (int64_t)e * d, d, lane, xv);
+    float qk[HEADS];
 #pragma unroll
-      for (int k = 0; k < HEADS; ++k) {
-        float t = 0.f;
-#pragma unroll
-        for (int i = 0; i < XI; ++i) t = fmaf(g[k][i], xv[i], t);
-        pv[k] = t;
-      }
-      const float r = tr_reduce<HEADS>(pv, lane);
-      if (writer) dalpha[(int64_t)e * HEADS + my] = r;
-    }
-    __syncwarp();
-    float qk[HEADS], dot[HEADS], share[HEADS];
-#pragma unroll
-    for (int k = 0; k < HEADS; ++k) {
-      qk[k] = q[v * HEADS + k];
-      dot[k] = 0.f;
-      share[k] = 0.f;
-    }
-    for (int32_t e = e0; e < e1; ++e)
-#pragma unroll
-      for (int k = 0; k < HEADS; ++k)
-        dot[k] = fmaf(alpha[(int64_t)e * HEADS + k], dalpha[(int64_t)e * HEADS + k], dot[k]);
-    for (int32_t e = e0; e < e1; ++e)
-#pragma unroll
-      for (int k = 0; k < HEADS; ++k) {
-        const float ds = alpha[(int64_t)e * HEADS + k] * (dalpha[(int64_t)e * HEADS + k] - dot[k]);
-        share[k] += sc[(int64_t)e * V + k] + qk[k] > 0.f ? ds : slope * ds;
-      }
-    const float rc = 1.f / (float)(e1 - e0);
-#pragma unroll
-    for (int k = 0; k < HEADS; ++k) share[k] *= rc;
-    for (int32_t e = e0; e < e1; ++e) {  // dc += [del | der]_e x_e
-      float xv[XI], dl[HEADS];
-#pragma unroll
-      for (int k = 0; k < HEADS; ++k) {
-        const float ds = alpha[(int64_t)e * HEADS + k] * (dalpha[(int64_t)e * HEADS + k] - dot[k]);
-        dl[k] = sc[(int64_t)e * V + k] + qk[k] > 0.f ? ds : slope * ds;
-      }
-      load_row<XI>(x + (int64_t)e * d, d, lane, xv);
-#pragma unroll
-      for (int i = 0; i < XI; ++i)
-#pragma unroll
-        for (int k = 0; k < HEADS; ++k) {
-          dc[k][i] = fmaf(dl[k], xv[i], dc[k][i]);
-          dc[HEADS + k][i] = fmaf(share[k], xv[i], dc[HEADS + k][i]);
-        }
+    for (int k = 0; k < HEADS; ++k) qk[k] = q[v * HEADS + k];
+    switch (e1 - e0) {
+      case 1: b.template body<1>(e0, qk); break;
+      case 2: b.template body<2>(e0, qk); break;
+      case 3: b.template body<3>(e0, qk); break;
+      case 4: b.template body<4>(e0, qk); break;
+      case 5: b.template body<5>(e0, qk); break;
+      case 6: b.template body<6>(e0, qk); break;
+      default: b.general(e0, e1, qk); break;
     }
   }
   // CTA partial in fixed warp order
@@ -1046,9 +1218,12 @@ k_gat_input_attn_bwd(const __nv_bfloat16* __restrict__ x, int d, const float* __
 #pragma unroll
       for (int s = 0; s < V; ++s)
 #pragma unroll
-        for (int i = 0; i < XI; ++i) {
-          const int j = lane + 32 * i;
-          if (j < d) s_dc[s * d + j] = (w == 0 ? 0.f : s_dc[s * d + j]) + dc[s][i];
+        for (int i = 0; i < XP; ++i) {
+          const int j = 2 * (lane + 32 * i);
+          if (j < d) {
+            s_dc[s * d + j] = (w == 0 ? 0.f : s_dc[s * d + j]) + b.dc[s][i].x;
+            s_dc[s * d + j + 1] = (w == 0 ? 0.f : s_dc[s * d + j + 1]) + b.dc[s][i].y;
+          }
         }
     __syncthreads();
   }
@@ -1065,8 +1240,9 @@ extern "C" int fg_gat_input_attn_fwd(const uint16_t* x, int64_t d, int heads, co
                                      float* alpha, float* q, uint16_t* out, int64_t out_ld,
                                      void* s) {
   FG_CHECK_ARG(x && c && indptr && n_dst_dev && scores && alpha && q && out && rows >= max_dst &&
-                   (heads == 1 || heads == 2 || heads == 4 || heads == 8) && d >= 1 && d <= 256,
-               "fg_gat_input_attn_fwd: bad argument (heads in {1,2,4,8}, d <= 256)");
+                   (heads == 1 || heads == 2 || heads == 4 || heads == 8) && d >= 2 &&
+                   d <= 256 && d % 2 == 0,
+               "fg_gat_input_attn_fwd: bad argument (heads in {1,2,4,8}, even d <= 256)");
   if (out_ld == 0) out_ld = heads * d;
   FG_CHECK_ARG(out_ld >= heads * d, "fg_gat_input_attn_fwd: out_ld < heads * d");
   if (rows == 0) return FG_OK;
@@ -1074,16 +1250,16 @@ extern "C" int fg_gat_input_attn_fwd(const uint16_t* x, int64_t d, int heads, co
   auto* ob = reinterpret_cast<__nv_bfloat16*>(out);
   const dim3 grid(grid_for(rows * 32, 256));
   cudaStream_t st = as_stream(s);
-#define FG_IA_FWD(H, XI)                                                                   \
-  fg::k_gat_input_attn_fwd<H, XI><<<grid, 256, 0, st>>>(xb, (int)d, c, indptr, max_dst, rows, \
+#define FG_IA_FWD(H, XP)                                                                   \
+  fg::k_gat_input_attn_fwd<H, XP><<<grid, 256, 0, st>>>(xb, (int)d, c, indptr, max_dst, rows, \
                                                         n_dst_dev, slope, scores, alpha, q,  \
                                                         ob, out_ld)
   const bool small = d <= 128;
   switch (heads) {
-    case 1: if (small) FG_IA_FWD(1, 4); else FG_IA_FWD(1, 8); break;
-    case 2: if (small) FG_IA_FWD(2, 4); else FG_IA_FWD(2, 8); break;
-    case 4: if (small) FG_IA_FWD(4, 4); else FG_IA_FWD(4, 8); break;
-    default: if (small) FG_IA_FWD(8, 4); else FG_IA_FWD(8, 8); break;
+    case 1: if (small) FG_IA_FWD(1, 2); else FG_IA_FWD(1, 4); break;
+    case 2: if (small) FG_IA_FWD(2, 2); else FG_IA_FWD(2, 4); break;
+    case 4: if (small) FG_IA_FWD(4, 2); else FG_IA_FWD(4, 4); break;
+    default: if (small) FG_IA_FWD(8, 2); else FG_IA_FWD(8, 4); break;
   }
 #undef FG_IA_FWD
   FG_LAUNCH_CHECK();
@@ -1096,23 +1272,24 @@ extern "C" int fg_gat_input_attn_bwd(const uint16_t* x, int64_t d, int heads,
                                      const int64_t* n_dst_dev, float slope, float* dalpha,
                                      float* partial, void* s) {
   FG_CHECK_ARG(x && scores && alpha && q && dA && indptr && n_dst_dev && dalpha && partial &&
-                   (heads == 1 || heads == 2 || heads == 4 || heads == 8) && d >= 1 && d <= 256,
-               "fg_gat_input_attn_bwd: bad argument (heads in {1,2,4,8}, d <= 256)");
+                   (heads == 1 || heads == 2 || heads == 4 || heads == 8) && d >= 2 &&
+                   d <= 256 && d % 2 == 0,
+               "fg_gat_input_attn_bwd: bad argument (heads in {1,2,4,8}, even d <= 256)");
   const auto* xb = reinterpret_cast<const __nv_bfloat16*>(x);
   const auto* gb = reinterpret_cast<const __nv_bfloat16*>(dA);
   const dim3 grid((unsigned)fg_gat_input_attn_bwd_blocks());
   const size_t smem = (size_t)2 * heads * d * sizeof(float);
   cudaStream_t st = as_stream(s);
-#define FG_IA_BWD(H, XI)                                                                  \
-  fg::k_gat_input_attn_bwd<H, XI><<<grid, 256, smem, st>>>(xb, (int)d, scores, alpha, q, gb, \
+#define FG_IA_BWD(H, XP)                                                                  \
+  fg::k_gat_input_attn_bwd<H, XP><<<grid, 256, smem, st>>>(xb, (int)d, scores, alpha, q, gb, \
                                                            indptr, max_dst, n_dst_dev, slope, \
                                                            dalpha, partial)
   const bool small = d <= 128;
   switch (heads) {
-    case 1: if (small) FG_IA_BWD(1, 4); else FG_IA_BWD(1, 8); break;
-    case 2: if (small) FG_IA_BWD(2, 4); else FG_IA_BWD(2, 8); break;
-    case 4: if (small) FG_IA_BWD(4, 4); else FG_IA_BWD(4, 8); break;
-    default: if (small) FG_IA_BWD(8, 4); else FG_IA_BWD(8, 8); break;
+    case 1: if (small) FG_IA_BWD(1, 2); else FG_IA_BWD(1, 4); break;
+    case 2: if (small) FG_IA_BWD(2, 2); else FG_IA_BWD(2, 4); break;
+    case 4: if (small) FG_IA_BWD(4, 2); else FG_IA_BWD(4, 4); break;
+    default: if (small) FG_IA_BWD(8, 2); else FG_IA_BWD(8, 4); break;
   }
 #undef FG_IA_BWD
   FG_LAUNCH_CHECK();
