@@ -905,6 +905,10 @@ struct IaFwd {
   template <int C>
   __device__ __forceinline__ void body(int32_t e0, float* __restrict__ qv,
                                        float2 (&acc)[XP][HEADS]) const {
+    // after the transpose-reduce lane L holds score my(L) of every pick: the
+    // lanes with my = k < H run head k's softmax on their own registers
+    // (one instruction per pick for all heads); the accumulation then takes
+    // alpha[e][k] from a lane of head k (H shuffles per pick)
     float2 xr[C][XP];
     float rs[C];
 #pragma unroll
@@ -914,38 +918,30 @@ struct IaFwd {
     for (int e = 0; e < C; ++e) {
       rs[e] = scores(xr[e]);
       if (writer) sc[(int64_t)(e0 + e) * V + my] = rs[e];
-      qacc += my >= HEADS ? rs[e] : 0.f;
+      qacc += rs[e];
     }
-    float qk[HEADS], mx[HEADS], den[HEADS], sl[C][HEADS];
-#pragma unroll
-    for (int k = 0; k < HEADS; ++k) {
-      qk[k] = __shfl_sync(0xffffffffu, qacc, tr_lane<V>(HEADS + k)) * (1.f / C);
-      if (lane == k) qv[k] = qk[k];
-    }
-#pragma unroll
-    for (int e = 0; e < C; ++e)
-#pragma unroll
-      for (int k = 0; k < HEADS; ++k) {
-        sl[e][k] = leaky(__shfl_sync(0xffffffffu, rs[e], tr_lane<V>(k)) + qk[k], slope);
-        mx[k] = e ? fmaxf(mx[k], sl[e][k]) : sl[e][k];
-      }
-#pragma unroll
-    for (int e = 0; e < C; ++e)
-#pragma unroll
-      for (int k = 0; k < HEADS; ++k) {
-        sl[e][k] = __expf(sl[e][k] - mx[k]);
-        den[k] = e ? den[k] + sl[e][k] : sl[e][k];
-      }
-#pragma unroll
-    for (int k = 0; k < HEADS; ++k) den[k] = 1.f / den[k];
+    const int hk = my & (HEADS - 1);  // this lane's head (el lanes: my; er lanes: my - H)
+    const float qk = __shfl_sync(0xffffffffu, qacc, tr_lane<V>(HEADS + hk)) * (1.f / C);
+    if (writer && my < HEADS) qv[my] = qk;
+    float mx = -INFINITY, den = 0.f;
 #pragma unroll
     for (int e = 0; e < C; ++e) {
+      rs[e] = leaky(rs[e] + qk, slope);
+      mx = fmaxf(mx, rs[e]);
+    }
+#pragma unroll
+    for (int e = 0; e < C; ++e) {
+      rs[e] = __expf(rs[e] - mx);
+      den += rs[e];
+    }
+    const float inv = 1.f / den;
+#pragma unroll
+    for (int e = 0; e < C; ++e) {
+      rs[e] *= inv;  // alpha[e][hk] (meaningful on the el lanes)
+      if (writer && my < HEADS) alpha[(int64_t)(e0 + e) * HEADS + my] = rs[e];
       float al[HEADS];
 #pragma unroll
-      for (int k = 0; k < HEADS; ++k) {
-        al[k] = sl[e][k] * den[k];
-        if (lane == k) alpha[(int64_t)(e0 + e) * HEADS + k] = al[k];
-      }
+      for (int k = 0; k < HEADS; ++k) al[k] = __shfl_sync(0xffffffffu, rs[e], tr_lane<V>(k));
       accum(acc, al, xr[e]);
     }
   }
@@ -1093,35 +1089,42 @@ struct IaBwd {
   }
   template <int C>
   __device__ __forceinline__ void body(int32_t e0, const float (&qk)[HEADS]) {
+    // after the transpose-reduce lane L holds dalpha[e][my(L)]: the softmax
+    // backward of head my runs on that lane's registers; the accumulation
+    // takes del[e][k] (and the er share) from a lane of head k
     float2 xr[C][XP];
-    float al[C][HEADS], dl[C][HEADS], dot[HEADS], sh[HEADS];
+    float da[C], al[C];
+#pragma unroll
+    for (int e = 0; e < C; ++e) load_row2<XP>(x + (int64_t)(e0 + e) * d, d, lane, xr[e]);
+#pragma unroll
+    for (int e = 0; e < C; ++e) al[e] = alpha[(int64_t)(e0 + e) * HEADS + my];
+    float dot = 0.f;
 #pragma unroll
     for (int e = 0; e < C; ++e) {
-      load_row2<XP>(x + (int64_t)(e0 + e) * d, d, lane, xr[e]);
-#pragma unroll
-      for (int k = 0; k < HEADS; ++k) al[e][k] = alpha[(int64_t)(e0 + e) * HEADS + k];
+      da[e] = dots(xr[e]);
+      dot = fmaf(al[e], da[e], dot);
     }
+    float qm = qk[0];
+#pragma unroll
+    for (int k = 1; k < HEADS; ++k) qm = my == k ? qk[k] : qm;
+    float shm = 0.f;
 #pragma unroll
     for (int e = 0; e < C; ++e) {
-      const float r = dots(xr[e]);
-#pragma unroll
-      for (int k = 0; k < HEADS; ++k) {
-        dl[e][k] = __shfl_sync(0xffffffffu, r, tr_lane<HEADS>(k));  // dalpha
-        dot[k] = e ? fmaf(al[e][k], dl[e][k], dot[k]) : al[e][k] * dl[e][k];
-      }
+      const float ds = al[e] * (da[e] - dot);
+      da[e] = sc[(int64_t)(e0 + e) * V + my] + qm > 0.f ? ds : slope * ds;  // del[e][my]
+      shm += da[e];
     }
+    shm *= 1.f / C;
+    float sh[HEADS];
 #pragma unroll
-    for (int e = 0; e < C; ++e)
+    for (int k = 0; k < HEADS; ++k) sh[k] = __shfl_sync(0xffffffffu, shm, tr_lane<HEADS>(k));
 #pragma unroll
-      for (int k = 0; k < HEADS; ++k) {
-        const float ds = al[e][k] * (dl[e][k] - dot[k]);
-        dl[e][k] = sc[(int64_t)(e0 + e) * V + k] + qk[k] > 0.f ? ds : slope * ds;
-        sh[k] = e ? sh[k] + dl[e][k] : dl[e][k];
-      }
+    for (int e = 0; e < C; ++e) {
+      float dl[HEADS];
 #pragma unroll
-    for (int k = 0; k < HEADS; ++k) sh[k] *= 1.f / C;
-#pragma unroll
-    for (int e = 0; e < C; ++e) accum(xr[e], dl[e], sh);
+      for (int k = 0; k < HEADS; ++k) dl[k] = __shfl_sync(0xffffffffu, da[e], tr_lane<HEADS>(k));
+      accum(xr[e], dl, sh);
+    }
   }
   __device__ void general(int32_t e0, int32_t e1, const float (&qk)[HEADS]) {
     float dot[HEADS], sh[HEADS];
