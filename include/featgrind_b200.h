@@ -434,8 +434,11 @@ int fg_gat_code_xagg_fwd(const fg_codec_desc* codec, const uint16_t* x_rows,
                          const int32_t* picks, int64_t d, int heads, const float* alpha,
                          const int32_t* indptr, int64_t max_dst, const int64_t* n_dst_dev,
                          uint16_t* out, int64_t out_ld, void* cuda_stream);
-/* Fused GAT input layer over the decoded picks x [E, d] (bf16, row e = pick
- * e; each pick belongs to one destination), heads in {1, 2, 4, 8}, d <= 256,
+/* Fused GAT input layer over the picks (each pick belongs to one
+ * destination): x_rows = decoded bf16 rows [E, d] (row e = pick e), or
+ * x_rows NULL with an 8-bit SQ codec (fp32 LUT) and picks [E] -- the code
+ * rows are then read in place and decoded in registers; heads in {1, 2, 4, 8},
+ * even d <= 256,
  * c = [a_l . W_k ; a_r . W_k] fp32 [2 heads, d]:
  *   fg_gat_input_attn_fwd  scores[e] = [el | er] = x_e c^T (fp32 [E, 2 heads]),
  *                          q, alpha as fg_gat_softmax_fwd, and
@@ -447,12 +450,14 @@ int fg_gat_code_xagg_fwd(const fg_codec_desc* codec, const uint16_t* x_rows,
  *                          partial[b] = sum_{e in CTA b} [del | der]_e x_e
  *                          (fp32 [fg_gat_input_attn_bwd_blocks()][2 heads][d],
  *                          summed by the caller; deterministic). */
-int fg_gat_input_attn_fwd(const uint16_t* x, int64_t d, int heads, const float* c,
+int fg_gat_input_attn_fwd(const fg_codec_desc* codec, const uint16_t* x_rows,
+                          const int32_t* picks, int64_t d, int heads, const float* c,
                           const int32_t* indptr, int64_t max_dst, int64_t rows,
                           const int64_t* n_dst_dev, float slope, float* scores, float* alpha,
                           float* q, uint16_t* out, int64_t out_ld, void* cuda_stream);
 int64_t fg_gat_input_attn_bwd_blocks(void);
-int fg_gat_input_attn_bwd(const uint16_t* x, int64_t d, int heads, const float* scores,
+int fg_gat_input_attn_bwd(const fg_codec_desc* codec, const uint16_t* x_rows,
+                          const int32_t* picks, int64_t d, int heads, const float* scores,
                           const float* alpha, const float* q, const uint16_t* dA,
                           const int32_t* indptr, int64_t max_dst, const int64_t* n_dst_dev,
                           float slope, float* dalpha, float* partial, void* cuda_stream);

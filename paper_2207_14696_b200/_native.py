@@ -94,11 +94,11 @@ _SIGS = {
     "fg_gat_code_xagg_fwd": (ci, [C.POINTER(CodecDesc), vp, vp, i64, ci, vp, vp, i64, vp, vp,
                                   i64, vp]),
     "fg_gat_elu_fwd": (ci, [vp, ci, i64, vp, i64, i64, vp, vp]),
-    "fg_gat_input_attn_fwd": (ci, [vp, i64, ci, vp, vp, i64, i64, vp, C.c_float, vp, vp, vp, vp,
-                                   i64, vp]),
+    "fg_gat_input_attn_fwd": (ci, [C.POINTER(CodecDesc), vp, vp, i64, ci, vp, vp, i64, i64, vp,
+                                   C.c_float, vp, vp, vp, vp, i64, vp]),
     "fg_gat_input_attn_bwd_blocks": (i64, []),
-    "fg_gat_input_attn_bwd": (ci, [vp, i64, ci, vp, vp, vp, vp, vp, i64, vp, C.c_float, vp, vp,
-                                   vp]),
+    "fg_gat_input_attn_bwd": (ci, [C.POINTER(CodecDesc), vp, vp, i64, ci, vp, vp, vp, vp, vp,
+                                   i64, vp, C.c_float, vp, vp, vp]),
     "fg_gat_elu_bwd": (ci, [vp, vp, i64, vp, ci, vp]),
     "fg_gat_code_xagg_bwd": (ci, [C.POINTER(CodecDesc), vp, vp, i64, ci, vp, i64, vp, vp, vp,
                                   vp]),

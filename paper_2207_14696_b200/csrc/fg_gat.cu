@@ -732,8 +732,8 @@ __global__ void k_gat_elu_fwd(const void* __restrict__ in, int64_t ld_in,
     uint32_t w[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      const float x0 = f[2 * i] > 0.f ? f[2 * i] : expm1f(f[2 * i]);
-      const float x1 = f[2 * i + 1] > 0.f ? f[2 * i + 1] : expm1f(f[2 * i + 1]);
+      const float x0 = f[2 * i] > 0.f ? f[2 * i] : __expf(f[2 * i]) - 1.f;
+      const float x1 = f[2 * i + 1] > 0.f ? f[2 * i + 1] : __expf(f[2 * i + 1]) - 1.f;
       const __nv_bfloat162 h = __floats2bfloat162_rn(x0, x1);
       w[i] = *reinterpret_cast<const uint32_t*>(&h);
     }
@@ -864,16 +864,47 @@ __device__ __forceinline__ void load_row2(const __nv_bfloat16* __restrict__ xr, 
   }
 }
 
+// Pick rows as the fused kernels read them: KIND 0 = decoded bf16 rows (row
+// e = pick e, pitch d); KIND 1 = 8-bit SQ code rows read in place (row of
+// node picks[e], decoded through the 256-entry LUT in shared memory): the
+// picks' decoded matrix is never written.
+struct IaSrc {
+  const __nv_bfloat16* __restrict__ x;
+  const uint8_t* __restrict__ rows;
+  int64_t stride;
+  const int32_t* __restrict__ picks;
+  const float* lut;  // shared memory (KIND 1)
+};
+template <int XP, int KIND>
+__device__ __forceinline__ void ia_load(const IaSrc& src, int64_t e, int d, int lane,
+                                        float2 (&xv)[XP]) {
+  if (KIND == 0) {
+    load_row2<XP>(src.x + e * d, d, lane, xv);
+  } else {
+    const uint8_t* r = src.rows + (int64_t)__ldg(src.picks + e) * src.stride;
+#pragma unroll
+    for (int i = 0; i < XP; ++i) {
+      const int j = 2 * (lane + 32 * i);
+      if (j < d) {
+        const uint32_t w = *reinterpret_cast<const uint16_t*>(r + j);
+        xv[i] = make_float2(src.lut[w & 255u], src.lut[w >> 8]);
+      } else {
+        xv[i] = make_float2(0.f, 0.f);
+      }
+    }
+  }
+}
+
 // Destinations with C <= kIaMaxP picks run a body specialised on C (rows,
 // scores and attention in registers, no per-pick branches: the counts are
 // warp-uniform, one switch per destination); larger ones take the general
 // path through the scores / alpha / dalpha buffers.
 constexpr int kIaMaxP = 6;
 
-template <int HEADS, int XP>
+template <int HEADS, int XP, int KIND>
 struct IaFwd {
   static constexpr int V = 2 * HEADS;
-  const __nv_bfloat16* __restrict__ x;
+  IaSrc src;
   int d, lane, my;
   bool writer;
   float slope;
@@ -912,7 +943,7 @@ struct IaFwd {
     float2 xr[C][XP];
     float rs[C];
 #pragma unroll
-    for (int e = 0; e < C; ++e) load_row2<XP>(x + (int64_t)(e0 + e) * d, d, lane, xr[e]);
+    for (int e = 0; e < C; ++e) ia_load<XP, KIND>(src, e0 + e, d, lane, xr[e]);
     float qacc = 0.f;
 #pragma unroll
     for (int e = 0; e < C; ++e) {
@@ -951,7 +982,7 @@ struct IaFwd {
     float qacc = 0.f;
     for (int32_t e = e0; e < e1; ++e) {
       float2 xv[XP];
-      load_row2<XP>(x + (int64_t)e * d, d, lane, xv);
+      ia_load<XP, KIND>(src, e, d, lane, xv);
       const float r = scores(xv);
       if (writer) sc[(int64_t)e * V + my] = r;
       if (my >= HEADS) qacc += r;
@@ -979,7 +1010,7 @@ struct IaFwd {
     for (int32_t e = e0; e < e1; ++e) {
       float2 xv[XP];
       float al[HEADS];
-      load_row2<XP>(x + (int64_t)e * d, d, lane, xv);
+      ia_load<XP, KIND>(src, e, d, lane, xv);
 #pragma unroll
       for (int k = 0; k < HEADS; ++k) {
         al[k] = __expf(leaky(sc[(int64_t)e * V + k] + qk[k], slope) - mx[k]) * inv[k];
@@ -990,17 +1021,23 @@ struct IaFwd {
   }
 };
 
-template <int HEADS, int XP>
+template <int HEADS, int XP, int KIND>
 __global__ void __launch_bounds__(256, 2)
-k_gat_input_attn_fwd(const __nv_bfloat16* __restrict__ x, int d, const float* __restrict__ c,
+k_gat_input_attn_fwd(IaSrc src, int d, const float* __restrict__ c,
                      const int32_t* __restrict__ indptr, int64_t max_dst, int64_t rows,
                      const int64_t* __restrict__ ndst_dev, float slope, float* __restrict__ sc,
                      float* __restrict__ alpha, float* __restrict__ q,
                      __nv_bfloat16* __restrict__ out, int64_t out_ld) {
   constexpr int V = 2 * HEADS;
   const int64_t live = min64(*ndst_dev, max_dst);
-  IaFwd<HEADS, XP> f;
-  f.x = x;
+  __shared__ float s_lut[KIND ? 256 : 1];
+  if (KIND) {
+    for (int t = threadIdx.x; t < 256; t += blockDim.x) s_lut[t] = src.lut[t];
+    __syncthreads();
+    src.lut = s_lut;
+  }
+  IaFwd<HEADS, XP, KIND> f;
+  f.src = src;
   f.d = d;
   f.lane = threadIdx.x & 31;
   f.my = tr_index<V>(f.lane);
@@ -1051,10 +1088,10 @@ k_gat_input_attn_fwd(const __nv_bfloat16* __restrict__ x, int d, const float* __
   }
 }
 
-template <int HEADS, int XP>
+template <int HEADS, int XP, int KIND>
 struct IaBwd {
   static constexpr int V = 2 * HEADS;
-  const __nv_bfloat16* __restrict__ x;
+  IaSrc src;
   const float* __restrict__ sc;
   const float* __restrict__ alpha;
   float* __restrict__ dalpha;
@@ -1095,7 +1132,7 @@ struct IaBwd {
     float2 xr[C][XP];
     float da[C], al[C];
 #pragma unroll
-    for (int e = 0; e < C; ++e) load_row2<XP>(x + (int64_t)(e0 + e) * d, d, lane, xr[e]);
+    for (int e = 0; e < C; ++e) ia_load<XP, KIND>(src, e0 + e, d, lane, xr[e]);
 #pragma unroll
     for (int e = 0; e < C; ++e) al[e] = alpha[(int64_t)(e0 + e) * HEADS + my];
     float dot = 0.f;
@@ -1132,7 +1169,7 @@ struct IaBwd {
     for (int k = 0; k < HEADS; ++k) dot[k] = sh[k] = 0.f;
     for (int32_t e = e0; e < e1; ++e) {  // dalpha[e, k] = <dA[v, k], x_e>
       float2 xv[XP];
-      load_row2<XP>(x + (int64_t)e * d, d, lane, xv);
+      ia_load<XP, KIND>(src, e, d, lane, xv);
       const float r = dots(xv);
       if (writer) dalpha[(int64_t)e * HEADS + my] = r;
     }
@@ -1158,15 +1195,15 @@ struct IaBwd {
         const float ds = alpha[(int64_t)e * HEADS + k] * (dalpha[(int64_t)e * HEADS + k] - dot[k]);
         dl[k] = sc[(int64_t)e * V + k] + qk[k] > 0.f ? ds : slope * ds;
       }
-      load_row2<XP>(x + (int64_t)e * d, d, lane, xv);
+      ia_load<XP, KIND>(src, e, d, lane, xv);
       accum(xv, dl, sh);
     }
   }
 };
 
-template <int HEADS, int XP>
+template <int HEADS, int XP, int KIND>
 __global__ void __launch_bounds__(256, 2)
-k_gat_input_attn_bwd(const __nv_bfloat16* __restrict__ x, int d, const float* __restrict__ sc,
+k_gat_input_attn_bwd(IaSrc src, int d, const float* __restrict__ sc,
                      const float* __restrict__ alpha, const float* __restrict__ q,
                      const __nv_bfloat16* __restrict__ dA, const int32_t* __restrict__ indptr,
                      int64_t max_dst, const int64_t* __restrict__ ndst_dev, float slope,
@@ -1175,8 +1212,14 @@ k_gat_input_attn_bwd(const __nv_bfloat16* __restrict__ x, int d, const float* __
   extern __shared__ float s_dc[];  // [V][d]
   const int64_t live = min64(*ndst_dev, max_dst);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  IaBwd<HEADS, XP> b;
-  b.x = x;
+  __shared__ float s_lut[KIND ? 256 : 1];
+  if (KIND) {
+    for (int t = threadIdx.x; t < 256; t += blockDim.x) s_lut[t] = src.lut[t];
+    __syncthreads();
+    src.lut = s_lut;
+  }
+  IaBwd<HEADS, XP, KIND> b;
+  b.src = src;
   b.sc = sc;
   b.alpha = alpha;
   b.dalpha = dalpha;
@@ -1237,26 +1280,54 @@ k_gat_input_attn_bwd(const __nv_bfloat16* __restrict__ x, int d, const float* __
 
 extern "C" int64_t fg_gat_input_attn_bwd_blocks(void) { return 2 * sm_count(); }
 
-extern "C" int fg_gat_input_attn_fwd(const uint16_t* x, int64_t d, int heads, const float* c,
+static bool ia_source(const fg_codec_desc* codec, const uint16_t* x_rows, const int32_t* picks,
+                      int64_t d, fg::IaSrc& src, int& kind) {
+  src = fg::IaSrc{};
+  if (x_rows) {
+    src.x = reinterpret_cast<const __nv_bfloat16*>(x_rows);
+    kind = 0;
+    return true;
+  }
+  if (!codec || !picks || codec->kind != FG_CODEC_SQ || codec->bits != 8 ||
+      codec->elem_bits != 32 || codec->d != d || codec->row_stride % 2)
+    return false;
+  src.rows = codec->rows;
+  src.stride = codec->row_stride;
+  src.picks = picks;
+  src.lut = static_cast<const float*>(codec->table);
+  kind = 1;
+  return true;
+}
+
+extern "C" int fg_gat_input_attn_fwd(const fg_codec_desc* codec, const uint16_t* x_rows,
+                                     const int32_t* picks, int64_t d, int heads, const float* c,
                                      const int32_t* indptr, int64_t max_dst, int64_t rows,
                                      const int64_t* n_dst_dev, float slope, float* scores,
                                      float* alpha, float* q, uint16_t* out, int64_t out_ld,
                                      void* s) {
-  FG_CHECK_ARG(x && c && indptr && n_dst_dev && scores && alpha && q && out && rows >= max_dst &&
+  fg::IaSrc src;
+  int kind = 0;
+  FG_CHECK_ARG(ia_source(codec, x_rows, picks, d, src, kind),
+               "fg_gat_input_attn_fwd: x_rows, or an 8-bit SQ codec (fp32 LUT) + picks");
+  FG_CHECK_ARG(c && indptr && n_dst_dev && scores && alpha && q && out && rows >= max_dst &&
                    (heads == 1 || heads == 2 || heads == 4 || heads == 8) && d >= 2 &&
                    d <= 256 && d % 2 == 0,
                "fg_gat_input_attn_fwd: bad argument (heads in {1,2,4,8}, even d <= 256)");
   if (out_ld == 0) out_ld = heads * d;
   FG_CHECK_ARG(out_ld >= heads * d, "fg_gat_input_attn_fwd: out_ld < heads * d");
   if (rows == 0) return FG_OK;
-  const auto* xb = reinterpret_cast<const __nv_bfloat16*>(x);
   auto* ob = reinterpret_cast<__nv_bfloat16*>(out);
   const dim3 grid(grid_for(rows * 32, 256));
   cudaStream_t st = as_stream(s);
-#define FG_IA_FWD(H, XP)                                                                   \
-  fg::k_gat_input_attn_fwd<H, XP><<<grid, 256, 0, st>>>(xb, (int)d, c, indptr, max_dst, rows, \
-                                                        n_dst_dev, slope, scores, alpha, q,  \
-                                                        ob, out_ld)
+#define FG_IA_FWD(H, XP)                                                                       \
+  do {                                                                                         \
+    if (kind)                                                                                  \
+      fg::k_gat_input_attn_fwd<H, XP, 1><<<grid, 256, 0, st>>>(src, (int)d, c, indptr,         \
+          max_dst, rows, n_dst_dev, slope, scores, alpha, q, ob, out_ld);                      \
+    else                                                                                       \
+      fg::k_gat_input_attn_fwd<H, XP, 0><<<grid, 256, 0, st>>>(src, (int)d, c, indptr,         \
+          max_dst, rows, n_dst_dev, slope, scores, alpha, q, ob, out_ld);                      \
+  } while (0)
   const bool small = d <= 128;
   switch (heads) {
     case 1: if (small) FG_IA_FWD(1, 2); else FG_IA_FWD(1, 4); break;
@@ -1269,24 +1340,33 @@ extern "C" int fg_gat_input_attn_fwd(const uint16_t* x, int64_t d, int heads, co
   return FG_OK;
 }
 
-extern "C" int fg_gat_input_attn_bwd(const uint16_t* x, int64_t d, int heads,
+extern "C" int fg_gat_input_attn_bwd(const fg_codec_desc* codec, const uint16_t* x_rows,
+                                     const int32_t* picks, int64_t d, int heads,
                                      const float* scores, const float* alpha, const float* q,
                                      const uint16_t* dA, const int32_t* indptr, int64_t max_dst,
                                      const int64_t* n_dst_dev, float slope, float* dalpha,
                                      float* partial, void* s) {
-  FG_CHECK_ARG(x && scores && alpha && q && dA && indptr && n_dst_dev && dalpha && partial &&
+  fg::IaSrc src;
+  int kind = 0;
+  FG_CHECK_ARG(ia_source(codec, x_rows, picks, d, src, kind),
+               "fg_gat_input_attn_bwd: x_rows, or an 8-bit SQ codec (fp32 LUT) + picks");
+  FG_CHECK_ARG(scores && alpha && q && dA && indptr && n_dst_dev && dalpha && partial &&
                    (heads == 1 || heads == 2 || heads == 4 || heads == 8) && d >= 2 &&
                    d <= 256 && d % 2 == 0,
                "fg_gat_input_attn_bwd: bad argument (heads in {1,2,4,8}, even d <= 256)");
-  const auto* xb = reinterpret_cast<const __nv_bfloat16*>(x);
   const auto* gb = reinterpret_cast<const __nv_bfloat16*>(dA);
   const dim3 grid((unsigned)fg_gat_input_attn_bwd_blocks());
   const size_t smem = (size_t)2 * heads * d * sizeof(float);
   cudaStream_t st = as_stream(s);
-#define FG_IA_BWD(H, XP)                                                                  \
-  fg::k_gat_input_attn_bwd<H, XP><<<grid, 256, smem, st>>>(xb, (int)d, scores, alpha, q, gb, \
-                                                           indptr, max_dst, n_dst_dev, slope, \
-                                                           dalpha, partial)
+#define FG_IA_BWD(H, XP)                                                                       \
+  do {                                                                                         \
+    if (kind)                                                                                  \
+      fg::k_gat_input_attn_bwd<H, XP, 1><<<grid, 256, smem, st>>>(src, (int)d, scores, alpha, \
+          q, gb, indptr, max_dst, n_dst_dev, slope, dalpha, partial);                          \
+    else                                                                                       \
+      fg::k_gat_input_attn_bwd<H, XP, 0><<<grid, 256, smem, st>>>(src, (int)d, scores, alpha, \
+          q, gb, indptr, max_dst, n_dst_dev, slope, dalpha, partial);                          \
+  } while (0)
   const bool small = d <= 128;
   switch (heads) {
     case 1: if (small) FG_IA_BWD(1, 2); else FG_IA_BWD(1, 4); break;

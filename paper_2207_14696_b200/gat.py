@@ -412,6 +412,9 @@ class GatTrainer:
         self._views = [_LayerViews(layer, self.flat_param, self.flat_grad, self.flat_bf16)
                        for layer in self.model.layers]
         self._ones = torch.ones(max(self.caps), dtype=torch.float32, device=self.device)
+        desc = codec.desc
+        self._direct = (os.environ.get("FG_GAT_DIRECT", "0") == "1" and desc.kind == N.CODEC_SQ
+                        and desc.bits == 8 and desc.elem_bits == 32 and desc.row_stride % 2 == 0)
         self.graph = None
 
     def _decode(self, sb):
@@ -467,9 +470,14 @@ class GatTrainer:
         s = N.stream_handle()
         dev = self.device
         f32, bf16 = torch.float32, torch.bfloat16
-        x = self._decode(sb).x  # [pick_cap, d] bf16, pick order
+        # the picks: decoded bf16 rows, one per pick (k_sq_gather); FG_GAT_DIRECT=1
+        # reads 8-bit SQ code rows in place instead (no decoded matrix, but a
+        # dependent pick-id load per row: measured 1.225 vs 1.169 ms/step)
+        L1 = L - 1
+        src = PickSource(self.codec, sb.picks[L1], sb.n_picks[L1], self.pick_cap,
+                         decoded=not self._direct)
         saved = []
-        h = x
+        h = src
         for i, v in enumerate(self._views):
             l = L - 1 - i
             Hh, Fh, D = v.heads, v.F, v.D
@@ -489,7 +497,7 @@ class GatTrainer:
                 sc = torch.empty((e_cap, 2 * Hh), dtype=f32, device=dev)
                 rows = _round_up(self.caps[l], 64)
                 A = torch.empty((rows, Hh * D + 8), dtype=bf16, device=dev)
-                N.call("fg_gat_input_attn_fwd", N.ptr(h), D, Hh, N.ptr(c), N.ptr(sb.indptr[l]),
+                N.call("fg_gat_input_attn_fwd", *src.head(), D, Hh, N.ptr(c), N.ptr(sb.indptr[l]),
                        self.caps[l], rows, N.ptr(sb.n_nodes[l]), 0.2, N.ptr(sc), N.ptr(alpha),
                        N.ptr(q), N.ptr(A), Hh * D + 8, s)
                 v.refresh_block_diag()
@@ -539,9 +547,9 @@ class GatTrainer:
                 dalpha = torch.empty((e_cap, Hh), dtype=f32, device=dev)
                 part = torch.empty((N.lib().fg_gat_input_attn_bwd_blocks(), 2 * Hh, D),
                                    dtype=f32, device=dev)
-                N.call("fg_gat_input_attn_bwd", N.ptr(h), D, Hh, N.ptr(sc), N.ptr(alpha), N.ptr(q),
-                       N.ptr(dA), N.ptr(sb.indptr[l]), self.caps[l], N.ptr(sb.n_nodes[l]), 0.2,
-                       N.ptr(dalpha), N.ptr(part), s)
+                N.call("fg_gat_input_attn_bwd", *src.head(), D, Hh, N.ptr(sc), N.ptr(alpha),
+                       N.ptr(q), N.ptr(dA), N.ptr(sb.indptr[l]), self.caps[l],
+                       N.ptr(sb.n_nodes[l]), 0.2, N.ptr(dalpha), N.ptr(part), s)
                 dc = part.sum(0)
             else:
                 ds = torch.zeros((h.shape[0], 2 * Hh), dtype=f32, device=dev)

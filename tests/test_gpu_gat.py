@@ -183,9 +183,11 @@ def test_gat_gradients_match_cpu_oracle_model(codec_kind, decoded):
         assert g_ref is not None and g_ref.norm() > 0, name
         rel = ((g - g_ref).norm() / g_ref.norm()).item()
         assert rel < 1e-1, (name, rel)  # bf16 autocast vs fp32
-    if decoded:
-        # the trainer's explicit step (no autograd) on the same batch: same
-        # loss, same gradient for every parameter, written into flat_grad
+    # the trainer's explicit step (no autograd) on the same batch: same loss,
+    # same gradient for every parameter, written into flat_grad; decoded=False
+    # runs it with the fused input kernels reading SQ8 code rows in place
+    if decoded or codec_kind == "sq8":
+        t._direct = not decoded
         t.flat_grad.fill_(float("nan"))   # every element must be written
         t.forward_backward(sb)
         torch.cuda.synchronize()
