@@ -333,6 +333,15 @@ int fg_block_transpose(const int32_t* src_local, const int64_t* n_edges_dev,
                        int32_t* t_indptr, int32_t* t_dst, float* t_w,
                        const float* edge_w, void* scratch,
                        int64_t scratch_bytes, void* cuda_stream);
+/* Same transpose, also recording for every entry its edge id (t_eid: the
+ * edge's position in local[]; GAT's gather-form backward reads the edge's
+ * attention coefficient). */
+int fg_block_transpose_ex(const int32_t* src_local, const int64_t* n_edges_dev,
+                          int64_t cap_e, const int32_t* indptr,
+                          const int64_t* num_dst_dev, int64_t max_dst, int max_per_dst,
+                          int64_t cap_src, int32_t* t_indptr, int32_t* t_dst, float* t_w,
+                          int32_t* t_eid, const float* edge_w, void* scratch,
+                          int64_t scratch_bytes, void* cuda_stream);
 int fg_block_mean_bwd_t(const uint16_t* grad_out, int64_t h_dim, int64_t g_ld,
                         const int32_t* t_indptr, const int32_t* t_dst,
                         const float* t_w, const int64_t* n_src_dev, int64_t cap_src,
@@ -461,6 +470,17 @@ int fg_gat_input_attn_bwd(const fg_codec_desc* codec, const uint16_t* x_rows,
                           const float* alpha, const float* q, const uint16_t* dA,
                           const int32_t* indptr, int64_t max_dst, const int64_t* n_dst_dev,
                           float slope, float* dalpha, float* partial, void* cuda_stream);
+/* Gather-form fg_gat_agg_bwd over the block's transpose with edge ids
+ * (fg_block_transpose_ex): dz written once in bf16 [cap_src, hf] (rows
+ * without entries or past *n_src_dev: zeros), dalpha written once per live
+ * edge and head; no zero fills or atomics.  Needs hf <= 256 and hf/8 lanes
+ * split into power-of-2 groups per head (or heads == 1):
+ * fg_gat_agg_bwd_t_supported. */
+int fg_gat_agg_bwd_t_supported(int64_t hf, int heads);
+int fg_gat_agg_bwd_t(const uint16_t* z, int64_t hf, int heads, const float* alpha,
+                     const int32_t* t_indptr, const int32_t* t_dst, const int32_t* t_eid,
+                     const int64_t* n_src_dev, int64_t cap_src, const float* dout, uint16_t* dz,
+                     float* dalpha, void* cuda_stream);
 /* ELU between GAT layers: h = bf16(ELU(in + bias)) for in fp32 (in_f32 = 1)
  * or bf16 rows of pitch ld_in, bias fp32 [cols] or NULL (cols % 8 == 0); and
  * out = dh * ELU'(.) from the forward's output h (1 where h > 0, h + 1

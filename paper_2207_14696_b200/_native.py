@@ -74,6 +74,8 @@ _SIGS = {
     "fg_f32_to_bf16": (ci, [vp, i64, vp, vp, vp]),
     "fg_block_transpose_scratch_bytes": (i64, [i64]),
     "fg_block_transpose": (ci, [vp, vp, i64, vp, vp, i64, ci, i64, vp, vp, vp, vp, vp, i64, vp]),
+    "fg_block_transpose_ex": (ci, [vp, vp, i64, vp, vp, i64, ci, i64, vp, vp, vp, vp, vp, vp, i64,
+                                   vp]),
     "fg_block_mean_bwd_t": (ci, [vp, i64, i64, vp, vp, vp, vp, i64, vp, vp, vp]),
     "fg_block_mean_bwd_t_bits": (ci, [vp, i64, i64, vp, vp, vp, vp, i64, vp, vp, vp]),
     "fg_block_mean_wgrad_supported": (ci, [i64, i64]),
@@ -94,6 +96,8 @@ _SIGS = {
     "fg_gat_code_xagg_fwd": (ci, [C.POINTER(CodecDesc), vp, vp, i64, ci, vp, vp, i64, vp, vp,
                                   i64, vp]),
     "fg_gat_elu_fwd": (ci, [vp, ci, i64, vp, i64, i64, vp, vp]),
+    "fg_gat_agg_bwd_t_supported": (ci, [i64, ci]),
+    "fg_gat_agg_bwd_t": (ci, [vp, i64, ci, vp, vp, vp, vp, vp, i64, vp, vp, vp, vp]),
     "fg_gat_input_attn_fwd": (ci, [C.POINTER(CodecDesc), vp, vp, i64, ci, vp, vp, i64, i64, vp,
                                    C.c_float, vp, vp, vp, vp, i64, vp]),
     "fg_gat_input_attn_bwd_blocks": (i64, []),

@@ -286,7 +286,8 @@ __global__ void k_t_place(const int32_t* __restrict__ local, const int64_t* __re
                           int64_t cap_e, const int32_t* __restrict__ indptr,
                           const int64_t* __restrict__ nd_dev, int64_t max_dst,
                           int32_t* __restrict__ cursor, int32_t* __restrict__ t_dst,
-                          float* __restrict__ t_w, int fmax, const float* __restrict__ ew) {
+                          float* __restrict__ t_w, int fmax, const float* __restrict__ ew,
+                          int32_t* __restrict__ t_eid) {
   const int64_t nd = min64(*nd_dev, max_dst);
   // thread per (destination, pick slot k < fmax): picks of v are contiguous
   // in [indptr[v], indptr[v+1]) and number at most fmax
@@ -301,6 +302,7 @@ __global__ void k_t_place(const int32_t* __restrict__ local, const int64_t* __re
     const int32_t slot = atomicAdd(cursor + local[e], 1);
     t_dst[slot] = (int32_t)v;
     t_w[slot] = ew ? ew[e] : 1.0f / (float)(e1 - e0);
+    if (t_eid) t_eid[slot] = e;
   }
 }
 
@@ -462,12 +464,12 @@ extern "C" int64_t fg_block_transpose_scratch_bytes(int64_t cap_src) {
   return 2 * cap_src * 4 + 64 + nt * 8 + 256;
 }
 
-extern "C" int fg_block_transpose(const int32_t* local, const int64_t* n_edges_dev, int64_t cap_e,
-                                  const int32_t* indptr, const int64_t* n_dst_dev,
-                                  int64_t max_dst, int max_per_dst, int64_t cap_src,
-                                  int32_t* t_indptr, int32_t* t_dst, float* t_w,
-                                  const float* edge_w, void* scratch, int64_t scratch_bytes,
-                                  void* s) {
+extern "C" int fg_block_transpose_ex(const int32_t* local, const int64_t* n_edges_dev,
+                                     int64_t cap_e, const int32_t* indptr,
+                                     const int64_t* n_dst_dev, int64_t max_dst, int max_per_dst,
+                                     int64_t cap_src, int32_t* t_indptr, int32_t* t_dst,
+                                     float* t_w, int32_t* t_eid, const float* edge_w,
+                                     void* scratch, int64_t scratch_bytes, void* s) {
   FG_CHECK_ARG(max_per_dst >= 1, "fg_block_transpose: max_per_dst must be >= 1");
   FG_CHECK_ARG(cap_src >= 1, "fg_block_transpose: empty source capacity");
   FG_CHECK_ARG(scratch_bytes >= fg_block_transpose_scratch_bytes(cap_src),
@@ -488,9 +490,20 @@ extern "C" int fg_block_transpose(const int32_t* local, const int64_t* n_edges_d
   FG_LAUNCH_CHECK();
   fg::k_t_place<<<grid_for(max_dst * max_per_dst, 256), 256, 0, st>>>(
       local, n_edges_dev, cap_e, indptr, n_dst_dev, max_dst, cursor, t_dst, t_w, max_per_dst,
-      edge_w);
+      edge_w, t_eid);
   FG_LAUNCH_CHECK();
   return FG_OK;
+}
+
+extern "C" int fg_block_transpose(const int32_t* local, const int64_t* n_edges_dev, int64_t cap_e,
+                                  const int32_t* indptr, const int64_t* n_dst_dev,
+                                  int64_t max_dst, int max_per_dst, int64_t cap_src,
+                                  int32_t* t_indptr, int32_t* t_dst, float* t_w,
+                                  const float* edge_w, void* scratch, int64_t scratch_bytes,
+                                  void* s) {
+  return fg_block_transpose_ex(local, n_edges_dev, cap_e, indptr, n_dst_dev, max_dst,
+                               max_per_dst, cap_src, t_indptr, t_dst, t_w, nullptr, edge_w,
+                               scratch, scratch_bytes, s);
 }
 
 static int block_mean_bwd_t(const uint16_t* g, int64_t H, int64_t g_ld, const int32_t* t_indptr,

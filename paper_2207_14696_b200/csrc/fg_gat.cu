@@ -1378,3 +1378,90 @@ extern "C" int fg_gat_input_attn_bwd(const fg_codec_desc* codec, const uint16_t*
   FG_LAUNCH_CHECK();
   return FG_OK;
 }
+
+// ------------------------------------------------ gather-form aggregation backward
+// Over the block's transpose (per source row u its entries (v, e), from
+// fg_block_transpose_ex): dz[u] = sum_entries alpha[e, head] dout[v] written
+// once in bf16 (rows without entries or past the live count: zeros), and
+// dalpha[e, k] = <dout[v, head k], z[u, head k]> written once per edge and
+// head -- no zero fills, no float atomics, no fp32 dz.  Warp per source row,
+// lane per 8-feature chunk (hf <= 256); the per-head dot is reduced over the
+// head's G = hf/heads/8 lanes (heads == 1: the whole warp).
+namespace fg {
+__global__ void __launch_bounds__(256)
+k_gat_agg_bwd_t(const __nv_bfloat16* __restrict__ z, int64_t hf, int heads,
+                const float* __restrict__ alpha, const int32_t* __restrict__ t_indptr,
+                const int32_t* __restrict__ t_dst, const int32_t* __restrict__ t_eid,
+                const int64_t* __restrict__ nsrc_dev, int64_t cap_src,
+                const float* __restrict__ dout, __nv_bfloat16* __restrict__ dz,
+                float* __restrict__ dalpha) {
+  const int64_t live = min64(*nsrc_dev, cap_src);
+  const int lane = threadIdx.x & 31;
+  const int chunks = (int)(hf >> 3);
+  const int G = chunks / heads;
+  const bool act = lane < chunks;
+  const int k = act ? lane / G : 0;
+  for (int64_t u = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; u < cap_src;
+       u += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if (u < live) {
+      float zr[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      if (act) ld8(z + u * hf + lane * 8, zr);
+      const int32_t s0 = t_indptr[u], s1 = t_indptr[u + 1];
+      for (int32_t t = s0; t < s1; ++t) {
+        const int32_t v = t_dst[t], e = t_eid[t];
+        float p = 0.f;
+        if (act) {
+          const float4* gp = reinterpret_cast<const float4*>(dout + (int64_t)v * hf + lane * 8);
+          const float4 g0 = gp[0], g1 = gp[1];
+          const float g[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+          const float a = alpha[(int64_t)e * heads + k];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            acc[j] = fmaf(a, g[j], acc[j]);
+            p = fmaf(g[j], zr[j], p);
+          }
+        }
+        if (heads == 1) {
+#pragma unroll
+          for (int off = 16; off >= 1; off >>= 1) p += __shfl_xor_sync(0xffffffffu, p, off);
+        } else {
+          for (int off = G >> 1; off >= 1; off >>= 1) p += __shfl_xor_sync(0xffffffffu, p, off);
+        }
+        if (act && lane % G == 0) dalpha[(int64_t)e * heads + k] = p;
+      }
+    }
+    if (act) {
+      uint32_t w[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const __nv_bfloat162 b = __floats2bfloat162_rn(acc[2 * i], acc[2 * i + 1]);
+        w[i] = *reinterpret_cast<const uint32_t*>(&b);
+      }
+      reinterpret_cast<uint4*>(dz + u * hf + lane * 8)[0] = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+  }
+}
+}  // namespace fg
+
+extern "C" int fg_gat_agg_bwd_t_supported(int64_t hf, int heads) {
+  if (hf % 8 || hf > 256 || heads < 1 || (hf / 8) % heads) return 0;
+  const int64_t G = hf / 8 / heads;
+  return heads == 1 || (G & (G - 1)) == 0;
+}
+
+extern "C" int fg_gat_agg_bwd_t(const uint16_t* z, int64_t hf, int heads, const float* alpha,
+                                const int32_t* t_indptr, const int32_t* t_dst,
+                                const int32_t* t_eid, const int64_t* n_src_dev, int64_t cap_src,
+                                const float* dout, uint16_t* dz, float* dalpha, void* s) {
+  FG_CHECK_ARG(z && alpha && t_indptr && t_dst && t_eid && n_src_dev && dout && dz && dalpha,
+               "fg_gat_agg_bwd_t: null argument");
+  FG_CHECK_ARG(fg_gat_agg_bwd_t_supported(hf, heads),
+               "fg_gat_agg_bwd_t: hf <= 256, hf/8 lanes split evenly into power-of-2 heads");
+  if (cap_src == 0) return FG_OK;
+  fg::k_gat_agg_bwd_t<<<grid_for(cap_src * 32, 256), 256, 0, as_stream(s)>>>(
+      reinterpret_cast<const __nv_bfloat16*>(z), hf, heads, alpha, t_indptr, t_dst, t_eid,
+      n_src_dev, cap_src, dout, reinterpret_cast<__nv_bfloat16*>(dz), dalpha);
+  FG_LAUNCH_CHECK();
+  return FG_OK;
+}

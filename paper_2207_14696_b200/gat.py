@@ -366,14 +366,18 @@ class GatTrainer:
         self.world = torch.distributed.get_world_size(process_group) if process_group else 1
         torch.manual_seed(cfg.seed)
         L = len(cfg.fanouts)
-        self.sampler = DeviceSampler(graph, cfg.fanouts, cfg.batch_size, need_local=True)
+        # transposes with edge ids of the non-input blocks: the gather-form
+        # aggregation backward (fg_gat_agg_bwd_t)
+        self.sampler = DeviceSampler(graph, cfg.fanouts, cfg.batch_size, need_local=True,
+                                     need_transpose=True, need_eid=True)
         # pipelined like SageTrainer: batch b+1 is sampled into the other slot
         # on a side stream while batch b trains (one shared PCG64 stream)
         self.samplers = [self.sampler]
         self.pipeline = cfg.pipeline
         if self.pipeline:
             self.samplers.append(DeviceSampler(graph, cfg.fanouts, cfg.batch_size,
-                                               need_local=True, share=self.sampler))
+                                               need_local=True, need_transpose=True,
+                                               need_eid=True, share=self.sampler))
             self.side = torch.cuda.Stream(self.device,
                                           priority=int(os.environ.get("FG_SIDE_PRIORITY", "-1")))
         self.graphs = {}
@@ -554,15 +558,27 @@ class GatTrainer:
             else:
                 ds = torch.zeros((h.shape[0], 2 * Hh), dtype=f32, device=dev)
                 torch.mv(do.t(), self._ones[:do.shape[0]], out=v.db)
-                dz = torch.zeros((h.shape[0], v.width), dtype=f32, device=dev)
-                dalpha = torch.zeros((e_cap, Hh), dtype=f32, device=dev)
-                N.call("fg_gat_agg_bwd", N.ptr(z), v.width, Hh, N.ptr(alpha), N.ptr(sb.indptr[l]),
-                       N.ptr(local), self.caps[l], N.ptr(sb.n_nodes[l]), N.ptr(do), N.ptr(dz),
-                       N.ptr(dalpha), s)
+                teid = sb.t_eid[l] if sb.t_eid else None
+                if teid is not None and N.lib().fg_gat_agg_bwd_t_supported(v.width, Hh):
+                    # gather form over the block's transpose: dz in bf16, no
+                    # zero fill / atomics / cast
+                    t_indptr, t_dst, _, n_src = sb.trans[l]
+                    dzb = torch.empty((h.shape[0], v.width), dtype=bf16, device=dev)
+                    dalpha = torch.empty((e_cap, Hh), dtype=f32, device=dev)
+                    N.call("fg_gat_agg_bwd_t", N.ptr(z), v.width, Hh, N.ptr(alpha),
+                           N.ptr(t_indptr), N.ptr(t_dst), N.ptr(teid), N.ptr(n_src), h.shape[0],
+                           N.ptr(do), N.ptr(dzb), N.ptr(dalpha), s)
+                else:
+                    dz = torch.zeros((h.shape[0], v.width), dtype=f32, device=dev)
+                    dalpha = torch.zeros((e_cap, Hh), dtype=f32, device=dev)
+                    N.call("fg_gat_agg_bwd", N.ptr(z), v.width, Hh, N.ptr(alpha),
+                           N.ptr(sb.indptr[l]), N.ptr(local), self.caps[l], N.ptr(sb.n_nodes[l]),
+                           N.ptr(do), N.ptr(dz), N.ptr(dalpha), s)
+                    dzb = dz.to(bf16)
                 N.call("fg_gat_softmax_bwd", N.ptr(sc), 2 * Hh, N.ptr(q), N.ptr(alpha),
                        N.ptr(dalpha), N.ptr(sb.indptr[l]), N.ptr(local), self.caps[l],
                        N.ptr(sb.n_nodes[l]), Hh, 0.2, N.ptr(ds), N.ptr(ds[:, Hh:]), s)
-                dzb, dsb = dz.to(bf16), ds.to(bf16)
+                dsb = ds.to(bf16)
                 _kgemm(dzb, h, v.dW)
                 dc = _kgemm(dsb, h, torch.empty((2 * Hh, D), dtype=f32, device=dev))
             dcv = dc.view(2, Hh, D).permute(1, 0, 2)                            # [Hh, 2, D]

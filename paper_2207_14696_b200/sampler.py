@@ -104,6 +104,7 @@ class SampledBatch:
     frontier: object = None
     n_frontier: object = None
     trans: list = None   # per block (t_indptr, t_dst) or None
+    t_eid: list = None   # per block transpose entry -> edge id (need_eid) or None
     ew: list = None      # per block edge weights (aggregator variants) or None
 
 
@@ -114,6 +115,7 @@ class DeviceSampler:
                  need_local: bool = True, want_frontier: bool = False,
                  unique_last: bool = False, need_transpose: bool = False,
                  transpose_layers=None, share: "DeviceSampler | None" = None,
+                 need_eid: bool = False,
                  aggregator: str = "mean"):
         """``share``: a second buffer set (slot) for pipelined training that
         continues ``share``'s PCG64 stream, permutation and scratch (only the
@@ -154,13 +156,14 @@ class DeviceSampler:
         # (``transpose_layers`` limits it to some hidden blocks; default all)
         self.need_transpose = need_transpose and need_local
         self.t_layers = set(range(L - 1) if transpose_layers is None else transpose_layers)
-        self.t_indptr, self.t_dst, self.t_w = [], [], []
+        self.t_indptr, self.t_dst, self.t_w, self.t_eid = [], [], [], []
         if self.need_transpose:
             for l in range(L - 1):
                 on = l in self.t_layers
                 self.t_indptr.append(z(caps[l + 1] + 1) if on else None)
                 self.t_dst.append(z(pcaps[l]) if on else None)
                 self.t_w.append(z(pcaps[l], dt=torch.float32) if on else None)
+                self.t_eid.append(z(pcaps[l]) if on and need_eid else None)
             if share is None:
                 self._alloc_t_scratch()
         self.owner = share or self
@@ -278,6 +281,7 @@ class DeviceSampler:
         if self.need_transpose:
             out.trans = [(self.t_indptr[l], self.t_dst[l], self.t_w[l], self.n_nodes[l + 1])
                          if l in self.t_layers else None for l in range(L - 1)] + [None]
+            out.t_eid = self.t_eid + [None]
         out.ew = self.ew
         return out
 
@@ -347,9 +351,10 @@ class DeviceSampler:
     def _transpose(self, l: int, s) -> None:
         """Block l's transpose (source rank -> dst of each incoming edge) for
         the gather-form backward of the hidden block mean."""
-        N.call("fg_block_transpose", N.ptr(self.local[l]), N.ptr(self.n_picks[l]), self.pcaps[l],
-               N.ptr(self.indptr[l]), N.ptr(self.n_nodes[l]), self.caps[l], self.fanouts[l],
-               self.caps[l + 1], N.ptr(self.t_indptr[l]), N.ptr(self.t_dst[l]), N.ptr(self.t_w[l]),
+        N.call("fg_block_transpose_ex", N.ptr(self.local[l]), N.ptr(self.n_picks[l]),
+               self.pcaps[l], N.ptr(self.indptr[l]), N.ptr(self.n_nodes[l]), self.caps[l],
+               self.fanouts[l], self.caps[l + 1], N.ptr(self.t_indptr[l]), N.ptr(self.t_dst[l]),
+               N.ptr(self.t_w[l]), N.ptr(self.t_eid[l]) if self.t_eid else None,
                N.ptr(self.ew[l]) if self.ew is not None else None, N.ptr(self.t_scratch),
                self.t_scratch.numel(), s)
 

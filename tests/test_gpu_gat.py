@@ -224,3 +224,52 @@ def test_gat_elu_kernels_match_torch(in_f32):
     want = torch.where(hf > 0, dh.float(), dh.float() * (hf + 1))
     torch.cuda.synchronize()
     assert (out.float() - want).abs().max().item() <= (0 if in_f32 else 2e-2)
+
+
+@pytest.mark.parametrize("heads,hf", [(4, 256), (1, 48), (2, 64)])
+def test_gat_gather_backward_matches_atomic(heads, hf):
+    """fg_gat_agg_bwd_t over the sampler-style transpose with edge ids
+    (fg_block_transpose_ex) == the atomic fg_gat_agg_bwd: dz (bf16 vs fp32)
+    and dalpha, live and padded rows."""
+    from paper_2207_14696_b200 import _native as N
+    rng = np.random.default_rng(hf + heads)
+    n_src, n_dst, max_dst, fan = 3000, 700, 760, 9
+    counts = rng.integers(0, fan + 1, n_dst)
+    indptr = np.zeros(max_dst + 1, np.int32)
+    indptr[1:n_dst + 1] = np.cumsum(counts)
+    indptr[n_dst + 1:] = indptr[n_dst]
+    E = int(indptr[n_dst])
+    local = rng.integers(0, n_src - 50, E).astype(np.int32)   # the last 50 sources unused
+    dev = "cuda"
+    cap_e, cap_src = E + 40, n_src + 24                       # padded capacities
+    lc = torch.zeros(cap_e, dtype=torch.int32, device=dev)
+    lc[:E] = torch.from_numpy(local).to(dev)
+    ip = torch.from_numpy(indptr).to(dev)
+    ne, nd, ns = (torch.tensor([x], device=dev) for x in (E, n_dst, n_src))
+    t_indptr = torch.zeros(n_src + 1, dtype=torch.int32, device=dev)
+    t_dst = torch.zeros(cap_e, dtype=torch.int32, device=dev)
+    t_w = torch.zeros(cap_e, dtype=torch.float32, device=dev)
+    t_eid = torch.zeros(cap_e, dtype=torch.int32, device=dev)
+    scratch = torch.zeros(N.lib().fg_block_transpose_scratch_bytes(n_src), dtype=torch.uint8,
+                          device=dev)
+    s = N.stream_handle()
+    N.call("fg_block_transpose_ex", N.ptr(lc), N.ptr(ne), cap_e, N.ptr(ip), N.ptr(nd), max_dst,
+           fan, n_src, N.ptr(t_indptr), N.ptr(t_dst), N.ptr(t_w), N.ptr(t_eid), None,
+           N.ptr(scratch), scratch.numel(), s)
+    z = torch.randn(cap_src, hf, device=dev).to(torch.bfloat16)
+    alpha = torch.rand(cap_e, heads, device=dev)
+    dout = torch.randn(max_dst, hf, device=dev)
+    dz_a = torch.zeros(cap_src, hf, device=dev)
+    da_a = torch.zeros(cap_e, heads, device=dev)
+    N.call("fg_gat_agg_bwd", N.ptr(z), hf, heads, N.ptr(alpha), N.ptr(ip), N.ptr(lc), max_dst,
+           N.ptr(nd), N.ptr(dout), N.ptr(dz_a), N.ptr(da_a), s)
+    assert N.lib().fg_gat_agg_bwd_t_supported(hf, heads)
+    dz_t = torch.full((cap_src, hf), 9.0, device=dev).to(torch.bfloat16)
+    da_t = torch.zeros(cap_e, heads, device=dev)
+    N.call("fg_gat_agg_bwd_t", N.ptr(z), hf, heads, N.ptr(alpha), N.ptr(t_indptr), N.ptr(t_dst),
+           N.ptr(t_eid), N.ptr(ns), cap_src, N.ptr(dout), N.ptr(dz_t), N.ptr(da_t), s)
+    torch.cuda.synchronize()
+    assert (dz_t.float() - dz_a.to(torch.bfloat16).float()).abs().max().item() <= \
+        2e-2 * dz_a.abs().max().item()
+    assert (dz_t[n_src:] == 0).all()
+    assert torch.allclose(da_t[:E], da_a[:E], rtol=1e-4, atol=1e-4)
