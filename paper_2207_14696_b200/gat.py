@@ -366,18 +366,21 @@ class GatTrainer:
         self.world = torch.distributed.get_world_size(process_group) if process_group else 1
         torch.manual_seed(cfg.seed)
         L = len(cfg.fanouts)
-        # transposes with edge ids of the non-input blocks: the gather-form
-        # aggregation backward (fg_gat_agg_bwd_t)
+        # FG_GAT_GATHER=1: transposes with edge ids of the non-input blocks for
+        # the gather-form aggregation backward (fg_gat_agg_bwd_t; measured
+        # 1.228 vs 1.169 ms/step with the atomic form: a warp walks a hub
+        # source's entries serially)
+        self._gather = os.environ.get("FG_GAT_GATHER", "0") == "1"
         self.sampler = DeviceSampler(graph, cfg.fanouts, cfg.batch_size, need_local=True,
-                                     need_transpose=True, need_eid=True)
+                                     need_transpose=self._gather, need_eid=self._gather)
         # pipelined like SageTrainer: batch b+1 is sampled into the other slot
         # on a side stream while batch b trains (one shared PCG64 stream)
         self.samplers = [self.sampler]
         self.pipeline = cfg.pipeline
         if self.pipeline:
             self.samplers.append(DeviceSampler(graph, cfg.fanouts, cfg.batch_size,
-                                               need_local=True, need_transpose=True,
-                                               need_eid=True, share=self.sampler))
+                                               need_local=True, need_transpose=self._gather,
+                                               need_eid=self._gather, share=self.sampler))
             self.side = torch.cuda.Stream(self.device,
                                           priority=int(os.environ.get("FG_SIDE_PRIORITY", "-1")))
         self.graphs = {}
