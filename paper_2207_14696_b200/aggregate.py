@@ -232,3 +232,21 @@ class SoftmaxCE(torch.autograd.Function):
 
 def softmax_ce(logits, labels, row_node, n_valid, num_classes: int | None = None):
     return SoftmaxCE.apply(logits, labels, row_node, n_valid, num_classes)
+
+
+def kgemm(a, b, out, chunks: int = 64, min_k: int = 32768):
+    """out [M, N] fp32 = a^T b for bf16 a [K, M], b [K, N].  Past min_k rows
+    K is cut into `chunks` slices multiplied by one batched GEMM (fp32 out)
+    and summed: for K ~ 1e5 with M, N <= 400 cuBLAS's single-GEMM choice (no
+    split-K) runs several times slower.  A K % chunks tail is one more GEMM."""
+    K = a.shape[0]
+    if K < min_k:
+        return torch.mm(a.t(), b, out_dtype=torch.float32, out=out)
+    kc = K // chunks
+    Kc = kc * chunks
+    part = torch.bmm(a[:Kc].view(chunks, kc, -1).transpose(1, 2), b[:Kc].view(chunks, kc, -1),
+                     out_dtype=torch.float32)
+    torch.sum(part, 0, out=out)
+    if Kc < K:
+        out += torch.mm(a[Kc:].t(), b[Kc:], out_dtype=torch.float32)
+    return out

@@ -32,7 +32,7 @@ import torch.nn.functional as F
 
 from . import _native as N
 from . import ddp
-from .aggregate import softmax_ce
+from .aggregate import kgemm as _kgemm, softmax_ce
 from .sampler import DeviceSampler
 
 
@@ -277,24 +277,6 @@ class GatModel(nn.Module):
 
 def _round_up(n: int, m: int) -> int:
     return (n + m - 1) // m * m
-
-
-def _kgemm(a, b, out, chunks: int = 64, min_k: int = 32768):
-    """out [M, N] fp32 = a^T b for bf16 a [K, M], b [K, N].  Past min_k rows
-    K is cut into `chunks` slices multiplied by one batched GEMM (fp32 out)
-    and summed: for K ~ 1e5 with M, N <= 400 cuBLAS's single-GEMM choice (no
-    split-K) runs several times slower.  A K % chunks tail is one more GEMM."""
-    K = a.shape[0]
-    if K < min_k:
-        return torch.mm(a.t(), b, out_dtype=torch.float32, out=out)
-    kc = K // chunks
-    Kc = kc * chunks
-    part = torch.bmm(a[:Kc].view(chunks, kc, -1).transpose(1, 2), b[:Kc].view(chunks, kc, -1),
-                     out_dtype=torch.float32)
-    torch.sum(part, 0, out=out)
-    if Kc < K:
-        out += torch.mm(a[Kc:].t(), b[Kc:], out_dtype=torch.float32)
-    return out
 
 
 class _LayerViews:

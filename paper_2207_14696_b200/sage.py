@@ -29,7 +29,7 @@ import torch.nn.functional as F
 
 from . import ddp
 from . import _native as N
-from .aggregate import (alloc_aggregate, block_mean, gather_dequant_mean, input_block_mean,
+from .aggregate import (alloc_aggregate, block_mean, gather_dequant_mean, input_block_mean, kgemm,
                         padded_dim, softmax_ce, wgrad_scratch, wgrad_supported)
 from .sampler import DeviceSampler
 
@@ -246,6 +246,7 @@ class SageTrainer:
                           and (mode == "2" or (mode == "1" and cfg.aggregator == "mean"))
                           and N.lib().fg_input_block_mean_supported(
                               w0.shape[0], w0.shape[1], cfg.fanouts[L - 2]))
+        self.kgemm = os.environ.get("FG_SAGE_KGEMM", "0") == "1"
         self.graph = None
         self.graphs = {}
         self._primed, self._next = False, 0
@@ -331,7 +332,10 @@ class SageTrainer:
                N.ptr(sb.n_nodes[0]), N.ptr(self.labels), N.ptr(sb.nodes[0]), N.ptr(dh),
                N.ptr(row_loss), N.ptr(self.loss_buf), N.ptr(self.ce_ctr), s)
         for i in range(L - 1, -1, -1):
-            torch.mm(dh.t(), ins[i], out_dtype=torch.float32, out=dW[i])
+            if self.kgemm:  # K ~ 1e5 rows (MAG's GEMM-path dW0): chunked batched GEMM
+                kgemm(dh, ins[i], dW[i])
+            else:
+                torch.mm(dh.t(), ins[i], out_dtype=torch.float32, out=dW[i])
             if i == 0:
                 break
             H = W[i - 1].shape[0]
