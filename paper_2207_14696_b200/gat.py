@@ -553,26 +553,36 @@ class GatTrainer:
                     N.call("fg_gat_agg_bwd_t", N.ptr(z), v.width, Hh, N.ptr(alpha),
                            N.ptr(t_indptr), N.ptr(t_dst), N.ptr(teid), N.ptr(n_src), h.shape[0],
                            N.ptr(do), N.ptr(dzb), N.ptr(dalpha), s)
+                    dz = dzb
                 else:
                     dz = torch.zeros((h.shape[0], v.width), dtype=f32, device=dev)
                     dalpha = torch.zeros((e_cap, Hh), dtype=f32, device=dev)
                     N.call("fg_gat_agg_bwd", N.ptr(z), v.width, Hh, N.ptr(alpha),
                            N.ptr(sb.indptr[l]), N.ptr(local), self.caps[l], N.ptr(sb.n_nodes[l]),
                            N.ptr(do), N.ptr(dz), N.ptr(dalpha), s)
-                    dzb = dz.to(bf16)
                 N.call("fg_gat_softmax_bwd", N.ptr(sc), 2 * Hh, N.ptr(q), N.ptr(alpha),
                        N.ptr(dalpha), N.ptr(sb.indptr[l]), N.ptr(local), self.caps[l],
                        N.ptr(sb.n_nodes[l]), Hh, 0.2, N.ptr(ds), N.ptr(ds[:, Hh:]), s)
-                dsb = ds.to(bf16)
-                _kgemm(dzb, h, v.dW)
-                dc = _kgemm(dsb, h, torch.empty((2 * Hh, D), dtype=f32, device=dev))
+                # g = [dz | ds | 0] (bf16, 8-aligned width) against [W; c; 0]:
+                # one K-GEMM gives dW and dc, one GEMM gives dh = dz W + ds c
+                w2 = v.width + 2 * Hh
+                Wp = _round_up(w2, 8)
+                gcat = torch.empty((h.shape[0], Wp), dtype=bf16, device=dev)
+                gcat[:, :v.width].copy_(dz)
+                gcat[:, v.width:w2].copy_(ds)
+                if Wp > w2:
+                    gcat[:, w2:].zero_()
+                full = _kgemm(gcat, h, torch.empty((Wp, D), dtype=f32, device=dev))
+                v.dW.copy_(full[:v.width])
+                dc = full[v.width:w2]
             dcv = dc.view(2, Hh, D).permute(1, 0, 2)                            # [Hh, 2, D]
             # d[a_l | a_r][k, f] = <W[kF+f], dc[el|er row k]>;  dW += a . dc
             v.dattn.copy_(torch.bmm(v.W.view(Hh, Fh, D), dcv.transpose(1, 2)).permute(2, 0, 1))
             v.dW.view(Hh, Fh, D).baddbmm_(v.attn.permute(1, 2, 0), dcv)
             if i == 0:
                 break
-            dh = torch.addmm(torch.mm(dzb, v.Wb), dsb, cb)                      # [src rows, D] bf16
+            wcat = torch.cat([v.Wb, cb, cb.new_zeros((Wp - w2, D))])           # [Wp, D]
+            dh = torch.mm(gcat, wcat)                                           # [src rows, D] bf16
             # ELU'(o) from its output h; fp32 for a hidden layer's aggregation
             # backward, bf16 for the input layer's GEMMs
             nxt = torch.empty(dh.shape, dtype=f32 if i - 1 > 0 else bf16, device=dev)
