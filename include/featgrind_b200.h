@@ -481,6 +481,10 @@ int fg_gat_agg_bwd_t(const uint16_t* z, int64_t hf, int heads, const float* alph
                      const int32_t* t_indptr, const int32_t* t_dst, const int32_t* t_eid,
                      const int64_t* n_src_dev, int64_t cap_src, const float* dout, uint16_t* dz,
                      float* dalpha, void* cuda_stream);
+/* out[r] = bf16([a[r, :ac] | b[r, :bc] | 0 ...]) for r < rows, row pitch out_ld
+ * (a multiple of 8; a and out 16-byte aligned): the GAT backward's [dz | ds]. */
+int fg_cat_rows_bf16(const float* a, int64_t ac, const float* b, int64_t bc, int64_t rows,
+                     uint16_t* out, int64_t out_ld, void* cuda_stream);
 /* ELU between GAT layers: h = bf16(ELU(in + bias)) for in fp32 (in_f32 = 1)
  * or bf16 rows of pitch ld_in, bias fp32 [cols] or NULL (cols % 8 == 0); and
  * out = dh * ELU'(.) from the forward's output h (1 where h > 0, h + 1

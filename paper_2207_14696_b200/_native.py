@@ -96,6 +96,7 @@ _SIGS = {
     "fg_gat_code_xagg_fwd": (ci, [C.POINTER(CodecDesc), vp, vp, i64, ci, vp, vp, i64, vp, vp,
                                   i64, vp]),
     "fg_gat_elu_fwd": (ci, [vp, ci, i64, vp, i64, i64, vp, vp]),
+    "fg_cat_rows_bf16": (ci, [vp, i64, vp, i64, i64, vp, i64, vp]),
     "fg_gat_agg_bwd_t_supported": (ci, [i64, ci]),
     "fg_gat_agg_bwd_t": (ci, [vp, i64, ci, vp, vp, vp, vp, vp, i64, vp, vp, vp, vp]),
     "fg_gat_input_attn_fwd": (ci, [C.POINTER(CodecDesc), vp, vp, i64, ci, vp, vp, i64, i64, vp,

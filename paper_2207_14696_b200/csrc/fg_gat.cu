@@ -1465,3 +1465,51 @@ extern "C" int fg_gat_agg_bwd_t(const uint16_t* z, int64_t hf, int heads, const 
   FG_LAUNCH_CHECK();
   return FG_OK;
 }
+
+// ------------------------------------------------ [a | b | 0] rows in bf16
+// out[r] = bf16([a[r, :ac] | b[r, :bc] | 0 ...]) with row pitch out_ld (a
+// multiple of 8): the GAT backward's [dz | ds] operand in one pass (a torch
+// copy into the strided column slice runs the non-vectorised path).
+namespace fg {
+__global__ void k_cat_rows_bf16(const float* __restrict__ a, int64_t ac,
+                                const float* __restrict__ b, int64_t bc, int64_t rows,
+                                uint16_t* __restrict__ out, int64_t out_ld) {
+  const int64_t ch = out_ld >> 3;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < rows * ch;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = t / ch, c0 = (t - r * ch) * 8;
+    float f[8];
+    if (c0 + 8 <= ac && (ac & 3) == 0) {
+      const float4* p = reinterpret_cast<const float4*>(a + r * ac + c0);
+      const float4 x = p[0], y = p[1];
+      f[0] = x.x; f[1] = x.y; f[2] = x.z; f[3] = x.w; f[4] = y.x; f[5] = y.y; f[6] = y.z; f[7] = y.w;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int64_t c = c0 + j;
+        f[j] = c < ac ? a[r * ac + c] : (c < ac + bc ? b[r * bc + (c - ac)] : 0.f);
+      }
+    }
+    uint32_t w[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const __nv_bfloat162 h = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+      w[i] = *reinterpret_cast<const uint32_t*>(&h);
+    }
+    reinterpret_cast<uint4*>(out + r * out_ld + c0)[0] = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+}  // namespace fg
+
+extern "C" int fg_cat_rows_bf16(const float* a, int64_t ac, const float* b, int64_t bc,
+                                int64_t rows, uint16_t* out, int64_t out_ld, void* s) {
+  FG_CHECK_ARG(a && out && out_ld % 8 == 0 && out_ld >= ac + bc && (bc == 0 || b),
+               "fg_cat_rows_bf16: bad argument (out_ld % 8 == 0, >= ac + bc)");
+  FG_CHECK_ARG((uintptr_t)out % 16 == 0 && (uintptr_t)a % 16 == 0,
+               "fg_cat_rows_bf16: a / out must be 16-byte aligned");
+  if (rows == 0) return FG_OK;
+  fg::k_cat_rows_bf16<<<grid_for(rows * (out_ld / 8), 256), 256, 0, as_stream(s)>>>(
+      a, ac, b, bc, rows, out, out_ld);
+  FG_LAUNCH_CHECK();
+  return FG_OK;
+}

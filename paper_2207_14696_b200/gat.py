@@ -568,10 +568,14 @@ class GatTrainer:
                 w2 = v.width + 2 * Hh
                 Wp = _round_up(w2, 8)
                 gcat = torch.empty((h.shape[0], Wp), dtype=bf16, device=dev)
-                gcat[:, :v.width].copy_(dz)
-                gcat[:, v.width:w2].copy_(ds)
-                if Wp > w2:
-                    gcat[:, w2:].zero_()
+                if dz.dtype == f32:
+                    N.call("fg_cat_rows_bf16", N.ptr(dz), v.width, N.ptr(ds), 2 * Hh, h.shape[0],
+                           N.ptr(gcat), Wp, s)
+                else:  # gather form: dz already bf16
+                    gcat[:, :v.width].copy_(dz)
+                    gcat[:, v.width:w2].copy_(ds)
+                    if Wp > w2:
+                        gcat[:, w2:].zero_()
                 full = _kgemm(gcat, h, torch.empty((Wp, D), dtype=f32, device=dev))
                 v.dW.copy_(full[:v.width])
                 dc = full[v.width:w2]
