@@ -401,6 +401,7 @@ class GatTrainer:
         self._views = [_LayerViews(layer, self.flat_param, self.flat_grad, self.flat_bf16)
                        for layer in self.model.layers]
         self._ones = torch.ones(max(self.caps), dtype=torch.float32, device=self.device)
+        self._wstream = torch.cuda.Stream(self.device)
         desc = codec.desc
         self._direct = (os.environ.get("FG_GAT_DIRECT", "0") == "1" and desc.kind == N.CODEC_SQ
                         and desc.bits == 8 and desc.elem_bits == 32 and desc.row_stride % 2 == 0)
@@ -526,11 +527,13 @@ class GatTrainer:
             if i == 0:
                 A = z
                 dA = torch.mm(do, v.wbd[:Hh * D].t())                          # [rows, Hh*D]
-                # do^T A: the diagonal blocks are dW_k, the ones column db
-                full = _kgemm(do, A, torch.empty((v.width, A.shape[1]), dtype=f32, device=dev))
-                v.dW.view(Hh, Fh, D).copy_(
-                    full[:, :Hh * D].view(Hh, Fh, Hh, D).diagonal(dim1=0, dim2=2).permute(2, 0, 1))
-                v.db.copy_(full[:, Hh * D])
+                with self._wgrad_branch(do, A):
+                    # do^T A: the diagonal blocks are dW_k, the ones column db
+                    full = _kgemm(do, A, torch.empty((v.width, A.shape[1]), dtype=f32,
+                                                     device=dev))
+                    v.dW.view(Hh, Fh, D).copy_(full[:, :Hh * D].view(Hh, Fh, Hh, D)
+                                               .diagonal(dim1=0, dim2=2).permute(2, 0, 1))
+                    v.db.copy_(full[:, Hh * D])
                 # dalpha, the softmax backward and dc = [del|der]^T x in one
                 # pass over the picks (fg_gat_input_attn_bwd)
                 dalpha = torch.empty((e_cap, Hh), dtype=f32, device=dev)
@@ -539,7 +542,8 @@ class GatTrainer:
                 N.call("fg_gat_input_attn_bwd", *src.head(), D, Hh, N.ptr(sc), N.ptr(alpha),
                        N.ptr(q), N.ptr(dA), N.ptr(sb.indptr[l]), self.caps[l],
                        N.ptr(sb.n_nodes[l]), 0.2, N.ptr(dalpha), N.ptr(part), s)
-                dc = part.sum(0)
+                with self._wgrad_branch(part):
+                    self._attn_grads(v, part.sum(0))
             else:
                 ds = torch.zeros((h.shape[0], 2 * Hh), dtype=f32, device=dev)
                 torch.mv(do.t(), self._ones[:do.shape[0]], out=v.db)
@@ -576,13 +580,10 @@ class GatTrainer:
                     gcat[:, v.width:w2].copy_(ds)
                     if Wp > w2:
                         gcat[:, w2:].zero_()
-                full = _kgemm(gcat, h, torch.empty((Wp, D), dtype=f32, device=dev))
-                v.dW.copy_(full[:v.width])
-                dc = full[v.width:w2]
-            dcv = dc.view(2, Hh, D).permute(1, 0, 2)                            # [Hh, 2, D]
-            # d[a_l | a_r][k, f] = <W[kF+f], dc[el|er row k]>;  dW += a . dc
-            v.dattn.copy_(torch.bmm(v.W.view(Hh, Fh, D), dcv.transpose(1, 2)).permute(2, 0, 1))
-            v.dW.view(Hh, Fh, D).baddbmm_(v.attn.permute(1, 2, 0), dcv)
+                with self._wgrad_branch(gcat, h):
+                    full = _kgemm(gcat, h, torch.empty((Wp, D), dtype=f32, device=dev))
+                    v.dW.copy_(full[:v.width])
+                    self._attn_grads(v, full[v.width:w2])
             if i == 0:
                 break
             wcat = torch.cat([v.Wb, cb, cb.new_zeros((Wp - w2, D))])           # [Wp, D]
@@ -593,6 +594,35 @@ class GatTrainer:
             N.call("fg_gat_elu_bwd", N.ptr(dh), N.ptr(h), dh.numel(), N.ptr(nxt),
                    int(i - 1 > 0), s)
             do = nxt
+        # the weight-gradient branch ran on its own stream: join before the
+        # all-reduce / Adam read flat_grad
+        torch.cuda.current_stream().wait_stream(self._wstream)
+
+    @staticmethod
+    def _attn_grads(v, dc):
+        """From dc = d[c] ([2H, D]: el rows then er rows): d[a_l | a_r][k, f] =
+        <W[kF+f], dc[row k]> and dW += a . dc."""
+        Hh, Fh, D = v.heads, v.F, v.D
+        dcv = dc.view(2, Hh, D).permute(1, 0, 2)                                # [Hh, 2, D]
+        v.dattn.copy_(torch.bmm(v.W.view(Hh, Fh, D), dcv.transpose(1, 2)).permute(2, 0, 1))
+        v.dW.view(Hh, Fh, D).baddbmm_(v.attn.permute(1, 2, 0), dcv)
+
+    def _wgrad_branch(self, *inputs):
+        """Context: the ops inside run on the weight-gradient stream after the
+        main stream's work so far (they only feed flat_grad, so they overlap
+        the rest of the backward); the inputs are marked in use there."""
+        import contextlib
+        main = torch.cuda.current_stream()
+        ws = self._wstream
+        ws.wait_stream(main)
+        for t in inputs:
+            t.record_stream(ws)
+
+        @contextlib.contextmanager
+        def ctx():
+            with torch.cuda.stream(ws):
+                yield
+        return ctx()
 
     # epoch / step API and CUDA-graph capture: SageTrainer's (same slot
     # logic, same attribute names; one graph per sampler slot)
