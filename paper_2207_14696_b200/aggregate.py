@@ -14,6 +14,7 @@ one CUDA graph.
 from __future__ import annotations
 
 import ctypes
+import os
 
 import torch
 
@@ -234,14 +235,19 @@ def softmax_ce(logits, labels, row_node, n_valid, num_classes: int | None = None
     return SoftmaxCE.apply(logits, labels, row_node, n_valid, num_classes)
 
 
-def kgemm(a, b, out, chunks: int = 64, min_k: int = 32768):
+def kgemm(a, b, out, chunks: int | None = None, min_k: int = 32768):
     """out [M, N] fp32 = a^T b for bf16 a [K, M], b [K, N].  Past min_k rows
     K is cut into `chunks` slices multiplied by one batched GEMM (fp32 out)
     and summed: for K ~ 1e5 with M, N <= 400 cuBLAS's single-GEMM choice (no
-    split-K) runs several times slower.  A K % chunks tail is one more GEMM."""
+    split-K) runs several times slower.  A K % chunks tail is one more GEMM.
+    Default chunks: 64, or 32 for outputs past 64 K elements (the fp32
+    partials are written and summed once more)."""
     K = a.shape[0]
     if K < min_k:
         return torch.mm(a.t(), b, out_dtype=torch.float32, out=out)
+    if chunks is None:
+        chunks = int(os.environ.get("FG_KGEMM_CHUNKS", "0")) or (
+            32 if a.shape[1] * b.shape[1] > 65536 else 64)
     kc = K // chunks
     Kc = kc * chunks
     part = torch.bmm(a[:Kc].view(chunks, kc, -1).transpose(1, 2), b[:Kc].view(chunks, kc, -1),
