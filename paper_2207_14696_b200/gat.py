@@ -402,6 +402,9 @@ class GatTrainer:
                        for layer in self.model.layers]
         self._ones = torch.ones(max(self.caps), dtype=torch.float32, device=self.device)
         self._wstream = torch.cuda.Stream(self.device)
+        # FG_GAT_OVERLAP=1: the forward's z GEMM and the backward's dz zero
+        # fills on the side stream too (measured 1.047 vs 1.038 ms: contention)
+        self._overlap = os.environ.get("FG_GAT_OVERLAP", "0") == "1"
         desc = codec.desc
         self._direct = (os.environ.get("FG_GAT_DIRECT", "0") == "1" and desc.kind == N.CODEC_SQ
                         and desc.bits == 8 and desc.elem_bits == 32 and desc.row_stride % 2 == 0)
@@ -495,11 +498,18 @@ class GatTrainer:
                 z = A
                 bias, in_f32 = None, 0
             else:
+                if self._overlap:
+                    with self._side_branch(h):  # z = h W^T beside the score path
+                        z = torch.mm(h, v.Wb.t())                               # [src rows, Wd]
+                    z.record_stream(torch.cuda.current_stream())
+                else:
+                    z = torch.mm(h, v.Wb.t())
                 sc = torch.mm(h, cb.t(), out_dtype=f32)                     # [src rows, 2Hh]
                 N.call("fg_gat_softmax_fwd", N.ptr(sc), N.ptr(sc[:, Hh:]), 2 * Hh,
                        N.ptr(sb.indptr[l]), N.ptr(local), self.caps[l], N.ptr(sb.n_nodes[l]),
                        Hh, 0.2, N.ptr(alpha), N.ptr(q), s)
-                z = torch.mm(h, v.Wb.t())                                       # [src rows, Wd]
+                if self._overlap:
+                    torch.cuda.current_stream().wait_stream(self._wstream)
                 o = torch.empty((self.caps[l], v.width), dtype=f32, device=dev)
                 N.call("fg_gat_agg_fwd", N.ptr(z), v.width, Hh, N.ptr(alpha), N.ptr(sb.indptr[l]),
                        N.ptr(local), self.caps[l], N.ptr(sb.n_nodes[l]), N.ptr(o), s)
@@ -519,6 +529,19 @@ class GatTrainer:
                N.ptr(self.labels), N.ptr(sb.nodes[0]), N.ptr(do), N.ptr(row_loss),
                N.ptr(self.loss_buf), N.ptr(self.ce_ctr), s)
         # ---- backward
+        # the atomic aggregation backward's zeroed dz buffers, filled on the
+        # side stream while the loss and the last layer's first kernels run
+        gather = self._gather and sb.t_eid
+        dz_pre = {}
+        if not gather and self._overlap:
+            with self._side_branch():
+                for i in range(1, L):
+                    dz_pre[i] = torch.zeros((saved[i][0].shape[0], self._views[i].width),
+                                            dtype=f32, device=dev)
+            ev_fill = torch.cuda.Event()
+            ev_fill.record(self._wstream)
+            for t in dz_pre.values():
+                t.record_stream(torch.cuda.current_stream())
         for i in range(L - 1, -1, -1):
             v = self._views[i]
             l = L - 1 - i
@@ -527,7 +550,7 @@ class GatTrainer:
             if i == 0:
                 A = z
                 dA = torch.mm(do, v.wbd[:Hh * D].t())                          # [rows, Hh*D]
-                with self._wgrad_branch(do, A):
+                with self._side_branch(do, A):
                     # do^T A: the diagonal blocks are dW_k, the ones column db
                     full = _kgemm(do, A, torch.empty((v.width, A.shape[1]), dtype=f32,
                                                      device=dev))
@@ -542,7 +565,7 @@ class GatTrainer:
                 N.call("fg_gat_input_attn_bwd", *src.head(), D, Hh, N.ptr(sc), N.ptr(alpha),
                        N.ptr(q), N.ptr(dA), N.ptr(sb.indptr[l]), self.caps[l],
                        N.ptr(sb.n_nodes[l]), 0.2, N.ptr(dalpha), N.ptr(part), s)
-                with self._wgrad_branch(part):
+                with self._side_branch(part):
                     self._attn_grads(v, part.sum(0))
             else:
                 ds = torch.zeros((h.shape[0], 2 * Hh), dtype=f32, device=dev)
@@ -559,7 +582,11 @@ class GatTrainer:
                            N.ptr(do), N.ptr(dzb), N.ptr(dalpha), s)
                     dz = dzb
                 else:
-                    dz = torch.zeros((h.shape[0], v.width), dtype=f32, device=dev)
+                    if i in dz_pre:
+                        torch.cuda.current_stream().wait_event(ev_fill)
+                        dz = dz_pre.pop(i)
+                    else:
+                        dz = torch.zeros((h.shape[0], v.width), dtype=f32, device=dev)
                     dalpha = torch.zeros((e_cap, Hh), dtype=f32, device=dev)
                     N.call("fg_gat_agg_bwd", N.ptr(z), v.width, Hh, N.ptr(alpha),
                            N.ptr(sb.indptr[l]), N.ptr(local), self.caps[l], N.ptr(sb.n_nodes[l]),
@@ -580,7 +607,7 @@ class GatTrainer:
                     gcat[:, v.width:w2].copy_(ds)
                     if Wp > w2:
                         gcat[:, w2:].zero_()
-                with self._wgrad_branch(gcat, h):
+                with self._side_branch(gcat, h):
                     full = _kgemm(gcat, h, torch.empty((Wp, D), dtype=f32, device=dev))
                     v.dW.copy_(full[:v.width])
                     self._attn_grads(v, full[v.width:w2])
@@ -607,10 +634,11 @@ class GatTrainer:
         v.dattn.copy_(torch.bmm(v.W.view(Hh, Fh, D), dcv.transpose(1, 2)).permute(2, 0, 1))
         v.dW.view(Hh, Fh, D).baddbmm_(v.attn.permute(1, 2, 0), dcv)
 
-    def _wgrad_branch(self, *inputs):
-        """Context: the ops inside run on the weight-gradient stream after the
-        main stream's work so far (they only feed flat_grad, so they overlap
-        the rest of the backward); the inputs are marked in use there."""
+    def _side_branch(self, *inputs):
+        """Context: the ops inside run on the side stream after the main
+        stream's work so far (the weight-gradient branch, which only feeds
+        flat_grad and so overlaps the rest of the backward; a forward GEMM
+        independent of the score path); the inputs are marked in use there."""
         import contextlib
         main = torch.cuda.current_stream()
         ws = self._wstream
