@@ -955,11 +955,40 @@ k_vq_mean8_lane(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
     const uint8_t* s_codes = CODES(k & 1);
     const int32_t e0 = s_ip[0];
     const bool staged = s_ip[kTD] - e0 <= kSrcCap;
-    for (int vl = warp; vl < kTD; vl += kLaneWarps) {
+    const int nv = (int)min64((int64_t)kTD, live - tile * kTD);  // live destinations of the tile
+    for (int vl = warp; vl < nv; vl += kLaneWarps) {
       const int64_t v = tile * kTD + vl;
-      if (v >= live) break;
       const int a = s_ip[vl] - e0;
       const int cnt = s_ip[vl + 1] - e0 - a;
+      if constexpr (F16 && W == 8) {
+        // fanout-5 input layer (every BASELINE config; 99.5 % of a MAG240M-
+        // shape block's destinations): straight to the 5-pick body, no
+        // dispatch, the first pick initialises the sums, constant 1/cnt
+        if (staged && cnt == 5) {
+          uint32_t h[W / 2];
+          lane_f16_body<5, W>(s_codes + a * 32 + lane, lbase, h);
+          if (active) {
+            const float inv = 0.2f * pscale;
+            uint32_t wv[W / 2];
+#pragma unroll
+            for (int j = 0; j < W / 2; ++j) {
+              const u64 f = h2_to_f32x2(h[j]);
+              const __nv_bfloat162 b2 = __floats2bfloat162_rn(lo2(f) * inv, hi2(f) * inv);
+              wv[j] = *reinterpret_cast<const uint32_t*>(&b2);
+            }
+            __nv_bfloat16* o = out + v * ld + col0;
+            if (full_part && vec_ok) {
+              *reinterpret_cast<uint4*>(o) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+            } else {
+#pragma unroll
+              for (int j = 0; j < W; ++j)
+                if (col0 + j < d)
+                  o[j] = __ushort_as_bfloat16((unsigned short)(wv[j / 2] >> (16 * (j & 1))));
+            }
+          }
+          continue;
+        }
+      }
       if constexpr (F16) {
         // bf16 row segment of destination vv from its fp16 sums
         auto emit = [&](int64_t vv, const uint32_t* h, float inv) {
@@ -1213,15 +1242,17 @@ k_sq_mean_lane(const uint8_t* __restrict__ rows, int64_t stride, const float* __
     const uint8_t* s_rw = ROWS(k & 1);
     const int32_t e0 = s_ip[0];
     const bool staged = s_ip[kTD] - e0 <= cap;
-    for (int vl = warp; vl < kTD; vl += kLaneWarps) {
+    const int nv = (int)min64((int64_t)kTD, live - tile * kTD);  // live destinations of the tile
+    for (int vl = warp; vl < nv; vl += kLaneWarps) {
       const int64_t v = tile * kTD + vl;
-      if (v >= live) break;
       const int a = s_ip[vl] - e0;
       const int cnt = s_ip[vl + 1] - e0 - a;
       u64 acc[NA];
 #pragma unroll
       for (int j = 0; j < NA; ++j) acc[j] = 0ull;
-      if (staged) {
+      if (staged && cnt == 5) {  // fanout-5 input layer: no dispatch
+        sq_lane_body<K, NB, 5>(s_rw + (size_t)a * RB + lane * NB, tb, acc);
+      } else if (staged) {
         const uint8_t* cp = s_rw + (size_t)a * RB + lane * NB;
         int u0 = 0;
         for (; u0 + 8 <= cnt; u0 += 8) sq_lane_body<K, NB, 8>(cp + (size_t)u0 * RB, tb, acc);

@@ -467,16 +467,41 @@ class GatTrainer:
         # reads 8-bit SQ code rows in place instead (no decoded matrix, but a
         # dependent pick-id load per row: measured 1.225 vs 1.169 ms/step)
         L1 = L - 1
+        # parameter-only operands of every layer (score vectors c, their bf16
+        # copy, the input layer's block-diagonal weight, the backward's
+        # [W; c; 0]) on the side stream, beside the pick decode
+        if self._views[0].wbd is None:
+            self._views[0].refresh_block_diag()
+        pre = []
+        with self._side_branch():
+            for i, v in enumerate(self._views):
+                Hh, Fh, D = v.heads, v.F, v.D
+                c = torch.bmm(v.attn.permute(1, 0, 2), v.W.view(Hh, Fh, D))    # [Hh, 2, D]
+                c = c.permute(1, 0, 2).reshape(2 * Hh, D)                       # [el | er] rows
+                cb = c.to(bf16)
+                if i == 0:
+                    v.refresh_block_diag()
+                    wcat = None
+                else:
+                    w2 = v.width + 2 * Hh
+                    wcat = torch.cat([v.Wb, cb, cb.new_zeros((_round_up(w2, 8) - w2, D))])
+                pre.append((c, cb, wcat))
+            ev_pre = torch.cuda.Event()
+            ev_pre.record(self._wstream)
+        main = torch.cuda.current_stream()
+        for t in pre:
+            for x in t:
+                if x is not None:
+                    x.record_stream(main)
         src = PickSource(self.codec, sb.picks[L1], sb.n_picks[L1], self.pick_cap,
                          decoded=not self._direct)
+        main.wait_event(ev_pre)
         saved = []
         h = src
         for i, v in enumerate(self._views):
             l = L - 1 - i
             Hh, Fh, D = v.heads, v.F, v.D
-            c = torch.bmm(v.attn.permute(1, 0, 2), v.W.view(Hh, Fh, D))    # [Hh, 2, D]
-            c = c.permute(1, 0, 2).reshape(2 * Hh, D)                       # [el | er] rows
-            cb = c.to(bf16)
+            c, cb, _ = pre[i]
             first = i == 0
             local = None if first else sb.local[l]
             e_cap = self.pick_cap if first else sb.local[l].numel()
@@ -493,7 +518,6 @@ class GatTrainer:
                 N.call("fg_gat_input_attn_fwd", *src.head(), D, Hh, N.ptr(c), N.ptr(sb.indptr[l]),
                        self.caps[l], rows, N.ptr(sb.n_nodes[l]), 0.2, N.ptr(sc), N.ptr(alpha),
                        N.ptr(q), N.ptr(A), Hh * D + 8, s)
-                v.refresh_block_diag()
                 o = torch.mm(A, v.wbd)                                          # bf16
                 z = A
                 bias, in_f32 = None, 0
@@ -569,7 +593,8 @@ class GatTrainer:
                     self._attn_grads(v, part.sum(0))
             else:
                 ds = torch.zeros((h.shape[0], 2 * Hh), dtype=f32, device=dev)
-                torch.mv(do.t(), self._ones[:do.shape[0]], out=v.db)
+                with self._side_branch(do):
+                    torch.mv(do.t(), self._ones[:do.shape[0]], out=v.db)
                 teid = sb.t_eid[l] if sb.t_eid else None
                 if teid is not None and N.lib().fg_gat_agg_bwd_t_supported(v.width, Hh):
                     # gather form over the block's transpose: dz in bf16, no
@@ -613,8 +638,7 @@ class GatTrainer:
                     self._attn_grads(v, full[v.width:w2])
             if i == 0:
                 break
-            wcat = torch.cat([v.Wb, cb, cb.new_zeros((Wp - w2, D))])           # [Wp, D]
-            dh = torch.mm(gcat, wcat)                                           # [src rows, D] bf16
+            dh = torch.mm(gcat, pre[i][2])                                      # [src rows, D] bf16
             # ELU'(o) from its output h; fp32 for a hidden layer's aggregation
             # backward, bf16 for the input layer's GEMMs
             nxt = torch.empty(dh.shape, dtype=f32 if i - 1 > 0 else bf16, device=dev)

@@ -46,6 +46,25 @@ def main():
         flop = 2.0 * M * K * N
         print(f"M{M} K{K} N{N}: " + ", ".join(f"{k} {v:.1f}us ({flop / v / 1e6:.0f} TF/s)"
                                                 for k, v in r.items()))
+    # MAG240M-shape layer 1 (GEMM path, P = 784): dW0 and h0 formulations
+    sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(
+        __import__("os").path.abspath(__file__))))
+    from paper_2207_14696_b200.aggregate import kgemm
+    for K in (96000, 150000):
+        dh = torch.randn(K, 256, device=dev).bfloat16()
+        x = torch.randn(K, 784, device=dev).bfloat16()
+        o32 = torch.empty(256, 784, device=dev)
+        o32t = torch.empty(784, 256, device=dev)
+        w = torch.randn(256, 784, device=dev).bfloat16()
+        h = torch.empty(K, 256, device=dev, dtype=torch.bfloat16)
+        flop = 2.0 * 256 * K * 784
+        r = {"dhT@x": timed_graph(lambda: torch.mm(dh.t(), x, out_dtype=torch.float32, out=o32)),
+             "xT@dh": timed_graph(lambda: torch.mm(x.t(), dh, out_dtype=torch.float32, out=o32t)),
+             "h0=x@wT": timed_graph(lambda: torch.mm(x, w.t(), out=h))}
+        for c in (8, 16, 32, 64):
+            r[f"kgemm{c}"] = timed_graph(lambda: kgemm(dh, x, o32, chunks=c))
+        print(f"MAG K{K}: " + ", ".join(f"{k} {v:.1f}us ({flop / v / 1e6:.0f} TF/s)"
+                                        for k, v in r.items()))
     x = torch.randn(60000, 784, device=dev).bfloat16()
     w = torch.randn(256, 784, device=dev).bfloat16()
     print(f"h0 = agg W0^T (60000x784x256): {timed_graph(lambda: torch.mm(x, w.t())):.1f}us")
