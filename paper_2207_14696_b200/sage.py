@@ -246,7 +246,13 @@ class SageTrainer:
                           and (mode == "2" or (mode == "1" and cfg.aggregator == "mean"))
                           and N.lib().fg_input_block_mean_supported(
                               w0.shape[0], w0.shape[1], cfg.fanouts[L - 2]))
-        self.kgemm = os.environ.get("FG_SAGE_KGEMM", "0") == "1"
+        # dW0 on the GEMM path (MAG240M-shape: K = 153,600 aggregate rows,
+        # 256 x 784 output): K cut into 16 slices by one batched GEMM + a
+        # sum (tools/gemm_probe.py on the B200: 65 vs 90 us for one cuBLAS
+        # GEMM; 32 slices: 77 us).  FG_SAGE_KGEMM=0/1 forces it off/on.
+        kg = os.environ.get("FG_SAGE_KGEMM", "auto")
+        self.kgemm = kg == "1" or (kg == "auto" and not fused)
+        self.kgemm_chunks = int(os.environ.get("FG_SAGE_KGEMM_CHUNKS", "16"))
         self.graph = None
         self.graphs = {}
         self._primed, self._next = False, 0
@@ -333,7 +339,7 @@ class SageTrainer:
                N.ptr(row_loss), N.ptr(self.loss_buf), N.ptr(self.ce_ctr), s)
         for i in range(L - 1, -1, -1):
             if self.kgemm:  # K ~ 1e5 rows (MAG's GEMM-path dW0): chunked batched GEMM
-                kgemm(dh, ins[i], dW[i])
+                kgemm(dh, ins[i], dW[i], chunks=self.kgemm_chunks)
             else:
                 torch.mm(dh.t(), ins[i], out_dtype=torch.float32, out=dW[i])
             if i == 0:
