@@ -551,3 +551,21 @@ def test_input_block_mean_fwd_tcgen05(H, P, fan, weighted, n_dst):
     gbits = ((bits[used][..., None] >> sh) & 1).view(-1, H).bool()
     clear = h[used].abs() > 1e-3
     assert torch.equal(gbits[clear], hb[clear])
+
+
+@pytest.mark.parametrize("K,M,N,chunks", [(153600, 256, 784, 16), (70001, 256, 112, 32),
+                                          (40000, 48, 264, None)])
+def test_kgemm_matches_fp32_reference(K, M, N, chunks):
+    """kgemm (the K-sliced weight-gradient GEMM: MAG's GEMM-path dW0 with 16
+    slices, GAT's K-GEMMs, a K % chunks tail) against an fp32 GEMM of the
+    same bf16 operands; fp32 partials summed, so within fp32 rounding of a
+    K-long dot product."""
+    from paper_2207_14696_b200.aggregate import kgemm
+    g = torch.Generator(device="cuda").manual_seed(K)
+    a = torch.randn(K, M, device="cuda", generator=g).to(torch.bfloat16)
+    b = torch.randn(K, N, device="cuda", generator=g).to(torch.bfloat16)
+    out = torch.full((M, N), float("nan"), device="cuda")
+    kgemm(a, b, out, chunks=chunks)
+    ref = a.double().t() @ b.double()
+    err = (out.double() - ref).abs().max().item()
+    assert err <= 1e-4 * K ** 0.5, err
