@@ -878,8 +878,8 @@ __device__ __forceinline__ void lane_f16_chunk(const uint8_t* cp, int cb, uint32
   }
 }
 
-template <int W, bool WT, bool F16 = false>
-__global__ void __launch_bounds__(kLaneThreads, 1)
+template <int W, bool WT, bool F16 = false, int NT = kLaneThreads>
+__global__ void __launch_bounds__(NT, 1)
 k_vq_mean8_lane(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
                 const __nv_bfloat16* __restrict__ books, int length, int parts,
                 const int32_t* __restrict__ indptr, const int32_t* __restrict__ src,
@@ -956,11 +956,11 @@ k_vq_mean8_lane(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
     const int32_t e0 = s_ip[0];
     const bool staged = s_ip[kTD] - e0 <= kSrcCap;
     const int nv = (int)min64((int64_t)kTD, live - tile * kTD);  // live destinations of the tile
-    for (int vl = warp; vl < nv; vl += kLaneWarps) {
+    for (int vl = warp; vl < nv; vl += (NT / 32)) {
       const int64_t v = tile * kTD + vl;
       const int a = s_ip[vl] - e0;
       const int cnt = s_ip[vl + 1] - e0 - a;
-      if constexpr (F16 && W == 8) {
+      if constexpr (F16 && W == 8 && NT > 512) {
         // fanout-5 input layer (every BASELINE config; 99.5 % of a MAG240M-
         // shape block's destinations): straight to the 5-pick body, no
         // dispatch, the first pick initialises the sums, constant 1/cnt
@@ -1015,10 +1015,11 @@ k_vq_mean8_lane(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
         };
         // two 5-pick destinations of this warp (vl, vl + 32) in one pass:
         // the loop / dispatch / bookkeeping is shared, the bodies interleave.
-        // W = 4 only (products-shape 30.9 -> 29.8 us); at W = 8 the doubled
-        // live registers cost more than they save (MAG 74.1 -> 79.2 us).
-        const int vl2 = vl + kLaneWarps;
-        if (W == 4 && staged && cnt == 5 && vl2 < kTD && v + kLaneWarps < live) {
+        // W = 4, or any W at 512 threads (112 registers): products-shape
+        // 30.9 -> 29.8 us; at W = 8 and 64 registers the doubled live
+        // registers cost more than they save (MAG 74.1 -> 79.2 us).
+        const int vl2 = vl + (NT / 32);
+        if ((W == 4 || NT <= 512) && staged && cnt == 5 && vl2 < kTD && v + (NT / 32) < live) {
           const int a2 = s_ip[vl2] - e0;
           if (s_ip[vl2 + 1] - e0 - a2 == 5) {
             uint32_t h[W / 2], h2[W / 2];
@@ -1026,7 +1027,7 @@ k_vq_mean8_lane(const uint8_t* __restrict__ rows, int64_t d, int64_t stride,
             lane_f16_body<5, W>(s_codes + a2 * 32 + lane, lbase, h2);
             const float inv = 0.2f * pscale;
             emit(v, h, inv);
-            emit(v + kLaneWarps, h2, inv);
+            emit(v + (NT / 32), h2, inv);
             vl = vl2;  // the loop step moves past the partner
             continue;
           }
@@ -1859,11 +1860,25 @@ int launch_vq_w(const fg_codec_desc* c, const int32_t* indptr, const int32_t* sr
     if (lp && lane_env && c->row_stride % 32 == 0 && lane_smem <= 227 * 1024) {
       const int ns = (int)ceil_div(c->num_parts, 32);
       const bool f16 = !WT && c->table_h != nullptr && c->part_scale != nullptr && lane_env == 2;
-      auto kern = f16 ? k_vq_mean8_lane<W, false, true> : k_vq_mean8_lane<W, WT, false>;
+      // fp16 tables: FG_VQ_LANE_NT=512 (112 registers, two 5-pick
+      // destinations per warp pass) / 768 (80 registers) / 1024 (default).
+      // Measured: MAG 71.2 / 71.1 / 71.2 us; products-shape kernel 28.7 vs
+      // 29.9 us at 512 but the pipelined step 0.2408 vs 0.2381 ms (the
+      // overlapped sampler), so 1024 everywhere
+      static const int lane_nt_env = [] {
+        const char* e = getenv("FG_VQ_LANE_NT");
+        return e ? atoi(e) : 0;
+      }();
+      const int lane_nt = !f16 ? kLaneThreads : (lane_nt_env ? lane_nt_env : kLaneThreads);
+      auto kern = !f16 ? k_vq_mean8_lane<W, WT, false>
+                  : lane_nt == 512 ? k_vq_mean8_lane<W, false, true, 512>
+                  : lane_nt == 768 ? k_vq_mean8_lane<W, false, true, 768>
+                                   : k_vq_mean8_lane<W, false, true>;
+      const int nthreads = (f16 && (lane_nt == 512 || lane_nt == 768)) ? lane_nt : kLaneThreads;
       FG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)lane_smem));
       const int64_t per_slice = std::max<int64_t>(1, min64(ntiles, sm_count() / ns));
-      kern<<<(int)(per_slice * ns), kLaneThreads, lane_smem, st>>>(
+      kern<<<(int)(per_slice * ns), nthreads, lane_smem, st>>>(
           c->rows, c->d, c->row_stride,
           (const __nv_bfloat16*)(f16 ? c->table_h : c->table_lp), c->length,
           c->num_parts, indptr, src, ndst, max_dst, (__nv_bfloat16*)out, ld, ns, ew,
