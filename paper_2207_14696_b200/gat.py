@@ -681,6 +681,7 @@ class GatTrainer:
     from .sage import SageTrainer as _S
     begin_epoch = _S.begin_epoch
     prepare = _S.prepare
+    _load_seeds_staged = _S._load_seeds_staged
     replay = _S.replay
     step = _S.step
     capture = _S.capture

@@ -448,10 +448,46 @@ class SageTrainer:
             cur.sample_loaded()
         nxt = self.samplers[(b + 1) % 2]
         if seeds_host is not None:
-            nxt.load_seeds_host(seeds_host)
+            self._load_seeds_staged(nxt, seeds_host)
         else:
             nxt.load_seeds((b + 1) % self._nb)
         self._primed, self._next = True, b + 1
+
+    def _load_seeds_staged(self, smp, seeds_host) -> None:
+        """Pipelined end-to-end input: the H2D copy of batch b+1's seeds runs
+        on a copy stream into one of two device staging buffers, so it
+        overlaps the step still running (the slot's own seed layer is read by
+        that step's loss until it ends); the main stream then only waits for
+        it and moves the 4 KB device to device.  The staging buffer of the
+        same parity is rewritten only after its previous device copy ran.
+        Unsorted, non-int32 or pageable seeds take the plain path."""
+        if not (seeds_host.dtype == torch.int32 and seeds_host.is_pinned()
+                and 0 < seeds_host.numel() <= smp.bs
+                and bool((seeds_host[1:] >= seeds_host[:-1]).all())):
+            smp.load_seeds_host(seeds_host)
+            return
+        if getattr(self, "_h2d", None) is None:
+            self._h2d = torch.cuda.Stream(self.device)
+            self._stage = [torch.empty(smp.bs, dtype=torch.int32, device=self.device)
+                           for _ in range(2)]
+            self._stage_done = [None, None]
+            self._stage_i = 0
+        j = self._stage_i
+        self._stage_i ^= 1
+        cnt = seeds_host.numel()
+        if self._stage_done[j] is not None:
+            self._h2d.wait_event(self._stage_done[j])
+        with torch.cuda.stream(self._h2d):
+            self._stage[j][:cnt].copy_(seeds_host, non_blocking=True)
+        ready = torch.cuda.Event()
+        ready.record(self._h2d)
+        cur = torch.cuda.current_stream()
+        cur.wait_event(ready)
+        smp.nodes[0][:cnt].copy_(self._stage[j][:cnt], non_blocking=True)
+        smp.n_nodes[0].fill_(cnt)
+        done = torch.cuda.Event()
+        done.record(cur)
+        self._stage_done[j] = done
 
     def replay(self, b: int):
         """Run step b (after ``prepare(b)``) from its CUDA graph, or eagerly."""

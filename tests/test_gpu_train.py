@@ -355,3 +355,30 @@ def test_accuracy_parity_config_a(codec):
     for a_gpu, a_cpu in accs:
         assert a_cpu > 1.0 / C * 3
         assert abs(a_gpu - a_cpu) <= 0.005 + 1e-12, accs
+
+
+@pytest.mark.parametrize("graphed", [False, True])
+def test_host_seeds_match_device_permutation(graphed):
+    """The end-to-end input path (each step's next-batch seeds from pinned
+    host memory, staged on a copy stream) trains on exactly the batches the
+    device permutation gives: same losses step for step."""
+    dg, labels, dc, train, val = _small_world(vq=True, d=100)
+    out = []
+    for host in (False, True):
+        cfg = TrainConfig(fanouts=(15, 10, 5), batch_size=512, hidden=128, pipeline=True)
+        t = SageTrainer(dg, dc, labels, 8, cfg)
+        nb = t.begin_epoch(train, 0)
+        if graphed:
+            t.capture(warmup_batches=2)
+        perm = t.sampler.perm_host
+        bs = cfg.batch_size
+        pinned = [torch.from_numpy(perm[(b + 1) * bs:(b + 2) * bs].astype(np.int32)).pin_memory()
+                  for b in range(min(nb, 6))]
+        losses = []
+        for b in range(min(nb, 6)):
+            loss = t.step(b, seeds_host=pinned[b]) if host else t.step(b)
+            losses.append(float(loss.item()))
+        t.sampler.check_errors()
+        out.append(losses)
+    assert all(np.isfinite(out[0]))
+    np.testing.assert_allclose(out[0], out[1], rtol=1e-4)
