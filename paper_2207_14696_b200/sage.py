@@ -461,33 +461,37 @@ class SageTrainer:
         it and moves the 4 KB device to device.  The staging buffer of the
         same parity is rewritten only after its previous device copy ran.
         Unsorted, non-int32 or pageable seeds take the plain path."""
+        import numpy as np
         if not (seeds_host.dtype == torch.int32 and seeds_host.is_pinned()
-                and 0 < seeds_host.numel() <= smp.bs
-                and bool((seeds_host[1:] >= seeds_host[:-1]).all())):
+                and 0 < seeds_host.numel() <= smp.bs):
+            smp.load_seeds_host(seeds_host)
+            return
+        a = seeds_host.numpy()
+        if not bool(np.all(a[1:] >= a[:-1])):
             smp.load_seeds_host(seeds_host)
             return
         if getattr(self, "_h2d", None) is None:
             self._h2d = torch.cuda.Stream(self.device)
             self._stage = [torch.empty(smp.bs, dtype=torch.int32, device=self.device)
                            for _ in range(2)]
-            self._stage_done = [None, None]
+            self._stage_ready = [torch.cuda.Event() for _ in range(2)]
+            self._stage_done = [torch.cuda.Event() for _ in range(2)]
+            self._stage_used = [False, False]
             self._stage_i = 0
         j = self._stage_i
         self._stage_i ^= 1
         cnt = seeds_host.numel()
-        if self._stage_done[j] is not None:
+        if self._stage_used[j]:
             self._h2d.wait_event(self._stage_done[j])
         with torch.cuda.stream(self._h2d):
             self._stage[j][:cnt].copy_(seeds_host, non_blocking=True)
-        ready = torch.cuda.Event()
-        ready.record(self._h2d)
+            self._stage_ready[j].record()
         cur = torch.cuda.current_stream()
-        cur.wait_event(ready)
+        cur.wait_event(self._stage_ready[j])
         smp.nodes[0][:cnt].copy_(self._stage[j][:cnt], non_blocking=True)
         smp.n_nodes[0].fill_(cnt)
-        done = torch.cuda.Event()
-        done.record(cur)
-        self._stage_done[j] = done
+        self._stage_done[j].record(cur)
+        self._stage_used[j] = True
 
     def replay(self, b: int):
         """Run step b (after ``prepare(b)``) from its CUDA graph, or eagerly."""

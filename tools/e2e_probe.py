@@ -30,8 +30,12 @@ def main():
               for b in range(200)]
     loss_host = torch.zeros(200, dtype=torch.float32).pin_memory()
 
+    import time
+
     def run(mode, b0):
         evs = []
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
         for i in range(K):
             b = b0 + i
             bench.flush_l2(flush)
@@ -53,12 +57,15 @@ def main():
                 loss_host[i].copy_(loss, non_blocking=True)
             e.record()
             evs.append((s, e))
+        host_us = (time.perf_counter() - t0) / K * 1e6  # enqueue rate (no sync in the loop)
         torch.cuda.synchronize()
-        return statistics.median(s.elapsed_time(e) for s, e in evs) * 1e3
+        return statistics.median(s.elapsed_time(e) for s, e in evs) * 1e3, host_us
 
     b = 10
     for mode in ["device", "device+prep", "h2d", "h2d+d2h", "device", "h2d+d2h"]:
-        print(f"{desc}: {mode:12s} {run(mode, b):.1f} us/step (median of {K})", flush=True)
+        dev_us, host_us = run(mode, b)
+        print(f"{desc}: {mode:12s} {dev_us:.1f} us/step device (median of {K}), "
+              f"host enqueue {host_us:.1f} us/step", flush=True)
         b += K + 2
 
 
