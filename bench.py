@@ -367,10 +367,45 @@ def run_ours(args, rank, world, local):
     L = len(fanouts)
     row_bytes = dc.num_parts * dc.bits / 8 if hasattr(dc, "num_parts") else dc.d * dc.params.k / 8
     kt, kbytes = [], []
+    # the sampler alone (sampler edges/s), replayed from a CUDA
+    # graph as in the training step (eager, its ~40 small launches would be
+    # host-bound); eager if the capture is refused
+    st_ms, st_edges = [], []
+    samp_graph = None
+    try:
+        tr.sampler.load_seeds(args.warmup)
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            tr.sampler.sample_loaded()
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        samp_graph = torch.cuda.CUDAGraph()
+        tr.sampler.load_seeds(args.warmup)
+        with torch.cuda.graph(samp_graph):
+            tr.sampler.sample_loaded()
+        for w in range(2):  # untimed replays (the first one uploads the graph)
+            tr.sampler.load_seeds(args.warmup + w)
+            samp_graph.replay()
+        torch.cuda.synchronize()
+    except Exception as ex:  # noqa: BLE001 -- diagnostic leg only
+        print(f"[bench] sampler graph capture refused ({ex}); timing it eagerly", file=sys.stderr)
+        samp_graph = None
+        torch.cuda.synchronize()
     for i in range(args.steps):
         tr.sampler.load_seeds(args.warmup + i)
-        sb = tr.sampler.sample_loaded()
+        flush_l2(flush)
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record()
+        if samp_graph is not None:
+            samp_graph.replay()
+            sb = tr.sampler.batch_view()
+        else:
+            sb = tr.sampler.sample_loaded()
+        s1.record()
         torch.cuda.synchronize()
+        st_ms.append(s0.elapsed_time(s1))
+        st_edges.append(sum(int(x.item()) for x in sb.n_picks))
         E = int(sb.n_picks[L - 1].item())
         nd = int(sb.n_nodes[L - 1].item())
         flush_l2(flush)
@@ -427,6 +462,14 @@ def run_ours(args, rank, world, local):
                           "steps enqueued back to back, CUDA events around each step, one "
                           "host sync after the K steps"},
         "epoch": epoch,
+        "sampler": {"edges_per_s": round(sum(st_edges) / (sum(st_ms) * 1e-3), 1),
+                    "us_per_batch": round(sum(st_ms) / len(st_ms) * 1e3, 2),
+                    "edges_per_batch": int(sum(st_edges) / len(st_edges)),
+                    "graphed": samp_graph is not None,
+                    "method": "one batch's sampling alone (all layers: prefix, sample, fix-up, "
+                              "unique, transposes) replayed from a CUDA graph, L2 flushed "
+                              "before, CUDA events; in the training step it runs overlapped "
+                              "on a side stream"},
         "gpu_launches": int(launches_per_step * args.steps),
         "roofline": {"kernel": ("fg_sq_gather_dequant / fg_vq_gather_decode" if agg_kind == "gat"
                                else "fg_gather_dequant_mean"),
