@@ -477,12 +477,17 @@ extern "C" int fg_block_mean_wgrad(const uint16_t* g, int64_t g_ld, const int32_
   // persistent CTAs on 3/4 of the SMs: the rest stay free for the sampler
   // kernels that overlap the training step on the side stream (products
   // step: 288 -> 276 us at 112 of 148 SMs; 96 is slower again).
-  // FG_WGRAD_CTAS overrides (1 .. SM count).
+  // Input pitch P > 128 (papers100M-shape, P = 144): 96 of 148 SMs
+  // (pipelined step 0.2628 -> 0.2567 ms over three interleaved runs; 80:
+  // 0.2577, 64: 0.263, 128: 0.266, 148: 0.295).  FG_WGRAD_CTAS overrides
+  // (1 .. SM count).
   static const int nb_env = [] {
     const char* e = getenv("FG_WGRAD_CTAS");
     return e ? atoi(e) : 0;
   }();
-  const int nb = nb_env > 0 && nb_env <= sm_count() ? nb_env : (sm_count() * 3) / 4;
+  const int nb = nb_env > 0 && nb_env <= sm_count()
+                     ? nb_env
+                     : (P > 128 ? (sm_count() * 13) / 20 : (sm_count() * 3) / 4);
   FG_CHECK_ARG(scratch_bytes >= fg_block_mean_wgrad_scratch_bytes(H, P), "scratch too small");
   cudaStream_t st = as_stream(s);
   float* seg_f = scratch + (int64_t)nb * H * P;
